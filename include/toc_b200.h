@@ -1,0 +1,132 @@
+/*
+ * toc_b200.h -- C ABI of the B200-native TOC (tuple-oriented compression, arXiv 1702.06943)
+ * hot path: compress -> TOC1 blocks in HBM -> A.v / v^T.A / A.M / M.A over compressed
+ * mini-batches -> the MGD step that drives them.
+ *
+ * Plain C: device pointers, sizes and a cudaStream_t passed as void*.  No torch types.  Every
+ * call is asynchronous on `stream` unless it says otherwise; no call allocates device memory or
+ * synchronises except toc_encode_plan (one device->host copy of the per-batch sizes).
+ *
+ * The reference is a pure-Python package (`toc`, reference pkg/src/toc); its public functions are
+ * the interface each entry point replaces.  INTEGRATION.md shows the ctypes binding.
+ *
+ * Return value of every function: TOC_OK or a TOC_E* code.  Per-batch format / encoding errors
+ * are reported in TocBlockMeta.status and map to the reference's exception classes:
+ *   TOC_E_BAD_MAGIC   -> BadMagicError            (reference physical.py:33-34)
+ *   TOC_E_BAD_VERSION -> UnsupportedVersionError  (physical.py:37-38)
+ *   TOC_E_TRUNCATED   -> TruncatedBlockError      (physical.py:41-42)
+ *   TOC_E_FORMAT      -> BlockFormatError         (physical.py:33)
+ *   TOC_E_CORRUPT     -> CorruptEncodingError     (codec.py:33, raised lazily like codec.py:235-244)
+ *   TOC_E_INPUT       -> ValueError               (matrix.py:90-114 row validation)
+ */
+#ifndef TOC_B200_H
+#define TOC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  TOC_OK = 0,
+  TOC_E_BAD_MAGIC = 1,
+  TOC_E_BAD_VERSION = 2,
+  TOC_E_TRUNCATED = 3,
+  TOC_E_FORMAT = 4,
+  TOC_E_CORRUPT = 5,
+  TOC_E_INPUT = 6,
+  TOC_E_CUDA = 7,
+  TOC_E_ARG = 8,
+};
+
+/* detail codes for TocBlockMeta.detail (which check failed; messages are rebuilt on the host) */
+enum {
+  TOC_D_NONE = 0,
+  TOC_D_WIDTH = 1,       /* bytes_per_int must be 1..4           physical.py:77-78   */
+  TOC_D_PAIR_COUNT = 2,  /* pair count does not match            physical.py:151-154 */
+  TOC_D_CODE_COUNT = 3,  /* code count does not match            physical.py:160-161 */
+  TOC_D_TRAILING = 4,    /* trailing bytes after block           physical.py:163-164 */
+  TOC_D_OFFS_COUNT = 5,  /* expected n_rows+1 row offsets        physical.py:165-166 */
+  TOC_D_OFFS_SPAN = 6,   /* row offsets do not span the codes    physical.py:167-168 */
+  TOC_D_OFFS_MONO = 7,   /* row offsets not monotone             physical.py:172-173 */
+  TOC_D_REF_RANGE = 8,   /* value ref out of range               physical.py:104-107 */
+  TOC_D_PAIR_COL = 9,    /* pair column out of range             codec.py:155-156    */
+  TOC_D_PAIR_VAL = 10,   /* pair value is not finite             codec.py:157-158    */
+  TOC_D_CODE_LT1 = 11,   /* code is not a valid node             codec.py:159-162    */
+  TOC_D_UNDEF = 12,      /* code references an undefined node    codec.py:235-244    */
+  TOC_D_MAGIC = 13,
+  TOC_D_VERSION = 14,
+  TOC_D_TRUNC = 15,
+};
+
+/*
+ * Per-batch index of one TOC1 block (layout: reference physical.py:1-21), written on the device
+ * by toc_index_blocks.  68 bytes.  Offsets are relative to the block's first byte.
+ */
+typedef struct TocBlockMeta {
+  uint32_t n_rows, n_cols;   /* header                                                  */
+  uint32_t n_uniques;        /* distinct value bit patterns                             */
+  uint32_t n_pairs;          /* |I|: first-layer pairs                                  */
+  uint32_t n_codes;          /* C = sum len(D[r])                                       */
+  uint32_t n_derived;        /* sum max(len(D[r]) - 1, 0)  (codec.py:168-170)           */
+  uint32_t off_uniques;      /* raw f64 x n_uniques                                     */
+  uint32_t off_cols;         /* packed pair columns payload                             */
+  uint32_t off_refs;         /* packed value refs payload                               */
+  uint32_t off_codes;        /* packed concatenated codes payload                       */
+  uint32_t off_offsets;      /* packed row offsets payload (n_rows + 1 entries)         */
+  uint8_t w_cols, w_refs, w_codes, w_offsets; /* bytes per packed int, 1..4              */
+  int32_t status;            /* TOC_OK or TOC_E_* (format errors, eager like deserialize)*/
+  int32_t corrupt;           /* 1 if the tree build would raise CorruptEncodingError     */
+  uint32_t detail;           /* TOC_D_* for status / corrupt                            */
+  uint32_t detail_a;         /* offset / row of the failed check                         */
+  uint32_t detail_b;         /* offending value (code, column, ref, count)               */
+} TocBlockMeta;
+
+/* Launch plan for the compressed linear-algebra kernels over an arena of indexed blocks. */
+typedef struct TocPlan {
+  int32_t threads;           /* CTA size                                                */
+  int32_t ctas;              /* persistent grid size                                     */
+  int32_t smem_bytes;        /* dynamic shared memory per CTA                            */
+  int32_t wide;              /* 1 if some tree has >= 65536 nodes (32-bit node ids)      */
+  int32_t vec_in_smem;       /* 1 if the n_cols-long vectors are staged in shared memory */
+  int32_t n_cols;            /* common n_cols of the arena                                */
+  int32_t max_rows;
+  int32_t global_tables;     /* 1 if some batch's tables exceed shared memory            */
+  int64_t scratch_bytes;     /* device workspace needed when global_tables (0 otherwise) */
+} TocPlan;
+
+/* kind bits for toc_plan / toc_linalg */
+enum { TOC_MATVEC = 1, TOC_VECMAT = 2 };
+
+/* ---- indexing (replaces physical.deserialize_block's parse + LogicalEncoding validation,
+ *      reference physical.py:138-186, codec.py:151-162, and the tree-validity checks of
+ *      codec.build_prefix_tree, codec.py:233-244) ---------------------------------------- */
+int toc_index_blocks(const uint8_t* d_arena, const int64_t* d_block_off, const int64_t* d_block_len,
+                     int64_t n_blocks, TocBlockMeta* d_meta, void* stream);
+
+/* Host-side planning from a host copy of the metadata (pure host code, no CUDA calls except
+ * reading device properties).  kind = TOC_MATVEC | TOC_VECMAT. */
+int toc_plan(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t kind, TocPlan* plan);
+
+/* ---- compressed linear algebra (reference kernels.py:115-174) ----------------------------
+ * Batch b's rows are rows [d_row_base[b], d_row_base[b] + n_rows_b) of the concatenated row
+ * space.  matvec:  d_R[row_base[b] + r] = (A_b . v)[r]                 (kernels.py:115 matvec)
+ * vecmat:  d_O[b * n_cols + c] = (u_b^T . A_b)[c], u_b = d_u[row_base[b] ...] (kernels.py:145)
+ * kind selects one or both; with both, each block is read once for the pair.
+ * d_scratch: plan.scratch_bytes of device memory (may be NULL when scratch_bytes == 0). */
+int toc_linalg(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+               const int64_t* d_row_base, int64_t n_blocks, const TocPlan* plan, int32_t kind,
+               const double* d_v, double* d_R, const double* d_u, double* d_O, void* d_scratch,
+               void* stream);
+
+/* ---- version / self-description ---------------------------------------------------------- */
+const char* toc_version(void);
+int toc_device_info(int32_t* sm_count, int32_t* smem_optin, int64_t* l2_bytes);
+int toc_sizeof_meta(void); /* 68: ABI check for bindings */
+int toc_sizeof_plan(void); /* 40 */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TOC_B200_H */

@@ -1,0 +1,144 @@
+"""Device-resident arena of TOC1 blocks: the HBM layout every kernel reads.
+
+Layout:
+  * ``data``: one uint8 buffer holding the exact TOC1 bytes of every batch (reference
+    physical.py:1-21), batch b at ``block_off[b]``, each block 16-byte aligned;
+  * ``meta``: one 68-byte TocBlockMeta per batch, written on the device by toc_index_blocks;
+  * ``row_base``: the first row of each batch in the concatenated row space (outputs of A.v and
+    the u operand of v^T.A are indexed by it).
+
+The arena replaces a list of reference ``CompressedMatrix`` objects (kernels.py:41-84) and the
+per-batch Python loops of cli.py:299-383 / training.py:355-358 with one launch per operation.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Sequence
+
+import numpy as np
+
+from . import _native as N
+from .errors import raise_for_meta
+
+
+def _align16(x: int) -> int:
+    return (x + 15) & ~15
+
+
+class BlockArena:
+    def __init__(self, data, block_off: np.ndarray, block_len: np.ndarray, meta_d=None, *,
+                 check: bool = True):
+        torch = N.require_cuda()
+        self.torch = torch
+        self.data = data
+        self.block_off = np.ascontiguousarray(block_off, np.int64)
+        self.block_len = np.ascontiguousarray(block_len, np.int64)
+        self.n_blocks = len(self.block_off)
+        dev = data.device
+        self.block_off_d = torch.from_numpy(self.block_off).to(dev)
+        self.block_len_d = torch.from_numpy(self.block_len).to(dev)
+        if meta_d is None:
+            meta_d = torch.empty(max(self.n_blocks, 1) * N.META_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+            rc = N.lib().toc_index_blocks(data.data_ptr(), self.block_off_d.data_ptr(),
+                                          self.block_len_d.data_ptr(), self.n_blocks, meta_d.data_ptr(),
+                                          N.stream_handle())
+            N.check(rc, "toc_index_blocks")
+        self.meta_d = meta_d
+        self.meta = np.frombuffer(meta_d.cpu().numpy().tobytes(), dtype=N.META_DTYPE)[: self.n_blocks].copy()
+        if check:
+            self.raise_format_errors()
+        rows = self.meta["n_rows"].astype(np.int64)
+        self.row_base = np.zeros(self.n_blocks, np.int64)
+        if self.n_blocks:
+            np.cumsum(rows[:-1], out=self.row_base[1:])
+        self.n_rows_total = int(rows.sum())
+        self.row_base_d = torch.from_numpy(self.row_base).to(dev)
+        self.n_cols = int(self.meta["n_cols"][0]) if self.n_blocks else 0
+        self._plans: dict[int, N.TocPlan] = {}
+        self._scratch = None
+
+    # ---- construction ------------------------------------------------------------------------
+    @classmethod
+    def from_bytes(cls, blocks: Sequence[bytes], device: str = "cuda", check: bool = True) -> "BlockArena":
+        """Upload serialized TOC1 blocks (reference physical.serialize_block output)."""
+        torch = N.require_cuda()
+        lens = np.fromiter((len(b) for b in blocks), dtype=np.int64, count=len(blocks))
+        offs = np.zeros(len(blocks), np.int64)
+        pos = 0
+        for i, n in enumerate(lens):
+            offs[i] = pos
+            pos = _align16(pos + int(n))
+        host = torch.zeros(max(pos, 16), dtype=torch.uint8, pin_memory=True)
+        hv = host.numpy()
+        for i, b in enumerate(blocks):
+            hv[offs[i] : offs[i] + lens[i]] = np.frombuffer(b, dtype=np.uint8)
+        data = host.to(device, non_blocking=True)
+        return cls(data, offs, lens, check=check)
+
+    def raise_format_errors(self) -> None:
+        bad = np.flatnonzero(self.meta["status"] != N.TOC_OK)
+        if len(bad):
+            b = int(bad[0])
+            head = bytes(self.data[int(self.block_off[b]) : int(self.block_off[b]) + 4].cpu().numpy())
+            raise_for_meta(self.meta[b], head)
+
+    def raise_corrupt(self) -> None:
+        bad = np.flatnonzero(self.meta["corrupt"] != 0)
+        if len(bad):
+            raise_for_meta(self.meta[int(bad[0])], lazy=True)
+
+    # ---- accounting --------------------------------------------------------------------------
+    @property
+    def block_bytes(self) -> int:
+        """Sum of the TOC1 block sizes (the algorithmic bytes of one pass)."""
+        return int(self.block_len.sum())
+
+    def tree_lengths(self) -> np.ndarray:
+        return 1 + self.meta["n_pairs"].astype(np.int64) + self.meta["n_derived"].astype(np.int64)
+
+    # ---- kernels -----------------------------------------------------------------------------
+    def plan(self, kind: int) -> N.TocPlan:
+        p = self._plans.get(kind)
+        if p is None:
+            p = N.TocPlan()
+            rc = N.lib().toc_plan(self.meta.ctypes.data_as(ctypes.c_void_p), self.n_blocks, kind, ctypes.byref(p))
+            N.check(rc, "toc_plan")
+            self._plans[kind] = p
+        return p
+
+    def _scratch_for(self, plan: N.TocPlan):
+        if plan.scratch_bytes == 0:
+            return None
+        if self._scratch is None or self._scratch.numel() < plan.scratch_bytes:
+            self._scratch = self.torch.empty(plan.scratch_bytes, dtype=self.torch.uint8, device=self.data.device)
+        return self._scratch
+
+    def linalg(self, kind: int, v=None, u=None, R=None, O=None):
+        """kind = TOC_MATVEC | TOC_VECMAT.  v: device float64 [n_cols]; u: device float64
+        [n_rows_total].  Returns (R [n_rows_total], O [n_blocks, n_cols]) device tensors."""
+        torch = self.torch
+        self.raise_corrupt()
+        dev = self.data.device
+        if kind & N.TOC_MATVEC:
+            if R is None:
+                R = torch.empty(self.n_rows_total, dtype=torch.float64, device=dev)
+        if kind & N.TOC_VECMAT:
+            if O is None:
+                O = torch.empty((self.n_blocks, self.n_cols), dtype=torch.float64, device=dev)
+        plan = self.plan(kind)
+        scratch = self._scratch_for(plan)
+        rc = N.lib().toc_linalg(
+            self.data.data_ptr(), self.block_off_d.data_ptr(), self.meta_d.data_ptr(), self.row_base_d.data_ptr(),
+            self.n_blocks, ctypes.byref(plan), kind,
+            v.data_ptr() if v is not None else None, R.data_ptr() if R is not None else None,
+            u.data_ptr() if u is not None else None, O.data_ptr() if O is not None else None,
+            scratch.data_ptr() if scratch is not None else None, N.stream_handle())
+        N.check(rc, "toc_linalg")
+        return R, O
+
+    def matvec(self, v):
+        return self.linalg(N.TOC_MATVEC, v=v)[0]
+
+    def vecmat(self, u):
+        return self.linalg(N.TOC_VECMAT, u=u)[1]

@@ -1,0 +1,404 @@
+// toc_linalg.cu -- A.v and v^T.A directly on TOC1 blocks resident in HBM (sm_100a).
+//
+// Reference: kernels.py:115-142 (matvec, Algorithm 5) and kernels.py:145-174 (vecmat,
+// Algorithm 6); the tree they walk is codec.py:215-259 (build_prefix_tree).
+//
+// Design: a persistent grid, one CTA per mini-batch at a time.  The CTA
+// reads only the batch's TOC1 bytes and rebuilds, in shared memory, the part of the decode tree
+// C' the products need:
+//   par[d] = D-code at the position that derived node d           (codec.py:247)
+//   key[d] = first-layer pair that node d appends = F(next code)   (codec.py:248-249)
+// (d = derived node id - 1 - |I|).  Node values are never materialised: a code's partial sum
+// is produced by walking par[] to the first layer, summing P1[key] (P1[i] = value_i * v[col_i])
+// on the way.  Work per batch is O(|I| + C + nnz) shared-memory accesses, no HBM traffic
+// beyond the block itself, v / u and the outputs.
+//
+//   matvec: P1 in tab[1..|I|]; each warp owns rows; lanes expand 32 codes at a time, a warp
+//           reduction folds them into the row sum.
+//   vecmat: G in tab[1..|I|]: each code adds u[row] to every pair key on its chain (the
+//           transpose of the matvec walk, an fp64 shared-memory atomic per pair), then
+//           out[col_i] += value_i * G[i].
+#include "toc_common.cuh"
+
+namespace toc {
+
+struct LinalgArgs {
+  const uint8_t* arena;
+  const int64_t* block_off;
+  const TocBlockMeta* meta;
+  const int64_t* row_base;
+  int64_t n_blocks;
+  int32_t kind;
+  int32_t n_cols;
+  int32_t batch_smem_budget;  // bytes of dynamic smem available for one batch's tables
+  int64_t slab_bytes;         // global fallback slab per CTA
+  const double* v;
+  double* R;
+  const double* u;
+  double* O;
+  uint8_t* scratch;
+};
+
+// Byte layout of one batch's tables (all regions 16-B aligned).
+struct BatchLayout {
+  uint32_t off_rowoff, off_dbase, off_uniq, off_tab, off_pk, total;
+};
+
+template <bool kWide>
+TOC_HD BatchLayout batch_layout(const TocBlockMeta& m) {
+  BatchLayout L;
+  uint32_t o = 0;
+  L.off_rowoff = o;
+  o += align16(4u * (m.n_rows + 1));
+  L.off_dbase = o;
+  o += align16(4u * (m.n_rows + 1));
+  L.off_uniq = o;
+  o += align16(8u * m.n_uniques);
+  L.off_tab = o;
+  o += align16(8u * (m.n_pairs + 1));
+  L.off_pk = o;
+  o += align16((kWide ? 8u : 4u) * m.n_derived);
+  L.total = o;
+  return L;
+}
+
+// Node-table accessors: narrow trees pack (par, key) as two u16 in one u32; wide ones use uint2.
+template <bool kWide>
+struct PK;
+
+template <>
+struct PK<false> {
+  uint32_t* p;
+  TOC_D void set_par(uint32_t d, uint32_t x) { reinterpret_cast<uint16_t*>(p)[2 * d] = (uint16_t)x; }
+  TOC_D void set_key(uint32_t d, uint32_t x) { reinterpret_cast<uint16_t*>(p)[2 * d + 1] = (uint16_t)x; }
+  TOC_D uint32_t par(uint32_t d) const { return reinterpret_cast<const uint16_t*>(p)[2 * d]; }
+  TOC_D void get(uint32_t d, uint32_t& par, uint32_t& key) const {
+    uint32_t w = p[d];
+    par = w & 0xffffu;
+    key = w >> 16;
+  }
+};
+
+template <>
+struct PK<true> {
+  uint2* p;
+  TOC_D void set_par(uint32_t d, uint32_t x) { p[d].x = x; }
+  TOC_D void set_key(uint32_t d, uint32_t x) { p[d].y = x; }
+  TOC_D uint32_t par(uint32_t d) const { return p[d].x; }
+  TOC_D void get(uint32_t d, uint32_t& par, uint32_t& key) const {
+    uint2 w = p[d];
+    par = w.x;
+    key = w.y;
+  }
+};
+
+// Exclusive scan over rows of max(len-1, 0): the id base of the nodes each row derives.
+TOC_D void scan_derived_base(const uint32_t* rowoff, uint32_t* dbase, uint32_t n, uint32_t* s_warp) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  uint32_t carry = 0;
+  for (uint32_t base = 0; base < n; base += blockDim.x) {
+    uint32_t r = base + tid;
+    uint32_t len = (r < n) ? rowoff[r + 1] - rowoff[r] : 0u;
+    uint32_t v = len ? len - 1 : 0u;
+    uint32_t x = warp_excl_scan(v, lane);
+    if (lane == 31) s_warp[warp] = x + v;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t t = lane < nwarps ? s_warp[lane] : 0u;
+      uint32_t e = warp_excl_scan(t, lane);
+      if (lane < nwarps) s_warp[lane] = e;
+      if (lane == 31) s_warp[32] = e + t;
+    }
+    __syncthreads();
+    if (r < n) dbase[r] = carry + s_warp[warp] + x;
+    carry += s_warp[32];
+    __syncthreads();
+  }
+}
+
+// One batch: rebuild par/key, then the requested products.  `tab`, `pk`, `uniq`, `rowoff`,
+// `dbase` point either into shared memory or into this CTA's global slab.
+template <bool kWide, bool kVecSmem>
+__device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, const TocBlockMeta& m,
+                                              uint8_t* tables, const double* vec_s, double* acc_s,
+                                              uint32_t* s_warp) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const uint8_t* blk = a.arena + a.block_off[b];
+  const BatchLayout L = batch_layout<kWide>(m);
+  uint32_t* rowoff = reinterpret_cast<uint32_t*>(tables + L.off_rowoff);
+  uint32_t* dbase = reinterpret_cast<uint32_t*>(tables + L.off_dbase);
+  double* uniq = reinterpret_cast<double*>(tables + L.off_uniq);
+  double* tab = reinterpret_cast<double*>(tables + L.off_tab);
+  PK<kWide> pk;
+  pk.p = reinterpret_cast<decltype(pk.p)>(tables + L.off_pk);
+
+  const uint32_t n = m.n_rows, nI = m.n_pairs, nU = m.n_uniques;
+  const uint8_t* cols = blk + m.off_cols;
+  const uint8_t* refs = blk + m.off_refs;
+  const uint8_t* codes = blk + m.off_codes;
+  const uint8_t* offs = blk + m.off_offsets;
+  const uint32_t wc = m.w_cols, wr = m.w_refs, wk = m.w_codes, wo = m.w_offsets;
+  const int64_t row_base = a.row_base[b];
+  const int32_t ncol = a.n_cols;
+  const double* vec = kVecSmem ? vec_s : a.v;
+
+  // ---- phase 0: row offsets, value index, derived-node bases --------------------------------
+  for (uint32_t r = tid; r <= n; r += blockDim.x) rowoff[r] = ld_packed(offs, r, wo);
+  for (uint32_t i = tid; i < nU; i += blockDim.x) uniq[i] = ld_f64_unaligned(blk + m.off_uniques + 8u * i);
+  if ((a.kind & TOC_VECMAT) && kVecSmem)
+    for (int32_t c = tid; c < ncol; c += blockDim.x) acc_s[c] = 0.0;
+  __syncthreads();
+  scan_derived_base(rowoff, dbase, n, s_warp);
+
+  // ---- phase 1: first-layer products (matvec) and par[] -------------------------------------
+  if (a.kind & TOC_MATVEC) {
+    for (uint32_t i = tid; i < nI; i += blockDim.x) {
+      double val = uniq[ld_packed(refs, i, wr)];
+      tab[i + 1] = val * vec[ld_packed(cols, i, wc)];
+    }
+  } else {
+    for (uint32_t i = tid; i <= nI; i += blockDim.x) tab[i] = 0.0;
+  }
+  for (uint32_t r = warp; r < n; r += nwarps) {
+    const uint32_t lo = rowoff[r], hi = rowoff[r + 1], db = dbase[r];
+    for (uint32_t j = lo + lane; j + 1 < hi; j += 32) pk.set_par(db + (j - lo), ld_packed(codes, j, wk));
+  }
+  __syncthreads();
+
+  // ---- phase 2: key[d] = F(next code): follow par[] down to the first layer -----------------
+  for (uint32_t r = warp; r < n; r += nwarps) {
+    const uint32_t lo = rowoff[r], hi = rowoff[r + 1], db = dbase[r];
+    for (uint32_t j = lo + lane; j + 1 < hi; j += 32) {
+      uint32_t x = ld_packed(codes, j + 1, wk);
+      while (x > nI) x = pk.par(x - 1 - nI);
+      pk.set_key(db + (j - lo), x);
+    }
+  }
+  __syncthreads();
+
+  // ---- phase 3: A.v -------------------------------------------------------------------------
+  if (a.kind & TOC_MATVEC) {
+    for (uint32_t r = warp; r < n; r += nwarps) {
+      const uint32_t lo = rowoff[r], hi = rowoff[r + 1];
+      double acc = 0.0;
+      for (uint32_t base = lo; base < hi; base += 32) {
+        const uint32_t j = base + lane;
+        double h = 0.0;
+        if (j < hi) {
+          uint32_t x = ld_packed(codes, j, wk);
+          while (x > nI) {
+            uint32_t p, k;
+            pk.get(x - 1 - nI, p, k);
+            h += tab[k];
+            x = p;
+          }
+          h += tab[x];
+        }
+        acc += warp_sum(h);
+      }
+      if (lane == 0) a.R[row_base + r] = acc;
+    }
+  }
+
+  // ---- phase 4: u^T.A -----------------------------------------------------------------------
+  if (a.kind & TOC_VECMAT) {
+    if (a.kind & TOC_MATVEC) {
+      __syncthreads();
+      for (uint32_t i = tid; i <= nI; i += blockDim.x) tab[i] = 0.0;
+      __syncthreads();
+    }
+    for (uint32_t r = warp; r < n; r += nwarps) {
+      const uint32_t lo = rowoff[r], hi = rowoff[r + 1];
+      const double w = a.u[row_base + r];
+      for (uint32_t j = lo + lane; j < hi; j += 32) {
+        uint32_t x = ld_packed(codes, j, wk);
+        while (x > nI) {
+          uint32_t p, k;
+          pk.get(x - 1 - nI, p, k);
+          atomicAdd(&tab[k], w);
+          x = p;
+        }
+        atomicAdd(&tab[x], w);
+      }
+    }
+    __syncthreads();
+    double* out = kVecSmem ? acc_s : a.O + b * (int64_t)ncol;
+    for (uint32_t i = tid; i < nI; i += blockDim.x) {
+      const double g = tab[i + 1];
+      if (g != 0.0) {
+        double val = uniq[ld_packed(refs, i, wr)];
+        atomicAdd(&out[ld_packed(cols, i, wc)], val * g);
+      }
+    }
+    if (kVecSmem) {
+      __syncthreads();
+      double* o = a.O + b * (int64_t)ncol;
+      for (int32_t c = tid; c < ncol; c += blockDim.x) o[c] = acc_s[c];
+    }
+  }
+}
+
+template <bool kWide, bool kVecSmem>
+__global__ void __launch_bounds__(1024, 1) linalg_kernel(LinalgArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint32_t* s_warp = reinterpret_cast<uint32_t*>(smem);  // 33 words, padded to 256 B
+  uint8_t* p = smem + 256;
+  double* vec_s = nullptr;
+  double* acc_s = nullptr;
+  if (kVecSmem) {
+    if (a.kind & TOC_MATVEC) {
+      vec_s = reinterpret_cast<double*>(p);
+      p += align16(8u * a.n_cols);
+    }
+    if (a.kind & TOC_VECMAT) {
+      acc_s = reinterpret_cast<double*>(p);
+      p += align16(8u * a.n_cols);
+    }
+    if (vec_s)
+      for (int32_t c = threadIdx.x; c < a.n_cols; c += blockDim.x) vec_s[c] = a.v[c];
+  }
+  uint8_t* slab = a.scratch ? a.scratch + (int64_t)blockIdx.x * a.slab_bytes : nullptr;
+  for (int64_t b = blockIdx.x; b < a.n_blocks; b += gridDim.x) {
+    const TocBlockMeta m = a.meta[b];
+    if (m.status != TOC_OK || m.corrupt) continue;  // host refuses such arenas up front
+    const uint32_t need = batch_layout<kWide>(m).total;
+    __syncthreads();
+    if (need <= (uint32_t)a.batch_smem_budget)
+      process_batch<kWide, kVecSmem>(a, b, m, p, vec_s, acc_s, s_warp);
+    else
+      process_batch<kWide, kVecSmem>(a, b, m, slab, vec_s, acc_s, s_warp);
+  }
+}
+
+}  // namespace toc
+
+// ------------------------------------------------------------------------------------------
+// Host side: planning and launch.
+namespace {
+
+struct DevProps {
+  int sm_count = 0, smem_optin = 0, smem_per_sm = 0;
+  int64_t l2 = 0;
+};
+
+const DevProps& dev_props() {
+  static DevProps p;
+  static bool init = false;
+  if (!init) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&p.sm_count, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&p.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&p.smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    int l2 = 0;
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    p.l2 = l2;
+    if (p.sm_count <= 0) {  // no device visible (planning on a CPU host): B200 figures
+      p.sm_count = 148;
+      p.smem_optin = 232448;
+      p.smem_per_sm = 233472;
+      p.l2 = 126 << 20;
+    }
+    init = true;
+  }
+  return p;
+}
+
+template <bool W, bool V>
+cudaError_t launch(const toc::LinalgArgs& a, const TocPlan& plan, cudaStream_t s) {
+  static int configured = -1;
+  if (configured < plan.smem_bytes) {
+    cudaError_t e = cudaFuncSetAttribute(toc::linalg_kernel<W, V>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, plan.smem_bytes);
+    if (e != cudaSuccess) return e;
+    configured = plan.smem_bytes;
+  }
+  toc::linalg_kernel<W, V><<<plan.ctas, plan.threads, plan.smem_bytes, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+extern "C" int toc_plan(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t kind, TocPlan* plan) {
+  if (!plan || (n_blocks > 0 && !h_meta) || !(kind & (TOC_MATVEC | TOC_VECMAT))) return TOC_E_ARG;
+  memset(plan, 0, sizeof(*plan));
+  const DevProps& d = dev_props();
+  uint64_t max_T = 0;
+  int32_t n_cols = n_blocks ? (int32_t)h_meta[0].n_cols : 0;
+  for (int64_t b = 0; b < n_blocks; b++) {
+    const TocBlockMeta& m = h_meta[b];
+    if ((int32_t)m.n_cols != n_cols) return TOC_E_ARG;
+    uint64_t T = 1ull + m.n_pairs + m.n_derived;
+    if (T > max_T) max_T = T;
+    if ((int32_t)m.n_rows > plan->max_rows) plan->max_rows = (int32_t)m.n_rows;
+  }
+  plan->wide = max_T > 65536ull;
+  plan->n_cols = n_cols;
+  uint32_t max_need = 0;
+  for (int64_t b = 0; b < n_blocks; b++) {
+    uint32_t need = plan->wide ? toc::batch_layout<true>(h_meta[b]).total
+                               : toc::batch_layout<false>(h_meta[b]).total;
+    if (need > max_need) max_need = need;
+  }
+  const int nvec = ((kind & TOC_MATVEC) ? 1 : 0) + ((kind & TOC_VECMAT) ? 1 : 0);
+  const uint32_t vec_bytes = nvec * toc::align16(8u * (uint32_t)n_cols);
+  plan->vec_in_smem = vec_bytes <= 64u * 1024u;
+  const uint32_t fixed = 256u + (plan->vec_in_smem ? vec_bytes : 0u);
+  const uint32_t optin = (uint32_t)d.smem_optin;
+  if (fixed + max_need <= optin) {
+    plan->smem_bytes = (int32_t)(fixed + max_need);
+    plan->global_tables = 0;
+  } else {
+    plan->smem_bytes = (int32_t)optin;
+    plan->global_tables = 1;
+  }
+  int per_sm = (int)(((uint32_t)d.smem_per_sm) / ((uint32_t)plan->smem_bytes + 1024u));
+  if (per_sm < 1) per_sm = 1;
+  if (per_sm > 4) per_sm = 4;
+  plan->threads = per_sm == 1 ? 1024 : 512;
+  if (per_sm * plan->threads > 2048) per_sm = 2048 / plan->threads;
+  int64_t ctas = (int64_t)d.sm_count * per_sm;
+  if (ctas > n_blocks) ctas = n_blocks > 0 ? n_blocks : 1;
+  plan->ctas = (int32_t)ctas;
+  plan->scratch_bytes = plan->global_tables ? (int64_t)plan->ctas * toc::align16(max_need) : 0;
+  return TOC_OK;
+}
+
+extern "C" int toc_linalg(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+                          const int64_t* d_row_base, int64_t n_blocks, const TocPlan* plan, int32_t kind,
+                          const double* d_v, double* d_R, const double* d_u, double* d_O, void* d_scratch,
+                          void* stream) {
+  if (!plan || n_blocks < 0 || !(kind & (TOC_MATVEC | TOC_VECMAT))) return TOC_E_ARG;
+  if ((kind & TOC_MATVEC) && (!d_v || !d_R)) return TOC_E_ARG;
+  if ((kind & TOC_VECMAT) && (!d_u || !d_O)) return TOC_E_ARG;
+  if (plan->global_tables && !d_scratch) return TOC_E_ARG;
+  if (n_blocks == 0) return TOC_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  toc::LinalgArgs a;
+  a.arena = d_arena;
+  a.block_off = d_block_off;
+  a.meta = d_meta;
+  a.row_base = d_row_base;
+  a.n_blocks = n_blocks;
+  a.kind = kind;
+  a.n_cols = plan->n_cols;
+  const int nvec = ((kind & TOC_MATVEC) ? 1 : 0) + ((kind & TOC_VECMAT) ? 1 : 0);
+  const uint32_t fixed = 256u + (plan->vec_in_smem ? nvec * toc::align16(8u * (uint32_t)plan->n_cols) : 0u);
+  a.batch_smem_budget = plan->smem_bytes - (int32_t)fixed;
+  a.slab_bytes = plan->global_tables ? plan->scratch_bytes / plan->ctas : 0;
+  a.v = d_v;
+  a.R = d_R;
+  a.u = d_u;
+  a.O = d_O;
+  a.scratch = (uint8_t*)d_scratch;
+  if ((kind & TOC_VECMAT) && !plan->vec_in_smem) {
+    if (cudaMemsetAsync(d_O, 0, sizeof(double) * (size_t)n_blocks * plan->n_cols, s) != cudaSuccess)
+      return TOC_E_CUDA;
+  }
+  cudaError_t e;
+  if (plan->wide)
+    e = plan->vec_in_smem ? launch<true, true>(a, *plan, s) : launch<true, false>(a, *plan, s);
+  else
+    e = plan->vec_in_smem ? launch<false, true>(a, *plan, s) : launch<false, false>(a, *plan, s);
+  return e == cudaSuccess ? TOC_OK : TOC_E_CUDA;
+}

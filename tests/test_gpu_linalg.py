@@ -1,0 +1,119 @@
+"""GPU parity: compressed A.v / v^T.A over device-resident TOC1 blocks vs the oracle.
+
+Tolerance: 1e-9 relative in the reference's within_rel form (BASELINE.json north_star; the
+reference's own bar, test_acceptance.py:139-203).  A.v is evaluated in a different summation
+order than the reference (warp-parallel), so it is not required to be bit-exact.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import max_rel_err, within_rel
+from helpers import TOY_ROWS, TREE_ROWS, random_alphabet_rows
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-9
+
+
+def _arena(blocks):
+    from paper_1702_06943_b200.arena import BlockArena
+
+    return BlockArena.from_bytes(blocks)
+
+
+def _check_sweep(oracle, encs, v, seed=0):
+    import torch
+
+    blocks = [oracle.serialize(e) for e in encs]
+    arena = _arena(blocks)
+    trees = [oracle.Tree.from_encoding(e) for e in encs]
+    n_total = sum(e.n_rows for e in encs)
+    u = np.random.default_rng(seed).standard_normal(n_total)
+    vd = torch.from_numpy(np.asarray(v, np.float64)).cuda()
+    ud = torch.from_numpy(u).cuda()
+    from paper_1702_06943_b200 import _native as N
+
+    for kind in (N.TOC_MATVEC, N.TOC_VECMAT, N.TOC_MATVEC | N.TOC_VECMAT):
+        R, O = arena.linalg(kind, v=vd if kind & 1 else None, u=ud if kind & 2 else None)
+        torch.cuda.synchronize()
+        base = 0
+        for b, (e, t) in enumerate(zip(encs, trees)):
+            if kind & N.TOC_MATVEC:
+                want = t.matvec(v)
+                got = R[base : base + e.n_rows].cpu().numpy()
+                assert within_rel(got, want, REL), (kind, b, max_rel_err(got, want))
+            if kind & N.TOC_VECMAT:
+                want = t.vecmat(u[base : base + e.n_rows])
+                got = O[b].cpu().numpy()
+                assert within_rel(got, want, REL), (kind, b, max_rel_err(got, want))
+            base += e.n_rows
+
+
+def test_toy_known_answers(oracle):
+    import torch
+
+    enc = oracle.encode_rows(5, TOY_ROWS)
+    arena = _arena([oracle.serialize(enc)])
+    R = arena.matvec(torch.ones(5, dtype=torch.float64, device="cuda"))
+    O = arena.vecmat(torch.ones(2, dtype=torch.float64, device="cuda"))
+    assert R.cpu().tolist() == [15.0, 25.0]  # reference tests/test_kernels.py:55-62
+    assert O[0].cpu().tolist() == [7.0, 9.0, 6.0, 8.0, 10.0]  # test_kernels.py:64-69
+
+
+def test_tree_example(oracle):
+    enc = oracle.encode_rows(5, TREE_ROWS)
+    _check_sweep(oracle, [enc], np.arange(1.0, 6.0))
+
+
+def test_random_alphabet_many_blocks(oracle):
+    rng = np.random.default_rng(7)
+    encs = []
+    n_cols = 12
+    for i in range(60):
+        rows = random_alphabet_rows(rng, int(rng.integers(0, 40)), n_cols, float(rng.uniform(0.05, 1.0)),
+                                    16, integer_alphabet=bool(i % 2))
+        encs.append(oracle.encode_rows(n_cols, rows))
+    _check_sweep(oracle, encs, rng.standard_normal(n_cols), seed=1)
+
+
+def test_cfg1_batch(oracle):
+    from paper_1702_06943_b200 import synth
+
+    A = synth.cfg1_dense(0)
+    enc = oracle.encode_csr(128, *synth.dense_to_csr(A))
+    v, u = synth.cfg1_operands(0)
+    _check_sweep(oracle, [enc], v)
+
+
+def test_cfg2_batches(oracle):
+    from paper_1702_06943_b200 import synth
+
+    encs = []
+    for b in range(6):
+        enc = oracle.encode_csr(784, *synth.dense_to_csr(synth.cfg2_batch_dense(0, b)))
+        encs.append(enc)
+    v, _ = synth.cfg2_operands(0, 6)
+    _check_sweep(oracle, encs, v, seed=3)
+
+
+def test_empty_and_zero_rows(oracle):
+    encs = [oracle.encode_rows(4, []), oracle.encode_rows(3, [[(1, 2.0)], [], [(0, 4.0)]]),
+            oracle.encode_rows(3, [[], []])]
+    # n_cols differ from 4 -> keep one arena per n_cols
+    _check_sweep(oracle, encs[1:], np.array([1.0, 1.0, 1.0]))
+    _check_sweep(oracle, encs[:1], np.ones(4))
+
+
+def test_wide_tree_global_tables(oracle):
+    """A batch whose tree exceeds 65536 nodes (32-bit node ids) and shared memory (global
+    table fallback): identical rows compress into long chains."""
+    rng = np.random.default_rng(5)
+    n_cols = 400
+    base = random_alphabet_rows(rng, 30, n_cols, 0.9, 64)
+    rows = [base[i % 30] if i % 3 else random_alphabet_rows(rng, 1, n_cols, 0.9, 64)[0] for i in range(600)]
+    enc = oracle.encode_rows(n_cols, rows)
+    assert enc.tree_length() > 65536
+    _check_sweep(oracle, [enc], rng.standard_normal(n_cols), seed=9)
