@@ -120,11 +120,64 @@ int toc_linalg(const uint8_t* d_arena, const int64_t* d_block_off, const TocBloc
                const double* d_v, double* d_R, const double* d_u, double* d_O, void* d_scratch,
                void* stream);
 
+/* ---- compression (replaces codec.encode, codec.py:112-191, and physical.serialize_block,
+ *      physical.py:88-130; physical.deserialize_block's unpack, physical.py:138-186) --------
+ * Mini-batch b is rows [batch_row[b], batch_row[b+1]) of a CSR matrix (row_ptr int64, cols
+ * int32, vals f64; SparseRowMatrix contract, matrix.py:90-114, checked on the device).
+ * elem_base[b] = row_ptr[batch_row[b]] (n_batches + 1 entries).  The logical encoding of batch b
+ * is written at element base elem_base[b] (I_cols, I_vals, codes) and at batch_row[b] + b
+ * (offsets, n_rows_b + 1 entries); TocBatchInfo[b] receives the counts. */
+typedef struct TocBatchInfo {
+  uint32_t n_rows, n_cols, n_pairs, n_codes, n_uniques;
+  uint8_t w_cols, w_refs, w_codes, w_offsets;
+  int32_t status;      /* TOC_OK, or TOC_E_INPUT for a row violating the input contract */
+  uint32_t detail_a;   /* offending row                                                  */
+  uint32_t detail_b;   /* offending position within the row                              */
+  uint32_t pad_;
+  int64_t block_bytes; /* serialized TOC1 size (after toc_serialize_sizes)               */
+} TocBatchInfo;        /* 48 bytes */
+
+typedef struct TocEncodeSizes {
+  int64_t hash_slots;  /* total hash-table slots over the batches                        */
+  int64_t n_elems;     /* element-index extent of the logical arrays                      */
+  int64_t work_bytes;  /* device workspace for toc_encode / toc_serialize_sizes           */
+} TocEncodeSizes;
+
+/* Host-only sizing from a host copy of elem_base. */
+int toc_encode_sizes(int64_t n_batches, const int64_t* h_elem_base, TocEncodeSizes* out);
+
+/* Row-bounded LZW encoding of every batch (codec.encode), bit-exact with the reference. */
+int toc_encode(int64_t n_batches, int32_t n_cols, const int64_t* d_row_ptr, const int32_t* d_cols,
+               const double* d_vals, const int64_t* d_batch_row, const int64_t* d_elem_base,
+               const TocEncodeSizes* sizes, void* d_work, uint32_t* d_I_cols, double* d_I_vals,
+               uint32_t* d_codes, uint32_t* d_offsets, TocBatchInfo* d_info, void* stream);
+
+/* Value index (physical.py:88-101), packed widths (physical.py:49-51) and the TOC1 size of each
+ * batch's logical encoding; fills the remaining TocBatchInfo fields, refs and uniques. */
+int toc_serialize_sizes(int64_t n_batches, const int64_t* d_batch_row, const int64_t* d_elem_base,
+                        const uint32_t* d_I_cols, const double* d_I_vals, const uint32_t* d_codes,
+                        const uint32_t* d_offsets, const TocEncodeSizes* sizes, void* d_work,
+                        uint32_t* d_refs, double* d_uniques, TocBatchInfo* d_info, void* stream);
+
+/* Write each batch's TOC1 bytes at d_arena + d_block_off[b] (serialize_block, physical.py:110-130). */
+int toc_pack_blocks(int64_t n_batches, const int64_t* d_batch_row, const int64_t* d_elem_base,
+                    const uint32_t* d_I_cols, const uint32_t* d_refs, const double* d_uniques,
+                    const uint32_t* d_codes, const uint32_t* d_offsets, const TocBatchInfo* d_info,
+                    const int64_t* d_block_off, uint8_t* d_arena, void* stream);
+
+/* Unpack indexed blocks into logical arrays (deserialize_block): pairs at pair_base[b], codes at
+ * code_base[b], offsets at offs_base[b]. */
+int toc_unpack_blocks(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+                      int64_t n_blocks, const int64_t* d_pair_base, const int64_t* d_code_base,
+                      const int64_t* d_offs_base, uint32_t* d_I_cols, double* d_I_vals,
+                      uint32_t* d_codes, uint32_t* d_offsets, void* stream);
+
 /* ---- version / self-description ---------------------------------------------------------- */
 const char* toc_version(void);
 int toc_device_info(int32_t* sm_count, int32_t* smem_optin, int64_t* l2_bytes);
 int toc_sizeof_meta(void); /* 68: ABI check for bindings */
 int toc_sizeof_plan(void); /* 40 */
+int toc_sizeof_batch_info(void); /* 48 */
 
 #ifdef __cplusplus
 }

@@ -22,6 +22,18 @@ from . import _native as N
 from .errors import raise_for_meta
 
 
+def _ptr(t):
+    """Device pointer of a tensor; a 1-element dummy stands in for empty operands."""
+    if t is None:
+        return None
+    if t.numel() == 0:
+        return _EMPTY.setdefault((t.device, t.dtype), t.new_zeros(1)).data_ptr()
+    return t.data_ptr()
+
+
+_EMPTY: dict = {}
+
+
 def _align16(x: int) -> int:
     return (x + 15) & ~15
 
@@ -121,18 +133,18 @@ class BlockArena:
         self.raise_corrupt()
         dev = self.data.device
         if kind & N.TOC_MATVEC:
-            if R is None:
-                R = torch.empty(self.n_rows_total, dtype=torch.float64, device=dev)
+            if R is None:  # never a NULL pointer, even for zero rows
+                R = torch.empty(max(self.n_rows_total, 1), dtype=torch.float64, device=dev)[: self.n_rows_total]
         if kind & N.TOC_VECMAT:
             if O is None:
-                O = torch.empty((self.n_blocks, self.n_cols), dtype=torch.float64, device=dev)
+                O = torch.empty(max(self.n_blocks * self.n_cols, 1), dtype=torch.float64,
+                                device=dev)[: self.n_blocks * self.n_cols].view(self.n_blocks, self.n_cols)
         plan = self.plan(kind)
         scratch = self._scratch_for(plan)
         rc = N.lib().toc_linalg(
             self.data.data_ptr(), self.block_off_d.data_ptr(), self.meta_d.data_ptr(), self.row_base_d.data_ptr(),
             self.n_blocks, ctypes.byref(plan), kind,
-            v.data_ptr() if v is not None else None, R.data_ptr() if R is not None else None,
-            u.data_ptr() if u is not None else None, O.data_ptr() if O is not None else None,
+            _ptr(v), _ptr(R), _ptr(u), _ptr(O),
             scratch.data_ptr() if scratch is not None else None, N.stream_handle())
         N.check(rc, "toc_linalg")
         return R, O

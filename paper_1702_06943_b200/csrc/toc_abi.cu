@@ -20,3 +20,6 @@ static_assert(sizeof(TocPlan) == 40, "TocPlan layout is part of the ABI");
 
 extern "C" int toc_sizeof_meta(void) { return (int)sizeof(TocBlockMeta); }
 extern "C" int toc_sizeof_plan(void) { return (int)sizeof(TocPlan); }
+
+static_assert(sizeof(TocBatchInfo) == 48, "TocBatchInfo layout is part of the ABI");
+extern "C" int toc_sizeof_batch_info(void) { return (int)sizeof(TocBatchInfo); }
