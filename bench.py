@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""Benchmark of the TOC hot path on B200 (BASELINE.json metric, config 2 = the matrix-op sweep).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one pass of the hot path over this GPU's shard of config 2: A.v AND v^T.A over 1024
+compressed 250x784 float64 mini-batches (one fused launch reads each TOC1 block once for the
+pair).  Batches shard across ranks with no collective (weak scaling); time is the max over ranks
+of the device time (CUDA events) of the K timed steps; L2 (126 MB, larger than one shard's 87 MB
+of blocks) is flushed by a 256 MiB write between steps, outside the events.
+
+Prints ONE JSON line on rank 0 (contract in the task statement): value (rows/s, whole job),
+roofline of the dominant kernel, cpu_baseline (the oracle port on this host's cores, rank 0 at
+N=1, bounded sample), e2e (same metric through the public API with host buffers), clocks.
+``--impl reference`` times the CPU oracle port (the reference is pure Python and cannot run on
+the GPU box) on the same config and prints the same line with "impl": "reference".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TOC A·v / vᵀ·A rows/s and MGD epoch seconds; % of HBM roofline, 1/2/4/8 GPU"
+ROWS, COLS, BATCHES_PER_GPU, SEED = 250, 784, 1024, 20261020
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=200)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--batches-per-gpu", type=int, default=BATCHES_PER_GPU)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--e2e-steps", type=int, default=20)
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """SM clock and throttle reasons sampled during the timed region (NVML, 20 ms period)."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        names = [n for bit, n in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz, "reasons": names,
+                "samples": len(self.samples)}
+
+
+def make_shard(rank: int, nb: int):
+    """Config-2 batches [rank*nb, (rank+1)*nb) (seeded per batch) as concatenated CSR."""
+    from paper_1702_06943_b200 import synth
+
+    rp, c, v, counts = synth.cfg2_batches_csr(SEED, range(rank * nb, (rank + 1) * nb), ROWS, COLS)
+    batch_row = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    return rp, c, v, batch_row
+
+
+def algorithmic_bytes(arena, kind: int) -> int:
+    """TOC1 blocks read once, v read once, the outputs written,
+    u read (v^T.A).  Per launch over the whole shard."""
+    m = arena.n_cols
+    n = arena.n_rows_total
+    b = arena.block_bytes + 68 * arena.n_blocks  # blocks + their 68-byte index records
+    if kind & 1:
+        b += 8 * m + 8 * n
+    if kind & 2:
+        b += 8 * n + 8 * m * arena.n_blocks
+    return b
+
+
+def time_kernel(torch, fn, steps: int, warmup: int, flush):
+    """Per-step device time (CUDA events on the launching stream) with an L2 flush between steps,
+    outside the events.  Returns the list of step durations in ms."""
+    s = torch.cuda.current_stream()
+    for _ in range(warmup):
+        flush.fill_(1)
+        fn()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for i in range(steps):
+        flush.fill_(i & 0xFF)
+        ev[i][0].record(s)
+        fn()
+        ev[i][1].record(s)
+    torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in ev]
+
+
+def cpu_reference(arena_bytes_h, block_off, block_len, v, u, row_base, budget_s: float, steps: int,
+                  warmup: int, oracle_mod):
+    """The oracle port timed on this host (trees built outside the timed region, like the
+    reference's own bench-kernels, cli.py:316-317).  Returns (rows/s, sample description, cores)."""
+    O = oracle_mod
+    O.build()
+    nb = len(block_off)
+    trees = [O.Tree.from_block(bytes(arena_bytes_h[block_off[b] : block_off[b] + block_len[b]])) for b in range(nb)]
+    threads = O.max_threads()
+    # calibrate: one sweep over min(64, nb) batches
+    k = min(64, nb)
+    t0 = time.perf_counter()
+    O.sweep(trees[:k], row_base[:k], v, u, 2, threads)
+    per_batch = max((time.perf_counter() - t0) / k, 1e-7)
+    sample = int(max(1, min(nb, budget_s / max(steps + warmup, 1) / per_batch)))
+    sel = trees[:sample]
+    rb = row_base[:sample]
+    for _ in range(warmup):
+        O.sweep(sel, rb, v, u, 2, threads)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        O.sweep(sel, rb, v, u, 2, threads)
+    dt = time.perf_counter() - t0
+    rows = sample * ROWS * steps
+    desc = (f"oracle port (C, OpenMP {threads} threads) A.v+v^T.A over the first {sample} of {nb} config-2 "
+            f"batches x {steps} steps, trees prebuilt")
+    return rows / dt, desc, threads, dt
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+    import torch
+
+    from paper_1702_06943_b200 import _native as N
+    from paper_1702_06943_b200.codec import compress_csr
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    nb = args.batches_per_gpu
+    t0 = time.perf_counter()
+    rp, c, vals, batch_row = make_shard(rank, nb)
+    t_gen = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    arena = compress_csr(COLS, rp, c, vals, batch_row)
+    torch.cuda.synchronize()
+    t_enc = time.perf_counter() - t0
+    rng = np.random.default_rng(np.random.SeedSequence([SEED, 7, rank]))
+    v_h = rng.standard_normal(COLS)
+    u_h = rng.standard_normal(arena.n_rows_total)
+    v = torch.from_numpy(v_h).cuda()
+    u = torch.from_numpy(u_h).cuda()
+    kind = N.TOC_MATVEC | N.TOC_VECMAT
+    R = torch.empty(arena.n_rows_total, dtype=torch.float64, device="cuda")
+    O = torch.empty((arena.n_blocks, COLS), dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step():
+        arena.linalg(kind, v=v, u=u, R=R, O=O)
+
+    sampler = ClockSampler(local)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        times = time_kernel(torch, step, args.steps, args.warmup, flush)
+    total_ms = float(np.sum(times))
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    rows_per_step = arena.n_rows_total  # per rank
+    value = world * rows_per_step * args.steps / (total_ms / 1e3)
+    ms_per_step = total_ms / args.steps
+
+    # separate A.v-only and v^T.A-only launches (same protocol) for the per-op rows/s
+    mv_t = time_kernel(torch, lambda: arena.linalg(N.TOC_MATVEC, v=v, R=R), max(args.steps // 4, 10), 3, flush)
+    vm_t = time_kernel(torch, lambda: arena.linalg(N.TOC_VECMAT, u=u, O=O), max(args.steps // 4, 10), 3, flush)
+
+    peak, peak_src = measured_peaks()
+    alg = algorithmic_bytes(arena, kind)
+    achieved = alg / (ms_per_step / 1e3) / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        traffic = json.load(open(tpath)).get("linalg_kernel_both")
+
+    # ---- e2e: public API call with host buffers (pinned), copies inside the timed region ----
+    e2e = run_e2e(torch, arena, v_h, u_h, args.e2e_steps)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import oracle as Omod
+
+        data_h = arena.data.cpu().numpy()
+        rps, desc, cores, dt = cpu_reference(data_h, arena.block_off, arena.block_len, v_h, u_h,
+                                             arena.row_base, 12.0, 5, 1, Omod)
+        cpu = {"value": rps, "unit": "rows/s", "cores": cores, "kind": "port", "sample": desc}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "rows/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic (config-2 generator, seeded; DESIGN.md)",
+            "config": {
+                "workload": f"config 2 sweep: {nb} TOC-compressed 250x784 f64 mini-batches per GPU; one step = "
+                            "A.v and v^T.A over every batch in one fused launch",
+                "batches_per_gpu": nb, "rows_per_batch": ROWS, "n_cols": COLS,
+                "parallelism": f"batch-sharded x{world} (no collective)",
+                "l2": "flushed between steps (256 MiB write outside the timed events)",
+                "toc_block_bytes_per_gpu": arena.block_bytes,
+                "csr_bytes_per_gpu": int(len(c) * 12 + (len(rp)) * 8),
+                "encode_seconds": t_enc, "generate_seconds": t_gen,
+            },
+            "matvec_rows_per_s": world * rows_per_step / (np.mean(mv_t) / 1e3),
+            "vecmat_rows_per_s": world * rows_per_step / (np.mean(vm_t) / 1e3),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": alg, "kernel": "toc::linalg_kernel (A.v + v^T.A)"},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": args.steps,
+            "clocks": sampler.summary(),
+        }
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def run_e2e(torch, arena, v_h, u_h, steps: int):
+    """Same metric through the public API: host TOC1 bytes + host v/u in pinned memory -> device
+    (H2D inside the timed region) -> validate/index -> fused A.v + v^T.A -> host R/O (D2H)."""
+    from paper_1702_06943_b200.kernels import BatchSweep
+
+    sweep = BatchSweep.from_host_blocks(arena.data[: int(arena.block_off[-1] + arena.block_len[-1])].cpu().numpy(),
+                                        arena.block_off, arena.block_len)
+    for _ in range(2):
+        sweep.run(v_h, u_h)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        sweep.run(v_h, u_h)
+    dt = time.perf_counter() - t0
+    return {"value": sweep.n_rows * steps / dt, "unit": "rows/s", "h2d_bytes_per_step": sweep.h2d_bytes,
+            "d2h_bytes_per_step": sweep.d2h_bytes, "api": "paper_1702_06943_b200.kernels.BatchSweep.run"}
+
+
+def run_reference(args, rank, world):
+    """The reference arm: the CPU oracle port on this host's cores (rank 0 only)."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+
+    O.build()
+    nb = args.batches_per_gpu
+    rp, c, vals, batch_row = make_shard(0, nb)
+    trees = []
+    for b in range(nb):
+        lo, hi = rp[batch_row[b]], rp[batch_row[b + 1]]
+        enc = O.encode_csr(COLS, rp[batch_row[b] : batch_row[b + 1] + 1] - lo, c[lo:hi], vals[lo:hi])
+        trees.append(O.Tree.from_encoding(enc))
+    rng = np.random.default_rng(np.random.SeedSequence([SEED, 7, 0]))
+    v = rng.standard_normal(COLS)
+    u = rng.standard_normal(nb * ROWS)
+    row_base = np.arange(nb, dtype=np.int64) * ROWS
+    threads = O.max_threads()
+    k = min(32, nb)
+    t0 = time.perf_counter()
+    O.sweep(trees[:k], row_base[:k], v, u, 2, threads)
+    per_batch = max((time.perf_counter() - t0) / k, 1e-7)
+    budget = 90.0
+    sample = int(max(1, min(nb, budget / max(args.steps + args.warmup, 1) / per_batch)))
+    for _ in range(args.warmup):
+        O.sweep(trees[:sample], row_base[:sample], v, u, 2, threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.sweep(trees[:sample], row_base[:sample], v, u, 2, threads)
+    dt = time.perf_counter() - t0
+    value = sample * ROWS * args.steps / dt
+    desc = (f"oracle port (C restatement of reference kernels.py:115-174, OpenMP {threads} threads): A.v+v^T.A over "
+            f"the first {sample} of {nb} config-2 batches per step, trees prebuilt (cli.py:316-317)")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (config-2 generator, seeded)",
+        "config": {"workload": f"config 2 sweep: {nb} TOC-compressed 250x784 f64 mini-batches; step = A.v and v^T.A",
+                   "batches_per_gpu": nb, "rows_per_batch": ROWS, "n_cols": COLS},
+        "cpu_baseline": {"value": value, "unit": "rows/s", "cores": threads, "kind": "port", "sample": desc},
+        "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+if __name__ == "__main__":
+    main()

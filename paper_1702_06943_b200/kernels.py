@@ -1,0 +1,225 @@
+"""Linear algebra on compressed matrices (reference kernels.py:1-285), on the device.
+
+Reference-API mirror: ``CompressedMatrix``, ``matvec``, ``vecmat``, ``matmat_right``,
+``matmat_left``, ``kernel_cost``, ``OpCounter``.  Each call runs the sm_100a kernels of
+libtoc_b200.so on the matrix's device-resident TOC1 block; the operation counters are charged
+from the block metadata with the reference's closed form (kernels.py:250-266), which its kernels
+report exactly.
+
+``BatchSweep`` is the batched public entry point: many mini-batches' TOC1 bytes on the host,
+one call = upload + validate + A.v and v^T.A for every batch + download.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .arena import BlockArena
+from .codec import LogicalEncoding, compress_csr
+from .matrix import DenseMatrix, SparseRowMatrix, as_vector
+
+KERNEL_KINDS = ("matvec", "vecmat", "matmat_right", "matmat_left")
+
+
+@dataclass
+class OpCounter:
+    """Tally of work done by compressed kernels (kernels.py:32-38)."""
+
+    multiply_adds: int = 0
+    tree_nodes_visited: int = 0
+    codes_visited: int = 0
+
+
+class CompressedMatrix:
+    """A TOC1 block resident on the device plus its logical encoding (kernels.py:41-84).
+
+    The device "tree" (the par/key tables the kernels rebuild in shared memory) costs nothing to
+    keep, so there is no lazy host tree build; ``tree`` materialises the reference's DecodeTree
+    on demand, once, under a lock (kernels.py:68-77)."""
+
+    __slots__ = ("_enc", "_arena", "_lock", "_tree", "_block")
+
+    def __init__(self, encoding: LogicalEncoding | None = None, *, _arena: BlockArena | None = None):
+        self._enc = encoding
+        self._arena = _arena
+        self._lock = threading.Lock()
+        self._tree = None
+        self._block = None
+
+    @classmethod
+    def from_sparse(cls, s: SparseRowMatrix) -> "CompressedMatrix":
+        arena, logical = compress_csr(s.n_cols, s.row_ptr, s.cols, s.vals, np.array([0, s.n_rows], np.int64),
+                                      keep_logical=True)
+        ic, iv, cd, of = logical[0]
+        cdl = cd.tolist()
+        enc = LogicalEncoding(n_rows=s.n_rows, n_cols=s.n_cols,
+                              pairs=[(int(c), float(v)) for c, v in zip(ic.tolist(), iv.tolist())],
+                              rows=[cdl[of[i] : of[i + 1]] for i in range(s.n_rows)])
+        return cls(enc, _arena=arena)
+
+    @property
+    def encoding(self) -> LogicalEncoding:
+        return self._enc
+
+    @property
+    def arena(self) -> BlockArena:
+        if self._arena is None:
+            from .physical import serialize_block
+
+            with self._lock:
+                if self._arena is None:
+                    self._arena = BlockArena.from_bytes([serialize_block(self._enc)])
+        return self._arena
+
+    @property
+    def n_rows(self) -> int:
+        return self._enc.n_rows
+
+    @property
+    def n_cols(self) -> int:
+        return self._enc.n_cols
+
+    @property
+    def tree(self):
+        if self._tree is None:
+            with self._lock:
+                if self._tree is None:
+                    from .codec_tree import build_prefix_tree
+
+                    self._tree = build_prefix_tree(self._enc)
+        return self._tree
+
+    def decode(self) -> SparseRowMatrix:
+        from .codec_tree import decode
+
+        return decode(self._enc)
+
+    def _charge(self, counter: OpCounter | None, width: int) -> None:
+        if counter is not None:
+            m = self.arena.meta[0]
+            nodes = int(m["n_pairs"]) + int(m["n_derived"])
+            codes = int(m["n_codes"])
+            counter.multiply_adds += (nodes + codes) * width
+            counter.tree_nodes_visited += nodes
+            counter.codes_visited += codes
+
+    def __repr__(self):
+        e = self._enc
+        return f"CompressedMatrix({e.n_rows}x{e.n_cols}, I={len(e.pairs)}, codes={e.total_codes})"
+
+
+def _dev(x: np.ndarray):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x, np.float64)).cuda()
+
+
+def matvec(a: CompressedMatrix, v, counter: OpCounter | None = None) -> np.ndarray:
+    """A @ v without decompressing A (kernels.py:115-142, Algorithm 5)."""
+    vec = as_vector(v, a.n_cols, "vector")
+    arena = a.arena
+    arena.raise_corrupt()
+    R = arena.matvec(_dev(vec)) if a.n_cols else None
+    out = R.cpu().numpy() if R is not None else np.zeros(a.n_rows)
+    a._charge(counter, 1)
+    return np.asarray(out, dtype=np.float64)
+
+
+def vecmat(v, a: CompressedMatrix, counter: OpCounter | None = None) -> np.ndarray:
+    """v @ A without decompressing A (kernels.py:145-174, Algorithm 6)."""
+    vec = as_vector(v, a.n_rows, "vector")
+    arena = a.arena
+    arena.raise_corrupt()
+    out = arena.vecmat(_dev(vec))[0].cpu().numpy() if a.n_cols else np.zeros(0)
+    a._charge(counter, 1)
+    return np.asarray(out, dtype=np.float64)
+
+
+def kernel_cost(a: CompressedMatrix, kind: str, width: int = 1) -> int:
+    """Predicted multiply-add count (kernels.py:250-266)."""
+    if kind not in KERNEL_KINDS:
+        raise ValueError(f"unknown kernel kind {kind!r}; expected one of {KERNEL_KINDS}")
+    if width < 1:
+        raise ValueError(f"width must be positive, got {width}")
+    if kind in ("matvec", "vecmat") and width != 1:
+        raise ValueError(f"{kind} has a single lane; width {width} is meaningless")
+    e = a.encoding
+    return (len(e.pairs) + e.derived_node_count() + e.total_codes) * width
+
+
+def dense_kernel_cost(n_rows: int, n_cols: int, kind: str, width: int = 1) -> int:
+    if kind not in KERNEL_KINDS:
+        raise ValueError(f"unknown kernel kind {kind!r}; expected one of {KERNEL_KINDS}")
+    return 2 * n_rows * n_cols * width
+
+
+def csr_kernel_cost(nnz: int, kind: str, width: int = 1) -> int:
+    if kind not in KERNEL_KINDS:
+        raise ValueError(f"unknown kernel kind {kind!r}; expected one of {KERNEL_KINDS}")
+    return 2 * nnz * width
+
+
+class BatchSweep:
+    """Public batched API over host-resident TOC1 blocks.
+
+    ``run(v, u)`` uploads the blocks and operands from pinned host memory, validates/indexes the
+    blocks on the device, runs A.v and v^T.A for every batch in one fused launch, and returns
+    host arrays (R: concatenated row results, O: one n_cols row per batch).  This replaces the
+    reference's per-batch loop over ``matvec`` / ``vecmat`` (cli.py:340-356)."""
+
+    def __init__(self, blocks_h: np.ndarray, block_off, block_len):
+        torch = N.require_cuda()
+        self.torch = torch
+        nbytes = int(len(blocks_h))
+        self.host = torch.empty(max(nbytes, 16), dtype=torch.uint8, pin_memory=True)
+        self.host.numpy()[:nbytes] = blocks_h[:nbytes]
+        self.nbytes = nbytes
+        self.dev = torch.empty_like(self.host, device="cuda")
+        self.dev.copy_(self.host)
+        self.arena = BlockArena(self.dev, block_off, block_len)
+        self.n_rows = self.arena.n_rows_total
+        self.n_cols = self.arena.n_cols
+        nb = self.arena.n_blocks
+        self.v_h = torch.empty(max(self.n_cols, 1), dtype=torch.float64, pin_memory=True)
+        self.u_h = torch.empty(max(self.n_rows, 1), dtype=torch.float64, pin_memory=True)
+        self.v_d = torch.empty_like(self.v_h, device="cuda")
+        self.u_d = torch.empty_like(self.u_h, device="cuda")
+        self.R_d = torch.empty(max(self.n_rows, 1), dtype=torch.float64, device="cuda")
+        self.O_d = torch.empty((max(nb, 1), max(self.n_cols, 1)), dtype=torch.float64, device="cuda")
+        self.R_h = torch.empty_like(self.R_d, device="cpu").pin_memory()
+        self.O_h = torch.empty_like(self.O_d, device="cpu").pin_memory()
+        self.meta_h = torch.empty(self.arena.meta_d.numel(), dtype=torch.uint8, pin_memory=True)
+        self.h2d_bytes = nbytes + 8 * self.n_cols + 8 * self.n_rows
+        self.d2h_bytes = 8 * self.n_rows + 8 * nb * self.n_cols + self.arena.meta_d.numel()
+
+    @classmethod
+    def from_host_blocks(cls, blocks_h, block_off, block_len) -> "BatchSweep":
+        return cls(np.asarray(blocks_h, np.uint8), block_off, block_len)
+
+    def run(self, v, u):
+        torch = self.torch
+        a = self.arena
+        self.v_h.numpy()[: self.n_cols] = as_vector(v, self.n_cols, "vector")
+        self.u_h.numpy()[: self.n_rows] = as_vector(u, self.n_rows, "vector")
+        self.dev.copy_(self.host, non_blocking=True)
+        self.v_d.copy_(self.v_h, non_blocking=True)
+        self.u_d.copy_(self.u_h, non_blocking=True)
+        rc = N.lib().toc_index_blocks(a.data.data_ptr(), a.block_off_d.data_ptr(), a.block_len_d.data_ptr(),
+                                      a.n_blocks, a.meta_d.data_ptr(), N.stream_handle())
+        N.check(rc, "toc_index_blocks")
+        a.linalg(N.TOC_MATVEC | N.TOC_VECMAT, v=self.v_d, u=self.u_d, R=self.R_d, O=self.O_d)
+        self.R_h.copy_(self.R_d, non_blocking=True)
+        self.O_h.copy_(self.O_d, non_blocking=True)
+        self.meta_h.copy_(a.meta_d, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        meta = np.frombuffer(self.meta_h.numpy().tobytes(), dtype=N.META_DTYPE)[: a.n_blocks]
+        if np.any(meta["status"] != N.TOC_OK) or np.any(meta["corrupt"] != 0):
+            a.meta = meta.copy()
+            a.raise_format_errors()
+            a.raise_corrupt()
+        return self.R_h.numpy()[: self.n_rows], self.O_h.numpy()[: a.n_blocks, : self.n_cols]
