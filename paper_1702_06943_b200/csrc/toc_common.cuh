@@ -62,3 +62,53 @@ TOC_D uint32_t warp_excl_scan(uint32_t v, uint32_t lane) {
 TOC_HD uint32_t align16(uint32_t x) { return (x + 15u) & ~15u; }
 
 }  // namespace toc
+
+namespace toc {
+
+// ---- warp-cooperative unpack of packed ints ------------------------------------------------
+// A TOC1 section packs fixed-width (W = 1..4 bytes) little-endian ints at an arbitrary byte
+// offset (physical.py:54-68).  A warp unpacks a range [lo, hi) in tiles of kTile values: the
+// covering aligned 32-bit words are loaded once, coalesced, into a per-warp shared staging
+// buffer, and each lane extracts its values with a funnel shift.  f(i, value) is called for
+// every i, lane-parallel.  Reading to the next 4-byte boundary past the section is safe because
+// every block in an arena starts on, and is padded to, a 16-byte boundary.
+constexpr uint32_t kTile = 64;
+constexpr uint32_t kStageWords = kTile + 4;  // (3 + 64*4 + 3) / 4 = 65.5 -> 66 words + guard
+
+template <int W, typename F>
+TOC_D void warp_unpack(const uint8_t* __restrict__ sec, uint32_t lo, uint32_t hi, uint32_t* stage,
+                       uint32_t lane, F&& f) {
+  for (uint32_t t = lo; t < hi; t += kTile) {
+    const uint32_t n = min(kTile, hi - t);
+    const uintptr_t b0 = reinterpret_cast<uintptr_t>(sec) + (uintptr_t)t * W;
+    const uintptr_t a0 = b0 & ~(uintptr_t)3;
+    const uint32_t nw = (uint32_t)((((b0 + (uintptr_t)n * W) + 3) & ~(uintptr_t)3) - a0) >> 2;
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(a0);
+    for (uint32_t k = lane; k < nw; k += 32) stage[k] = __ldg(src + k);
+    if (lane == 0) stage[nw] = 0u;
+    __syncwarp();
+    const uint32_t d0 = (uint32_t)(b0 - a0);
+#pragma unroll 2
+    for (uint32_t j = lane; j < n; j += 32) {
+      const uint32_t off = d0 + j * W, q = off >> 2, s = (off & 3u) * 8u;
+      uint32_t v = __funnelshift_r(stage[q], stage[q + 1], s);
+      if constexpr (W < 4) v &= (1u << (8 * W)) - 1u;
+      f(t + j, v);
+    }
+    __syncwarp();
+  }
+}
+
+// Dispatch a runtime width to the templated unpack.
+template <typename F>
+TOC_D void warp_unpack_w(uint32_t w, const uint8_t* sec, uint32_t lo, uint32_t hi, uint32_t* stage,
+                         uint32_t lane, F&& f) {
+  switch (w) {
+    case 1: warp_unpack<1>(sec, lo, hi, stage, lane, f); break;
+    case 2: warp_unpack<2>(sec, lo, hi, stage, lane, f); break;
+    case 3: warp_unpack<3>(sec, lo, hi, stage, lane, f); break;
+    default: warp_unpack<4>(sec, lo, hi, stage, lane, f); break;
+  }
+}
+
+}  // namespace toc

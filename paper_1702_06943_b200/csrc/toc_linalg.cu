@@ -41,7 +41,7 @@ struct LinalgArgs {
 
 // Byte layout of one batch's tables (all regions 16-B aligned).
 struct BatchLayout {
-  uint32_t off_rowoff, off_dbase, off_uniq, off_tab, off_pk, total;
+  uint32_t off_rowoff, off_dbase, off_last, off_uniq, off_tab, off_pk, total;
 };
 
 template <bool kWide>
@@ -52,6 +52,8 @@ TOC_HD BatchLayout batch_layout(const TocBlockMeta& m) {
   o += align16(4u * (m.n_rows + 1));
   L.off_dbase = o;
   o += align16(4u * (m.n_rows + 1));
+  L.off_last = o;
+  o += align16(4u * (m.n_rows + 1));
   L.off_uniq = o;
   o += align16(8u * m.n_uniques);
   L.off_tab = o;
@@ -61,6 +63,11 @@ TOC_HD BatchLayout batch_layout(const TocBlockMeta& m) {
   L.total = o;
   return L;
 }
+
+// Fixed shared-memory prefix of every CTA: block-scan scratch + per-warp unpack staging.
+constexpr uint32_t kScanBytes = 256;
+constexpr uint32_t kStageBytes = 32u * kStageWords * 4u;  // sized for 32 warps
+constexpr uint32_t kFixedBytes = kScanBytes + kStageBytes;
 
 // Node-table accessors: narrow trees pack (par, key) as two u16 in one u32; wide ones use uint2.
 template <bool kWide>
@@ -116,19 +123,21 @@ TOC_D void scan_derived_base(const uint32_t* rowoff, uint32_t* dbase, uint32_t n
   }
 }
 
-// One batch: rebuild par/key, then the requested products.  `tab`, `pk`, `uniq`, `rowoff`,
-// `dbase` point either into shared memory or into this CTA's global slab.
+// One batch: rebuild par/key, then the requested products.  `tables` points either into shared
+// memory or into this CTA's global slab.
 template <bool kWide, bool kVecSmem>
 __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, const TocBlockMeta& m,
                                               uint8_t* tables, const double* vec_s, double* acc_s,
-                                              uint32_t* s_warp) {
+                                              uint32_t* s_warp, uint32_t* stage) {
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const uint8_t* blk = a.arena + a.block_off[b];
   const BatchLayout L = batch_layout<kWide>(m);
   uint32_t* rowoff = reinterpret_cast<uint32_t*>(tables + L.off_rowoff);
   uint32_t* dbase = reinterpret_cast<uint32_t*>(tables + L.off_dbase);
+  uint32_t* last = reinterpret_cast<uint32_t*>(tables + L.off_last);
   double* uniq = reinterpret_cast<double*>(tables + L.off_uniq);
   double* tab = reinterpret_cast<double*>(tables + L.off_tab);
+  uint32_t* tabw = reinterpret_cast<uint32_t*>(tab);  // tab viewed as words (ref staging)
   PK<kWide> pk;
   pk.p = reinterpret_cast<decltype(pk.p)>(tables + L.off_pk);
 
@@ -136,40 +145,54 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
   const uint8_t* cols = blk + m.off_cols;
   const uint8_t* refs = blk + m.off_refs;
   const uint8_t* codes = blk + m.off_codes;
-  const uint8_t* offs = blk + m.off_offsets;
-  const uint32_t wc = m.w_cols, wr = m.w_refs, wk = m.w_codes, wo = m.w_offsets;
+  const uint32_t wc = m.w_cols, wr = m.w_refs, wk = m.w_codes;
   const int64_t row_base = a.row_base[b];
   const int32_t ncol = a.n_cols;
   const double* vec = kVecSmem ? vec_s : a.v;
 
-  // ---- phase 0: row offsets, value index, derived-node bases --------------------------------
-  for (uint32_t r = tid; r <= n; r += blockDim.x) rowoff[r] = ld_packed(offs, r, wo);
+  // ---- phase 0: row offsets, value index ------------------------------------------------
+  if (warp == 0)
+    warp_unpack_w(m.w_offsets, blk + m.off_offsets, 0, n + 1, stage, lane,
+                  [&](uint32_t r, uint32_t v) { rowoff[r] = v; });
   for (uint32_t i = tid; i < nU; i += blockDim.x) uniq[i] = ld_f64_unaligned(blk + m.off_uniques + 8u * i);
   if ((a.kind & TOC_VECMAT) && kVecSmem)
     for (int32_t c = tid; c < ncol; c += blockDim.x) acc_s[c] = 0.0;
   __syncthreads();
   scan_derived_base(rowoff, dbase, n, s_warp);
 
-  // ---- phase 1: first-layer products (matvec) and par[] -------------------------------------
+  // ---- phase 1: one pass over the code stream: par[] (non-final codes) + last code per row,
+  //      and the first-layer products P1[i] = value_i * v[col_i] (matvec) ---------------------
+  for (uint32_t r = warp; r < n; r += nwarps) {
+    const uint32_t lo = rowoff[r], hi = rowoff[r + 1], db = dbase[r];
+    warp_unpack_w(wk, codes, lo, hi, stage, lane, [&](uint32_t j, uint32_t c) {
+      if (j + 1 < hi) pk.set_par(db + (j - lo), c);
+      else last[r] = c;
+    });
+  }
+  const uint32_t ntiles = (nI + kTile - 1) / kTile;
   if (a.kind & TOC_MATVEC) {
-    for (uint32_t i = tid; i < nI; i += blockDim.x) {
-      double val = uniq[ld_packed(refs, i, wr)];
-      tab[i + 1] = val * vec[ld_packed(cols, i, wc)];
+    for (uint32_t t = warp; t < ntiles; t += nwarps) {
+      const uint32_t lo = t * kTile, hi = min(nI, lo + kTile);
+      warp_unpack_w(wr, refs, lo, hi, stage, lane, [&](uint32_t i, uint32_t ref) { tabw[2 * (i + 1)] = ref; });
+      warp_unpack_w(wc, cols, lo, hi, stage, lane, [&](uint32_t i, uint32_t col) {
+        tab[i + 1] = uniq[tabw[2 * (i + 1)]] * vec[col];
+      });
     }
   } else {
     for (uint32_t i = tid; i <= nI; i += blockDim.x) tab[i] = 0.0;
   }
-  for (uint32_t r = warp; r < n; r += nwarps) {
-    const uint32_t lo = rowoff[r], hi = rowoff[r + 1], db = dbase[r];
-    for (uint32_t j = lo + lane; j + 1 < hi; j += 32) pk.set_par(db + (j - lo), ld_packed(codes, j, wk));
-  }
   __syncthreads();
+
+  // code at flat position j of row r: par[] for non-final positions, last[] for the final one
+  auto code_at = [&](uint32_t j, uint32_t lo, uint32_t hi, uint32_t db, uint32_t r) -> uint32_t {
+    return (j + 1 < hi) ? pk.par(db + (j - lo)) : last[r];
+  };
 
   // ---- phase 2: key[d] = F(next code): follow par[] down to the first layer -----------------
   for (uint32_t r = warp; r < n; r += nwarps) {
     const uint32_t lo = rowoff[r], hi = rowoff[r + 1], db = dbase[r];
     for (uint32_t j = lo + lane; j + 1 < hi; j += 32) {
-      uint32_t x = ld_packed(codes, j + 1, wk);
+      uint32_t x = code_at(j + 1, lo, hi, db, r);
       while (x > nI) x = pk.par(x - 1 - nI);
       pk.set_key(db + (j - lo), x);
     }
@@ -179,23 +202,20 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
   // ---- phase 3: A.v -------------------------------------------------------------------------
   if (a.kind & TOC_MATVEC) {
     for (uint32_t r = warp; r < n; r += nwarps) {
-      const uint32_t lo = rowoff[r], hi = rowoff[r + 1];
-      double acc = 0.0;
-      for (uint32_t base = lo; base < hi; base += 32) {
-        const uint32_t j = base + lane;
+      const uint32_t lo = rowoff[r], hi = rowoff[r + 1], db = dbase[r];
+      double part = 0.0;
+      for (uint32_t j = lo + lane; j < hi; j += 32) {
+        uint32_t x = code_at(j, lo, hi, db, r);
         double h = 0.0;
-        if (j < hi) {
-          uint32_t x = ld_packed(codes, j, wk);
-          while (x > nI) {
-            uint32_t p, k;
-            pk.get(x - 1 - nI, p, k);
-            h += tab[k];
-            x = p;
-          }
-          h += tab[x];
+        while (x > nI) {
+          uint32_t p, k;
+          pk.get(x - 1 - nI, p, k);
+          h += tab[k];
+          x = p;
         }
-        acc += warp_sum(h);
+        part += h + tab[x];
       }
+      const double acc = warp_sum(part);
       if (lane == 0) a.R[row_base + r] = acc;
     }
   }
@@ -208,10 +228,10 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
       __syncthreads();
     }
     for (uint32_t r = warp; r < n; r += nwarps) {
-      const uint32_t lo = rowoff[r], hi = rowoff[r + 1];
+      const uint32_t lo = rowoff[r], hi = rowoff[r + 1], db = dbase[r];
       const double w = a.u[row_base + r];
       for (uint32_t j = lo + lane; j < hi; j += 32) {
-        uint32_t x = ld_packed(codes, j, wk);
+        uint32_t x = code_at(j, lo, hi, db, r);
         while (x > nI) {
           uint32_t p, k;
           pk.get(x - 1 - nI, p, k);
@@ -223,12 +243,16 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
     }
     __syncthreads();
     double* out = kVecSmem ? acc_s : a.O + b * (int64_t)ncol;
-    for (uint32_t i = tid; i < nI; i += blockDim.x) {
-      const double g = tab[i + 1];
-      if (g != 0.0) {
-        double val = uniq[ld_packed(refs, i, wr)];
-        atomicAdd(&out[ld_packed(cols, i, wc)], val * g);
-      }
+    for (uint32_t t = warp; t < ntiles; t += nwarps) {
+      const uint32_t lo = t * kTile, hi = min(nI, lo + kTile);
+      // contribution value_i * G[i] replaces G[i] in place, then scatter by column
+      warp_unpack_w(wr, refs, lo, hi, stage, lane, [&](uint32_t i, uint32_t ref) {
+        tab[i + 1] = uniq[ref] * tab[i + 1];
+      });
+      warp_unpack_w(wc, cols, lo, hi, stage, lane, [&](uint32_t i, uint32_t col) {
+        const double g = tab[i + 1];
+        if (g != 0.0) atomicAdd(&out[col], g);
+      });
     }
     if (kVecSmem) {
       __syncthreads();
@@ -241,8 +265,9 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
 template <bool kWide, bool kVecSmem>
 __global__ void __launch_bounds__(1024, 1) linalg_kernel(LinalgArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  uint32_t* s_warp = reinterpret_cast<uint32_t*>(smem);  // 33 words, padded to 256 B
-  uint8_t* p = smem + 256;
+  uint32_t* s_warp = reinterpret_cast<uint32_t*>(smem);  // 33 words
+  uint32_t* stage = reinterpret_cast<uint32_t*>(smem + kScanBytes) + (threadIdx.x >> 5) * kStageWords;
+  uint8_t* p = smem + kFixedBytes;
   double* vec_s = nullptr;
   double* acc_s = nullptr;
   if (kVecSmem) {
@@ -264,9 +289,9 @@ __global__ void __launch_bounds__(1024, 1) linalg_kernel(LinalgArgs a) {
     const uint32_t need = batch_layout<kWide>(m).total;
     __syncthreads();
     if (need <= (uint32_t)a.batch_smem_budget)
-      process_batch<kWide, kVecSmem>(a, b, m, p, vec_s, acc_s, s_warp);
+      process_batch<kWide, kVecSmem>(a, b, m, p, vec_s, acc_s, s_warp, stage);
     else
-      process_batch<kWide, kVecSmem>(a, b, m, slab, vec_s, acc_s, s_warp);
+      process_batch<kWide, kVecSmem>(a, b, m, slab, vec_s, acc_s, s_warp, stage);
   }
 }
 
@@ -343,7 +368,7 @@ extern "C" int toc_plan(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t ki
   const int nvec = ((kind & TOC_MATVEC) ? 1 : 0) + ((kind & TOC_VECMAT) ? 1 : 0);
   const uint32_t vec_bytes = nvec * toc::align16(8u * (uint32_t)n_cols);
   plan->vec_in_smem = vec_bytes <= 64u * 1024u;
-  const uint32_t fixed = 256u + (plan->vec_in_smem ? vec_bytes : 0u);
+  const uint32_t fixed = toc::kFixedBytes + (plan->vec_in_smem ? vec_bytes : 0u);
   const uint32_t optin = (uint32_t)d.smem_optin;
   if (fixed + max_need <= optin) {
     plan->smem_bytes = (int32_t)(fixed + max_need);
@@ -383,7 +408,7 @@ extern "C" int toc_linalg(const uint8_t* d_arena, const int64_t* d_block_off, co
   a.kind = kind;
   a.n_cols = plan->n_cols;
   const int nvec = ((kind & TOC_MATVEC) ? 1 : 0) + ((kind & TOC_VECMAT) ? 1 : 0);
-  const uint32_t fixed = 256u + (plan->vec_in_smem ? nvec * toc::align16(8u * (uint32_t)plan->n_cols) : 0u);
+  const uint32_t fixed = toc::kFixedBytes + (plan->vec_in_smem ? nvec * toc::align16(8u * (uint32_t)plan->n_cols) : 0u);
   a.batch_smem_budget = plan->smem_bytes - (int32_t)fixed;
   a.slab_bytes = plan->global_tables ? plan->scratch_bytes / plan->ctas : 0;
   a.v = d_v;
