@@ -4,6 +4,8 @@ Layout (DESIGN.md "Data layout in HBM"):
   * ``data``: one uint8 buffer holding the exact TOC1 bytes of every batch (reference
     physical.py:1-21), batch b at ``block_off[b]``, each block 16-byte aligned;
   * ``meta``: one 68-byte TocBlockMeta per batch, written on the device by toc_index_blocks;
+  * 16 bytes of tail padding after the last block (the sequential unpackers may read one
+    aligned word past a section);
   * ``row_base``: the first row of each batch in the concatenated row space (outputs of A.v and
     the u operand of v^T.A are indexed by it).
 
@@ -81,7 +83,7 @@ class BlockArena:
         for i, n in enumerate(lens):
             offs[i] = pos
             pos = _align16(pos + int(n))
-        host = torch.zeros(max(pos, 16), dtype=torch.uint8, pin_memory=True)
+        host = torch.zeros(pos + 16, dtype=torch.uint8, pin_memory=True)  # +16: tail padding (unpackers)
         hv = host.numpy()
         for i, b in enumerate(blocks):
             hv[offs[i] : offs[i] + lens[i]] = np.frombuffer(b, dtype=np.uint8)

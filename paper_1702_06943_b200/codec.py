@@ -159,7 +159,7 @@ def compress_csr(n_cols: int, row_ptr, cols, vals, batch_row, *, max_work_bytes:
         for i in range(nb):
             boff[i] = pos
             pos = _align16(pos + int(blen[i]))
-        arena = torch.zeros(max(pos, 16), dtype=torch.uint8, device=dev)
+        arena = torch.zeros(pos + 16, dtype=torch.uint8, device=dev)  # +16: tail padding read by the unpackers
         d_boff = torch.from_numpy(boff).to(dev)
         N.check(L.toc_pack_blocks(nb, d_br.data_ptr(), d_eb.data_ptr(), I_cols.data_ptr(), refs.data_ptr(),
                                   uniques.data_ptr(), codes.data_ptr(), offsets.data_ptr(), info.data_ptr(),
@@ -179,7 +179,7 @@ def compress_csr(n_cols: int, row_ptr, cols, vals, batch_row, *, max_work_bytes:
         arena, boff, blen, _ = pieces[0]
     else:
         total = sum(p[3] for p in pieces)
-        arena = torch.empty(max(total, 16), dtype=torch.uint8, device=dev)
+        arena = torch.zeros(total + 16, dtype=torch.uint8, device=dev)
         boffs, blens, pos = [], [], 0
         for a, bo, bl, size in pieces:
             arena[pos : pos + size].copy_(a[:size])

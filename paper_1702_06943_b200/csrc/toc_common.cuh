@@ -112,3 +112,46 @@ TOC_D void warp_unpack_w(uint32_t w, const uint8_t* sec, uint32_t lo, uint32_t h
 }
 
 }  // namespace toc
+
+namespace toc {
+
+// Sequential reader of a packed-int section for one thread: walks values i0, i0+1, ... with one
+// aligned 32-bit load per 32/(8W) values and a funnel shift per value.  May read up to 4 bytes
+// past the last value; arenas carry 16 bytes of tail padding for that.
+template <int W>
+struct SeqReader {
+  const uint32_t* wp;
+  uint32_t cur, nxt, sh;
+  TOC_D void init(const uint8_t* __restrict__ sec, uint32_t i0) {
+    const uintptr_t b = reinterpret_cast<uintptr_t>(sec) + (uintptr_t)i0 * W;
+    wp = reinterpret_cast<const uint32_t*>(b & ~(uintptr_t)3);
+    sh = (uint32_t)(b & 3u) * 8u;
+    cur = __ldg(wp);
+    nxt = __ldg(wp + 1);
+  }
+  TOC_D uint32_t next() {
+    uint32_t v = __funnelshift_r(cur, nxt, sh);
+    if constexpr (W < 4) v &= (1u << (8 * W)) - 1u;
+    sh += 8u * W;
+    if (sh >= 32u) {
+      sh -= 32u;
+      cur = nxt;
+      ++wp;
+      nxt = __ldg(wp + 1);
+    }
+    return v;
+  }
+};
+
+// Call f.template operator()<W>() with the runtime width as a template argument.
+template <typename F>
+TOC_D void with_width(uint32_t w, F&& f) {
+  switch (w) {
+    case 1: f.template operator()<1>(); break;
+    case 2: f.template operator()<2>(); break;
+    case 3: f.template operator()<3>(); break;
+    default: f.template operator()<4>(); break;
+  }
+}
+
+}  // namespace toc

@@ -64,12 +64,13 @@ TOC_HD BatchLayout batch_layout(const TocBlockMeta& m) {
   return L;
 }
 
-// Fixed shared-memory prefix of every CTA: block-scan scratch + per-warp unpack staging.
-constexpr uint32_t kScanBytes = 256;
-constexpr uint32_t kStageBytes = 32u * kStageWords * 4u;  // sized for 32 warps
-constexpr uint32_t kFixedBytes = kScanBytes + kStageBytes;
+// Fixed shared-memory prefix of every CTA: block-scan scratch.
+constexpr uint32_t kFixedBytes = 256;
 
-// Node-table accessors: narrow trees pack (par, key) as two u16 in one u32; wide ones use uint2.
+// Node-table accessors.  Derived node d (id 1 + |I| + d) stores the two codes around the
+// position that created it: par = D-code at that position (its parent, codec.py:247) and
+// nxt = the following D-code, whose first pair is the one node d appends (codec.py:248-249).
+// Narrow trees pack (par, nxt) as two u16 in one u32; wide ones use uint2.
 template <bool kWide>
 struct PK;
 
@@ -77,12 +78,12 @@ template <>
 struct PK<false> {
   uint32_t* p;
   TOC_D void set_par(uint32_t d, uint32_t x) { reinterpret_cast<uint16_t*>(p)[2 * d] = (uint16_t)x; }
-  TOC_D void set_key(uint32_t d, uint32_t x) { reinterpret_cast<uint16_t*>(p)[2 * d + 1] = (uint16_t)x; }
+  TOC_D void set_nxt(uint32_t d, uint32_t x) { reinterpret_cast<uint16_t*>(p)[2 * d + 1] = (uint16_t)x; }
   TOC_D uint32_t par(uint32_t d) const { return reinterpret_cast<const uint16_t*>(p)[2 * d]; }
-  TOC_D void get(uint32_t d, uint32_t& par, uint32_t& key) const {
+  TOC_D void get(uint32_t d, uint32_t& par, uint32_t& nxt) const {
     uint32_t w = p[d];
     par = w & 0xffffu;
-    key = w >> 16;
+    nxt = w >> 16;
   }
 };
 
@@ -90,12 +91,12 @@ template <>
 struct PK<true> {
   uint2* p;
   TOC_D void set_par(uint32_t d, uint32_t x) { p[d].x = x; }
-  TOC_D void set_key(uint32_t d, uint32_t x) { p[d].y = x; }
+  TOC_D void set_nxt(uint32_t d, uint32_t x) { p[d].y = x; }
   TOC_D uint32_t par(uint32_t d) const { return p[d].x; }
-  TOC_D void get(uint32_t d, uint32_t& par, uint32_t& key) const {
+  TOC_D void get(uint32_t d, uint32_t& par, uint32_t& nxt) const {
     uint2 w = p[d];
     par = w.x;
-    key = w.y;
+    nxt = w.y;
   }
 };
 
@@ -123,13 +124,20 @@ TOC_D void scan_derived_base(const uint32_t* rowoff, uint32_t* dbase, uint32_t n
   }
 }
 
-// One batch: rebuild par/key, then the requested products.  `tables` points either into shared
-// memory or into this CTA's global slab.
+// Lanes per row: the largest power of two <= min(32, threads / rows).  Each thread then owns
+// one contiguous segment of one row, so the code stream is walked sequentially per thread.
+TOC_D uint32_t seg_lanes(uint32_t n, uint32_t nthreads) {
+  uint32_t s = 1;
+  while (s < 32 && 2 * s * (n ? n : 1) <= nthreads) s <<= 1;
+  return s;
+}
+
+// One batch.  `tables` points either into shared memory or into this CTA's global slab.
 template <bool kWide, bool kVecSmem>
 __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, const TocBlockMeta& m,
                                               uint8_t* tables, const double* vec_s, double* acc_s,
-                                              uint32_t* s_warp, uint32_t* stage) {
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+                                              uint32_t* s_warp) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nth = blockDim.x;
   const uint8_t* blk = a.arena + a.block_off[b];
   const BatchLayout L = batch_layout<kWide>(m);
   uint32_t* rowoff = reinterpret_cast<uint32_t*>(tables + L.off_rowoff);
@@ -145,41 +153,64 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
   const uint8_t* cols = blk + m.off_cols;
   const uint8_t* refs = blk + m.off_refs;
   const uint8_t* codes = blk + m.off_codes;
-  const uint32_t wc = m.w_cols, wr = m.w_refs, wk = m.w_codes;
   const int64_t row_base = a.row_base[b];
   const int32_t ncol = a.n_cols;
   const double* vec = kVecSmem ? vec_s : a.v;
 
-  // ---- phase 0: row offsets, value index ------------------------------------------------
-  if (warp == 0)
-    warp_unpack_w(m.w_offsets, blk + m.off_offsets, 0, n + 1, stage, lane,
-                  [&](uint32_t r, uint32_t v) { rowoff[r] = v; });
-  for (uint32_t i = tid; i < nU; i += blockDim.x) uniq[i] = ld_f64_unaligned(blk + m.off_uniques + 8u * i);
+  // ---- phase 0: row offsets, value index, derived-node bases --------------------------------
+  if (warp == 0) {
+    const uint32_t per = (n + 1 + 31) / 32, i0 = min(n + 1, lane * per), i1 = min(n + 1, i0 + per);
+    with_width(m.w_offsets, [&]<int W>() {
+      if (i0 < i1) {
+        SeqReader<W> rd;
+        rd.init(blk + m.off_offsets, i0);
+        for (uint32_t i = i0; i < i1; ++i) rowoff[i] = rd.next();
+      }
+    });
+  }
+  for (uint32_t i = tid; i < nU; i += nth) uniq[i] = ld_f64_unaligned(blk + m.off_uniques + 8u * i);
   if ((a.kind & TOC_VECMAT) && kVecSmem)
-    for (int32_t c = tid; c < ncol; c += blockDim.x) acc_s[c] = 0.0;
+    for (int32_t c = tid; c < ncol; c += nth) acc_s[c] = 0.0;
   __syncthreads();
   scan_derived_base(rowoff, dbase, n, s_warp);
 
-  // ---- phase 1: one pass over the code stream: par[] (non-final codes) + last code per row,
-  //      and the first-layer products P1[i] = value_i * v[col_i] (matvec) ---------------------
-  for (uint32_t r = warp; r < n; r += nwarps) {
-    const uint32_t lo = rowoff[r], hi = rowoff[r + 1], db = dbase[r];
-    warp_unpack_w(wk, codes, lo, hi, stage, lane, [&](uint32_t j, uint32_t c) {
-      if (j + 1 < hi) pk.set_par(db + (j - lo), c);
-      else last[r] = c;
-    });
-  }
-  const uint32_t ntiles = (nI + kTile - 1) / kTile;
+  const uint32_t S = seg_lanes(n, nth), RP = nth / S, passes = (n + RP - 1) / RP, sub = tid % S;
+  const uint32_t per_pair = (nI + nth - 1) / nth, p0 = min(nI, tid * per_pair), p1 = min(nI, p0 + per_pair);
+
+  // ---- phase 1: one sequential pass over each thread's code segment -------------------------
+  with_width(m.w_codes, [&]<int W>() {
+    for (uint32_t k = 0; k < passes; ++k) {
+      const uint32_t r = tid / S + k * RP;
+      if (r >= n) break;
+      const uint32_t lo = rowoff[r], hi = rowoff[r + 1], db = dbase[r], len = hi - lo;
+      const uint32_t j0 = lo + (len * sub) / S, j1 = lo + (len * (sub + 1)) / S;
+      if (j0 >= j1) continue;
+      SeqReader<W> rd;
+      rd.init(codes, j0);
+      for (uint32_t j = j0; j < j1; ++j) {
+        const uint32_t c = rd.next();
+        if (j + 1 < hi) pk.set_par(db + (j - lo), c);
+        else last[r] = c;
+        if (j > lo) pk.set_nxt(db + (j - 1 - lo), c);
+      }
+    }
+  });
+  // first-layer products P1[i] = value_i * v[col_i] (matvec), or G = 0 (vecmat)
   if (a.kind & TOC_MATVEC) {
-    for (uint32_t t = warp; t < ntiles; t += nwarps) {
-      const uint32_t lo = t * kTile, hi = min(nI, lo + kTile);
-      warp_unpack_w(wr, refs, lo, hi, stage, lane, [&](uint32_t i, uint32_t ref) { tabw[2 * (i + 1)] = ref; });
-      warp_unpack_w(wc, cols, lo, hi, stage, lane, [&](uint32_t i, uint32_t col) {
-        tab[i + 1] = uniq[tabw[2 * (i + 1)]] * vec[col];
+    if (p0 < p1) {
+      with_width(m.w_refs, [&]<int W>() {
+        SeqReader<W> rd;
+        rd.init(refs, p0);
+        for (uint32_t i = p0; i < p1; ++i) tabw[2 * (i + 1)] = rd.next();
+      });
+      with_width(m.w_cols, [&]<int W>() {
+        SeqReader<W> rd;
+        rd.init(cols, p0);
+        for (uint32_t i = p0; i < p1; ++i) tab[i + 1] = uniq[tabw[2 * (i + 1)]] * vec[rd.next()];
       });
     }
   } else {
-    for (uint32_t i = tid; i <= nI; i += blockDim.x) tab[i] = 0.0;
+    for (uint32_t i = tid; i <= nI; i += nth) tab[i] = 0.0;
   }
   __syncthreads();
 
@@ -187,55 +218,56 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
   auto code_at = [&](uint32_t j, uint32_t lo, uint32_t hi, uint32_t db, uint32_t r) -> uint32_t {
     return (j + 1 < hi) ? pk.par(db + (j - lo)) : last[r];
   };
+  // first-layer pair a node appends: F(nxt), F = follow par[] down to the first layer
+  auto key_of = [&](uint32_t nc) -> uint32_t {
+    while (nc > nI) nc = pk.par(nc - 1 - nI);
+    return nc;
+  };
 
-  // ---- phase 2: key[d] = F(next code): follow par[] down to the first layer -----------------
-  for (uint32_t r = warp; r < n; r += nwarps) {
-    const uint32_t lo = rowoff[r], hi = rowoff[r + 1], db = dbase[r];
-    for (uint32_t j = lo + lane; j + 1 < hi; j += 32) {
-      uint32_t x = code_at(j + 1, lo, hi, db, r);
-      while (x > nI) x = pk.par(x - 1 - nI);
-      pk.set_key(db + (j - lo), x);
-    }
-  }
-  __syncthreads();
-
-  // ---- phase 3: A.v -------------------------------------------------------------------------
+  // ---- phase 2: A.v -------------------------------------------------------------------------
   if (a.kind & TOC_MATVEC) {
-    for (uint32_t r = warp; r < n; r += nwarps) {
-      const uint32_t lo = rowoff[r], hi = rowoff[r + 1], db = dbase[r];
+    for (uint32_t k = 0; k < passes; ++k) {
+      const uint32_t r = tid / S + k * RP;
       double part = 0.0;
-      for (uint32_t j = lo + lane; j < hi; j += 32) {
-        uint32_t x = code_at(j, lo, hi, db, r);
-        double h = 0.0;
-        while (x > nI) {
-          uint32_t p, k;
-          pk.get(x - 1 - nI, p, k);
-          h += tab[k];
-          x = p;
+      if (r < n) {
+        const uint32_t lo = rowoff[r], hi = rowoff[r + 1], db = dbase[r], len = hi - lo;
+        const uint32_t j0 = lo + (len * sub) / S, j1 = lo + (len * (sub + 1)) / S;
+        for (uint32_t j = j0; j < j1; ++j) {
+          uint32_t x = code_at(j, lo, hi, db, r);
+          double h = 0.0;
+          while (x > nI) {
+            uint32_t p, nc;
+            pk.get(x - 1 - nI, p, nc);
+            h += tab[key_of(nc)];
+            x = p;
+          }
+          part += h + tab[x];
         }
-        part += h + tab[x];
       }
-      const double acc = warp_sum(part);
-      if (lane == 0) a.R[row_base + r] = acc;
+      for (uint32_t o = S >> 1; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if (r < n && sub == 0) a.R[row_base + r] = part;
     }
   }
 
-  // ---- phase 4: u^T.A -----------------------------------------------------------------------
+  // ---- phase 3: u^T.A -----------------------------------------------------------------------
   if (a.kind & TOC_VECMAT) {
     if (a.kind & TOC_MATVEC) {
       __syncthreads();
-      for (uint32_t i = tid; i <= nI; i += blockDim.x) tab[i] = 0.0;
+      for (uint32_t i = tid; i <= nI; i += nth) tab[i] = 0.0;
       __syncthreads();
     }
-    for (uint32_t r = warp; r < n; r += nwarps) {
-      const uint32_t lo = rowoff[r], hi = rowoff[r + 1], db = dbase[r];
+    for (uint32_t k = 0; k < passes; ++k) {
+      const uint32_t r = tid / S + k * RP;
+      if (r >= n) break;
+      const uint32_t lo = rowoff[r], hi = rowoff[r + 1], db = dbase[r], len = hi - lo;
+      const uint32_t j0 = lo + (len * sub) / S, j1 = lo + (len * (sub + 1)) / S;
       const double w = a.u[row_base + r];
-      for (uint32_t j = lo + lane; j < hi; j += 32) {
+      for (uint32_t j = j0; j < j1; ++j) {
         uint32_t x = code_at(j, lo, hi, db, r);
         while (x > nI) {
-          uint32_t p, k;
-          pk.get(x - 1 - nI, p, k);
-          atomicAdd(&tab[k], w);
+          uint32_t p, nc;
+          pk.get(x - 1 - nI, p, nc);
+          atomicAdd(&tab[key_of(nc)], w);
           x = p;
         }
         atomicAdd(&tab[x], w);
@@ -243,21 +275,27 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
     }
     __syncthreads();
     double* out = kVecSmem ? acc_s : a.O + b * (int64_t)ncol;
-    for (uint32_t t = warp; t < ntiles; t += nwarps) {
-      const uint32_t lo = t * kTile, hi = min(nI, lo + kTile);
+    if (p0 < p1) {
       // contribution value_i * G[i] replaces G[i] in place, then scatter by column
-      warp_unpack_w(wr, refs, lo, hi, stage, lane, [&](uint32_t i, uint32_t ref) {
-        tab[i + 1] = uniq[ref] * tab[i + 1];
+      with_width(m.w_refs, [&]<int W>() {
+        SeqReader<W> rd;
+        rd.init(refs, p0);
+        for (uint32_t i = p0; i < p1; ++i) tab[i + 1] = uniq[rd.next()] * tab[i + 1];
       });
-      warp_unpack_w(wc, cols, lo, hi, stage, lane, [&](uint32_t i, uint32_t col) {
-        const double g = tab[i + 1];
-        if (g != 0.0) atomicAdd(&out[col], g);
+      with_width(m.w_cols, [&]<int W>() {
+        SeqReader<W> rd;
+        rd.init(cols, p0);
+        for (uint32_t i = p0; i < p1; ++i) {
+          const uint32_t c = rd.next();
+          const double g = tab[i + 1];
+          if (g != 0.0) atomicAdd(&out[c], g);
+        }
       });
     }
     if (kVecSmem) {
       __syncthreads();
       double* o = a.O + b * (int64_t)ncol;
-      for (int32_t c = tid; c < ncol; c += blockDim.x) o[c] = acc_s[c];
+      for (int32_t c = tid; c < ncol; c += nth) o[c] = acc_s[c];
     }
   }
 }
@@ -266,7 +304,6 @@ template <bool kWide, bool kVecSmem>
 __global__ void __launch_bounds__(1024, 1) linalg_kernel(LinalgArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint32_t* s_warp = reinterpret_cast<uint32_t*>(smem);  // 33 words
-  uint32_t* stage = reinterpret_cast<uint32_t*>(smem + kScanBytes) + (threadIdx.x >> 5) * kStageWords;
   uint8_t* p = smem + kFixedBytes;
   double* vec_s = nullptr;
   double* acc_s = nullptr;
@@ -289,9 +326,9 @@ __global__ void __launch_bounds__(1024, 1) linalg_kernel(LinalgArgs a) {
     const uint32_t need = batch_layout<kWide>(m).total;
     __syncthreads();
     if (need <= (uint32_t)a.batch_smem_budget)
-      process_batch<kWide, kVecSmem>(a, b, m, p, vec_s, acc_s, s_warp, stage);
+      process_batch<kWide, kVecSmem>(a, b, m, p, vec_s, acc_s, s_warp);
     else
-      process_batch<kWide, kVecSmem>(a, b, m, slab, vec_s, acc_s, s_warp, stage);
+      process_batch<kWide, kVecSmem>(a, b, m, slab, vec_s, acc_s, s_warp);
   }
 }
 

@@ -176,7 +176,7 @@ class BatchSweep:
         torch = N.require_cuda()
         self.torch = torch
         nbytes = int(len(blocks_h))
-        self.host = torch.empty(max(nbytes, 16), dtype=torch.uint8, pin_memory=True)
+        self.host = torch.zeros(nbytes + 16, dtype=torch.uint8, pin_memory=True)  # +16 tail padding
         self.host.numpy()[:nbytes] = blocks_h[:nbytes]
         self.nbytes = nbytes
         self.dev = torch.empty_like(self.host, device="cuda")
