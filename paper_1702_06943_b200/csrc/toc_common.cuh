@@ -155,3 +155,33 @@ TOC_D void with_width(uint32_t w, F&& f) {
 }
 
 }  // namespace toc
+
+namespace toc {
+
+// Block-wide sum / max of a double over <= 32 warps; s_red holds 32 doubles.
+TOC_D double block_sum(double v, double* s_red) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) s_red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (uint32_t w = 0; w < nwarps; ++w) t += s_red[w];
+  __syncthreads();
+  return t;
+}
+
+TOC_D double block_max_d(double v, double* s_red) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  __syncthreads();
+  if (lane == 0) s_red[warp] = v;
+  __syncthreads();
+  double t = 0.0;
+  for (uint32_t w = 0; w < nwarps; ++w) t = fmax(t, s_red[w]);
+  __syncthreads();
+  return t;
+}
+
+}  // namespace toc

@@ -65,7 +65,7 @@ TOC_HD BatchLayout batch_layout(const TocBlockMeta& m) {
 }
 
 // Fixed shared-memory prefix of every CTA: block-scan scratch.
-constexpr uint32_t kFixedBytes = 256;
+constexpr uint32_t kFixedBytes = 512;  // s_warp (33 words) at 0, s_red (32 doubles) at 160
 
 // Node-table accessors.  Derived node d (id 1 + |I| + d) stores the two codes around the
 // position that created it: par = D-code at that position (its parent, codec.py:247) and
@@ -132,12 +132,39 @@ TOC_D uint32_t seg_lanes(uint32_t n, uint32_t nthreads) {
   return s;
 }
 
+// ---- exact fixed-point accumulation with native 32-bit shared/global atomics ---------------
+// fp64 atomics are CAS loops on sm_100a (shared) and the reduction order would make v^T.A
+// non-deterministic.  Instead each accumulator is a 64-bit two's-complement integer (lo, hi
+// words) holding value * 2^F; an add is atomicAdd on lo plus, when needed, atomicAdd of
+// (x_hi + carry) on hi, the carry taken from lo's returned old value.  Modular 64-bit addition
+// commutes, so concurrent adds are exact.  F is chosen per batch from an a-priori bound of the
+// largest partial sum (below), so nothing overflows; the conversion error per term is 2^-(F+1).
+TOC_D void fix_add(uint32_t* acc, long long x) {
+  const uint32_t xl = (uint32_t)x, xh = (uint32_t)((unsigned long long)x >> 32);
+  const uint32_t old = atomicAdd(acc, xl);
+  const uint32_t hi = xh + (old + xl < old ? 1u : 0u);
+  if (hi) atomicAdd(acc + 1, hi);
+}
+
+TOC_D double fix_value(const uint32_t* acc, double inv_scale) {
+  const long long v = (long long)(((unsigned long long)acc[1] << 32) | acc[0]);
+  return (double)v * inv_scale;
+}
+
+// 2^F such that |sum| <= bound stays below 2^62.
+TOC_D double fix_scale(double bound) {
+  if (!(bound > 0.0)) return 1.0;
+  int e;
+  frexp(bound, &e);  // bound < 2^e
+  return ldexp(1.0, 61 - e);
+}
+
 // One batch.  `tables` points either into shared memory or into this CTA's global slab.
 template <bool kWide, bool kVecSmem>
 __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, const TocBlockMeta& m,
-                                              uint8_t* tables, const double* vec_s, double* acc_s,
-                                              uint32_t* s_warp) {
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nth = blockDim.x;
+                                              uint8_t* tables, const double* vec_s, uint32_t* acc_s,
+                                              uint32_t* s_warp, double* s_red) {
+  const uint32_t tid = threadIdx.x, nth = blockDim.x;
   const uint8_t* blk = a.arena + a.block_off[b];
   const BatchLayout L = batch_layout<kWide>(m);
   uint32_t* rowoff = reinterpret_cast<uint32_t*>(tables + L.off_rowoff);
@@ -145,7 +172,7 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
   uint32_t* last = reinterpret_cast<uint32_t*>(tables + L.off_last);
   double* uniq = reinterpret_cast<double*>(tables + L.off_uniq);
   double* tab = reinterpret_cast<double*>(tables + L.off_tab);
-  uint32_t* tabw = reinterpret_cast<uint32_t*>(tab);  // tab viewed as words (ref staging)
+  uint32_t* tabw = reinterpret_cast<uint32_t*>(tab);  // tab as words: ref staging / fixed point
   PK<kWide> pk;
   pk.p = reinterpret_cast<decltype(pk.p)>(tables + L.off_pk);
 
@@ -156,23 +183,30 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
   const int64_t row_base = a.row_base[b];
   const int32_t ncol = a.n_cols;
   const double* vec = kVecSmem ? vec_s : a.v;
+  const bool do_mv = a.kind & TOC_MATVEC, do_vm = a.kind & TOC_VECMAT;
 
-  // ---- phase 0: row offsets, value index, derived-node bases --------------------------------
-  if (warp == 0) {
-    const uint32_t per = (n + 1 + 31) / 32, i0 = min(n + 1, lane * per), i1 = min(n + 1, i0 + per);
-    with_width(m.w_offsets, [&]<int W>() {
-      if (i0 < i1) {
-        SeqReader<W> rd;
-        rd.init(blk + m.off_offsets, i0);
-        for (uint32_t i = i0; i < i1; ++i) rowoff[i] = rd.next();
-      }
-    });
+  // ---- phase 0: row offsets, value index, bounds for the fixed-point scales -----------------
+  const uint32_t wo = m.w_offsets;
+  for (uint32_t r = tid; r <= n; r += nth) rowoff[r] = ld_packed(blk + m.off_offsets, r, wo);
+  double umax = 0.0, vmax = 0.0;
+  for (uint32_t i = tid; i < nU; i += nth) {
+    const double x = ld_f64_unaligned(blk + m.off_uniques + 8u * i);
+    uniq[i] = x;
+    vmax = fmax(vmax, fabs(x));
   }
-  for (uint32_t i = tid; i < nU; i += nth) uniq[i] = ld_f64_unaligned(blk + m.off_uniques + 8u * i);
-  if ((a.kind & TOC_VECMAT) && kVecSmem)
-    for (int32_t c = tid; c < ncol; c += nth) acc_s[c] = 0.0;
+  if (do_vm) {
+    for (uint32_t r = tid; r < n; r += nth) umax += fabs(a.u[row_base + r]);
+    if (kVecSmem)
+      for (int32_t c = tid; c < 2 * ncol; c += nth) acc_s[c] = 0u;
+  }
   __syncthreads();
   scan_derived_base(rowoff, dbase, n, s_warp);
+  double g_scale = 1.0, o_scale = 1.0;
+  if (do_vm) {  // sum |u| over the batch and max |value|: the a-priori bounds (see fix_add)
+    const double su = block_sum(umax, s_red), mv = block_max_d(vmax, s_red);
+    g_scale = fix_scale(su);
+    o_scale = fix_scale(su * mv);
+  }
 
   const uint32_t S = seg_lanes(n, nth), RP = nth / S, passes = (n + RP - 1) / RP, sub = tid % S;
   const uint32_t per_pair = (nI + nth - 1) / nth, p0 = min(nI, tid * per_pair), p1 = min(nI, p0 + per_pair);
@@ -195,8 +229,8 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
       }
     }
   });
-  // first-layer products P1[i] = value_i * v[col_i] (matvec), or G = 0 (vecmat)
-  if (a.kind & TOC_MATVEC) {
+  // first-layer products P1[i] = value_i * v[col_i] (matvec), or G = 0 (vecmat only)
+  if (do_mv) {
     if (p0 < p1) {
       with_width(m.w_refs, [&]<int W>() {
         SeqReader<W> rd;
@@ -214,44 +248,61 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
   }
   __syncthreads();
 
-  // code at flat position j of row r: par[] for non-final positions, last[] for the final one
-  auto code_at = [&](uint32_t j, uint32_t lo, uint32_t hi, uint32_t db, uint32_t r) -> uint32_t {
-    return (j + 1 < hi) ? pk.par(db + (j - lo)) : last[r];
-  };
-  // first-layer pair a node appends: F(nxt), F = follow par[] down to the first layer
-  auto key_of = [&](uint32_t nc) -> uint32_t {
-    while (nc > nI) nc = pk.par(nc - 1 - nI);
-    return nc;
+  // The walk of one code: a flattened loop, one shared-memory access per iteration, so lanes
+  // with long and short chains stay converged.  A derived node contributes the first pair of its
+  // nxt code (its key, codec.py:248-249); resolving that key follows par links to the first
+  // layer.  visit(i) is called once per pair of the code, i = first-layer id.
+  auto walk_segment = [&](uint32_t r, uint32_t j0, uint32_t j1, uint32_t lo, uint32_t hi, uint32_t db,
+                          auto&& visit) {
+    uint32_t j = j0, x = 0, kk = 0;
+    for (;;) {
+      uint32_t node;
+      if (kk) {
+        node = kk;
+      } else {
+        if (x == 0) {
+          if (j >= j1) break;
+          x = (j + 1 < hi) ? pk.par(db + (j - lo)) : last[r];
+          ++j;
+        }
+        node = x;
+      }
+      if (node <= nI) {
+        visit(node);
+        if (kk) kk = 0;
+        else x = 0;
+      } else {
+        uint32_t p, nc;
+        pk.get(node - 1 - nI, p, nc);
+        if (kk) {
+          kk = p;
+        } else {
+          x = p;
+          kk = nc;
+        }
+      }
+    }
   };
 
   // ---- phase 2: A.v -------------------------------------------------------------------------
-  if (a.kind & TOC_MATVEC) {
+  if (do_mv) {
     for (uint32_t k = 0; k < passes; ++k) {
       const uint32_t r = tid / S + k * RP;
       double part = 0.0;
       if (r < n) {
         const uint32_t lo = rowoff[r], hi = rowoff[r + 1], db = dbase[r], len = hi - lo;
         const uint32_t j0 = lo + (len * sub) / S, j1 = lo + (len * (sub + 1)) / S;
-        for (uint32_t j = j0; j < j1; ++j) {
-          uint32_t x = code_at(j, lo, hi, db, r);
-          double h = 0.0;
-          while (x > nI) {
-            uint32_t p, nc;
-            pk.get(x - 1 - nI, p, nc);
-            h += tab[key_of(nc)];
-            x = p;
-          }
-          part += h + tab[x];
-        }
+        walk_segment(r, j0, j1, lo, hi, db, [&](uint32_t i) { part += tab[i]; });
       }
+      __syncwarp();
       for (uint32_t o = S >> 1; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
       if (r < n && sub == 0) a.R[row_base + r] = part;
     }
   }
 
   // ---- phase 3: u^T.A -----------------------------------------------------------------------
-  if (a.kind & TOC_VECMAT) {
-    if (a.kind & TOC_MATVEC) {
+  if (do_vm) {
+    if (do_mv) {
       __syncthreads();
       for (uint32_t i = tid; i <= nI; i += nth) tab[i] = 0.0;
       __syncthreads();
@@ -261,41 +312,41 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
       if (r >= n) break;
       const uint32_t lo = rowoff[r], hi = rowoff[r + 1], db = dbase[r], len = hi - lo;
       const uint32_t j0 = lo + (len * sub) / S, j1 = lo + (len * (sub + 1)) / S;
-      const double w = a.u[row_base + r];
-      for (uint32_t j = j0; j < j1; ++j) {
-        uint32_t x = code_at(j, lo, hi, db, r);
-        while (x > nI) {
-          uint32_t p, nc;
-          pk.get(x - 1 - nI, p, nc);
-          atomicAdd(&tab[key_of(nc)], w);
-          x = p;
-        }
-        atomicAdd(&tab[x], w);
-      }
+      const long long w = __double2ll_rn(a.u[row_base + r] * g_scale);
+      if (w == 0) continue;
+      walk_segment(r, j0, j1, lo, hi, db, [&](uint32_t i) { fix_add(tabw + 2 * i, w); });
     }
     __syncthreads();
-    double* out = kVecSmem ? acc_s : a.O + b * (int64_t)ncol;
+    uint32_t* out = kVecSmem ? acc_s : reinterpret_cast<uint32_t*>(a.O + b * (int64_t)ncol);
+    const double g_inv = 1.0 / g_scale;
     if (p0 < p1) {
       // contribution value_i * G[i] replaces G[i] in place, then scatter by column
       with_width(m.w_refs, [&]<int W>() {
         SeqReader<W> rd;
         rd.init(refs, p0);
-        for (uint32_t i = p0; i < p1; ++i) tab[i + 1] = uniq[rd.next()] * tab[i + 1];
+        for (uint32_t i = p0; i < p1; ++i) tab[i + 1] = uniq[rd.next()] * fix_value(tabw + 2 * (i + 1), g_inv);
       });
       with_width(m.w_cols, [&]<int W>() {
         SeqReader<W> rd;
         rd.init(cols, p0);
         for (uint32_t i = p0; i < p1; ++i) {
           const uint32_t c = rd.next();
-          const double g = tab[i + 1];
-          if (g != 0.0) atomicAdd(&out[c], g);
+          const long long g = __double2ll_rn(tab[i + 1] * o_scale);
+          if (g) fix_add(out + 2 * c, g);
         }
       });
     }
+    __syncthreads();
+    const double o_inv = 1.0 / o_scale;
+    double* o = a.O + b * (int64_t)ncol;
     if (kVecSmem) {
-      __syncthreads();
-      double* o = a.O + b * (int64_t)ncol;
-      for (int32_t c = tid; c < ncol; c += nth) o[c] = acc_s[c];
+      for (int32_t c = tid; c < ncol; c += nth) o[c] = fix_value(acc_s + 2 * c, o_inv);
+    } else {
+      uint32_t* ow = reinterpret_cast<uint32_t*>(o);
+      for (int32_t c = tid; c < ncol; c += nth) {
+        const uint32_t w2[2] = {__ldcg(ow + 2 * c), __ldcg(ow + 2 * c + 1)};
+        o[c] = fix_value(w2, o_inv);
+      }
     }
   }
 }
@@ -305,15 +356,16 @@ __global__ void __launch_bounds__(1024, 1) linalg_kernel(LinalgArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint32_t* s_warp = reinterpret_cast<uint32_t*>(smem);  // 33 words
   uint8_t* p = smem + kFixedBytes;
+  double* s_red = reinterpret_cast<double*>(smem + 160);  // 12 doubles
   double* vec_s = nullptr;
-  double* acc_s = nullptr;
+  uint32_t* acc_s = nullptr;
   if (kVecSmem) {
     if (a.kind & TOC_MATVEC) {
       vec_s = reinterpret_cast<double*>(p);
       p += align16(8u * a.n_cols);
     }
     if (a.kind & TOC_VECMAT) {
-      acc_s = reinterpret_cast<double*>(p);
+      acc_s = reinterpret_cast<uint32_t*>(p);
       p += align16(8u * a.n_cols);
     }
     if (vec_s)
@@ -324,11 +376,18 @@ __global__ void __launch_bounds__(1024, 1) linalg_kernel(LinalgArgs a) {
     const TocBlockMeta m = a.meta[b];
     if (m.status != TOC_OK || m.corrupt) continue;  // host refuses such arenas up front
     const uint32_t need = batch_layout<kWide>(m).total;
+    if (threadIdx.x == 0 && b + gridDim.x < a.n_blocks) {  // pull the CTA's next block into L2
+      const TocBlockMeta& mn = a.meta[b + gridDim.x];
+      const uint32_t bytes = align16(mn.off_offsets + (mn.n_rows + 1u) * mn.w_offsets);
+      const uint8_t* nb = a.arena + a.block_off[b + gridDim.x];
+      if (mn.status == TOC_OK && bytes > 0)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nb), "r"(bytes) : "memory");
+    }
     __syncthreads();
     if (need <= (uint32_t)a.batch_smem_budget)
-      process_batch<kWide, kVecSmem>(a, b, m, p, vec_s, acc_s, s_warp);
+      process_batch<kWide, kVecSmem>(a, b, m, p, vec_s, acc_s, s_warp, s_red);
     else
-      process_batch<kWide, kVecSmem>(a, b, m, slab, vec_s, acc_s, s_warp);
+      process_batch<kWide, kVecSmem>(a, b, m, slab, vec_s, acc_s, s_warp, s_red);
   }
 }
 
