@@ -158,17 +158,20 @@ TOC_D void with_width(uint32_t w, F&& f) {
 
 namespace toc {
 
-// Block-wide sum / max of a double over <= 32 warps; s_red holds 32 doubles.
+// Block-wide sum / max of a double over <= 32 warps; s_red holds 33 doubles.
 TOC_D double block_sum(double v, double* s_red) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   v = warp_sum(v);
   __syncthreads();
   if (lane == 0) s_red[warp] = v;
   __syncthreads();
-  double t = 0.0;
-  for (uint32_t w = 0; w < nwarps; ++w) t += s_red[w];
+  if (warp == 0) {
+    double t = lane < nwarps ? s_red[lane] : 0.0;
+    t = warp_sum(t);
+    if (lane == 0) s_red[32] = t;
+  }
   __syncthreads();
-  return t;
+  return s_red[32];
 }
 
 TOC_D double block_max_d(double v, double* s_red) {
@@ -178,10 +181,14 @@ TOC_D double block_max_d(double v, double* s_red) {
   __syncthreads();
   if (lane == 0) s_red[warp] = v;
   __syncthreads();
-  double t = 0.0;
-  for (uint32_t w = 0; w < nwarps; ++w) t = fmax(t, s_red[w]);
+  if (warp == 0) {
+    double t = lane < nwarps ? s_red[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, o));
+    if (lane == 0) s_red[32] = t;
+  }
   __syncthreads();
-  return t;
+  return s_red[32];
 }
 
 }  // namespace toc

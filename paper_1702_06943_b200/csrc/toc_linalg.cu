@@ -65,12 +65,13 @@ TOC_HD BatchLayout batch_layout(const TocBlockMeta& m) {
 }
 
 // Fixed shared-memory prefix of every CTA: block-scan scratch.
-constexpr uint32_t kFixedBytes = 512;  // s_warp (33 words) at 0, s_red (32 doubles) at 160
+constexpr uint32_t kFixedBytes = 512;  // s_warp (33 words) at 0, s_red (33 doubles) at 160
 
-// Node-table accessors.  Derived node d (id 1 + |I| + d) stores the two codes around the
-// position that created it: par = D-code at that position (its parent, codec.py:247) and
-// nxt = the following D-code, whose first pair is the one node d appends (codec.py:248-249).
-// Narrow trees pack (par, nxt) as two u16 in one u32; wide ones use uint2.
+// Node-table accessors.  Derived node d (id 1 + |I| + d) stores par = the D-code at the
+// position that created it (its parent, codec.py:247) and, in the second field, first the
+// following D-code and then -- after the key pass -- the first-layer pair node d appends, the
+// first pair of that following code (codec.py:248-249).  Narrow trees pack the two fields as u16
+// halves of one u32; wide ones use uint2.
 template <bool kWide>
 struct PK;
 
@@ -80,6 +81,7 @@ struct PK<false> {
   TOC_D void set_par(uint32_t d, uint32_t x) { reinterpret_cast<uint16_t*>(p)[2 * d] = (uint16_t)x; }
   TOC_D void set_nxt(uint32_t d, uint32_t x) { reinterpret_cast<uint16_t*>(p)[2 * d + 1] = (uint16_t)x; }
   TOC_D uint32_t par(uint32_t d) const { return reinterpret_cast<const uint16_t*>(p)[2 * d]; }
+  TOC_D uint32_t nxt(uint32_t d) const { return reinterpret_cast<const uint16_t*>(p)[2 * d + 1]; }
   TOC_D void get(uint32_t d, uint32_t& par, uint32_t& nxt) const {
     uint32_t w = p[d];
     par = w & 0xffffu;
@@ -93,6 +95,7 @@ struct PK<true> {
   TOC_D void set_par(uint32_t d, uint32_t x) { p[d].x = x; }
   TOC_D void set_nxt(uint32_t d, uint32_t x) { p[d].y = x; }
   TOC_D uint32_t par(uint32_t d) const { return p[d].x; }
+  TOC_D uint32_t nxt(uint32_t d) const { return p[d].y; }
   TOC_D void get(uint32_t d, uint32_t& par, uint32_t& nxt) const {
     uint2 w = p[d];
     par = w.x;
@@ -248,39 +251,35 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
   }
   __syncthreads();
 
-  // The walk of one code: a flattened loop, one shared-memory access per iteration, so lanes
-  // with long and short chains stay converged.  A derived node contributes the first pair of its
-  // nxt code (its key, codec.py:248-249); resolving that key follows par links to the first
-  // layer.  visit(i) is called once per pair of the code, i = first-layer id.
+  // ---- key pass: the pair each derived node appends is the first pair of its next code:
+  //      follow par[] from that code down to the first layer (codec.py:248-251) ---------------
+  for (uint32_t k = 0; k < passes; ++k) {
+    const uint32_t r = tid / S + k * RP;
+    if (r >= n) break;
+    const uint32_t lo = rowoff[r], hi = rowoff[r + 1], db = dbase[r], len = hi - lo;
+    const uint32_t j0 = lo + (len * sub) / S, j1 = min(lo + (len * (sub + 1)) / S, hi - 1);
+    for (uint32_t j = j0; j < j1; ++j) {
+      const uint32_t d = db + (j - lo);
+      uint32_t x = pk.nxt(d);
+      while (x > nI) x = pk.par(x - 1 - nI);
+      pk.set_nxt(d, x);
+    }
+  }
+  __syncthreads();
+
+  // The walk of one code x: each derived node on the chain contributes its key, the first-layer
+  // node at the end contributes itself.  visit(i) is called once per pair, i = first-layer id.
   auto walk_segment = [&](uint32_t r, uint32_t j0, uint32_t j1, uint32_t lo, uint32_t hi, uint32_t db,
                           auto&& visit) {
-    uint32_t j = j0, x = 0, kk = 0;
-    for (;;) {
-      uint32_t node;
-      if (kk) {
-        node = kk;
-      } else {
-        if (x == 0) {
-          if (j >= j1) break;
-          x = (j + 1 < hi) ? pk.par(db + (j - lo)) : last[r];
-          ++j;
-        }
-        node = x;
+    for (uint32_t j = j0; j < j1; ++j) {
+      uint32_t x = (j + 1 < hi) ? pk.par(db + (j - lo)) : last[r];
+      while (x > nI) {
+        uint32_t p, key;
+        pk.get(x - 1 - nI, p, key);
+        visit(key);
+        x = p;
       }
-      if (node <= nI) {
-        visit(node);
-        if (kk) kk = 0;
-        else x = 0;
-      } else {
-        uint32_t p, nc;
-        pk.get(node - 1 - nI, p, nc);
-        if (kk) {
-          kk = p;
-        } else {
-          x = p;
-          kk = nc;
-        }
-      }
+      visit(x);
     }
   };
 
@@ -356,7 +355,7 @@ __global__ void __launch_bounds__(1024, 1) linalg_kernel(LinalgArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint32_t* s_warp = reinterpret_cast<uint32_t*>(smem);  // 33 words
   uint8_t* p = smem + kFixedBytes;
-  double* s_red = reinterpret_cast<double*>(smem + 160);  // 12 doubles
+  double* s_red = reinterpret_cast<double*>(smem + 160);  // 33 doubles
   double* vec_s = nullptr;
   uint32_t* acc_s = nullptr;
   if (kVecSmem) {
