@@ -80,6 +80,7 @@ struct PK<false> {
   uint32_t* p;
   TOC_D void set_par(uint32_t d, uint32_t x) { reinterpret_cast<uint16_t*>(p)[2 * d] = (uint16_t)x; }
   TOC_D void set_nxt(uint32_t d, uint32_t x) { reinterpret_cast<uint16_t*>(p)[2 * d + 1] = (uint16_t)x; }
+  TOC_D void set(uint32_t d, uint32_t par, uint32_t nxt) { p[d] = (par & 0xffffu) | (nxt << 16); }
   TOC_D uint32_t par(uint32_t d) const { return reinterpret_cast<const uint16_t*>(p)[2 * d]; }
   TOC_D uint32_t nxt(uint32_t d) const { return reinterpret_cast<const uint16_t*>(p)[2 * d + 1]; }
   TOC_D void get(uint32_t d, uint32_t& par, uint32_t& nxt) const {
@@ -94,6 +95,7 @@ struct PK<true> {
   uint2* p;
   TOC_D void set_par(uint32_t d, uint32_t x) { p[d].x = x; }
   TOC_D void set_nxt(uint32_t d, uint32_t x) { p[d].y = x; }
+  TOC_D void set(uint32_t d, uint32_t par, uint32_t nxt) { p[d] = make_uint2(par, nxt); }
   TOC_D uint32_t par(uint32_t d) const { return p[d].x; }
   TOC_D uint32_t nxt(uint32_t d) const { return p[d].y; }
   TOC_D void get(uint32_t d, uint32_t& par, uint32_t& nxt) const {
@@ -224,11 +226,15 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
       if (j0 >= j1) continue;
       SeqReader<W> rd;
       rd.init(codes, j0);
+      uint32_t c = rd.next();
       for (uint32_t j = j0; j < j1; ++j) {
-        const uint32_t c = rd.next();
-        if (j + 1 < hi) pk.set_par(db + (j - lo), c);
-        else last[r] = c;
-        if (j > lo) pk.set_nxt(db + (j - 1 - lo), c);
+        if (j + 1 < hi) {  // non-final: node (par = this code, nxt = next code), one store
+          const uint32_t cn = rd.next();
+          pk.set(db + (j - lo), c, cn);
+          c = cn;
+        } else {
+          last[r] = c;
+        }
       }
     }
   });
