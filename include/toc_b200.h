@@ -172,6 +172,34 @@ int toc_unpack_blocks(const uint8_t* d_arena, const int64_t* d_block_off, const 
                       const int64_t* d_offs_base, uint32_t* d_I_cols, double* d_I_vals,
                       uint32_t* d_codes, uint32_t* d_offsets, void* stream);
 
+/* ---- mini-batch gradient descent for GLMs (training.py:261-361) ---------------------------
+ * The arena's blocks are the epoch's mini-batches in order (shuffle_once + make_batches,
+ * training.py:131-167); labels are per row in the same order.  Losses: */
+enum { TOC_LOSS_SQUARED = 0, TOC_LOSS_LOGISTIC = 1, TOC_LOSS_HINGE = 2 };
+
+/* Device workspace (bytes) for toc_glm_epoch (kind 0) or toc_glm_grad (kind 1); host-only. */
+int toc_mgd_workspace(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t n_cols, int32_t kind,
+                      int64_t* scratch_bytes);
+
+/* One epoch: for each batch b in order, g = s^T A_b with s = loss'(A_b w, y_b) and
+ * w -= (lr / n_rows_b) * g (mgd_step, training.py:303-316).  One cooperative launch; d_sync:
+ * 2 device words of scratch (step counter, abort flag).  h_meta: host copy of the metadata. */
+int toc_glm_epoch(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+                  const TocBlockMeta* h_meta, const int64_t* d_row_base, int64_t n_blocks,
+                  int32_t n_cols, int32_t loss, double lr, const double* d_labels, double* d_w,
+                  uint32_t* d_sync, void* d_scratch, void* stream);
+
+/* Summed gradient of every batch at fixed w (glm_gradient, training.py:261-281):
+ * d_grad[b * n_cols + c].  The data-parallel trainer all-reduces these. */
+int toc_glm_grad(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+                 const TocBlockMeta* h_meta, const int64_t* d_row_base, int64_t n_blocks,
+                 int32_t n_cols, int32_t loss, const double* d_labels, const double* d_w,
+                 double* d_grad, void* d_scratch, void* stream);
+
+/* Per-row loss of empirical_risk (training.py:231-258) summed into n_partial partial sums. */
+int toc_glm_risk(const double* d_z, const double* d_y, int64_t n, int32_t loss, double* d_partial,
+                 int32_t n_partial, void* stream);
+
 /* ---- version / self-description ---------------------------------------------------------- */
 const char* toc_version(void);
 int toc_device_info(int32_t* sm_count, int32_t* smem_optin, int64_t* l2_bytes);

@@ -1,0 +1,347 @@
+// toc_batch.cuh -- per-mini-batch device machinery shared by the compressed linear-algebra
+// sweep (toc_linalg.cu) and the MGD kernels (toc_mgd.cu).
+//
+// Reference: codec.py:215-259 (build_prefix_tree: the decode tree C'), kernels.py:115-142
+// (matvec, Algorithm 5), kernels.py:145-174 (vecmat, Algorithm 6).
+//
+// One CTA works on one TOC1 block at a time.  It reads only the block's bytes and rebuilds in
+// shared memory (or in a global slab for oversized batches) the part of C' the products need:
+//   node[d] = (par, key) for derived node d = id - 1 - |I|:
+//     par = the D-code at the position that derived node d           (codec.py:247)
+//     key = the first-layer pair node d appends = first pair of the next D-code (codec.py:248)
+//   last[r] = the final code of row r (the only codes that derive no node)
+// so the code stream D itself is recoverable from node[] + last[] and is read from HBM once.
+// Node partial sums are never materialised: a code's contribution is produced by walking par
+// links down to the first layer, visiting key on the way (Algorithm 5's H recurrence unrolled).
+#pragma once
+#include "toc_common.cuh"
+
+namespace toc {
+
+// Byte layout of one batch's tables (all regions 16-B aligned).
+struct BatchLayout {
+  uint32_t off_rowoff, off_dbase, off_last, off_uniq, off_tab, off_pk, total;
+};
+
+template <bool kWide>
+TOC_HD BatchLayout batch_layout(const TocBlockMeta& m) {
+  BatchLayout L;
+  uint32_t o = 0;
+  L.off_rowoff = o;
+  o += align16(4u * (m.n_rows + 1));
+  L.off_dbase = o;
+  o += align16(4u * (m.n_rows + 1));
+  L.off_last = o;
+  o += align16(4u * (m.n_rows + 1));
+  L.off_uniq = o;
+  o += align16(8u * m.n_uniques);
+  L.off_tab = o;
+  o += align16(8u * (m.n_pairs + 1));
+  L.off_pk = o;
+  o += align16((kWide ? 8u : 4u) * m.n_derived);
+  L.total = o;
+  return L;
+}
+
+// Fixed shared-memory prefix of every CTA: block-scan words and block-reduction doubles.
+constexpr uint32_t kFixedBytes = 512;  // s_warp (33 words) at 0, s_red (33 doubles) at 160
+
+// Node table.  Narrow trees (< 65536 nodes) pack the two fields as u16 halves of one u32;
+// wide ones use uint2.  The second field first holds the next D-code and, after the key pass,
+// the key.
+template <bool kWide>
+struct PK;
+
+template <>
+struct PK<false> {
+  uint32_t* p;
+  TOC_D void set(uint32_t d, uint32_t par, uint32_t nxt) { p[d] = (par & 0xffffu) | (nxt << 16); }
+  TOC_D void set_key(uint32_t d, uint32_t x) { reinterpret_cast<uint16_t*>(p)[2 * d + 1] = (uint16_t)x; }
+  TOC_D uint32_t par(uint32_t d) const { return reinterpret_cast<const uint16_t*>(p)[2 * d]; }
+  TOC_D uint32_t nxt(uint32_t d) const { return reinterpret_cast<const uint16_t*>(p)[2 * d + 1]; }
+  TOC_D void get(uint32_t d, uint32_t& par, uint32_t& key) const {
+    uint32_t w = p[d];
+    par = w & 0xffffu;
+    key = w >> 16;
+  }
+};
+
+template <>
+struct PK<true> {
+  uint2* p;
+  TOC_D void set(uint32_t d, uint32_t par, uint32_t nxt) { p[d] = make_uint2(par, nxt); }
+  TOC_D void set_key(uint32_t d, uint32_t x) { p[d].y = x; }
+  TOC_D uint32_t par(uint32_t d) const { return p[d].x; }
+  TOC_D uint32_t nxt(uint32_t d) const { return p[d].y; }
+  TOC_D void get(uint32_t d, uint32_t& par, uint32_t& key) const {
+    uint2 w = p[d];
+    par = w.x;
+    key = w.y;
+  }
+};
+
+// Exclusive scan over rows of max(len-1, 0): the id base of the nodes each row derives.
+TOC_D void scan_derived_base(const uint32_t* rowoff, uint32_t* dbase, uint32_t n, uint32_t* s_warp) {
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  uint32_t carry = 0;
+  for (uint32_t base = 0; base < n; base += blockDim.x) {
+    uint32_t r = base + tid;
+    uint32_t len = (r < n) ? rowoff[r + 1] - rowoff[r] : 0u;
+    uint32_t v = len ? len - 1 : 0u;
+    uint32_t x = warp_excl_scan(v, lane);
+    if (lane == 31) s_warp[warp] = x + v;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t t = lane < nwarps ? s_warp[lane] : 0u;
+      uint32_t e = warp_excl_scan(t, lane);
+      if (lane < nwarps) s_warp[lane] = e;
+      if (lane == 31) s_warp[32] = e + t;
+    }
+    __syncthreads();
+    if (r < n) dbase[r] = carry + s_warp[warp] + x;
+    carry += s_warp[32];
+    __syncthreads();
+  }
+}
+
+// Lanes per row: the largest power of two <= min(32, threads / rows).  Each thread then owns
+// one contiguous segment of one row, so the code stream is walked sequentially per thread.
+TOC_D uint32_t seg_lanes(uint32_t n, uint32_t nthreads) {
+  uint32_t s = 1;
+  while (s < 32 && 2 * s * (n ? n : 1) <= nthreads) s <<= 1;
+  return s;
+}
+
+// ---- exact fixed-point accumulation with native 32-bit atomics -----------------------------
+// fp64 atomics are CAS loops on sm_100a (shared) and their order would make v^T.A
+// non-deterministic.  Each accumulator is a 64-bit two's-complement integer (lo, hi words)
+// holding value * 2^F; an add is atomicAdd on lo plus, when needed, atomicAdd of (x_hi + carry)
+// on hi, the carry taken from lo's returned old value.  Modular 64-bit addition commutes, so
+// concurrent adds are exact.  F is chosen from an a-priori bound of the largest partial sum so
+// nothing overflows; the conversion error per term is at most 2^-(F+1).
+TOC_D void fix_add(uint32_t* acc, long long x) {
+  const uint32_t xl = (uint32_t)x, xh = (uint32_t)((unsigned long long)x >> 32);
+  const uint32_t old = atomicAdd(acc, xl);
+  const uint32_t hi = xh + (old + xl < old ? 1u : 0u);
+  if (hi) atomicAdd(acc + 1, hi);
+}
+
+TOC_D double fix_value(uint32_t lo, uint32_t hi, double inv_scale) {
+  const long long v = (long long)(((unsigned long long)hi << 32) | lo);
+  return (double)v * inv_scale;
+}
+
+// 2^F such that |sum| <= bound stays below 2^62.
+TOC_D double fix_scale(double bound) {
+  if (!(bound > 0.0)) return 1.0;
+  int e;
+  frexp(bound, &e);  // bound < 2^e
+  return ldexp(1.0, 61 - e);
+}
+
+// ---- one batch in one CTA -------------------------------------------------------------------
+template <bool kWide>
+struct Batch {
+  const uint8_t* blk;
+  TocBlockMeta m;
+  uint32_t* rowoff;
+  uint32_t* dbase;
+  uint32_t* last;
+  double* uniq;
+  double* tab;     // P1 (matvec) or G (vecmat, fixed point), index = first-layer id
+  uint32_t* tabw;  // tab as words
+  PK<kWide> pk;
+  uint32_t n, nI, S, RP, passes, sub, p0, p1;
+  double vmax;     // max |value| over the value index (this thread's part until reduced)
+
+  TOC_D void init(const uint8_t* block, const TocBlockMeta& meta, uint8_t* tables) {
+    blk = block;
+    m = meta;
+    const BatchLayout L = batch_layout<kWide>(m);
+    rowoff = reinterpret_cast<uint32_t*>(tables + L.off_rowoff);
+    dbase = reinterpret_cast<uint32_t*>(tables + L.off_dbase);
+    last = reinterpret_cast<uint32_t*>(tables + L.off_last);
+    uniq = reinterpret_cast<double*>(tables + L.off_uniq);
+    tab = reinterpret_cast<double*>(tables + L.off_tab);
+    tabw = reinterpret_cast<uint32_t*>(tab);
+    pk.p = reinterpret_cast<decltype(pk.p)>(tables + L.off_pk);
+    n = m.n_rows;
+    nI = m.n_pairs;
+    const uint32_t nth = blockDim.x, tid = threadIdx.x;
+    S = seg_lanes(n, nth);
+    RP = nth / S;
+    passes = (n + RP - 1) / RP;
+    sub = tid % S;
+    const uint32_t per = (nI + nth - 1) / nth;
+    p0 = min(nI, tid * per);
+    p1 = min(nI, p0 + per);
+  }
+
+  // Row r's code range and this thread's segment of it.
+  TOC_D bool segment(uint32_t k, uint32_t& r, uint32_t& lo, uint32_t& hi, uint32_t& db, uint32_t& j0,
+                     uint32_t& j1) const {
+    r = threadIdx.x / S + k * RP;
+    if (r >= n) return false;
+    lo = rowoff[r];
+    hi = rowoff[r + 1];
+    db = dbase[r];
+    const uint32_t len = hi - lo;
+    j0 = lo + (len * sub) / S;
+    j1 = lo + (len * (sub + 1)) / S;
+    return true;
+  }
+
+  // Phase 0: row offsets, value index, derived-node bases.  Ends with a barrier.
+  TOC_D void load_index(uint32_t* s_warp) {
+    const uint32_t tid = threadIdx.x, nth = blockDim.x;
+    for (uint32_t r = tid; r <= n; r += nth) rowoff[r] = ld_packed(blk + m.off_offsets, r, m.w_offsets);
+    vmax = 0.0;
+    for (uint32_t i = tid; i < m.n_uniques; i += nth) {
+      const double x = ld_f64_unaligned(blk + m.off_uniques + 8u * i);
+      uniq[i] = x;
+      vmax = fmax(vmax, fabs(x));
+    }
+    __syncthreads();
+    scan_derived_base(rowoff, dbase, n, s_warp);
+  }
+
+  // Phase 1: one sequential pass over each thread's code segment: node[] + last[].
+  TOC_D void build_nodes() {
+    const uint8_t* codes = blk + m.off_codes;
+    with_width(m.w_codes, [&]<int W>() {
+      for (uint32_t k = 0; k < passes; ++k) {
+        uint32_t r, lo, hi, db, j0, j1;
+        if (!segment(k, r, lo, hi, db, j0, j1)) break;
+        if (j0 >= j1) continue;
+        SeqReader<W> rd;
+        rd.init(codes, j0);
+        uint32_t c = rd.next();
+        for (uint32_t j = j0; j < j1; ++j) {
+          if (j + 1 < hi) {  // non-final: node (par = this code, nxt = next code), one store
+            const uint32_t cn = rd.next();
+            pk.set(db + (j - lo), c, cn);
+            c = cn;
+          } else {
+            last[r] = c;
+          }
+        }
+      }
+    });
+  }
+
+  // Key pass (after a barrier following build_nodes): key = first pair of the next code, found
+  // by following par links down to the first layer (codec.py:248-251).
+  TOC_D void resolve_keys() {
+    for (uint32_t k = 0; k < passes; ++k) {
+      uint32_t r, lo, hi, db, j0, j1;
+      if (!segment(k, r, lo, hi, db, j0, j1)) break;
+      j1 = min(j1, hi - 1);
+      for (uint32_t j = j0; j < j1; ++j) {
+        const uint32_t d = db + (j - lo);
+        uint32_t x = pk.nxt(d);
+        while (x > nI) x = pk.par(x - 1 - nI);
+        pk.set_key(d, x);
+      }
+    }
+  }
+
+  // First-layer products P1[i] = value_i * vec[col_i] (Algorithm 5's H for depth-1 nodes).
+  // kCG: vec lives in global memory written by other CTAs of the same launch (read via L2).
+  template <bool kCG>
+  TOC_D void compute_p1(const double* vec) {
+    if (p0 >= p1) return;
+    with_width(m.w_refs, [&]<int W>() {
+      SeqReader<W> rd;
+      rd.init(blk + m.off_refs, p0);
+      for (uint32_t i = p0; i < p1; ++i) tabw[2 * (i + 1)] = rd.next();
+    });
+    with_width(m.w_cols, [&]<int W>() {
+      SeqReader<W> rd;
+      rd.init(blk + m.off_cols, p0);
+      for (uint32_t i = p0; i < p1; ++i) {
+        const uint32_t c = rd.next();
+        const double x = kCG ? __ldcg(vec + c) : vec[c];
+        tab[i + 1] = uniq[tabw[2 * (i + 1)]] * x;
+      }
+    });
+  }
+
+  TOC_D void zero_tab() {
+    for (uint32_t i = threadIdx.x; i <= nI; i += blockDim.x) tab[i] = 0.0;
+  }
+
+  // Walk the codes of [j0, j1) of row r; visit(i) once per pair (i = first-layer id).
+  template <typename V>
+  TOC_D void walk(uint32_t r, uint32_t lo, uint32_t hi, uint32_t db, uint32_t j0, uint32_t j1, V&& visit) const {
+    for (uint32_t j = j0; j < j1; ++j) {
+      uint32_t x = (j + 1 < hi) ? pk.par(db + (j - lo)) : last[r];
+      while (x > nI) {
+        uint32_t p, key;
+        pk.get(x - 1 - nI, p, key);
+        visit(key);
+        x = p;
+      }
+      visit(x);
+    }
+  }
+
+  // A.v with P1 in tab: emit(r, (A.v)[r]) once per row (by the row's first segment lane).
+  template <typename E>
+  TOC_D void matvec_rows(E&& emit) const {
+    for (uint32_t k = 0; k < passes; ++k) {
+      uint32_t r, lo, hi, db, j0, j1;
+      double part = 0.0;
+      const bool ok = segment(k, r, lo, hi, db, j0, j1);
+      if (ok) walk(r, lo, hi, db, j0, j1, [&](uint32_t i) { part += tab[i]; });
+      __syncwarp();
+      for (uint32_t o = S >> 1; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if (ok && sub == 0) emit(r, part);
+    }
+  }
+
+  // G[i] += sum over the pair occurrences of weight(r) (fixed point, scale g_scale); tab must be
+  // zeroed.  weight(r) returns u[r].
+  template <typename Wt>
+  TOC_D void vecmat_rows(Wt&& weight, double g_scale) {
+    for (uint32_t k = 0; k < passes; ++k) {
+      uint32_t r, lo, hi, db, j0, j1;
+      if (!segment(k, r, lo, hi, db, j0, j1)) break;
+      const long long w = __double2ll_rn(weight(r) * g_scale);
+      if (w == 0) continue;
+      walk(r, lo, hi, db, j0, j1, [&](uint32_t i) { fix_add(tabw + 2 * i, w); });
+    }
+  }
+
+  // out[col_i] += value_i * G[i] for this thread's pairs (fixed point at o_scale).
+  TOC_D void scatter_columns(uint32_t* out, double g_inv, double o_scale) {
+    if (p0 >= p1) return;
+    with_width(m.w_refs, [&]<int W>() {
+      SeqReader<W> rd;
+      rd.init(blk + m.off_refs, p0);
+      for (uint32_t i = p0; i < p1; ++i)
+        tab[i + 1] = uniq[rd.next()] * fix_value(tabw[2 * (i + 1)], tabw[2 * (i + 1) + 1], g_inv);
+    });
+    with_width(m.w_cols, [&]<int W>() {
+      SeqReader<W> rd;
+      rd.init(blk + m.off_cols, p0);
+      for (uint32_t i = p0; i < p1; ++i) {
+        const uint32_t c = rd.next();
+        const long long g = __double2ll_rn(tab[i + 1] * o_scale);
+        if (g) fix_add(out + 2 * c, g);
+      }
+    });
+  }
+
+  // Column c of this batch's first layer, for the thread's pairs (used to visit touched columns).
+  template <typename F>
+  TOC_D void for_each_pair_column(F&& f) const {
+    if (p0 >= p1) return;
+    with_width(m.w_cols, [&]<int W>() {
+      SeqReader<W> rd;
+      rd.init(blk + m.off_cols, p0);
+      for (uint32_t i = p0; i < p1; ++i) f(i, rd.next());
+    });
+  }
+};
+
+}  // namespace toc

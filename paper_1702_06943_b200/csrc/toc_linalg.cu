@@ -18,7 +18,7 @@
 //   vecmat: G in tab[1..|I|]: each code adds u[row] to every pair key on its chain (the
 //           transpose of the matvec walk, an fp64 shared-memory atomic per pair), then
 //           out[col_i] += value_i * G[i].
-#include "toc_common.cuh"
+#include "toc_batch.cuh"
 
 namespace toc {
 
@@ -39,319 +39,54 @@ struct LinalgArgs {
   uint8_t* scratch;
 };
 
-// Byte layout of one batch's tables (all regions 16-B aligned).
-struct BatchLayout {
-  uint32_t off_rowoff, off_dbase, off_last, off_uniq, off_tab, off_pk, total;
-};
-
-template <bool kWide>
-TOC_HD BatchLayout batch_layout(const TocBlockMeta& m) {
-  BatchLayout L;
-  uint32_t o = 0;
-  L.off_rowoff = o;
-  o += align16(4u * (m.n_rows + 1));
-  L.off_dbase = o;
-  o += align16(4u * (m.n_rows + 1));
-  L.off_last = o;
-  o += align16(4u * (m.n_rows + 1));
-  L.off_uniq = o;
-  o += align16(8u * m.n_uniques);
-  L.off_tab = o;
-  o += align16(8u * (m.n_pairs + 1));
-  L.off_pk = o;
-  o += align16((kWide ? 8u : 4u) * m.n_derived);
-  L.total = o;
-  return L;
-}
-
-// Fixed shared-memory prefix of every CTA: block-scan scratch.
-constexpr uint32_t kFixedBytes = 512;  // s_warp (33 words) at 0, s_red (33 doubles) at 160
-
-// Node-table accessors.  Derived node d (id 1 + |I| + d) stores par = the D-code at the
-// position that created it (its parent, codec.py:247) and, in the second field, first the
-// following D-code and then -- after the key pass -- the first-layer pair node d appends, the
-// first pair of that following code (codec.py:248-249).  Narrow trees pack the two fields as u16
-// halves of one u32; wide ones use uint2.
-template <bool kWide>
-struct PK;
-
-template <>
-struct PK<false> {
-  uint32_t* p;
-  TOC_D void set_par(uint32_t d, uint32_t x) { reinterpret_cast<uint16_t*>(p)[2 * d] = (uint16_t)x; }
-  TOC_D void set_nxt(uint32_t d, uint32_t x) { reinterpret_cast<uint16_t*>(p)[2 * d + 1] = (uint16_t)x; }
-  TOC_D void set(uint32_t d, uint32_t par, uint32_t nxt) { p[d] = (par & 0xffffu) | (nxt << 16); }
-  TOC_D uint32_t par(uint32_t d) const { return reinterpret_cast<const uint16_t*>(p)[2 * d]; }
-  TOC_D uint32_t nxt(uint32_t d) const { return reinterpret_cast<const uint16_t*>(p)[2 * d + 1]; }
-  TOC_D void get(uint32_t d, uint32_t& par, uint32_t& nxt) const {
-    uint32_t w = p[d];
-    par = w & 0xffffu;
-    nxt = w >> 16;
-  }
-};
-
-template <>
-struct PK<true> {
-  uint2* p;
-  TOC_D void set_par(uint32_t d, uint32_t x) { p[d].x = x; }
-  TOC_D void set_nxt(uint32_t d, uint32_t x) { p[d].y = x; }
-  TOC_D void set(uint32_t d, uint32_t par, uint32_t nxt) { p[d] = make_uint2(par, nxt); }
-  TOC_D uint32_t par(uint32_t d) const { return p[d].x; }
-  TOC_D uint32_t nxt(uint32_t d) const { return p[d].y; }
-  TOC_D void get(uint32_t d, uint32_t& par, uint32_t& nxt) const {
-    uint2 w = p[d];
-    par = w.x;
-    nxt = w.y;
-  }
-};
-
-// Exclusive scan over rows of max(len-1, 0): the id base of the nodes each row derives.
-TOC_D void scan_derived_base(const uint32_t* rowoff, uint32_t* dbase, uint32_t n, uint32_t* s_warp) {
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  uint32_t carry = 0;
-  for (uint32_t base = 0; base < n; base += blockDim.x) {
-    uint32_t r = base + tid;
-    uint32_t len = (r < n) ? rowoff[r + 1] - rowoff[r] : 0u;
-    uint32_t v = len ? len - 1 : 0u;
-    uint32_t x = warp_excl_scan(v, lane);
-    if (lane == 31) s_warp[warp] = x + v;
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t t = lane < nwarps ? s_warp[lane] : 0u;
-      uint32_t e = warp_excl_scan(t, lane);
-      if (lane < nwarps) s_warp[lane] = e;
-      if (lane == 31) s_warp[32] = e + t;
-    }
-    __syncthreads();
-    if (r < n) dbase[r] = carry + s_warp[warp] + x;
-    carry += s_warp[32];
-    __syncthreads();
-  }
-}
-
-// Lanes per row: the largest power of two <= min(32, threads / rows).  Each thread then owns
-// one contiguous segment of one row, so the code stream is walked sequentially per thread.
-TOC_D uint32_t seg_lanes(uint32_t n, uint32_t nthreads) {
-  uint32_t s = 1;
-  while (s < 32 && 2 * s * (n ? n : 1) <= nthreads) s <<= 1;
-  return s;
-}
-
-// ---- exact fixed-point accumulation with native 32-bit shared/global atomics ---------------
-// fp64 atomics are CAS loops on sm_100a (shared) and the reduction order would make v^T.A
-// non-deterministic.  Instead each accumulator is a 64-bit two's-complement integer (lo, hi
-// words) holding value * 2^F; an add is atomicAdd on lo plus, when needed, atomicAdd of
-// (x_hi + carry) on hi, the carry taken from lo's returned old value.  Modular 64-bit addition
-// commutes, so concurrent adds are exact.  F is chosen per batch from an a-priori bound of the
-// largest partial sum (below), so nothing overflows; the conversion error per term is 2^-(F+1).
-TOC_D void fix_add(uint32_t* acc, long long x) {
-  const uint32_t xl = (uint32_t)x, xh = (uint32_t)((unsigned long long)x >> 32);
-  const uint32_t old = atomicAdd(acc, xl);
-  const uint32_t hi = xh + (old + xl < old ? 1u : 0u);
-  if (hi) atomicAdd(acc + 1, hi);
-}
-
-TOC_D double fix_value(const uint32_t* acc, double inv_scale) {
-  const long long v = (long long)(((unsigned long long)acc[1] << 32) | acc[0]);
-  return (double)v * inv_scale;
-}
-
-// 2^F such that |sum| <= bound stays below 2^62.
-TOC_D double fix_scale(double bound) {
-  if (!(bound > 0.0)) return 1.0;
-  int e;
-  frexp(bound, &e);  // bound < 2^e
-  return ldexp(1.0, 61 - e);
-}
-
-// One batch.  `tables` points either into shared memory or into this CTA's global slab.
+// One batch of the sweep.  `tables` points either into shared memory or into this CTA's slab.
 template <bool kWide, bool kVecSmem>
 __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, const TocBlockMeta& m,
                                               uint8_t* tables, const double* vec_s, uint32_t* acc_s,
                                               uint32_t* s_warp, double* s_red) {
   const uint32_t tid = threadIdx.x, nth = blockDim.x;
-  const uint8_t* blk = a.arena + a.block_off[b];
-  const BatchLayout L = batch_layout<kWide>(m);
-  uint32_t* rowoff = reinterpret_cast<uint32_t*>(tables + L.off_rowoff);
-  uint32_t* dbase = reinterpret_cast<uint32_t*>(tables + L.off_dbase);
-  uint32_t* last = reinterpret_cast<uint32_t*>(tables + L.off_last);
-  double* uniq = reinterpret_cast<double*>(tables + L.off_uniq);
-  double* tab = reinterpret_cast<double*>(tables + L.off_tab);
-  uint32_t* tabw = reinterpret_cast<uint32_t*>(tab);  // tab as words: ref staging / fixed point
-  PK<kWide> pk;
-  pk.p = reinterpret_cast<decltype(pk.p)>(tables + L.off_pk);
-
-  const uint32_t n = m.n_rows, nI = m.n_pairs, nU = m.n_uniques;
-  const uint8_t* cols = blk + m.off_cols;
-  const uint8_t* refs = blk + m.off_refs;
-  const uint8_t* codes = blk + m.off_codes;
+  const bool do_mv = a.kind & TOC_MATVEC, do_vm = a.kind & TOC_VECMAT;
   const int64_t row_base = a.row_base[b];
   const int32_t ncol = a.n_cols;
-  const double* vec = kVecSmem ? vec_s : a.v;
-  const bool do_mv = a.kind & TOC_MATVEC, do_vm = a.kind & TOC_VECMAT;
-
-  // ---- phase 0: row offsets, value index, bounds for the fixed-point scales -----------------
-  const uint32_t wo = m.w_offsets;
-  for (uint32_t r = tid; r <= n; r += nth) rowoff[r] = ld_packed(blk + m.off_offsets, r, wo);
-  double umax = 0.0, vmax = 0.0;
-  for (uint32_t i = tid; i < nU; i += nth) {
-    const double x = ld_f64_unaligned(blk + m.off_uniques + 8u * i);
-    uniq[i] = x;
-    vmax = fmax(vmax, fabs(x));
-  }
-  if (do_vm) {
-    for (uint32_t r = tid; r < n; r += nth) umax += fabs(a.u[row_base + r]);
-    if (kVecSmem)
-      for (int32_t c = tid; c < 2 * ncol; c += nth) acc_s[c] = 0u;
-  }
-  __syncthreads();
-  scan_derived_base(rowoff, dbase, n, s_warp);
+  Batch<kWide> B;
+  B.init(a.arena + a.block_off[b], m, tables);
+  if (do_vm && kVecSmem)
+    for (int32_t c = tid; c < 2 * ncol; c += nth) acc_s[c] = 0u;
+  B.load_index(s_warp);
   double g_scale = 1.0, o_scale = 1.0;
-  if (do_vm) {  // sum |u| over the batch and max |value|: the a-priori bounds (see fix_add)
-    const double su = block_sum(umax, s_red), mv = block_max_d(vmax, s_red);
+  if (do_vm) {  // a-priori bounds of every partial sum (see fix_add): sum |u| and max |value|
+    double su = 0.0;
+    for (uint32_t r = tid; r < B.n; r += nth) su += fabs(a.u[row_base + r]);
+    su = block_sum(su, s_red);
+    const double mv = block_max_d(B.vmax, s_red);
     g_scale = fix_scale(su);
     o_scale = fix_scale(su * mv);
   }
-
-  const uint32_t S = seg_lanes(n, nth), RP = nth / S, passes = (n + RP - 1) / RP, sub = tid % S;
-  const uint32_t per_pair = (nI + nth - 1) / nth, p0 = min(nI, tid * per_pair), p1 = min(nI, p0 + per_pair);
-
-  // ---- phase 1: one sequential pass over each thread's code segment -------------------------
-  with_width(m.w_codes, [&]<int W>() {
-    for (uint32_t k = 0; k < passes; ++k) {
-      const uint32_t r = tid / S + k * RP;
-      if (r >= n) break;
-      const uint32_t lo = rowoff[r], hi = rowoff[r + 1], db = dbase[r], len = hi - lo;
-      const uint32_t j0 = lo + (len * sub) / S, j1 = lo + (len * (sub + 1)) / S;
-      if (j0 >= j1) continue;
-      SeqReader<W> rd;
-      rd.init(codes, j0);
-      uint32_t c = rd.next();
-      for (uint32_t j = j0; j < j1; ++j) {
-        if (j + 1 < hi) {  // non-final: node (par = this code, nxt = next code), one store
-          const uint32_t cn = rd.next();
-          pk.set(db + (j - lo), c, cn);
-          c = cn;
-        } else {
-          last[r] = c;
-        }
-      }
-    }
-  });
-  // first-layer products P1[i] = value_i * v[col_i] (matvec), or G = 0 (vecmat only)
-  if (do_mv) {
-    if (p0 < p1) {
-      with_width(m.w_refs, [&]<int W>() {
-        SeqReader<W> rd;
-        rd.init(refs, p0);
-        for (uint32_t i = p0; i < p1; ++i) tabw[2 * (i + 1)] = rd.next();
-      });
-      with_width(m.w_cols, [&]<int W>() {
-        SeqReader<W> rd;
-        rd.init(cols, p0);
-        for (uint32_t i = p0; i < p1; ++i) tab[i + 1] = uniq[tabw[2 * (i + 1)]] * vec[rd.next()];
-      });
-    }
-  } else {
-    for (uint32_t i = tid; i <= nI; i += nth) tab[i] = 0.0;
-  }
+  B.build_nodes();
+  if (do_mv) B.template compute_p1<false>(kVecSmem ? vec_s : a.v);
+  else B.zero_tab();
   __syncthreads();
-
-  // ---- key pass: the pair each derived node appends is the first pair of its next code:
-  //      follow par[] from that code down to the first layer (codec.py:248-251) ---------------
-  for (uint32_t k = 0; k < passes; ++k) {
-    const uint32_t r = tid / S + k * RP;
-    if (r >= n) break;
-    const uint32_t lo = rowoff[r], hi = rowoff[r + 1], db = dbase[r], len = hi - lo;
-    const uint32_t j0 = lo + (len * sub) / S, j1 = min(lo + (len * (sub + 1)) / S, hi - 1);
-    for (uint32_t j = j0; j < j1; ++j) {
-      const uint32_t d = db + (j - lo);
-      uint32_t x = pk.nxt(d);
-      while (x > nI) x = pk.par(x - 1 - nI);
-      pk.set_nxt(d, x);
-    }
-  }
+  B.resolve_keys();
   __syncthreads();
-
-  // The walk of one code x: each derived node on the chain contributes its key, the first-layer
-  // node at the end contributes itself.  visit(i) is called once per pair, i = first-layer id.
-  auto walk_segment = [&](uint32_t r, uint32_t j0, uint32_t j1, uint32_t lo, uint32_t hi, uint32_t db,
-                          auto&& visit) {
-    for (uint32_t j = j0; j < j1; ++j) {
-      uint32_t x = (j + 1 < hi) ? pk.par(db + (j - lo)) : last[r];
-      while (x > nI) {
-        uint32_t p, key;
-        pk.get(x - 1 - nI, p, key);
-        visit(key);
-        x = p;
-      }
-      visit(x);
-    }
-  };
-
-  // ---- phase 2: A.v -------------------------------------------------------------------------
-  if (do_mv) {
-    for (uint32_t k = 0; k < passes; ++k) {
-      const uint32_t r = tid / S + k * RP;
-      double part = 0.0;
-      if (r < n) {
-        const uint32_t lo = rowoff[r], hi = rowoff[r + 1], db = dbase[r], len = hi - lo;
-        const uint32_t j0 = lo + (len * sub) / S, j1 = lo + (len * (sub + 1)) / S;
-        walk_segment(r, j0, j1, lo, hi, db, [&](uint32_t i) { part += tab[i]; });
-      }
-      __syncwarp();
-      for (uint32_t o = S >> 1; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      if (r < n && sub == 0) a.R[row_base + r] = part;
-    }
-  }
-
-  // ---- phase 3: u^T.A -----------------------------------------------------------------------
+  if (do_mv) B.matvec_rows([&](uint32_t r, double s) { a.R[row_base + r] = s; });
   if (do_vm) {
     if (do_mv) {
       __syncthreads();
-      for (uint32_t i = tid; i <= nI; i += nth) tab[i] = 0.0;
+      B.zero_tab();
       __syncthreads();
     }
-    for (uint32_t k = 0; k < passes; ++k) {
-      const uint32_t r = tid / S + k * RP;
-      if (r >= n) break;
-      const uint32_t lo = rowoff[r], hi = rowoff[r + 1], db = dbase[r], len = hi - lo;
-      const uint32_t j0 = lo + (len * sub) / S, j1 = lo + (len * (sub + 1)) / S;
-      const long long w = __double2ll_rn(a.u[row_base + r] * g_scale);
-      if (w == 0) continue;
-      walk_segment(r, j0, j1, lo, hi, db, [&](uint32_t i) { fix_add(tabw + 2 * i, w); });
-    }
+    B.vecmat_rows([&](uint32_t r) { return a.u[row_base + r]; }, g_scale);
     __syncthreads();
     uint32_t* out = kVecSmem ? acc_s : reinterpret_cast<uint32_t*>(a.O + b * (int64_t)ncol);
-    const double g_inv = 1.0 / g_scale;
-    if (p0 < p1) {
-      // contribution value_i * G[i] replaces G[i] in place, then scatter by column
-      with_width(m.w_refs, [&]<int W>() {
-        SeqReader<W> rd;
-        rd.init(refs, p0);
-        for (uint32_t i = p0; i < p1; ++i) tab[i + 1] = uniq[rd.next()] * fix_value(tabw + 2 * (i + 1), g_inv);
-      });
-      with_width(m.w_cols, [&]<int W>() {
-        SeqReader<W> rd;
-        rd.init(cols, p0);
-        for (uint32_t i = p0; i < p1; ++i) {
-          const uint32_t c = rd.next();
-          const long long g = __double2ll_rn(tab[i + 1] * o_scale);
-          if (g) fix_add(out + 2 * c, g);
-        }
-      });
-    }
+    B.scatter_columns(out, 1.0 / g_scale, o_scale);
     __syncthreads();
     const double o_inv = 1.0 / o_scale;
     double* o = a.O + b * (int64_t)ncol;
     if (kVecSmem) {
-      for (int32_t c = tid; c < ncol; c += nth) o[c] = fix_value(acc_s + 2 * c, o_inv);
+      for (int32_t c = tid; c < ncol; c += nth) o[c] = fix_value(acc_s[2 * c], acc_s[2 * c + 1], o_inv);
     } else {
       uint32_t* ow = reinterpret_cast<uint32_t*>(o);
-      for (int32_t c = tid; c < ncol; c += nth) {
-        const uint32_t w2[2] = {__ldcg(ow + 2 * c), __ldcg(ow + 2 * c + 1)};
-        o[c] = fix_value(w2, o_inv);
-      }
+      for (int32_t c = tid; c < ncol; c += nth) o[c] = fix_value(__ldcg(ow + 2 * c), __ldcg(ow + 2 * c + 1), o_inv);
     }
   }
 }

@@ -1,0 +1,356 @@
+// toc_mgd.cu -- mini-batch gradient descent for GLMs directly on TOC-compressed batches.
+//
+// Reference: training.py:261-281 (glm_gradient: z = A.w, per-example scalar s, g = s^T.A, summed),
+// :296-316 (apply_update / mgd_step: w - (lr / |B|) * g), :336-361 (train), :231-258
+// (empirical_risk).
+//
+// Epoch kernel ("relay"): one cooperative launch runs a whole epoch.  CTA c owns steps
+// t = c, c + G, c + 2G, ...  For step t it first rebuilds batch t's node tables (independent of
+// w, so this overlaps the G-1 steps in flight on other SMs), then waits until the global step
+// counter reaches t, reads the current weights through L2, runs A.w -> s -> s^T.A -> update,
+// and publishes the new weights with a release store of t + 1.  The dependency chain therefore
+// costs only the weight-dependent part of each step plus one L2 handoff.
+#include "toc_batch.cuh"
+
+namespace toc {
+
+struct MgdArgs {
+  const uint8_t* arena;
+  const int64_t* block_off;
+  const TocBlockMeta* meta;
+  const int64_t* row_base;
+  int64_t n_blocks;       // steps of the epoch, in batch order
+  int32_t n_cols;
+  int32_t loss;           // TOC_LOSS_*
+  double lr;
+  const double* labels;   // per row, batch order
+  double* w;              // weights (n_cols), updated in place
+  uint32_t* counter;      // completed steps (0 at launch)
+  uint32_t* abort_flag;   // set on a spin timeout; every CTA then exits
+  int32_t batch_smem_budget;
+  int32_t small_m;        // 1: gradient accumulators + touched bitmap in shared memory
+  int64_t slab_bytes;     // global slab per CTA (tables of oversized batches)
+  uint8_t* scratch;       // [ctas * slab_bytes] tables, then [ctas * 8 * n_cols] accumulators
+  double* grad_out;       // gradient kernel only: [n_blocks x n_cols] summed gradients
+};
+
+// Per-example scalar of glm_gradient (training.py:272-280).
+TOC_D double loss_scalar(int loss, double y, double z) {
+  if (loss == TOC_LOSS_SQUARED) return z - y;
+  if (loss == TOC_LOSS_LOGISTIC) return -y / (1.0 + exp(y * z));
+  return (y * z < 1.0) ? -y : 0.0;  // hinge subgradient: flat side contributes zero
+}
+
+TOC_D uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+TOC_D void st_release(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Gradient of one batch into fixed-point column accumulators `acc` (2 words per column).
+// Returns the inverse output scale.  srow: n doubles of shared memory.  Entered after the node
+// tables are complete (keys resolved) and `w` is current.
+template <bool kWide, bool kCG>
+TOC_D double batch_gradient(Batch<kWide>& B, const MgdArgs& a, int64_t b, double* srow, uint32_t* acc,
+                            double* s_red) {
+  const uint32_t tid = threadIdx.x, nth = blockDim.x;
+  const int64_t rb = a.row_base[b];
+  B.template compute_p1<kCG>(a.w);
+  __syncthreads();
+  B.matvec_rows([&](uint32_t r, double z) { srow[r] = z; });
+  __syncthreads();
+  double su = 0.0;
+  for (uint32_t r = tid; r < B.n; r += nth) {
+    const double s = loss_scalar(a.loss, a.labels[rb + r], srow[r]);
+    srow[r] = s;
+    su += fabs(s);
+  }
+  B.zero_tab();
+  su = block_sum(su, s_red);  // contains barriers
+  const double mv = block_max_d(B.vmax, s_red);
+  const double g_scale = fix_scale(su), o_scale = fix_scale(su * mv);
+  B.vecmat_rows([&](uint32_t r) { return srow[r]; }, g_scale);
+  __syncthreads();
+  B.scatter_columns(acc, 1.0 / g_scale, o_scale);
+  __syncthreads();
+  return 1.0 / o_scale;
+}
+
+// w[c] -= (lr / |B|) * g[c] for every column of the batch's first layer, once per column
+// (apply_update, training.py:296-300; untouched columns have g = 0 and stay bit-identical).
+// The accumulators of updated columns are cleared for the CTA's next step.
+template <bool kWide>
+TOC_D void apply_update(Batch<kWide>& B, const MgdArgs& a, uint32_t* acc, uint32_t* touched, double o_inv) {
+  const double step = a.lr / (double)B.n;
+  B.for_each_pair_column([&](uint32_t, uint32_t c) {
+    const uint32_t bit = 1u << (c & 31);
+    if (atomicOr(&touched[c >> 5], bit) & bit) return;  // another pair of this column won
+    const uint32_t* ac = acc + 2 * c;
+    const double g = fix_value(a.small_m ? ac[0] : __ldcg(ac), a.small_m ? ac[1] : __ldcg(ac + 1), o_inv);
+    a.w[c] = __dsub_rn(__ldcg(a.w + c), __dmul_rn(step, g));  // L2: other CTAs wrote w
+    acc[2 * c] = 0u;
+    acc[2 * c + 1] = 0u;
+  });
+}
+
+template <bool kWide>
+__global__ void __launch_bounds__(1024, 1) glm_epoch_kernel(MgdArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint32_t* s_warp = reinterpret_cast<uint32_t*>(smem);
+  double* s_red = reinterpret_cast<double*>(smem + 160);
+  __shared__ uint32_t s_go;
+  uint8_t* p = smem + kFixedBytes;
+  const uint32_t tid = threadIdx.x, nth = blockDim.x, m = (uint32_t)a.n_cols, words = (m + 31) / 32;
+  uint32_t* touched = reinterpret_cast<uint32_t*>(p);
+  p += align16(4u * words);
+  uint32_t* acc = nullptr;
+  if (a.small_m) {
+    acc = reinterpret_cast<uint32_t*>(p);
+    p += align16(8u * m);
+    for (uint32_t c = tid; c < 2 * m; c += nth) acc[c] = 0u;
+  } else {
+    acc = reinterpret_cast<uint32_t*>(a.scratch + (int64_t)gridDim.x * a.slab_bytes) + (int64_t)blockIdx.x * 2 * m;
+  }
+  for (int64_t t = blockIdx.x; t < a.n_blocks; t += gridDim.x) {
+    const TocBlockMeta mt = a.meta[t];
+    Batch<kWide> B;
+    double* srow = reinterpret_cast<double*>(p);
+    uint8_t* tables = p + align16(8u * mt.n_rows);
+    const uint32_t need = batch_layout<kWide>(mt).total + align16(8u * mt.n_rows);
+    if (need > (uint32_t)a.batch_smem_budget) tables = a.scratch + (int64_t)blockIdx.x * a.slab_bytes;
+    B.init(a.arena + a.block_off[t], mt, tables);
+    for (uint32_t w = tid; w < words; w += nth) touched[w] = 0u;
+    B.load_index(s_warp);
+    B.build_nodes();
+    __syncthreads();
+    B.resolve_keys();
+    // wait for the weights of step t (bounded: a hang would take the GPU down with it)
+    if (tid == 0) {
+      uint32_t go = 1;
+      long long spins = 0;
+      while (ld_acquire(a.counter) != (uint32_t)t) {
+        if (ld_acquire(a.abort_flag)) { go = 0; break; }
+        if (++spins > (1ll << 26)) { atomicExch(a.abort_flag, 1u); go = 0; break; }
+        __nanosleep(64);
+      }
+      s_go = go;
+    }
+    __syncthreads();
+    if (!s_go) return;
+    const double o_inv = batch_gradient<kWide, true>(B, a, t, srow, acc, s_red);
+    apply_update(B, a, acc, touched, o_inv);
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release(a.counter, (uint32_t)t + 1);
+  }
+}
+
+// Summed gradient of each batch (no update): grad_out[b, :] = s_b^T A_b.  Data-parallel MGD
+// all-reduces these across ranks before the update.
+template <bool kWide>
+__global__ void __launch_bounds__(1024, 1) glm_grad_kernel(MgdArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint32_t* s_warp = reinterpret_cast<uint32_t*>(smem);
+  double* s_red = reinterpret_cast<double*>(smem + 160);
+  uint8_t* p = smem + kFixedBytes;
+  const uint32_t tid = threadIdx.x, nth = blockDim.x, m = (uint32_t)a.n_cols;
+  uint32_t* acc;
+  if (a.small_m) {
+    acc = reinterpret_cast<uint32_t*>(p);
+    p += align16(8u * m);
+  }
+  for (int64_t b = blockIdx.x; b < a.n_blocks; b += gridDim.x) {
+    const TocBlockMeta mb = a.meta[b];
+    double* srow = reinterpret_cast<double*>(p);
+    uint8_t* tables = p + align16(8u * mb.n_rows);
+    const uint32_t need = batch_layout<kWide>(mb).total + align16(8u * mb.n_rows);
+    if (need > (uint32_t)a.batch_smem_budget) tables = a.scratch + (int64_t)blockIdx.x * a.slab_bytes;
+    double* g = a.grad_out + b * (int64_t)m;
+    if (!a.small_m) acc = reinterpret_cast<uint32_t*>(g);  // accumulate in place (zeroed by the host)
+    __syncthreads();
+    if (a.small_m)
+      for (uint32_t c = tid; c < 2 * m; c += nth) acc[c] = 0u;
+    Batch<kWide> B;
+    B.init(a.arena + a.block_off[b], mb, tables);
+    B.load_index(s_warp);
+    B.build_nodes();
+    __syncthreads();
+    B.resolve_keys();
+    __syncthreads();
+    const double o_inv = batch_gradient<kWide, false>(B, a, b, srow, acc, s_red);
+    if (a.small_m) {
+      for (uint32_t c = tid; c < m; c += nth) g[c] = fix_value(acc[2 * c], acc[2 * c + 1], o_inv);
+    } else {
+      uint32_t* gw = reinterpret_cast<uint32_t*>(g);
+      for (uint32_t c = tid; c < m; c += nth) g[c] = fix_value(__ldcg(gw + 2 * c), __ldcg(gw + 2 * c + 1), o_inv);
+    }
+  }
+}
+
+// Per-row loss of empirical_risk (training.py:231-258) and its sum (one double per CTA).
+__global__ void risk_kernel(const double* z, const double* y, int64_t n, int32_t loss, double* part) {
+  __shared__ double s_red[33];
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double yz = y[i] * z[i];
+    double l;
+    if (loss == TOC_LOSS_SQUARED) {
+      const double d = y[i] - z[i];
+      l = 0.5 * d * d;
+    } else if (loss == TOC_LOSS_LOGISTIC) {  // softplus(-y z), overflow-free (training.py:206-212)
+      const double t = -yz;
+      l = t > 0.0 ? t + log1p(exp(-t)) : log1p(exp(t));
+    } else {
+      l = fmax(0.0, 1.0 - yz);
+    }
+    acc += l;
+  }
+  acc = block_sum(acc, s_red);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+
+}  // namespace toc
+
+// ------------------------------------------------------------------------------------------
+namespace {
+
+struct MgdLaunch {
+  int threads, ctas, smem;
+  int32_t budget, small_m;
+  int64_t slab, scratch;
+};
+
+int dev_count(int attr) {
+  int dev = 0, v = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&v, (cudaDeviceAttr)attr, dev);
+  return v;
+}
+
+MgdLaunch mgd_plan(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t n_cols, bool wide, bool epoch) {
+  MgdLaunch L{};
+  int sm = dev_count(cudaDevAttrMultiProcessorCount), optin = dev_count(cudaDevAttrMaxSharedMemoryPerBlockOptin);
+  if (sm <= 0) {
+    sm = 148;
+    optin = 232448;
+  }
+  uint32_t max_need = 0;
+  for (int64_t b = 0; b < n_blocks; ++b) {
+    const uint32_t need = (wide ? toc::batch_layout<true>(h_meta[b]).total : toc::batch_layout<false>(h_meta[b]).total) +
+                          toc::align16(8u * h_meta[b].n_rows);
+    if (need > max_need) max_need = need;
+  }
+  const uint32_t m = (uint32_t)n_cols;
+  const uint32_t small_bytes = toc::align16(8u * m);
+  L.small_m = small_bytes <= 32u * 1024u;
+  uint32_t fixed = toc::kFixedBytes + (epoch ? toc::align16(4u * ((m + 31) / 32)) : 0u) + (L.small_m ? small_bytes : 0u);
+  uint32_t avail = (uint32_t)optin > fixed ? (uint32_t)optin - fixed : 0u;
+  L.budget = (int32_t)(max_need <= avail ? max_need : avail);
+  L.smem = (int)(fixed + (uint32_t)L.budget);
+  L.threads = 1024;
+  L.ctas = (int)(n_blocks < sm ? (n_blocks > 0 ? n_blocks : 1) : sm);
+  L.slab = max_need > (uint32_t)L.budget ? (int64_t)toc::align16(max_need) : 0;
+  L.scratch = (int64_t)L.ctas * L.slab + (L.small_m ? 0 : (int64_t)L.ctas * 8 * m);
+  return L;
+}
+
+}  // namespace
+
+extern "C" int toc_mgd_workspace(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t n_cols, int32_t kind,
+                                 int64_t* scratch_bytes) {
+  if (!h_meta || n_blocks < 0 || !scratch_bytes) return TOC_E_ARG;
+  bool wide = false;
+  for (int64_t b = 0; b < n_blocks; ++b)
+    if (1ull + h_meta[b].n_pairs + h_meta[b].n_derived > 65536ull) wide = true;
+  *scratch_bytes = mgd_plan(h_meta, n_blocks, n_cols, wide, kind == 0).scratch;
+  return TOC_OK;
+}
+
+static int mgd_launch(const TocBlockMeta* h_meta, const toc::MgdArgs& a0, bool epoch, cudaStream_t s) {
+  bool wide = false;
+  for (int64_t b = 0; b < a0.n_blocks; ++b)
+    if (1ull + h_meta[b].n_pairs + h_meta[b].n_derived > 65536ull) wide = true;
+  MgdLaunch L = mgd_plan(h_meta, a0.n_blocks, a0.n_cols, wide, epoch);
+  toc::MgdArgs a = a0;
+  a.batch_smem_budget = L.budget;
+  a.small_m = L.small_m;
+  a.slab_bytes = L.slab;
+  if (L.scratch > 0 && !a.scratch) return TOC_E_ARG;
+  if (epoch && !L.small_m)  // per-CTA global gradient accumulators start at zero
+    if (cudaMemsetAsync(a.scratch + (int64_t)L.ctas * L.slab, 0, (size_t)L.ctas * 8 * a.n_cols, s) != cudaSuccess)
+      return TOC_E_CUDA;
+  void* fn;
+  if (epoch) fn = wide ? (void*)toc::glm_epoch_kernel<true> : (void*)toc::glm_epoch_kernel<false>;
+  else fn = wide ? (void*)toc::glm_grad_kernel<true> : (void*)toc::glm_grad_kernel<false>;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem) != cudaSuccess) return TOC_E_CUDA;
+  void* args[] = {&a};
+  cudaError_t e;
+  if (epoch) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, L.threads, L.smem);
+    if (per_sm < 1) return TOC_E_CUDA;
+    e = cudaLaunchCooperativeKernel(fn, dim3(L.ctas), dim3(L.threads), args, L.smem, s);
+  } else {
+    e = cudaLaunchKernel(fn, dim3(L.ctas), dim3(L.threads), args, L.smem, s);
+  }
+  return e == cudaSuccess ? TOC_OK : TOC_E_CUDA;
+}
+
+extern "C" int toc_glm_epoch(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+                             const TocBlockMeta* h_meta, const int64_t* d_row_base, int64_t n_blocks, int32_t n_cols,
+                             int32_t loss, double lr, const double* d_labels, double* d_w, uint32_t* d_sync,
+                             void* d_scratch, void* stream) {
+  if (n_blocks <= 0) return n_blocks == 0 ? TOC_OK : TOC_E_ARG;
+  if (!h_meta || !d_w || !d_labels || !d_sync || loss < 0 || loss > 2) return TOC_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemsetAsync(d_sync, 0, 8, s) != cudaSuccess) return TOC_E_CUDA;
+  toc::MgdArgs a{};
+  a.arena = d_arena;
+  a.block_off = d_block_off;
+  a.meta = d_meta;
+  a.row_base = d_row_base;
+  a.n_blocks = n_blocks;
+  a.n_cols = n_cols;
+  a.loss = loss;
+  a.lr = lr;
+  a.labels = d_labels;
+  a.w = d_w;
+  a.counter = d_sync;
+  a.abort_flag = d_sync + 1;
+  a.scratch = (uint8_t*)d_scratch;
+  return mgd_launch(h_meta, a, true, s);
+}
+
+extern "C" int toc_glm_grad(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+                            const TocBlockMeta* h_meta, const int64_t* d_row_base, int64_t n_blocks, int32_t n_cols,
+                            int32_t loss, const double* d_labels, const double* d_w, double* d_grad,
+                            void* d_scratch, void* stream) {
+  if (n_blocks <= 0) return n_blocks == 0 ? TOC_OK : TOC_E_ARG;
+  if (!h_meta || !d_w || !d_labels || !d_grad || loss < 0 || loss > 2) return TOC_E_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemsetAsync(d_grad, 0, sizeof(double) * (size_t)n_blocks * n_cols, s) != cudaSuccess) return TOC_E_CUDA;
+  toc::MgdArgs a{};
+  a.arena = d_arena;
+  a.block_off = d_block_off;
+  a.meta = d_meta;
+  a.row_base = d_row_base;
+  a.n_blocks = n_blocks;
+  a.n_cols = n_cols;
+  a.loss = loss;
+  a.labels = d_labels;
+  a.w = const_cast<double*>(d_w);
+  a.scratch = (uint8_t*)d_scratch;
+  a.grad_out = d_grad;
+  return mgd_launch(h_meta, a, false, s);
+}
+
+extern "C" int toc_glm_risk(const double* d_z, const double* d_y, int64_t n, int32_t loss, double* d_partial,
+                            int32_t n_partial, void* stream) {
+  if (n < 0 || n_partial < 1 || loss < 0 || loss > 2) return TOC_E_ARG;
+  toc::risk_kernel<<<n_partial, 256, 0, (cudaStream_t)stream>>>(d_z, d_y, n, loss, d_partial);
+  return cudaGetLastError() == cudaSuccess ? TOC_OK : TOC_E_CUDA;
+}

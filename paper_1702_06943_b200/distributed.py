@@ -1,0 +1,183 @@
+"""Multi-GPU execution.
+
+* Matrix-op sweep: mini-batches are independent, so rank r of G simply owns a contiguous shard
+  of the batches -- no collective on the data path (weak scaling).
+* Synchronous data-parallel MGD: at step t the global batch is rows [t*B*G, (t+1)*B*G) of the
+  once-shuffled order (training.py:131-167 with batch_size = B*G); rank r compresses and holds the
+  rows [t*B*G + r*B, t*B*G + (r+1)*B) as its local mini-batch.  Each step every rank computes the
+  summed gradient of its local batch on the device (toc_glm_grad), the gradients are all-reduced
+  (sum), and every rank applies w <- w - (lr / |B_t|) * g with |B_t| the global batch size
+  (training.py:296-300).  The union of the local batches is exactly the reference's batch at
+  batch_size = B*G, so the parity oracle is the reference trainer at that batch size.
+
+The per-step gradient function and the all-reduce are injectable so the host logic runs (and is
+tested) on CPU with the gloo backend; on the device path they are toc_glm_grad and NCCL.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Callable
+
+import numpy as np
+
+from . import _native as N
+
+
+def shard_range(n_items: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous near-equal shard [lo, hi) of n_items for rank (sweep: batches per GPU)."""
+    base, extra = divmod(n_items, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+@dataclass
+class StepPlan:
+    """Rows of the shuffled order this rank holds at each step, and the global batch sizes."""
+
+    local_rows: list  # per step: (lo, hi) in shuffled-row space (hi == lo: empty local batch)
+    global_sizes: np.ndarray  # per step: |B_t|
+
+
+def dp_step_plan(n_rows: int, local_batch: int, world: int, rank: int) -> StepPlan:
+    gb = local_batch * world
+    steps = (n_rows + gb - 1) // gb
+    rows, sizes = [], np.zeros(steps, np.int64)
+    for t in range(steps):
+        g0 = t * gb
+        sizes[t] = min(gb, n_rows - g0)
+        lo = min(n_rows, g0 + rank * local_batch)
+        hi = min(n_rows, lo + local_batch, g0 + gb)
+        rows.append((lo, max(lo, hi)))
+    return StepPlan(rows, sizes)
+
+
+def apply_update(w, g, lr: float, batch_size: int):
+    """w - (lr / batch_size) * g (training.py:296-300), in place on a torch tensor."""
+    step = lr / batch_size
+    w.sub_(g * step)
+    return w
+
+
+class DataParallelGLM:
+    """Synchronous DP-MGD over local mini-batches.
+
+    grad_fn(t, w) -> summed gradient of this rank's local batch of step t (zeros if empty);
+    allreduce(g) sums g across ranks in place."""
+
+    def __init__(self, n_cols: int, plan: StepPlan, lr: float, grad_fn: Callable, allreduce: Callable, w0):
+        self.n_cols = n_cols
+        self.plan = plan
+        self.lr = float(lr)
+        self.grad_fn = grad_fn
+        self.allreduce = allreduce
+        self.w = w0
+
+    def epoch(self):
+        for t, gsize in enumerate(self.plan.global_sizes):
+            g = self.grad_fn(t, self.w)
+            self.allreduce(g)
+            apply_update(self.w, g, self.lr, int(gsize))
+        return self.w
+
+
+# ---- device pieces -------------------------------------------------------------------------
+def batch_gradients(batches, loss_kind: str, w, out=None):
+    """Summed gradient of every batch of a DeviceBatches at weights w (device tensor), on the GPU
+    (toc_glm_grad).  Returns a [n_batches, n_cols] float64 device tensor."""
+    from .training import LOSS_CODE, _bind
+
+    torch = N.require_cuda()
+    a = batches.arena
+    L = _bind()
+    m = batches.n_cols
+    if out is None:
+        out = torch.empty((a.n_blocks, m), dtype=torch.float64, device="cuda")
+    nbytes = ctypes.c_int64()
+    N.check(L.toc_mgd_workspace(a.meta.ctypes.data_as(ctypes.c_void_p), a.n_blocks, m, 1, ctypes.byref(nbytes)),
+            "toc_mgd_workspace")
+    scratch = torch.empty(max(nbytes.value, 16), dtype=torch.uint8, device="cuda")
+    N.check(L.toc_glm_grad(a.data.data_ptr(), a.block_off_d.data_ptr(), a.meta_d.data_ptr(),
+                           a.meta.ctypes.data_as(ctypes.c_void_p), a.row_base_d.data_ptr(), a.n_blocks, m,
+                           LOSS_CODE[loss_kind], batches.labels.data_ptr(), w.data_ptr(), out.data_ptr(),
+                           scratch.data_ptr(), N.stream_handle()), "toc_glm_grad")
+    return out
+
+
+class _OneBatch:
+    """View of a single batch of a DeviceBatches (for per-step gradients)."""
+
+    def __init__(self, batches, b: int):
+        from .arena import BlockArena
+
+        a = batches.arena
+        self.arena = BlockArena(a.data, a.block_off[b : b + 1], a.block_len[b : b + 1], a.meta_d[b * 68 : (b + 1) * 68])
+        self.labels = batches.labels[int(a.row_base[b]) : int(a.row_base[b]) + int(a.meta["n_rows"][b])]
+        self.n_cols = batches.n_cols
+
+
+def train_data_parallel(dataset, config, world: int, rank: int, group=None):
+    """DP-MGD on this rank's GPU; every rank returns the same weights and the risk trace (the
+    risk is all-reduced).  Launch one process per GPU (torchrun); NCCL all-reduces the gradient."""
+    import torch
+    import torch.distributed as dist
+
+    from .matrix import LabeledDataset
+    from .training import DeviceBatches, LossTrace, GlmModel, LOSS_CODE, shuffle_order
+
+    order = shuffle_order(dataset.n_rows, config.seed)
+    plan = dp_step_plan(dataset.n_rows, config.batch_size, world, rank)
+    # this rank's local batches, in step order, as one arena (empty local batches are skipped)
+    idx = [order[lo:hi] for lo, hi in plan.local_rows if hi > lo]
+    steps_with_rows = [t for t, (lo, hi) in enumerate(plan.local_rows) if hi > lo]
+    local = np.concatenate(idx) if idx else np.zeros(0, np.int64)
+    sub = LabeledDataset(features=dataset.features.take_rows(local), labels=dataset.labels[local])
+    batches = DeviceBatches(sub, config.batch_size) if len(local) else None
+    m = dataset.n_cols
+    w = torch.zeros(m, dtype=torch.float64, device="cuda")
+    step_to_local = {t: i for i, t in enumerate(steps_with_rows)}
+    views = [_OneBatch(batches, i) for i in range(len(steps_with_rows))] if batches else []
+    g_buf = torch.zeros((1, m), dtype=torch.float64, device="cuda")
+
+    def grad_fn(t, w_):
+        i = step_to_local.get(t)
+        if i is None:
+            g_buf.zero_()
+        else:
+            batch_gradients(views[i], config.loss_kind, w_, out=g_buf)
+        return g_buf[0]
+
+    def allreduce(g):
+        dist.all_reduce(g, op=dist.ReduceOp.SUM, group=group)
+
+    trainer = DataParallelGLM(m, plan, config.learning_rate, grad_fn, allreduce, w)
+    trace = LossTrace()
+    for _ in range(config.epochs):
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record()
+        trainer.epoch()
+        end.record()
+        end.synchronize()
+        t = torch.tensor([start.elapsed_time(end) / 1e3], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        trace.seconds.append(float(t.item()))
+        trace.risks.append(_dp_risk(batches, w, config.loss_kind, dataset.n_rows, group))
+    return GlmModel(weights=w.cpu().numpy()), trace
+
+
+def _dp_risk(batches, w, loss_kind, n_total, group):
+    import torch
+    import torch.distributed as dist
+
+    from .training import LOSS_CODE, _bind
+
+    s = torch.zeros(1, dtype=torch.float64, device="cuda")
+    if batches is not None:
+        z = batches.arena.matvec(w)
+        part = torch.zeros(148, dtype=torch.float64, device="cuda")
+        N.check(_bind().toc_glm_risk(z.data_ptr(), batches.labels.data_ptr(), batches.n_rows, LOSS_CODE[loss_kind],
+                                     part.data_ptr(), 148, N.stream_handle()), "toc_glm_risk")
+        s += part.sum()
+    dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
+    return float(s.item()) / n_total

@@ -93,3 +93,78 @@ def cfg2_operands(seed: int, n_batches: int, n_rows: int = 250, n_cols: int = 78
     """One shared v ~ N(0,1)[n_cols] and a per-batch slice of u ~ N(0,1) (cli.py:321-334)."""
     rng = np.random.default_rng(np.random.SeedSequence([seed, 1 << 30]))
     return rng.standard_normal(n_cols), rng.standard_normal(n_rows * n_batches)
+
+
+# ---- config 3: logistic-regression MGD data -------------------------------------------------
+def cfg3_dataset(n_rows: int = 2_000_000, n_cols: int = 68, seed: int = 3, n_levels: int = 16,
+                 zipf_s: float = 1.5, flip: float = 0.05, chunk: int = 250_000):
+    """BASELINE.json configs[2]: each column a categorical integer 0..15 with Zipf(1.5)
+    frequencies (category k has weight (k+1)^-1.5, so 0 -- dropped by the sparse encoding -- is the
+    most frequent), stored as float64.  Labels sign(x . w*) with w* ~ N(0,1)^68 (0 -> +1), then 5%
+    flipped.  Returns (row_ptr, cols, vals, labels)."""
+    rng = np.random.default_rng(seed)
+    p = _zipf_probs(n_levels, zipf_s)
+    w_star = rng.standard_normal(n_cols)
+    ptrs, cols, vals, labels = [np.zeros(1, np.int64)], [], [], []
+    base = 0
+    for lo in range(0, n_rows, chunk):
+        k = min(chunk, n_rows - lo)
+        X = rng.choice(n_levels, size=(k, n_cols), p=p).astype(np.float64)
+        z = X @ w_star
+        y = np.where(z >= 0, 1.0, -1.0)
+        y[rng.random(k) < flip] *= -1.0
+        rp, c, v = dense_to_csr(X)
+        ptrs.append(rp[1:] + base)
+        base += int(rp[-1])
+        cols.append(c)
+        vals.append(v)
+        labels.append(y)
+    return np.concatenate(ptrs), np.concatenate(cols), np.concatenate(vals), np.concatenate(labels)
+
+
+# ---- config 4: sparse high-dimensional hinge MGD data --------------------------------------
+def cfg4_dataset(n_rows: int = 800_000, n_cols: int = 47_236, seed: int = 4, nnz: int = 75,
+                 zipf_s: float = 1.1, levels: int = 1000, chunk: int = 50_000):
+    """BASELINE.json configs[3]: ~75 distinct columns per row with Zipf(1.1) column popularity
+    (drawn without replacement: 4x oversampling with replacement, de-duplicated, then a random 75
+    of the distinct ones), raw values U(0,1], each row L2-normalised and THEN quantised to 1000
+    levels in (0,1] (q = ceil(1000 x) / 1000) so the value alphabet stays small.
+    Labels sign(x . w*) for a random sparse hyperplane w* (10% of columns N(0,1)), 0 -> +1."""
+    rng = np.random.default_rng(seed)
+    p = _zipf_probs(n_cols, zipf_s)
+    perm = rng.permutation(n_cols)  # popularity rank -> column id
+    cdf = np.cumsum(p)
+    w_star = np.where(rng.random(n_cols) < 0.1, rng.standard_normal(n_cols), 0.0)
+    ptrs, cols_out, vals_out, labels = [np.zeros(1, np.int64)], [], [], []
+    base = 0
+    for lo in range(0, n_rows, chunk):
+        k = min(chunk, n_rows - lo)
+        cand = perm[np.minimum(np.searchsorted(cdf, rng.random((k, 4 * nnz))), n_cols - 1)]
+        cand.sort(axis=1)
+        dup = np.zeros_like(cand, dtype=bool)
+        dup[:, 1:] = cand[:, 1:] == cand[:, :-1]
+        prio = rng.random(cand.shape)
+        prio[dup] = 2.0  # duplicates last
+        pick = np.argsort(prio, axis=1)[:, :nnz]
+        chosen = np.take_along_axis(cand, pick, axis=1)
+        ok = np.take_along_axis(prio, pick, axis=1) < 2.0
+        chosen = np.where(ok, chosen, -1)
+        chosen.sort(axis=1)
+        raw = rng.random(chosen.shape)
+        raw = np.where(chosen >= 0, raw, 0.0)
+        raw /= np.sqrt((raw * raw).sum(axis=1, keepdims=True))
+        q = np.where(chosen >= 0, np.maximum(np.ceil(raw * levels), 1.0) / levels, 0.0)
+        keep = chosen >= 0
+        lens = keep.sum(axis=1)
+        rp = np.zeros(k + 1, np.int64)
+        np.cumsum(lens, out=rp[1:])
+        c = chosen[keep].astype(np.int32)
+        v = q[keep]
+        z = np.add.reduceat(v * w_star[c], rp[:-1]) if len(v) else np.zeros(k)
+        z[lens == 0] = 0.0
+        labels.append(np.where(z >= 0, 1.0, -1.0))
+        ptrs.append(rp[1:] + base)
+        base += int(rp[-1])
+        cols_out.append(c)
+        vals_out.append(v)
+    return np.concatenate(ptrs), np.concatenate(cols_out), np.concatenate(vals_out), np.concatenate(labels)

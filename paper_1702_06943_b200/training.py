@@ -1,0 +1,207 @@
+"""Mini-batch gradient descent over TOC-compressed batches on the device (reference
+training.py:1-361).
+
+``train`` keeps the reference's contract: shuffle once with the stdlib RNG (training.py:131-142),
+carve contiguous batches (the last may be short, :145-167), start GLM weights at zero (:319-326),
+run the configured epochs with ``w <- w - (lr / |B|) * g`` per batch (:296-316), and record the
+full-dataset empirical risk after every epoch plus the epoch's batch-loop time (:336-361).
+Compression happens once, on the GPU (codec.compress_csr); each epoch is ONE cooperative kernel
+launch (toc_glm_epoch) whose CTAs relay the weights step to step through L2.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import random
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native as N
+from .codec import compress_csr
+from .kernels import OpCounter
+from .matrix import LabeledDataset, SparseRowMatrix, as_vector
+
+LOSS_KINDS = ("squared", "logistic", "hinge", "nn_mse")
+EXECUTION_MODES = ("compressed", "dense", "csr")
+LOSS_CODE = {"squared": 0, "logistic": 1, "hinge": 2}
+
+
+@dataclass
+class TrainConfig:
+    """Training hyper-parameters (reference training.py:46-68)."""
+
+    loss_kind: str
+    batch_size: int
+    learning_rate: float
+    epochs: int
+    seed: int = 0
+    hidden_units: int = 16
+    execution: str = "compressed"
+
+    def __post_init__(self) -> None:
+        if self.loss_kind not in LOSS_KINDS:
+            raise ValueError(f"loss_kind must be one of {LOSS_KINDS}, got {self.loss_kind!r}")
+        if self.execution not in EXECUTION_MODES:
+            raise ValueError(f"execution must be one of {EXECUTION_MODES}, got {self.execution!r}")
+        if self.batch_size < 1:
+            raise ValueError(f"batch_size must be at least 1, got {self.batch_size}")
+        if self.epochs < 1:
+            raise ValueError(f"epochs must be at least 1, got {self.epochs}")
+        if not (math.isfinite(self.learning_rate) and self.learning_rate > 0):
+            raise ValueError(f"learning_rate must be positive and finite, got {self.learning_rate}")
+        if self.loss_kind == "nn_mse" and self.hidden_units < 1:
+            raise ValueError(f"hidden_units must be at least 1, got {self.hidden_units}")
+
+
+@dataclass
+class GlmModel:
+    """Linear model x . weights (training.py:71-78)."""
+
+    weights: np.ndarray
+
+    def __post_init__(self) -> None:
+        self.weights = as_vector(self.weights, len(self.weights), "weights")
+
+
+@dataclass
+class LossTrace:
+    """Per-epoch full-dataset risk plus the batch-loop time (training.py:123-128)."""
+
+    risks: list = field(default_factory=list)
+    seconds: list = field(default_factory=list)
+
+
+def shuffle_order(n_rows: int, seed: int) -> np.ndarray:
+    """The permutation of shuffle_once (training.py:138-139): stdlib Fisher-Yates, once."""
+    order = list(range(n_rows))
+    random.Random(seed).shuffle(order)
+    return np.asarray(order, dtype=np.int64)
+
+
+def shuffle_once(dataset: LabeledDataset, seed: int) -> LabeledDataset:
+    order = shuffle_order(dataset.n_rows, seed)
+    return LabeledDataset(features=dataset.features.take_rows(order), labels=dataset.labels[order])
+
+
+class DeviceBatches:
+    """The epoch's mini-batches as TOC1 blocks in HBM, labels per row (make_batches with
+    execution='compressed', training.py:145-167, but one arena instead of one object per batch)."""
+
+    def __init__(self, dataset: LabeledDataset, batch_size: int):
+        torch = N.require_cuda()
+        s = dataset.features
+        n = s.n_rows
+        if n == 0:
+            raise ValueError("cannot batch an empty dataset")
+        if batch_size < 1:
+            raise ValueError(f"batch_size must be at least 1, got {batch_size}")
+        batch_row = np.concatenate([np.arange(0, n, batch_size), [n]]).astype(np.int64)
+        self.arena = compress_csr(s.n_cols, s.row_ptr, s.cols, s.vals, batch_row)
+        self.labels = torch.from_numpy(np.ascontiguousarray(dataset.labels, np.float64)).cuda()
+        self.n_cols = s.n_cols
+        self.n_rows = n
+        self.batch_sizes = np.diff(batch_row)
+
+    def kernel_cost_per_step(self) -> np.ndarray:
+        m = self.arena.meta
+        return (m["n_pairs"].astype(np.int64) + m["n_derived"] + m["n_codes"]).astype(np.int64)
+
+
+def _bind():
+    L = N.lib()
+    if not getattr(L, "_mgd_bound", False):
+        P, I64, I32, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_double
+        L.toc_mgd_workspace.argtypes = [P, I64, I32, I32, ctypes.POINTER(ctypes.c_int64)]
+        L.toc_glm_epoch.argtypes = [P, P, P, P, P, I64, I32, I32, D, P, P, P, P, P]
+        L.toc_glm_grad.argtypes = [P, P, P, P, P, I64, I32, I32, P, P, P, P, P]
+        L.toc_glm_risk.argtypes = [P, P, I64, I32, P, I32, P]
+        L._mgd_bound = True
+    return L
+
+
+class GlmTrainer:
+    """Device-resident GLM training state over DeviceBatches."""
+
+    def __init__(self, batches: DeviceBatches, loss_kind: str, learning_rate: float):
+        self.torch = N.require_cuda()
+        self.b = batches
+        self.loss = LOSS_CODE[loss_kind]
+        self.lr = float(learning_rate)
+        torch = self.torch
+        self.w = torch.zeros(max(batches.n_cols, 1), dtype=torch.float64, device="cuda")
+        self.sync = torch.zeros(2, dtype=torch.int32, device="cuda")
+        self.partial = torch.zeros(148, dtype=torch.float64, device="cuda")
+        L = _bind()
+        a = batches.arena
+        nbytes = ctypes.c_int64()
+        N.check(L.toc_mgd_workspace(a.meta.ctypes.data_as(ctypes.c_void_p), a.n_blocks, batches.n_cols, 0,
+                                    ctypes.byref(nbytes)), "toc_mgd_workspace")
+        self.scratch = torch.empty(max(nbytes.value, 16), dtype=torch.uint8, device="cuda")
+
+    def epoch(self) -> float:
+        """One epoch; returns its device time in seconds (CUDA events on the launch stream)."""
+        torch = self.torch
+        a = self.b.arena
+        a.raise_corrupt()
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record()
+        N.check(_bind().toc_glm_epoch(a.data.data_ptr(), a.block_off_d.data_ptr(), a.meta_d.data_ptr(),
+                                      a.meta.ctypes.data_as(ctypes.c_void_p), a.row_base_d.data_ptr(), a.n_blocks,
+                                      self.b.n_cols, self.loss, self.lr, self.b.labels.data_ptr(), self.w.data_ptr(),
+                                      self.sync.data_ptr(), self.scratch.data_ptr(), N.stream_handle()),
+                "toc_glm_epoch")
+        end.record()
+        end.synchronize()
+        if int(self.sync[1].item()):
+            raise RuntimeError("toc_glm_epoch aborted (step hand-off timed out)")
+        return start.elapsed_time(end) / 1e3
+
+    def risk(self) -> float:
+        """Mean loss over every row (empirical_risk, training.py:231-258), on the device."""
+        a = self.b.arena
+        z = a.matvec(self.w[: self.b.n_cols])
+        N.check(_bind().toc_glm_risk(z.data_ptr(), self.b.labels.data_ptr(), self.b.n_rows, self.loss,
+                                     self.partial.data_ptr(), self.partial.numel(), N.stream_handle()), "toc_glm_risk")
+        return float(self.partial.sum().item()) / self.b.n_rows
+
+    def weights(self) -> np.ndarray:
+        return self.w[: self.b.n_cols].cpu().numpy().copy()
+
+
+def init_model(config: TrainConfig, n_cols: int):
+    """Zero weights for GLMs (training.py:319-326)."""
+    if config.loss_kind != "nn_mse":
+        return GlmModel(weights=np.zeros(n_cols, dtype=np.float64))
+    raise NotImplementedError("nn_mse is trained by paper_1702_06943_b200.mlp (matmat kernels)")
+
+
+def train(dataset: LabeledDataset, config: TrainConfig, counter: OpCounter | None = None):
+    """Shuffle once, batch once, then run the configured epochs (training.py:336-361)."""
+    if dataset.n_rows == 0:
+        raise ValueError("cannot train on an empty dataset")
+    if config.loss_kind in ("logistic", "hinge"):
+        bad = [float(v) for v in np.unique(dataset.labels) if v not in (-1.0, 1.0)]
+        if bad:
+            raise ValueError(f"{config.loss_kind} loss needs labels in {{-1, +1}}, found {bad}")
+    if config.loss_kind == "nn_mse":
+        from .mlp import train_nn
+
+        return train_nn(dataset, config, counter)
+    if config.execution != "compressed":
+        raise ValueError(f"execution {config.execution!r}: the device path trains on compressed batches only")
+    shuffled = shuffle_once(dataset, config.seed)
+    batches = DeviceBatches(shuffled, config.batch_size)
+    trainer = GlmTrainer(batches, config.loss_kind, config.learning_rate)
+    trace = LossTrace()
+    per_step = batches.kernel_cost_per_step()
+    for _ in range(config.epochs):
+        trace.seconds.append(trainer.epoch())
+        trace.risks.append(trainer.risk())
+        if counter is not None:  # one matvec + one vecmat per step (test_training.py:217-223)
+            counter.multiply_adds += int(2 * per_step.sum())
+            nodes = int((batches.arena.meta["n_pairs"].astype(np.int64) + batches.arena.meta["n_derived"]).sum())
+            counter.tree_nodes_visited += 2 * nodes
+            counter.codes_visited += 2 * int(batches.arena.meta["n_codes"].astype(np.int64).sum())
+    return GlmModel(weights=trainer.weights()), trace

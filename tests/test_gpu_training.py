@@ -1,0 +1,131 @@
+"""GPU parity for MGD on compressed batches.
+
+Bar (BASELINE.json north_star): per-epoch loss curves within 1e-6 relative of the reference
+(here: the reference's own golden curves, tests/golden, and the oracle port on larger seeded
+data); final weights within 1e-6 relative (max(1,|w|) scale).
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import struct
+
+import numpy as np
+import pytest
+
+from conftest import max_rel_err, within_rel
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = json.load(open(os.path.join(HERE, "golden", "golden.json")))
+REL = 1e-6
+
+
+def unhex(xs):
+    return np.array([struct.unpack("<d", bytes.fromhex(x))[0] for x in xs], dtype=np.float64)
+
+
+def dataset_from_csr(n_cols, rp, c, v, y):
+    from paper_1702_06943_b200.matrix import LabeledDataset, SparseRowMatrix
+
+    return LabeledDataset(features=SparseRowMatrix.from_csr(n_cols, rp, c, v), labels=y)
+
+
+@pytest.mark.parametrize("i", range(len(GOLD["training"])))
+def test_train_matches_reference_curves(i):
+    from paper_1702_06943_b200.matrix import LabeledDataset, SparseRowMatrix
+    from paper_1702_06943_b200.training import TrainConfig, train
+
+    c = GOLD["training"][i]
+    rows = [[(col, struct.unpack("<d", bytes.fromhex(x))[0]) for col, x in r] for r in c["rows"]]
+    ds = LabeledDataset(features=SparseRowMatrix(c["n_cols"], rows), labels=unhex(c["labels"]))
+    cfg = TrainConfig(loss_kind=c["loss"], batch_size=c["batch_size"], learning_rate=c["lr"], epochs=c["epochs"],
+                      seed=c["seed"])
+    model, trace = train(ds, cfg)
+    want = unhex(c["risks"])
+    assert len(trace.risks) == c["epochs"] and len(trace.seconds) == c["epochs"]
+    assert np.all(np.abs(np.array(trace.risks) - want) <= REL * np.abs(want)), (trace.risks, want)
+    assert within_rel(model.weights, unhex(c["weights"]), REL), max_rel_err(model.weights, unhex(c["weights"]))
+
+
+def _vs_oracle(oracle, n_cols, rp, c, v, y, loss, bs, lr, epochs, seed=0):
+    from paper_1702_06943_b200.training import TrainConfig, train
+
+    w_ref, risks_ref = oracle.train_glm(rp, c, v, y, n_cols, loss, bs, lr, epochs, seed)
+    model, trace = train(dataset_from_csr(n_cols, rp, c, v, y),
+                         TrainConfig(loss_kind=loss, batch_size=bs, learning_rate=lr, epochs=epochs, seed=seed))
+    risks_ref = np.asarray(risks_ref)
+    assert np.all(np.abs(np.array(trace.risks) - risks_ref) <= REL * np.abs(risks_ref)), (trace.risks, risks_ref)
+    assert within_rel(model.weights, w_ref, REL), max_rel_err(model.weights, w_ref)
+    return trace
+
+
+def test_cfg3_logistic_vs_oracle(oracle):
+    from paper_1702_06943_b200 import synth
+
+    rp, c, v, y = synth.cfg3_dataset(20_000, seed=13)
+    _vs_oracle(oracle, 68, rp, c, v, y, "logistic", 250, 0.1, 3)
+
+
+def test_cfg4_hinge_large_m_vs_oracle(oracle):
+    """47,236 columns: gradient accumulators and the touched-column set live in global memory."""
+    from paper_1702_06943_b200 import synth
+
+    rp, c, v, y = synth.cfg4_dataset(6_000, seed=14)
+    _vs_oracle(oracle, 47_236, rp, c, v, y, "hinge", 250, 0.01, 2)
+
+
+def test_squared_short_last_batch(oracle):
+    from helpers import random_alphabet_rows
+
+    rng = np.random.default_rng(21)
+    rows = random_alphabet_rows(rng, 1003, 9, 0.6)
+    rp, c, v = oracle.rows_to_csr(rows)
+    w = rng.standard_normal(9)
+    y = np.array([sum(val * w[col] for col, val in r) for r in rows])
+    _vs_oracle(oracle, 9, rp, c, v, y, "squared", 64, 1e-3, 3, seed=5)
+
+
+def test_batch_gradients_vs_oracle(oracle):
+    """toc_glm_grad: the summed per-batch gradient the data-parallel trainer all-reduces."""
+    import torch
+
+    from paper_1702_06943_b200 import synth
+    from paper_1702_06943_b200.distributed import batch_gradients
+    from paper_1702_06943_b200.training import DeviceBatches
+
+    rp, c, v, y = synth.cfg3_dataset(3_000, seed=15)
+    ds = dataset_from_csr(68, rp, c, v, y)
+    batches = DeviceBatches(ds, 250)
+    w = np.random.default_rng(1).standard_normal(68) * 0.1
+    G = batch_gradients(batches, "logistic", torch.from_numpy(w).cuda()).cpu().numpy()
+    for b in range(len(batches.batch_sizes)):
+        lo, hi = 250 * b, min(250 * (b + 1), 3000)
+        enc = oracle.encode_csr(68, rp[lo : hi + 1] - rp[lo], c[rp[lo] : rp[hi]], v[rp[lo] : rp[hi]])
+        t = oracle.Tree.from_encoding(enc)
+        z = t.matvec(w)
+        s = -y[lo:hi] / (1.0 + np.exp(y[lo:hi] * z))
+        want = t.vecmat(s)
+        assert within_rel(G[b], want, 1e-9), max_rel_err(G[b], want)
+
+
+def test_counter_charges_matvec_and_vecmat(oracle):
+    from paper_1702_06943_b200 import synth
+    from paper_1702_06943_b200.kernels import OpCounter
+    from paper_1702_06943_b200.training import TrainConfig, train
+
+    rp, c, v, y = synth.cfg3_dataset(1_000, seed=16)
+    counter = OpCounter()
+    train(dataset_from_csr(68, rp, c, v, y), TrainConfig("logistic", 250, 0.1, 1), counter)
+    order = oracle.shuffle_order(1000, 0)
+    want = 0
+    for lo in range(0, 1000, 250):
+        idx = order[lo : lo + 250]
+        lens = np.diff(rp)[idx]
+        brp = np.concatenate([[0], np.cumsum(lens)])
+        g = np.concatenate([np.arange(rp[i], rp[i + 1]) for i in idx])
+        enc = oracle.encode_csr(68, brp, c[g], v[g])
+        want += 2 * ((enc.tree_length() - 1) + len(enc.codes))
+    assert counter.multiply_adds == want
