@@ -189,6 +189,13 @@ int toc_glm_epoch(const uint8_t* d_arena, const int64_t* d_block_off, const TocB
                   int32_t n_cols, int32_t loss, double lr, const double* d_labels, double* d_w,
                   uint32_t* d_sync, void* d_scratch, void* stream);
 
+/* toc_glm_epoch plus a phase trace: d_trace receives 8 clock64 stamps per step (tables built,
+ * weights acquired, P1, A.w, loss scalar, s^T.A, column scatter, update published). */
+int toc_glm_epoch_traced(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+                         const TocBlockMeta* h_meta, const int64_t* d_row_base, int64_t n_blocks,
+                         int32_t n_cols, int32_t loss, double lr, const double* d_labels, double* d_w,
+                         uint32_t* d_sync, void* d_scratch, long long* d_trace, void* stream);
+
 /* Summed gradient of every batch at fixed w (glm_gradient, training.py:261-281):
  * d_grad[b * n_cols + c].  The data-parallel trainer all-reduces these. */
 int toc_glm_grad(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,

@@ -258,10 +258,16 @@ struct Batch {
     with_width(m.w_cols, [&]<int W>() {
       SeqReader<W> rd;
       rd.init(blk + m.off_cols, p0);
-      for (uint32_t i = p0; i < p1; ++i) {
-        const uint32_t c = rd.next();
-        const double x = kCG ? __ldcg(vec + c) : vec[c];
-        tab[i + 1] = uniq[tabw[2 * (i + 1)]] * x;
+      for (uint32_t i = p0; i < p1; i += 8) {  // 8 independent vec loads in flight
+        uint32_t c[8];
+        double x[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) c[k] = (i + k < p1) ? rd.next() : 0u;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = (i + k < p1) ? (kCG ? __ldcg(vec + c[k]) : vec[c[k]]) : 0.0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (i + k < p1) tab[i + k + 1] = uniq[tabw[2 * (i + k + 1)]] * x[k];
       }
     });
   }
@@ -328,6 +334,27 @@ struct Batch {
         const uint32_t c = rd.next();
         const long long g = __double2ll_rn(tab[i + 1] * o_scale);
         if (g) fix_add(out + 2 * c, g);
+      }
+    });
+  }
+
+  // w[col_i] -= step * value_i * G[i] directly (global fp64 reductions, no accumulators): the
+  // update of apply_update (training.py:296-300) distributed over the first-layer pairs.
+  TOC_D void scatter_update(double* w, double g_inv, double step) {
+    if (p0 >= p1) return;
+    with_width(m.w_refs, [&]<int W>() {
+      SeqReader<W> rd;
+      rd.init(blk + m.off_refs, p0);
+      for (uint32_t i = p0; i < p1; ++i)
+        tab[i + 1] = uniq[rd.next()] * fix_value(tabw[2 * (i + 1)], tabw[2 * (i + 1) + 1], g_inv);
+    });
+    with_width(m.w_cols, [&]<int W>() {
+      SeqReader<W> rd;
+      rd.init(blk + m.off_cols, p0);
+      for (uint32_t i = p0; i < p1; ++i) {
+        const uint32_t c = rd.next();
+        const double g = tab[i + 1];
+        if (g != 0.0) atomicAdd(w + c, -__dmul_rn(step, g));
       }
     });
   }

@@ -32,7 +32,14 @@ struct MgdArgs {
   int64_t slab_bytes;     // global slab per CTA (tables of oversized batches)
   uint8_t* scratch;       // [ctas * slab_bytes] tables, then [ctas * 8 * n_cols] accumulators
   double* grad_out;       // gradient kernel only: [n_blocks x n_cols] summed gradients
+  long long* trace;       // optional: kTracePoints clock64 stamps per step (phase profiling)
 };
+
+constexpr int kTracePoints = 8;
+
+TOC_D void stamp(const MgdArgs& a, int64_t t, int k) {
+  if (a.trace && threadIdx.x == 0) a.trace[t * kTracePoints + k] = clock64();
+}
 
 // Per-example scalar of glm_gradient (training.py:272-280).
 TOC_D double loss_scalar(int loss, double y, double z) {
@@ -54,43 +61,67 @@ TOC_D void st_release(uint32_t* p, uint32_t v) {
 // Gradient of one batch into fixed-point column accumulators `acc` (2 words per column).
 // Returns the inverse output scale.  srow: n doubles of shared memory.  Entered after the node
 // tables are complete (keys resolved) and `w` is current.
+// Weight-independent part of a step, done while earlier steps run on other SMs: the node
+// tables plus the bounds that fix the fixed-point scales (max |value|, sum |y|).
+template <bool kWide>
+TOC_D void build_step(Batch<kWide>& B, const MgdArgs& a, int64_t b, uint32_t* s_warp, double* s_red,
+                      double& vmax, double& ysum) {
+  const int64_t rb = a.row_base[b];
+  B.load_index(s_warp);
+  B.build_nodes();
+  double ys = 0.0;
+  for (uint32_t r = threadIdx.x; r < B.n; r += blockDim.x) ys += fabs(a.labels[rb + r]);
+  __syncthreads();
+  B.resolve_keys();
+  vmax = block_max_d(B.vmax, s_red);
+  ysum = block_sum(ys, s_red);
+}
+
+// Gradient of one batch: P1 from w, A.w, the loss scalar, s^T.A into G (fixed point).  Returns
+// g_scale.  srow: n doubles of shared memory.  For logistic and hinge |s| <= |y|, so the scale
+// comes from the precomputed sum |y| and no reduction sits on the critical path.
 template <bool kWide, bool kCG>
-TOC_D double batch_gradient(Batch<kWide>& B, const MgdArgs& a, int64_t b, double* srow, uint32_t* acc,
-                            double* s_red) {
+TOC_D double batch_gradient(Batch<kWide>& B, const MgdArgs& a, int64_t b, double* srow, double ysum,
+                            double* s_red, double& bound_out) {
   const uint32_t tid = threadIdx.x, nth = blockDim.x;
   const int64_t rb = a.row_base[b];
   B.template compute_p1<kCG>(a.w);
   __syncthreads();
-  B.matvec_rows([&](uint32_t r, double z) { srow[r] = z; });
+  stamp(a, b, 2);
+  B.matvec_rows([&](uint32_t r, double z) { srow[r] = loss_scalar(a.loss, a.labels[rb + r], z); });
   __syncthreads();
-  double su = 0.0;
-  for (uint32_t r = tid; r < B.n; r += nth) {
-    const double s = loss_scalar(a.loss, a.labels[rb + r], srow[r]);
-    srow[r] = s;
-    su += fabs(s);
+  stamp(a, b, 3);
+  double bound = ysum;
+  if (a.loss == TOC_LOSS_SQUARED) {
+    double su = 0.0;
+    for (uint32_t r = tid; r < B.n; r += nth) su += fabs(srow[r]);
+    bound = block_sum(su, s_red);
   }
   B.zero_tab();
-  su = block_sum(su, s_red);  // contains barriers
-  const double mv = block_max_d(B.vmax, s_red);
-  const double g_scale = fix_scale(su), o_scale = fix_scale(su * mv);
+  __syncthreads();
+  stamp(a, b, 4);
+  const double g_scale = fix_scale(bound);
+  bound_out = bound;
   B.vecmat_rows([&](uint32_t r) { return srow[r]; }, g_scale);
   __syncthreads();
-  B.scatter_columns(acc, 1.0 / g_scale, o_scale);
-  __syncthreads();
-  return 1.0 / o_scale;
+  stamp(a, b, 5);
+  return g_scale;
 }
 
-// w[c] -= (lr / |B|) * g[c] for every column of the batch's first layer, once per column
-// (apply_update, training.py:296-300; untouched columns have g = 0 and stay bit-identical).
-// The accumulators of updated columns are cleared for the CTA's next step.
+// Small n_cols: column gradients in shared fixed-point accumulators (deterministic), then
+// w[c] -= (lr / |B|) * g[c] once per touched column (apply_update, training.py:296-300; untouched
+// columns have g = 0 and stay bit-identical).  Accumulators are cleared for the next step.
 template <bool kWide>
-TOC_D void apply_update(Batch<kWide>& B, const MgdArgs& a, uint32_t* acc, uint32_t* touched, double o_inv) {
+TOC_D void update_small(Batch<kWide>& B, const MgdArgs& a, uint32_t* acc, uint32_t* touched, double g_scale,
+                        double vmax, double ysum_or_bound) {
+  const double o_scale = fix_scale(ysum_or_bound * vmax), o_inv = 1.0 / o_scale;
+  B.scatter_columns(acc, 1.0 / g_scale, o_scale);
+  __syncthreads();
   const double step = a.lr / (double)B.n;
   B.for_each_pair_column([&](uint32_t, uint32_t c) {
     const uint32_t bit = 1u << (c & 31);
     if (atomicOr(&touched[c >> 5], bit) & bit) return;  // another pair of this column won
-    const uint32_t* ac = acc + 2 * c;
-    const double g = fix_value(a.small_m ? ac[0] : __ldcg(ac), a.small_m ? ac[1] : __ldcg(ac + 1), o_inv);
+    const double g = fix_value(acc[2 * c], acc[2 * c + 1], o_inv);
     a.w[c] = __dsub_rn(__ldcg(a.w + c), __dmul_rn(step, g));  // L2: other CTAs wrote w
     acc[2 * c] = 0u;
     acc[2 * c + 1] = 0u;
@@ -105,15 +136,14 @@ __global__ void __launch_bounds__(1024, 1) glm_epoch_kernel(MgdArgs a) {
   __shared__ uint32_t s_go;
   uint8_t* p = smem + kFixedBytes;
   const uint32_t tid = threadIdx.x, nth = blockDim.x, m = (uint32_t)a.n_cols, words = (m + 31) / 32;
-  uint32_t* touched = reinterpret_cast<uint32_t*>(p);
-  p += align16(4u * words);
+  uint32_t* touched = nullptr;
   uint32_t* acc = nullptr;
   if (a.small_m) {
+    touched = reinterpret_cast<uint32_t*>(p);
+    p += align16(4u * words);
     acc = reinterpret_cast<uint32_t*>(p);
     p += align16(8u * m);
     for (uint32_t c = tid; c < 2 * m; c += nth) acc[c] = 0u;
-  } else {
-    acc = reinterpret_cast<uint32_t*>(a.scratch + (int64_t)gridDim.x * a.slab_bytes) + (int64_t)blockIdx.x * 2 * m;
   }
   for (int64_t t = blockIdx.x; t < a.n_blocks; t += gridDim.x) {
     const TocBlockMeta mt = a.meta[t];
@@ -123,11 +153,11 @@ __global__ void __launch_bounds__(1024, 1) glm_epoch_kernel(MgdArgs a) {
     const uint32_t need = batch_layout<kWide>(mt).total + align16(8u * mt.n_rows);
     if (need > (uint32_t)a.batch_smem_budget) tables = a.scratch + (int64_t)blockIdx.x * a.slab_bytes;
     B.init(a.arena + a.block_off[t], mt, tables);
-    for (uint32_t w = tid; w < words; w += nth) touched[w] = 0u;
-    B.load_index(s_warp);
-    B.build_nodes();
-    __syncthreads();
-    B.resolve_keys();
+    if (a.small_m)
+      for (uint32_t w = tid; w < words; w += nth) touched[w] = 0u;
+    double vmax, ysum;
+    build_step(B, a, t, s_warp, s_red, vmax, ysum);
+    stamp(a, t, 0);
     // wait for the weights of step t (bounded: a hang would take the GPU down with it)
     if (tid == 0) {
       uint32_t go = 1;
@@ -135,16 +165,21 @@ __global__ void __launch_bounds__(1024, 1) glm_epoch_kernel(MgdArgs a) {
       while (ld_acquire(a.counter) != (uint32_t)t) {
         if (ld_acquire(a.abort_flag)) { go = 0; break; }
         if (++spins > (1ll << 26)) { atomicExch(a.abort_flag, 1u); go = 0; break; }
-        __nanosleep(64);
+        __nanosleep(32);
       }
       s_go = go;
     }
     __syncthreads();
     if (!s_go) return;
-    const double o_inv = batch_gradient<kWide, true>(B, a, t, srow, acc, s_red);
-    apply_update(B, a, acc, touched, o_inv);
+    stamp(a, t, 1);
+    double bound;
+    const double g_scale = batch_gradient<kWide, true>(B, a, t, srow, ysum, s_red, bound);
+    if (a.small_m) update_small(B, a, acc, touched, g_scale, vmax, bound);
+    else B.scatter_update(a.w, 1.0 / g_scale, a.lr / (double)B.n);
+    stamp(a, t, 6);
     __threadfence();
     __syncthreads();
+    stamp(a, t, 7);
     if (tid == 0) st_release(a.counter, (uint32_t)t + 1);
   }
 }
@@ -176,12 +211,13 @@ __global__ void __launch_bounds__(1024, 1) glm_grad_kernel(MgdArgs a) {
       for (uint32_t c = tid; c < 2 * m; c += nth) acc[c] = 0u;
     Batch<kWide> B;
     B.init(a.arena + a.block_off[b], mb, tables);
-    B.load_index(s_warp);
-    B.build_nodes();
+    double vmax, ysum, bound;
+    build_step(B, a, b, s_warp, s_red, vmax, ysum);
     __syncthreads();
-    B.resolve_keys();
+    const double g_scale = batch_gradient<kWide, false>(B, a, b, srow, ysum, s_red, bound);
+    const double o_scale = fix_scale(bound * vmax), o_inv = 1.0 / o_scale;
+    B.scatter_columns(acc, 1.0 / g_scale, o_scale);
     __syncthreads();
-    const double o_inv = batch_gradient<kWide, false>(B, a, b, srow, acc, s_red);
     if (a.small_m) {
       for (uint32_t c = tid; c < m; c += nth) g[c] = fix_value(acc[2 * c], acc[2 * c + 1], o_inv);
     } else {
@@ -247,14 +283,14 @@ MgdLaunch mgd_plan(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t n_cols,
   const uint32_t m = (uint32_t)n_cols;
   const uint32_t small_bytes = toc::align16(8u * m);
   L.small_m = small_bytes <= 32u * 1024u;
-  uint32_t fixed = toc::kFixedBytes + (epoch ? toc::align16(4u * ((m + 31) / 32)) : 0u) + (L.small_m ? small_bytes : 0u);
+  uint32_t fixed = toc::kFixedBytes + (L.small_m ? small_bytes + (epoch ? toc::align16(4u * ((m + 31) / 32)) : 0u) : 0u);
   uint32_t avail = (uint32_t)optin > fixed ? (uint32_t)optin - fixed : 0u;
   L.budget = (int32_t)(max_need <= avail ? max_need : avail);
   L.smem = (int)(fixed + (uint32_t)L.budget);
   L.threads = 1024;
   L.ctas = (int)(n_blocks < sm ? (n_blocks > 0 ? n_blocks : 1) : sm);
   L.slab = max_need > (uint32_t)L.budget ? (int64_t)toc::align16(max_need) : 0;
-  L.scratch = (int64_t)L.ctas * L.slab + (L.small_m ? 0 : (int64_t)L.ctas * 8 * m);
+  L.scratch = (int64_t)L.ctas * L.slab;
   return L;
 }
 
@@ -280,9 +316,6 @@ static int mgd_launch(const TocBlockMeta* h_meta, const toc::MgdArgs& a0, bool e
   a.small_m = L.small_m;
   a.slab_bytes = L.slab;
   if (L.scratch > 0 && !a.scratch) return TOC_E_ARG;
-  if (epoch && !L.small_m)  // per-CTA global gradient accumulators start at zero
-    if (cudaMemsetAsync(a.scratch + (int64_t)L.ctas * L.slab, 0, (size_t)L.ctas * 8 * a.n_cols, s) != cudaSuccess)
-      return TOC_E_CUDA;
   void* fn;
   if (epoch) fn = wide ? (void*)toc::glm_epoch_kernel<true> : (void*)toc::glm_epoch_kernel<false>;
   else fn = wide ? (void*)toc::glm_grad_kernel<true> : (void*)toc::glm_grad_kernel<false>;
@@ -300,10 +333,22 @@ static int mgd_launch(const TocBlockMeta* h_meta, const toc::MgdArgs& a0, bool e
   return e == cudaSuccess ? TOC_OK : TOC_E_CUDA;
 }
 
+extern "C" int toc_glm_epoch_traced(const uint8_t*, const int64_t*, const TocBlockMeta*, const TocBlockMeta*,
+                                    const int64_t*, int64_t, int32_t, int32_t, double, const double*, double*, uint32_t*,
+                                    void*, long long*, void*);
+
 extern "C" int toc_glm_epoch(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
                              const TocBlockMeta* h_meta, const int64_t* d_row_base, int64_t n_blocks, int32_t n_cols,
                              int32_t loss, double lr, const double* d_labels, double* d_w, uint32_t* d_sync,
                              void* d_scratch, void* stream) {
+  return toc_glm_epoch_traced(d_arena, d_block_off, d_meta, h_meta, d_row_base, n_blocks, n_cols, loss, lr, d_labels,
+                              d_w, d_sync, d_scratch, nullptr, stream);
+}
+
+extern "C" int toc_glm_epoch_traced(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+                                    const TocBlockMeta* h_meta, const int64_t* d_row_base, int64_t n_blocks,
+                                    int32_t n_cols, int32_t loss, double lr, const double* d_labels, double* d_w,
+                                    uint32_t* d_sync, void* d_scratch, long long* d_trace, void* stream) {
   if (n_blocks <= 0) return n_blocks == 0 ? TOC_OK : TOC_E_ARG;
   if (!h_meta || !d_w || !d_labels || !d_sync || loss < 0 || loss > 2) return TOC_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;
@@ -322,6 +367,7 @@ extern "C" int toc_glm_epoch(const uint8_t* d_arena, const int64_t* d_block_off,
   a.counter = d_sync;
   a.abort_flag = d_sync + 1;
   a.scratch = (uint8_t*)d_scratch;
+  a.trace = d_trace;
   return mgd_launch(h_meta, a, true, s);
 }
 
