@@ -177,6 +177,14 @@ int toc_unpack_blocks(const uint8_t* d_arena, const int64_t* d_block_off, const 
  * training.py:131-167); labels are per row in the same order.  Losses: */
 enum { TOC_LOSS_SQUARED = 0, TOC_LOSS_LOGISTIC = 1, TOC_LOSS_HINGE = 2 };
 
+/* Launch plan of the MGD kernels (diagnostic): info[8] = smem, table budget, small_m,
+ * 0, max |I|, ctas, slab bytes, wide. */
+int toc_mgd_plan_info(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t n_cols, int32_t kind,
+                      int64_t* info);
+
+/* Diagnostic: cap the MGD grid at n CTAs (0 restores one CTA per SM). */
+int toc_mgd_set_max_ctas(int32_t n);
+
 /* Device workspace (bytes) for toc_glm_epoch (kind 0) or toc_glm_grad (kind 1); host-only. */
 int toc_mgd_workspace(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t n_cols, int32_t kind,
                       int64_t* scratch_bytes);
@@ -190,7 +198,7 @@ int toc_glm_epoch(const uint8_t* d_arena, const int64_t* d_block_off, const TocB
                   uint32_t* d_sync, void* d_scratch, void* stream);
 
 /* toc_glm_epoch plus a phase trace: d_trace receives 8 clock64 stamps per step (tables built,
- * weights acquired, P1, A.w, loss scalar, s^T.A, column scatter, update published). */
+ * weights acquired, P1, A.w + loss scalar, bound, s^T.A, column update, published).  Diagnostic. */
 int toc_glm_epoch_traced(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
                          const TocBlockMeta* h_meta, const int64_t* d_row_base, int64_t n_blocks,
                          int32_t n_cols, int32_t loss, double lr, const double* d_labels, double* d_w,

@@ -338,27 +338,6 @@ struct Batch {
     });
   }
 
-  // w[col_i] -= step * value_i * G[i] directly (global fp64 reductions, no accumulators): the
-  // update of apply_update (training.py:296-300) distributed over the first-layer pairs.
-  TOC_D void scatter_update(double* w, double g_inv, double step) {
-    if (p0 >= p1) return;
-    with_width(m.w_refs, [&]<int W>() {
-      SeqReader<W> rd;
-      rd.init(blk + m.off_refs, p0);
-      for (uint32_t i = p0; i < p1; ++i)
-        tab[i + 1] = uniq[rd.next()] * fix_value(tabw[2 * (i + 1)], tabw[2 * (i + 1) + 1], g_inv);
-    });
-    with_width(m.w_cols, [&]<int W>() {
-      SeqReader<W> rd;
-      rd.init(blk + m.off_cols, p0);
-      for (uint32_t i = p0; i < p1; ++i) {
-        const uint32_t c = rd.next();
-        const double g = tab[i + 1];
-        if (g != 0.0) atomicAdd(w + c, -__dmul_rn(step, g));
-      }
-    });
-  }
-
   // Column c of this batch's first layer, for the thread's pairs (used to visit touched columns).
   template <typename F>
   TOC_D void for_each_pair_column(F&& f) const {

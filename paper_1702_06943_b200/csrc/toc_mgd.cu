@@ -33,6 +33,10 @@ struct MgdArgs {
   uint8_t* scratch;       // [ctas * slab_bytes] tables, then [ctas * 8 * n_cols] accumulators
   double* grad_out;       // gradient kernel only: [n_blocks x n_cols] summed gradients
   long long* trace;       // optional: kTracePoints clock64 stamps per step (phase profiling)
+  uint32_t* minidx;       // large n_cols: per-CTA [n_cols] scratch, all 0xffffffff between steps
+  uint32_t* leaders;      // large n_cols: per-CTA [max |I|] leader of each first-layer pair
+  uint2* irec;            // large n_cols: per-CTA [max |I|] unpacked (column, value ref) per pair
+  int32_t max_pairs;
 };
 
 constexpr int kTracePoints = 8;
@@ -54,6 +58,12 @@ TOC_D uint32_t ld_acquire(const uint32_t* p) {
   return v;
 }
 
+TOC_D unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 TOC_D void st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -65,16 +75,86 @@ TOC_D void st_release(uint32_t* p, uint32_t v) {
 // tables plus the bounds that fix the fixed-point scales (max |value|, sum |y|).
 template <bool kWide>
 TOC_D void build_step(Batch<kWide>& B, const MgdArgs& a, int64_t b, uint32_t* s_warp, double* s_red,
-                      double& vmax, double& ysum) {
+                      double& vmax, double& ysum, uint32_t* minidx = nullptr, uint32_t* leaders = nullptr) {
   const int64_t rb = a.row_base[b];
+  if (threadIdx.x == 0) {  // the whole block into L2: the weight-dependent phases re-read I
+    const uint32_t bytes = align16(B.m.off_offsets + (B.m.n_rows + 1u) * B.m.w_offsets);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(B.blk), "r"(bytes) : "memory");
+  }
   B.load_index(s_warp);
   B.build_nodes();
   double ys = 0.0;
   for (uint32_t r = threadIdx.x; r < B.n; r += blockDim.x) ys += fabs(a.labels[rb + r]);
   __syncthreads();
   B.resolve_keys();
+  if (minidx) {
+    // Unpack every first-layer pair to an aligned record and find each column's leader (its
+    // smallest pair id in this batch).  All weight-independent, so it runs here, off the critical
+    // path: atomicMin into a per-CTA column table, read back, then reset for the CTA's next step.
+    const uint8_t* cols = B.blk + B.m.off_cols;
+    const uint8_t* refs = B.blk + B.m.off_refs;
+    for (uint32_t i = threadIdx.x; i < B.nI; i += blockDim.x) {
+      const uint32_t c = ld_packed(cols, i, B.m.w_cols);
+      a.irec[i] = make_uint2(c, ld_packed(refs, i, B.m.w_refs));
+      atomicMin(minidx + c, i);
+    }
+    __threadfence();  // the minima are performed in L2; read them back through L2
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < B.nI; i += blockDim.x) leaders[i] = __ldcg(minidx + __ldcg(&a.irec[i].x));
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < B.nI; i += blockDim.x) minidx[__ldcg(&a.irec[i].x)] = 0xffffffffu;
+  }
   vmax = block_max_d(B.vmax, s_red);
   ysum = block_sum(ys, s_red);
+}
+
+// Large n_cols: g[c] = sum of value_i * G_i over the first-layer pairs i of column c, reduced in
+// shared memory into the column's leader slot (fixed point: exact and order-independent), then
+// w[c] -= (lr / |B|) * g[c] by the leader with one plain read-modify-write (apply_update,
+// training.py:296-300).  No global atomics on the critical path.
+template <bool kWide>
+TOC_D void update_leaders(Batch<kWide>& B, const MgdArgs& a, const uint32_t* leaders, double g_scale,
+                          double o_scale) {
+  const double g_inv = 1.0 / g_scale, o_inv = 1.0 / o_scale, step = a.lr / (double)B.n;
+  const uint32_t nI = B.nI, nth = blockDim.x, tid = threadIdx.x;
+  // contributions value_i * G_i, as fixed point at o_scale, in place
+#pragma unroll 4
+  for (uint32_t i = tid; i < nI; i += nth) {
+    const uint32_t ref = __ldcg(&a.irec[i].y);
+    const double c = B.uniq[ref] * fix_value(B.tabw[2 * (i + 1)], B.tabw[2 * (i + 1) + 1], g_inv);
+    const long long f = __double2ll_rn(c * o_scale);
+    B.tabw[2 * (i + 1)] = (uint32_t)f;
+    B.tabw[2 * (i + 1) + 1] = (uint32_t)((unsigned long long)f >> 32);
+  }
+  __syncthreads();
+#pragma unroll 4
+  for (uint32_t i = tid; i < nI; i += nth) {  // non-leaders fold into their leader
+    const uint32_t l = __ldcg(leaders + i);
+    if (l != i) {
+      const long long f = (long long)(((unsigned long long)B.tabw[2 * (i + 1) + 1] << 32) | B.tabw[2 * (i + 1)]);
+      if (f) fix_add(B.tabw + 2 * (l + 1), f);
+    }
+  }
+  __syncthreads();
+#pragma unroll 4
+  for (uint32_t i = tid; i < nI; i += nth) {
+    if (__ldcg(leaders + i) != i) continue;
+    const double g = fix_value(B.tabw[2 * (i + 1)], B.tabw[2 * (i + 1) + 1], o_inv);
+    if (g == 0.0) continue;
+    const uint32_t c = __ldcg(&a.irec[i].x);
+    a.w[c] = __dsub_rn(__ldcg(a.w + c), __dmul_rn(step, g));
+  }
+}
+
+// P1[i] = value_i * w[col_i] from the unpacked records (large n_cols: thread-strided and unrolled
+// so the dependent record -> weight loads of different pairs overlap).
+template <bool kWide>
+TOC_D void p1_records(Batch<kWide>& B, const MgdArgs& a) {
+#pragma unroll 4
+  for (uint32_t i = threadIdx.x; i < B.nI; i += blockDim.x) {
+    const uint2 rec = __ldcg(a.irec + i);
+    B.tab[i + 1] = B.uniq[rec.y] * __ldcg(a.w + rec.x);
+  }
 }
 
 // Gradient of one batch: P1 from w, A.w, the loss scalar, s^T.A into G (fixed point).  Returns
@@ -85,7 +165,8 @@ TOC_D double batch_gradient(Batch<kWide>& B, const MgdArgs& a, int64_t b, double
                             double* s_red, double& bound_out) {
   const uint32_t tid = threadIdx.x, nth = blockDim.x;
   const int64_t rb = a.row_base[b];
-  B.template compute_p1<kCG>(a.w);
+  if (a.irec) p1_records(B, a);
+  else B.template compute_p1<kCG>(a.w);
   __syncthreads();
   stamp(a, b, 2);
   B.matvec_rows([&](uint32_t r, double z) { srow[r] = loss_scalar(a.loss, a.labels[rb + r], z); });
@@ -138,6 +219,21 @@ __global__ void __launch_bounds__(1024, 1) glm_epoch_kernel(MgdArgs a) {
   const uint32_t tid = threadIdx.x, nth = blockDim.x, m = (uint32_t)a.n_cols, words = (m + 31) / 32;
   uint32_t* touched = nullptr;
   uint32_t* acc = nullptr;
+  uint32_t* minidx = nullptr;
+  uint32_t* leaders = nullptr;
+  if (!a.small_m) {
+    // scratch after the slabs: [ctas][m4] minidx, [ctas][p4] leaders, [ctas][p4] irec (uint2);
+    // m4 / p4 rounded to multiples of 4 so every region stays 16-byte aligned
+    const int64_t m4 = ((int64_t)m + 3) & ~3ll, p4 = ((int64_t)a.max_pairs + 3) & ~3ll;
+    uint8_t* base = a.scratch + (int64_t)gridDim.x * a.slab_bytes;
+    minidx = reinterpret_cast<uint32_t*>(base) + (int64_t)blockIdx.x * m4;
+    base += (int64_t)gridDim.x * 4 * m4;
+    leaders = reinterpret_cast<uint32_t*>(base) + (int64_t)blockIdx.x * p4;
+    base += (int64_t)gridDim.x * 4 * p4;
+    a.irec = reinterpret_cast<uint2*>(base) + (int64_t)blockIdx.x * p4;
+  } else {
+    a.irec = nullptr;
+  }
   if (a.small_m) {
     touched = reinterpret_cast<uint32_t*>(p);
     p += align16(4u * words);
@@ -156,16 +252,24 @@ __global__ void __launch_bounds__(1024, 1) glm_epoch_kernel(MgdArgs a) {
     if (a.small_m)
       for (uint32_t w = tid; w < words; w += nth) touched[w] = 0u;
     double vmax, ysum;
-    build_step(B, a, t, s_warp, s_red, vmax, ysum);
+    build_step(B, a, t, s_warp, s_red, vmax, ysum, minidx, leaders);
     stamp(a, t, 0);
-    // wait for the weights of step t (bounded: a hang would take the GPU down with it)
+    // Wait for the weights of step t.  Only the owner of the next step polls tightly; owners of
+    // later steps back off in proportion to their distance, so the counter's L2 slice is not
+    // flooded (a hot slice stalls every access hashed to it, including the critical path's).
+    // Bounded by a 4 s timeout: a hang would take the GPU down with it.
     if (tid == 0) {
       uint32_t go = 1;
-      long long spins = 0;
-      while (ld_acquire(a.counter) != (uint32_t)t) {
-        if (ld_acquire(a.abort_flag)) { go = 0; break; }
-        if (++spins > (1ll << 26)) { atomicExch(a.abort_flag, 1u); go = 0; break; }
-        __nanosleep(32);
+      const unsigned long long t0 = globaltimer_ns();
+      for (uint32_t it = 0;; ++it) {
+        const uint32_t c = ld_acquire(a.counter);
+        if (c == (uint32_t)t) break;
+        const uint32_t dist = (uint32_t)t - c;
+        if ((it & 255u) == 255u) {
+          if (ld_acquire(a.abort_flag)) { go = 0; break; }
+          if (globaltimer_ns() - t0 > 4000000000ull) { atomicExch(a.abort_flag, 1u); go = 0; break; }
+        }
+        __nanosleep(dist <= 1 ? 20u : (dist < 16 ? 200u * dist : 4000u));
       }
       s_go = go;
     }
@@ -175,7 +279,7 @@ __global__ void __launch_bounds__(1024, 1) glm_epoch_kernel(MgdArgs a) {
     double bound;
     const double g_scale = batch_gradient<kWide, true>(B, a, t, srow, ysum, s_red, bound);
     if (a.small_m) update_small(B, a, acc, touched, g_scale, vmax, bound);
-    else B.scatter_update(a.w, 1.0 / g_scale, a.lr / (double)B.n);
+    else update_leaders(B, a, leaders, g_scale, fix_scale(bound * vmax));
     stamp(a, t, 6);
     __threadfence();
     __syncthreads();
@@ -254,9 +358,11 @@ __global__ void risk_kernel(const double* z, const double* y, int64_t n, int32_t
 // ------------------------------------------------------------------------------------------
 namespace {
 
+int g_max_ctas = 0;  // diagnostic cap on the MGD grid (0: one CTA per SM)
+
 struct MgdLaunch {
   int threads, ctas, smem;
-  int32_t budget, small_m;
+  int32_t budget, small_m, max_pairs;
   int64_t slab, scratch;
 };
 
@@ -284,17 +390,46 @@ MgdLaunch mgd_plan(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t n_cols,
   const uint32_t small_bytes = toc::align16(8u * m);
   L.small_m = small_bytes <= 32u * 1024u;
   uint32_t fixed = toc::kFixedBytes + (L.small_m ? small_bytes + (epoch ? toc::align16(4u * ((m + 31) / 32)) : 0u) : 0u);
+  uint32_t max_ni = 0;
+  for (int64_t b = 0; b < n_blocks; ++b) max_ni = max_ni > h_meta[b].n_pairs ? max_ni : h_meta[b].n_pairs;
+  L.max_pairs = (int32_t)max_ni;
   uint32_t avail = (uint32_t)optin > fixed ? (uint32_t)optin - fixed : 0u;
   L.budget = (int32_t)(max_need <= avail ? max_need : avail);
   L.smem = (int)(fixed + (uint32_t)L.budget);
   L.threads = 1024;
   L.ctas = (int)(n_blocks < sm ? (n_blocks > 0 ? n_blocks : 1) : sm);
+  if (g_max_ctas > 0 && L.ctas > g_max_ctas) L.ctas = g_max_ctas;
   L.slab = max_need > (uint32_t)L.budget ? (int64_t)toc::align16(max_need) : 0;
   L.scratch = (int64_t)L.ctas * L.slab;
+  if (epoch && !L.small_m)  // minidx, leaders, irec (see glm_epoch_kernel)
+    L.scratch += (int64_t)L.ctas * 4 * ((((int64_t)m + 3) & ~3ll) + 3 * (((int64_t)max_ni + 3) & ~3ll));
   return L;
 }
 
 }  // namespace
+
+extern "C" int toc_mgd_set_max_ctas(int32_t n) {
+  g_max_ctas = n;
+  return TOC_OK;
+}
+
+extern "C" int toc_mgd_plan_info(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t n_cols, int32_t kind,
+                                 int64_t* info /* 8: smem, budget, small_m, sorted_cols, key_slots, ctas, slab, wide */) {
+  if (!h_meta || n_blocks < 0 || !info) return TOC_E_ARG;
+  bool wide = false;
+  for (int64_t b = 0; b < n_blocks; ++b)
+    if (1ull + h_meta[b].n_pairs + h_meta[b].n_derived > 65536ull) wide = true;
+  MgdLaunch L = mgd_plan(h_meta, n_blocks, n_cols, wide, kind == 0);
+  info[0] = L.smem;
+  info[1] = L.budget;
+  info[2] = L.small_m;
+  info[3] = 0;
+  info[4] = L.max_pairs;
+  info[5] = L.ctas;
+  info[6] = L.slab;
+  info[7] = wide;
+  return TOC_OK;
+}
 
 extern "C" int toc_mgd_workspace(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t n_cols, int32_t kind,
                                  int64_t* scratch_bytes) {
@@ -314,6 +449,11 @@ static int mgd_launch(const TocBlockMeta* h_meta, const toc::MgdArgs& a0, bool e
   toc::MgdArgs a = a0;
   a.batch_smem_budget = L.budget;
   a.small_m = L.small_m;
+  a.max_pairs = L.max_pairs;
+  if (epoch && !L.small_m)  // column tables start "empty"
+    if (cudaMemsetAsync(a.scratch + (int64_t)L.ctas * L.slab, 0xff, (size_t)L.ctas * 4 * ((a.n_cols + 3) & ~3), s) !=
+        cudaSuccess)
+      return TOC_E_CUDA;
   a.slab_bytes = L.slab;
   if (L.scratch > 0 && !a.scratch) return TOC_E_ARG;
   void* fn;
@@ -352,7 +492,7 @@ extern "C" int toc_glm_epoch_traced(const uint8_t* d_arena, const int64_t* d_blo
   if (n_blocks <= 0) return n_blocks == 0 ? TOC_OK : TOC_E_ARG;
   if (!h_meta || !d_w || !d_labels || !d_sync || loss < 0 || loss > 2) return TOC_E_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  if (cudaMemsetAsync(d_sync, 0, 8, s) != cudaSuccess) return TOC_E_CUDA;
+  if (cudaMemsetAsync(d_sync, 0, 256, s) != cudaSuccess) return TOC_E_CUDA;
   toc::MgdArgs a{};
   a.arena = d_arena;
   a.block_off = d_block_off;
@@ -365,7 +505,7 @@ extern "C" int toc_glm_epoch_traced(const uint8_t* d_arena, const int64_t* d_blo
   a.labels = d_labels;
   a.w = d_w;
   a.counter = d_sync;
-  a.abort_flag = d_sync + 1;
+  a.abort_flag = d_sync + 32;  // its own 128-byte line
   a.scratch = (uint8_t*)d_scratch;
   a.trace = d_trace;
   return mgd_launch(h_meta, a, true, s);

@@ -131,7 +131,7 @@ class GlmTrainer:
         self.lr = float(learning_rate)
         torch = self.torch
         self.w = torch.zeros(max(batches.n_cols, 1), dtype=torch.float64, device="cuda")
-        self.sync = torch.zeros(2, dtype=torch.int32, device="cuda")
+        self.sync = torch.zeros(64, dtype=torch.int32, device="cuda")  # counter @0, abort flag @32
         self.partial = torch.zeros(148, dtype=torch.float64, device="cuda")
         L = _bind()
         a = batches.arena
@@ -154,7 +154,7 @@ class GlmTrainer:
                 "toc_glm_epoch")
         end.record()
         end.synchronize()
-        if int(self.sync[1].item()):
+        if int(self.sync[32].item()):
             raise RuntimeError("toc_glm_epoch aborted (step hand-off timed out)")
         return start.elapsed_time(end) / 1e3
 

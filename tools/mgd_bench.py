@@ -13,6 +13,7 @@ p = argparse.ArgumentParser()
 p.add_argument("--config", type=int, default=3)
 p.add_argument("--rows", type=int, default=0)
 p.add_argument("--epochs", type=int, default=0)
+p.add_argument("--max-ctas", type=int, default=0)
 a = p.parse_args()
 
 from paper_1702_06943_b200 import synth  # noqa: E402
@@ -29,6 +30,9 @@ ds = LabeledDataset(features=SparseRowMatrix.from_csr(m, rp, c, v, check=False),
 t = time.time(); sh = shuffle_once(ds, 0); ts = time.time() - t
 t = time.time(); batches = DeviceBatches(sh, 250); import torch; torch.cuda.synchronize(); te = time.time() - t
 tr = GlmTrainer(batches, loss, lr)
+if a.max_ctas:
+    from paper_1702_06943_b200 import _native as _N
+    _N.lib().toc_mgd_set_max_ctas(a.max_ctas)
 secs, risks = [], []
 for _ in range(epochs):
     secs.append(tr.epoch())
@@ -53,8 +57,12 @@ N.check(L.toc_glm_epoch_traced(ar.data.data_ptr(), ar.block_off_d.data_ptr(), ar
                                tr.loss, tr.lr, batches.labels.data_ptr(), tr.w.data_ptr(), tr.sync.data_ptr(),
                                tr.scratch.data_ptr(), trace.data_ptr(), N.stream_handle()), "traced")
 torch.cuda.synchronize()
+info = np.zeros(8, np.int64)
+L.toc_mgd_plan_info.argtypes = [P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, P]
+L.toc_mgd_plan_info(ar.meta.ctypes.data_as(P), ar.n_blocks, batches.n_cols, 0, info.ctypes.data_as(P))
+print("plan (smem, budget, small_m, -, max_pairs, ctas, slab, wide):", info.tolist())
 T = trace.view(-1, 8).cpu().numpy().astype(np.int64)
 d = np.diff(T, axis=1)
-names = ["wait", "p1", "matvec", "loss+bounds", "vecmat", "scatter", "update+fence"]
+names = ["wait", "p1", "matvec+loss", "bound", "vecmat", "update", "fence"]
 print("phase cycles (median per step):", {n: int(np.median(d[:, i])) for i, n in enumerate(names)})
 print("step critical path (median cycles, acquire->release):", int(np.median(T[:, 7] - T[:, 1])))
