@@ -43,6 +43,8 @@ def parse():
     p.add_argument("--batches-per-gpu", type=int, default=BATCHES_PER_GPU)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=20)
+    p.add_argument("--no-mgd", action="store_true", help="skip the MGD epoch measurement (config 3)")
+    p.add_argument("--mgd-cfg4", action="store_true", help="also measure config 4 (hinge, 47,236 cols)")
     return p.parse_args()
 
 
@@ -257,6 +259,12 @@ def main():
                                              arena.row_base, 12.0, 5, 1, Omod)
         cpu = {"value": rps, "unit": "rows/s", "cores": cores, "kind": "port", "sample": desc}
 
+    mgd = {}
+    if not args.no_mgd:
+        mgd["config3_logistic"] = run_mgd(3, rank, world, cpu_sample=(rank == 0 and world == 1 and not args.no_cpu_baseline))
+        if args.mgd_cfg4:
+            mgd["config4_hinge"] = run_mgd(4, rank, world, cpu_sample=False)
+
     if rank == 0:
         line = {
             "metric": METRIC,
@@ -290,10 +298,73 @@ def main():
             "e2e": e2e,
             "gpu_launches": args.steps,
             "clocks": sampler.summary(),
+            "mgd": mgd,
         }
         print(json.dumps(line))
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def run_mgd(cfg: int, rank: int, world: int, cpu_sample: bool):
+    """MGD epoch seconds at the config's full size (BASELINE.json configs[2] / [3]).  N=1: one
+    cooperative relay launch per epoch; N>1: synchronous data parallel with NCCL (per-replica batch
+    250, global 250*N).  Device time (CUDA events), max over ranks."""
+    import torch
+
+    from paper_1702_06943_b200 import synth
+    from paper_1702_06943_b200.matrix import LabeledDataset, SparseRowMatrix
+    from paper_1702_06943_b200.training import DeviceBatches, GlmTrainer, TrainConfig, shuffle_once
+
+    if cfg == 3:
+        rp, c, v, y = synth.cfg3_dataset()
+        m, loss, lr, epochs = 68, "logistic", 0.1, 10
+    else:
+        rp, c, v, y = synth.cfg4_dataset()
+        m, loss, lr, epochs = 47_236, "hinge", 0.01, 5
+    ds = LabeledDataset(features=SparseRowMatrix.from_csr(m, rp, c, v, check=False), labels=y)
+    out = {"rows": len(y), "n_cols": m, "loss": loss, "batch_size": 250, "lr": lr, "epochs": epochs}
+    if world == 1:
+        batches = DeviceBatches(shuffle_once(ds, 0), 250)
+        tr = GlmTrainer(batches, loss, lr)
+        secs, risks = [], []
+        for _ in range(epochs):
+            secs.append(tr.epoch())
+            risks.append(tr.risk())
+        out.update({"steps_per_epoch": int(batches.arena.n_blocks), "epoch_seconds": secs, "risk_per_epoch": risks,
+                     "mode": "one cooperative relay launch per epoch"})
+        if cpu_sample:
+            out["cpu_port"] = cpu_mgd_sample(rp, c, v, y, m, loss, lr, batches.arena.n_blocks)
+    else:
+        from paper_1702_06943_b200.distributed import train_data_parallel
+
+        _, trace = train_data_parallel(ds, TrainConfig(loss, 250, lr, epochs), world, rank)
+        out.update({"steps_per_epoch": -(-len(y) // (250 * world)), "epoch_seconds": trace.seconds,
+                    "risk_per_epoch": trace.risks, "mode": f"data parallel x{world}, NCCL all-reduce per step"})
+    return out
+
+
+def cpu_mgd_sample(rp, c, v, y, m, loss, lr, steps_full: int, sample_batches: int = 400):
+    """The oracle port's MGD epoch time on a bounded sample (first sample_batches batches of the
+    shuffled order, trees built outside the timing like the reference's own), scaled to a full
+    epoch.  Single thread: MGD steps are sequential."""
+    from oracle import oracle as O
+
+    O.build()
+    order = O.shuffle_order(len(y), 0)[: 250 * sample_batches]
+    lens = np.diff(rp)[order]
+    srp = np.concatenate([[0], np.cumsum(lens)])
+    g = np.concatenate([np.arange(rp[i], rp[i + 1]) for i in order])
+    trees, bases = O.make_batch_trees(srp, c[g], v[g], m, np.arange(len(order)), 250)
+    ys = np.ascontiguousarray(y[order], np.float64)
+    import ctypes as C
+
+    handles = (C.c_void_p * len(trees))(*[t._h for t in trees])
+    w = np.zeros(m)
+    t0 = time.perf_counter()
+    O.lib().or_glm_epoch(len(trees), handles, O._ptr(bases), O._ptr(ys), O._ptr(w), O.LOSS_CODE[loss], float(lr))
+    dt = time.perf_counter() - t0
+    return {"epoch_seconds_est": dt * steps_full / len(trees), "sample": f"{len(trees)} of {steps_full} steps, 1 thread",
+            "kind": "port"}
 
 
 def run_e2e(torch, arena, v_h, u_h, steps: int):
