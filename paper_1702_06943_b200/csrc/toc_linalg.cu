@@ -1,23 +1,9 @@
 // toc_linalg.cu -- A.v and v^T.A directly on TOC1 blocks resident in HBM (sm_100a).
 //
 // Reference: kernels.py:115-142 (matvec, Algorithm 5) and kernels.py:145-174 (vecmat,
-// Algorithm 6); the tree they walk is codec.py:215-259 (build_prefix_tree).
-//
-// Design: a persistent grid, one CTA per mini-batch at a time.  The CTA
-// reads only the batch's TOC1 bytes and rebuilds, in shared memory, the part of the decode tree
-// C' the products need:
-//   par[d] = D-code at the position that derived node d           (codec.py:247)
-//   key[d] = first-layer pair that node d appends = F(next code)   (codec.py:248-249)
-// (d = derived node id - 1 - |I|).  Node values are never materialised: a code's partial sum
-// is produced by walking par[] to the first layer, summing P1[key] (P1[i] = value_i * v[col_i])
-// on the way.  Work per batch is O(|I| + C + nnz) shared-memory accesses, no HBM traffic
-// beyond the block itself, v / u and the outputs.
-//
-//   matvec: P1 in tab[1..|I|]; each warp owns rows; lanes expand 32 codes at a time, a warp
-//           reduction folds them into the row sum.
-//   vecmat: G in tab[1..|I|]: each code adds u[row] to every pair key on its chain (the
-//           transpose of the matvec walk, an fp64 shared-memory atomic per pair), then
-//           out[col_i] += value_i * G[i].
+// Algorithm 6).  A persistent grid walks the arena, one CTA per mini-batch at a time, the next
+// block prefetched into L2; the per-batch machinery (node tables rebuilt from the block in
+// shared memory, chain walks, fixed-point v^T.A) is in toc_batch.cuh.  DESIGN.md section 4.1.
 #include "toc_batch.cuh"
 
 namespace toc {
