@@ -168,23 +168,39 @@ class BatchSweep:
     """Public batched API over host-resident TOC1 blocks.
 
     ``run(v, u)`` uploads the blocks and operands from pinned host memory, validates/indexes the
-    blocks on the device, runs A.v and v^T.A for every batch in one fused launch, and returns
-    host arrays (R: concatenated row results, O: one n_cols row per batch).  This replaces the
-    reference's per-batch loop over ``matvec`` / ``vecmat`` (cli.py:340-356)."""
+    blocks on the device, runs A.v and v^T.A for every batch (fused launches), and returns host
+    arrays (R: concatenated row results, O: one n_cols row per batch).  The batches are split
+    into chunks: the host->device copy of chunk k+1 (copy stream) overlaps validation and compute
+    of chunk k (compute stream).  This replaces the reference's per-batch loop over ``matvec`` /
+    ``vecmat`` (cli.py:340-356)."""
 
-    def __init__(self, blocks_h: np.ndarray, block_off, block_len):
+    def __init__(self, blocks_h: np.ndarray, block_off, block_len, chunks: int = 8):
         torch = N.require_cuda()
         self.torch = torch
+        block_off = np.asarray(block_off, np.int64)
+        block_len = np.asarray(block_len, np.int64)
         nbytes = int(len(blocks_h))
         self.host = torch.zeros(nbytes + 16, dtype=torch.uint8, pin_memory=True)  # +16 tail padding
         self.host.numpy()[:nbytes] = blocks_h[:nbytes]
         self.nbytes = nbytes
         self.dev = torch.empty_like(self.host, device="cuda")
         self.dev.copy_(self.host)
-        self.arena = BlockArena(self.dev, block_off, block_len)
-        self.n_rows = self.arena.n_rows_total
-        self.n_cols = self.arena.n_cols
-        nb = self.arena.n_blocks
+        nb = len(block_off)
+        bounds = np.linspace(0, nb, min(max(chunks, 1), max(nb, 1)) + 1).astype(np.int64)
+        self.chunks = []
+        row0 = 0
+        for b0, b1 in zip(bounds[:-1], bounds[1:]):
+            if b1 <= b0:
+                continue
+            arena = BlockArena(self.dev, block_off[b0:b1], block_len[b0:b1])
+            lo = int(block_off[b0])
+            hi = int(block_off[b1 - 1] + block_len[b1 - 1]) if b1 < nb else nbytes
+            hi = min(nbytes + 16, (hi + 15) & ~15) if b1 < nb else nbytes + 16
+            self.chunks.append((arena, int(b0), int(b1), lo, hi, row0))
+            row0 += arena.n_rows_total
+        self.n_rows = row0
+        self.n_cols = self.chunks[0][0].n_cols if self.chunks else 0
+        self.n_blocks = nb
         self.v_h = torch.empty(max(self.n_cols, 1), dtype=torch.float64, pin_memory=True)
         self.u_h = torch.empty(max(self.n_rows, 1), dtype=torch.float64, pin_memory=True)
         self.v_d = torch.empty_like(self.v_h, device="cuda")
@@ -193,33 +209,48 @@ class BatchSweep:
         self.O_d = torch.empty((max(nb, 1), max(self.n_cols, 1)), dtype=torch.float64, device="cuda")
         self.R_h = torch.empty_like(self.R_d, device="cpu").pin_memory()
         self.O_h = torch.empty_like(self.O_d, device="cpu").pin_memory()
-        self.meta_h = torch.empty(self.arena.meta_d.numel(), dtype=torch.uint8, pin_memory=True)
+        self.meta_h = [torch.empty(c[0].meta_d.numel(), dtype=torch.uint8, pin_memory=True) for c in self.chunks]
+        self.copy_stream = torch.cuda.Stream()
         self.h2d_bytes = nbytes + 8 * self.n_cols + 8 * self.n_rows
-        self.d2h_bytes = 8 * self.n_rows + 8 * nb * self.n_cols + self.arena.meta_d.numel()
+        self.d2h_bytes = 8 * self.n_rows + 8 * nb * self.n_cols + sum(c[0].meta_d.numel() for c in self.chunks)
 
     @classmethod
-    def from_host_blocks(cls, blocks_h, block_off, block_len) -> "BatchSweep":
-        return cls(np.asarray(blocks_h, np.uint8), block_off, block_len)
+    def from_host_blocks(cls, blocks_h, block_off, block_len, chunks: int = 8) -> "BatchSweep":
+        return cls(np.asarray(blocks_h, np.uint8), block_off, block_len, chunks)
 
     def run(self, v, u):
         torch = self.torch
-        a = self.arena
         self.v_h.numpy()[: self.n_cols] = as_vector(v, self.n_cols, "vector")
         self.u_h.numpy()[: self.n_rows] = as_vector(u, self.n_rows, "vector")
-        self.dev.copy_(self.host, non_blocking=True)
-        self.v_d.copy_(self.v_h, non_blocking=True)
-        self.u_d.copy_(self.u_h, non_blocking=True)
-        rc = N.lib().toc_index_blocks(a.data.data_ptr(), a.block_off_d.data_ptr(), a.block_len_d.data_ptr(),
-                                      a.n_blocks, a.meta_d.data_ptr(), N.stream_handle())
-        N.check(rc, "toc_index_blocks")
-        a.linalg(N.TOC_MATVEC | N.TOC_VECMAT, v=self.v_d, u=self.u_d, R=self.R_d, O=self.O_d)
-        self.R_h.copy_(self.R_d, non_blocking=True)
-        self.O_h.copy_(self.O_d, non_blocking=True)
-        self.meta_h.copy_(a.meta_d, non_blocking=True)
-        torch.cuda.current_stream().synchronize()
-        meta = np.frombuffer(self.meta_h.numpy().tobytes(), dtype=N.META_DTYPE)[: a.n_blocks]
-        if np.any(meta["status"] != N.TOC_OK) or np.any(meta["corrupt"] != 0):
-            a.meta = meta.copy()
-            a.raise_format_errors()
-            a.raise_corrupt()
-        return self.R_h.numpy()[: self.n_rows], self.O_h.numpy()[: a.n_blocks, : self.n_cols]
+        comp = torch.cuda.current_stream()
+        cs = self.copy_stream
+        cs.wait_stream(comp)  # previous run's readers of the device buffers are done
+        ready = []
+        with torch.cuda.stream(cs):
+            self.v_d.copy_(self.v_h, non_blocking=True)
+            for arena, b0, b1, lo, hi, r0 in self.chunks:
+                self.dev[lo:hi].copy_(self.host[lo:hi], non_blocking=True)
+                nr = arena.n_rows_total
+                self.u_d[r0 : r0 + nr].copy_(self.u_h[r0 : r0 + nr], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                ready.append(ev)
+        for k, (arena, b0, b1, lo, hi, r0) in enumerate(self.chunks):
+            comp.wait_event(ready[k])
+            N.check(N.lib().toc_index_blocks(arena.data.data_ptr(), arena.block_off_d.data_ptr(),
+                                             arena.block_len_d.data_ptr(), arena.n_blocks, arena.meta_d.data_ptr(),
+                                             N.stream_handle()), "toc_index_blocks")
+            nr = arena.n_rows_total
+            arena.linalg(N.TOC_MATVEC | N.TOC_VECMAT, v=self.v_d[: self.n_cols], u=self.u_d[r0 : r0 + nr],
+                         R=self.R_d[r0 : r0 + nr], O=self.O_d[b0:b1])
+            self.R_h[r0 : r0 + nr].copy_(self.R_d[r0 : r0 + nr], non_blocking=True)
+            self.O_h[b0:b1].copy_(self.O_d[b0:b1], non_blocking=True)
+            self.meta_h[k].copy_(arena.meta_d, non_blocking=True)
+        comp.synchronize()
+        for k, (arena, *_rest) in enumerate(self.chunks):
+            meta = np.frombuffer(self.meta_h[k].numpy().tobytes(), dtype=N.META_DTYPE)[: arena.n_blocks]
+            if np.any(meta["status"] != N.TOC_OK) or np.any(meta["corrupt"] != 0):
+                arena.meta = meta.copy()
+                arena.raise_format_errors()
+                arena.raise_corrupt()
+        return self.R_h.numpy()[: self.n_rows], self.O_h.numpy()[: self.n_blocks, : self.n_cols]

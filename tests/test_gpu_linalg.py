@@ -117,3 +117,26 @@ def test_wide_tree_global_tables(oracle):
     enc = oracle.encode_rows(n_cols, rows)
     assert enc.tree_length() > 65536
     _check_sweep(oracle, [enc], rng.standard_normal(n_cols), seed=9)
+
+
+def test_batch_sweep_public_api(oracle):
+    """BatchSweep (host blocks in, host results out, chunked + overlapped) equals per-batch oracle."""
+    from paper_1702_06943_b200 import synth
+    from paper_1702_06943_b200.codec import compress_csr
+    from paper_1702_06943_b200.kernels import BatchSweep
+
+    nb = 13
+    rp, c, v, counts = synth.cfg2_batches_csr(5, range(nb))
+    br = np.concatenate([[0], np.cumsum(counts)])
+    arena = compress_csr(784, rp, c, v, br)
+    end = int(arena.block_off[-1] + arena.block_len[-1])
+    host = arena.data[:end].cpu().numpy()
+    sweep = BatchSweep.from_host_blocks(host, arena.block_off, arena.block_len, chunks=4)
+    x, u = synth.cfg2_operands(5, nb)
+    for _ in range(2):
+        R, O = sweep.run(x, u)
+    for b in range(nb):
+        t = oracle.Tree.from_block(host[arena.block_off[b] : arena.block_off[b] + arena.block_len[b]].tobytes())
+        assert within_rel(R[250 * b : 250 * (b + 1)], t.matvec(x), REL)
+        assert within_rel(O[b], t.vecmat(u[250 * b : 250 * (b + 1)]), REL)
+    assert sweep.h2d_bytes == end + 8 * 784 + 8 * 250 * nb
