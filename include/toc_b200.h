@@ -120,6 +120,21 @@ int toc_linalg(const uint8_t* d_arena, const int64_t* d_block_off, const TocBloc
                const double* d_v, double* d_R, const double* d_u, double* d_O, void* d_scratch,
                void* stream);
 
+/* ---- compressed matrix-matrix products (reference kernels.py:177-234) ----------------------
+ * side 0 (matmat_right, kernels.py:177-203): d_out[row_base[b] + r, :] = (A_b . M)[r, :],
+ *         d_M = M [n_cols x p] row-major, d_out [n_rows_total x p].
+ * side 1 (matmat_left, kernels.py:206-234): d_out[b] = M_b . A_b  [p x n_cols] per batch,
+ *         d_M = M^T [n_rows_total x p] row-major (rows of M^T are batch rows), d_out
+ *         [n_blocks x p x n_cols].
+ * h_meta: host copy of the metadata.  d_scratch: toc_matmat_scratch bytes (0 unless some batch's
+ * tables exceed shared memory). */
+int toc_matmat(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+               const TocBlockMeta* h_meta, const int64_t* d_row_base, int64_t n_blocks, int32_t n_cols,
+               int32_t side, int32_t p, const double* d_M, double* d_out, void* d_scratch,
+               int64_t scratch_bytes, void* stream);
+int toc_matmat_scratch(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t n_cols, int32_t side,
+                       int32_t p, int64_t* bytes);
+
 /* ---- compression (replaces codec.encode, codec.py:112-191, and physical.serialize_block,
  *      physical.py:88-130; physical.deserialize_block's unpack, physical.py:138-186) --------
  * Mini-batch b is rows [batch_row[b], batch_row[b+1]) of a CSR matrix (row_ptr int64, cols

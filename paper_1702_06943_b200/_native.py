@@ -64,6 +64,8 @@ def lib():
     L.toc_index_blocks.argtypes = [P, P, P, I64, P, P]
     L.toc_plan.argtypes = [P, I64, I32, ctypes.POINTER(TocPlan)]
     L.toc_linalg.argtypes = [P, P, P, P, I64, ctypes.POINTER(TocPlan), I32, P, P, P, P, P, P]
+    L.toc_matmat.argtypes = [P, P, P, P, P, I64, I32, I32, I32, P, P, P, I64, P]
+    L.toc_matmat_scratch.argtypes = [P, I64, I32, I32, I32, ctypes.POINTER(ctypes.c_int64)]
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype or ctypes.c_int
     if L.toc_sizeof_meta() != META_DTYPE.itemsize or L.toc_sizeof_plan() != ctypes.sizeof(TocPlan):

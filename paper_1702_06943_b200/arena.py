@@ -151,6 +151,28 @@ class BlockArena:
         N.check(rc, "toc_linalg")
         return R, O
 
+    def matmat(self, side: int, M, p: int):
+        """side 0: A.M for every batch (M: device [n_cols x p]) -> [n_rows_total x p];
+        side 1: M_b.A_b per batch (M: device M^T [n_rows_total x p]) -> [n_blocks, p, n_cols]."""
+        torch = self.torch
+        self.raise_corrupt()
+        L = N.lib()
+        nbytes = ctypes.c_int64()
+        N.check(L.toc_matmat_scratch(self.meta.ctypes.data_as(ctypes.c_void_p), self.n_blocks, self.n_cols, side, p,
+                                     ctypes.byref(nbytes)), "toc_matmat_scratch")
+        dev = self.data.device
+        if side == 0:
+            out = torch.empty((max(self.n_rows_total, 1), p), dtype=torch.float64, device=dev)[: self.n_rows_total]
+        else:
+            out = torch.empty((max(self.n_blocks, 1), p, max(self.n_cols, 1)), dtype=torch.float64,
+                              device=dev)[: self.n_blocks, :, : self.n_cols]
+        scratch = torch.empty(max(nbytes.value, 16), dtype=torch.uint8, device=dev)
+        N.check(L.toc_matmat(self.data.data_ptr(), self.block_off_d.data_ptr(), self.meta_d.data_ptr(),
+                             self.meta.ctypes.data_as(ctypes.c_void_p), self.row_base_d.data_ptr(), self.n_blocks,
+                             self.n_cols, side, p, _ptr(M), _ptr(out), scratch.data_ptr(), scratch.numel(),
+                             N.stream_handle()), "toc_matmat")
+        return out
+
     def matvec(self, v):
         return self.linalg(N.TOC_MATVEC, v=v)[0]
 

@@ -140,6 +140,34 @@ def vecmat(v, a: CompressedMatrix, counter: OpCounter | None = None) -> np.ndarr
     return np.asarray(out, dtype=np.float64)
 
 
+def matmat_right(a: CompressedMatrix, m: DenseMatrix, counter: OpCounter | None = None) -> DenseMatrix:
+    """A @ M without decompressing A (kernels.py:177-203, Algorithm 8)."""
+    if a.n_cols != m.n_rows:
+        raise ValueError(f"inner dimensions differ: left has {a.n_cols} columns, right has {m.n_rows} rows")
+    p = m.n_cols
+    if a.n_rows == 0 or p == 0:
+        out = np.zeros((a.n_rows, p))
+    else:
+        arena = a.arena
+        out = arena.matmat(0, _dev(m.values), p).cpu().numpy()
+    a._charge(counter, p)
+    return DenseMatrix(out)
+
+
+def matmat_left(m: DenseMatrix, a: CompressedMatrix, counter: OpCounter | None = None) -> DenseMatrix:
+    """M @ A without decompressing A (kernels.py:206-234, Algorithm 9)."""
+    if m.n_cols != a.n_rows:
+        raise ValueError(f"inner dimensions differ: left has {m.n_cols} columns, right has {a.n_rows} rows")
+    p = m.n_rows
+    if a.n_rows == 0 or p == 0 or a.n_cols == 0:
+        out = np.zeros((p, a.n_cols))
+    else:
+        arena = a.arena
+        out = arena.matmat(1, _dev(np.ascontiguousarray(m.values.T)), p)[0].cpu().numpy()
+    a._charge(counter, p)
+    return DenseMatrix(out)
+
+
 def kernel_cost(a: CompressedMatrix, kind: str, width: int = 1) -> int:
     """Predicted multiply-add count (kernels.py:250-266)."""
     if kind not in KERNEL_KINDS:
