@@ -382,3 +382,102 @@ def train_glm(row_ptr, cols, vals, labels, n_cols, loss_kind, batch_size, lr, ep
             raise OracleError(ERROR_KIND[rc], 0, 0)
         risks.append(empirical_risk_glm(w, row_ptr, cols, vals, labels, loss_kind))
     return w, risks
+
+
+# ------------------------------------------------------------------------------------------
+# The reference's one-hidden-layer network (training.py:81-98, 206-228, 284-293, 319-333).
+
+def _sigmoid(z):  # training.py:215-221
+    out = np.empty_like(z)
+    pos = z >= 0
+    out[pos] = 1.0 / (1.0 + np.exp(-z[pos]))
+    ez = np.exp(z[~pos])
+    out[~pos] = ez / (1.0 + ez)
+    return out
+
+
+def csr_matmat_right(row_ptr, cols, vals, M):
+    """matrix.csr_matmat_right (matrix.py:260-272): row-wise acc += val * M[col]."""
+    n = len(row_ptr) - 1
+    out = np.zeros((n, M.shape[1]))
+    for i in range(n):
+        acc = out[i]
+        for e in range(row_ptr[i], row_ptr[i + 1]):
+            acc += vals[e] * M[cols[e]]
+    return out
+
+
+def init_nn(n_cols, hidden, seed):  # training.py:327-333
+    import math
+
+    rng = np.random.default_rng(seed)
+    s1 = 1.0 / math.sqrt(max(n_cols, 1))
+    s2 = 1.0 / math.sqrt(hidden)
+    return rng.uniform(-s1, s1, size=(n_cols, hidden)), rng.uniform(-s2, s2, size=(hidden, 1))
+
+
+def train_nn(row_ptr, cols, vals, labels, n_cols, hidden, batch_size, lr, epochs, seed=0):
+    """training.train with loss_kind='nn_mse', compressed execution.  Returns (w1, w2, risks)."""
+    order = shuffle_order(len(labels), seed)
+    trees, bases = make_batch_trees(row_ptr, cols, vals, n_cols, order, batch_size)
+    y_sh = labels[order]
+    w1, w2 = init_nn(n_cols, hidden, seed)
+    risks = []
+    for _ in range(epochs):
+        for t, lo in zip(trees, bases):
+            y = y_sh[lo : lo + t.n_rows]
+            h1 = _sigmoid(t.matmat_right(w1))
+            yhat = h1 @ w2
+            err = yhat - y[:, None]
+            g_w2 = h1.T @ err
+            delta = (err @ w2.T) * h1 * (1.0 - h1)
+            g_w1 = t.matmat_left(np.ascontiguousarray(delta.T)).T.copy()
+            n = t.n_rows
+            w1 = w1 - (lr / n) * g_w1
+            w2 = w2 - (lr / n) * g_w2
+        h1 = _sigmoid(csr_matmat_right(row_ptr, cols, vals, w1))
+        yhat = h1 @ w2
+        risks.append(float(np.mean(0.5 * (labels - yhat[:, 0]) ** 2)))
+    return w1, w2, risks
+
+
+def train_mlp(row_ptr, cols, vals, labels, n_cols, hidden, classes, batch_size, lr, epochs, seed=0):
+    """CPU restatement of the config-5 MLP step (ReLU, softmax cross-entropy, biases, Xavier init)
+    with the first layer through the oracle's matmat_right / matmat_left.  Not a reference
+    function (the reference has no such model): parity for it is unpinned by reference outputs."""
+    import math
+
+    rng = np.random.default_rng(seed)
+    l1 = math.sqrt(6.0 / (n_cols + hidden))
+    l2 = math.sqrt(6.0 / (hidden + classes))
+    w1 = rng.uniform(-l1, l1, size=(n_cols, hidden))
+    b1 = np.zeros(hidden)
+    w2 = rng.uniform(-l2, l2, size=(hidden, classes))
+    b2 = np.zeros(classes)
+    order = shuffle_order(len(labels), seed)
+    trees, bases = make_batch_trees(row_ptr, cols, vals, n_cols, order, batch_size)
+    y_sh = labels[order].astype(np.int64)
+    risks = []
+
+    def softmax(x):
+        e = np.exp(x - x.max(axis=1, keepdims=True))
+        return e / e.sum(axis=1, keepdims=True)
+
+    for _ in range(epochs):
+        for t, lo in zip(trees, bases):
+            y = y_sh[lo : lo + t.n_rows]
+            a1 = np.maximum(t.matmat_right(w1) + b1, 0.0)
+            p = softmax(a1 @ w2 + b2)
+            p[np.arange(len(y)), y] -= 1.0
+            g_w2, g_b2 = a1.T @ p, p.sum(0)
+            delta = (p @ w2.T) * (a1 > 0)
+            g_b1 = delta.sum(0)
+            g_w1 = t.matmat_left(np.ascontiguousarray(delta.T)).T
+            s = lr / len(y)
+            w1, b1, w2, b2 = w1 - s * g_w1, b1 - s * g_b1, w2 - s * g_w2, b2 - s * g_b2
+        z = csr_matmat_right(row_ptr, cols, vals, w1)
+        logits = np.maximum(z + b1, 0.0) @ w2 + b2
+        lp = logits - logits.max(axis=1, keepdims=True)
+        lp = lp - np.log(np.exp(lp).sum(axis=1, keepdims=True))
+        risks.append(float(-np.mean(lp[np.arange(len(labels)), labels.astype(np.int64)])))
+    return (w1, b1, w2, b2), risks

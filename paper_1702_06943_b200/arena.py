@@ -151,26 +151,48 @@ class BlockArena:
         N.check(rc, "toc_linalg")
         return R, O
 
-    def matmat(self, side: int, M, p: int):
-        """side 0: A.M for every batch (M: device [n_cols x p]) -> [n_rows_total x p];
-        side 1: M_b.A_b per batch (M: device M^T [n_rows_total x p]) -> [n_blocks, p, n_cols]."""
+    def matmat(self, side: int, M, p: int, batch: int | None = None, out=None):
+        """side 0: A.M (M: device [n_cols x p]) -> [rows x p];  side 1: M_b.A_b (M: device M^T
+        [rows x p]) -> [blocks, p, n_cols].  batch=None: every batch of the arena; batch=b: only
+        batch b (rows indexed from 0)."""
         torch = self.torch
         self.raise_corrupt()
         L = N.lib()
-        nbytes = ctypes.c_int64()
-        N.check(L.toc_matmat_scratch(self.meta.ctypes.data_as(ctypes.c_void_p), self.n_blocks, self.n_cols, side, p,
-                                     ctypes.byref(nbytes)), "toc_matmat_scratch")
-        dev = self.data.device
-        if side == 0:
-            out = torch.empty((max(self.n_rows_total, 1), p), dtype=torch.float64, device=dev)[: self.n_rows_total]
+        if batch is None:
+            b0, nb, rows = 0, self.n_blocks, self.n_rows_total
+            row_base = self.row_base_d.data_ptr()
         else:
-            out = torch.empty((max(self.n_blocks, 1), p, max(self.n_cols, 1)), dtype=torch.float64,
-                              device=dev)[: self.n_blocks, :, : self.n_cols]
-        scratch = torch.empty(max(nbytes.value, 16), dtype=torch.uint8, device=dev)
-        N.check(L.toc_matmat(self.data.data_ptr(), self.block_off_d.data_ptr(), self.meta_d.data_ptr(),
-                             self.meta.ctypes.data_as(ctypes.c_void_p), self.row_base_d.data_ptr(), self.n_blocks,
-                             self.n_cols, side, p, _ptr(M), _ptr(out), scratch.data_ptr(), scratch.numel(),
-                             N.stream_handle()), "toc_matmat")
+            b0, nb, rows = int(batch), 1, int(self.meta["n_rows"][batch])
+            if getattr(self, "_zero_rb", None) is None:
+                self._zero_rb = torch.zeros(1, dtype=torch.int64, device=self.data.device)
+            row_base = self._zero_rb.data_ptr()
+        hmeta = self.meta[b0 : b0 + nb]
+        key = (side, p, batch is None)
+        nbytes = self._mm_scratch.get(key) if hasattr(self, "_mm_scratch") else None
+        if nbytes is None:
+            c = ctypes.c_int64()
+            meta_all = np.ascontiguousarray(self.meta)
+            N.check(L.toc_matmat_scratch(meta_all.ctypes.data_as(ctypes.c_void_p), self.n_blocks if batch is None else 1,
+                                         self.n_cols, side, p, ctypes.byref(c)), "toc_matmat_scratch")
+            if not hasattr(self, "_mm_scratch"):
+                self._mm_scratch = {}
+            nbytes = self._mm_scratch[key] = c.value
+        dev = self.data.device
+        if out is None:
+            if side == 0:
+                out = torch.empty((max(rows, 1), p), dtype=torch.float64, device=dev)[:rows]
+            else:
+                out = torch.empty((max(nb, 1), p, max(self.n_cols, 1)), dtype=torch.float64,
+                                  device=dev)[:nb, :, : self.n_cols]
+        if nbytes > 0 and (self._scratch is None or self._scratch.numel() < nbytes):
+            self._scratch = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+        scratch = self._scratch
+        hm = np.ascontiguousarray(hmeta)
+        N.check(L.toc_matmat(self.data.data_ptr(), self.block_off_d.data_ptr() + 8 * b0,
+                             self.meta_d.data_ptr() + N.META_DTYPE.itemsize * b0, hm.ctypes.data_as(ctypes.c_void_p),
+                             row_base, nb, self.n_cols, side, p, _ptr(M), _ptr(out),
+                             scratch.data_ptr() if scratch is not None else None,
+                             scratch.numel() if scratch is not None else 0, N.stream_handle()), "toc_matmat")
         return out
 
     def matvec(self, v):

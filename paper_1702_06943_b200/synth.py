@@ -168,3 +168,38 @@ def cfg4_dataset(n_rows: int = 800_000, n_cols: int = 47_236, seed: int = 4, nnz
         cols_out.append(c)
         vals_out.append(v)
     return np.concatenate(ptrs), np.concatenate(cols_out), np.concatenate(vals_out), np.concatenate(labels)
+
+
+# ---- config 5: MLP inputs ---------------------------------------------------------------------
+def cfg5_teacher(n_in: int = 784, hidden: int = 200, classes: int = 10, seed: int = 5):
+    rng = np.random.default_rng(seed)
+    return (rng.standard_normal((n_in, hidden)) / np.sqrt(n_in), rng.standard_normal(hidden) * 0.1,
+            rng.standard_normal((hidden, classes)) / np.sqrt(hidden))
+
+
+def cfg5_batches(n_rows: int, seed: int = 5, batch: int = 250, n_cols: int = 784):
+    """BASELINE.json configs[4] (decision): rows "generated as in config 1" -- each
+    250-row batch from its own 32 templates over a 16-value Zipf(1.2) vocabulary U[-1,1] with 10%
+    mutation, widened to 784 columns -- and labels argmax of a random 784-200-10 ReLU teacher.
+    Yields (row_ptr, cols, vals, labels) per batch."""
+    W1, b1, W2 = cfg5_teacher(n_cols, seed=seed)
+    offset = None  # per-class centring (from the first batch) so the classes come out near uniform
+    for lo in range(0, n_rows, batch):
+        k = min(batch, n_rows - lo)
+        A = cfg1_dense(seed=int(np.random.SeedSequence([seed, lo]).generate_state(1)[0]), n_rows=k, n_cols=n_cols)
+        logits = np.maximum(A @ W1 + b1, 0.0) @ W2
+        if offset is None:
+            offset = logits.mean(axis=0)
+        rp, c, v = dense_to_csr(A)
+        yield rp, c, v, np.argmax(logits - offset, axis=1).astype(np.float64)
+
+
+def cfg5_dataset(n_rows: int, seed: int = 5):
+    ptrs, cols, vals, labels, base = [np.zeros(1, np.int64)], [], [], [], 0
+    for rp, c, v, y in cfg5_batches(n_rows, seed):
+        ptrs.append(rp[1:] + base)
+        base += int(rp[-1])
+        cols.append(c)
+        vals.append(v)
+        labels.append(y)
+    return np.concatenate(ptrs), np.concatenate(cols), np.concatenate(vals), np.concatenate(labels)

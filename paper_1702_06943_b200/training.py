@@ -22,6 +22,7 @@ from . import _native as N
 from .codec import compress_csr
 from .kernels import OpCounter
 from .matrix import LabeledDataset, SparseRowMatrix, as_vector
+from .mlp import NnModel  # noqa: F401  (reference training.NnModel)
 
 LOSS_KINDS = ("squared", "logistic", "hinge", "nn_mse")
 EXECUTION_MODES = ("compressed", "dense", "csr")

@@ -125,6 +125,14 @@ def training_cases():
         out.append({"loss": loss, "n_cols": 6, "rows": [[[c, struct.pack("<d", x).hex()] for c, x in r] for r in rows],
                     "labels": fhex(labels), "batch_size": 16, "lr": lr, "epochs": 4, "seed": 3,
                     "risks": fhex(trace.risks), "weights": fhex(model.weights)})
+    # the reference's one-hidden-layer network (training.py:81-98, 224-228, 284-293)
+    ds = LabeledDataset(features=SparseRowMatrix(6, rows), labels=z)
+    cfg = training.TrainConfig(loss_kind="nn_mse", batch_size=16, learning_rate=2e-2, epochs=3, seed=5,
+                               hidden_units=4)
+    model, trace = training.train(ds, cfg)
+    out.append({"loss": "nn_mse", "n_cols": 6, "rows": [[[c, struct.pack("<d", x).hex()] for c, x in r] for r in rows],
+                "labels": fhex(z), "batch_size": 16, "lr": 2e-2, "epochs": 3, "seed": 5, "hidden_units": 4,
+                "risks": fhex(trace.risks), "w1": fhex(model.w1), "w2": fhex(model.w2)})
     return out
 
 

@@ -1,0 +1,56 @@
+"""GPU parity for the network trainers on compressed batches.
+
+* nn_mse (the reference's own net): against the reference's golden curve and weights (1e-6).
+* the config-5 MLP (784-200-10, ReLU, softmax-CE): against the oracle's CPU restatement (1e-6);
+  the reference has no such model, so this one is not pinned to reference outputs.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import struct
+
+import numpy as np
+import pytest
+
+from conftest import max_rel_err, within_rel
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = json.load(open(os.path.join(HERE, "golden", "golden.json")))
+REL = 1e-6
+
+
+def unhex(xs):
+    return np.array([struct.unpack("<d", bytes.fromhex(x))[0] for x in xs], dtype=np.float64)
+
+
+def test_nn_mse_matches_reference_curve():
+    from paper_1702_06943_b200.matrix import LabeledDataset, SparseRowMatrix
+    from paper_1702_06943_b200.training import NnModel, TrainConfig, train
+
+    c = [t for t in GOLD["training"] if t["loss"] == "nn_mse"][0]
+    rows = [[(col, struct.unpack("<d", bytes.fromhex(x))[0]) for col, x in r] for r in c["rows"]]
+    ds = LabeledDataset(features=SparseRowMatrix(c["n_cols"], rows), labels=unhex(c["labels"]))
+    cfg = TrainConfig("nn_mse", c["batch_size"], c["lr"], c["epochs"], seed=c["seed"], hidden_units=c["hidden_units"])
+    model, trace = train(ds, cfg)
+    assert isinstance(model, NnModel)
+    want = unhex(c["risks"])
+    assert np.all(np.abs(np.array(trace.risks) - want) <= REL * np.abs(want)), (trace.risks, want)
+    assert within_rel(model.w1.ravel(), unhex(c["w1"]), REL)
+    assert within_rel(model.w2.ravel(), unhex(c["w2"]), REL)
+
+
+def test_cfg5_mlp_vs_cpu_restatement(oracle):
+    from paper_1702_06943_b200 import synth
+    from paper_1702_06943_b200.matrix import LabeledDataset, SparseRowMatrix
+    from paper_1702_06943_b200.mlp import train_mlp
+
+    rp, c, v, y = synth.cfg5_dataset(1000, seed=9)
+    ds = LabeledDataset(features=SparseRowMatrix.from_csr(784, rp, c, v), labels=y)
+    model, trace = train_mlp(ds, hidden=32, classes=10, batch_size=250, learning_rate=0.05, epochs=2, seed=0)
+    (w1, b1, w2, b2), risks = oracle.train_mlp(rp, c, v, y, 784, 32, 10, 250, 0.05, 2, 0)
+    assert np.all(np.abs(np.array(trace.risks) - np.array(risks)) <= REL * np.abs(risks)), (trace.risks, risks)
+    for got, want in ((model.w1, w1), (model.b1, b1), (model.w2, w2), (model.b2, b2)):
+        assert within_rel(got, want, REL), max_rel_err(got, want)

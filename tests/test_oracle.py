@@ -125,6 +125,13 @@ def test_golden_training(oracle, i):
     rows = rows_of(c)
     rp, cols, vals = oracle.rows_to_csr(rows)
     labels = unhex(c["labels"])
+    if c["loss"] == "nn_mse":
+        w1, w2, risks = oracle.train_nn(rp, cols, vals, labels, c["n_cols"], c["hidden_units"], c["batch_size"],
+                                        c["lr"], c["epochs"], c["seed"])
+        assert np.allclose(risks, unhex(c["risks"]), rtol=1e-12, atol=0)
+        assert np.allclose(w1.ravel(), unhex(c["w1"]), rtol=1e-12, atol=1e-15)
+        assert np.allclose(w2.ravel(), unhex(c["w2"]), rtol=1e-12, atol=1e-15)
+        return
     w, risks = oracle.train_glm(rp, cols, vals, labels, c["n_cols"], c["loss"], c["batch_size"], c["lr"],
                                 c["epochs"], c["seed"])
     want_r = unhex(c["risks"])
