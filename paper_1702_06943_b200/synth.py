@@ -183,15 +183,13 @@ def cfg5_batches(n_rows: int, seed: int = 5, batch: int = 250, n_cols: int = 784
     mutation, widened to 784 columns -- and labels argmax of a random 784-200-10 ReLU teacher.
     Yields (row_ptr, cols, vals, labels) per batch."""
     W1, b1, W2 = cfg5_teacher(n_cols, seed=seed)
-    offset = None  # per-class centring (from the first batch) so the classes come out near uniform
+    # each batch's teacher logits are centred per class so the classes come out near uniform
     for lo in range(0, n_rows, batch):
         k = min(batch, n_rows - lo)
         A = cfg1_dense(seed=int(np.random.SeedSequence([seed, lo]).generate_state(1)[0]), n_rows=k, n_cols=n_cols)
         logits = np.maximum(A @ W1 + b1, 0.0) @ W2
-        if offset is None:
-            offset = logits.mean(axis=0)
         rp, c, v = dense_to_csr(A)
-        yield rp, c, v, np.argmax(logits - offset, axis=1).astype(np.float64)
+        yield rp, c, v, np.argmax(logits - logits.mean(axis=0), axis=1).astype(np.float64)
 
 
 def cfg5_dataset(n_rows: int, seed: int = 5):
