@@ -120,6 +120,21 @@ int toc_linalg(const uint8_t* d_arena, const int64_t* d_block_off, const TocBloc
                const double* d_v, double* d_R, const double* d_u, double* d_O, void* d_scratch,
                void* stream);
 
+/* ---- device tree cache (the reference's lazily built, reused CompressedMatrix.tree,
+ * kernels.py:68-77) -----------------------------------------------------------------------
+ * toc_tree_offsets (host): byte offsets (n_blocks + 1 entries) of each batch's tree prefix
+ * (row offsets, derived-node bases, final codes, node table; 16-B aligned) given plan.wide.
+ * toc_build_trees: build every prefix once into d_trees.  toc_linalg_trees: toc_linalg reading
+ * the prefixes from the cache (one bulk copy per batch) instead of rebuilding them. */
+int toc_tree_offsets(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t wide, int64_t* h_tree_off);
+int toc_build_trees(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+                    int64_t n_blocks, const TocPlan* plan, const int64_t* d_tree_off, uint8_t* d_trees,
+                    void* d_scratch, void* stream);
+int toc_linalg_trees(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+                     const int64_t* d_row_base, int64_t n_blocks, const TocPlan* plan, int32_t kind,
+                     const double* d_v, double* d_R, const double* d_u, double* d_O, void* d_scratch,
+                     const uint8_t* d_trees, const int64_t* d_tree_off, void* stream);
+
 /* ---- compressed matrix-matrix products (reference kernels.py:177-234) ----------------------
  * side 0 (matmat_right, kernels.py:177-203): d_out[row_base[b] + r, :] = (A_b . M)[r, :],
  *         d_M = M [n_cols x p] row-major, d_out [n_rows_total x p].

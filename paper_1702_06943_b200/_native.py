@@ -64,6 +64,9 @@ def lib():
     L.toc_index_blocks.argtypes = [P, P, P, I64, P, P]
     L.toc_plan.argtypes = [P, I64, I32, ctypes.POINTER(TocPlan)]
     L.toc_linalg.argtypes = [P, P, P, P, I64, ctypes.POINTER(TocPlan), I32, P, P, P, P, P, P]
+    L.toc_tree_offsets.argtypes = [P, I64, I32, P]
+    L.toc_build_trees.argtypes = [P, P, P, I64, ctypes.POINTER(TocPlan), P, P, P, P]
+    L.toc_linalg_trees.argtypes = [P, P, P, P, I64, ctypes.POINTER(TocPlan), I32, P, P, P, P, P, P, P, P]
     L.toc_matmat.argtypes = [P, P, P, P, P, I64, I32, I32, I32, P, P, P, I64, P]
     L.toc_matmat_scratch.argtypes = [P, I64, I32, I32, I32, ctypes.POINTER(ctypes.c_int64)]
     for name in EXPORTS:
@@ -75,8 +78,8 @@ def lib():
 
 
 # Every symbol include/toc_b200.h declares (tests check the library exports all of them).
-EXPORTS = ["toc_index_blocks", "toc_plan", "toc_linalg", "toc_version", "toc_device_info",
-           "toc_sizeof_meta", "toc_sizeof_plan"]
+EXPORTS = ["toc_index_blocks", "toc_plan", "toc_linalg", "toc_linalg_trees", "toc_build_trees", "toc_tree_offsets",
+           "toc_version", "toc_device_info", "toc_sizeof_meta", "toc_sizeof_plan"]
 
 
 def check(rc: int, what: str) -> None:

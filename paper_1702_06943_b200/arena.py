@@ -71,6 +71,7 @@ class BlockArena:
         self.n_cols = int(self.meta["n_cols"][0]) if self.n_blocks else 0
         self._plans: dict[int, N.TocPlan] = {}
         self._scratch = None
+        self.trees = None  # device tree cache (build_trees)
 
     # ---- construction ------------------------------------------------------------------------
     @classmethod
@@ -128,9 +129,31 @@ class BlockArena:
             self._scratch = self.torch.empty(plan.scratch_bytes, dtype=self.torch.uint8, device=self.data.device)
         return self._scratch
 
-    def linalg(self, kind: int, v=None, u=None, R=None, O=None):
+    def build_trees(self):
+        """Build the device tree cache: each batch's tree prefix (row offsets, derived-node bases,
+        final codes, node table), once -- the device counterpart of the reference's lazily built,
+        reused CompressedMatrix.tree (kernels.py:68-77).  Later linalg calls pull it into shared
+        memory with one bulk copy per batch instead of rebuilding it from the codes."""
+        torch = self.torch
+        self.raise_corrupt()
+        plan = self.plan(N.TOC_MATVEC | N.TOC_VECMAT)
+        off = np.zeros(self.n_blocks + 1, np.int64)
+        N.check(N.lib().toc_tree_offsets(self.meta.ctypes.data_as(ctypes.c_void_p), self.n_blocks, plan.wide,
+                                         off.ctypes.data_as(ctypes.c_void_p)), "toc_tree_offsets")
+        trees = torch.empty(int(off[-1]) + 16, dtype=torch.uint8, device=self.data.device)
+        tree_off_d = torch.from_numpy(off[:-1].copy()).to(self.data.device)
+        scratch = self._scratch_for(plan)
+        N.check(N.lib().toc_build_trees(self.data.data_ptr(), self.block_off_d.data_ptr(), self.meta_d.data_ptr(),
+                                        self.n_blocks, ctypes.byref(plan), tree_off_d.data_ptr(), trees.data_ptr(),
+                                        scratch.data_ptr() if scratch is not None else None, N.stream_handle()),
+                "toc_build_trees")
+        self.trees, self.tree_off_d, self.tree_bytes = trees, tree_off_d, int(off[-1])
+        return self
+
+    def linalg(self, kind: int, v=None, u=None, R=None, O=None, use_trees: bool = True):
         """kind = TOC_MATVEC | TOC_VECMAT.  v: device float64 [n_cols]; u: device float64
-        [n_rows_total].  Returns (R [n_rows_total], O [n_blocks, n_cols]) device tensors."""
+        [n_rows_total].  Returns (R [n_rows_total], O [n_blocks, n_cols]) device tensors.  Uses
+        the tree cache when it has been built (and use_trees), else rebuilds trees per call."""
         torch = self.torch
         self.raise_corrupt()
         dev = self.data.device
@@ -143,11 +166,14 @@ class BlockArena:
                                 device=dev)[: self.n_blocks * self.n_cols].view(self.n_blocks, self.n_cols)
         plan = self.plan(kind)
         scratch = self._scratch_for(plan)
-        rc = N.lib().toc_linalg(
+        trees = self.trees is not None and use_trees
+        rc = N.lib().toc_linalg_trees(
             self.data.data_ptr(), self.block_off_d.data_ptr(), self.meta_d.data_ptr(), self.row_base_d.data_ptr(),
             self.n_blocks, ctypes.byref(plan), kind,
             _ptr(v), _ptr(R), _ptr(u), _ptr(O),
-            scratch.data_ptr() if scratch is not None else None, N.stream_handle())
+            scratch.data_ptr() if scratch is not None else None,
+            self.trees.data_ptr() if trees else None, self.tree_off_d.data_ptr() if trees else None,
+            N.stream_handle())
         N.check(rc, "toc_linalg")
         return R, O
 

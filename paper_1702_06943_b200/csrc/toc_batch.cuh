@@ -18,9 +18,12 @@
 
 namespace toc {
 
-// Byte layout of one batch's tables (all regions 16-B aligned).
+// Byte layout of one batch's tables (all regions 16-B aligned).  The first four regions --
+// row offsets, derived-node bases, final codes and the node table -- depend only on the block and
+// form the "tree" prefix [0, tree): the device tree cache stores exactly these bytes per batch so a
+// kernel can pull them into shared memory with one bulk copy instead of rebuilding them.
 struct BatchLayout {
-  uint32_t off_rowoff, off_dbase, off_last, off_uniq, off_tab, off_pk, total;
+  uint32_t off_rowoff, off_dbase, off_last, off_pk, tree, off_uniq, off_tab, total;
 };
 
 template <bool kWide>
@@ -33,14 +36,45 @@ TOC_HD BatchLayout batch_layout(const TocBlockMeta& m) {
   o += align16(4u * (m.n_rows + 1));
   L.off_last = o;
   o += align16(4u * (m.n_rows + 1));
+  L.off_pk = o;
+  o += align16((kWide ? 8u : 4u) * m.n_derived);
+  L.tree = o;
   L.off_uniq = o;
   o += align16(8u * m.n_uniques);
   L.off_tab = o;
   o += align16(8u * (m.n_pairs + 1));
-  L.off_pk = o;
-  o += align16((kWide ? 8u : 4u) * m.n_derived);
   L.total = o;
   return L;
+}
+
+// ---- TMA bulk copy global -> shared with an mbarrier (sm_90+ async proxy) ------------------
+TOC_D uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+TOC_D void mbar_init(uint64_t* mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// One thread: order earlier generic shared accesses before the async copy, announce the bytes,
+// start the copy (dst, src 16-B aligned, bytes a multiple of 16).
+TOC_D void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(mbar))
+               : "memory");
+}
+
+TOC_D void mbar_wait(uint64_t* mbar, uint32_t phase) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(mbar)), "r"(phase)
+        : "memory");
+  }
 }
 
 // Fixed shared-memory prefix of every CTA: block-scan words and block-reduction doubles.
@@ -154,17 +188,20 @@ struct Batch {
   uint32_t n, nI, S, RP, passes, sub, p0, p1;
   double vmax;     // max |value| over the value index (this thread's part until reduced)
 
-  TOC_D void init(const uint8_t* block, const TocBlockMeta& meta, uint8_t* tables) {
+  // tables: shared (or slab) base of the whole layout; tree: where the tree prefix lives (the same
+  // base, or a cached tree blob in global memory read in place).
+  TOC_D void init(const uint8_t* block, const TocBlockMeta& meta, uint8_t* tables, uint8_t* tree = nullptr) {
     blk = block;
     m = meta;
     const BatchLayout L = batch_layout<kWide>(m);
-    rowoff = reinterpret_cast<uint32_t*>(tables + L.off_rowoff);
-    dbase = reinterpret_cast<uint32_t*>(tables + L.off_dbase);
-    last = reinterpret_cast<uint32_t*>(tables + L.off_last);
+    uint8_t* t = tree ? tree : tables;
+    rowoff = reinterpret_cast<uint32_t*>(t + L.off_rowoff);
+    dbase = reinterpret_cast<uint32_t*>(t + L.off_dbase);
+    last = reinterpret_cast<uint32_t*>(t + L.off_last);
+    pk.p = reinterpret_cast<decltype(pk.p)>(t + L.off_pk);
     uniq = reinterpret_cast<double*>(tables + L.off_uniq);
     tab = reinterpret_cast<double*>(tables + L.off_tab);
     tabw = reinterpret_cast<uint32_t*>(tab);
-    pk.p = reinterpret_cast<decltype(pk.p)>(tables + L.off_pk);
     n = m.n_rows;
     nI = m.n_pairs;
     const uint32_t nth = blockDim.x, tid = threadIdx.x;
@@ -191,16 +228,21 @@ struct Batch {
     return true;
   }
 
-  // Phase 0: row offsets, value index, derived-node bases.  Ends with a barrier.
-  TOC_D void load_index(uint32_t* s_warp) {
-    const uint32_t tid = threadIdx.x, nth = blockDim.x;
-    for (uint32_t r = tid; r <= n; r += nth) rowoff[r] = ld_packed(blk + m.off_offsets, r, m.w_offsets);
+  // The value index (and this thread's part of max |value|).  No barrier.
+  TOC_D void load_values() {
     vmax = 0.0;
-    for (uint32_t i = tid; i < m.n_uniques; i += nth) {
+    for (uint32_t i = threadIdx.x; i < m.n_uniques; i += blockDim.x) {
       const double x = ld_f64_unaligned(blk + m.off_uniques + 8u * i);
       uniq[i] = x;
       vmax = fmax(vmax, fabs(x));
     }
+  }
+
+  // Phase 0: row offsets, value index, derived-node bases.  Ends with a barrier.
+  TOC_D void load_index(uint32_t* s_warp) {
+    const uint32_t tid = threadIdx.x, nth = blockDim.x;
+    for (uint32_t r = tid; r <= n; r += nth) rowoff[r] = ld_packed(blk + m.off_offsets, r, m.w_offsets);
+    load_values();
     __syncthreads();
     scan_derived_base(rowoff, dbase, n, s_warp);
   }

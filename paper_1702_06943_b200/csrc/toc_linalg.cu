@@ -23,22 +23,35 @@ struct LinalgArgs {
   const double* u;
   double* O;
   uint8_t* scratch;
+  const uint8_t* trees;     // optional device tree cache (toc_build_trees); NULL: rebuild per call
+  const int64_t* tree_off;  // byte offset of batch b's tree prefix in `trees`
 };
 
 // One batch of the sweep.  `tables` points either into shared memory or into this CTA's slab.
 template <bool kWide, bool kVecSmem>
 __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, const TocBlockMeta& m,
-                                              uint8_t* tables, const double* vec_s, uint32_t* acc_s,
-                                              uint32_t* s_warp, double* s_red) {
+                                              uint8_t* tables, bool in_smem, const double* vec_s, uint32_t* acc_s,
+                                              uint32_t* s_warp, double* s_red, uint64_t* mbar, uint32_t& phase) {
   const uint32_t tid = threadIdx.x, nth = blockDim.x;
   const bool do_mv = a.kind & TOC_MATVEC, do_vm = a.kind & TOC_VECMAT;
   const int64_t row_base = a.row_base[b];
   const int32_t ncol = a.n_cols;
+  const uint8_t* blk = a.arena + a.block_off[b];
   Batch<kWide> B;
-  B.init(a.arena + a.block_off[b], m, tables);
+  const bool cached = a.trees != nullptr;
+  if (cached) {
+    // Tree prefix from the device cache: one bulk copy into shared memory (or read in place
+    // from global memory when the batch's tables do not fit), overlapped with the value work.
+    uint8_t* tree = const_cast<uint8_t*>(a.trees + a.tree_off[b]);
+    B.init(blk, m, tables, in_smem ? nullptr : tree);
+    if (in_smem && tid == 0) bulk_load(tables, tree, batch_layout<kWide>(m).tree, mbar);
+    B.load_values();
+  } else {
+    B.init(blk, m, tables);
+  }
   if (do_vm && kVecSmem)
     for (int32_t c = tid; c < 2 * ncol; c += nth) acc_s[c] = 0u;
-  B.load_index(s_warp);
+  if (!cached) B.load_index(s_warp);
   double g_scale = 1.0, o_scale = 1.0;
   if (do_vm) {  // a-priori bounds of every partial sum (see fix_add): sum |u| and max |value|
     double su = 0.0;
@@ -48,12 +61,23 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
     g_scale = fix_scale(su);
     o_scale = fix_scale(su * mv);
   }
-  B.build_nodes();
-  if (do_mv) B.template compute_p1<false>(kVecSmem ? vec_s : a.v);
-  else B.zero_tab();
-  __syncthreads();
-  B.resolve_keys();
-  __syncthreads();
+  if (cached) {
+    __syncthreads();  // uniq complete
+    if (do_mv) B.template compute_p1<false>(kVecSmem ? vec_s : a.v);
+    else B.zero_tab();
+    if (in_smem) {
+      mbar_wait(mbar, phase);
+      phase ^= 1u;
+    }
+    __syncthreads();
+  } else {
+    B.build_nodes();
+    if (do_mv) B.template compute_p1<false>(kVecSmem ? vec_s : a.v);
+    else B.zero_tab();
+    __syncthreads();
+    B.resolve_keys();
+    __syncthreads();
+  }
   if (do_mv) B.matvec_rows([&](uint32_t r, double s) { a.R[row_base + r] = s; });
   if (do_vm) {
     if (do_mv) {
@@ -83,6 +107,10 @@ __global__ void __launch_bounds__(1024, 1) linalg_kernel(LinalgArgs a) {
   uint32_t* s_warp = reinterpret_cast<uint32_t*>(smem);  // 33 words
   uint8_t* p = smem + kFixedBytes;
   double* s_red = reinterpret_cast<double*>(smem + 160);  // 33 doubles
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + 448);  // tree-cache bulk copies
+  uint32_t phase = 0;
+  if (threadIdx.x == 0) mbar_init(mbar, 1);
+  __syncthreads();
   double* vec_s = nullptr;
   uint32_t* acc_s = nullptr;
   if (kVecSmem) {
@@ -111,9 +139,37 @@ __global__ void __launch_bounds__(1024, 1) linalg_kernel(LinalgArgs a) {
     }
     __syncthreads();
     if (need <= (uint32_t)a.batch_smem_budget)
-      process_batch<kWide, kVecSmem>(a, b, m, p, vec_s, acc_s, s_warp, s_red);
+      process_batch<kWide, kVecSmem>(a, b, m, p, true, vec_s, acc_s, s_warp, s_red, mbar, phase);
     else
-      process_batch<kWide, kVecSmem>(a, b, m, slab, vec_s, acc_s, s_warp, s_red);
+      process_batch<kWide, kVecSmem>(a, b, m, slab, false, vec_s, acc_s, s_warp, s_red, mbar, phase);
+  }
+}
+
+// Device tree cache: rebuild each batch's tree prefix (row offsets, derived-node bases, final
+// codes, node table with resolved keys) once and store it, byte for byte as it sits in shared
+// memory, at trees + tree_off[b].
+template <bool kWide>
+__global__ void __launch_bounds__(1024, 1) build_trees_kernel(LinalgArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint32_t* s_warp = reinterpret_cast<uint32_t*>(smem);
+  uint8_t* p = smem + kFixedBytes;
+  uint8_t* slab = a.scratch ? a.scratch + (int64_t)blockIdx.x * a.slab_bytes : nullptr;
+  for (int64_t b = blockIdx.x; b < a.n_blocks; b += gridDim.x) {
+    const TocBlockMeta m = a.meta[b];
+    if (m.status != TOC_OK || m.corrupt) continue;
+    const BatchLayout L = batch_layout<kWide>(m);
+    uint8_t* tables = L.total <= (uint32_t)a.batch_smem_budget ? p : slab;
+    __syncthreads();
+    Batch<kWide> B;
+    B.init(a.arena + a.block_off[b], m, tables);
+    B.load_index(s_warp);
+    B.build_nodes();
+    __syncthreads();
+    B.resolve_keys();
+    __syncthreads();
+    const uint4* src = reinterpret_cast<const uint4*>(tables);
+    uint4* dst = reinterpret_cast<uint4*>(const_cast<uint8_t*>(a.trees) + a.tree_off[b]);
+    for (uint32_t k = threadIdx.x; k < L.tree / 16u; k += blockDim.x) dst[k] = src[k];
   }
 }
 
@@ -211,10 +267,60 @@ extern "C" int toc_plan(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t ki
   return TOC_OK;
 }
 
+extern "C" int toc_linalg_trees(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+                                const int64_t* d_row_base, int64_t n_blocks, const TocPlan* plan, int32_t kind,
+                                const double* d_v, double* d_R, const double* d_u, double* d_O, void* d_scratch,
+                                const uint8_t* d_trees, const int64_t* d_tree_off, void* stream);
+
 extern "C" int toc_linalg(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
                           const int64_t* d_row_base, int64_t n_blocks, const TocPlan* plan, int32_t kind,
                           const double* d_v, double* d_R, const double* d_u, double* d_O, void* d_scratch,
                           void* stream) {
+  return toc_linalg_trees(d_arena, d_block_off, d_meta, d_row_base, n_blocks, plan, kind, d_v, d_R, d_u, d_O,
+                          d_scratch, nullptr, nullptr, stream);
+}
+
+extern "C" int toc_tree_offsets(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t wide, int64_t* h_tree_off) {
+  if (!h_meta || !h_tree_off || n_blocks < 0) return TOC_E_ARG;
+  int64_t o = 0;
+  for (int64_t b = 0; b < n_blocks; ++b) {
+    h_tree_off[b] = o;
+    o += wide ? toc::batch_layout<true>(h_meta[b]).tree : toc::batch_layout<false>(h_meta[b]).tree;
+  }
+  h_tree_off[n_blocks] = o;
+  return TOC_OK;
+}
+
+extern "C" int toc_build_trees(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+                               int64_t n_blocks, const TocPlan* plan, const int64_t* d_tree_off, uint8_t* d_trees,
+                               void* d_scratch, void* stream) {
+  if (!plan || n_blocks < 0 || !d_trees || !d_tree_off) return TOC_E_ARG;
+  if (plan->global_tables && !d_scratch) return TOC_E_ARG;
+  if (n_blocks == 0) return TOC_OK;
+  toc::LinalgArgs a{};
+  a.arena = d_arena;
+  a.block_off = d_block_off;
+  a.meta = d_meta;
+  a.n_blocks = n_blocks;
+  a.batch_smem_budget = plan->smem_bytes - (int32_t)toc::kFixedBytes;
+  a.slab_bytes = plan->global_tables ? plan->scratch_bytes / plan->ctas : 0;
+  a.scratch = (uint8_t*)d_scratch;
+  a.trees = d_trees;
+  a.tree_off = d_tree_off;
+  void* fn = plan->wide ? (void*)toc::build_trees_kernel<true> : (void*)toc::build_trees_kernel<false>;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, plan->smem_bytes) != cudaSuccess)
+    return TOC_E_CUDA;
+  void* args[] = {&a};
+  return cudaLaunchKernel(fn, dim3(plan->ctas), dim3(plan->threads), args, plan->smem_bytes, (cudaStream_t)stream) ==
+                 cudaSuccess
+             ? TOC_OK
+             : TOC_E_CUDA;
+}
+
+extern "C" int toc_linalg_trees(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+                                const int64_t* d_row_base, int64_t n_blocks, const TocPlan* plan, int32_t kind,
+                                const double* d_v, double* d_R, const double* d_u, double* d_O, void* d_scratch,
+                                const uint8_t* d_trees, const int64_t* d_tree_off, void* stream) {
   if (!plan || n_blocks < 0 || !(kind & (TOC_MATVEC | TOC_VECMAT))) return TOC_E_ARG;
   if ((kind & TOC_MATVEC) && (!d_v || !d_R)) return TOC_E_ARG;
   if ((kind & TOC_VECMAT) && (!d_u || !d_O)) return TOC_E_ARG;
@@ -238,6 +344,8 @@ extern "C" int toc_linalg(const uint8_t* d_arena, const int64_t* d_block_off, co
   a.u = d_u;
   a.O = d_O;
   a.scratch = (uint8_t*)d_scratch;
+  a.trees = d_trees;
+  a.tree_off = d_tree_off;
   if ((kind & TOC_VECMAT) && !plan->vec_in_smem) {
     if (cudaMemsetAsync(d_O, 0, sizeof(double) * (size_t)n_blocks * plan->n_cols, s) != cudaSuccess)
       return TOC_E_CUDA;

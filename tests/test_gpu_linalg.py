@@ -24,11 +24,18 @@ def _arena(blocks):
     return BlockArena.from_bytes(blocks)
 
 
-def _check_sweep(oracle, encs, v, seed=0):
+@pytest.fixture(params=["rebuild", "tree_cache"])
+def tree_mode(request):
+    return request.param
+
+
+def _check_sweep(oracle, encs, v, seed=0, mode="rebuild"):
     import torch
 
     blocks = [oracle.serialize(e) for e in encs]
     arena = _arena(blocks)
+    if mode == "tree_cache":
+        arena.build_trees()
     trees = [oracle.Tree.from_encoding(e) for e in encs]
     n_total = sum(e.n_rows for e in encs)
     u = np.random.default_rng(seed).standard_normal(n_total)
@@ -63,12 +70,12 @@ def test_toy_known_answers(oracle):
     assert O[0].cpu().tolist() == [7.0, 9.0, 6.0, 8.0, 10.0]  # test_kernels.py:64-69
 
 
-def test_tree_example(oracle):
+def test_tree_example(oracle, tree_mode):
     enc = oracle.encode_rows(5, TREE_ROWS)
-    _check_sweep(oracle, [enc], np.arange(1.0, 6.0))
+    _check_sweep(oracle, [enc], np.arange(1.0, 6.0), mode=tree_mode)
 
 
-def test_random_alphabet_many_blocks(oracle):
+def test_random_alphabet_many_blocks(oracle, tree_mode):
     rng = np.random.default_rng(7)
     encs = []
     n_cols = 12
@@ -76,19 +83,19 @@ def test_random_alphabet_many_blocks(oracle):
         rows = random_alphabet_rows(rng, int(rng.integers(0, 40)), n_cols, float(rng.uniform(0.05, 1.0)),
                                     16, integer_alphabet=bool(i % 2))
         encs.append(oracle.encode_rows(n_cols, rows))
-    _check_sweep(oracle, encs, rng.standard_normal(n_cols), seed=1)
+    _check_sweep(oracle, encs, rng.standard_normal(n_cols), seed=1, mode=tree_mode)
 
 
-def test_cfg1_batch(oracle):
+def test_cfg1_batch(oracle, tree_mode):
     from paper_1702_06943_b200 import synth
 
     A = synth.cfg1_dense(0)
     enc = oracle.encode_csr(128, *synth.dense_to_csr(A))
     v, u = synth.cfg1_operands(0)
-    _check_sweep(oracle, [enc], v)
+    _check_sweep(oracle, [enc], v, mode=tree_mode)
 
 
-def test_cfg2_batches(oracle):
+def test_cfg2_batches(oracle, tree_mode):
     from paper_1702_06943_b200 import synth
 
     encs = []
@@ -96,18 +103,18 @@ def test_cfg2_batches(oracle):
         enc = oracle.encode_csr(784, *synth.dense_to_csr(synth.cfg2_batch_dense(0, b)))
         encs.append(enc)
     v, _ = synth.cfg2_operands(0, 6)
-    _check_sweep(oracle, encs, v, seed=3)
+    _check_sweep(oracle, encs, v, seed=3, mode=tree_mode)
 
 
-def test_empty_and_zero_rows(oracle):
+def test_empty_and_zero_rows(oracle, tree_mode):
     encs = [oracle.encode_rows(4, []), oracle.encode_rows(3, [[(1, 2.0)], [], [(0, 4.0)]]),
             oracle.encode_rows(3, [[], []])]
     # n_cols differ from 4 -> keep one arena per n_cols
-    _check_sweep(oracle, encs[1:], np.array([1.0, 1.0, 1.0]))
-    _check_sweep(oracle, encs[:1], np.ones(4))
+    _check_sweep(oracle, encs[1:], np.array([1.0, 1.0, 1.0]), mode=tree_mode)
+    _check_sweep(oracle, encs[:1], np.ones(4), mode=tree_mode)
 
 
-def test_wide_tree_global_tables(oracle):
+def test_wide_tree_global_tables(oracle, tree_mode):
     """A batch whose tree exceeds 65536 nodes (32-bit node ids) and shared memory (global
     table fallback): identical rows compress into long chains."""
     rng = np.random.default_rng(5)
@@ -116,7 +123,7 @@ def test_wide_tree_global_tables(oracle):
     rows = [base[i % 30] if i % 3 else random_alphabet_rows(rng, 1, n_cols, 0.9, 64)[0] for i in range(600)]
     enc = oracle.encode_rows(n_cols, rows)
     assert enc.tree_length() > 65536
-    _check_sweep(oracle, [enc], rng.standard_normal(n_cols), seed=9)
+    _check_sweep(oracle, [enc], rng.standard_normal(n_cols), seed=9, mode=tree_mode)
 
 
 def test_batch_sweep_public_api(oracle):
