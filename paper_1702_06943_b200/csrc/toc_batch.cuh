@@ -319,9 +319,27 @@ struct Batch {
   }
 
   // Walk the codes of [j0, j1) of row r; visit(i) once per pair (i = first-layer id).
+  // Two codes per iteration, their chains stepped in lockstep: the dependent shared loads of one
+  // chain overlap those of the other (the walk is latency-bound on these loads).
   template <typename V>
   TOC_D void walk(uint32_t r, uint32_t lo, uint32_t hi, uint32_t db, uint32_t j0, uint32_t j1, V&& visit) const {
-    for (uint32_t j = j0; j < j1; ++j) {
+    uint32_t j = j0;
+    for (; j + 1 < j1; j += 2) {
+      uint32_t x = pk.par(db + (j - lo));  // j + 1 < j1 <= hi: j is never the final code
+      uint32_t y = (j + 2 < hi) ? pk.par(db + (j + 1 - lo)) : last[r];
+      while (x > nI || y > nI) {
+        uint32_t px = x, kx = 0, py = y, ky = 0;
+        if (x > nI) pk.get(x - 1 - nI, px, kx);
+        if (y > nI) pk.get(y - 1 - nI, py, ky);
+        if (kx) visit(kx);
+        if (ky) visit(ky);
+        x = px;
+        y = py;
+      }
+      visit(x);
+      visit(y);
+    }
+    if (j < j1) {
       uint32_t x = (j + 1 < hi) ? pk.par(db + (j - lo)) : last[r];
       while (x > nI) {
         uint32_t p, key;

@@ -12,6 +12,7 @@ p = argparse.ArgumentParser()
 p.add_argument("--batches", type=int, default=1024)
 p.add_argument("--kind", type=int, default=3)
 p.add_argument("--reps", type=int, default=3)
+p.add_argument("--trees", type=int, default=1)
 a = p.parse_args()
 
 import torch  # noqa: E402
@@ -21,6 +22,8 @@ from paper_1702_06943_b200.codec import compress_csr  # noqa: E402
 
 rp, c, v, br = bench.make_shard(0, a.batches)
 arena = compress_csr(bench.COLS, rp, c, v, br)
+if a.trees:
+    arena.build_trees()
 vd = torch.randn(bench.COLS, dtype=torch.float64, device="cuda")
 ud = torch.randn(arena.n_rows_total, dtype=torch.float64, device="cuda")
 for _ in range(a.reps):
