@@ -245,6 +245,35 @@ int toc_glm_grad(const uint8_t* d_arena, const int64_t* d_block_off, const TocBl
 int toc_glm_risk(const double* d_z, const double* d_y, int64_t n, int32_t loss, double* d_partial,
                  int32_t n_partial, void* stream);
 
+/* Cached step images (the device form of the reference's once-only per-batch tree cache,
+ * kernels.py:68-77): each batch's code stream, decode-tree node table, unpacked first-layer pairs
+ * (also sorted by column), value index, and per-CTA row parts (lane splits, labels), 16-byte
+ * aligned, built once per training run (layout: toc_images.cu).  The epoch runs on a cluster of
+ * `cluster` CTAs (1, 2, 4 or 8) that split each batch's rows.
+ * toc_mgd_image_plan: host-only.  cluster_req 0 = choose; *cluster = the chosen size, or 0 when
+ * images do not fit shared memory (use toc_glm_epoch); h_image_off: n_blocks + 1 byte offsets.
+ * TOC_E_* of the first malformed / corrupt block. */
+int toc_mgd_image_plan(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t n_cols, int32_t cluster_req,
+                       int32_t* cluster, int64_t* h_image_off);
+int toc_mgd_build_images(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+                         const TocBlockMeta* h_meta, const int64_t* d_row_base, int64_t n_blocks,
+                         int32_t n_cols, int32_t cluster, const double* d_labels, uint8_t* d_images,
+                         const int64_t* d_image_off, void* stream);
+/* One epoch (training.py:303-316) on one cluster: weights in shared memory, the next image
+ * prefetched by TMA (multicast) during each step, one cluster barrier per step.  Same results as
+ * toc_glm_epoch up to fp64 summation order of the per-column sums (fixed, deterministic). */
+int toc_glm_epoch_images(const uint8_t* d_images, const int64_t* d_image_off, const TocBlockMeta* d_meta,
+                         const TocBlockMeta* h_meta, int64_t n_blocks, int32_t n_cols, int32_t cluster,
+                         int32_t loss, double lr, double* d_w, void* stream);
+/* Diagnostic: CTA width (power of two, 64..1024; 0 = 512) of cluster epochs planned afterwards. */
+int toc_mgd_set_image_threads(int32_t threads);
+/* toc_glm_epoch_images plus 8 clock64 stamps per step from CTA 0 (step start, image landed, P1,
+ * A.w and loss, bound, s^T.A, cluster barrier passed, update).  Diagnostic. */
+int toc_glm_epoch_images_traced(const uint8_t* d_images, const int64_t* d_image_off,
+                                const TocBlockMeta* d_meta, const TocBlockMeta* h_meta, int64_t n_blocks,
+                                int32_t n_cols, int32_t cluster, int32_t loss, double lr, double* d_w,
+                                long long* d_trace, void* stream);
+
 /* ---- version / self-description ---------------------------------------------------------- */
 const char* toc_version(void);
 int toc_device_info(int32_t* sm_count, int32_t* smem_optin, int64_t* l2_bytes);

@@ -202,6 +202,27 @@ struct Batch {
     uniq = reinterpret_cast<double*>(tables + L.off_uniq);
     tab = reinterpret_cast<double*>(tables + L.off_tab);
     tabw = reinterpret_cast<uint32_t*>(tab);
+    shape();
+  }
+
+  // A batch whose tree prefix, value index and tables all live elsewhere (a cached step image,
+  // toc_mgd.cu): P1 in p1tab, G (fixed point) in gtab -- separate, so G needs no zeroing barrier
+  // after A.v has read P1.
+  TOC_D void bind(const TocBlockMeta& meta, uint8_t* tree, double* uniq_, double* p1tab, uint32_t* gtab) {
+    blk = nullptr;
+    m = meta;
+    const BatchLayout L = batch_layout<kWide>(m);
+    rowoff = reinterpret_cast<uint32_t*>(tree + L.off_rowoff);
+    dbase = reinterpret_cast<uint32_t*>(tree + L.off_dbase);
+    last = reinterpret_cast<uint32_t*>(tree + L.off_last);
+    pk.p = reinterpret_cast<decltype(pk.p)>(tree + L.off_pk);
+    uniq = uniq_;
+    tab = p1tab;
+    tabw = gtab;
+    shape();
+  }
+
+  TOC_D void shape() {
     n = m.n_rows;
     nI = m.n_pairs;
     const uint32_t nth = blockDim.x, tid = threadIdx.x;

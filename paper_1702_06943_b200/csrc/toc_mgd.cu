@@ -10,7 +10,9 @@
 // counter reaches t, reads the current weights through L2, runs A.w -> s -> s^T.A -> update,
 // and publishes the new weights with a release store of t + 1.  The dependency chain therefore
 // costs only the weight-dependent part of each step plus one L2 handoff.
-#include "toc_batch.cuh"
+#include <algorithm>
+
+#include "toc_glm.cuh"
 
 namespace toc {
 
@@ -39,33 +41,8 @@ struct MgdArgs {
   int32_t max_pairs;
 };
 
-constexpr int kTracePoints = 8;
-
 TOC_D void stamp(const MgdArgs& a, int64_t t, int k) {
   if (a.trace && threadIdx.x == 0) a.trace[t * kTracePoints + k] = clock64();
-}
-
-// Per-example scalar of glm_gradient (training.py:272-280).
-TOC_D double loss_scalar(int loss, double y, double z) {
-  if (loss == TOC_LOSS_SQUARED) return z - y;
-  if (loss == TOC_LOSS_LOGISTIC) return -y / (1.0 + exp(y * z));
-  return (y * z < 1.0) ? -y : 0.0;  // hinge subgradient: flat side contributes zero
-}
-
-TOC_D uint32_t ld_acquire(const uint32_t* p) {
-  uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return v;
-}
-
-TOC_D unsigned long long globaltimer_ns() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
-TOC_D void st_release(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 // Gradient of one batch into fixed-point column accumulators `acc` (2 words per column).

@@ -118,14 +118,27 @@ def _bind():
         L.toc_glm_epoch.argtypes = [P, P, P, P, P, I64, I32, I32, D, P, P, P, P, P]
         L.toc_glm_grad.argtypes = [P, P, P, P, P, I64, I32, I32, P, P, P, P, P]
         L.toc_glm_risk.argtypes = [P, P, I64, I32, P, I32, P]
+        L.toc_mgd_image_plan.argtypes = [P, I64, I32, I32, ctypes.POINTER(ctypes.c_int32), P]
+        L.toc_mgd_build_images.argtypes = [P, P, P, P, P, I64, I32, I32, P, P, P, P]
+        L.toc_glm_epoch_images.argtypes = [P, P, P, P, I64, I32, I32, I32, D, P, P]
         L._mgd_bound = True
     return L
 
 
 class GlmTrainer:
-    """Device-resident GLM training state over DeviceBatches."""
+    """Device-resident GLM training state over DeviceBatches.
 
-    def __init__(self, batches: DeviceBatches, loss_kind: str, learning_rate: float):
+    mode "images" (the default when it fits shared memory): each batch's step image -- its decode
+    tree, value index, unpacked first-layer pairs and labels -- is built once here, the device form
+    of the reference's once-only per-batch tree cache (kernels.py:68-77), and every epoch is one
+    launch of a thread-block cluster over them (toc_glm_epoch_images; cluster=0 picks its size).
+    mode "relay": no cache, each step rebuilds its tables from the TOC1 block (toc_glm_epoch).
+    Both give the same results up to fp64 summation order."""
+
+    def __init__(self, batches: DeviceBatches, loss_kind: str, learning_rate: float, mode: str = "auto",
+                 cluster: int = 0):
+        if mode not in ("auto", "images", "relay"):
+            raise ValueError(f"mode must be auto, images or relay, got {mode!r}")
         self.torch = N.require_cuda()
         self.b = batches
         self.loss = LOSS_CODE[loss_kind]
@@ -140,6 +153,41 @@ class GlmTrainer:
         N.check(L.toc_mgd_workspace(a.meta.ctypes.data_as(ctypes.c_void_p), a.n_blocks, batches.n_cols, 0,
                                     ctypes.byref(nbytes)), "toc_mgd_workspace")
         self.scratch = torch.empty(max(nbytes.value, 16), dtype=torch.uint8, device="cuda")
+        self.mode = "relay"
+        self.image_build_seconds = 0.0
+        self.cluster = 0
+        if mode != "relay":
+            self._build_images(mode == "images", cluster)
+
+    def _build_images(self, required: bool, cluster_req: int) -> None:
+        torch = self.torch
+        a = self.b.arena
+        a.raise_corrupt()
+        L = _bind()
+        meta = a.meta.ctypes.data_as(ctypes.c_void_p)
+        off = np.zeros(a.n_blocks + 1, dtype=np.int64)
+        ok = ctypes.c_int32()
+        N.check(L.toc_mgd_image_plan(meta, a.n_blocks, self.b.n_cols, int(cluster_req), ctypes.byref(ok),
+                                     off.ctypes.data_as(ctypes.c_void_p)), "toc_mgd_image_plan")
+        if not ok.value:
+            if required:
+                raise ValueError("step images do not fit the single-CTA epoch (shared memory); use mode='relay'")
+            return
+        self.image_off = off
+        self.image_off_d = torch.from_numpy(off).cuda()
+        self.images = torch.empty(max(int(off[-1]), 16), dtype=torch.uint8, device="cuda")
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record()
+        N.check(L.toc_mgd_build_images(a.data.data_ptr(), a.block_off_d.data_ptr(), a.meta_d.data_ptr(), meta,
+                                       a.row_base_d.data_ptr(), a.n_blocks, self.b.n_cols, ok.value,
+                                       self.b.labels.data_ptr(),
+                                       self.images.data_ptr(), self.image_off_d.data_ptr(), N.stream_handle()),
+                "toc_mgd_build_images")
+        end.record()
+        end.synchronize()
+        self.image_build_seconds = start.elapsed_time(end) / 1e3
+        self.mode = "images"
+        self.cluster = ok.value
 
     def epoch(self) -> float:
         """One epoch; returns its device time in seconds (CUDA events on the launch stream)."""
@@ -147,6 +195,16 @@ class GlmTrainer:
         a = self.b.arena
         a.raise_corrupt()
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if self.mode == "images":
+            start.record()
+            N.check(_bind().toc_glm_epoch_images(self.images.data_ptr(), self.image_off_d.data_ptr(),
+                                                 a.meta_d.data_ptr(), a.meta.ctypes.data_as(ctypes.c_void_p),
+                                                 a.n_blocks, self.b.n_cols, self.cluster, self.loss, self.lr,
+                                                 self.w.data_ptr(), N.stream_handle()),
+                    "toc_glm_epoch_images")
+            end.record()
+            end.synchronize()
+            return start.elapsed_time(end) / 1e3
         start.record()
         N.check(_bind().toc_glm_epoch(a.data.data_ptr(), a.block_off_d.data_ptr(), a.meta_d.data_ptr(),
                                       a.meta.ctypes.data_as(ctypes.c_void_p), a.row_base_d.data_ptr(), a.n_blocks,

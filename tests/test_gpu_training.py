@@ -132,3 +132,61 @@ def test_counter_charges_matvec_and_vecmat(oracle):
         enc = oracle.encode_csr(68, brp, c[g], v[g])
         want += 2 * ((enc.tree_length() - 1) + len(enc.codes))
     assert counter.multiply_adds == want
+
+
+def _trainer(rp, c, v, y, n_cols, bs, loss, lr, mode, cluster=0):
+    from paper_1702_06943_b200.training import DeviceBatches, GlmTrainer
+
+    return GlmTrainer(DeviceBatches(dataset_from_csr(n_cols, rp, c, v, y), bs), loss, lr, mode=mode, cluster=cluster)
+
+
+@pytest.mark.parametrize("loss,lr,cluster", [("logistic", 0.1, 1), ("logistic", 0.1, 2), ("logistic", 0.1, 4),
+                                             ("logistic", 0.1, 8), ("hinge", 0.05, 8), ("squared", 1e-3, 1),
+                                             ("squared", 1e-3, 4)])
+def test_step_images_match_relay(loss, lr, cluster):
+    """The cluster epoch over cached step images computes what the relay computes: the same fixed-
+    point G per row set; only the per-column sums of value * G run in fp64 in (column, pair, CTA)
+    order instead of a fixed-point scatter, so the weights agree to ~1e-15."""
+    from paper_1702_06943_b200 import synth
+
+    rp, c, v, y = synth.cfg3_dataset(6_000, seed=31)
+    if loss == "squared":
+        y = y * 0.5 + 0.25
+    ti = _trainer(rp, c, v, y, 68, 250, loss, lr, "images", cluster)
+    tr = _trainer(rp, c, v, y, 68, 250, loss, lr, "relay")
+    assert ti.mode == "images" and tr.mode == "relay" and ti.cluster == cluster
+    for _ in range(2):
+        ti.epoch()
+        tr.epoch()
+        wi, wr = ti.weights(), tr.weights()
+        assert within_rel(wi, wr, 1e-12), max_rel_err(wi, wr)
+        assert ti.risk() == pytest.approx(tr.risk(), rel=1e-12)
+
+
+def test_step_images_ragged_batches(oracle):
+    """Short last batch, rows of very different lengths, a batch size that is not a multiple of 32."""
+    from helpers import random_alphabet_rows
+
+    rng = np.random.default_rng(33)
+    rows = random_alphabet_rows(rng, 777, 40, 0.3) + [[(0, 1.0)], [], [(39, 2.0)]] * 5
+    rp, c, v = oracle.rows_to_csr(rows)
+    y = np.where(rng.random(len(rows)) < 0.5, -1.0, 1.0)
+    t = _trainer(rp, c, v, y, 40, 37, "logistic", 0.2, "images")
+    assert t.mode == "images" and t.image_build_seconds > 0
+    from paper_1702_06943_b200.training import TrainConfig, train
+
+    model, trace = train(dataset_from_csr(40, rp, c, v, y), TrainConfig("logistic", 37, 0.2, 2))
+    w_ref, risks_ref = oracle.train_glm(rp, c, v, y, 40, "logistic", 37, 0.2, 2, 0)
+    risks_ref = np.asarray(risks_ref)
+    assert np.all(np.abs(np.array(trace.risks) - risks_ref) <= REL * np.abs(risks_ref)), (trace.risks, risks_ref)
+    assert within_rel(model.weights, w_ref, REL), max_rel_err(model.weights, w_ref)
+
+
+def test_large_m_falls_back_to_relay():
+    from paper_1702_06943_b200 import synth
+
+    rp, c, v, y = synth.cfg4_dataset(1_000, seed=34)
+    t = _trainer(rp, c, v, y, 47_236, 250, "hinge", 0.01, "auto")
+    assert t.mode == "relay"
+    with pytest.raises(ValueError):
+        _trainer(rp, c, v, y, 47_236, 250, "hinge", 0.01, "images")

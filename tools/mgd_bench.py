@@ -14,6 +14,8 @@ p.add_argument("--config", type=int, default=3)
 p.add_argument("--rows", type=int, default=0)
 p.add_argument("--epochs", type=int, default=0)
 p.add_argument("--max-ctas", type=int, default=0)
+p.add_argument("--cluster", type=int, default=0)
+p.add_argument("--threads", type=int, default=0)
 a = p.parse_args()
 
 from paper_1702_06943_b200 import synth  # noqa: E402
@@ -29,7 +31,10 @@ else:
 ds = LabeledDataset(features=SparseRowMatrix.from_csr(m, rp, c, v, check=False), labels=y)
 t = time.time(); sh = shuffle_once(ds, 0); ts = time.time() - t
 t = time.time(); batches = DeviceBatches(sh, 250); import torch; torch.cuda.synchronize(); te = time.time() - t
-tr = GlmTrainer(batches, loss, lr)
+if a.threads:
+    from paper_1702_06943_b200 import _native as _N0
+    _N0.lib().toc_mgd_set_image_threads(a.threads)
+tr = GlmTrainer(batches, loss, lr, cluster=a.cluster)
 if a.max_ctas:
     from paper_1702_06943_b200 import _native as _N
     _N.lib().toc_mgd_set_max_ctas(a.max_ctas)
@@ -37,6 +42,8 @@ secs, risks = [], []
 for _ in range(epochs):
     secs.append(tr.epoch())
     risks.append(tr.risk())
+print("untraced epoch s:", [round(x, 5) for x in secs], "us/step:", round(min(secs) / batches.arena.n_blocks * 1e6, 3),
+      "mode", tr.mode, "cluster", tr.cluster)
 print(json.dumps({"config": a.config, "rows": n, "steps_per_epoch": batches.arena.n_blocks, "epoch_seconds": secs,
                   "risks": risks, "gen_s": tg, "shuffle_s": ts, "compress_s": te,
                   "block_bytes": batches.arena.block_bytes}))
@@ -66,3 +73,22 @@ d = np.diff(T, axis=1)
 names = ["wait", "p1", "matvec+loss", "bound", "vecmat", "update", "fence"]
 print("phase cycles (median per step):", {n: int(np.median(d[:, i])) for i, n in enumerate(names)})
 print("step critical path (median cycles, acquire->release):", int(np.median(T[:, 7] - T[:, 1])))
+
+if tr.mode == "images":
+    L.toc_glm_epoch_images_traced.argtypes = [P, P, P, P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                              ctypes.c_int32, ctypes.c_double, P, P, P]
+    trace.zero_()
+    N.check(L.toc_glm_epoch_images_traced(tr.images.data_ptr(), tr.image_off_d.data_ptr(), ar.meta_d.data_ptr(),
+                                          ar.meta.ctypes.data_as(P), ar.n_blocks, batches.n_cols, tr.cluster, tr.loss,
+                                          tr.lr, tr.w.data_ptr(), trace.data_ptr(), N.stream_handle()),
+            "images traced")
+    torch.cuda.synchronize()
+    T = trace.view(-1, 8).cpu().numpy().astype(np.int64)
+    d = np.diff(T, axis=1)
+    names = ["image wait", "p1", "matvec+loss", "bound", "vecmat", "col partials+cluster sync", "update"]
+    print("cluster", tr.cluster, "phase cycles (median per step):",
+          {n: int(np.median(d[:, i])) for i, n in enumerate(names)})
+    print("step (median cycles):", int(np.median(np.diff(T[:, 0]))), "image build s", tr.image_build_seconds)
+    m = ar.meta
+    print("batch shape (median): rows", int(np.median(m["n_rows"])), "pairs", int(np.median(m["n_pairs"])),
+          "codes", int(np.median(m["n_codes"])), "derived", int(np.median(m["n_derived"])))
