@@ -130,12 +130,21 @@ __global__ void __launch_bounds__(1024, 1) linalg_kernel(LinalgArgs a) {
     const TocBlockMeta m = a.meta[b];
     if (m.status != TOC_OK || m.corrupt) continue;  // host refuses such arenas up front
     const uint32_t need = batch_layout<kWide>(m).total;
-    if (threadIdx.x == 0 && b + gridDim.x < a.n_blocks) {  // pull the CTA's next block into L2
-      const TocBlockMeta& mn = a.meta[b + gridDim.x];
-      const uint32_t bytes = align16(mn.off_offsets + (mn.n_rows + 1u) * mn.w_offsets);
-      const uint8_t* nb = a.arena + a.block_off[b + gridDim.x];
-      if (mn.status == TOC_OK && bytes > 0)
+    if (threadIdx.x == 0 && b + gridDim.x < a.n_blocks) {  // pull what the next batch reads into L2
+      const int64_t bn = b + gridDim.x;
+      const TocBlockMeta& mn = a.meta[bn];
+      const uint8_t* nb = a.arena + a.block_off[bn];
+      // block-only: the whole block; tree cache: the block up to the end of I (values, columns,
+      // refs -- the codes are in the cached tree) plus the cached tree itself
+      const uint32_t bytes = a.trees ? align16(mn.off_refs + mn.n_pairs * mn.w_refs)
+                                     : align16(mn.off_offsets + (mn.n_rows + 1u) * mn.w_offsets);
+      if (mn.status == TOC_OK && bytes > 0) {
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nb), "r"(bytes) : "memory");
+        if (a.trees)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.trees + a.tree_off[bn]),
+                       "r"(batch_layout<kWide>(mn).tree)
+                       : "memory");
+      }
     }
     __syncthreads();
     if (need <= (uint32_t)a.batch_smem_budget)
