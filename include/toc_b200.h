@@ -122,10 +122,12 @@ int toc_linalg(const uint8_t* d_arena, const int64_t* d_block_off, const TocBloc
 
 /* ---- device tree cache (the reference's lazily built, reused CompressedMatrix.tree,
  * kernels.py:68-77) -----------------------------------------------------------------------
- * toc_tree_offsets (host): byte offsets (n_blocks + 1 entries) of each batch's tree prefix
- * (row offsets, derived-node bases, final codes, node table; 16-B aligned) given plan.wide.
- * toc_build_trees: build every prefix once into d_trees.  toc_linalg_trees: toc_linalg reading
- * the prefixes from the cache (one bulk copy per batch) instead of rebuilding them. */
+ * toc_tree_offsets (host): byte offsets (n_blocks + 1 entries) of each batch's cache entry given
+ * plan.wide: the tree prefix (row offsets, derived-node bases, final codes, node table), the
+ * unpacked first-layer pairs, and the pairs sorted by column with column segments (16-B aligned;
+ * layout: csrc/toc_batch.cuh CacheLayout).  toc_build_trees: build every entry once into d_trees.
+ * toc_linalg_trees: toc_linalg reading the entries (one bulk copy of the prefix per batch) instead
+ * of rebuilding the tree; v^T.A's output is then a fixed-order per-column sum. */
 int toc_tree_offsets(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t wide, int64_t* h_tree_off);
 int toc_build_trees(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
                     int64_t n_blocks, const TocPlan* plan, const int64_t* d_tree_off, uint8_t* d_trees,

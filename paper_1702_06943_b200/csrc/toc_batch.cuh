@@ -47,6 +47,58 @@ TOC_HD BatchLayout batch_layout(const TocBlockMeta& m) {
   return L;
 }
 
+// Device tree cache entry of one batch (toc_build_trees): the tree prefix above, then
+//   irec  (column, value ref) per first-layer pair, unpacked   -- P1 with coalesced loads
+//   prec  (pair id, value ref) sorted by (column, pair id)    } v^T.A's output as a fixed-order
+//   segs  (start in prec, column) per distinct column, + end  } segmented sum, no atomics
+//   info  n_segs (0xffffffff: not sorted, the atomic scatter is used)
+struct CacheLayout {
+  uint32_t tree, off_irec, off_prec, off_segs, off_info, total;
+};
+
+// A pair record (two small ids).  Narrow trees (< 65,536 nodes, n_cols <= 65,536: toc_plan) pack
+// both as u16 halves of one u32; wide ones use uint2.
+template <bool kWide>
+struct PairRec;
+
+template <>
+struct PairRec<false> {
+  using T = uint32_t;
+  TOC_HD static T make(uint32_t a, uint32_t b) { return a | (b << 16); }
+  TOC_D static uint32_t a(T r) { return r & 0xffffu; }
+  TOC_D static uint32_t b(T r) { return r >> 16; }
+  TOC_D static T none() { return 0u; }
+};
+
+template <>
+struct PairRec<true> {
+  using T = uint2;
+  TOC_HD static T make(uint32_t a, uint32_t b) { return T{a, b}; }
+  TOC_D static uint32_t a(T r) { return r.x; }
+  TOC_D static uint32_t b(T r) { return r.y; }
+  TOC_D static T none() { return make_uint2(0u, 0u); }
+};
+
+template <bool kWide>
+TOC_HD CacheLayout cache_layout(const TocBlockMeta& m) {
+  CacheLayout C;
+  const uint32_t nI = m.n_pairs, segs = (nI < m.n_cols ? nI : m.n_cols) + 1u;
+  C.tree = batch_layout<kWide>(m).tree;
+  uint32_t o = C.tree;
+  C.off_irec = o;
+  o += align16((uint32_t)sizeof(typename PairRec<kWide>::T) * nI);
+  C.off_prec = o;
+  o += align16((uint32_t)sizeof(typename PairRec<kWide>::T) * nI);
+  C.off_segs = o;
+  o += align16(8u * segs);
+  C.off_info = o;
+  o += 16u;
+  C.total = o;
+  return C;
+}
+
+constexpr uint32_t kNoSegs = 0xffffffffu;
+
 // ---- TMA bulk copy global -> shared with an mbarrier (sm_90+ async proxy) ------------------
 TOC_D uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
@@ -158,6 +210,14 @@ TOC_D void fix_add(uint32_t* acc, long long x) {
   const uint32_t old = atomicAdd(acc, xl);
   const uint32_t hi = xh + (old + xl < old ? 1u : 0u);
   if (hi) atomicAdd(acc + 1, hi);
+}
+
+// The same with the two words in separate arrays (lo[i], hi[i]): random adds then spread over
+// all 32 banks instead of the 16 even ones.
+TOC_D void fix_add_split(uint32_t* lo, uint32_t* hi, uint32_t i, uint32_t xl, uint32_t xh) {
+  const uint32_t old = atomicAdd(lo + i, xl);
+  const uint32_t h = xh + (old + xl < old ? 1u : 0u);
+  if (h) atomicAdd(hi + i, h);
 }
 
 TOC_D double fix_value(uint32_t lo, uint32_t hi, double inv_scale) {
@@ -396,6 +456,73 @@ struct Batch {
       const long long w = __double2ll_rn(weight(r) * g_scale);
       if (w == 0) continue;
       walk(r, lo, hi, db, j0, j1, [&](uint32_t i) { fix_add(tabw + 2 * i, w); });
+    }
+  }
+
+  // G with split words (fix_add_split): lo = tabw[0..nI], hi = tabw[nI+1..2nI+1]; tab zeroed.
+  template <typename Wt>
+  TOC_D void vecmat_rows_split(Wt&& weight, double g_scale) {
+    uint32_t* lo = tabw;
+    uint32_t* hi = tabw + (nI + 1);
+    for (uint32_t k = 0; k < passes; ++k) {
+      uint32_t r, lo_, hi_, db, j0, j1;
+      if (!segment(k, r, lo_, hi_, db, j0, j1)) break;
+      const long long w = __double2ll_rn(weight(r) * g_scale);
+      if (w == 0) continue;
+      const uint32_t xl = (uint32_t)w, xh = (uint32_t)((unsigned long long)w >> 32);
+      walk(r, lo_, hi_, db, j0, j1, [&](uint32_t i) { fix_add_split(lo, hi, i, xl, xh); });
+    }
+  }
+
+  // out[col] = sum over the column's pairs of value * G (split words), in (column, pair) order:
+  // 4 lanes per column, a fixed shuffle tree.  prec / segs from the tree cache (global, in L2):
+  // each lane issues its record loads as one batch, so a column costs one L2 round trip.
+  template <typename Out>
+  TOC_D void column_sums(const typename PairRec<kWide>::T* prec, const uint2* segs, uint32_t n_segs, double g_inv,
+                         Out&& out) const {
+    using R = PairRec<kWide>;
+    constexpr uint32_t U = 4;
+    const uint32_t* lo = tabw;
+    const uint32_t* hi = tabw + (nI + 1);
+    const uint32_t tid = threadIdx.x, quads = blockDim.x >> 2;
+    const uint32_t span = ((n_segs + quads - 1) / quads) * quads;
+    for (uint32_t s = tid >> 2; s < span; s += quads) {
+      double c = 0.0;
+      uint2 sg = make_uint2(0u, 0u);
+      if (s < n_segs) {
+        sg = __ldg(segs + s);
+        const uint32_t end = __ldg(&segs[s + 1].x);
+        for (uint32_t q0 = sg.x + (tid & 3u); q0 < end; q0 += 4 * U) {
+          typename R::T pr[U];
+#pragma unroll
+          for (uint32_t k = 0; k < U; ++k) pr[k] = q0 + 4 * k < end ? __ldg(prec + q0 + 4 * k) : R::none();
+#pragma unroll
+          for (uint32_t k = 0; k < U; ++k)
+            if (q0 + 4 * k < end) {
+              const uint32_t i = R::a(pr[k]) + 1;
+              c += uniq[R::b(pr[k])] * fix_value(lo[i], hi[i], g_inv);
+            }
+        }
+      }
+      c += __shfl_xor_sync(0xffffffffu, c, 1);
+      c += __shfl_xor_sync(0xffffffffu, c, 2);
+      if (s < n_segs && (tid & 3u) == 0) out(sg.y, c);
+    }
+  }
+
+  // P1 from the cache's unpacked pair records, interleaved over the threads (coalesced loads,
+  // conflict-free stores); up to 8 record loads in flight per thread.
+  TOC_D void compute_p1_records(const typename PairRec<kWide>::T* irec, const double* vec) {
+    using R = PairRec<kWide>;
+    constexpr uint32_t U = 8;
+    const uint32_t nth = blockDim.x;
+    for (uint32_t i0 = threadIdx.x; i0 < nI; i0 += U * nth) {
+      typename R::T r[U];
+#pragma unroll
+      for (uint32_t k = 0; k < U; ++k) r[k] = i0 + k * nth < nI ? __ldg(irec + i0 + k * nth) : R::none();
+#pragma unroll
+      for (uint32_t k = 0; k < U; ++k)
+        if (i0 + k * nth < nI) tab[i0 + k * nth + 1] = uniq[R::b(r[k])] * vec[R::a(r[k])];
     }
   }
 

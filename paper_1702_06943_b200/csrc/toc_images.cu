@@ -156,7 +156,7 @@ TOC_D void walk_flat(const Nodes<kWide>& N, uint32_t j0, uint32_t j1, V&& visit)
 
 // Fixed-point add (see fix_add, toc_batch.cuh) with the two words in separate arrays, so random
 // adds spread over all 32 banks, and no branch.
-TOC_D void fix_add_split(uint32_t* lo, uint32_t* hi, uint32_t i, uint32_t xl, uint32_t xh) {
+TOC_D void fix_add_pair(uint32_t* lo, uint32_t* hi, uint32_t i, uint32_t xl, uint32_t xh) {
   const uint32_t old = atomicAdd(lo + i, xl);
   atomicAdd(hi + i, xh + (old + xl < old ? 1u : 0u));
 }
@@ -577,7 +577,7 @@ __global__ void __launch_bounds__(1024, 1) epoch_cluster_kernel(ImageArgs a) {
       if (wr == 0) continue;
       const uint32_t xl = (uint32_t)wr, xh = (uint32_t)((unsigned long long)wr >> 32);
       walk_flat(N, split[(q << lg) + sub], split[(q << lg) + sub + 1],
-                [&](uint32_t i) { fix_add_split(glo, ghi, i, xl, xh); });
+                [&](uint32_t i) { fix_add_pair(glo, ghi, i, xl, xh); });
     }
     __syncthreads();
     trace_stamp(a, cta, t, 5);

@@ -28,7 +28,7 @@ struct LinalgArgs {
 };
 
 // One batch of the sweep.  `tables` points either into shared memory or into this CTA's slab.
-template <bool kWide, bool kVecSmem>
+template <bool kWide, bool kVecSmem, bool kCached>
 __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, const TocBlockMeta& m,
                                               uint8_t* tables, bool in_smem, const double* vec_s, uint32_t* acc_s,
                                               uint32_t* s_warp, double* s_red, uint64_t* mbar, uint32_t& phase) {
@@ -38,13 +38,23 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
   const int32_t ncol = a.n_cols;
   const uint8_t* blk = a.arena + a.block_off[b];
   Batch<kWide> B;
-  const bool cached = a.trees != nullptr;
+  constexpr bool cached = kCached;
+  using Rec = typename PairRec<kWide>::T;
+  const Rec* irec = nullptr;
+  const Rec* prec = nullptr;
+  const uint2* segs = nullptr;
+  uint32_t n_segs = kNoSegs;
   if (cached) {
     // Tree prefix from the device cache: one bulk copy into shared memory (or read in place
     // from global memory when the batch's tables do not fit), overlapped with the value work.
     uint8_t* tree = const_cast<uint8_t*>(a.trees + a.tree_off[b]);
+    const CacheLayout CL = cache_layout<kWide>(m);
+    irec = reinterpret_cast<const Rec*>(tree + CL.off_irec);
+    prec = reinterpret_cast<const Rec*>(tree + CL.off_prec);
+    segs = reinterpret_cast<const uint2*>(tree + CL.off_segs);
+    n_segs = __ldg(reinterpret_cast<const uint32_t*>(tree + CL.off_info));
     B.init(blk, m, tables, in_smem ? nullptr : tree);
-    if (in_smem && tid == 0) bulk_load(tables, tree, batch_layout<kWide>(m).tree, mbar);
+    if (in_smem && tid == 0) bulk_load(tables, tree, CL.tree, mbar);
     B.load_values();
   } else {
     B.init(blk, m, tables);
@@ -63,7 +73,7 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
   }
   if (cached) {
     __syncthreads();  // uniq complete
-    if (do_mv) B.template compute_p1<false>(kVecSmem ? vec_s : a.v);
+    if (do_mv) B.compute_p1_records(irec, kVecSmem ? vec_s : a.v);
     else B.zero_tab();
     if (in_smem) {
       mbar_wait(mbar, phase);
@@ -85,6 +95,21 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
       B.zero_tab();
       __syncthreads();
     }
+    if (n_segs != kNoSegs) {
+      // split-word G, then out[col] as a fixed-order segmented sum over the column-sorted pairs
+      B.vecmat_rows_split([&](uint32_t r) { return a.u[row_base + r]; }, g_scale);
+      __syncthreads();
+      double* o = a.O + b * (int64_t)ncol;
+      if (kVecSmem) {
+        double* os = reinterpret_cast<double*>(acc_s);  // zeroed above: absent columns stay 0
+        B.column_sums(prec, segs, n_segs, 1.0 / g_scale, [&](uint32_t c, double x) { os[c] = x; });
+        __syncthreads();
+        for (int32_t c = tid; c < ncol; c += nth) o[c] = os[c];
+      } else {  // O zeroed by the host
+        B.column_sums(prec, segs, n_segs, 1.0 / g_scale, [&](uint32_t c, double x) { o[c] = x; });
+      }
+      return;
+    }
     B.vecmat_rows([&](uint32_t r) { return a.u[row_base + r]; }, g_scale);
     __syncthreads();
     uint32_t* out = kVecSmem ? acc_s : reinterpret_cast<uint32_t*>(a.O + b * (int64_t)ncol);
@@ -101,7 +126,7 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
   }
 }
 
-template <bool kWide, bool kVecSmem>
+template <bool kWide, bool kVecSmem, bool kCached>
 __global__ void __launch_bounds__(1024, 1) linalg_kernel(LinalgArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint32_t* s_warp = reinterpret_cast<uint32_t*>(smem);  // 33 words
@@ -134,23 +159,23 @@ __global__ void __launch_bounds__(1024, 1) linalg_kernel(LinalgArgs a) {
       const int64_t bn = b + gridDim.x;
       const TocBlockMeta& mn = a.meta[bn];
       const uint8_t* nb = a.arena + a.block_off[bn];
-      // block-only: the whole block; tree cache: the block up to the end of I (values, columns,
-      // refs -- the codes are in the cached tree) plus the cached tree itself
-      const uint32_t bytes = a.trees ? align16(mn.off_refs + mn.n_pairs * mn.w_refs)
+      // block-only: the whole block; tree cache: the block's value index (columns, refs and
+      // codes are in the cache entry) plus the cache entry itself
+      const uint32_t bytes = kCached ? align16(mn.off_uniques + 8u * mn.n_uniques)
                                      : align16(mn.off_offsets + (mn.n_rows + 1u) * mn.w_offsets);
       if (mn.status == TOC_OK && bytes > 0) {
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(nb), "r"(bytes) : "memory");
-        if (a.trees)
+        if (kCached)
           asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.trees + a.tree_off[bn]),
-                       "r"(batch_layout<kWide>(mn).tree)
+                       "r"(cache_layout<kWide>(mn).total)
                        : "memory");
       }
     }
     __syncthreads();
     if (need <= (uint32_t)a.batch_smem_budget)
-      process_batch<kWide, kVecSmem>(a, b, m, p, true, vec_s, acc_s, s_warp, s_red, mbar, phase);
+      process_batch<kWide, kVecSmem, kCached>(a, b, m, p, true, vec_s, acc_s, s_warp, s_red, mbar, phase);
     else
-      process_batch<kWide, kVecSmem>(a, b, m, slab, false, vec_s, acc_s, s_warp, s_red, mbar, phase);
+      process_batch<kWide, kVecSmem, kCached>(a, b, m, slab, false, vec_s, acc_s, s_warp, s_red, mbar, phase);
   }
 }
 
@@ -176,9 +201,73 @@ __global__ void __launch_bounds__(1024, 1) build_trees_kernel(LinalgArgs a) {
     __syncthreads();
     B.resolve_keys();
     __syncthreads();
+    uint8_t* entry = const_cast<uint8_t*>(a.trees) + a.tree_off[b];
+    const CacheLayout CL = cache_layout<kWide>(m);
     const uint4* src = reinterpret_cast<const uint4*>(tables);
-    uint4* dst = reinterpret_cast<uint4*>(const_cast<uint8_t*>(a.trees) + a.tree_off[b]);
+    uint4* dst = reinterpret_cast<uint4*>(entry);
     for (uint32_t k = threadIdx.x; k < L.tree / 16u; k += blockDim.x) dst[k] = src[k];
+    // unpacked first-layer records, and the (column, pair)-sorted order with column segments
+    const uint8_t* blk = a.arena + a.block_off[b];
+    const uint32_t nI = m.n_pairs, tid = threadIdx.x, nth = blockDim.x;
+    using R = PairRec<kWide>;
+    typename R::T* irec = reinterpret_cast<typename R::T*>(entry + CL.off_irec);
+    uint32_t npad = 1;
+    while (npad < nI) npad <<= 1;
+    const bool sort_here = tables == p && 8ull * npad <= (uint64_t)a.batch_smem_budget;
+    __syncthreads();  // the tables have been copied out: their shared memory is free
+    unsigned long long* keys = reinterpret_cast<unsigned long long*>(p);
+    for (uint32_t i = tid; i < npad; i += nth) {
+      if (i < nI) {
+        const uint32_t c = ld_packed(blk + m.off_cols, i, m.w_cols), r = ld_packed(blk + m.off_refs, i, m.w_refs);
+        irec[i] = R::make(c, r);
+        if (sort_here) keys[i] = ((unsigned long long)c << 32) | i;
+      } else if (sort_here) {
+        keys[i] = ~0ull;
+      }
+    }
+    uint32_t* info = reinterpret_cast<uint32_t*>(entry + CL.off_info);
+    if (!sort_here) {
+      if (tid == 0) info[0] = kNoSegs;
+      continue;
+    }
+    for (uint32_t k = 2; k <= npad; k <<= 1) {  // bitonic sort of (column, pair id): stable order
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        __syncthreads();
+        for (uint32_t i = tid; i < npad; i += nth) {
+          const uint32_t ij = i ^ j;
+          if (ij > i) {
+            const unsigned long long x = keys[i], z = keys[ij];
+            if ((x > z) == ((i & k) == 0)) {
+              keys[i] = z;
+              keys[ij] = x;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+    typename R::T* prec = reinterpret_cast<typename R::T*>(entry + CL.off_prec);
+    for (uint32_t q = tid; q < nI; q += nth) {
+      const uint32_t i = (uint32_t)keys[q];
+      prec[q] = R::make(i, ld_packed(blk + m.off_refs, i, m.w_refs));
+    }
+    if (tid < 32) {  // column segments of the sorted order
+      const uint32_t lane = tid;
+      uint2* segs = reinterpret_cast<uint2*>(entry + CL.off_segs);
+      uint32_t carry = 0;
+      for (uint32_t base = 0; base < nI; base += 32) {
+        const uint32_t q = base + lane;
+        const uint32_t c = q < nI ? (uint32_t)(keys[q] >> 32) : 0u;
+        const bool f = q < nI && (q == 0 || (uint32_t)(keys[q - 1] >> 32) != c);
+        const uint32_t bal = __ballot_sync(0xffffffffu, f);
+        if (f) segs[carry + __popc(bal & ((1u << lane) - 1u))] = make_uint2(q, c);
+        carry += __popc(bal);
+      }
+      if (lane == 0) {
+        segs[carry] = make_uint2(nI, 0u);
+        info[0] = carry;
+      }
+    }
   }
 }
 
@@ -216,17 +305,22 @@ const DevProps& dev_props() {
   return p;
 }
 
-template <bool W, bool V>
-cudaError_t launch(const toc::LinalgArgs& a, const TocPlan& plan, cudaStream_t s) {
+template <bool W, bool V, bool C>
+cudaError_t launch_mode(const toc::LinalgArgs& a, const TocPlan& plan, cudaStream_t s) {
   static int configured = -1;
   if (configured < plan.smem_bytes) {
-    cudaError_t e = cudaFuncSetAttribute(toc::linalg_kernel<W, V>,
+    cudaError_t e = cudaFuncSetAttribute(toc::linalg_kernel<W, V, C>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, plan.smem_bytes);
     if (e != cudaSuccess) return e;
     configured = plan.smem_bytes;
   }
-  toc::linalg_kernel<W, V><<<plan.ctas, plan.threads, plan.smem_bytes, s>>>(a);
+  toc::linalg_kernel<W, V, C><<<plan.ctas, plan.threads, plan.smem_bytes, s>>>(a);
   return cudaGetLastError();
+}
+
+template <bool W, bool V>
+cudaError_t launch(const toc::LinalgArgs& a, const TocPlan& plan, cudaStream_t s) {
+  return a.trees ? launch_mode<W, V, true>(a, plan, s) : launch_mode<W, V, false>(a, plan, s);
 }
 
 }  // namespace
@@ -244,7 +338,7 @@ extern "C" int toc_plan(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t ki
     if (T > max_T) max_T = T;
     if ((int32_t)m.n_rows > plan->max_rows) plan->max_rows = (int32_t)m.n_rows;
   }
-  plan->wide = max_T > 65536ull;
+  plan->wide = max_T > 65536ull || n_cols > 65536;  // narrow: every id fits u16 (PairRec)
   plan->n_cols = n_cols;
   uint32_t max_need = 0;
   for (int64_t b = 0; b < n_blocks; b++) {
@@ -294,7 +388,7 @@ extern "C" int toc_tree_offsets(const TocBlockMeta* h_meta, int64_t n_blocks, in
   int64_t o = 0;
   for (int64_t b = 0; b < n_blocks; ++b) {
     h_tree_off[b] = o;
-    o += wide ? toc::batch_layout<true>(h_meta[b]).tree : toc::batch_layout<false>(h_meta[b]).tree;
+    o += wide ? toc::cache_layout<true>(h_meta[b]).total : toc::cache_layout<false>(h_meta[b]).total;
   }
   h_tree_off[n_blocks] = o;
   return TOC_OK;
