@@ -192,7 +192,7 @@ TOC_D void scan_derived_base(const uint32_t* rowoff, uint32_t* dbase, uint32_t n
 
 // Lanes per row: the largest power of two <= min(32, threads / rows).  Each thread then owns
 // one contiguous segment of one row, so the code stream is walked sequentially per thread.
-TOC_D uint32_t seg_lanes(uint32_t n, uint32_t nthreads) {
+TOC_HD uint32_t seg_lanes(uint32_t n, uint32_t nthreads) {
   uint32_t s = 1;
   while (s < 32 && 2 * s * (n ? n : 1) <= nthreads) s <<= 1;
   return s;
@@ -213,11 +213,11 @@ TOC_D void fix_add(uint32_t* acc, long long x) {
 }
 
 // The same with the two words in separate arrays (lo[i], hi[i]): random adds then spread over
-// all 32 banks instead of the 16 even ones.
+// all 32 banks instead of the 16 even ones.  No branch: at the scales used the high word of an
+// addend is almost never zero, so skipping its add only costs divergence handling.
 TOC_D void fix_add_split(uint32_t* lo, uint32_t* hi, uint32_t i, uint32_t xl, uint32_t xh) {
   const uint32_t old = atomicAdd(lo + i, xl);
-  const uint32_t h = xh + (old + xl < old ? 1u : 0u);
-  if (h) atomicAdd(hi + i, h);
+  atomicAdd(hi + i, xh + (old + xl < old ? 1u : 0u));
 }
 
 TOC_D double fix_value(uint32_t lo, uint32_t hi, double inv_scale) {
@@ -245,7 +245,7 @@ struct Batch {
   double* tab;     // P1 (matvec) or G (vecmat, fixed point), index = first-layer id
   uint32_t* tabw;  // tab as words
   PK<kWide> pk;
-  uint32_t n, nI, S, RP, passes, sub, p0, p1;
+  uint32_t n, nI, S, lgS, RP, passes, sub, p0, p1;
   double vmax;     // max |value| over the value index (this thread's part until reduced)
 
   // tables: shared (or slab) base of the whole layout; tree: where the tree prefix lives (the same
@@ -287,6 +287,7 @@ struct Batch {
     nI = m.n_pairs;
     const uint32_t nth = blockDim.x, tid = threadIdx.x;
     S = seg_lanes(n, nth);
+    lgS = __ffs(S) - 1;
     RP = nth / S;
     passes = (n + RP - 1) / RP;
     sub = tid % S;
@@ -298,14 +299,14 @@ struct Batch {
   // Row r's code range and this thread's segment of it.
   TOC_D bool segment(uint32_t k, uint32_t& r, uint32_t& lo, uint32_t& hi, uint32_t& db, uint32_t& j0,
                      uint32_t& j1) const {
-    r = threadIdx.x / S + k * RP;
+    r = (threadIdx.x >> lgS) + k * RP;
     if (r >= n) return false;
     lo = rowoff[r];
     hi = rowoff[r + 1];
     db = dbase[r];
     const uint32_t len = hi - lo;
-    j0 = lo + (len * sub) / S;
-    j1 = lo + (len * (sub + 1)) / S;
+    j0 = lo + ((len * sub) >> lgS);
+    j1 = lo + ((len * (sub + 1)) >> lgS);
     return true;
   }
 

@@ -63,16 +63,27 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
     for (int32_t c = tid; c < 2 * ncol; c += nth) acc_s[c] = 0u;
   if (!cached) B.load_index(s_warp);
   double g_scale = 1.0, o_scale = 1.0;
-  if (do_vm) {  // a-priori bounds of every partial sum (see fix_add): sum |u| and max |value|
+  if (do_vm && !cached) {  // a-priori bounds of every partial sum (see fix_add): sum |u| and max |value|
     double su = 0.0;
     for (uint32_t r = tid; r < B.n; r += nth) su += fabs(a.u[row_base + r]);
     su = block_sum(su, s_red);
-    const double mv = block_max_d(B.vmax, s_red);
     g_scale = fix_scale(su);
-    o_scale = fix_scale(su * mv);
+    o_scale = fix_scale(su * block_max_d(B.vmax, s_red));
   }
   if (cached) {
-    __syncthreads();  // uniq complete
+    if (do_vm) {  // sum |u| as warp partials, read after the barrier below (no extra barrier)
+      double su = 0.0;
+      for (uint32_t r = tid; r < B.n; r += nth) su += fabs(a.u[row_base + r]);
+      su = warp_sum(su);
+      if ((tid & 31) == 0) s_red[tid >> 5] = su;
+    }
+    __syncthreads();  // uniq and the partials complete
+    if (do_vm) {
+      double su = 0.0;
+      for (uint32_t w = 0; w < (nth >> 5); ++w) su += s_red[w];
+      g_scale = fix_scale(su);
+      if (n_segs == kNoSegs) o_scale = fix_scale(su * block_max_d(B.vmax, s_red));  // fixed-point scatter only
+    }
     if (do_mv) B.compute_p1_records(irec, kVecSmem ? vec_s : a.v);
     else B.zero_tab();
     if (in_smem) {
