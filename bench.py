@@ -305,8 +305,9 @@ def main():
             "matvec_rows_per_s": world * rows_per_step / (np.mean(mv_t) / 1e3),
             "vecmat_rows_per_s": world * rows_per_step / (np.mean(vm_t) / 1e3),
             "tree_cache": {"used_for_value": True, "bytes_per_gpu": arena.tree_bytes, "build_seconds": t_trees,
-                           "note": "per-batch decode-tree prefix built once (reference caches C' too, "
-                                   "kernels.py:68-77); each launch reads it plus the TOC1 I-section"},
+                           "note": "per-batch cache entry built once (the reference caches C' too, "
+                                   "kernels.py:68-77): decode-tree prefix plus unpacked and column-sorted "
+                                   "pair records; each launch reads it plus the TOC1 value index"},
             "block_only": {"ms_per_step": float(np.mean(bo_t)),
                            "rows_per_s": world * rows_per_step / (np.mean(bo_t) / 1e3),
                            "roofline_frac": alg / (np.mean(bo_t) / 1e3) / 1e9 / peak, "traffic": bo_traffic,
