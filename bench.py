@@ -352,7 +352,8 @@ def run_mgd(cfg: int, rank: int, world: int, cpu_sample: bool):
         for _ in range(epochs):
             secs.append(tr.epoch())
             risks.append(tr.risk())
-        modes = {"images": "one single-CTA launch per epoch over cached step images (built once per run)",
+        modes = {"images": f"one launch per epoch: a {tr.cluster}-CTA thread-block cluster over cached step images "
+                           "(built once per run, like the reference's cached trees)",
                  "relay": "one cooperative relay launch per epoch (tables rebuilt per step)"}
         out.update({"steps_per_epoch": int(batches.arena.n_blocks), "epoch_seconds": secs, "risk_per_epoch": risks,
                     "mode": modes[tr.mode], "image_build_seconds": tr.image_build_seconds,

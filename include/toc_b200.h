@@ -276,6 +276,24 @@ int toc_glm_epoch_images_traced(const uint8_t* d_images, const int64_t* d_image_
                                 int32_t n_cols, int32_t cluster, int32_t loss, double lr, double* d_w,
                                 long long* d_trace, void* stream);
 
+/* ---- decode (codec.py:262-292 node_sequence / decode; cli.py:194-221 verify) -----------------
+ * Two passes with a plan from toc_plan(kind = TOC_MATVEC) and its scratch: toc_decode_counts writes
+ * each row's pair count at d_row_nnz[row_base[b] + r]; the caller scans them into d_row_ptr
+ * (total_rows + 1 entries, row_ptr[0] = 0); toc_decode_rows writes every row's (column, value)
+ * pairs in row order, values bit for bit from the block's value index. */
+int toc_decode_counts(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+                      const int64_t* d_row_base, int64_t n_blocks, const TocPlan* plan, int64_t* d_row_nnz,
+                      void* d_scratch, void* stream);
+int toc_decode_rows(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+                    const int64_t* d_row_base, int64_t n_blocks, const TocPlan* plan, const int64_t* d_row_ptr,
+                    int32_t* d_cols, double* d_vals, void* d_scratch, void* stream);
+/* The reference's DecodeTree arrays (build_prefix_tree, codec.py:194-259) for every block, node 0
+ * the root (-1 / 0.0 sentinels); block b's T_b = 1 + |I| + derived nodes start at d_tree_base[b]. */
+int toc_tree_arrays(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+                    int64_t n_blocks, const TocPlan* plan, const int64_t* d_tree_base, int32_t* d_parent,
+                    int32_t* d_column, double* d_value, int32_t* d_first_col, double* d_first_val,
+                    void* d_scratch, void* stream);
+
 /* ---- version / self-description ---------------------------------------------------------- */
 const char* toc_version(void);
 int toc_device_info(int32_t* sm_count, int32_t* smem_optin, int64_t* l2_bytes);

@@ -69,6 +69,9 @@ def lib():
     L.toc_linalg_trees.argtypes = [P, P, P, P, I64, ctypes.POINTER(TocPlan), I32, P, P, P, P, P, P, P, P]
     L.toc_matmat.argtypes = [P, P, P, P, P, I64, I32, I32, I32, P, P, P, I64, P]
     L.toc_matmat_scratch.argtypes = [P, I64, I32, I32, I32, ctypes.POINTER(ctypes.c_int64)]
+    L.toc_decode_counts.argtypes = [P, P, P, P, I64, ctypes.POINTER(TocPlan), P, P, P]
+    L.toc_decode_rows.argtypes = [P, P, P, P, I64, ctypes.POINTER(TocPlan), P, P, P, P, P]
+    L.toc_tree_arrays.argtypes = [P, P, P, I64, ctypes.POINTER(TocPlan), P, P, P, P, P, P, P, P]
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype or ctypes.c_int
     if L.toc_sizeof_meta() != META_DTYPE.itemsize or L.toc_sizeof_plan() != ctypes.sizeof(TocPlan):

@@ -129,6 +129,64 @@ class BlockArena:
             self._scratch = self.torch.empty(plan.scratch_bytes, dtype=self.torch.uint8, device=self.data.device)
         return self._scratch
 
+    def decode(self):
+        """All rows back as CSR on the device: (row_ptr int64 [n_rows_total + 1], cols int32, vals
+        float64), batch b's rows at row_base[b] (codec.py:274-292, bit for bit)."""
+        self.raise_format_errors()
+        self.raise_corrupt()
+        torch = self.torch
+        dev = self.data.device
+        plan = self.plan(N.TOC_MATVEC)
+        scratch = self._scratch_for(plan)
+        sp = scratch.data_ptr() if scratch is not None else None
+        L = N.lib()
+        nnz = torch.zeros(max(self.n_rows_total, 1), dtype=torch.int64, device=dev)
+        N.check(L.toc_decode_counts(self.data.data_ptr(), self.block_off_d.data_ptr(), self.meta_d.data_ptr(),
+                                    self.row_base_d.data_ptr(), self.n_blocks, ctypes.byref(plan), nnz.data_ptr(), sp,
+                                    N.stream_handle()), "toc_decode_counts")
+        row_ptr = torch.zeros(self.n_rows_total + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(nnz[: self.n_rows_total], 0, out=row_ptr[1:])
+        total = int(row_ptr[-1].item())
+        cols = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+        vals = torch.empty(max(total, 1), dtype=torch.float64, device=dev)
+        N.check(L.toc_decode_rows(self.data.data_ptr(), self.block_off_d.data_ptr(), self.meta_d.data_ptr(),
+                                  self.row_base_d.data_ptr(), self.n_blocks, ctypes.byref(plan), row_ptr.data_ptr(),
+                                  cols.data_ptr(), vals.data_ptr(), sp, N.stream_handle()), "toc_decode_rows")
+        return row_ptr, cols[:total], vals[:total]
+
+    def decode_trees(self) -> list:
+        """Every block's DecodeTree (reference codec.py:194-259) built on the device."""
+        from .codec import DecodeTree
+
+        self.raise_format_errors()
+        self.raise_corrupt()
+        torch = self.torch
+        dev = self.data.device
+        plan = self.plan(N.TOC_MATVEC)
+        scratch = self._scratch_for(plan)
+        T = self.tree_lengths()
+        base = np.concatenate([[0], np.cumsum(T)]).astype(np.int64)
+        total = int(base[-1])
+        base_d = torch.from_numpy(base[:-1].copy()).to(dev)
+        par = torch.empty(max(total, 1), dtype=torch.int32, device=dev)
+        col = torch.empty_like(par)
+        fcol = torch.empty_like(par)
+        val = torch.empty(max(total, 1), dtype=torch.float64, device=dev)
+        fval = torch.empty_like(val)
+        N.check(N.lib().toc_tree_arrays(self.data.data_ptr(), self.block_off_d.data_ptr(), self.meta_d.data_ptr(),
+                                        self.n_blocks, ctypes.byref(plan), base_d.data_ptr(), par.data_ptr(),
+                                        col.data_ptr(), val.data_ptr(), fcol.data_ptr(), fval.data_ptr(),
+                                        scratch.data_ptr() if scratch is not None else None, N.stream_handle()),
+                "toc_tree_arrays")
+        h = [x.cpu().numpy() for x in (par, col, val, fcol, fval)]
+        out = []
+        for b in range(self.n_blocks):
+            lo, hi = int(base[b]), int(base[b + 1])
+            out.append(DecodeTree(n_cols=int(self.meta["n_cols"][b]), parent=h[0][lo:hi].tolist(),
+                                  column=h[1][lo:hi].tolist(), value=h[2][lo:hi].tolist(),
+                                  first_col=h[3][lo:hi].tolist(), first_val=h[4][lo:hi].tolist()))
+        return out
+
     def build_trees(self):
         """Build the device tree cache: each batch's tree prefix (row offsets, derived-node bases,
         final codes, node table), once -- the device counterpart of the reference's lazily built,

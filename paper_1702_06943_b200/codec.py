@@ -200,3 +200,53 @@ def encode(s: SparseRowMatrix) -> LogicalEncoding:
     cdl = cd.tolist()
     rows = [cdl[of[i] : of[i + 1]] for i in range(s.n_rows)]
     return LogicalEncoding(n_rows=s.n_rows, n_cols=s.n_cols, pairs=pairs, rows=rows)
+
+
+NOT_FOUND = -1  # reference codec.py:30
+
+
+@dataclass
+class DecodeTree:
+    """Prefix tree rebuilt from a logical encoding (reference codec.py:194-212): node 0 is the root,
+    nodes 1..len(pairs) mirror I, later nodes are derived one per non-final code in scan order;
+    first_col / first_val hold each node's first pair.  Built on the device (toc_tree_arrays)."""
+
+    n_cols: int
+    parent: list
+    column: list
+    value: list
+    first_col: list
+    first_val: list
+
+    def __len__(self) -> int:
+        return len(self.parent)
+
+
+def build_prefix_tree(enc: LogicalEncoding) -> DecodeTree:
+    """Rebuild C' (reference codec.py:215-259) on the device.  Raises CorruptEncodingError when a
+    code references a node that does not exist yet at its point of use."""
+    from .arena import BlockArena
+    from .physical import serialize_block
+
+    return BlockArena.from_bytes([serialize_block(enc)]).decode_trees()[0]
+
+
+def node_sequence(tree: DecodeTree, code: int) -> list:
+    """The (column, value) pairs a tree node stands for, in row order (reference codec.py:262-271)."""
+    if not 1 <= code < len(tree):
+        raise ValueError(f"code {code} out of range for tree of length {len(tree)}")
+    pairs = []
+    while code != 0:
+        pairs.append((tree.column[code], tree.value[code]))
+        code = tree.parent[code]
+    pairs.reverse()
+    return pairs
+
+
+def decode(enc: LogicalEncoding) -> SparseRowMatrix:
+    """Invert encode exactly, values bit for bit (reference codec.py:274-292), on the device."""
+    from .arena import BlockArena
+    from .physical import serialize_block
+
+    rp, c, v = BlockArena.from_bytes([serialize_block(enc)]).decode()
+    return SparseRowMatrix.from_csr(enc.n_cols, rp.cpu().numpy(), c.cpu().numpy(), v.cpu().numpy(), check=False)

@@ -86,18 +86,18 @@ class CompressedMatrix:
 
     @property
     def tree(self):
+        """The reference's DecodeTree, built on the device once, under a lock (kernels.py:68-77)."""
         if self._tree is None:
+            arena = self.arena  # takes the lock itself when it has to serialize
             with self._lock:
                 if self._tree is None:
-                    from .codec_tree import build_prefix_tree
-
-                    self._tree = build_prefix_tree(self._enc)
+                    self._tree = arena.decode_trees()[0]
         return self._tree
 
     def decode(self) -> SparseRowMatrix:
-        from .codec_tree import decode
-
-        return decode(self._enc)
+        """Rows back bit for bit (kernels.py:79-80 -> codec.decode), decoded on the device."""
+        rp, c, v = self.arena.decode()
+        return SparseRowMatrix.from_csr(self.n_cols, rp.cpu().numpy(), c.cpu().numpy(), v.cpu().numpy(), check=False)
 
     def _charge(self, counter: OpCounter | None, width: int) -> None:
         if counter is not None:
