@@ -154,6 +154,25 @@ class BlockArena:
                                   cols.data_ptr(), vals.data_ptr(), sp, N.stream_handle()), "toc_decode_rows")
         return row_ptr, cols[:total], vals[:total]
 
+    def scalar_multiply(self, c: float) -> "BlockArena":
+        """Every block's values scaled by c, rebuilt on the device (kernels.py:87-102 per block)."""
+        import math
+
+        from .physical import rewrite_arena
+
+        c = float(c)
+        if not math.isfinite(c):
+            raise ValueError("scale factor must be finite")
+        return rewrite_arena(self, fn=lambda x: x * c)
+
+    def elementwise_power(self, p: float) -> "BlockArena":
+        """Every block's values raised to p on the device (kernels.py:105-112 per block).  torch.pow:
+        exact for p = 1, 2 and 0.5 (square, sqrt); otherwise within CUDA pow's 2 ulp of math.pow."""
+        from .physical import rewrite_arena
+
+        p = float(p)
+        return rewrite_arena(self, fn=lambda x: self.torch.pow(x, p))
+
     def decode_trees(self) -> list:
         """Every block's DecodeTree (reference codec.py:194-259) built on the device."""
         from .codec import DecodeTree

@@ -13,6 +13,7 @@ one call = upload + validate + A.v and v^T.A for every batch + download.
 from __future__ import annotations
 
 import ctypes
+import math
 import threading
 from dataclasses import dataclass
 
@@ -111,6 +112,48 @@ class CompressedMatrix:
     def __repr__(self):
         e = self._enc
         return f"CompressedMatrix({e.n_rows}x{e.n_cols}, I={len(e.pairs)}, codes={e.total_codes})"
+
+
+def scalar_multiply(a: CompressedMatrix, c: float) -> CompressedMatrix:
+    """Scale every stored value; code rows are shared, not copied (kernels.py:87-102).  The new
+    block is rebuilt on the device (value index + repack, physical.rewrite_arena); no tree is
+    built.  Scaling by zero keeps the entries as explicit zeros."""
+    c = float(c)
+    if not math.isfinite(c):
+        raise ValueError("scale factor must be finite")
+    e = a.encoding
+    enc = LogicalEncoding(n_rows=e.n_rows, n_cols=e.n_cols, pairs=[(col, c * val) for col, val in e.pairs],
+                          rows=e.rows)
+    from .physical import rewrite_arena
+
+    return CompressedMatrix(enc, _arena=rewrite_arena(a.arena, fn=lambda x: x * c))
+
+
+def elementwise_power(a: CompressedMatrix, p: float) -> CompressedMatrix:
+    """Raise every stored value to the power p (kernels.py:105-112).  The values are math.pow's,
+    exactly the reference's; the block is rebuilt on the device."""
+    p = float(p)
+    e = a.encoding
+    enc = LogicalEncoding(n_rows=e.n_rows, n_cols=e.n_cols, pairs=[(col, math.pow(val, p)) for col, val in e.pairs],
+                          rows=e.rows)
+    from .physical import rewrite_arena
+
+    return CompressedMatrix(enc, _arena=rewrite_arena(a.arena, values=[v for _, v in enc.pairs]))
+
+
+def scalar_add(a: CompressedMatrix, c: float) -> DenseMatrix:
+    """A + c as a dense matrix (kernels.py:237-247): adding to the implicit zeros densifies, so this
+    decodes -- on the device -- and adds there."""
+    c = float(c)
+    if not math.isfinite(c):
+        raise ValueError("addend must be finite")
+    import torch
+
+    rp, cols, vals = a.arena.decode()
+    out = torch.zeros((a.n_rows, a.n_cols), dtype=torch.float64, device=vals.device)
+    r = torch.repeat_interleave(torch.arange(a.n_rows, device=vals.device), rp[1:] - rp[:-1])
+    out[r, cols.long()] = vals
+    return DenseMatrix((out + c).cpu().numpy())
 
 
 def _dev(x: np.ndarray):

@@ -148,3 +148,71 @@ def deserialize_block(data: bytes) -> LogicalEncoding:
     cdl = cd.tolist()
     rows = [cdl[of[i] : of[i + 1]] for i in range(int(rec["n_rows"]))]
     return LogicalEncoding(n_rows=int(rec["n_rows"]), n_cols=int(rec["n_cols"]), pairs=pairs, rows=rows)
+
+
+def rewrite_arena(arena, fn=None, values=None):
+    """Every block with its pair values replaced, the value index rebuilt (physical.py:88-101) and
+    the blocks repacked (physical.py:110-130) -- all on the device; codes, columns and row
+    offsets are carried over unchanged.  The sparse-safe rewrites (kernels.py:87-112) over a whole
+    arena.  ``fn`` maps the float64 tensor of all pair values (pair order, block by block) on the
+    device; or ``values`` gives them directly.  Raises ValueError like LogicalEncoding
+    (codec.py:151-162) when a new value is not finite."""
+    from .arena import BlockArena
+
+    torch = arena.torch
+    L = _bind()
+    arena.raise_format_errors()
+    m = arena.meta
+    B = arena.n_blocks
+    nI = m["n_pairs"].astype(np.int64)
+    C = m["n_codes"].astype(np.int64)
+    n = m["n_rows"].astype(np.int64)
+    cap = np.maximum(np.maximum(nI, C), 1)
+    eb = np.concatenate([[0], np.cumsum(cap)]).astype(np.int64)
+    br = np.concatenate([[0], np.cumsum(n)]).astype(np.int64)
+    ob = (br[:-1] + np.arange(B)).astype(np.int64)
+    dev = arena.data.device
+    d = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in dict(eb=eb, br=br, ob=ob).items()}
+    E = int(eb[-1])
+    I_cols = torch.zeros(E, dtype=torch.int32, device=dev)
+    I_vals = torch.zeros(E, dtype=torch.float64, device=dev)
+    codes = torch.zeros(E, dtype=torch.int32, device=dev)
+    offsets = torch.zeros(int(br[-1]) + B, dtype=torch.int32, device=dev)
+    s = N.stream_handle()
+    N.check(L.toc_unpack_blocks(arena.data.data_ptr(), arena.block_off_d.data_ptr(), arena.meta_d.data_ptr(), B,
+                                d["eb"].data_ptr(), d["eb"].data_ptr(), d["ob"].data_ptr(), I_cols.data_ptr(),
+                                I_vals.data_ptr(), codes.data_ptr(), offsets.data_ptr(), s), "toc_unpack_blocks")
+    # pair slots of every block, in pair order
+    slot = (torch.arange(int(nI.sum()), device=dev, dtype=torch.int64)
+            - torch.from_numpy(np.repeat(np.concatenate([[0], np.cumsum(nI)[:-1]]) - eb[:-1], nI)).to(dev))
+    old = I_vals[slot]
+    new = fn(old) if fn is not None else torch.as_tensor(values, dtype=torch.float64, device=dev)
+    if new.shape != old.shape:
+        raise ValueError(f"{new.numel()} new values for {old.numel()} pairs")
+    bad = torch.nonzero(~torch.isfinite(new))
+    if bad.numel():
+        col = int(I_cols[slot[int(bad[0, 0])]].item())
+        raise ValueError(f"pair value for column {col} is not finite")
+    I_vals[slot] = new
+    sizes = TocEncodeSizes()
+    N.check(L.toc_encode_sizes(B, eb.ctypes.data_as(ctypes.c_void_p), ctypes.byref(sizes)), "toc_encode_sizes")
+    info = np.zeros(B, INFO_DTYPE)
+    info["n_rows"], info["n_cols"], info["n_pairs"], info["n_codes"] = n, m["n_cols"], nI, C
+    info_d = torch.from_numpy(info.view(np.uint8)).to(dev)
+    work = torch.empty(max(sizes.work_bytes, 16), dtype=torch.uint8, device=dev)
+    refs = torch.empty(E, dtype=torch.int32, device=dev)
+    uniques = torch.empty(E, dtype=torch.float64, device=dev)
+    N.check(L.toc_serialize_sizes(B, d["br"].data_ptr(), d["eb"].data_ptr(), I_cols.data_ptr(), I_vals.data_ptr(),
+                                  codes.data_ptr(), offsets.data_ptr(), ctypes.byref(sizes), work.data_ptr(),
+                                  refs.data_ptr(), uniques.data_ptr(), info_d.data_ptr(), s), "toc_serialize_sizes")
+    info_h = np.frombuffer(info_d.cpu().numpy().tobytes(), INFO_DTYPE)
+    blen = info_h["block_bytes"].astype(np.int64)
+    padded = (blen + 15) & ~15
+    boff = np.concatenate([[0], np.cumsum(padded)[:-1]]).astype(np.int64)
+    total = int(padded.sum())
+    data = torch.zeros(total + 16, dtype=torch.uint8, device=dev)  # +16: tail padding (arena.py)
+    boff_d = torch.from_numpy(boff).to(dev)
+    N.check(L.toc_pack_blocks(B, d["br"].data_ptr(), d["eb"].data_ptr(), I_cols.data_ptr(), refs.data_ptr(),
+                              uniques.data_ptr(), codes.data_ptr(), offsets.data_ptr(), info_d.data_ptr(),
+                              boff_d.data_ptr(), data.data_ptr(), s), "toc_pack_blocks")
+    return BlockArena(data, boff, blen)

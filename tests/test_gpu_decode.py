@@ -156,3 +156,103 @@ def test_compressed_matrix_tree_is_lazy_and_once(oracle):
     for th in threads:
         th.join()
     assert len(seen) == 8 and all(t is seen[0] for t in seen)
+
+
+# ---- sparse-safe rewrites (reference kernels.py:87-112, tests/test_kernels.py:98-130) -------------
+def _toy():
+    from paper_1702_06943_b200.kernels import CompressedMatrix
+    from paper_1702_06943_b200.matrix import SparseRowMatrix
+
+    return CompressedMatrix.from_sparse(SparseRowMatrix(5, TOY_ROWS))
+
+
+def test_scalar_multiply_scales_values():
+    from paper_1702_06943_b200.kernels import scalar_multiply
+    from paper_1702_06943_b200.matrix import SparseRowMatrix, sparse_to_dense
+
+    cm = _toy()
+    scaled = scalar_multiply(cm, 2.5)
+    assert np.array_equal(sparse_to_dense(scaled.decode()).values, sparse_to_dense(SparseRowMatrix(5, TOY_ROWS)).values * 2.5)
+    assert scaled.encoding.rows is cm.encoding.rows
+    assert cm._tree is None and scaled._tree is None
+
+
+def test_rewrites_match_host_serialization(oracle):
+    """The device-rebuilt block equals serialize_block of the rewritten logical encoding, byte for byte
+    (value index rebuilt: scaling by 0 collapses every unique into one)."""
+    from paper_1702_06943_b200.kernels import CompressedMatrix, elementwise_power, scalar_multiply
+    from paper_1702_06943_b200.matrix import SparseRowMatrix
+
+    rng = np.random.default_rng(11)
+    rows = random_alphabet_rows(rng, 120, 30, 0.5)
+    cm = CompressedMatrix.from_sparse(SparseRowMatrix(30, rows))
+    from paper_1702_06943_b200.physical import serialize_block
+
+    for out in (scalar_multiply(cm, -1.75), scalar_multiply(cm, 0.0), elementwise_power(cm, 2.0),
+                elementwise_power(cm, 3.0), elementwise_power(cm, -1.0)):
+        enc = out.encoding
+        oenc = oracle.Encoding(enc.n_rows, 30, np.array([c for c, _ in enc.pairs], np.int32),
+                               np.array([v for _, v in enc.pairs], np.float64),
+                               np.array([c for r in enc.rows for c in r], np.uint32),
+                               np.concatenate([[0], np.cumsum([len(r) for r in enc.rows])]).astype(np.int64))
+        got = bytes(out.arena.data[: int(out.arena.block_len[0])].cpu().numpy())
+        assert got == oracle.serialize(oenc)
+        assert got == serialize_block(enc)
+        assert out._tree is None
+
+
+def test_scale_by_zero_keeps_structure():
+    from paper_1702_06943_b200.kernels import scalar_multiply
+
+    cm = _toy()
+    zeroed = scalar_multiply(cm, 0.0)
+    assert all(v == 0.0 for _, v in zeroed.encoding.pairs)
+    got = zeroed.decode()
+    assert [[c for c, _ in r] for r in got.rows] == [[c for c, _ in r] for r in TOY_ROWS]
+    assert all(v == 0.0 for r in got.rows for _, v in r)
+
+
+def test_rewrite_rejects_non_finite():
+    from paper_1702_06943_b200.kernels import elementwise_power, scalar_multiply
+
+    cm = _toy()
+    with pytest.raises(ValueError):
+        scalar_multiply(cm, float("inf"))
+    with pytest.raises(ValueError):
+        scalar_multiply(cm, 1e308)  # overflows to inf
+    neg = scalar_multiply(cm, -1.0)
+    with pytest.raises(ValueError):
+        elementwise_power(neg, 0.5)  # nan
+
+
+def test_arena_rewrites_many_batches(oracle):
+    """Arena-level rewrites (device map + rebuild) over config-2 batches: decode equals the mapped
+    input bit for bit for multiply; within 2 ulp for pow."""
+    from paper_1702_06943_b200 import synth
+    from paper_1702_06943_b200.codec import compress_csr
+
+    dense = [synth.cfg2_batch_dense(1, b) for b in range(4)]
+    parts = [synth.dense_to_csr(d) for d in dense]
+    rp = np.concatenate([[0], np.cumsum(np.concatenate([np.diff(p[0]) for p in parts]))]).astype(np.int64)
+    c = np.concatenate([p[1] for p in parts])
+    v = np.concatenate([p[2] for p in parts])
+    arena = compress_csr(784, rp, c, v, np.arange(0, 1001, 250, dtype=np.int64))
+    s = arena.scalar_multiply(-3.25)
+    rp2, c2, v2 = s.decode()
+    assert np.array_equal(c2.cpu().numpy(), c) and np.array_equal(bits(v2.cpu().numpy()), bits(v * -3.25))
+    pw = arena.elementwise_power(2.0)
+    _, _, v3 = pw.decode()
+    assert np.array_equal(bits(v3.cpu().numpy()), bits(v * v))
+    pw3 = arena.elementwise_power(1.5)
+    _, _, v4 = pw3.decode()
+    assert np.allclose(v4.cpu().numpy(), v ** 1.5, rtol=5e-16, atol=0)
+
+
+def test_scalar_add_densifies():
+    from paper_1702_06943_b200.kernels import scalar_add
+    from paper_1702_06943_b200.matrix import SparseRowMatrix, sparse_to_dense
+
+    got = scalar_add(_toy(), 0.5).values
+    assert np.array_equal(got, sparse_to_dense(SparseRowMatrix(5, TOY_ROWS)).values + 0.5)
+    with pytest.raises(ValueError):
+        scalar_add(_toy(), float("nan"))
