@@ -264,3 +264,53 @@ def train(dataset: LabeledDataset, config: TrainConfig, counter: OpCounter | Non
             counter.tree_nodes_visited += 2 * nodes
             counter.codes_visited += 2 * int(batches.arena.meta["n_codes"].astype(np.int64).sum())
     return GlmModel(weights=trainer.weights()), trace
+
+
+class _ChunkBatches:
+    """DeviceBatches-shaped view of one streamed store chunk."""
+
+    def __init__(self, arena, labels, n_cols: int):
+        self.arena = arena
+        self.labels = labels
+        self.n_cols = n_cols
+        self.n_rows = arena.n_rows_total
+
+
+def train_store(path, config: TrainConfig, chunk: int = 4096):
+    """MGD over the batches of a TOCS store, streamed from disk chunk by chunk (SURVEY.md 8(f) #2:
+    datasets larger than HBM).  The store's batches are the mini-batches, in store order (the
+    reference's compress step writes them from the dataset in order, cli.py:152-174); each epoch
+    runs the same epoch kernels as ``train`` over every chunk with the weights carried across
+    chunks, then the risk (empirical_risk, training.py:231-258) over the store's rows, also
+    streamed.  GLM losses only.  Returns (GlmModel, LossTrace)."""
+    from .store import BatchStoreStream
+
+    torch = N.require_cuda()
+    if config.loss_kind not in LOSS_CODE:
+        raise ValueError(f"train_store trains GLMs; got loss_kind={config.loss_kind!r}")
+    with BatchStoreStream(path, chunk) as probe:
+        n_cols, n_rows = probe.n_cols, probe.index.total_rows
+    if n_rows == 0:
+        raise ValueError("cannot train on an empty dataset")
+    w = torch.zeros(max(n_cols, 1), dtype=torch.float64, device="cuda")
+    trace = LossTrace()
+    loss = LOSS_CODE[config.loss_kind]
+    partial = torch.zeros(148, dtype=torch.float64, device="cuda")
+    L = _bind()
+    for _ in range(config.epochs):
+        secs = 0.0
+        with BatchStoreStream(path, chunk) as st:
+            for ch in st:
+                tr = GlmTrainer(_ChunkBatches(ch.arena, ch.labels, n_cols), config.loss_kind, config.learning_rate)
+                tr.w = w
+                secs += tr.epoch()
+        trace.seconds.append(secs)
+        total = 0.0
+        with BatchStoreStream(path, chunk) as st:
+            for ch in st:
+                z = ch.arena.matvec(w[:n_cols])
+                N.check(L.toc_glm_risk(z.data_ptr(), ch.labels.data_ptr(), ch.arena.n_rows_total, loss,
+                                       partial.data_ptr(), partial.numel(), N.stream_handle()), "toc_glm_risk")
+                total += float(partial.sum().item())
+        trace.risks.append(total / n_rows)
+    return GlmModel(weights=w[:n_cols].cpu().numpy().copy()), trace

@@ -139,3 +139,29 @@ def test_verify_store(tmp_path):
         verify_store(path, LabeledDataset(features=SparseRowMatrix.from_csr(784, rp, c, v2), labels=y))
     with pytest.raises(VerificationError, match="columns"):
         verify_store(path, LabeledDataset(features=SparseRowMatrix.from_csr(785, rp, c, v), labels=y))
+
+
+def test_train_from_store_matches_oracle(tmp_path, oracle):
+    """Streaming MGD from a store (3 chunks of 7 batches) equals the oracle trainer: the store holds
+    the seed-0 shuffled dataset's batches in order, exactly the batches train(seed=0) uses, and the
+    mean risk does not depend on row order."""
+    from conftest import max_rel_err, within_rel
+
+    from paper_1702_06943_b200 import synth
+    from paper_1702_06943_b200.codec import compress_csr
+    from paper_1702_06943_b200.matrix import LabeledDataset, SparseRowMatrix
+    from paper_1702_06943_b200.store import save_arena_store
+    from paper_1702_06943_b200.training import TrainConfig, shuffle_once, train_store
+
+    rp, c, v, y = synth.cfg3_dataset(5_000, seed=41)
+    ds = shuffle_once(LabeledDataset(features=SparseRowMatrix.from_csr(68, rp, c, v), labels=y), 0)
+    s = ds.features
+    arena = compress_csr(68, s.row_ptr, s.cols, s.vals, np.concatenate([np.arange(0, 5000, 250), [5000]]))
+    path = tmp_path / "cfg3.tocs"
+    save_arena_store(path, arena, ds.labels, 250, 0)
+    m_store, t_store = train_store(path, TrainConfig("logistic", 250, 0.1, 3), chunk=7)
+    w_ref, risks_ref = oracle.train_glm(rp, c, v, y, 68, "logistic", 250, 0.1, 3, 0)
+    risks_ref = np.asarray(risks_ref)
+    assert np.all(np.abs(np.array(t_store.risks) - risks_ref) <= 1e-6 * np.abs(risks_ref)), (t_store.risks, risks_ref)
+    assert within_rel(m_store.weights, w_ref, 1e-6), max_rel_err(m_store.weights, w_ref)
+    assert len(t_store.seconds) == 3
