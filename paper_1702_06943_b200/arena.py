@@ -254,12 +254,81 @@ class BlockArena:
         N.check(rc, "toc_linalg")
         return R, O
 
+    def build_matcache(self):
+        """Per-batch node-record cache for the matmat kernels (toc_matcache_*): built once, after
+        which matmat reads it instead of rebuilding each batch's tree per call -- the path for
+        batches whose trees exceed shared memory (config 5)."""
+        torch = self.torch
+        self.raise_corrupt()
+        L = N.lib()
+        off = np.zeros(self.n_blocks + 1, np.int64)
+        N.check(L.toc_matcache_offsets(self.meta.ctypes.data_as(ctypes.c_void_p), self.n_blocks,
+                                       off.ctypes.data_as(ctypes.c_void_p)), "toc_matcache_offsets")
+        plan = self.plan(N.TOC_MATVEC)
+        scratch = self._scratch_for(plan)
+        cache = torch.empty(int(off[-1]) + 16, dtype=torch.uint8, device=self.data.device)
+        off_d = torch.from_numpy(off[:-1].copy()).to(self.data.device)
+        N.check(L.toc_matcache_build(self.data.data_ptr(), self.block_off_d.data_ptr(), self.meta_d.data_ptr(),
+                                     self.n_blocks, ctypes.byref(plan), off_d.data_ptr(), cache.data_ptr(),
+                                     scratch.data_ptr() if scratch is not None else None, N.stream_handle()),
+                "toc_matcache_build")
+        self.matcache, self.matcache_off, self.matcache_off_d = cache, off, off_d
+        return self
+
+    def _matmat_cached(self, side: int, M, p: int, batch, out):
+        torch = self.torch
+        L = N.lib()
+        dev = self.data.device
+        b0, nb = (0, self.n_blocks) if batch is None else (int(batch), 1)
+        rows = self.n_rows_total if batch is None else int(self.meta["n_rows"][batch])
+        if side == 0:
+            if out is None:
+                out = torch.empty((max(rows, 1), p), dtype=torch.float64, device=dev)[:rows]
+            if batch is None:
+                rb = self.row_base_d.data_ptr()
+            else:
+                if getattr(self, "_zero_rb", None) is None:
+                    self._zero_rb = torch.zeros(1, dtype=torch.int64, device=dev)
+                rb = self._zero_rb.data_ptr()
+            N.check(L.toc_matcache_right(self.matcache.data_ptr(), self.matcache_off_d.data_ptr() + 8 * b0, rb, nb,
+                                         rows, p, _ptr(M), _ptr(out), N.stream_handle()), "toc_matcache_right")
+            return out
+        if out is None:
+            out = torch.empty((max(nb, 1), p, max(self.n_cols, 1)), dtype=torch.float64, device=dev)[:nb, :, : self.n_cols]
+        key = ("mcl", p)
+        need = self._mm_scratch.get(key) if hasattr(self, "_mm_scratch") else None
+        if need is None:
+            c = ctypes.c_int64()
+            need = 0
+            for b in range(self.n_blocks):
+                N.check(L.toc_matcache_left_scratch(self.meta[b : b + 1].ctypes.data_as(ctypes.c_void_p), p,
+                                                    self.n_cols, ctypes.byref(c)), "toc_matcache_left_scratch")
+                need = max(need, c.value)
+            if not hasattr(self, "_mm_scratch"):
+                self._mm_scratch = {}
+            self._mm_scratch[key] = need
+        if self._scratch is None or self._scratch.numel() < need:
+            self._scratch = torch.empty(need, dtype=torch.uint8, device=dev)
+        for k in range(nb):
+            b = b0 + k
+            r0 = 0 if batch is not None else int(self.row_base[b])
+            n = int(self.meta["n_rows"][b])
+            hm = np.ascontiguousarray(self.meta[b : b + 1])
+            N.check(L.toc_matcache_left(self.matcache.data_ptr() + int(self.matcache_off[b]),
+                                        hm.ctypes.data_as(ctypes.c_void_p), p, self.n_cols,
+                                        _ptr(M) + 8 * r0 * p, _ptr(out[k]), self._scratch.data_ptr(),
+                                        self._scratch.numel(), N.stream_handle()), "toc_matcache_left")
+            del n
+        return out
+
     def matmat(self, side: int, M, p: int, batch: int | None = None, out=None):
         """side 0: A.M (M: device [n_cols x p]) -> [rows x p];  side 1: M_b.A_b (M: device M^T
         [rows x p]) -> [blocks, p, n_cols].  batch=None: every batch of the arena; batch=b: only
-        batch b (rows indexed from 0)."""
+        batch b (rows indexed from 0).  Uses the node-record cache when build_matcache() ran."""
         torch = self.torch
         self.raise_corrupt()
+        if getattr(self, "matcache", None) is not None:
+            return self._matmat_cached(side, M, p, batch, out)
         L = N.lib()
         if batch is None:
             b0, nb, rows = 0, self.n_blocks, self.n_rows_total
@@ -275,11 +344,19 @@ class BlockArena:
         if nbytes is None:
             c = ctypes.c_int64()
             meta_all = np.ascontiguousarray(self.meta)
-            N.check(L.toc_matmat_scratch(meta_all.ctypes.data_as(ctypes.c_void_p), self.n_blocks if batch is None else 1,
-                                         self.n_cols, side, p, ctypes.byref(c)), "toc_matmat_scratch")
+            if batch is None:
+                N.check(L.toc_matmat_scratch(meta_all.ctypes.data_as(ctypes.c_void_p), self.n_blocks, self.n_cols, side,
+                                             p, ctypes.byref(c)), "toc_matmat_scratch")
+                nbytes = c.value
+            else:  # one batch per call: the worst case over the batches
+                nbytes = 0
+                for b in range(self.n_blocks):
+                    N.check(L.toc_matmat_scratch(meta_all[b : b + 1].ctypes.data_as(ctypes.c_void_p), 1, self.n_cols,
+                                                 side, p, ctypes.byref(c)), "toc_matmat_scratch")
+                    nbytes = max(nbytes, c.value)
             if not hasattr(self, "_mm_scratch"):
                 self._mm_scratch = {}
-            nbytes = self._mm_scratch[key] = c.value
+            self._mm_scratch[key] = nbytes
         dev = self.data.device
         if out is None:
             if side == 0:

@@ -78,6 +78,7 @@ class _Net:
         self.torch = N.require_cuda()
         self.batches = DeviceBatches(shuffle_once(dataset, seed), batch_size)
         self.arena = self.batches.arena
+        self.arena.build_matcache()  # node records once per run: both first-layer products read them
         self.rb = self.arena.row_base
         self.nrows = self.arena.meta["n_rows"].astype(np.int64)
 

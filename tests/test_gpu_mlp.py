@@ -54,3 +54,26 @@ def test_cfg5_mlp_vs_cpu_restatement(oracle):
     assert np.all(np.abs(np.array(trace.risks) - np.array(risks)) <= REL * np.abs(risks)), (trace.risks, risks)
     for got, want in ((model.w1, w1), (model.b1, b1), (model.w2, w2), (model.b2, b2)):
         assert within_rel(got, want, REL), max_rel_err(got, want)
+
+
+def test_matmat_per_batch_scratch_covers_every_batch(oracle):
+    """Per-batch matmat (the MLP step's call) sizes its global-table scratch for the largest batch,
+    not the first: a small first batch followed by a > 65536-node one."""
+    import torch
+
+    from helpers import random_alphabet_rows
+
+    from paper_1702_06943_b200.arena import BlockArena
+
+    rng = np.random.default_rng(12)
+    small = oracle.encode_rows(400, random_alphabet_rows(rng, 5, 400, 0.5, 64))
+    base = random_alphabet_rows(rng, 30, 400, 0.9, 64)
+    big = oracle.encode_rows(400, [base[i % 30] if i % 3 else random_alphabet_rows(rng, 1, 400, 0.9, 64)[0]
+                                   for i in range(600)])
+    assert big.tree_length() > 65536
+    arena = BlockArena.from_bytes([oracle.serialize(small), oracle.serialize(big)])
+    M = torch.randn(400, 3, dtype=torch.float64, device="cuda")
+    for b, enc in enumerate((small, big)):
+        got = arena.matmat(0, M, 3, batch=b).cpu().numpy()
+        want = oracle.Tree.from_encoding(enc).matmat_right(M.cpu().numpy())
+        assert np.allclose(got, want, rtol=1e-9, atol=1e-12)
