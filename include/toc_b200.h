@@ -278,19 +278,21 @@ int toc_glm_epoch_images_traced(const uint8_t* d_images, const int64_t* d_image_
 
 /* ---- matmat over cached node records (kernels.py:177-234 for large batches) ----------------
  * toc_matcache_offsets (host): byte offsets (n_blocks + 1) of each batch's cache entry (row
- * offsets, code stream, a {parent, column, value} record per tree node; csrc/toc_matcache.cu).
+ * offsets, code stream, each code's first-pair offset, a {parent, column, value} record per tree
+ * node; csrc/toc_matcache.cu).  Rows are expanded in shared memory: 12 * n_cols bytes (A.M),
+ * 268 * n_cols (M.A); TOC_E_ARG when that exceeds shared memory (use toc_matmat).
  * toc_matcache_build: every entry, once (plan from toc_plan(TOC_MATVEC) + its scratch).
  * toc_matcache_right: out [rows x p] = A . M (M [m x p]) for the rows of n_blocks consecutive
  * entries, d_row_base giving each batch's first output row.
- * toc_matcache_left: one batch, out [p x m] = M_b . A_b with M^T given ([n x p]); exact fixed-point
- * accumulation; d_scratch of toc_matcache_left_scratch bytes. */
+ * toc_matcache_left: one batch, out [p x m] = M_b . A_b with M^T given ([n x p]), deterministic
+ * (fixed summation order); d_scratch of toc_matcache_left_scratch bytes. */
 int toc_matcache_offsets(const TocBlockMeta* h_meta, int64_t n_blocks, int64_t* h_cache_off);
 int toc_matcache_build(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
                        int64_t n_blocks, const TocPlan* plan, const int64_t* d_cache_off, uint8_t* d_cache,
                        void* d_scratch, void* stream);
 int toc_matcache_right(const uint8_t* d_cache, const int64_t* d_cache_off, const int64_t* d_row_base,
-                       int64_t n_blocks, int64_t n_rows, int32_t p, const double* d_M, double* d_out,
-                       void* stream);
+                       int64_t n_blocks, int64_t n_rows, int32_t n_cols, int32_t p, const double* d_M,
+                       double* d_out, void* stream);
 int toc_matcache_left_scratch(const TocBlockMeta* h_meta, int32_t p, int32_t n_cols, int64_t* bytes);
 int toc_matcache_left(const uint8_t* d_entry, const TocBlockMeta* h_meta, int32_t p, int32_t n_cols,
                       const double* d_MT, double* d_out, void* d_scratch, int64_t scratch_bytes,

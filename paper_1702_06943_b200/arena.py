@@ -291,7 +291,8 @@ class BlockArena:
                     self._zero_rb = torch.zeros(1, dtype=torch.int64, device=dev)
                 rb = self._zero_rb.data_ptr()
             N.check(L.toc_matcache_right(self.matcache.data_ptr(), self.matcache_off_d.data_ptr() + 8 * b0, rb, nb,
-                                         rows, p, _ptr(M), _ptr(out), N.stream_handle()), "toc_matcache_right")
+                                         rows, self.n_cols, p, _ptr(M), _ptr(out), N.stream_handle()),
+                    "toc_matcache_right")
             return out
         if out is None:
             out = torch.empty((max(nb, 1), p, max(self.n_cols, 1)), dtype=torch.float64, device=dev)[:nb, :, : self.n_cols]
@@ -327,7 +328,7 @@ class BlockArena:
         batch b (rows indexed from 0).  Uses the node-record cache when build_matcache() ran."""
         torch = self.torch
         self.raise_corrupt()
-        if getattr(self, "matcache", None) is not None:
+        if getattr(self, "matcache", None) is not None and 268 * self.n_cols <= 227 * 1024:
             return self._matmat_cached(side, M, p, batch, out)
         L = N.lib()
         if batch is None:

@@ -10,14 +10,16 @@
 //   rowoff   u32[n + 1]         codes   u32[C] (the code stream D)
 //   nodes    {par u32, col u32, value f64}[T]: node x's own pair and parent (node 0 unused), so
 //            one 16-byte load advances a chain by one pair
-// and both products walk chains with K codes in flight per warp (a slot takes the row's next code
-// as soon as its chain ends), lanes across 32 columns of M (warp-uniform control flow).
-//   A.M   CTA (row, 32-column chunk of M): 8 warps take consecutive eighths of the row's codes;
-//         partial sums reduced in shared memory in warp order.  No atomics.
-//   M.A   CTA (row group, chunk, column range): 32 warps walk the group's codes and add
-//         value * M^T[row, chunk] into a shared (columns x 32) tile in exact fixed point (split
-//         words, consecutive lanes -> consecutive banks); tiles of the row groups are summed
-//         exactly in a second pass.  Per-column scales from sum_r |M^T[r, j]| * max |value|.
+//   pstart   u32[C + 1]: each code's first pair, counted from the batch's first pair
+// A row is expanded in shared memory by threads walking different codes' chains (each chain once,
+// not once per output lane), each into its slot range, then the dense part runs with lanes across
+// 32 columns of M:
+//   A.M   CTA per output row: expand, then warps take 32-column chunks of M and sum value *
+//         M[col, j] over the row's pairs in row order.  No atomics.
+//   M.A   CTA (row group, chunk): rows one at a time -- expand, then warps split the row's pairs
+//         and add value * M^T[r, j] into a shared (m x 32) fp64 tile.  A row's pairs have distinct
+//         columns, so within a row no two threads touch one entry: plain adds in row order, no
+//         atomics; the row groups' tiles are summed in group order by a second kernel.
 #include <algorithm>
 
 #include "toc_batch.cuh"
@@ -30,7 +32,7 @@ struct NodeRec {
 };
 
 struct McLayout {
-  uint32_t off_rowoff, off_codes, off_nodes, total;
+  uint32_t off_rowoff, off_codes, off_pstart, off_nodes, total;
 };
 
 constexpr uint32_t kMcHeader = 32;
@@ -42,6 +44,8 @@ TOC_HD McLayout mc_layout(const TocBlockMeta& m) {
   o += align16(4u * (m.n_rows + 1));
   L.off_codes = o;
   o += align16(4u * m.n_codes);
+  L.off_pstart = o;  // first pair of each code, counted from the batch's first pair (C + 1)
+  o += align16(4u * (m.n_codes + 1));
   L.off_nodes = o;
   o += 16u * (1u + m.n_pairs + m.n_derived);
   L.total = o;
@@ -96,6 +100,38 @@ __global__ void __launch_bounds__(1024, 1) mc_build_kernel(McArgs a) {
       if (!B.segment(k, r, lo, hi, db, j0, j1)) break;
       for (uint32_t j = j0; j < j1; ++j) codes[j] = (j + 1 < hi) ? B.pk.par(db + (j - lo)) : B.last[r];
     }
+    __syncthreads();
+    {  // pstart: exclusive prefix of code lengths over the batch, in chunks of the block width
+      uint32_t* pstart = reinterpret_cast<uint32_t*>(e + L.off_pstart);
+      uint32_t carry = 0;
+      const uint32_t lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
+      for (uint32_t base = 0; base < m.n_codes; base += nth) {
+        const uint32_t j = base + tid;
+        uint32_t len = 0;
+        if (j < m.n_codes) {
+          uint32_t x = codes[j];
+          len = 1;
+          while (x > B.nI) {
+            x = B.pk.par(x - 1 - B.nI);
+            ++len;
+          }
+        }
+        const uint32_t xs = warp_excl_scan(len, lane);
+        if (lane == 31) s_warp[warp] = xs + len;
+        __syncthreads();
+        if (warp == 0) {
+          const uint32_t t = lane < nwarps ? s_warp[lane] : 0u;
+          const uint32_t ex = warp_excl_scan(t, lane);
+          if (lane < nwarps) s_warp[lane] = ex;
+          if (lane == 31) s_warp[32] = ex + t;
+        }
+        __syncthreads();
+        if (j < m.n_codes) pstart[j] = carry + s_warp[warp] + xs;
+        carry += s_warp[32];
+        __syncthreads();
+      }
+      if (tid == 0) pstart[m.n_codes] = carry;
+    }
     const uint32_t T = 1u + B.nI + m.n_derived;
     for (uint32_t x = tid; x < T; x += nth) {
       NodeRec n{0u, 0u, 0.0};
@@ -129,52 +165,70 @@ TOC_D NodeRec ld_node(const NodeRec* nodes, uint32_t x) {
   return n;
 }
 
-// Codes [j0, j1) with K chains in flight: visit(pair column, pair value, code position).
-template <int K, typename V>
-TOC_D void walk_slots(const NodeRec* nodes, const uint32_t* codes, uint32_t j0, uint32_t j1, V&& visit) {
-  uint32_t x[K], pos[K];
-  uint32_t nj = j0;
-#pragma unroll
-  for (int k = 0; k < K; ++k) {
-    pos[k] = nj;
-    x[k] = nj < j1 ? __ldg(codes + nj) : 0u;
-    nj += nj < j1 ? 1u : 0u;
-  }
-  for (;;) {
-    bool any = false;
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      if (x[k]) {
-        const NodeRec n = ld_node(nodes, x[k]);
-        visit(n.col, n.val, pos[k]);
-        x[k] = n.par;
-        if (!x[k] && nj < j1) {
-          pos[k] = nj;
-          x[k] = __ldg(codes + nj);
-          ++nj;
-        }
-        any = true;
-      }
+// Expand codes [j0, j1) (one row) into shared (column, value) arrays in row order: threads take
+// different codes and walk their chains (last pair first) into the code's slot range, given by
+// the cached pair offsets.  Returns the row's pair count.
+TOC_D uint32_t expand_row(const uint32_t* codes, const uint32_t* pstart, const NodeRec* nodes, uint32_t j0,
+                          uint32_t j1, uint32_t* s_col, double* s_val) {
+  const uint32_t base = __ldg(pstart + j0);
+  for (uint32_t j = j0 + threadIdx.x; j < j1; j += blockDim.x) {
+    uint32_t x = __ldg(codes + j);
+    uint32_t e = __ldg(pstart + j + 1) - base;
+    while (x) {
+      const NodeRec n = ld_node(nodes, x);
+      --e;
+      s_col[e] = n.col;
+      s_val[e] = n.val;
+      x = n.par;
     }
-    if (!any) break;
   }
+  return __ldg(pstart + j1) - base;
 }
 
-constexpr int kSlots = 8;
+struct McEntry {
+  const uint32_t* rowoff;
+  const uint32_t* codes;
+  const uint32_t* pstart;
+  const NodeRec* nodes;
+  uint32_t n_rows;
+};
+
+TOC_D McEntry mc_entry(const uint8_t* e) {
+  const uint32_t* h = reinterpret_cast<const uint32_t*>(e);
+  TocBlockMeta m{};
+  m.n_rows = h[0];
+  m.n_codes = h[1];
+  m.n_pairs = h[3];
+  m.n_derived = h[2] - 1 - h[3];
+  const McLayout L = mc_layout(m);
+  McEntry E;
+  E.rowoff = reinterpret_cast<const uint32_t*>(e + L.off_rowoff);
+  E.codes = reinterpret_cast<const uint32_t*>(e + L.off_codes);
+  E.pstart = reinterpret_cast<const uint32_t*>(e + L.off_pstart);
+  E.nodes = reinterpret_cast<const NodeRec*>(e + L.off_nodes);
+  E.n_rows = m.n_rows;
+  return E;
+}
 
 struct McRightArgs {
   const uint8_t* cache;
   const int64_t* cache_off;
   const int64_t* row_base;  // first output row of each batch
   int64_t n_blocks;
-  int32_t p;
+  int32_t p, n_cols;
   const double* M;  // [m x p]
   double* out;      // [rows x p]
 };
 
-// CTA (output row, 32-column chunk); 8 warps split the row's codes.
-__global__ void __launch_bounds__(256) mc_right_kernel(McRightArgs a) {
-  __shared__ double s_part[8][32];
+// CTA per output row: expand the row in shared memory, then each warp takes 32-column chunks of
+// M and sums value * M[col, j] over the row's pairs in row order.  No atomics.  (Measured: four
+// split accumulators or pair slices over more warps are slower, 80 vs 52 us at config 5.)
+constexpr uint32_t kRightThreads = 256;
+
+__global__ void __launch_bounds__(kRightThreads) mc_right_kernel(McRightArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  double* s_val = reinterpret_cast<double*>(smem);
+  uint32_t* s_col = reinterpret_cast<uint32_t*>(smem + 8u * (uint32_t)a.n_cols);
   const int64_t row = blockIdx.x;
   int64_t lo = 0, hi = a.n_blocks - 1;  // batch of this row: last b with row_base[b] <= row
   while (lo < hi) {
@@ -182,117 +236,73 @@ __global__ void __launch_bounds__(256) mc_right_kernel(McRightArgs a) {
     if (a.row_base[mid] <= row) lo = mid;
     else hi = mid - 1;
   }
-  const int64_t b = lo;
-  const uint8_t* e = a.cache + a.cache_off[b];
-  const uint32_t* h = reinterpret_cast<const uint32_t*>(e);
-  TocBlockMeta m{};
-  m.n_rows = h[0];
-  m.n_codes = h[1];
-  m.n_pairs = h[3];
-  m.n_derived = h[2] - 1 - h[3];
-  const McLayout L = mc_layout(m);
-  const uint32_t r = (uint32_t)(row - a.row_base[b]);
-  const uint32_t* rowoff = reinterpret_cast<const uint32_t*>(e + L.off_rowoff);
-  const uint32_t* codes = reinterpret_cast<const uint32_t*>(e + L.off_codes);
-  const NodeRec* nodes = reinterpret_cast<const NodeRec*>(e + L.off_nodes);
-  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t P = (uint32_t)a.p, j = blockIdx.y * 32 + lane;
-  const uint32_t c0 = __ldg(rowoff + r), len = __ldg(rowoff + r + 1) - c0;
-  const uint32_t j0 = c0 + (len * warp) / 8, j1 = c0 + (len * (warp + 1)) / 8;
-  double acc = 0.0;
-  const bool on = j < P;
-  walk_slots<kSlots>(nodes, codes, j0, j1, [&](uint32_t col, double val, uint32_t) {
-    if (on) acc = __dadd_rn(acc, __dmul_rn(val, __ldg(a.M + (int64_t)col * P + j)));
-  });
-  s_part[warp][lane] = acc;
+  const McEntry E = mc_entry(a.cache + a.cache_off[lo]);
+  const uint32_t r = (uint32_t)(row - a.row_base[lo]);
+  const uint32_t nnz = expand_row(E.codes, E.pstart, E.nodes, __ldg(E.rowoff + r), __ldg(E.rowoff + r + 1), s_col, s_val);
   __syncthreads();
-  if (warp == 0 && on) {
-    double s = 0.0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) s += s_part[w][lane];
-    a.out[row * (int64_t)P + j] = s;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const uint32_t P = (uint32_t)a.p;
+  for (uint32_t chunk = warp; chunk * 32 < P; chunk += nwarps) {
+    const uint32_t j = chunk * 32 + lane;
+    if (j >= P) continue;
+    double acc = 0.0;
+#pragma unroll 4
+    for (uint32_t q = 0; q < nnz; ++q) acc = __dadd_rn(acc, __dmul_rn(s_val[q], __ldg(a.M + (int64_t)s_col[q] * P + j)));
+    a.out[row * (int64_t)P + j] = acc;
   }
 }
 
 struct McLeftArgs {
   const uint8_t* entry;  // one batch's cache entry
   int32_t p, n_cols;
-  int32_t groups, cw;    // row groups; columns per range
+  int32_t groups;        // row groups
   const double* MT;      // M^T rows of this batch: [n x p]
-  const double* scale;   // [p] fixed-point scale per output column of M
-  long long* tiles;      // [groups][chunks][ranges][cw][32]
+  double* tiles;         // [groups][chunks][n_cols][32]
 };
 
-// Sum_r |M^T[r, j]| * max|value| -> fix_scale per j (one thread per j).
-__global__ void mc_scale_kernel(const double* MT, int32_t n, int32_t p, const uint8_t* entry, double* scale) {
-  const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= p) return;
-  double s = 0.0;
-  for (int32_t r = 0; r < n; ++r) s += fabs(MT[(int64_t)r * p + j]);
-  scale[j] = fix_scale(s * reinterpret_cast<const double*>(entry)[3]);
-}
-
-__global__ void __launch_bounds__(1024, 1) mc_left_kernel(McLeftArgs a) {
+// CTA (row group, 32-column chunk of M^T): rows one at a time -- expand, then warps split the
+// row's pairs and add value * M^T[r, j] into a shared (n_cols x 32) fp64 tile.  A row's pairs
+// have distinct columns, so no two threads touch one tile entry within a row and rows are
+// separated by barriers: plain adds in row order, deterministic, no atomics.
+__global__ void __launch_bounds__(512, 1) mc_left_kernel(McLeftArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
-  const uint8_t* e = a.entry;
-  const uint32_t* h = reinterpret_cast<const uint32_t*>(e);
-  TocBlockMeta m{};
-  m.n_rows = h[0];
-  m.n_codes = h[1];
-  m.n_pairs = h[3];
-  m.n_derived = h[2] - 1 - h[3];
-  const McLayout L = mc_layout(m);
-  const uint32_t* rowoff = reinterpret_cast<const uint32_t*>(e + L.off_rowoff);
-  const uint32_t* codes = reinterpret_cast<const uint32_t*>(e + L.off_codes);
-  const NodeRec* nodes = reinterpret_cast<const NodeRec*>(e + L.off_nodes);
-  const uint32_t g = blockIdx.x, chunk = blockIdx.y, range = blockIdx.z;
-  const uint32_t n = m.n_rows, G = (uint32_t)a.groups, CW = (uint32_t)a.cw;
+  const uint32_t ncol = (uint32_t)a.n_cols;
+  double* tile = reinterpret_cast<double*>(smem);       // [ncol][32]
+  double* s_val = tile + (size_t)ncol * 32;             // [ncol]
+  uint32_t* s_col = reinterpret_cast<uint32_t*>(s_val + ncol);
+  const McEntry E = mc_entry(a.entry);
+  const uint32_t g = blockIdx.x, chunk = blockIdx.y, G = (uint32_t)a.groups, n = E.n_rows;
   const uint32_t r0 = (uint32_t)(((uint64_t)n * g) / G), r1 = (uint32_t)(((uint64_t)n * (g + 1)) / G);
-  const uint32_t cbase = range * CW, cend = min((uint32_t)a.n_cols, cbase + CW);
-  uint32_t* tlo = reinterpret_cast<uint32_t*>(smem);
-  uint32_t* thi = tlo + CW * 32;
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
-  for (uint32_t k = tid; k < 2 * CW * 32; k += blockDim.x) tlo[k] = 0u;
-  __syncthreads();
+  for (uint32_t k = tid; k < ncol * 32; k += blockDim.x) tile[k] = 0.0;
   const uint32_t P = (uint32_t)a.p, j = chunk * 32 + lane;
   const bool on = j < P;
-  const double sc = on ? a.scale[j] : 0.0;
-  const uint32_t q0 = __ldg(rowoff + r0), q1 = __ldg(rowoff + r1), span = q1 - q0;
-  const uint32_t w0 = q0 + (uint32_t)(((uint64_t)span * warp) / nwarps);
-  const uint32_t w1 = q0 + (uint32_t)(((uint64_t)span * (warp + 1)) / nwarps);
-  uint32_t rr = r0;  // row of code position `pos` (positions visited in increasing order per slot refill)
-  double mt = 0.0;
-  uint32_t mt_row = 0xffffffffu;
-  walk_slots<kSlots>(nodes, codes, w0, w1, [&](uint32_t col, double val, uint32_t pos) {
-    if (col < cbase || col >= cend) return;
-    uint32_t r = rr;
-    while (__ldg(rowoff + r + 1) <= pos) ++r;  // rows advance monotonically with new codes
-    while (__ldg(rowoff + r) > pos) --r;       // an older slot may still hold an earlier row
-    rr = r;
-    if (r != mt_row) {
-      mt = on ? __ldg(a.MT + (int64_t)r * P + j) : 0.0;
-      mt_row = r;
+  for (uint32_t r = r0; r < r1; ++r) {
+    __syncthreads();  // the previous row's adds are done before its buffer is overwritten
+    const uint32_t nnz = expand_row(E.codes, E.pstart, E.nodes, __ldg(E.rowoff + r), __ldg(E.rowoff + r + 1), s_col, s_val);
+    const double mt = on ? __ldg(a.MT + (int64_t)r * P + j) : 0.0;
+    __syncthreads();
+#pragma unroll 4
+    for (uint32_t q = warp; q < nnz; q += nwarps) {
+      double* t = tile + (size_t)s_col[q] * 32 + lane;
+      *t = __dadd_rn(*t, __dmul_rn(s_val[q], mt));
     }
-    const long long f = __double2ll_rn(__dmul_rn(val, mt) * sc);
-    if (f) fix_add_split(tlo, thi, (col - cbase) * 32 + lane, (uint32_t)f, (uint32_t)((unsigned long long)f >> 32));
-  });
+  }
   __syncthreads();
-  long long* t = a.tiles + ((((int64_t)g * gridDim.y + chunk) * gridDim.z + range) * CW) * 32;
-  for (uint32_t k = tid; k < CW * 32; k += blockDim.x)
-    t[k] = (long long)(((unsigned long long)thi[k] << 32) | tlo[k]);
+  double* out = a.tiles + ((int64_t)g * gridDim.y + chunk) * (int64_t)ncol * 32;
+  for (uint32_t k = tid; k < ncol * 32; k += blockDim.x) out[k] = tile[k];
 }
 
-// out[j][c] (one batch: [p x m]) = sum over row groups of the tiles, fixed point -> f64.
-__global__ void mc_left_reduce_kernel(const long long* tiles, int32_t groups, int32_t chunks, int32_t ranges,
-                                      int32_t cw, int32_t p, int32_t n_cols, const double* scale, double* out) {
+// out[j][c] (one batch: [p x m]) = sum over row groups of the tiles, in group order.
+__global__ void mc_left_reduce_kernel(const double* tiles, int32_t groups, int32_t chunks, int32_t p, int32_t n_cols,
+                                      double* out) {
   const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;  // over p * n_cols, j-major
   if (k >= (int64_t)p * n_cols) return;
   const int32_t jj = (int32_t)(k / n_cols), c = (int32_t)(k % n_cols);
-  const int32_t chunk = jj >> 5, lane = jj & 31, range = c / cw, cc = c % cw;
-  unsigned long long s = 0;
-  for (int32_t g = 0; g < groups; ++g)
-    s += (unsigned long long)tiles[((((int64_t)g * chunks + chunk) * ranges + range) * cw + cc) * 32 + lane];
-  out[k] = (double)(long long)s / scale[jj];
+  const int32_t chunk = jj >> 5, lane = jj & 31;
+  double s = 0.0;
+  for (int32_t g = 0; g < groups; ++g) s += tiles[(((int64_t)g * chunks + chunk) * n_cols + c) * 32 + lane];
+  out[k] = s;
 }
 
 }  // namespace toc
@@ -347,25 +357,31 @@ extern "C" int toc_matcache_build(const uint8_t* d_arena, const int64_t* d_block
 }
 
 extern "C" int toc_matcache_right(const uint8_t* d_cache, const int64_t* d_cache_off, const int64_t* d_row_base,
-                                  int64_t n_blocks, int64_t n_rows, int32_t p, const double* d_M, double* d_out,
-                                  void* stream) {
-  if (n_blocks < 0 || n_rows < 0 || p < 1 || !d_cache || !d_cache_off || !d_row_base || !d_M || !d_out)
+                                  int64_t n_blocks, int64_t n_rows, int32_t n_cols, int32_t p, const double* d_M,
+                                  double* d_out, void* stream) {
+  if (n_blocks < 0 || n_rows < 0 || p < 1 || n_cols < 1 || !d_cache || !d_cache_off || !d_row_base || !d_M || !d_out)
     return TOC_E_ARG;
   if (n_blocks == 0 || n_rows == 0) return TOC_OK;
-  toc::McRightArgs a{d_cache, d_cache_off, d_row_base, n_blocks, p, d_M, d_out};
-  toc::mc_right_kernel<<<dim3((unsigned)n_rows, (unsigned)((p + 31) / 32)), 256, 0, (cudaStream_t)stream>>>(a);
+  const int smem = 12 * n_cols;  // one row's (value, column) pairs: at most n_cols
+  if (smem > mc_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin, 232448)) return TOC_E_ARG;
+  if (cudaFuncSetAttribute(toc::mc_right_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    return TOC_E_CUDA;
+  toc::McRightArgs a{d_cache, d_cache_off, d_row_base, n_blocks, p, n_cols, d_M, d_out};
+  toc::mc_right_kernel<<<(unsigned)n_rows, toc::kRightThreads, smem, (cudaStream_t)stream>>>(a);
   return cudaGetLastError() == cudaSuccess ? TOC_OK : TOC_E_CUDA;
 }
 
+namespace {
+int32_t left_groups(const TocBlockMeta* h_meta, int32_t p) {
+  const int sms = mc_attr(cudaDevAttrMultiProcessorCount, 148);
+  const int32_t chunks = (p + 31) / 32;
+  return std::max<int32_t>(1, std::min<int32_t>((int32_t)h_meta->n_rows, (sms + chunks - 1) / chunks));
+}
+}  // namespace
+
 extern "C" int toc_matcache_left_scratch(const TocBlockMeta* h_meta, int32_t p, int32_t n_cols, int64_t* bytes) {
   if (!h_meta || p < 1 || n_cols < 1 || !bytes) return TOC_E_ARG;
-  const int optin = mc_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin, 232448);
-  const int32_t cw = std::min<int32_t>(n_cols, (optin - 1024) / 256);
-  const int32_t ranges = (n_cols + cw - 1) / cw, chunks = (p + 31) / 32;
-  const int sms = mc_attr(cudaDevAttrMultiProcessorCount, 148);
-  const int32_t groups = std::max<int32_t>(1, std::min<int32_t>((int32_t)h_meta->n_rows,
-                                                                (sms + chunks * ranges - 1) / (chunks * ranges)));
-  *bytes = 8ll * groups * chunks * ranges * cw * 32 + 8ll * p;
+  *bytes = 8ll * left_groups(h_meta, p) * ((p + 31) / 32) * n_cols * 32;
   return TOC_OK;
 }
 
@@ -377,23 +393,16 @@ extern "C" int toc_matcache_left(const uint8_t* d_entry, const TocBlockMeta* h_m
   int64_t need = 0;
   toc_matcache_left_scratch(h_meta, p, n_cols, &need);
   if (scratch_bytes < need) return TOC_E_ARG;
-  const int optin = mc_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin, 232448);
-  const int32_t cw = std::min<int32_t>(n_cols, (optin - 1024) / 256);
-  const int32_t ranges = (n_cols + cw - 1) / cw, chunks = (p + 31) / 32;
-  const int sms = mc_attr(cudaDevAttrMultiProcessorCount, 148);
-  const int32_t groups = std::max<int32_t>(1, std::min<int32_t>((int32_t)h_meta->n_rows,
-                                                                (sms + chunks * ranges - 1) / (chunks * ranges)));
-  double* scale = reinterpret_cast<double*>(d_scratch);
-  long long* tiles = reinterpret_cast<long long*>(reinterpret_cast<uint8_t*>(d_scratch) + 8ll * p);
+  const int smem = 8 * 32 * n_cols + 12 * n_cols;  // tile + one row's pairs
+  if (smem > mc_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin, 232448)) return TOC_E_ARG;
+  const int32_t groups = left_groups(h_meta, p), chunks = (p + 31) / 32;
   cudaStream_t s = (cudaStream_t)stream;
-  toc::mc_scale_kernel<<<(p + 127) / 128, 128, 0, s>>>(d_MT, (int32_t)h_meta->n_rows, p, d_entry, scale);
-  toc::McLeftArgs a{d_entry, p, n_cols, groups, cw, d_MT, scale, tiles};
-  const int smem = cw * 32 * 8;
+  toc::McLeftArgs a{d_entry, p, n_cols, groups, d_MT, reinterpret_cast<double*>(d_scratch)};
   if (cudaFuncSetAttribute(toc::mc_left_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
     return TOC_E_CUDA;
-  toc::mc_left_kernel<<<dim3(groups, chunks, ranges), 1024, smem, s>>>(a);
+  toc::mc_left_kernel<<<dim3(groups, chunks), 512, smem, s>>>(a);
   const int64_t total = (int64_t)p * n_cols;
-  toc::mc_left_reduce_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(tiles, groups, chunks, ranges, cw, p,
-                                                                               n_cols, scale, d_out);
+  toc::mc_left_reduce_kernel<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(reinterpret_cast<double*>(d_scratch),
+                                                                               groups, chunks, p, n_cols, d_out);
   return cudaGetLastError() == cudaSuccess ? TOC_OK : TOC_E_CUDA;
 }
