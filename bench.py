@@ -43,8 +43,7 @@ def parse():
     p.add_argument("--batches-per-gpu", type=int, default=BATCHES_PER_GPU)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--e2e-steps", type=int, default=20)
-    p.add_argument("--no-mgd", action="store_true", help="skip the MGD epoch measurement (config 3)")
-    p.add_argument("--mgd-cfg4", action="store_true", help="also measure config 4 (hinge, 47,236 cols)")
+    p.add_argument("--no-mgd", action="store_true", help="skip the MGD epoch measurements (configs 3, 4, 5)")
     return p.parse_args()
 
 
@@ -274,9 +273,10 @@ def main():
 
     mgd = {}
     if not args.no_mgd:
-        mgd["config3_logistic"] = run_mgd(3, rank, world, cpu_sample=(rank == 0 and world == 1 and not args.no_cpu_baseline))
-        if args.mgd_cfg4:
-            mgd["config4_hinge"] = run_mgd(4, rank, world, cpu_sample=False)
+        cs = rank == 0 and world == 1 and not args.no_cpu_baseline
+        mgd["config3_logistic"] = run_mgd(3, rank, world, cpu_sample=cs)
+        mgd["config4_hinge"] = run_mgd(4, rank, world, cpu_sample=cs)
+        mgd["config5_mlp"] = run_mgd(5, rank, world, cpu_sample=cs)
 
     if rank == 0:
         line = {
@@ -327,16 +327,20 @@ def main():
 
 
 def run_mgd(cfg: int, rank: int, world: int, cpu_sample: bool):
-    """MGD epoch seconds at the config's full size (BASELINE.json configs[2] / [3]).  N=1: one
-    launch per epoch (single-CTA over step images when they fit shared memory, else the relay); N>1: synchronous data parallel with NCCL (per-replica batch
-    250, global 250*N).  Device time (CUDA events), max over ranks.  The one-time image build
-    (the reference's once-only tree cache) is reported beside the epochs, not inside them."""
+    """MGD epoch seconds at the config's full size (BASELINE.json configs[2] / [3] / [4]).  N=1: one
+    launch per epoch (GLMs: a thread-block cluster over cached step images when they fit shared
+    memory, else the relay; config 5: per-step first-layer matmat kernels over the node-record
+    cache plus torch for the dense tail); N>1: synchronous data parallel with NCCL (per-replica
+    batch 250, global 250*N).  Device time (CUDA events), max over ranks.  One-time cache builds
+    (the reference's once-only cached trees) are reported beside the epochs, not inside them."""
     import torch
 
     from paper_1702_06943_b200 import synth
     from paper_1702_06943_b200.matrix import LabeledDataset, SparseRowMatrix
     from paper_1702_06943_b200.training import DeviceBatches, GlmTrainer, TrainConfig, shuffle_once
 
+    if cfg == 5:
+        return run_mlp(rank, world, cpu_sample)
     if cfg == 3:
         rp, c, v, y = synth.cfg3_dataset()
         m, loss, lr, epochs = 68, "logistic", 0.1, 10
@@ -359,7 +363,8 @@ def run_mgd(cfg: int, rank: int, world: int, cpu_sample: bool):
                     "mode": modes[tr.mode], "image_build_seconds": tr.image_build_seconds,
                     "image_bytes": int(tr.image_off[-1]) if tr.mode == "images" else 0})
         if cpu_sample:
-            out["cpu_port"] = cpu_mgd_sample(rp, c, v, y, m, loss, lr, batches.arena.n_blocks)
+            out["cpu_port"] = cpu_mgd_sample(rp, c, v, y, m, loss, lr, batches.arena.n_blocks,
+                                             sample_batches=400 if cfg == 3 else 100)
     else:
         from paper_1702_06943_b200.distributed import train_data_parallel
 
@@ -367,6 +372,47 @@ def run_mgd(cfg: int, rank: int, world: int, cpu_sample: bool):
         out.update({"steps_per_epoch": -(-len(y) // (250 * world)), "epoch_seconds": trace.seconds,
                     "risk_per_epoch": trace.risks, "mode": f"data parallel x{world}, NCCL all-reduce per step"})
     return out
+
+
+def run_mlp(rank: int, world: int, cpu_sample: bool):
+    """Config 5: 784-200-10 ReLU softmax-CE MLP, 1,000,000 rows, batch 250, lr 0.05, 5 epochs (N=1;
+    the data-parallel MLP is not built)."""
+    from paper_1702_06943_b200 import synth
+    from paper_1702_06943_b200.matrix import LabeledDataset, SparseRowMatrix
+    from paper_1702_06943_b200.mlp import train_mlp
+
+    n, epochs = 1_000_000, 5
+    out = {"rows": n, "n_cols": 784, "model": "784-200-10 ReLU softmax-CE f64", "batch_size": 250, "lr": 0.05,
+           "epochs": epochs}
+    if world > 1:
+        out["unavailable"] = "data-parallel MLP not built; config 5 is reported at N=1"
+        return out
+    rp, c, v, y = synth.cfg5_dataset(n)
+    ds = LabeledDataset(features=SparseRowMatrix.from_csr(784, rp, c, v, check=False), labels=y)
+    t0 = time.perf_counter()
+    _, trace = train_mlp(ds, epochs=epochs)
+    out.update({"steps_per_epoch": n // 250, "epoch_seconds": trace.seconds, "risk_per_epoch": trace.risks,
+                "wall_seconds_incl_compress_and_cache": time.perf_counter() - t0,
+                "mode": "per step: A.W1 and (delta^T.A)^T over the node-record cache (toc_matcache_*), dense tail "
+                        "as torch ops"})
+    if cpu_sample:
+        out["cpu_port"] = cpu_mlp_sample(rp, c, v, y, n // 250)
+    return out
+
+
+def cpu_mlp_sample(rp, c, v, y, steps_full: int, sample_batches: int = 10):
+    """The oracle's config-5 step (C matmat_right / matmat_left + numpy dense tail) on the first
+    sample_batches batches, scaled to a full epoch.  Single thread."""
+    from oracle import oracle as O
+
+    O.build()
+    k = 250 * sample_batches
+    srp = rp[: k + 1]
+    t0 = time.perf_counter()
+    O.train_mlp(srp, c[: srp[-1]], v[: srp[-1]], y[:k], 784, 200, 10, 250, 0.05, 1, 0)
+    dt = time.perf_counter() - t0
+    return {"epoch_seconds_est": dt * steps_full / sample_batches,
+            "sample": f"{sample_batches} of {steps_full} steps (incl. their tree builds), 1 thread", "kind": "port"}
 
 
 def cpu_mgd_sample(rp, c, v, y, m, loss, lr, steps_full: int, sample_batches: int = 400):
