@@ -248,6 +248,11 @@ def main():
     vm_t = time_kernel(torch, lambda: arena.linalg(N.TOC_VECMAT, u=u, O=O), nsub, 3, flush)
     # block-only mode: the tree is rebuilt from the TOC1 codes inside every launch
     bo_t = time_kernel(torch, lambda: arena.linalg(kind, v=v, u=u, R=R, O=O, use_trees=False), nsub, 3, flush)
+    # the fp32 variant (north_star: 1e-4 bar): same batches, fused single walk for both products
+    v32, u32 = v.float(), u.float()
+    R32 = torch.empty_like(R, dtype=torch.float32)
+    O32 = torch.empty_like(O, dtype=torch.float32)
+    f32_t = time_kernel(torch, lambda: arena.linalg32(kind, v=v32, u=u32, R=R32, O=O32), nsub, 3, flush)
 
     peak, peak_src = measured_peaks()
     alg = algorithmic_bytes(arena, kind)
@@ -312,6 +317,11 @@ def main():
                            "rows_per_s": world * rows_per_step / (np.mean(bo_t) / 1e3),
                            "roofline_frac": alg / (np.mean(bo_t) / 1e3) / 1e9 / peak, "traffic": bo_traffic,
                            "note": "tree rebuilt from the TOC1 codes inside every launch; reads only the block"},
+            "fp32_variant": {"ms_per_step": float(np.mean(f32_t)),
+                             "rows_per_s": world * rows_per_step / (np.mean(f32_t) / 1e3),
+                             "roofline_frac": alg / (np.mean(f32_t) / 1e3) / 1e9 / peak, "dtype": "f32",
+                             "note": "toc_linalg32: fp32 operands, fixed-point 32-bit v^T.A, one walk for both "
+                                     "products; 1e-4 of the fp64 oracle (not the headline: the reference is f64)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": alg, "kernel": "toc::linalg_kernel (A.v + v^T.A)"},

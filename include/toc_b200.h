@@ -276,6 +276,15 @@ int toc_glm_epoch_images_traced(const uint8_t* d_images, const int64_t* d_image_
                                 int32_t n_cols, int32_t cluster, int32_t loss, double lr, double* d_w,
                                 long long* d_trace, void* stream);
 
+/* The fp32 variant of toc_linalg_trees (tree cache required; every batch's tables in shared memory,
+ * i.e. !plan->global_tables): v, R, u, O in float32, P1 in fp32, G in 32-bit fixed point, and a
+ * fused TOC_MATVEC | TOC_VECMAT walks every code once for both products.  Within 1e-4 of the fp64
+ * oracle (BASELINE.json north_star); the reference has no fp32 mode. */
+int toc_linalg32(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+                 const int64_t* d_row_base, int64_t n_blocks, const TocPlan* plan, int32_t kind,
+                 const float* d_v, float* d_R, const float* d_u, float* d_O, const uint8_t* d_trees,
+                 const int64_t* d_tree_off, void* stream);
+
 /* ---- matmat over cached node records (kernels.py:177-234 for large batches) ----------------
  * toc_matcache_offsets (host): byte offsets (n_blocks + 1) of each batch's cache entry (row
  * offsets, code stream, each code's first-pair offset, a {parent, column, value} record per tree

@@ -71,6 +71,7 @@ def lib():
     L.toc_matmat_scratch.argtypes = [P, I64, I32, I32, I32, ctypes.POINTER(ctypes.c_int64)]
     L.toc_decode_counts.argtypes = [P, P, P, P, I64, ctypes.POINTER(TocPlan), P, P, P]
     L.toc_decode_rows.argtypes = [P, P, P, P, I64, ctypes.POINTER(TocPlan), P, P, P, P, P]
+    L.toc_linalg32.argtypes = [P, P, P, P, I64, ctypes.POINTER(TocPlan), I32, P, P, P, P, P, P, P]
     L.toc_matcache_offsets.argtypes = [P, I64, P]
     L.toc_matcache_build.argtypes = [P, P, P, I64, ctypes.POINTER(TocPlan), P, P, P, P]
     L.toc_matcache_right.argtypes = [P, P, P, I64, I64, I32, I32, P, P, P]

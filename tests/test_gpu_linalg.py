@@ -147,3 +147,36 @@ def test_batch_sweep_public_api(oracle):
         assert within_rel(R[250 * b : 250 * (b + 1)], t.matvec(x), REL)
         assert within_rel(O[b], t.vecmat(u[250 * b : 250 * (b + 1)]), REL)
     assert sweep.h2d_bytes == end + 8 * 784 + 8 * 250 * nb
+
+
+@pytest.mark.parametrize("kind", [1, 2, 3])
+def test_fp32_variant_vs_oracle(oracle, kind):
+    """The fp32 variant (toc_linalg32, fused walk for kind 3) within 1e-4 of the fp64 oracle -- the
+    north_star's bar for it -- on config-2 batches, config 1 and a random alphabet with empty rows."""
+    import torch
+
+    from paper_1702_06943_b200 import synth
+
+    cases = [[oracle.encode_csr(784, *synth.dense_to_csr(synth.cfg2_batch_dense(2, b))) for b in range(4)],
+             [oracle.encode_csr(128, *synth.dense_to_csr(synth.cfg1_dense(0)))],
+             [oracle.encode_rows(30, random_alphabet_rows(np.random.default_rng(8), 90, 30, 0.4) + [[]]),
+              oracle.encode_rows(30, random_alphabet_rows(np.random.default_rng(9), 41, 30, 0.7))]]
+    for encs in cases:
+        m = encs[0].n_cols
+        arena = _arena([oracle.serialize(e) for e in encs])
+        rng = np.random.default_rng(kind)
+        v = rng.standard_normal(m).astype(np.float32)
+        u = rng.standard_normal(sum(e.n_rows for e in encs)).astype(np.float32)
+        R, O = arena.linalg32(kind, v=torch.from_numpy(v).cuda(), u=torch.from_numpy(u).cuda())
+        base = 0
+        for b, e in enumerate(encs):
+            t = oracle.Tree.from_encoding(e)
+            if kind & 1:
+                want = t.matvec(v.astype(np.float64))
+                got = R[base : base + e.n_rows].cpu().numpy().astype(np.float64)
+                assert within_rel(got, want, 1e-4), max_rel_err(got, want)
+            if kind & 2:
+                want = t.vecmat(u[base : base + e.n_rows].astype(np.float64))
+                got = O[b].cpu().numpy().astype(np.float64)
+                assert within_rel(got, want, 1e-4), max_rel_err(got, want)
+            base += e.n_rows
