@@ -368,10 +368,12 @@ def run_mgd(cfg: int, rank: int, world: int, cpu_sample: bool):
             risks.append(tr.risk())
         modes = {"images": f"one launch per epoch: a {tr.cluster}-CTA thread-block cluster over cached step images "
                            "(built once per run, like the reference's cached trees)",
+                 "parts": f"one launch per epoch: a {tr.cluster}-CTA cluster over per-CTA part images (built once per "
+                          "run), weights and an exact fixed-point gradient in global memory",
                  "relay": "one cooperative relay launch per epoch (tables rebuilt per step)"}
         out.update({"steps_per_epoch": int(batches.arena.n_blocks), "epoch_seconds": secs, "risk_per_epoch": risks,
                     "mode": modes[tr.mode], "image_build_seconds": tr.image_build_seconds,
-                    "image_bytes": int(tr.image_off[-1]) if tr.mode == "images" else 0})
+                    "image_bytes": int(tr.image_off[-1]) if tr.mode in ("images", "parts") else 0})
         if cpu_sample:
             out["cpu_port"] = cpu_mgd_sample(rp, c, v, y, m, loss, lr, batches.arena.n_blocks,
                                              sample_batches=400 if cfg == 3 else 100)

@@ -267,6 +267,33 @@ int toc_mgd_build_images(const uint8_t* d_arena, const int64_t* d_block_off, con
 int toc_glm_epoch_images(const uint8_t* d_images, const int64_t* d_image_off, const TocBlockMeta* d_meta,
                          const TocBlockMeta* h_meta, int64_t n_blocks, int32_t n_cols, int32_t cluster,
                          int32_t loss, double lr, double* d_w, void* stream);
+/* MGD for models too wide for shared memory (csrc/toc_images_large.cu): per-CTA part images of
+ * every batch (the CTA's rows, the part of C' their codes reach renumbered locally, its pairs'
+ * columns and values, the columns it owns, labels), built once per run in two passes:
+ * toc_mgd_parts_count -> d_counts[n_blocks][cluster][4] (pairs, derived nodes, codes, owned
+ * columns); toc_mgd_parts_offsets (host) -> h_part_off[n_blocks * cluster + 1] and the largest part;
+ * toc_mgd_parts_build writes them.  d_scratch: toc_mgd_parts_scratch bytes.
+ * toc_glm_epoch_parts: one epoch on a cluster (logistic / hinge); w and d_gacc (n_cols u64, zero,
+ * left zero) in global memory; each step's gradient accumulated in exact 64-bit fixed point.
+ * toc_mgd_parts_fit: whether the epoch's part buffers fit shared memory. */
+int toc_mgd_parts_scratch(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t n_cols, int64_t* bytes);
+int toc_mgd_parts_count(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+                        const TocBlockMeta* h_meta, const int64_t* d_row_base, int64_t n_blocks,
+                        int32_t n_cols, int32_t cluster, const double* d_labels, int32_t* d_counts,
+                        void* d_scratch, void* stream);
+int toc_mgd_parts_offsets(const TocBlockMeta* h_meta, const int32_t* h_counts, int64_t n_blocks,
+                          int32_t cluster, int64_t* h_part_off, int64_t* max_part);
+int toc_mgd_parts_build(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+                        const TocBlockMeta* h_meta, const int64_t* d_row_base, int64_t n_blocks,
+                        int32_t n_cols, int32_t cluster, const double* d_labels, const int32_t* d_counts,
+                        const int64_t* d_part_off, uint8_t* d_images, void* d_scratch, void* stream);
+int toc_mgd_parts_fit(const TocBlockMeta* h_meta, const int32_t* h_counts, int64_t n_blocks,
+                      int32_t cluster, int64_t max_part, int32_t* fits);
+int toc_glm_epoch_parts(const uint8_t* d_images, const int64_t* d_part_off, const TocBlockMeta* h_meta,
+                        const int32_t* h_counts, int64_t n_blocks, int32_t n_cols, int32_t cluster,
+                        int32_t loss, double lr, double* d_w, unsigned long long* d_gacc, int64_t max_part,
+                        void* stream);
+
 /* Diagnostic: CTA width (power of two, 64..1024; 0 = 512) of cluster epochs planned afterwards. */
 int toc_mgd_set_image_threads(int32_t threads);
 /* toc_glm_epoch_images plus 8 clock64 stamps per step from CTA 0 (step start, image landed, P1,

@@ -121,6 +121,12 @@ def _bind():
         L.toc_mgd_image_plan.argtypes = [P, I64, I32, I32, ctypes.POINTER(ctypes.c_int32), P]
         L.toc_mgd_build_images.argtypes = [P, P, P, P, P, I64, I32, I32, P, P, P, P]
         L.toc_glm_epoch_images.argtypes = [P, P, P, P, I64, I32, I32, I32, D, P, P]
+        L.toc_mgd_parts_scratch.argtypes = [P, I64, I32, ctypes.POINTER(ctypes.c_int64)]
+        L.toc_mgd_parts_count.argtypes = [P, P, P, P, P, I64, I32, I32, P, P, P, P]
+        L.toc_mgd_parts_offsets.argtypes = [P, P, I64, I32, P, ctypes.POINTER(ctypes.c_int64)]
+        L.toc_mgd_parts_build.argtypes = [P, P, P, P, P, I64, I32, I32, P, P, P, P, P, P]
+        L.toc_mgd_parts_fit.argtypes = [P, P, I64, I32, I64, ctypes.POINTER(ctypes.c_int32)]
+        L.toc_glm_epoch_parts.argtypes = [P, P, P, P, I64, I32, I32, I32, D, P, P, I64, P]
         L._mgd_bound = True
     return L
 
@@ -137,8 +143,8 @@ class GlmTrainer:
 
     def __init__(self, batches: DeviceBatches, loss_kind: str, learning_rate: float, mode: str = "auto",
                  cluster: int = 0):
-        if mode not in ("auto", "images", "relay"):
-            raise ValueError(f"mode must be auto, images or relay, got {mode!r}")
+        if mode not in ("auto", "images", "parts", "relay"):
+            raise ValueError(f"mode must be auto, images, parts or relay, got {mode!r}")
         self.torch = N.require_cuda()
         self.b = batches
         self.loss = LOSS_CODE[loss_kind]
@@ -156,8 +162,10 @@ class GlmTrainer:
         self.mode = "relay"
         self.image_build_seconds = 0.0
         self.cluster = 0
-        if mode != "relay":
+        if mode in ("auto", "images"):
             self._build_images(mode == "images", cluster)
+        if self.mode == "relay" and mode in ("auto", "parts"):
+            self._build_parts(mode == "parts", cluster or 8)
 
     def _build_images(self, required: bool, cluster_req: int) -> None:
         torch = self.torch
@@ -189,12 +197,73 @@ class GlmTrainer:
         self.mode = "images"
         self.cluster = ok.value
 
+    def _build_parts(self, required: bool, cluster: int) -> None:
+        """Per-CTA part images for models too wide for shared memory (toc_images_large.cu)."""
+        torch = self.torch
+        a = self.b.arena
+        if self.loss not in (LOSS_CODE["logistic"], LOSS_CODE["hinge"]):
+            if required:
+                raise ValueError("mode='parts' trains logistic / hinge losses (squared: use the relay)")
+            return
+        a.raise_corrupt()
+        L = _bind()
+        meta = a.meta.ctypes.data_as(ctypes.c_void_p)
+        nb = ctypes.c_int64()
+        N.check(L.toc_mgd_parts_scratch(meta, a.n_blocks, self.b.n_cols, ctypes.byref(nb)), "toc_mgd_parts_scratch")
+        scratch = torch.empty(max(nb.value, 16), dtype=torch.uint8, device="cuda")
+        counts = torch.zeros(a.n_blocks * cluster * 4, dtype=torch.int32, device="cuda")
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record()
+        N.check(L.toc_mgd_parts_count(a.data.data_ptr(), a.block_off_d.data_ptr(), a.meta_d.data_ptr(), meta,
+                                      a.row_base_d.data_ptr(), a.n_blocks, self.b.n_cols, cluster,
+                                      self.b.labels.data_ptr(), counts.data_ptr(), scratch.data_ptr(),
+                                      N.stream_handle()), "toc_mgd_parts_count")
+        counts_h = counts.cpu().numpy()
+        off = np.zeros(a.n_blocks * cluster + 1, dtype=np.int64)
+        mx = ctypes.c_int64()
+        N.check(L.toc_mgd_parts_offsets(meta, counts_h.ctypes.data_as(ctypes.c_void_p), a.n_blocks, cluster,
+                                        off.ctypes.data_as(ctypes.c_void_p), ctypes.byref(mx)), "toc_mgd_parts_offsets")
+        fits = ctypes.c_int32()
+        N.check(L.toc_mgd_parts_fit(meta, counts_h.ctypes.data_as(ctypes.c_void_p), a.n_blocks, cluster, mx.value,
+                                    ctypes.byref(fits)), "toc_mgd_parts_fit")
+        if not fits.value:
+            if required:
+                raise ValueError("part images do not fit shared memory; use mode='relay'")
+            return
+        self.part_off_d = torch.from_numpy(off).cuda()
+        self.images = torch.empty(max(int(off[-1]), 16), dtype=torch.uint8, device="cuda")
+        N.check(L.toc_mgd_parts_build(a.data.data_ptr(), a.block_off_d.data_ptr(), a.meta_d.data_ptr(), meta,
+                                      a.row_base_d.data_ptr(), a.n_blocks, self.b.n_cols, cluster,
+                                      self.b.labels.data_ptr(), counts.data_ptr(), self.part_off_d.data_ptr(),
+                                      self.images.data_ptr(), scratch.data_ptr(), N.stream_handle()),
+                "toc_mgd_parts_build")
+        end.record()
+        end.synchronize()
+        self.image_build_seconds = start.elapsed_time(end) / 1e3
+        self.parts_counts = counts_h
+        self.parts_max = mx.value
+        self.image_off = off
+        self.gacc = torch.zeros(max(self.b.n_cols, 1), dtype=torch.int64, device="cuda")
+        self.mode = "parts"
+        self.cluster = cluster
+
     def epoch(self) -> float:
         """One epoch; returns its device time in seconds (CUDA events on the launch stream)."""
         torch = self.torch
         a = self.b.arena
         a.raise_corrupt()
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if self.mode == "parts":
+            start.record()
+            N.check(_bind().toc_glm_epoch_parts(self.images.data_ptr(), self.part_off_d.data_ptr(),
+                                                a.meta.ctypes.data_as(ctypes.c_void_p),
+                                                self.parts_counts.ctypes.data_as(ctypes.c_void_p), a.n_blocks,
+                                                self.b.n_cols, self.cluster, self.loss, self.lr, self.w.data_ptr(),
+                                                self.gacc.data_ptr(), self.parts_max, N.stream_handle()),
+                    "toc_glm_epoch_parts")
+            end.record()
+            end.synchronize()
+            return start.elapsed_time(end) / 1e3
         if self.mode == "images":
             start.record()
             N.check(_bind().toc_glm_epoch_images(self.images.data_ptr(), self.image_off_d.data_ptr(),

@@ -182,11 +182,50 @@ def test_step_images_ragged_batches(oracle):
     assert within_rel(model.weights, w_ref, REL), max_rel_err(model.weights, w_ref)
 
 
-def test_large_m_falls_back_to_relay():
+def test_large_m_uses_parts_and_squared_uses_relay():
     from paper_1702_06943_b200 import synth
 
     rp, c, v, y = synth.cfg4_dataset(1_000, seed=34)
     t = _trainer(rp, c, v, y, 47_236, 250, "hinge", 0.01, "auto")
-    assert t.mode == "relay"
+    assert t.mode == "parts" and t.cluster == 8
     with pytest.raises(ValueError):
         _trainer(rp, c, v, y, 47_236, 250, "hinge", 0.01, "images")
+    ts = _trainer(rp, c, v, y * 0.5, 47_236, 250, "squared", 0.01, "auto")
+    assert ts.mode == "relay"
+
+
+@pytest.mark.parametrize("loss,lr,cluster", [("hinge", 0.01, 8), ("logistic", 0.05, 8)])
+def test_parts_match_relay(loss, lr, cluster):
+    """The large-n_cols cluster epoch (per-CTA part images, global fixed-point gradient) computes what
+    the relay computes, up to the per-CTA rounding of the fixed-point contributions (~1e-15)."""
+    from paper_1702_06943_b200 import synth
+
+    rp, c, v, y = synth.cfg4_dataset(3_000, seed=35)
+    tp = _trainer(rp, c, v, y, 47_236, 250, loss, lr, "parts", cluster)
+    tr = _trainer(rp, c, v, y, 47_236, 250, loss, lr, "relay")
+    assert tp.mode == "parts" and tp.cluster == cluster
+    for _ in range(2):
+        tp.epoch()
+        tr.epoch()
+        wp, wr = tp.weights(), tr.weights()
+        assert within_rel(wp, wr, 1e-12), max_rel_err(wp, wr)
+        assert tp.risk() == pytest.approx(tr.risk(), rel=1e-12)
+    assert int(tp.gacc.abs().sum().item()) == 0  # the fixed-point gradient is left cleared
+
+
+def test_parts_ragged_batches(oracle):
+    """Parts with short / empty CTA row ranges: 13-row batches over an 8-CTA cluster, a short last batch."""
+    from helpers import random_alphabet_rows
+
+    rng = np.random.default_rng(36)
+    rows = random_alphabet_rows(rng, 300, 40, 0.3) + [[], [(39, 1.0)]]
+    rp, c, v = oracle.rows_to_csr(rows)
+    y = np.where(rng.random(len(rows)) < 0.5, -1.0, 1.0)
+    from paper_1702_06943_b200.training import DeviceBatches, GlmTrainer
+
+    tp = GlmTrainer(DeviceBatches(dataset_from_csr(40, rp, c, v, y), 13), "hinge", 0.1, mode="parts", cluster=8)
+    tr = GlmTrainer(DeviceBatches(dataset_from_csr(40, rp, c, v, y), 13), "hinge", 0.1, mode="relay")
+    for _ in range(2):
+        tp.epoch()
+        tr.epoch()
+    assert within_rel(tp.weights(), tr.weights(), 1e-12), max_rel_err(tp.weights(), tr.weights())
