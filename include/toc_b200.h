@@ -352,6 +352,41 @@ int toc_tree_arrays(const uint8_t* d_arena, const int64_t* d_block_off, const To
                     int32_t* d_column, double* d_value, int32_t* d_first_col, double* d_first_val,
                     void* d_scratch, void* stream);
 
+/* ---- the batched public sweep's pipeline (kernels.BatchSweep; reference cli.py:299-383) --------
+ * One chunk of the sweep: its byte range in the host and device block buffers, its indexed view
+ * (offsets relative to d_arena; rows relative to the chunk) and its plan / scratch. */
+typedef struct TocSweepChunk {
+  int64_t byte_lo, byte_hi;
+  const uint8_t* d_arena;
+  const int64_t* d_block_off;
+  const int64_t* d_block_len;
+  TocBlockMeta* d_meta;
+  const int64_t* d_row_base;
+  void* d_scratch;
+  int64_t n_blocks, b0, row0, n_rows;
+  TocPlan plan;
+} TocSweepChunk; /* 136 bytes */
+
+/* Enqueue the block bytes of chunks [k0, k1) host -> device on copy_stream (pinned h_blocks). */
+int toc_sweep_upload(const uint8_t* h_blocks, uint8_t* d_blocks, const TocSweepChunk* chunks, int64_t k0,
+                     int64_t k1, void* copy_stream);
+/* Enqueue v and every chunk's u slice on copy_stream (host -> device copies are served in
+ * submission order: enqueue them after the first chunk's bytes, before the others). */
+int toc_sweep_operands(const TocSweepChunk* chunks, int64_t n_chunks, int32_t n_cols, const double* h_v,
+                       double* d_v, const double* h_u, double* d_u, void* copy_stream);
+/* Enqueue per chunk, after its bytes and operands: toc_index_blocks and the fused A.v + v^T.A
+ * (compute_stream), then R, O and the chunk's index to the pinned host buffers (d2h_stream).  The
+ * caller synchronizes d2h_stream and checks h_meta for format / corruption errors. */
+int toc_sweep_compute(const TocSweepChunk* chunks, int64_t n_chunks, int32_t n_cols, const double* d_v,
+                      const double* d_u, double* d_R, double* h_R, double* d_O, double* h_O,
+                      TocBlockMeta* h_meta, void* compute_stream, void* d2h_stream);
+int toc_sizeof_sweep_chunk(void); /* 136 */
+/* Diagnostic: record timed events in later runs; toc_sweep_timeline reads chunk k's upload end,
+ * validation start / end, compute end and download end (out[5k..5k+4], ms from the first upload)
+ * after a synchronized run. */
+int toc_sweep_set_timing(int32_t on);
+int toc_sweep_timeline(int64_t n_chunks, float* out);
+
 /* ---- version / self-description ---------------------------------------------------------- */
 const char* toc_version(void);
 int toc_device_info(int32_t* sm_count, int32_t* smem_optin, int64_t* l2_bytes);

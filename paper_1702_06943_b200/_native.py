@@ -39,6 +39,13 @@ class TocPlan(ctypes.Structure):
                 ("scratch_bytes", ctypes.c_int64)]
 
 
+class TocSweepChunk(ctypes.Structure):
+    _fields_ = [("byte_lo", ctypes.c_int64), ("byte_hi", ctypes.c_int64), ("d_arena", ctypes.c_void_p),
+                ("d_block_off", ctypes.c_void_p), ("d_block_len", ctypes.c_void_p), ("d_meta", ctypes.c_void_p),
+                ("d_row_base", ctypes.c_void_p), ("d_scratch", ctypes.c_void_p), ("n_blocks", ctypes.c_int64),
+                ("b0", ctypes.c_int64), ("row0", ctypes.c_int64), ("n_rows", ctypes.c_int64), ("plan", TocPlan)]
+
+
 class NativeError(RuntimeError):
     """A native call failed for a reason that is not a data error (CUDA error, bad argument)."""
 
@@ -71,6 +78,9 @@ def lib():
     L.toc_matmat_scratch.argtypes = [P, I64, I32, I32, I32, ctypes.POINTER(ctypes.c_int64)]
     L.toc_decode_counts.argtypes = [P, P, P, P, I64, ctypes.POINTER(TocPlan), P, P, P]
     L.toc_decode_rows.argtypes = [P, P, P, P, I64, ctypes.POINTER(TocPlan), P, P, P, P, P]
+    L.toc_sweep_upload.argtypes = [P, P, P, I64, I64, P]
+    L.toc_sweep_operands.argtypes = [P, I64, I32, P, P, P, P, P]
+    L.toc_sweep_compute.argtypes = [P, I64, I32, P, P, P, P, P, P, P, P, P]
     L.toc_linalg32.argtypes = [P, P, P, P, I64, ctypes.POINTER(TocPlan), I32, P, P, P, P, P, P, P]
     L.toc_matcache_offsets.argtypes = [P, I64, P]
     L.toc_matcache_build.argtypes = [P, P, P, I64, ctypes.POINTER(TocPlan), P, P, P, P]
@@ -80,7 +90,8 @@ def lib():
     L.toc_tree_arrays.argtypes = [P, P, P, I64, ctypes.POINTER(TocPlan), P, P, P, P, P, P, P, P]
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype or ctypes.c_int
-    if L.toc_sizeof_meta() != META_DTYPE.itemsize or L.toc_sizeof_plan() != ctypes.sizeof(TocPlan):
+    if (L.toc_sizeof_meta() != META_DTYPE.itemsize or L.toc_sizeof_plan() != ctypes.sizeof(TocPlan)
+            or L.toc_sizeof_sweep_chunk() != ctypes.sizeof(TocSweepChunk)):
         raise ImportError("libtoc_b200.so ABI mismatch with the Python binding")
     _lib = L
     return L

@@ -23,3 +23,4 @@ extern "C" int toc_sizeof_plan(void) { return (int)sizeof(TocPlan); }
 
 static_assert(sizeof(TocBatchInfo) == 48, "TocBatchInfo layout is part of the ABI");
 extern "C" int toc_sizeof_batch_info(void) { return (int)sizeof(TocBatchInfo); }
+extern "C" int toc_sizeof_sweep_chunk(void) { return (int)sizeof(TocSweepChunk); }

@@ -12,9 +12,48 @@ namespace toc {
 
 namespace {
 
+// The checks run out of shared memory when the block fits kStageBytes (copied in once with 16-byte
+// loads: the stages' scattered reads would otherwise each pay a global-memory latency, ~0.1 ms per
+// block), else straight from global memory; the readers below use generic loads for both.
+constexpr uint32_t kStageBytes = 110u * 1024u;
+
 struct Cursor {
   const uint8_t* p;
   int64_t len;
+};
+
+__device__ __forceinline__ uint32_t gu32(const uint8_t* q) {
+  return (uint32_t)q[0] | ((uint32_t)q[1] << 8) | ((uint32_t)q[2] << 16) | ((uint32_t)q[3] << 24);
+}
+
+__device__ __forceinline__ uint32_t gpacked(const uint8_t* p, uint32_t i, uint32_t w) {
+  const uint8_t* q = p + (size_t)i * w;
+  switch (w) {
+    case 1: return q[0];
+    case 2: return (uint32_t)q[0] | ((uint32_t)q[1] << 8);
+    case 3: return (uint32_t)q[0] | ((uint32_t)q[1] << 8) | ((uint32_t)q[2] << 16);
+    default: return gu32(q);
+  }
+}
+
+__device__ __forceinline__ double gf64(const uint8_t* q) {
+  const uint64_t lo = gu32(q), hi = gu32(q + 4);
+  return __longlong_as_double((long long)(lo | (hi << 32)));
+}
+
+// Sequential reader of a packed section (one value per call), byte loads from either space.
+template <int W>
+struct GSeqReader {
+  const uint8_t* q;
+  __device__ __forceinline__ void init(const uint8_t* sec, uint32_t i0) { q = sec + (size_t)i0 * W; }
+  __device__ __forceinline__ uint32_t next() {
+    uint32_t v = q[0];
+    if constexpr (W > 1) v |= (uint32_t)q[1] << 8;
+    if constexpr (W > 2) v |= (uint32_t)q[2] << 16;
+    if constexpr (W > 3) v |= (uint32_t)q[3] << 24;
+    q += W;
+    return v;
+  }
 };
 
 __device__ void fail(TocBlockMeta& m, int status, uint32_t detail, uint32_t a, uint32_t b) {
@@ -31,8 +70,8 @@ __device__ bool packed_hdr(const Cursor& c, int64_t off, uint32_t& count, uint32
     fail(m, TOC_E_TRUNCATED, TOC_D_TRUNC, (uint32_t)off, 0);
     return false;
   }
-  count = ld_u32_unaligned(c.p + off);
-  width = __ldg(c.p + off + 4);
+  count = gu32(c.p + off);
+  width = c.p[off + 4];
   off += 5;
   if (width < 1 || width > 4) {
     fail(m, TOC_E_FORMAT, TOC_D_WIDTH, (uint32_t)(off - 1), width);
@@ -58,6 +97,7 @@ __global__ void __launch_bounds__(256) index_blocks_kernel(const uint8_t* __rest
                                                            const int64_t* __restrict__ block_len,
                                                            int64_t n_blocks,
                                                            TocBlockMeta* __restrict__ meta_out) {
+  extern __shared__ __align__(16) uint8_t s_bytes[];
   __shared__ TocBlockMeta sm;
   __shared__ uint32_t s_warp[33];
   __shared__ uint32_t s_first, s_carry, s_ok;
@@ -65,7 +105,28 @@ __global__ void __launch_bounds__(256) index_blocks_kernel(const uint8_t* __rest
   const int64_t b = blockIdx.x;
   if (b >= n_blocks) return;
   const uint32_t tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
-  Cursor c{arena + block_off[b], block_len[b]};
+  const Cursor g{arena + block_off[b], block_len[b]};
+  bool staged = false;
+  uint32_t head = 0;
+  {
+    // stage the 16-byte granules covering the block (each holds a block byte, so none can fault),
+    // plus a zero guard for the readers' look-ahead
+    const uintptr_t a0 = reinterpret_cast<uintptr_t>(g.p) & ~(uintptr_t)15;
+    const uintptr_t a1 = (reinterpret_cast<uintptr_t>(g.p) + (uintptr_t)max(g.len, (int64_t)0) + 15) & ~(uintptr_t)15;
+    head = (uint32_t)(reinterpret_cast<uintptr_t>(g.p) - a0);
+    if (g.len >= 0 && a1 - a0 + 16 <= kStageBytes) {
+      const uint4* src = reinterpret_cast<const uint4*>(a0);
+      uint4* dst = reinterpret_cast<uint4*>(s_bytes);
+      const uint32_t n16 = (uint32_t)((a1 - a0) >> 4);
+#pragma unroll 8
+      for (uint32_t k = tid; k < n16; k += nth) dst[k] = __ldg(src + k);
+      if (tid == 0) dst[n16] = make_uint4(0u, 0u, 0u, 0u);
+      staged = true;
+      __syncthreads();
+    }
+  }
+  // the stages, instantiated separately for the staged copy (shared loads) and global memory
+  auto validate = [&](const Cursor c) {
 
   // ---- stage A (thread 0): header up to the refs array ------------------------------------
   if (tid == 0) {
@@ -74,21 +135,21 @@ __global__ void __launch_bounds__(256) index_blocks_kernel(const uint8_t* __rest
     uint32_t ok = 1;
     do {
       if (c.len < 4) { fail(m, TOC_E_TRUNCATED, TOC_D_TRUNC, 0, 0); ok = 0; break; }
-      if (ld_u32_unaligned(c.p) != 0x31434F54u) { fail(m, TOC_E_BAD_MAGIC, TOC_D_MAGIC, 0, 0); ok = 0; break; }
+      if (gu32(c.p) != 0x31434F54u) { fail(m, TOC_E_BAD_MAGIC, TOC_D_MAGIC, 0, 0); ok = 0; break; }
       if (c.len < 13) { fail(m, TOC_E_TRUNCATED, TOC_D_TRUNC, 4, 0); ok = 0; break; }
-      const uint32_t version = __ldg(c.p + 4);
-      m.n_rows = ld_u32_unaligned(c.p + 5);
-      m.n_cols = ld_u32_unaligned(c.p + 9);
+      const uint32_t version = c.p[4];
+      m.n_rows = gu32(c.p + 5);
+      m.n_cols = gu32(c.p + 9);
       if (version != 1) { fail(m, TOC_E_BAD_VERSION, TOC_D_VERSION, version, 0); ok = 0; break; }
       int64_t off = 13;
       if (off + 4 > c.len) { fail(m, TOC_E_TRUNCATED, TOC_D_TRUNC, (uint32_t)off, 0); ok = 0; break; }
-      m.n_uniques = ld_u32_unaligned(c.p + off);
+      m.n_uniques = gu32(c.p + off);
       off += 4;
       if (off + 8 * (int64_t)m.n_uniques > c.len) { fail(m, TOC_E_TRUNCATED, TOC_D_TRUNC, (uint32_t)off, 0); ok = 0; break; }
       m.off_uniques = (uint32_t)off;
       off += 8 * (int64_t)m.n_uniques;
       if (off + 4 > c.len) { fail(m, TOC_E_TRUNCATED, TOC_D_TRUNC, (uint32_t)off, 0); ok = 0; break; }
-      const uint32_t i_count = ld_u32_unaligned(c.p + off);
+      const uint32_t i_count = gu32(c.p + off);
       off += 4;
       uint32_t cnt, w;
       int64_t payload, end;
@@ -115,10 +176,10 @@ __global__ void __launch_bounds__(256) index_blocks_kernel(const uint8_t* __rest
     const uint8_t* refs = c.p + sm.off_refs;
     const uint32_t wr = sm.w_refs, nu = sm.n_uniques, nI = sm.n_pairs;
     for (uint32_t i = tid; i < nI; i += nth)
-      if (ld_packed(refs, i, wr) >= nu) atomicMin(&s_first, i);
+      if (gpacked(refs, i, wr) >= nu) atomicMin(&s_first, i);
     __syncthreads();
     if (tid == 0 && s_first != 0xffffffffu) {
-      fail(sm, TOC_E_FORMAT, TOC_D_REF_RANGE, s_first, ld_packed(refs, s_first, wr));
+      fail(sm, TOC_E_FORMAT, TOC_D_REF_RANGE, s_first, gpacked(refs, s_first, wr));
       s_ok = 0;
     }
   }
@@ -129,7 +190,7 @@ __global__ void __launch_bounds__(256) index_blocks_kernel(const uint8_t* __rest
     do {
       int64_t off = m.off_codes;
       if (off + 4 > c.len) { fail(m, TOC_E_TRUNCATED, TOC_D_TRUNC, (uint32_t)off, 0); ok = 0; break; }
-      const uint32_t total_codes = ld_u32_unaligned(c.p + off);
+      const uint32_t total_codes = gu32(c.p + off);
       off += 4;
       uint32_t cnt, w;
       int64_t payload, end;
@@ -145,8 +206,8 @@ __global__ void __launch_bounds__(256) index_blocks_kernel(const uint8_t* __rest
       off = end;
       if (off != c.len) { fail(m, TOC_E_FORMAT, TOC_D_TRAILING, (uint32_t)(c.len - off), 0); ok = 0; break; }
       if ((int64_t)cnt != (int64_t)m.n_rows + 1) { fail(m, TOC_E_FORMAT, TOC_D_OFFS_COUNT, m.n_rows + 1, cnt); ok = 0; break; }
-      const uint32_t first = ld_packed(c.p + m.off_offsets, 0, m.w_offsets);
-      const uint32_t last = ld_packed(c.p + m.off_offsets, m.n_rows, m.w_offsets);
+      const uint32_t first = gpacked(c.p + m.off_offsets, 0, m.w_offsets);
+      const uint32_t last = gpacked(c.p + m.off_offsets, m.n_rows, m.w_offsets);
       if (first != 0 || last != total_codes) { fail(m, TOC_E_FORMAT, TOC_D_OFFS_SPAN, first, last); ok = 0; break; }
     } while (0);
     s_ok = ok;
@@ -157,7 +218,7 @@ __global__ void __launch_bounds__(256) index_blocks_kernel(const uint8_t* __rest
   const uint32_t wo = sm.w_offsets, n = sm.n_rows;
   if (s_ok) {  // ---- stage D: monotone offsets (physical.py:170-174) -------------------------
     for (uint32_t r = tid; r < n; r += nth)
-      if (ld_packed(offs, r, wo) > ld_packed(offs, r + 1, wo)) atomicMin(&s_first, r);
+      if (gpacked(offs, r, wo) > gpacked(offs, r + 1, wo)) atomicMin(&s_first, r);
     __syncthreads();
     if (tid == 0 && s_first != 0xffffffffu) {
       fail(sm, TOC_E_FORMAT, TOC_D_OFFS_MONO, s_first, 0);
@@ -172,13 +233,13 @@ __global__ void __launch_bounds__(256) index_blocks_kernel(const uint8_t* __rest
     const uint8_t* uniq = c.p + sm.off_uniques;
     const uint32_t wc = sm.w_cols, wr = sm.w_refs, nc = sm.n_cols;
     for (uint32_t i = tid; i < sm.n_pairs; i += nth) {
-      bool bad = ld_packed(cols, i, wc) >= nc;
-      if (!bad) bad = !isfinite(ld_f64_unaligned(uniq + 8u * ld_packed(refs, i, wr)));
+      bool bad = gpacked(cols, i, wc) >= nc;
+      if (!bad) bad = !isfinite(gf64(uniq + 8u * gpacked(refs, i, wr)));
       if (bad) atomicMin(&s_first, i);
     }
     __syncthreads();
     if (tid == 0 && s_first != 0xffffffffu) {
-      const uint32_t col = ld_packed(cols, s_first, wc);
+      const uint32_t col = gpacked(cols, s_first, wc);
       if (col >= nc) fail(sm, TOC_E_FORMAT, TOC_D_PAIR_COL, s_first, col);
       else fail(sm, TOC_E_FORMAT, TOC_D_PAIR_VAL, s_first, col);
       s_ok = 0;
@@ -203,8 +264,8 @@ __global__ void __launch_bounds__(256) index_blocks_kernel(const uint8_t* __rest
       const uint32_t r = base + tid;
       uint32_t lo = 0, hi = 0;
       if (r < n) {
-        lo = ld_packed(offs, r, wo);
-        hi = ld_packed(offs, r + 1, wo);
+        lo = gpacked(offs, r, wo);
+        hi = gpacked(offs, r + 1, wo);
       }
       const uint32_t v = hi > lo ? hi - lo - 1 : 0u;
       const uint32_t x = warp_excl_scan(v, lane);
@@ -220,7 +281,7 @@ __global__ void __launch_bounds__(256) index_blocks_kernel(const uint8_t* __rest
       const uint32_t D = s_carry + s_warp[warp] + x;
       if (r < n && hi > lo) {
         with_width(wk, [&]<int W>() {
-          SeqReader<W> rd;
+          GSeqReader<W> rd;
           rd.init(codes, lo);
           bool undef = false;
           for (uint32_t j = lo; j < hi; ++j) {
@@ -249,16 +310,19 @@ __global__ void __launch_bounds__(256) index_blocks_kernel(const uint8_t* __rest
         uint32_t lo = 0, hi = n;  // row containing flat position s_first
         while (hi - lo > 1) {
           const uint32_t mid = (lo + hi) / 2;
-          if (ld_packed(offs, mid, wo) <= s_first) lo = mid;
+          if (gpacked(offs, mid, wo) <= s_first) lo = mid;
           else hi = mid;
         }
         sm.corrupt = 1;
         sm.detail = TOC_D_UNDEF;
         sm.detail_a = lo;
-        sm.detail_b = ld_packed(codes, s_first, wk);
+        sm.detail_b = gpacked(codes, s_first, wk);
       }
     }
   }
+  };
+  if (staged) validate(Cursor{s_bytes + head, g.len});
+  else validate(g);
   __syncthreads();
   if (tid == 0) meta_out[b] = sm;
 }
@@ -270,7 +334,14 @@ extern "C" int toc_index_blocks(const uint8_t* d_arena, const int64_t* d_block_o
                                 void* stream) {
   if (n_blocks < 0) return TOC_E_ARG;
   if (n_blocks == 0) return TOC_OK;
-  toc::index_blocks_kernel<<<(unsigned)n_blocks, 256, 0, (cudaStream_t)stream>>>(d_arena, d_block_off, d_block_len,
-                                                                                n_blocks, d_meta);
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(toc::index_blocks_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)toc::kStageBytes) != cudaSuccess)
+      return TOC_E_CUDA;
+    attr = true;
+  }
+  toc::index_blocks_kernel<<<(unsigned)n_blocks, 256, toc::kStageBytes, (cudaStream_t)stream>>>(
+      d_arena, d_block_off, d_block_len, n_blocks, d_meta);
   return cudaGetLastError() == cudaSuccess ? TOC_OK : TOC_E_CUDA;
 }

@@ -242,7 +242,7 @@ class BatchSweep:
     blocks on the device, runs A.v and v^T.A for every batch (fused launches), and returns host
     arrays (R: concatenated row results, O: one n_cols row per batch).  The batches are split
     into chunks: the host->device copy of chunk k+1 (copy stream) overlaps validation and compute
-    of chunk k (compute stream).  This replaces the reference's per-batch loop over ``matvec`` /
+    of chunk k (compute stream) and the device->host copy of chunk k-1's results (third stream).  This replaces the reference's per-batch loop over ``matvec`` /
     ``vecmat`` (cli.py:340-356)."""
 
     def __init__(self, blocks_h: np.ndarray, block_off, block_len, chunks: int = 8):
@@ -280,8 +280,24 @@ class BatchSweep:
         self.O_d = torch.empty((max(nb, 1), max(self.n_cols, 1)), dtype=torch.float64, device="cuda")
         self.R_h = torch.empty_like(self.R_d, device="cpu").pin_memory()
         self.O_h = torch.empty_like(self.O_d, device="cpu").pin_memory()
-        self.meta_h = [torch.empty(c[0].meta_d.numel(), dtype=torch.uint8, pin_memory=True) for c in self.chunks]
+        # own streams: work on the legacy default stream would wait for every upload enqueued before it
         self.copy_stream = torch.cuda.Stream()
+        self.comp_stream = torch.cuda.Stream()
+        self.d2h_stream = torch.cuda.Stream()
+        # the native pipeline's chunk descriptors (toc_sweep_upload / toc_sweep_compute)
+        self.meta_all_h = torch.empty(max(nb, 1) * N.META_DTYPE.itemsize, dtype=torch.uint8, pin_memory=True)
+        self.cdesc = (N.TocSweepChunk * max(len(self.chunks), 1))()
+        for k, (arena, b0, b1, lo, hi, r0) in enumerate(self.chunks):
+            plan = arena.plan(N.TOC_MATVEC | N.TOC_VECMAT)
+            scratch = arena._scratch_for(plan)
+            d = self.cdesc[k]
+            d.byte_lo, d.byte_hi = lo, hi
+            d.d_arena = arena.data.data_ptr()
+            d.d_block_off, d.d_block_len = arena.block_off_d.data_ptr(), arena.block_len_d.data_ptr()
+            d.d_meta, d.d_row_base = arena.meta_d.data_ptr(), arena.row_base_d.data_ptr()
+            d.d_scratch = scratch.data_ptr() if scratch is not None else None
+            d.n_blocks, d.b0, d.row0, d.n_rows = arena.n_blocks, b0, r0, arena.n_rows_total
+            d.plan = plan
         self.h2d_bytes = nbytes + 8 * self.n_cols + 8 * self.n_rows
         self.d2h_bytes = 8 * self.n_rows + 8 * nb * self.n_cols + sum(c[0].meta_d.numel() for c in self.chunks)
 
@@ -290,38 +306,34 @@ class BatchSweep:
         return cls(np.asarray(blocks_h, np.uint8), block_off, block_len, chunks)
 
     def run(self, v, u):
+        """The first chunk's block bytes are enqueued and stream in while the host prepares v / u;
+        then the operands, the other chunks' bytes (all on one copy stream: host -> device copies
+        are served in submission order), every chunk's validation and fused A.v + v^T.A (each as
+        soon as its bytes and operands are in) and the result downloads (toc_sweep.cu)."""
         torch = self.torch
+        L = N.lib()
+        caller = torch.cuda.current_stream()
+        cs, comp, ds = self.copy_stream, self.comp_stream, self.d2h_stream
+        for st in (cs, comp, ds):
+            st.wait_stream(caller)  # the caller's earlier work on these buffers is done
+        n = len(self.chunks)
+        N.check(L.toc_sweep_upload(self.host.data_ptr(), self.dev.data_ptr(), self.cdesc, 0, min(n, 1), cs.cuda_stream),
+                "toc_sweep_upload")
         self.v_h.numpy()[: self.n_cols] = as_vector(v, self.n_cols, "vector")
         self.u_h.numpy()[: self.n_rows] = as_vector(u, self.n_rows, "vector")
-        comp = torch.cuda.current_stream()
-        cs = self.copy_stream
-        cs.wait_stream(comp)  # previous run's readers of the device buffers are done
-        ready = []
-        with torch.cuda.stream(cs):
-            self.v_d.copy_(self.v_h, non_blocking=True)
-            for arena, b0, b1, lo, hi, r0 in self.chunks:
-                self.dev[lo:hi].copy_(self.host[lo:hi], non_blocking=True)
-                nr = arena.n_rows_total
-                self.u_d[r0 : r0 + nr].copy_(self.u_h[r0 : r0 + nr], non_blocking=True)
-                ev = torch.cuda.Event()
-                ev.record(cs)
-                ready.append(ev)
-        for k, (arena, b0, b1, lo, hi, r0) in enumerate(self.chunks):
-            comp.wait_event(ready[k])
-            N.check(N.lib().toc_index_blocks(arena.data.data_ptr(), arena.block_off_d.data_ptr(),
-                                             arena.block_len_d.data_ptr(), arena.n_blocks, arena.meta_d.data_ptr(),
-                                             N.stream_handle()), "toc_index_blocks")
-            nr = arena.n_rows_total
-            arena.linalg(N.TOC_MATVEC | N.TOC_VECMAT, v=self.v_d[: self.n_cols], u=self.u_d[r0 : r0 + nr],
-                         R=self.R_d[r0 : r0 + nr], O=self.O_d[b0:b1])
-            self.R_h[r0 : r0 + nr].copy_(self.R_d[r0 : r0 + nr], non_blocking=True)
-            self.O_h[b0:b1].copy_(self.O_d[b0:b1], non_blocking=True)
-            self.meta_h[k].copy_(arena.meta_d, non_blocking=True)
-        comp.synchronize()
-        for k, (arena, *_rest) in enumerate(self.chunks):
-            meta = np.frombuffer(self.meta_h[k].numpy().tobytes(), dtype=N.META_DTYPE)[: arena.n_blocks]
-            if np.any(meta["status"] != N.TOC_OK) or np.any(meta["corrupt"] != 0):
-                arena.meta = meta.copy()
+        N.check(L.toc_sweep_operands(self.cdesc, n, self.n_cols, self.v_h.data_ptr(), self.v_d.data_ptr(),
+                                     self.u_h.data_ptr(), self.u_d.data_ptr(), cs.cuda_stream), "toc_sweep_operands")
+        N.check(L.toc_sweep_upload(self.host.data_ptr(), self.dev.data_ptr(), self.cdesc, min(n, 1), n, cs.cuda_stream),
+                "toc_sweep_upload")
+        N.check(L.toc_sweep_compute(self.cdesc, n, self.n_cols, self.v_d.data_ptr(), self.u_d.data_ptr(),
+                                    self.R_d.data_ptr(), self.R_h.data_ptr(), self.O_d.data_ptr(), self.O_h.data_ptr(),
+                                    self.meta_all_h.data_ptr(), comp.cuda_stream, ds.cuda_stream), "toc_sweep_compute")
+        ds.synchronize()
+        caller.wait_stream(ds)
+        meta = np.frombuffer(self.meta_all_h.numpy().tobytes(), dtype=N.META_DTYPE)[: self.n_blocks]
+        if np.any(meta["status"] != N.TOC_OK) or np.any(meta["corrupt"] != 0):
+            for arena, b0, b1, *_rest in self.chunks:
+                arena.meta = meta[b0:b1].copy()
                 arena.raise_format_errors()
                 arena.raise_corrupt()
         return self.R_h.numpy()[: self.n_rows], self.O_h.numpy()[: self.n_blocks, : self.n_cols]
