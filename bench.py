@@ -405,8 +405,9 @@ def run_mlp(rank: int, world: int, cpu_sample: bool):
     _, trace = train_mlp(ds, epochs=epochs)
     out.update({"steps_per_epoch": n // 250, "epoch_seconds": trace.seconds, "risk_per_epoch": trace.risks,
                 "wall_seconds_incl_compress_and_cache": time.perf_counter() - t0,
-                "mode": "per step: A.W1 and (delta^T.A)^T over the node-record cache (toc_matcache_*), dense tail "
-                        "as torch ops"})
+                "mode": "native epoch (toc_mlp_epoch, one CUDA graph): per step the batch decoded from the "
+                        "node-record cache into an L2-resident buffer, A.W1 and A^T.delta on the fp64 tensor cores "
+                        "(DMMA), softmax-CE tail and parameter updates in CUDA kernels"})
     if cpu_sample:
         out["cpu_port"] = cpu_mlp_sample(rp, c, v, y, n // 250)
     return out

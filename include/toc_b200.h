@@ -334,6 +334,25 @@ int toc_matcache_left(const uint8_t* d_entry, const TocBlockMeta* h_meta, int32_
                       const double* d_MT, double* d_out, void* d_scratch, int64_t scratch_bytes,
                       void* stream);
 
+/* ---- config-5 MLP epoch (oracle.train_mlp's step; first layer = kernels.py:177-234) ---------
+ * One epoch over the batches in order, four kernels per step on `stream` (toc_mlp.cu): A_b . W1
+ * and A_b^T . delta on the fp64 tensor cores over rows decoded from the node-record cache
+ * (toc_matcache_build), the softmax cross-entropy tail and the parameter updates.  Weights are
+ * updated in place.  h_cache_off / h_row_base / h_n_rows: host copies; d_labels: class ids (f64).
+ * k must be 10; dense = 1 only if every row has all m columns (the decode then skips zeroing);
+ * scratch: toc_mlp_scratch(max rows per batch, m, h, k). */
+/* Diagnostic: launch only the step kernels in mask (bit 0 decode, 1 right, 2 tail, 3 left; 15 =
+ * all, the default) -- for timing them in the stream; any other mask trains wrongly. */
+int toc_mlp_set_kernels(int32_t mask);
+/* 1 (default): toc_mlp_epoch captures the epoch's launches into a CUDA graph on its first call and
+ * replays it while the arguments (and the host arrays' contents) are unchanged; 0: plain launches. */
+int toc_mlp_set_graph(int32_t on);
+int toc_mlp_scratch(int32_t max_rows, int32_t m, int32_t h, int32_t k, int64_t* bytes);
+int toc_mlp_epoch(const uint8_t* d_cache, const int64_t* h_cache_off, const int64_t* h_row_base,
+                  const int32_t* h_n_rows, int64_t n_blocks, int32_t m, int32_t h, int32_t k,
+                  const double* d_labels, double* d_W1, double* d_b1, double* d_W2, double* d_b2, double lr,
+                  int32_t dense, void* d_scratch, int64_t scratch_bytes, void* stream);
+
 /* ---- decode (codec.py:262-292 node_sequence / decode; cli.py:194-221 verify) -----------------
  * Two passes with a plan from toc_plan(kind = TOC_MATVEC) and its scratch: toc_decode_counts writes
  * each row's pair count at d_row_nnz[row_base[b] + r]; the caller scans them into d_row_ptr

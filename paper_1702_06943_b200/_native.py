@@ -87,6 +87,8 @@ def lib():
     L.toc_matcache_right.argtypes = [P, P, P, I64, I64, I32, I32, P, P, P]
     L.toc_matcache_left_scratch.argtypes = [P, I32, I32, ctypes.POINTER(ctypes.c_int64)]
     L.toc_matcache_left.argtypes = [P, P, I32, I32, P, P, P, I64, P]
+    L.toc_mlp_scratch.argtypes = [I32, I32, I32, I32, ctypes.POINTER(ctypes.c_int64)]
+    L.toc_mlp_epoch.argtypes = [P, P, P, P, I64, I32, I32, I32, P, P, P, P, P, ctypes.c_double, I32, P, I64, P]
     L.toc_tree_arrays.argtypes = [P, P, P, I64, ctypes.POINTER(TocPlan), P, P, P, P, P, P, P, P]
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype or ctypes.c_int

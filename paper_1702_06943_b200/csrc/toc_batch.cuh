@@ -402,7 +402,8 @@ struct Batch {
 
   // Walk the codes of [j0, j1) of row r; visit(i) once per pair (i = first-layer id).
   // Two codes per iteration, their chains stepped in lockstep: the dependent shared loads of one
-  // chain overlap those of the other (the walk is latency-bound on these loads).
+  // chain overlap those of the other (the walk is latency-bound on these loads).  The visit is
+  // inlined at four sites, so this suits a cheap visit (A.v: one gather and an add).
   template <typename V>
   TOC_D void walk(uint32_t r, uint32_t lo, uint32_t hi, uint32_t db, uint32_t j0, uint32_t j1, V&& visit) const {
     uint32_t j = j0;
@@ -433,6 +434,28 @@ struct Batch {
     }
   }
 
+  // The same walk one node per iteration, the visit inlined once: for a costly visit (v^T.A: two
+  // dependent atomics), where walk's predicated duplicate sites cost more than its overlap gains.
+  // A code <= nI is a pair and ends its chain.
+  template <typename V>
+  TOC_D void walk_flat(uint32_t r, uint32_t lo, uint32_t hi, uint32_t db, uint32_t j0, uint32_t j1,
+                       V&& visit) const {
+    if (j0 >= j1) return;
+    uint32_t j = j0;
+    uint32_t x = (j + 1 < hi) ? pk.par(db + (j - lo)) : last[r];
+    for (;;) {
+      uint32_t par = 0, key = x;
+      if (x > nI) pk.get(x - 1 - nI, par, key);
+      visit(key);
+      if (par) {
+        x = par;
+        continue;
+      }
+      if (++j >= j1) break;
+      x = (j + 1 < hi) ? pk.par(db + (j - lo)) : last[r];
+    }
+  }
+
   // A.v with P1 in tab: emit(r, (A.v)[r]) once per row (by the row's first segment lane).
   template <typename E>
   TOC_D void matvec_rows(E&& emit) const {
@@ -456,7 +479,7 @@ struct Batch {
       if (!segment(k, r, lo, hi, db, j0, j1)) break;
       const long long w = __double2ll_rn(weight(r) * g_scale);
       if (w == 0) continue;
-      walk(r, lo, hi, db, j0, j1, [&](uint32_t i) { fix_add(tabw + 2 * i, w); });
+      walk_flat(r, lo, hi, db, j0, j1, [&](uint32_t i) { fix_add(tabw + 2 * i, w); });
     }
   }
 
@@ -471,7 +494,7 @@ struct Batch {
       const long long w = __double2ll_rn(weight(r) * g_scale);
       if (w == 0) continue;
       const uint32_t xl = (uint32_t)w, xh = (uint32_t)((unsigned long long)w >> 32);
-      walk(r, lo_, hi_, db, j0, j1, [&](uint32_t i) { fix_add_split(lo, hi, i, xl, xh); });
+      walk_flat(r, lo_, hi_, db, j0, j1, [&](uint32_t i) { fix_add_split(lo, hi, i, xl, xh); });
     }
   }
 

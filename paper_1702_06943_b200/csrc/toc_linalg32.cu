@@ -119,14 +119,14 @@ __global__ void __launch_bounds__(1024, 1) linalg32_kernel(Linalg32Args a) {
       if (ok) {
         const uint32_t wr = do_vm ? (uint32_t)__double2int_rn((double)a.u[rb + r] * g_scale) : 0u;
         if (do_mv && do_vm)
-          B.walk(r, lo, hi, db, j0, j1, [&](uint32_t i) {
+          B.walk_flat(r, lo, hi, db, j0, j1, [&](uint32_t i) {
             part += p1[i];
             atomicAdd(g + i, wr);
           });
         else if (do_mv)
           B.walk(r, lo, hi, db, j0, j1, [&](uint32_t i) { part += p1[i]; });
         else if (wr)
-          B.walk(r, lo, hi, db, j0, j1, [&](uint32_t i) { atomicAdd(g + i, wr); });
+          B.walk_flat(r, lo, hi, db, j0, j1, [&](uint32_t i) { atomicAdd(g + i, wr); });
       }
       if (do_mv) {
         __syncwarp();

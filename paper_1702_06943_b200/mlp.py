@@ -81,6 +81,8 @@ class _Net:
         self.arena.build_matcache()  # node records once per run: both first-layer products read them
         self.rb = self.arena.row_base
         self.nrows = self.arena.meta["n_rows"].astype(np.int64)
+        lens = np.diff(np.asarray(dataset.features.row_ptr))
+        self.dense_rows = bool(len(lens) and np.all(lens == dataset.n_cols))  # every row has all columns
 
     def first_layer(self, b, W1, h):  # A_b . W1
         return self.arena.matmat(0, W1, h, batch=b)
@@ -131,10 +133,42 @@ def train_nn(dataset: LabeledDataset, config, counter=None):
     return NnModel(w1=W1.cpu().numpy(), w2=W2.cpu().numpy()), trace
 
 
+def _native_epoch(net, hidden: int, classes: int):
+    """toc_mlp_epoch's closure over the run's fixed buffers, or None where it does not apply (its tail
+    kernel is built for 10 classes and keeps W2 plus 8 rows in shared memory)."""
+    import ctypes
+
+    if classes != 10 or 8 * (hidden * classes + 9 * classes + 16 * hidden) > 200 * 1024:
+        return None
+    torch = net.torch
+    L = N.lib()
+    a = net.arena
+    nrows = np.ascontiguousarray(net.nrows, np.int32)
+    nb = ctypes.c_int64(0)
+    N.check(L.toc_mlp_scratch(int(nrows.max(initial=0)), a.n_cols, hidden, classes, ctypes.byref(nb)),
+            "toc_mlp_scratch")
+    scratch = torch.empty(max(int(nb.value), 8), dtype=torch.uint8, device=a.data.device)
+    cache_off = np.ascontiguousarray(a.matcache_off[:-1], np.int64)
+    row_base = np.ascontiguousarray(net.rb, np.int64)
+    labels = net.batches.labels.to(torch.float64).contiguous()
+
+    def run(w1, b1, w2, b2, lr):
+        N.check(L.toc_mlp_epoch(a.matcache.data_ptr(), cache_off.ctypes.data, row_base.ctypes.data, nrows.ctypes.data,
+                                a.n_blocks, a.n_cols, hidden, classes, labels.data_ptr(), w1.data_ptr(), b1.data_ptr(),
+                                w2.data_ptr(), b2.data_ptr(), lr, int(net.dense_rows), scratch.data_ptr(),
+                                scratch.numel(),
+                                N.stream_handle()), "toc_mlp_epoch")
+
+    return run
+
+
 def train_mlp(dataset: LabeledDataset, hidden: int = 200, classes: int = 10, batch_size: int = 250,
-              learning_rate: float = 0.05, epochs: int = 5, seed: int = 0):
+              learning_rate: float = 0.05, epochs: int = 5, seed: int = 0, native: bool = True):
     """Config-5 MLP on compressed batches: labels are class ids 0..classes-1 (as floats).
-    Returns (MlpModel, LossTrace) with the mean cross-entropy over all rows after each epoch."""
+    Returns (MlpModel, LossTrace) with the mean cross-entropy over all rows after each epoch.
+    native: each epoch is one toc_mlp_epoch call (four kernels per step, first layer on the fp64
+    tensor cores); False, or a shape it does not cover: the per-step path (matmat kernels plus
+    torch ops for the dense tail).  Both compute the same step; results agree to fp64 rounding."""
     from .training import LossTrace
 
     net = _Net(dataset, batch_size, seed)
@@ -143,6 +177,7 @@ def train_mlp(dataset: LabeledDataset, hidden: int = 200, classes: int = 10, bat
     lr = float(learning_rate)
     trace = LossTrace()
     labels_all = net.batches.labels.long()
+    epoch_fn = _native_epoch(net, hidden, classes) if native else None
 
     def forward(z1):
         a1 = torch.relu(z1 + b1)
@@ -151,7 +186,9 @@ def train_mlp(dataset: LabeledDataset, hidden: int = 200, classes: int = 10, bat
     for _ in range(epochs):
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         start.record()
-        for b in range(net.arena.n_blocks):
+        if epoch_fn is not None:
+            epoch_fn(w1, b1, w2, b2, lr)
+        for b in range(net.arena.n_blocks if epoch_fn is None else 0):
             y = net.labels(b).long()
             a1, logits = forward(net.first_layer(b, w1, hidden))
             p = torch.softmax(logits, dim=1)

@@ -77,3 +77,35 @@ def test_matmat_per_batch_scratch_covers_every_batch(oracle):
         got = arena.matmat(0, M, 3, batch=b).cpu().numpy()
         want = oracle.Tree.from_encoding(enc).matmat_right(M.cpu().numpy())
         assert np.allclose(got, want, rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("n,batch,hidden", [(1000, 300, 200), (777, 250, 40), (500, 250, 13)])
+def test_cfg5_native_epoch_vs_cpu_restatement(oracle, n, batch, hidden):
+    """The native epoch (toc_mlp_epoch: DMMA first layer over decoded tiles, fused tail) against the
+    oracle's step: ragged last batches, hidden sizes that leave partial 8-wide tiles."""
+    from paper_1702_06943_b200 import synth
+    from paper_1702_06943_b200.matrix import LabeledDataset, SparseRowMatrix
+    from paper_1702_06943_b200.mlp import train_mlp
+
+    rp, c, v, y = synth.cfg5_dataset(n, seed=11)
+    ds = LabeledDataset(features=SparseRowMatrix.from_csr(784, rp, c, v), labels=y)
+    model, trace = train_mlp(ds, hidden=hidden, classes=10, batch_size=batch, learning_rate=0.05, epochs=2, seed=3)
+    (w1, b1, w2, b2), risks = oracle.train_mlp(rp, c, v, y, 784, hidden, 10, batch, 0.05, 2, 3)
+    assert np.all(np.abs(np.array(trace.risks) - np.array(risks)) <= REL * np.abs(risks)), (trace.risks, risks)
+    for got, want in ((model.w1, w1), (model.b1, b1), (model.w2, w2), (model.b2, b2)):
+        assert within_rel(got, want, REL), max_rel_err(got, want)
+
+
+def test_cfg5_native_equals_per_step_path():
+    """Both implementations of the step: the same curve and weights to fp64 rounding."""
+    from paper_1702_06943_b200 import synth
+    from paper_1702_06943_b200.matrix import LabeledDataset, SparseRowMatrix
+    from paper_1702_06943_b200.mlp import train_mlp
+
+    rp, c, v, y = synth.cfg5_dataset(1500, seed=5)
+    ds = LabeledDataset(features=SparseRowMatrix.from_csr(784, rp, c, v), labels=y)
+    m1, t1 = train_mlp(ds, hidden=200, epochs=2, native=True)
+    m2, t2 = train_mlp(ds, hidden=200, epochs=2, native=False)
+    assert np.allclose(t1.risks, t2.risks, rtol=1e-9, atol=0)
+    for a, b in zip((m1.w1, m1.b1, m1.w2, m1.b2), (m2.w1, m2.b1, m2.w2, m2.b2)):
+        assert within_rel(a, b, 1e-9), max_rel_err(a, b)
