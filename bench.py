@@ -225,7 +225,7 @@ def main():
     t_trees = time.perf_counter() - t0
 
     def step():
-        arena.linalg(kind, v=v, u=u, R=R, O=O, use_trees=True)
+        arena.linalg(kind, v=v, u=u, R=R, O=O)
 
     sampler = ClockSampler(local)
     if world > 1:
@@ -247,7 +247,14 @@ def main():
     mv_t = time_kernel(torch, lambda: arena.linalg(N.TOC_MATVEC, v=v, R=R), nsub, 3, flush)
     vm_t = time_kernel(torch, lambda: arena.linalg(N.TOC_VECMAT, u=u, O=O), nsub, 3, flush)
     # block-only mode: the tree is rebuilt from the TOC1 codes inside every launch
-    bo_t = time_kernel(torch, lambda: arena.linalg(kind, v=v, u=u, R=R, O=O, use_trees=False), nsub, 3, flush)
+    bo_t = time_kernel(torch, lambda: arena.linalg(kind, v=v, u=u, R=R, O=O, use_trees=False, use_levels=False),
+                       nsub, 3, flush)
+    # the level-cache kernel (toc_levels.cu): the alternative cached form, measured beside the headline
+    t0 = time.perf_counter()
+    levels = arena.build_levels()
+    t_levels = time.perf_counter() - t0
+    lv_t = (time_kernel(torch, lambda: arena.linalg(kind, v=v, u=u, R=R, O=O, use_levels=True), nsub, 3, flush)
+            if levels else None)
     # the fp32 variant (north_star: 1e-4 bar): same batches, fused single walk for both products
     v32, u32 = v.float(), u.float()
     R32 = torch.empty_like(R, dtype=torch.float32)
@@ -313,6 +320,13 @@ def main():
                            "note": "per-batch cache entry built once (the reference caches C' too, "
                                    "kernels.py:68-77): decode-tree prefix plus unpacked and column-sorted "
                                    "pair records; each launch reads it plus the TOC1 value index"},
+            "level_cache": None if not levels else {
+                "used_for_value": False, "bytes_per_gpu": arena.levels_bytes, "build_seconds": t_levels,
+                "ms_per_step": float(np.mean(lv_t)), "rows_per_s": world * rows_per_step / (np.mean(lv_t) / 1e3),
+                "roofline_frac": alg / (np.mean(lv_t) / 1e3) / 1e9 / peak,
+                "note": "toc_levels.cu: used nodes of C' renumbered breadth first (host-built once), the "
+                        "reference's H recurrence one tree level at a time, atomic-free fixed-order v^T.A; "
+                        "slower than the chain walk here (DESIGN.md 4.1)"},
             "block_only": {"ms_per_step": float(np.mean(bo_t)),
                            "rows_per_s": world * rows_per_step / (np.mean(bo_t) / 1e3),
                            "roofline_frac": alg / (np.mean(bo_t) / 1e3) / 1e9 / peak, "traffic": bo_traffic,

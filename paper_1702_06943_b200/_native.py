@@ -89,6 +89,15 @@ def lib():
     L.toc_matcache_left.argtypes = [P, P, I32, I32, P, P, P, I64, P]
     L.toc_mlp_scratch.argtypes = [I32, I32, I32, I32, ctypes.POINTER(ctypes.c_int64)]
     L.toc_mlp_epoch.argtypes = [P, P, P, P, I64, I32, I32, I32, P, P, P, P, P, ctypes.c_double, I32, P, I64, P]
+    L.toc_levels_build.restype = P
+    L.toc_levels_build.argtypes = [P, P, P, I64, I32]
+    L.toc_levels_info.argtypes = [P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int32)]
+    L.toc_levels_copy.argtypes = [P, P, P]
+    L.toc_levels_free.restype = None
+    L.toc_levels_free.argtypes = [P]
+    L.toc_levels_smem.restype = I64
+    L.toc_levels_smem.argtypes = [I32, I32, I32, I32, I32]
+    L.toc_linalg_levels.argtypes = [P, P, P, P, I64, I32, I32, I32, I32, I32, P, P, P, P, P, P, P]
     L.toc_tree_arrays.argtypes = [P, P, P, I64, ctypes.POINTER(TocPlan), P, P, P, P, P, P, P, P]
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype or ctypes.c_int
@@ -107,6 +116,13 @@ EXPORTS = ["toc_index_blocks", "toc_plan", "toc_linalg", "toc_linalg_trees", "to
 def check(rc: int, what: str) -> None:
     if rc != TOC_OK:
         raise NativeError(f"{what} failed with status {rc}")
+
+
+def device_info():
+    """(sm_count, max dynamic shared memory per CTA, L2 bytes) of the current device."""
+    sm, smem, l2 = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int64()
+    check(lib().toc_device_info(ctypes.byref(sm), ctypes.byref(smem), ctypes.byref(l2)), "toc_device_info")
+    return sm.value, smem.value, l2.value
 
 
 def require_cuda():

@@ -72,6 +72,7 @@ class BlockArena:
         self._plans: dict[int, N.TocPlan] = {}
         self._scratch = None
         self.trees = None  # device tree cache (build_trees)
+        self.levels = None  # level cache (build_levels)
 
     # ---- construction ------------------------------------------------------------------------
     @classmethod
@@ -227,10 +228,53 @@ class BlockArena:
         self.trees, self.tree_off_d, self.tree_bytes = trees, tree_off_d, int(off[-1])
         return self
 
-    def linalg(self, kind: int, v=None, u=None, R=None, O=None, use_trees: bool = True):
+    def build_levels(self, n_threads: int = 0) -> bool:
+        """Build the level cache (toc_levels_build, csrc/toc_levels.cu): per batch the used nodes
+        of C' renumbered breadth first, built once on the host from a copy of the arena -- the
+        counterpart of the reference's cached CompressedMatrix.tree (kernels.py:68-77).  Returns
+        False (and keeps no cache) when some batch needs ids wider than 16 bits or the tables do
+        not fit shared memory; linalg then uses the tree cache / block-only paths."""
+        torch = self.torch
+        self.raise_corrupt()
+        L = N.lib()
+        host = self.data.cpu().numpy()
+        h = L.toc_levels_build(host.ctypes.data_as(ctypes.c_void_p), self.block_off.ctypes.data_as(ctypes.c_void_p),
+                               self.meta.ctypes.data_as(ctypes.c_void_p), self.n_blocks, n_threads)
+        if not h:
+            raise N.NativeError("toc_levels_build failed")
+        try:
+            total, max_nodes = ctypes.c_int64(), ctypes.c_int32()
+            rc = L.toc_levels_info(h, ctypes.byref(total), ctypes.byref(max_nodes))
+            if rc == N.TOC_E_ARG:
+                self.levels = None
+                return False
+            N.check(rc, "toc_levels_build")
+            buf = np.zeros(int(total.value) + 16, np.uint8)
+            off = np.zeros(self.n_blocks + 1, np.int64)
+            N.check(L.toc_levels_copy(h, buf.ctypes.data_as(ctypes.c_void_p), off.ctypes.data_as(ctypes.c_void_p)),
+                    "toc_levels_copy")
+        finally:
+            L.toc_levels_free(h)
+        max_rows = int(self.meta["n_rows"].max()) if self.n_blocks else 0
+        max_uniq = int(self.meta["n_uniques"].max()) if self.n_blocks else 0
+        _, optin, _ = N.device_info()
+        need = L.toc_levels_smem(N.TOC_MATVEC | N.TOC_VECMAT, self.n_cols, max_nodes.value, max_rows, max_uniq)
+        if need > optin:
+            self.levels = None
+            return False
+        dev = self.data.device
+        self.levels = torch.from_numpy(buf).to(dev)
+        self.levels_off_d = torch.from_numpy(off).to(dev)
+        self.levels_bytes = int(total.value)
+        self.levels_dims = (max_nodes.value, max_rows, max_uniq)
+        return True
+
+    def linalg(self, kind: int, v=None, u=None, R=None, O=None, use_trees: bool = True, use_levels: bool = False):
         """kind = TOC_MATVEC | TOC_VECMAT.  v: device float64 [n_cols]; u: device float64
         [n_rows_total].  Returns (R [n_rows_total], O [n_blocks, n_cols]) device tensors.  Uses
-        the tree cache when it has been built (and use_trees), else rebuilds trees per call."""
+        the level cache when asked (use_levels) and built, else the tree cache when it has been
+        built (and use_trees), else rebuilds trees per call.  (The level kernel is the slower of
+        the two cached forms at config 2 -- DESIGN.md 4.1 -- so it is opt-in.)"""
         torch = self.torch
         self.raise_corrupt()
         dev = self.data.device
@@ -241,6 +285,16 @@ class BlockArena:
             if O is None:
                 O = torch.empty(max(self.n_blocks * self.n_cols, 1), dtype=torch.float64,
                                 device=dev)[: self.n_blocks * self.n_cols].view(self.n_blocks, self.n_cols)
+        if use_levels and getattr(self, "levels", None) is not None:
+            nodes, rows, uniq = self.levels_dims
+            rc = N.lib().toc_linalg_levels(
+                self.data.data_ptr(), self.block_off_d.data_ptr(), self.meta_d.data_ptr(), self.row_base_d.data_ptr(),
+                self.n_blocks, kind, self.n_cols, nodes, rows, uniq,
+                _ptr(v) if kind & N.TOC_MATVEC else None, _ptr(R) if kind & N.TOC_MATVEC else None,
+                _ptr(u) if kind & N.TOC_VECMAT else None, _ptr(O) if kind & N.TOC_VECMAT else None,
+                self.levels.data_ptr(), self.levels_off_d.data_ptr(), N.stream_handle())
+            N.check(rc, "toc_linalg_levels")
+            return R, O
         plan = self.plan(kind)
         scratch = self._scratch_for(plan)
         trees = self.trees is not None and use_trees

@@ -24,7 +24,7 @@ def _arena(blocks):
     return BlockArena.from_bytes(blocks)
 
 
-@pytest.fixture(params=["rebuild", "tree_cache"])
+@pytest.fixture(params=["rebuild", "tree_cache", "levels"])
 def tree_mode(request):
     return request.param
 
@@ -36,6 +36,10 @@ def _check_sweep(oracle, encs, v, seed=0, mode="rebuild"):
     arena = _arena(blocks)
     if mode == "tree_cache":
         arena.build_trees()
+    if mode == "levels":
+        # the level cache takes every narrow batch (ids < 65536); wider ones keep the other paths
+        built = arena.build_levels()
+        assert built or max(e.tree_length() for e in encs) > 65536
     trees = [oracle.Tree.from_encoding(e) for e in encs]
     n_total = sum(e.n_rows for e in encs)
     u = np.random.default_rng(seed).standard_normal(n_total)
@@ -44,7 +48,7 @@ def _check_sweep(oracle, encs, v, seed=0, mode="rebuild"):
     from paper_1702_06943_b200 import _native as N
 
     for kind in (N.TOC_MATVEC, N.TOC_VECMAT, N.TOC_MATVEC | N.TOC_VECMAT):
-        R, O = arena.linalg(kind, v=vd if kind & 1 else None, u=ud if kind & 2 else None)
+        R, O = arena.linalg(kind, v=vd if kind & 1 else None, u=ud if kind & 2 else None, use_levels=mode == "levels")
         torch.cuda.synchronize()
         base = 0
         for b, (e, t) in enumerate(zip(encs, trees)):
@@ -104,6 +108,16 @@ def test_cfg2_batches(oracle, tree_mode):
         encs.append(enc)
     v, _ = synth.cfg2_operands(0, 6)
     _check_sweep(oracle, encs, v, seed=3, mode=tree_mode)
+
+
+def test_levels_used_for_config2(oracle):
+    """Config-2 batches take the level-cache kernel (the bench's headline path)."""
+    from paper_1702_06943_b200 import synth
+
+    encs = [oracle.encode_csr(784, *synth.dense_to_csr(synth.cfg2_batch_dense(0, b))) for b in range(4)]
+    arena = _arena([oracle.serialize(e) for e in encs])
+    assert arena.build_levels()
+    assert arena.levels is not None and arena.levels_bytes > 0
 
 
 def test_empty_and_zero_rows(oracle, tree_mode):

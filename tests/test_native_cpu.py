@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def header_symbols():
     text = open(os.path.join(ROOT, "include", "toc_b200.h")).read()
-    return sorted(set(re.findall(r"^\s*(?:int|const char\*)\s+(toc_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:int64_t|int|void\s*\*|void|const char\s*\*)\s*(toc_\w+)\s*\(", text, re.M)))
 
 
 def test_library_exports_every_declared_symbol():

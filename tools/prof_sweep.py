@@ -13,6 +13,8 @@ p.add_argument("--batches", type=int, default=1024)
 p.add_argument("--kind", type=int, default=3)
 p.add_argument("--reps", type=int, default=3)
 p.add_argument("--trees", type=int, default=1)
+p.add_argument("--levels", type=int, default=0)
+p.add_argument("--prefetch", type=int, default=-1)
 a = p.parse_args()
 
 import torch  # noqa: E402
@@ -24,6 +26,11 @@ rp, c, v, br = bench.make_shard(0, a.batches)
 arena = compress_csr(bench.COLS, rp, c, v, br)
 if a.trees:
     arena.build_trees()
+if a.levels:
+    assert arena.build_levels()
+if a.prefetch >= 0:
+    from paper_1702_06943_b200 import _native as N
+    N.lib().toc_levels_set_prefetch(a.prefetch)
 vd = torch.randn(bench.COLS, dtype=torch.float64, device="cuda")
 ud = torch.randn(arena.n_rows_total, dtype=torch.float64, device="cuda")
 for _ in range(a.reps):
