@@ -52,9 +52,24 @@ TOC_HD BatchLayout batch_layout(const TocBlockMeta& m) {
 //   prec  (pair id, value ref) sorted by (column, pair id)    } v^T.A's output as a fixed-order
 //   segs  (start in prec, column) per distinct column, + end  } segmented sum, no atomics
 //   info  n_segs (0xffffffff: not sorted, the atomic scatter is used)
+//   splits (first code of each lane's range, relative to the row start) per (row, lane) for the
+//         S = seg_lanes(n_rows, kSplitThreads) lanes of a row, balanced by PAIR count (the
+//         lanes' flat walks then take equal numbers of iterations); info[1] = S
 struct CacheLayout {
-  uint32_t tree, off_irec, off_prec, off_segs, off_info, total;
+  uint32_t tree, off_irec, off_prec, off_segs, off_info, off_splits, total;
 };
+
+// Lanes per row: the largest power of two <= min(32, threads / rows).  Each thread then owns
+// one contiguous segment of one row, so the code stream is walked sequentially per thread.
+TOC_HD uint32_t seg_lanes(uint32_t n, uint32_t nthreads) {
+  uint32_t s = 1;
+  while (s < 32 && 2 * s * (n ? n : 1) <= nthreads) s <<= 1;
+  return s;
+}
+
+// The CTA size the cached lane splits are computed for (the sweep's plan for tables that need
+// most of shared memory); other CTA sizes fall back to code-count splits.
+constexpr uint32_t kSplitThreads = 1024;
 
 // A pair record (two small ids).  Narrow trees (< 65,536 nodes, n_cols <= 65,536: toc_plan) pack
 // both as u16 halves of one u32; wide ones use uint2.
@@ -93,6 +108,8 @@ TOC_HD CacheLayout cache_layout(const TocBlockMeta& m) {
   o += align16(8u * segs);
   C.off_info = o;
   o += 16u;
+  C.off_splits = o;
+  o += align16(2u * m.n_rows * seg_lanes(m.n_rows, kSplitThreads));
   C.total = o;
   return C;
 }
@@ -190,14 +207,6 @@ TOC_D void scan_derived_base(const uint32_t* rowoff, uint32_t* dbase, uint32_t n
   }
 }
 
-// Lanes per row: the largest power of two <= min(32, threads / rows).  Each thread then owns
-// one contiguous segment of one row, so the code stream is walked sequentially per thread.
-TOC_HD uint32_t seg_lanes(uint32_t n, uint32_t nthreads) {
-  uint32_t s = 1;
-  while (s < 32 && 2 * s * (n ? n : 1) <= nthreads) s <<= 1;
-  return s;
-}
-
 // ---- exact fixed-point accumulation with native 32-bit atomics -----------------------------
 // fp64 atomics are CAS loops on sm_100a (shared) and their order would make v^T.A
 // non-deterministic.  Each accumulator is a 64-bit two's-complement integer (lo, hi words)
@@ -218,6 +227,30 @@ TOC_D void fix_add(uint32_t* acc, long long x) {
 TOC_D void fix_add_split(uint32_t* lo, uint32_t* hi, uint32_t i, uint32_t xl, uint32_t xh) {
   const uint32_t old = atomicAdd(lo + i, xl);
   atomicAdd(hi + i, xh + (old + xl < old ? 1u : 0u));
+}
+
+// Carry-free variant (two "limbs", both added with fire-and-forget RED.ADD): an addend x (exact
+// integer, value * 2^F) is split as x = xh * 2^L + xl with 0 <= xl < 2^L; lo[i] sums the xl
+// unsigned and hi[i] the xh signed.  A pair gets at most one add per row, so with
+// L = 32 - bits(n_rows) the lo word cannot wrap; F is chosen so |sum of x| < 2^(L+30) and the hi
+// word cannot either.  Exact and order-independent like fix_add, without the dependent
+// return-value carry.
+TOC_D uint32_t limb_bits(uint32_t n_rows) { return 32u - (32u - __clz(n_rows ? n_rows : 1u)); }
+
+TOC_D double limb_scale(double bound, uint32_t L) {  // 2^F with |sum| <= bound -> < 2^(L+30)
+  if (!(bound > 0.0)) return 1.0;
+  int e;
+  frexp(bound, &e);
+  return ldexp(1.0, (int)L + 30 - e);
+}
+
+TOC_D void limb_add(uint32_t* lo, int32_t* hi, uint32_t i, uint32_t xl, int32_t xh) {
+  atomicAdd(lo + i, xl);
+  atomicAdd(hi + i, xh);
+}
+
+TOC_D double limb_value(uint32_t lo, int32_t hi, uint32_t L, double inv_scale) {
+  return (double)(((long long)hi << L) + (long long)lo) * inv_scale;
 }
 
 TOC_D double fix_value(uint32_t lo, uint32_t hi, double inv_scale) {
@@ -245,6 +278,7 @@ struct Batch {
   double* tab;     // P1 (matvec) or G (vecmat, fixed point), index = first-layer id
   uint32_t* tabw;  // tab as words
   PK<kWide> pk;
+  const uint16_t* splits = nullptr;  // cached pair-balanced lane splits (tree cache), or NULL
   uint32_t n, nI, S, lgS, RP, passes, sub, p0, p1;
   double vmax;     // max |value| over the value index (this thread's part until reduced)
 
@@ -304,10 +338,40 @@ struct Batch {
     lo = rowoff[r];
     hi = rowoff[r + 1];
     db = dbase[r];
+    if (splits) {
+      j0 = lo + __ldg(splits + r * S + sub);
+      j1 = sub + 1 < S ? lo + __ldg(splits + r * S + sub + 1) : hi;
+      return true;
+    }
     const uint32_t len = hi - lo;
     j0 = lo + ((len * sub) >> lgS);
     j1 = lo + ((len * (sub + 1)) >> lgS);
     return true;
+  }
+
+  // Pair-balanced splits of every row for S lanes (after the key pass; node tables complete):
+  // lane s starts at the first code whose preceding pairs reach s/S of the row's pairs.
+  TOC_D void write_splits(uint16_t* out, uint32_t S_) const {
+    for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
+      const uint32_t lo = rowoff[r], hi = rowoff[r + 1], db = dbase[r];
+      auto depth = [&](uint32_t j) {
+        uint32_t x = (j + 1 < hi) ? pk.par(db + (j - lo)) : last[r], dpt = 1;
+        while (x > nI) {
+          x = pk.par(x - 1 - nI);
+          ++dpt;
+        }
+        return dpt;
+      };
+      uint32_t total = 0;
+      for (uint32_t j = lo; j < hi; ++j) total += depth(j);
+      uint32_t acc = 0, s = 1;
+      out[r * S_] = 0;
+      for (uint32_t j = lo; j < hi && s < S_; ++j) {
+        while (s < S_ && (uint64_t)acc * S_ >= (uint64_t)total * s) out[r * S_ + s++] = (uint16_t)(j - lo);
+        acc += depth(j);
+      }
+      while (s < S_) out[r * S_ + s++] = (uint16_t)(hi - lo);
+    }
   }
 
   // The value index (and this thread's part of max |value|).  No barrier.
@@ -457,8 +521,12 @@ struct Batch {
   }
 
   // A.v with P1 in tab: emit(r, (A.v)[r]) once per row (by the row's first segment lane).
+  // (Code-count lane ranges: the lockstep two-chain walk measured no faster with the cached
+  // pair-balanced splits, which v^T.A's flat walk uses.)
   template <typename E>
-  TOC_D void matvec_rows(E&& emit) const {
+  TOC_D void matvec_rows(E&& emit) {
+    const uint16_t* sp = splits;
+    splits = nullptr;
     for (uint32_t k = 0; k < passes; ++k) {
       uint32_t r, lo, hi, db, j0, j1;
       double part = 0.0;
@@ -468,6 +536,7 @@ struct Batch {
       for (uint32_t o = S >> 1; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
       if (ok && sub == 0) emit(r, part);
     }
+    splits = sp;
   }
 
   // G[i] += sum over the pair occurrences of weight(r) (fixed point, scale g_scale); tab must be
@@ -498,12 +567,28 @@ struct Batch {
     }
   }
 
+  // G with carry-free limbs (limb_add): lo = tabw[0..nI], hi = tabw[nI+1..2nI+1]; tab zeroed.
+  template <typename Wt>
+  TOC_D void vecmat_rows_limbs(Wt&& weight, double g_scale, uint32_t L) {
+    uint32_t* lo = tabw;
+    int32_t* hi = reinterpret_cast<int32_t*>(tabw + (nI + 1));
+    for (uint32_t k = 0; k < passes; ++k) {
+      uint32_t r, lo_, hi_, db, j0, j1;
+      if (!segment(k, r, lo_, hi_, db, j0, j1)) break;
+      const long long w = __double2ll_rn(weight(r) * g_scale);
+      if (w == 0) continue;
+      const int32_t xh = (int32_t)(w >> L);
+      const uint32_t xl = (uint32_t)(w - ((long long)xh << L));
+      walk_flat(r, lo_, hi_, db, j0, j1, [&](uint32_t i) { limb_add(lo, hi, i, xl, xh); });
+    }
+  }
+
   // out[col] = sum over the column's pairs of value * G (split words), in (column, pair) order:
   // 4 lanes per column, a fixed shuffle tree.  prec / segs from the tree cache (global, in L2):
   // each lane issues its record loads as one batch, so a column costs one L2 round trip.
   template <typename Out>
   TOC_D void column_sums(const typename PairRec<kWide>::T* prec, const uint2* segs, uint32_t n_segs, double g_inv,
-                         Out&& out) const {
+                         Out&& out, uint32_t L = 0) const {
     using R = PairRec<kWide>;
     constexpr uint32_t U = 4;
     const uint32_t* lo = tabw;
@@ -524,7 +609,7 @@ struct Batch {
           for (uint32_t k = 0; k < U; ++k)
             if (q0 + 4 * k < end) {
               const uint32_t i = R::a(pr[k]) + 1;
-              c += uniq[R::b(pr[k])] * fix_value(lo[i], hi[i], g_inv);
+              c += uniq[R::b(pr[k])] * (L ? limb_value(lo[i], (int32_t)hi[i], L, g_inv) : fix_value(lo[i], hi[i], g_inv));
             }
         }
       }

@@ -25,6 +25,7 @@ struct LinalgArgs {
   uint8_t* scratch;
   const uint8_t* trees;     // optional device tree cache (toc_build_trees); NULL: rebuild per call
   const int64_t* tree_off;  // byte offset of batch b's tree prefix in `trees`
+  int32_t use_splits;       // cached pair-balanced lane splits + flat walk for A.v (tuning knob)
 };
 
 // One batch of the sweep.  `tables` points either into shared memory or into this CTA's slab.
@@ -54,6 +55,8 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
     segs = reinterpret_cast<const uint2*>(tree + CL.off_segs);
     n_segs = __ldg(reinterpret_cast<const uint32_t*>(tree + CL.off_info));
     B.init(blk, m, tables, in_smem ? nullptr : tree);
+    if (a.use_splits && __ldg(reinterpret_cast<const uint32_t*>(tree + CL.off_info) + 1) == B.S)
+      B.splits = reinterpret_cast<const uint16_t*>(tree + CL.off_splits);
     if (in_smem && tid == 0) bulk_load(tables, tree, CL.tree, mbar);
     B.load_values();
   } else {
@@ -81,7 +84,7 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
     if (do_vm) {
       double su = 0.0;
       for (uint32_t w = 0; w < (nth >> 5); ++w) su += s_red[w];
-      g_scale = fix_scale(su);
+      g_scale = n_segs != kNoSegs ? limb_scale(su, limb_bits(B.n)) : fix_scale(su);
       if (n_segs == kNoSegs) o_scale = fix_scale(su * block_max_d(B.vmax, s_red));  // fixed-point scatter only
     }
     if (do_mv) B.compute_p1_records(irec, kVecSmem ? vec_s : a.v);
@@ -108,16 +111,17 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
     }
     if (n_segs != kNoSegs) {
       // split-word G, then out[col] as a fixed-order segmented sum over the column-sorted pairs
-      B.vecmat_rows_split([&](uint32_t r) { return a.u[row_base + r]; }, g_scale);
+      const uint32_t L = limb_bits(B.n);
+      B.vecmat_rows_limbs([&](uint32_t r) { return a.u[row_base + r]; }, g_scale, L);
       __syncthreads();
       double* o = a.O + b * (int64_t)ncol;
       if (kVecSmem) {
         double* os = reinterpret_cast<double*>(acc_s);  // zeroed above: absent columns stay 0
-        B.column_sums(prec, segs, n_segs, 1.0 / g_scale, [&](uint32_t c, double x) { os[c] = x; });
+        B.column_sums(prec, segs, n_segs, 1.0 / g_scale, [&](uint32_t c, double x) { os[c] = x; }, L);
         __syncthreads();
         for (int32_t c = tid; c < ncol; c += nth) o[c] = os[c];
       } else {  // O zeroed by the host
-        B.column_sums(prec, segs, n_segs, 1.0 / g_scale, [&](uint32_t c, double x) { o[c] = x; });
+        B.column_sums(prec, segs, n_segs, 1.0 / g_scale, [&](uint32_t c, double x) { o[c] = x; }, L);
       }
       return;
     }
@@ -214,6 +218,12 @@ __global__ void __launch_bounds__(1024, 1) build_trees_kernel(LinalgArgs a) {
     __syncthreads();
     uint8_t* entry = const_cast<uint8_t*>(a.trees) + a.tree_off[b];
     const CacheLayout CL = cache_layout<kWide>(m);
+    {  // pair-balanced lane splits for kSplitThreads-thread CTAs (row offsets fit u16: rows <= n_cols)
+      const uint32_t S = seg_lanes(m.n_rows, kSplitThreads);
+      const bool ok = m.n_cols <= 65535u;
+      if (ok) B.write_splits(reinterpret_cast<uint16_t*>(entry + CL.off_splits), S);
+      if (threadIdx.x == 0) reinterpret_cast<uint32_t*>(entry + CL.off_info)[1] = ok ? S : 0u;
+    }
     const uint4* src = reinterpret_cast<const uint4*>(tables);
     uint4* dst = reinterpret_cast<uint4*>(entry);
     for (uint32_t k = threadIdx.x; k < L.tree / 16u; k += blockDim.x) dst[k] = src[k];
@@ -287,6 +297,8 @@ __global__ void __launch_bounds__(1024, 1) build_trees_kernel(LinalgArgs a) {
 // ------------------------------------------------------------------------------------------
 // Host side: planning and launch.
 namespace {
+
+int g_use_splits = 1;
 
 struct DevProps {
   int sm_count = 0, smem_optin = 0, smem_per_sm = 0;
@@ -394,6 +406,11 @@ extern "C" int toc_linalg(const uint8_t* d_arena, const int64_t* d_block_off, co
                           d_scratch, nullptr, nullptr, stream);
 }
 
+extern "C" int toc_linalg_set_splits(int on) {
+  g_use_splits = on ? 1 : 0;
+  return TOC_OK;
+}
+
 extern "C" int toc_tree_offsets(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t wide, int64_t* h_tree_off) {
   if (!h_meta || !h_tree_off || n_blocks < 0) return TOC_E_ARG;
   int64_t o = 0;
@@ -460,6 +477,7 @@ extern "C" int toc_linalg_trees(const uint8_t* d_arena, const int64_t* d_block_o
   a.scratch = (uint8_t*)d_scratch;
   a.trees = d_trees;
   a.tree_off = d_tree_off;
+  a.use_splits = g_use_splits;
   if ((kind & TOC_VECMAT) && !plan->vec_in_smem) {
     if (cudaMemsetAsync(d_O, 0, sizeof(double) * (size_t)n_blocks * plan->n_cols, s) != cudaSuccess)
       return TOC_E_CUDA;

@@ -15,6 +15,7 @@ p.add_argument("--reps", type=int, default=3)
 p.add_argument("--trees", type=int, default=1)
 p.add_argument("--levels", type=int, default=0)
 p.add_argument("--prefetch", type=int, default=-1)
+p.add_argument("--splits", type=int, default=-1)
 a = p.parse_args()
 
 import torch  # noqa: E402
@@ -28,6 +29,9 @@ if a.trees:
     arena.build_trees()
 if a.levels:
     assert arena.build_levels()
+if a.splits >= 0:
+    from paper_1702_06943_b200 import _native as N
+    N.lib().toc_linalg_set_splits(a.splits)
 if a.prefetch >= 0:
     from paper_1702_06943_b200 import _native as N
     N.lib().toc_levels_set_prefetch(a.prefetch)
