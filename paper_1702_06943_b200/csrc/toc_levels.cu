@@ -5,23 +5,29 @@
 // Algorithm 6: H[code] += u[row]; descending i: out[col[i]] += value[i]*H[i], H[parent[i]] += H[i]).
 //
 // The chain-walk kernel (toc_linalg.cu) visits every non-zero through a lane's private pointer
-// chase: lanes of a warp walk chains of different lengths, so many issue slots idle, and v^T.A's
-// scatter needs shared-memory atomics.  Here the tree is evaluated the way the reference's own
-// recurrences run -- node by node -- but one LEVEL (tree depth) at a time, every lane busy:
+// chase (two random shared-memory reads per non-zero, lanes diverging on chain lengths).  Here the
+// tree is evaluated the way the reference's own recurrences run -- node by node, one tree depth at
+// a time -- so each used node is touched once:
 //
 //   cache entry (built once per arena on the host, the counterpart of the reference's cached
 //   CompressedMatrix.tree, kernels.py:68-77): only the nodes some code uses (every parent of a
 //   derived node is itself a code, so that set is closed under parents), renumbered breadth
 //   first: the |I| pairs sorted by column, then depth-2 nodes, depth-3 nodes, ..., each level
-//   sorted by its parents' new ids so siblings are contiguous.
+//   sorted by its parents' new ids, so siblings are contiguous and every subtree occupies one
+//   contiguous range per level.  The pairs (roots) are cut into 32 slices of similar subtree
+//   weight, one per warp: the tree phases run warp by warp with no block-wide barrier per level.
 //
 //   A.v   P1[p] = value_p * v[col_p]                 pairs
-//         H[x]  = P1[key_x] + H[par_x]                level 2, 3, ... (the reference's H, same operands)
+//         H[x]  = P1[key_x] + H[par_x]                warp-local, depth 2, 3, ... (the reference's H)
 //         R[r]  = sum of H over row r's codes         one warp per row
 //   v^T.A S[x]  = sum of u[r] over x's occurrences   node-indexed occurrence rows
-//         S[p] += sum of S over p's children          levels max..2, one thread per sibling run
-//         O[c]  = sum over the pairs p of column c of value_p * (S[p] + sum of S[x] over the derived
-//                 x whose key is p)                   pairs are column-sorted: a column is a range
+//         S[p] += sum of S over p's children          warp-local, depth max..2
+//         G[p]  = S[p] + sum of S[x] over the derived x keyed by p
+//         O[c]  = sum over column c's pairs of value_p * G[p]   (pairs are column-sorted: a range)
+//   The three scatters (children -> parent, derived node -> key pair, occurrence -> node) walk
+//   lists sorted by their target, 32 entries per warp step, and reduce equal targets with a warp
+//   segmented scan before one plain read-modify-write per target (a target split across steps is
+//   finished by the same warp in its next step).
 // No atomics, every sum has a fixed order (deterministic fp64), and the only shared table is one
 // fp64 slot per used node (H, then S).  DESIGN.md section 4.1.
 #include <algorithm>
@@ -34,25 +40,44 @@
 
 namespace toc {
 
+constexpr uint32_t kSlices = 32;  // one per warp of the 1024-thread CTA
+
 // Entry header (80 B); section offsets relative to the entry start, 16-B aligned.
 struct LvlHdr {
   uint32_t nP, nD, N, C;       // pairs, used derived nodes, N = nP + nD, codes
   uint32_t n_rows, maxd;       // rows; levels (depth of the deepest used node)
-  uint32_t n_multi, n_runs;    // multi-occurrence records; sibling runs
-  uint32_t n_csegs;            // distinct pair columns
+  uint32_t n_multi, n_segs;    // multi-occurrence records; distinct pair columns
   uint32_t off_lvl;            // u32[maxd + 1]: first new id of depth 1, 2, ..., then N
-  uint32_t off_runlvl;         // u32[maxd + 1]: first run of the children at each level
   uint32_t off_prs;            // u32[nP]: column | value ref << 16 (pairs in new, column order)
   uint32_t off_nrec;           // u32[nD]: par | key << 16 (new ids; key is a pair)
   uint32_t off_codes;          // u16[C]: the code stream in new ids (row offsets: the TOC1 block)
   uint32_t off_occ;            // u8/u16[N]: the one row a node occurs in, or none / multi
   uint32_t off_multi;          // u32[n_multi]: node | row << 16, sorted by (node, row)
-  uint32_t off_runs;           // u32[n_runs]: first child | parent << 16, per level by parent
-  uint32_t off_kstart;         // u16[nP + 1]: start in kl of the derived nodes keyed by each pair
-  uint32_t off_kl;             // u16[nD]: derived nodes sorted by (key, node)
-  uint32_t off_csegs;          // u32[n_csegs + 1]: first pair | column << 16; sentinel nP
+  uint32_t off_slnode;         // u16[maxd][33]: per depth-(d+1) level, first node of each slice
+  uint32_t off_kl;             // u16[nD]: derived nodes sorted by (key pair, node)
+  uint32_t off_wsplit;         // u16[2][33]: per warp, first kl entry / first multi record (cut at
+                               // key / node boundaries)
+  uint32_t off_segs;           // u32[n_segs + 1]: first pair | column << 16; sentinel nP
+  uint32_t pad[2];
 };
 static_assert(sizeof(LvlHdr) == 80, "level cache header");
+
+// Warp step of a scatter whose targets arrive sorted: lanes with equal `key` (contiguous) are
+// summed by a segmented inclusive scan; returns true on the lane that holds its segment's sum
+// (the segment's last lane in this step).  Invalid lanes must carry distinct keys.
+TOC_D bool seg_reduce(double& v, uint32_t key, uint32_t lane) {
+  // Hillis-Steele steps, stopping at the first distance no segment spans (segments are short)
+#pragma unroll 1
+  for (uint32_t o = 1; o < 32; o <<= 1) {
+    const uint32_t k = __shfl_up_sync(0xffffffffu, key, o);
+    const bool same = lane >= o && k == key;
+    if (__ballot_sync(0xffffffffu, same) == 0u) break;
+    const double t = __shfl_up_sync(0xffffffffu, v, o);
+    if (same) v += t;
+  }
+  const uint32_t knext = __shfl_down_sync(0xffffffffu, key, 1);
+  return lane == 31 || knext != key;
+}
 
 TOC_HD uint32_t occ_none(uint32_t w) { return w == 1 ? 0xffu : 0xffffu; }
 TOC_HD uint32_t occ_multi(uint32_t w) { return w == 1 ? 0xfeu : 0xfffeu; }
@@ -74,6 +99,7 @@ struct LvlArgs {
 };
 
 TOC_D uint32_t ld16(const uint16_t* p) { return __ldg(p); }
+TOC_D uint32_t ld32(const uint32_t* p) { return __ldg(p); }
 
 // TMA bulk copy global -> shared completing on mbar (the caller announced the bytes).
 TOC_D void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
@@ -82,13 +108,11 @@ TOC_D void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* mbar)
                "l"(src), "r"(bytes), "r"(smem_u32(mbar))
                : "memory");
 }
-TOC_D uint32_t ld32(const uint32_t* p) { return __ldg(p); }
 
-// U loads in flight per thread: every phase streams its records with U independent loads issued
-// before any is used (one CTA per SM holds the whole table, so latency is hidden by ILP, not by
-// other CTAs).
-constexpr uint32_t kU = 4;
-__constant__ int g_prefetch_mode = 0;  // tuning knob: L2 prefetch of the next entry (measured: costs DRAM re-reads)
+constexpr uint32_t kU = 4;  // independent loads in flight per thread in the streaming phases
+// L2 prefetch knob: 3 (default) = this batch's later sections at its start (measured 338 -> 310 us);
+// 1 = the next batch's whole entry (measured: +90 MB DRAM re-reads, no gain); 0 = none.
+__constant__ int g_prefetch_mode = 3;
 
 template <int kKind, int OW>
 __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
@@ -125,37 +149,42 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
     const TocBlockMeta& mg = a.meta[b];
     const uint32_t nU = mg.n_uniques, off_uniq = mg.off_uniques;
     const int64_t rb = a.row_base[b];
-    if (g_prefetch_mode && tid == 0 && b + gridDim.x < a.n_blocks) {
+    if (g_prefetch_mode == 3 && tid == 0) {  // this batch's later sections, ahead of their phases
+      const uint32_t from = h.off_codes, ebytes = (uint32_t)(a.lvl_off[b + 1] - a.lvl_off[b]);
+      if (ebytes > from)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ent + from), "r"((ebytes - from) & ~15u)
+                     : "memory");
+    }
+    if (g_prefetch_mode == 1 && tid == 0 && b + gridDim.x < a.n_blocks) {
       const int64_t bn = b + gridDim.x;
       const uint32_t ebytes = (uint32_t)(a.lvl_off[bn + 1] - a.lvl_off[bn]) & ~15u;
       if (ebytes)
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.lvl + a.lvl_off[bn]), "r"(ebytes) : "memory");
     }
-    // sections the level loops read (parent/key records; sibling runs and key lists) go to shared
-    // memory by TMA when they fit the staging area, overlapped with the streaming phases before them
-    const uint32_t nrec_bytes = align16(4u * h.nD), runs_bytes = align16(4u * h.n_runs), kl_bytes = align16(2u * h.nD);
-    const bool st_nrec = MV && h.nD && nrec_bytes <= stage_bytes;
-    const bool st_runs = VM && h.n_runs && runs_bytes <= stage_bytes;
-    const bool st_kl = VM && h.nD && runs_bytes + kl_bytes <= stage_bytes;
-    auto stage_vm = [&]() {  // one thread; one mbarrier phase for both copies
-      if (!st_runs && !st_kl) return;
+    // the parent/key records (read by every tree phase) go to shared memory by TMA when they fit the
+    // staging area, overlapped with the streaming phases before their first use
+    const uint32_t nrec_bytes = align16(4u * h.nD);
+    const bool st_nrec = h.nD && nrec_bytes <= stage_bytes;
+    if (tid == 0 && st_nrec) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)),
-                   "r"((st_runs ? runs_bytes : 0u) + (st_kl ? kl_bytes : 0u))
-                   : "memory");
-      if (st_runs) bulk_copy(stage, ent + h.off_runs, runs_bytes, mbar);
-      if (st_kl) bulk_copy(stage + runs_bytes, ent + h.off_kl, kl_bytes, mbar);
-    };
-    if (tid == 0) {
-      if (st_nrec) bulk_load(stage, ent + h.off_nrec, nrec_bytes, mbar);
-      else if (!MV) stage_vm();
+      asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(smem_u32(mbar)), "r"(nrec_bytes) : "memory");
+      bulk_copy(stage, ent + h.off_nrec, nrec_bytes, mbar);
     }
+    bool nrec_pending = st_nrec;
+    const uint32_t* nrec = st_nrec ? reinterpret_cast<const uint32_t*>(stage)
+                                   : reinterpret_cast<const uint32_t*>(ent + h.off_nrec);
+    auto nrec_wait = [&]() {  // before the barrier that precedes nrec's first use
+      if (nrec_pending) {
+        mbar_wait(mbar, phase);
+        phase ^= 1u;
+        nrec_pending = false;
+      }
+    };
     for (uint32_t i = tid; i < nU; i += nth) uniq_s[i] = ld_f64_unaligned(blk + off_uniq + 8u * i);
     if (VM)
       for (uint32_t r = tid; r < h.n_rows; r += nth) u_s[r] = a.u[rb + r];
-    const uint32_t* lvl = reinterpret_cast<const uint32_t*>(ent + h.off_lvl);
-    const uint32_t* nrec = st_nrec ? reinterpret_cast<const uint32_t*>(stage)
-                                   : reinterpret_cast<const uint32_t*>(ent + h.off_nrec);
+    const uint16_t* slnode = reinterpret_cast<const uint16_t*>(ent + h.off_slnode);
+    const uint16_t* wsplit = reinterpret_cast<const uint16_t*>(ent + h.off_wsplit);
     const uint32_t* prs = reinterpret_cast<const uint32_t*>(ent + h.off_prs);
     const uint32_t nP = h.nP, N = h.N;
     __syncthreads();
@@ -170,27 +199,19 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
         for (uint32_t k = 0; k < U; ++k)
           if (p0 + k * nth < nP) tab[p0 + k * nth] = uniq_s[r[k] >> 16] * v_s[r[k] & 0xffffu];
       }
+      nrec_wait();
       __syncthreads();
-      // H[x] = P1[key] + H[par], level by level (Algorithm 5's recurrence, same operands)
-      if (st_nrec) {
-        mbar_wait(mbar, phase);
-        phase ^= 1u;
-      }
+      // H[x] = P1[key] + H[par] (Algorithm 5's recurrence, same operands), this warp's slice of
+      // every level in turn; parents are in the same slice one level up
       for (uint32_t d = 1; d < h.maxd; ++d) {
-        const uint32_t lo = ld32(lvl + d), hi = ld32(lvl + d + 1);
-        for (uint32_t x0 = lo + tid; x0 < hi; x0 += U * nth) {
-          uint32_t r[U];
-#pragma unroll
-          for (uint32_t k = 0; k < U; ++k) r[k] = x0 + k * nth < hi ? nrec[x0 + k * nth - nP] : 0u;
-#pragma unroll
-          for (uint32_t k = 0; k < U; ++k)
-            if (x0 + k * nth < hi) tab[x0 + k * nth] = tab[r[k] >> 16] + tab[r[k] & 0xffffu];
+        const uint32_t lo = ld16(slnode + d * (kSlices + 1) + warp), hi = ld16(slnode + d * (kSlices + 1) + warp + 1);
+        for (uint32_t x = lo + lane; x < hi; x += 32) {
+          const uint32_t rec = nrec[x - nP];
+          tab[x] = tab[rec >> 16] + tab[rec & 0xffffu];
         }
-        __syncthreads();
+        __syncwarp();
       }
-      if (VM && tid == 0) {
-        stage_vm();  // the staged records are no longer read (barrier above)
-      }
+      __syncthreads();
       // R[r] = sum of H over the row's codes: one warp per row, U codes in flight per lane
       const uint8_t* offs = blk + mg.off_offsets;
       const uint32_t wo = mg.w_offsets;
@@ -215,7 +236,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
     if (VM) {
       double* o = a.O + b * (int64_t)ncol;
       for (int32_t c = tid; c < ncol; c += nth) o[c] = 0.0;  // columns no pair touches
-      // S[x] = sum of u over x's occurrences as a code
+      // S[x] = u of the one row x occurs in (nodes with several occurrences below; none: 0)
       const OccT* occ = reinterpret_cast<const OccT*>(ent + h.off_occ);
       for (uint32_t x0 = tid; x0 < N; x0 += U * nth) {
         uint32_t r[U];
@@ -227,82 +248,79 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
           else if (r[k] == kNone) tab[x0 + k * nth] = 0.0;
         }
       }
+      // nodes with several occurrences: this warp's range of (node, row) records, summed in row order
       const uint32_t* mrec = reinterpret_cast<const uint32_t*>(ent + h.off_multi);
-      for (uint32_t k = tid; k < h.n_multi; k += nth) {  // nodes with several occurrences: the first
-        const uint32_t e = ld32(mrec + k), x = e & 0xffffu;  // record of a run sums it in row order
-        if (k > 0 && (ld32(mrec + k - 1) & 0xffffu) == x) continue;
-        double s = u_s[e >> 16];
-        for (uint32_t q = k + 1; q < h.n_multi; ++q) {
-          const uint32_t f = ld32(mrec + q);
-          if ((f & 0xffffu) != x) break;
-          s += u_s[f >> 16];
+      {
+        const uint32_t q0 = ld16(wsplit + (kSlices + 1) + warp), q1 = ld16(wsplit + (kSlices + 1) + warp + 1);
+        uint32_t carry = 0xffffffffu;  // node of the previous step's last record
+        for (uint32_t q = q0; q < q1; q += 32) {
+          const bool ok = q + lane < q1;
+          const uint32_t e = ok ? ld32(mrec + q + lane) : 0u;
+          const uint32_t x = ok ? e & 0xffffu : 0xffff0000u + lane;
+          double s = ok ? u_s[e >> 16] : 0.0;
+          const uint32_t x0 = __shfl_sync(0xffffffffu, x, 0);
+          if (seg_reduce(s, x, lane) && ok) {
+            if (x == carry && x == x0) tab[x] += s;  // continues the previous step's run
+            else tab[x] = s;
+          }
+          carry = __shfl_sync(0xffffffffu, x, 31);
+          __syncwarp();
         }
-        tab[x] = s;
+      }
+      nrec_wait();
+      __syncthreads();
+      // bottom-up, this warp's slice: S[par] += S[x] for depth max .. 2 (children sorted by parent)
+      for (uint32_t d = h.maxd - 1; d >= 1 && d < h.maxd; --d) {
+        const uint32_t lo = ld16(slnode + d * (kSlices + 1) + warp), hi = ld16(slnode + d * (kSlices + 1) + warp + 1);
+        for (uint32_t x0 = lo; x0 < hi; x0 += 32) {
+          const uint32_t x = x0 + lane;
+          const bool ok = x < hi;
+          const uint32_t p = ok ? nrec[x - nP] & 0xffffu : 0xffff0000u + lane;
+          double s = ok ? tab[x] : 0.0;
+          if (seg_reduce(s, p, lane) && ok) tab[p] += s;
+          __syncwarp();
+        }
       }
       __syncthreads();
-      // bottom-up: each parent adds its children's subtree sums (one sibling run per parent, in order)
-      const uint32_t* runlvl = reinterpret_cast<const uint32_t*>(ent + h.off_runlvl);
-      const uint32_t* runs = st_runs ? reinterpret_cast<const uint32_t*>(stage)
-                                     : reinterpret_cast<const uint32_t*>(ent + h.off_runs);
-      if (st_runs || st_kl) {
-        mbar_wait(mbar, phase);
-        phase ^= 1u;
-      }
-      for (uint32_t d = h.maxd - 1; d >= 1 && d < h.maxd; --d) {
-        const uint32_t k0 = ld32(runlvl + d), k1 = ld32(runlvl + d + 1), hi = ld32(lvl + d + 1);
-        for (uint32_t q0 = k0 + tid; q0 < k1; q0 += U * nth) {
-          uint32_t e[U], f[U];
-#pragma unroll
-          for (uint32_t k = 0; k < U; ++k) {
-            const uint32_t q = q0 + k * nth;
-            e[k] = q < k1 ? runs[q] : 0u;
-            f[k] = q + 1 < k1 ? runs[q + 1] & 0xffffu : hi;
-          }
-#pragma unroll
-          for (uint32_t k = 0; k < U; ++k) {
-            if (q0 + k * nth >= k1) continue;
-            double s = 0.0;
-            for (uint32_t y = e[k] & 0xffffu; y < f[k]; ++y) s += tab[y];
-            tab[e[k] >> 16] += s;
-          }
+      // G[p] = S[p] + sum of S[x] over the derived x keyed by p: this warp's range of the key-sorted
+      // derived nodes
+      const uint16_t* kl = reinterpret_cast<const uint16_t*>(ent + h.off_kl);
+      {
+        const uint32_t k0 = ld16(wsplit + warp), k1 = ld16(wsplit + warp + 1);
+        for (uint32_t k = k0; k < k1; k += 32) {
+          const bool ok = k + lane < k1;
+          const uint32_t x = ok ? ld16(kl + k + lane) : 0u;
+          const uint32_t p = ok ? nrec[x - nP] >> 16 : 0xffff0000u + lane;
+          double s = ok ? tab[x] : 0.0;
+          if (seg_reduce(s, p, lane) && ok) tab[p] += s;
+          __syncwarp();
         }
-        __syncthreads();
       }
-      // O[c] = sum over column c's pairs p of value_p * (S[p] + sum of S[x] over the derived x keyed
-      // by p), in (pair, node) order: 4 lanes per column, a fixed shuffle tree
-      const uint16_t* kstart = reinterpret_cast<const uint16_t*>(ent + h.off_kstart);
-      const uint16_t* kl = st_kl ? reinterpret_cast<const uint16_t*>(stage + runs_bytes)
-                                 : reinterpret_cast<const uint16_t*>(ent + h.off_kl);
-      const uint32_t* csegs = reinterpret_cast<const uint32_t*>(ent + h.off_csegs);
-      const uint32_t quads = nth >> 2, span = ((h.n_csegs + quads - 1) / quads) * quads;
+      __syncthreads();
+      // O[c] = sum over column c's pairs p (a contiguous range) of value_p * G[p], in pair order:
+      // 4 lanes per column, a fixed shuffle tree
+      const uint32_t* segs = reinterpret_cast<const uint32_t*>(ent + h.off_segs);
+      const uint32_t quads = nth >> 2, span = ((h.n_segs + quads - 1) / quads) * quads;
       for (uint32_t s = tid >> 2; s < span; s += quads) {
         double c = 0.0;
         uint32_t col = 0;
-        if (s < h.n_csegs) {
-          const uint32_t sg = ld32(csegs + s), end = ld32(csegs + s + 1) & 0xffffu;
+        if (s < h.n_segs) {
+          const uint32_t sg = ld32(segs + s), end = ld32(segs + s + 1) & 0xffffu;
           col = sg >> 16;
-          for (uint32_t p0 = (sg & 0xffffu) + (tid & 3u); p0 < end; p0 += 4 * U) {
-            uint32_t pr[U], ks[U], ke[U];
-#pragma unroll
-            for (uint32_t k = 0; k < U; ++k) {
-              const uint32_t p = p0 + 4 * k;
-              pr[k] = p < end ? ld32(prs + p) : 0u;
-              ks[k] = p < end ? ld16(kstart + p) : 0u;
-              ke[k] = p < end ? ld16(kstart + p + 1) : 0u;
-            }
-#pragma unroll
-            for (uint32_t k = 0; k < U; ++k) {
-              if (p0 + 4 * k >= end) continue;
-              double g = tab[p0 + 4 * k];
-              for (uint32_t q = ks[k]; q < ke[k]; ++q) g += tab[kl[q]];
-              c += uniq_s[pr[k] >> 16] * g;
-            }
+          uint32_t p = (sg & 0xffffu) + (tid & 3u);
+          for (; p + 4 < end; p += 8) {
+            const uint32_t r0 = ld32(prs + p), r1 = ld32(prs + p + 4);
+            c += uniq_s[r0 >> 16] * tab[p];
+            c += uniq_s[r1 >> 16] * tab[p + 4];
           }
+          if (p < end) c += uniq_s[ld32(prs + p) >> 16] * tab[p];
         }
         c += __shfl_xor_sync(0xffffffffu, c, 1);
         c += __shfl_xor_sync(0xffffffffu, c, 2);
-        if (s < h.n_csegs && (tid & 3u) == 0) o[col] = c;
+        if (s < h.n_segs && (tid & 3u) == 0) o[col] = c;
       }
+    } else {
+      nrec_wait();  // (MV only: already waited)
     }
     __syncthreads();  // tables and staged vectors are reused by the next batch
   }
@@ -338,11 +356,12 @@ struct LvlCache {
 // One batch's entry.  Fails with TOC_E_CORRUPT for blocks the reference's tree build rejects, and
 // TOC_E_ARG when ids do not fit the 16-bit fields (the caller then keeps the chain-walk path).
 int build_entry(const uint8_t* blk, const TocBlockMeta& m, uint32_t ow, LvlEntry& out) {
+  constexpr uint32_t W = toc::kSlices;
   if (m.status != TOC_OK) return m.status;
   if (m.corrupt) return TOC_E_CORRUPT;
   const uint32_t n = m.n_rows, nI = m.n_pairs, C = m.n_codes;
   const uint64_t T = 1ull + nI + m.n_derived;
-  if (T > (1ull << 26) || m.n_cols > 65536u || m.n_uniques > 65536u || n > 65533u || C > 0xffffffu) return TOC_E_ARG;
+  if (T > (1ull << 26) || m.n_cols > 65536u || m.n_uniques > 65536u || n > 65533u) return TOC_E_ARG;
   std::vector<uint32_t> off(n + 1), code(C);
   for (uint32_t r = 0; r <= n; ++r) off[r] = rd_packed(blk + m.off_offsets, r, m.w_offsets);
   for (uint32_t j = 0; j < C; ++j) code[j] = rd_packed(blk + m.off_codes, j, m.w_codes);
@@ -372,7 +391,7 @@ int build_entry(const uint8_t* blk, const TocBlockMeta& m, uint32_t ow, LvlEntry
     }
   }
   // new ids: pairs by (column, old id); used derived nodes by depth, each level ordered by (new id
-  // of the parent, old id)
+  // of the parent, old id) -- so each pair's subtree is one contiguous range per level
   std::vector<uint32_t> nid(T, 0xffffffffu), order;  // order: old id of every new id
   for (uint32_t i = 1; i <= nI; ++i) order.push_back(i);
   std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return pcol[x] < pcol[y]; });
@@ -383,25 +402,49 @@ int build_entry(const uint8_t* blk, const TocBlockMeta& m, uint32_t ow, LvlEntry
   std::vector<std::vector<uint32_t>> lv(maxd + 1);
   for (uint64_t x = nI + 1; x < T; ++x)
     if (cnt[x]) lv[depth[x]].push_back((uint32_t)x);
-  std::vector<uint32_t> lvl_start{0u}, run_start{0u}, runs;
-  if (maxd >= 1) {
-    lvl_start.push_back(nI);
-    run_start.push_back(0u);
-  }
+  std::vector<uint32_t> lvl_start{0u};
+  if (maxd >= 1) lvl_start.push_back(nI);
   for (uint32_t dd = 2; dd <= maxd; ++dd) {
     auto& L = lv[dd];
     std::stable_sort(L.begin(), L.end(), [&](uint32_t x, uint32_t y) { return nid[par[x]] < nid[par[y]]; });
     for (uint32_t x : L) {
-      const uint32_t y = (uint32_t)order.size();
-      if (y >= 65535u) return TOC_E_ARG;
-      nid[x] = y;
+      if (order.size() >= 65535u) return TOC_E_ARG;
+      nid[x] = (uint32_t)order.size();
       order.push_back(x);
-      if (runs.empty() || y == lvl_start.back() || (runs.back() >> 16) != nid[par[x]]) runs.push_back(y | (nid[par[x]] << 16));
     }
     lvl_start.push_back((uint32_t)order.size());
-    run_start.push_back((uint32_t)runs.size());
   }
   const uint32_t N = (uint32_t)order.size(), nD = N - nI;
+  // root pair of every new id; slices of the roots with similar subtree weight (one per warp)
+  std::vector<uint32_t> root(N), npar(N, 0xffffffffu);
+  for (uint32_t y = 0; y < nI; ++y) root[y] = y;
+  for (uint32_t y = nI; y < N; ++y) {
+    npar[y] = nid[par[order[y]]];
+    root[y] = root[npar[y]];
+  }
+  std::vector<uint64_t> wsum(nI + 1, 0);  // prefix of per-root weight: 1 + derived nodes below
+  {
+    std::vector<uint32_t> wt(nI, 1);
+    for (uint32_t y = nI; y < N; ++y) ++wt[root[y]];
+    for (uint32_t p = 0; p < nI; ++p) wsum[p + 1] = wsum[p] + wt[p];
+  }
+  std::vector<uint32_t> rcut(W + 1, nI);  // slice w owns roots [rcut[w], rcut[w+1])
+  rcut[0] = 0;
+  for (uint32_t w = 1; w < W; ++w)
+    rcut[w] = (uint32_t)(std::lower_bound(wsum.begin(), wsum.end(), wsum[nI] * w / W) - wsum.begin());
+  for (uint32_t w = 1; w <= W; ++w) rcut[w] = std::max(std::min(rcut[w], nI), rcut[w - 1]);
+  // per level, first node of each slice (nodes are ordered by root)
+  std::vector<uint16_t> slnode((maxd + 1) * (W + 1), 0);
+  for (uint32_t L = 1; L < maxd; ++L) {  // level index L = depth L + 1
+    const uint32_t lo = lvl_start[L], hi = lvl_start[L + 1];
+    uint32_t y = lo;
+    for (uint32_t w = 0; w <= W; ++w) {
+      if (w == W) y = hi;
+      else
+        while (y < hi && root[y] < rcut[w]) ++y;
+      slnode[L * (W + 1) + w] = (uint16_t)y;
+    }
+  }
   // occurrence rows
   const uint32_t none = toc::occ_none(ow), multi = toc::occ_multi(ow);
   std::vector<uint32_t> occ(N, none), mrec;
@@ -415,24 +458,33 @@ int build_entry(const uint8_t* blk, const TocBlockMeta& m, uint32_t ow, LvlEntry
       }
     }
   std::stable_sort(mrec.begin(), mrec.end(), [](uint32_t a, uint32_t b) { return (a & 0xffffu) < (b & 0xffffu); });
-  // derived nodes grouped by key pair; column segments over the column-sorted pairs
-  std::vector<uint32_t> kcount(nI + 1, 0), kl(nD);
-  for (uint32_t k = 0; k < nD; ++k) ++kcount[nid[key[order[nI + k]]] + 1];
-  std::vector<uint32_t> kstart(nI + 1, 0);
-  for (uint32_t p = 0; p < nI; ++p) kstart[p + 1] = kstart[p] + kcount[p + 1];
-  {
-    std::vector<uint32_t> fill(kstart.begin(), kstart.end() - 1);
-    for (uint32_t k = 0; k < nD; ++k) kl[fill[nid[key[order[nI + k]]]]++] = nI + k;  // ascending node
-  }
-  std::vector<uint32_t> csegs;
+  if (mrec.size() > 65535u) return TOC_E_ARG;
+  // derived nodes sorted by key pair; per-warp ranges of it and of the multi records, cut at
+  // key / node boundaries; column segments over the pairs
+  std::vector<uint32_t> kl(nD);
+  for (uint32_t k = 0; k < nD; ++k) kl[k] = nI + k;
+  auto kof = [&](uint32_t y) { return nid[key[order[y]]]; };
+  std::stable_sort(kl.begin(), kl.end(), [&](uint32_t a, uint32_t b) { return kof(a) < kof(b); });
+  std::vector<uint16_t> wsplit(2 * (W + 1), 0);
+  auto cut = [&](uint32_t count, auto&& tgt, uint16_t* out) {
+    uint32_t q = 0;
+    for (uint32_t w = 0; w <= W; ++w) {
+      q = std::max(q, (uint32_t)((uint64_t)count * w / W));
+      while (q > 0 && q < count && tgt(q) == tgt(q - 1)) ++q;  // move to a target boundary
+      out[w] = (uint16_t)(w == W ? count : q);
+    }
+  };
+  cut(nD, [&](uint32_t k) { return kof(kl[k]); }, wsplit.data());
+  cut((uint32_t)mrec.size(), [&](uint32_t k) { return mrec[k] & 0xffffu; }, wsplit.data() + (W + 1));
+  std::vector<uint32_t> segs;
   for (uint32_t p = 0; p < nI; ++p)
-    if (p == 0 || pcol[order[p]] != pcol[order[p - 1]]) csegs.push_back(p | (pcol[order[p]] << 16));
-  const uint32_t n_csegs = (uint32_t)csegs.size();
-  csegs.push_back(nI);
+    if (p == 0 || pcol[order[p]] != pcol[order[p - 1]]) segs.push_back(p | (pcol[order[p]] << 16));
+  const uint32_t n_segs = (uint32_t)segs.size();
+  segs.push_back(nI);
   // serialize
   LvlHdr hd{};
   hd.nP = nI, hd.nD = nD, hd.N = N, hd.C = C, hd.n_rows = n, hd.maxd = maxd;
-  hd.n_multi = (uint32_t)mrec.size(), hd.n_runs = (uint32_t)runs.size(), hd.n_csegs = n_csegs;
+  hd.n_multi = (uint32_t)mrec.size(), hd.n_segs = n_segs;
   uint32_t o = sizeof(LvlHdr);
   auto sec = [&](uint32_t bytes) {
     const uint32_t s = o;
@@ -440,25 +492,23 @@ int build_entry(const uint8_t* blk, const TocBlockMeta& m, uint32_t ow, LvlEntry
     return s;
   };
   hd.off_lvl = sec(4u * (uint32_t)lvl_start.size());
-  hd.off_runlvl = sec(4u * (uint32_t)run_start.size());
   hd.off_prs = sec(4u * nI);
   hd.off_nrec = sec(4u * nD);
   hd.off_codes = sec(2u * C);
   hd.off_occ = sec(ow * N);
   hd.off_multi = sec(4u * hd.n_multi);
-  hd.off_runs = sec(4u * hd.n_runs);
-  hd.off_kstart = sec(2u * (nI + 1));
+  hd.off_slnode = sec(2u * (uint32_t)slnode.size());
   hd.off_kl = sec(2u * nD);
-  hd.off_csegs = sec(4u * (n_csegs + 1));
+  hd.off_wsplit = sec(2u * (uint32_t)wsplit.size());
+  hd.off_segs = sec(4u * (n_segs + 1));
   out.bytes.assign(o, 0);
   uint8_t* e = out.bytes.data();
   memcpy(e, &hd, sizeof hd);
   memcpy(e + hd.off_lvl, lvl_start.data(), 4 * lvl_start.size());
-  memcpy(e + hd.off_runlvl, run_start.data(), 4 * run_start.size());
   uint32_t* pr = reinterpret_cast<uint32_t*>(e + hd.off_prs);
   for (uint32_t p = 0; p < nI; ++p) pr[p] = pcol[order[p]] | (pref[order[p]] << 16);
   uint32_t* nr = reinterpret_cast<uint32_t*>(e + hd.off_nrec);
-  for (uint32_t k = 0; k < nD; ++k) nr[k] = nid[par[order[nI + k]]] | (nid[key[order[nI + k]]] << 16);
+  for (uint32_t k = 0; k < nD; ++k) nr[k] = npar[nI + k] | (nid[key[order[nI + k]]] << 16);
   uint16_t* cd = reinterpret_cast<uint16_t*>(e + hd.off_codes);
   for (uint32_t j = 0; j < C; ++j) cd[j] = (uint16_t)nid[code[j]];
   for (uint32_t y = 0; y < N; ++y) {
@@ -466,12 +516,11 @@ int build_entry(const uint8_t* blk, const TocBlockMeta& m, uint32_t ow, LvlEntry
     else reinterpret_cast<uint16_t*>(e + hd.off_occ)[y] = (uint16_t)occ[y];
   }
   if (!mrec.empty()) memcpy(e + hd.off_multi, mrec.data(), 4 * mrec.size());
-  if (!runs.empty()) memcpy(e + hd.off_runs, runs.data(), 4 * runs.size());
-  uint16_t* ks = reinterpret_cast<uint16_t*>(e + hd.off_kstart);
-  for (uint32_t p = 0; p <= nI; ++p) ks[p] = (uint16_t)kstart[p];
+  memcpy(e + hd.off_slnode, slnode.data(), 2 * slnode.size());
   uint16_t* klp = reinterpret_cast<uint16_t*>(e + hd.off_kl);
   for (uint32_t k = 0; k < nD; ++k) klp[k] = (uint16_t)kl[k];
-  memcpy(e + hd.off_csegs, csegs.data(), 4 * csegs.size());
+  memcpy(e + hd.off_wsplit, wsplit.data(), 2 * wsplit.size());
+  memcpy(e + hd.off_segs, segs.data(), 4 * segs.size());
   out.N = N;
   return TOC_OK;
 }

@@ -20,8 +20,9 @@ from conftest import max_rel_err, within_rel
 from helpers import TOY_ROWS, TREE_ROWS, random_alphabet_rows
 
 REL = 1e-9
-HDR = ["nP", "nD", "N", "C", "n_rows", "maxd", "n_multi", "n_runs", "n_csegs", "off_lvl", "off_runlvl", "off_prs",
-       "off_nrec", "off_codes", "off_occ", "off_multi", "off_runs", "off_kstart", "off_kl", "off_csegs"]
+HDR = ["nP", "nD", "N", "C", "n_rows", "maxd", "n_multi", "n_segs", "off_lvl", "off_prs", "off_nrec", "off_codes",
+       "off_occ", "off_multi", "off_slnode", "off_kl", "off_wsplit", "off_segs"]
+W = 32  # slices (one per warp)
 
 
 def host_meta(block: bytes, N):
@@ -81,21 +82,21 @@ def build(blocks):
 
 
 def entry(buf, o, occ_w=1):
-    h = dict(zip(HDR, struct.unpack_from("<20I", buf, o)))
+    h = dict(zip(HDR, struct.unpack_from("<18I", buf, o)))
     u32 = lambda off, n: np.frombuffer(buf, np.uint32, n, o + off).astype(np.int64)  # noqa: E731
     u16 = lambda off, n: np.frombuffer(buf, np.uint16, n, o + off).astype(np.int64)  # noqa: E731
     nl = h["maxd"] + 1 if h["maxd"] else 1
-    h["lvl"], h["runlvl"] = u32(h["off_lvl"], nl), u32(h["off_runlvl"], nl)
+    h["lvl"] = u32(h["off_lvl"], nl)
     h["prs"] = u32(h["off_prs"], h["nP"])
     h["nrec"] = u32(h["off_nrec"], h["nD"])
     h["codes"] = u16(h["off_codes"], h["C"])
     h["occ"] = np.frombuffer(buf, np.uint8 if occ_w == 1 else np.uint16, h["N"], o + h["off_occ"]).astype(np.int64)
     h["occ_w"] = occ_w
     h["multi"] = u32(h["off_multi"], h["n_multi"])
-    h["runs"] = u32(h["off_runs"], h["n_runs"])
-    h["kstart"] = u16(h["off_kstart"], h["nP"] + 1)
+    h["slnode"] = u16(h["off_slnode"], (h["maxd"] + 1) * (W + 1)).reshape(-1, W + 1)
     h["kl"] = u16(h["off_kl"], h["nD"])
-    h["csegs"] = u32(h["off_csegs"], h["n_csegs"] + 1)
+    h["wsplit"] = u16(h["off_wsplit"], 2 * (W + 1)).reshape(2, W + 1)
+    h["segs"] = u32(h["off_segs"], h["n_segs"] + 1)
     return h
 
 
@@ -113,42 +114,48 @@ def value_index(block):
 
 
 def emulate(h, enc, uniq, refs, v, u):
-    """The level kernel's arithmetic in numpy (same operation order per node)."""
-    nP, N, lvl = h["nP"], h["N"], h["lvl"]
+    """The level kernel's arithmetic in numpy (same operation order per node), walking the
+    per-warp slices the way the kernel does."""
+    nP, N = h["nP"], h["N"]
     par, key = h["nrec"] & 0xFFFF, h["nrec"] >> 16
     prs = h["prs"]
-    # pairs renumbered by (column, old id): the same multiset of (column, ref) as the block
+    # pairs renumbered by (column, old id): the same (column, ref) records as the block
     old = sorted(range(nP), key=lambda i: (enc.I_cols[i], i))
     assert np.array_equal(prs & 0xFFFF, np.asarray(enc.I_cols, np.int64)[old])
     assert np.array_equal(prs >> 16, refs[old])
     tab = np.zeros(N)
     tab[:nP] = uniq[prs >> 16] * v[prs & 0xFFFF]
-    for d in range(1, h["maxd"]):
-        for x in range(lvl[d], lvl[d + 1]):
-            tab[x] = tab[key[x - nP]] + tab[par[x - nP]]
+    for w in range(W):
+        for d in range(1, h["maxd"]):
+            for x in range(h["slnode"][d, w], h["slnode"][d, w + 1]):
+                tab[x] = tab[key[x - nP]] + tab[par[x - nP]]
     off = np.asarray(enc.offsets, np.int64)
     R = np.array([tab[h["codes"][off[r]:off[r + 1]]].sum() for r in range(h["n_rows"])])
     none, multi = (0xFF, 0xFE) if h["occ_w"] == 1 else (0xFFFF, 0xFFFE)
     S = np.where(h["occ"] < multi, u[np.minimum(h["occ"], len(u) - 1)], 0.0)
-    mx = h["multi"] & 0xFFFF
+    mrec = h["multi"]
+    ws = h["wsplit"]
+    assert ws[1][0] == 0 and ws[1][-1] == h["n_multi"] and ws[0][0] == 0 and ws[0][-1] == h["nD"]
+    for w in range(W):  # multi records: a warp's range never splits a node
+        a, b = ws[1][w], ws[1][w + 1]
+        if 0 < a < h["n_multi"]:
+            assert (mrec[a] & 0xFFFF) != (mrec[a - 1] & 0xFFFF)
+    mx = mrec & 0xFFFF
     for x in np.unique(mx):
-        S[x] = u[h["multi"][mx == x] >> 16].sum()
-    for d in range(h["maxd"] - 1, 0, -1):
-        k0, k1, hi = h["runlvl"][d], h["runlvl"][d + 1], lvl[d + 1]
-        for q in range(k0, k1):
-            a = h["runs"][q] & 0xFFFF
-            b = h["runs"][q + 1] & 0xFFFF if q + 1 < k1 else hi
-            assert np.all(par[a - nP:b - nP] == h["runs"][q] >> 16)
-            S[h["runs"][q] >> 16] += S[a:b].sum()
+        S[x] = u[mrec[mx == x] >> 16].sum()
+    for w in range(W):
+        for d in range(h["maxd"] - 1, 0, -1):
+            for x in range(h["slnode"][d, w], h["slnode"][d, w + 1]):
+                S[par[x - nP]] += S[x]
+    kl = h["kl"]
+    assert np.all(np.diff(key[kl - nP]) >= 0), "kl not sorted by key"
+    for x in kl:
+        S[key[x - nP]] += S[x]
     O = np.zeros(enc.n_cols)
-    for s in range(h["n_csegs"]):
-        a, b = h["csegs"][s] & 0xFFFF, h["csegs"][s + 1] & 0xFFFF
-        tot = 0.0
-        for p in range(a, b):
-            g = S[p] + S[h["kl"][h["kstart"][p]:h["kstart"][p + 1]]].sum()
-            assert np.all(key[h["kl"][h["kstart"][p]:h["kstart"][p + 1]] - nP] == p)
-            tot += uniq[prs[p] >> 16] * g
-        O[h["csegs"][s] >> 16] = tot
+    for s in range(h["n_segs"]):
+        a, b = h["segs"][s] & 0xFFFF, h["segs"][s + 1] & 0xFFFF
+        assert np.all((prs[a:b] & 0xFFFF) == h["segs"][s] >> 16)
+        O[h["segs"][s] >> 16] = np.sum(uniq[prs[a:b] >> 16] * S[a:b])
     return R, O
 
 
@@ -167,7 +174,13 @@ def structure(h, enc):
     used = np.zeros(N, bool)
     used[h["codes"]] = True
     assert used[nP:].all(), "every derived node in the cache is a code"
-    assert h["kstart"][-1] == h["nD"] and sorted(h["kl"]) == list(range(nP, N))
+    for d in range(1, h["maxd"]):  # the slices tile each level; a slice's parents are in the slice
+        sl = h["slnode"][d]
+        assert sl[0] == lvl[d] and sl[-1] == lvl[d + 1] and np.all(np.diff(sl) >= 0)
+        if d >= 2:
+            for w in range(W):
+                p = par[sl[w] - nP:sl[w + 1] - nP]
+                assert np.all((p >= h["slnode"][d - 1][w]) & (p < h["slnode"][d - 1][w + 1]))
 
 
 def cases():

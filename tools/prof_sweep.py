@@ -38,6 +38,7 @@ if a.prefetch >= 0:
 vd = torch.randn(bench.COLS, dtype=torch.float64, device="cuda")
 ud = torch.randn(arena.n_rows_total, dtype=torch.float64, device="cuda")
 for _ in range(a.reps):
-    arena.linalg(a.kind, v=vd, u=ud)
+    arena.linalg(a.kind, v=vd, u=ud, use_levels=bool(a.levels))
 torch.cuda.synchronize()
-print("ok", arena.n_blocks, arena.block_bytes)
+print("ok", arena.n_blocks, arena.block_bytes, "levels_bytes", getattr(arena, "levels_bytes", None),
+      "tree_bytes", getattr(arena, "tree_bytes", None))
