@@ -272,8 +272,8 @@ def main():
         bo_traffic = tj.get("linalg_kernel_both")
 
     # ---- e2e: public API call with host buffers (pinned), copies inside the timed region ----
-    e2e = run_e2e(torch, arena, v_h, u_h, args.e2e_steps)
-    e2e_resident = run_e2e_resident(torch, arena, v_h, u_h, args.e2e_steps)
+    e2e = run_e2e(torch, arena, v_h, u_h, args.e2e_steps, world)
+    e2e_resident = run_e2e_resident(torch, arena, v_h, u_h, args.e2e_steps, world)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -468,7 +468,23 @@ def cpu_mgd_sample(rp, c, v, y, m, loss, lr, steps_full: int, sample_batches: in
             "kind": "port"}
 
 
-def run_e2e(torch, arena, v_h, u_h, steps: int):
+def _wall_max(torch, dt: float, world: int) -> float:
+    """Slowest rank's wall time (every rank runs its own shard concurrently)."""
+    if world == 1:
+        return dt
+    t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _wall_start(torch, world: int) -> float:
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    return time.perf_counter()
+
+
+def run_e2e(torch, arena, v_h, u_h, steps: int, world: int = 1):
     """Same metric through the public API: host TOC1 bytes + host v/u in pinned memory -> device
     (H2D inside the timed region) -> validate/index -> fused A.v + v^T.A -> host R/O (D2H)."""
     from paper_1702_06943_b200.kernels import BatchSweep
@@ -477,16 +493,15 @@ def run_e2e(torch, arena, v_h, u_h, steps: int):
                                         arena.block_off, arena.block_len)
     for _ in range(2):
         sweep.run(v_h, u_h)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
+    t0 = _wall_start(torch, world)
     for _ in range(steps):
         sweep.run(v_h, u_h)
-    dt = time.perf_counter() - t0
-    return {"value": sweep.n_rows * steps / dt, "unit": "rows/s", "h2d_bytes_per_step": sweep.h2d_bytes,
+    dt = _wall_max(torch, time.perf_counter() - t0, world)
+    return {"value": world * sweep.n_rows * steps / dt, "unit": "rows/s", "h2d_bytes_per_step": sweep.h2d_bytes,
             "d2h_bytes_per_step": sweep.d2h_bytes, "api": "paper_1702_06943_b200.kernels.BatchSweep.run"}
 
 
-def run_e2e_resident(torch, arena, v_h, u_h, steps: int):
+def run_e2e_resident(torch, arena, v_h, u_h, steps: int, world: int = 1):
     """The same metric with the compressed arena resident in HBM (built once, like the reference's
     own bench-kernels keeps its CompressedMatrix objects, cli.py:299-334): per step v and u go
     host -> device from pinned memory, the fused launch runs, R and O come back to pinned host
@@ -511,11 +526,11 @@ def run_e2e_resident(torch, arena, v_h, u_h, steps: int):
 
     for _ in range(3):
         step()
-    t0 = time.perf_counter()
+    t0 = _wall_start(torch, world)
     for _ in range(steps):
         step()
-    dt = time.perf_counter() - t0
-    return {"value": arena.n_rows_total * steps / dt, "unit": "rows/s",
+    dt = _wall_max(torch, time.perf_counter() - t0, world)
+    return {"value": world * arena.n_rows_total * steps / dt, "unit": "rows/s",
             "h2d_bytes_per_step": 8 * (vh.numel() + uh.numel()), "d2h_bytes_per_step": 8 * (Rh.numel() + Oh.numel()),
             "api": "paper_1702_06943_b200.arena.BlockArena.linalg (arena resident, tree cache built once)",
             "note": "operands in, results out per step; the headline e2e above streams the TOC1 blocks too"}

@@ -321,6 +321,13 @@ int toc_glm_epoch_parts(const uint8_t* d_images, const int64_t* d_part_off, cons
                         const int32_t* h_counts, int64_t n_blocks, int32_t n_cols, int32_t cluster,
                         int32_t loss, double lr, double* d_w, unsigned long long* d_gacc, int64_t max_part,
                         void* stream);
+/* One data-parallel MGD step on the same part images (training.py:261-281 per rank; the caller
+ * all-reduces and applies training.py:296-300): the summed gradient of batch `step` at weights d_w
+ * into d_grad[touched columns] (d_grad zero elsewhere; d_gacc left zero). */
+int toc_glm_grad_parts(const uint8_t* d_images, const int64_t* d_part_off, const TocBlockMeta* h_meta,
+                       const int32_t* h_counts, int64_t n_blocks, int32_t n_cols, int32_t cluster, int32_t loss,
+                       int64_t step, const double* d_w, unsigned long long* d_gacc, double* d_grad,
+                       int64_t max_part, void* stream);
 
 /* Diagnostic: CTA width (power of two, 64..1024; 0 = 512) of cluster epochs planned afterwards. */
 int toc_mgd_set_image_threads(int32_t threads);

@@ -251,6 +251,9 @@ struct LargeEpochArgs {
   double* w;                 // n_cols, global
   unsigned long long* gacc;  // n_cols, zero between steps
   uint32_t max_part, max_pairs, max_rows;
+  int64_t t0, t1;            // steps [t0, t1) of the epoch
+  double* grad_out;          // gradient-only mode (data-parallel step): the summed gradient of the
+                             // batch into grad_out[touched columns] instead of the update
 };
 
 // One epoch on a cluster of C CTAs; w and the fixed-point gradient live in global memory.
@@ -271,23 +274,23 @@ __global__ void __launch_bounds__(1024, 1) epoch_large_kernel(LargeEpochArgs a) 
   p += align16(8u * a.max_rows);
   uint8_t* buf0 = p;
   uint8_t* buf1 = p + a.max_part;
-  const uint8_t* src = a.images + a.part_off[cta];  // thread 0: global address of the current part
+  const uint8_t* src = a.images + a.part_off[a.t0 * a.cluster + cta];  // thread 0: the current part
   if (tid == 0) {
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
-    const uint32_t bytes = (uint32_t)(a.part_off[cta + 1] - a.part_off[cta]);
+    const uint32_t bytes = (uint32_t)(a.part_off[a.t0 * a.cluster + cta + 1] - a.part_off[a.t0 * a.cluster + cta]);
     mbar_expect(&mbar[0], bytes);
     bulk_copy(buf0, src, bytes, &mbar[0]);
   }
   __syncthreads();
   uint32_t step_n = 0;
   double step = 0.0;
-  for (int64_t t = 0; t < a.n_blocks; ++t) {
-    const uint32_t k = (uint32_t)t & 1u;
+  for (int64_t t = a.t0; t < a.t1; ++t) {
+    const uint32_t k = (uint32_t)(t - a.t0) & 1u;
     const uint8_t* img = k ? buf1 : buf0;
-    mbar_wait_bounded(&mbar[k], (uint32_t)(t >> 1) & 1u);
+    mbar_wait_bounded(&mbar[k], (uint32_t)((t - a.t0) >> 1) & 1u);
     const uint32_t* h = reinterpret_cast<const uint32_t*>(img);
-    if (tid == 0 && t + 1 < a.n_blocks) {  // every thread is past step t-1: the other buffer is free
+    if (tid == 0 && t + 1 < a.t1) {  // every thread is past step t-1: the other buffer is free
       const int64_t d = *reinterpret_cast<const int64_t*>(img + 40);
       const uint32_t bytes = h[12];
       src += d;
@@ -353,6 +356,15 @@ __global__ void __launch_bounds__(1024, 1) epoch_large_kernel(LargeEpochArgs a) 
       if (f) atomicAdd(a.gacc + pcol[i], (unsigned long long)f);
     }
     cluster_barrier();  // every CTA's contributions are in the gradient
+    if (a.grad_out) {  // data-parallel step: hand the summed gradient to the all-reduce
+      for (uint32_t o = tid; o < n_own; o += nth) {
+        const uint32_t c = own[o];
+        const unsigned long long f = __ldcg(a.gacc + c);
+        a.gacc[c] = 0ull;
+        a.grad_out[c] = (double)(long long)f * o_inv;
+      }
+      continue;  // (one step per launch: nothing reads the weights after this)
+    }
     // apply_update (training.py:296-300) for the columns this CTA owns, then clear them
     for (uint32_t o = tid; o < n_own; o += nth) {
       const uint32_t c = own[o];
@@ -526,10 +538,10 @@ extern "C" int toc_mgd_parts_fit(const TocBlockMeta* h_meta, const int32_t* h_co
   return TOC_OK;
 }
 
-extern "C" int toc_glm_epoch_parts(const uint8_t* d_images, const int64_t* d_part_off, const TocBlockMeta* h_meta,
-                                   const int32_t* h_counts, int64_t n_blocks, int32_t n_cols, int32_t cluster,
-                                   int32_t loss, double lr, double* d_w, unsigned long long* d_gacc, int64_t max_part,
-                                   void* stream) {
+static int parts_launch(const uint8_t* d_images, const int64_t* d_part_off, const TocBlockMeta* h_meta,
+                        const int32_t* h_counts, int64_t n_blocks, int32_t n_cols, int32_t cluster, int32_t loss,
+                        double lr, double* d_w, unsigned long long* d_gacc, int64_t max_part, int64_t t0, int64_t t1,
+                        double* d_grad, void* stream) {
   if (n_blocks <= 0) return n_blocks == 0 ? TOC_OK : TOC_E_ARG;
   if (!d_images || !d_part_off || !h_meta || !h_counts || !d_w || !d_gacc || cluster < 1 ||
       cluster > (int32_t)toc::kMaxCluster || (loss != TOC_LOSS_LOGISTIC && loss != TOC_LOSS_HINGE))
@@ -551,6 +563,9 @@ extern "C" int toc_glm_epoch_parts(const uint8_t* d_images, const int64_t* d_par
   a.max_part = mp;
   a.max_pairs = max_pairs;
   a.max_rows = max_rows;
+  a.t0 = t0;
+  a.t1 = t1;
+  a.grad_out = d_grad;
   if (cudaFuncSetAttribute(toc::epoch_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return TOC_E_CUDA;
@@ -568,4 +583,21 @@ extern "C" int toc_glm_epoch_parts(const uint8_t* d_images, const int64_t* d_par
   cfg.numAttrs = 1;
   void* args[] = {&a};
   return cudaLaunchKernelExC(&cfg, (void*)toc::epoch_large_kernel, args) == cudaSuccess ? TOC_OK : TOC_E_CUDA;
+}
+
+extern "C" int toc_glm_epoch_parts(const uint8_t* d_images, const int64_t* d_part_off, const TocBlockMeta* h_meta,
+                                   const int32_t* h_counts, int64_t n_blocks, int32_t n_cols, int32_t cluster,
+                                   int32_t loss, double lr, double* d_w, unsigned long long* d_gacc, int64_t max_part,
+                                   void* stream) {
+  return parts_launch(d_images, d_part_off, h_meta, h_counts, n_blocks, n_cols, cluster, loss, lr, d_w, d_gacc,
+                      max_part, 0, n_blocks, nullptr, stream);
+}
+
+extern "C" int toc_glm_grad_parts(const uint8_t* d_images, const int64_t* d_part_off, const TocBlockMeta* h_meta,
+                                  const int32_t* h_counts, int64_t n_blocks, int32_t n_cols, int32_t cluster,
+                                  int32_t loss, int64_t step, const double* d_w, unsigned long long* d_gacc,
+                                  double* d_grad, int64_t max_part, void* stream) {
+  if (step < 0 || step >= n_blocks || !d_grad) return TOC_E_ARG;
+  return parts_launch(d_images, d_part_off, h_meta, h_counts, n_blocks, n_cols, cluster, loss, 0.0,
+                      const_cast<double*>(d_w), d_gacc, max_part, step, step + 1, d_grad, stream);
 }

@@ -105,26 +105,112 @@ def batch_gradients(batches, loss_kind: str, w, out=None):
     return out
 
 
-class _OneBatch:
-    """View of a single batch of a DeviceBatches (for per-step gradients)."""
+class DeviceDPEpoch:
+    """One DP-MGD epoch on this rank's GPU, recorded once as a CUDA graph and replayed:
+    per step t the summed gradient of the local batch, the NCCL all-reduce (sum) of the gradient,
+    and w <- w - (lr / |B_t|) * g (training.py:296-300).  The gradient comes from the thread-block
+    cluster kernel over per-CTA part images built once (toc_glm_grad_parts, logistic / hinge),
+    else from toc_glm_grad on the batch's slice of the local arena (offset pointers, no per-step
+    host work).  A step whose local batch is empty contributes a zero gradient.  `graph=False`
+    (or a capture failure) runs the same sequence eagerly."""
 
-    def __init__(self, batches, b: int):
-        from .arena import BlockArena
+    def __init__(self, batches, plan: StepPlan, steps_with_rows, loss_kind: str, lr: float, w, group=None,
+                 graph: bool = True):
+        import torch
 
-        a = batches.arena
-        self.arena = BlockArena(a.data, a.block_off[b : b + 1], a.block_len[b : b + 1], a.meta_d[b * 68 : (b + 1) * 68])
-        self.labels = batches.labels[int(a.row_base[b]) : int(a.row_base[b]) + int(a.meta["n_rows"][b])]
-        self.n_cols = batches.n_cols
+        from .training import LOSS_CODE, _bind
+
+        self.torch, self.group = torch, group
+        self.batches, self.plan, self.w, self.lr = batches, plan, w, float(lr)
+        self.loss = LOSS_CODE[loss_kind]
+        self.local_of = {t: i for i, t in enumerate(steps_with_rows)}
+        m = w.numel()
+        self.g = torch.zeros(m, dtype=torch.float64, device="cuda")
+        self.L = _bind()
+        if batches is not None:
+            a = batches.arena
+            nbytes = ctypes.c_int64()
+            N.check(self.L.toc_mgd_workspace(a.meta.ctypes.data_as(ctypes.c_void_p), a.n_blocks, m, 1,
+                                             ctypes.byref(nbytes)), "toc_mgd_workspace")
+            self.scratch = torch.empty(max(nbytes.value, 16), dtype=torch.uint8, device="cuda")
+        self.parts = None
+        if batches is not None and loss_kind in ("logistic", "hinge"):
+            from .training import GlmTrainer
+
+            try:
+                self.parts = GlmTrainer(batches, loss_kind, lr, mode="parts")
+            except ValueError:  # part images do not fit shared memory
+                self.parts = None
+        self.mode = "parts" if self.parts is not None else "grad"
+        self.graph = None
+        if graph:
+            try:
+                self._capture()
+            except Exception:  # capture unsupported here: keep the eager sequence
+                self.graph = None
+                torch.cuda.synchronize()
+
+    def _steps(self):
+        import torch.distributed as dist
+
+        a = self.batches.arena if self.batches is not None else None
+        m = self.w.numel()
+        for t, gsize in enumerate(self.plan.global_sizes):
+            i = self.local_of.get(t)
+            if i is None:
+                self.g.zero_()
+            elif self.parts is not None:  # touched columns of g; g stays zero elsewhere
+                tr = self.parts
+                N.check(self.L.toc_glm_grad_parts(
+                    tr.images.data_ptr(), tr.part_off_d.data_ptr(), a.meta.ctypes.data_as(ctypes.c_void_p),
+                    tr.parts_counts.ctypes.data_as(ctypes.c_void_p), a.n_blocks, m, tr.cluster, self.loss, i,
+                    self.w.data_ptr(), tr.gacc.data_ptr(), self.g.data_ptr(), tr.parts_max, N.stream_handle()),
+                    "toc_glm_grad_parts")
+            else:
+                N.check(self.L.toc_glm_grad(
+                    a.data.data_ptr(), a.block_off_d.data_ptr() + 8 * i, a.meta_d.data_ptr() + 68 * i,
+                    a.meta[i:].ctypes.data_as(ctypes.c_void_p), a.row_base_d.data_ptr() + 8 * i, 1, m, self.loss,
+                    self.batches.labels.data_ptr(), self.w.data_ptr(), self.g.data_ptr(), self.scratch.data_ptr(),
+                    N.stream_handle()), "toc_glm_grad")
+            dist.all_reduce(self.g, op=dist.ReduceOp.SUM, group=self.group)
+            self.w.add_(self.g, alpha=-self.lr / int(gsize))
+            if self.parts is not None:
+                self.g.zero_()
+
+    def _capture(self):
+        torch = self.torch
+        import torch.distributed as dist
+
+        w0 = self.w.clone()
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):  # warm the communicator and the kernels outside the capture
+            dist.all_reduce(self.g, op=dist.ReduceOp.SUM, group=self.group)
+        torch.cuda.current_stream().wait_stream(s)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._steps()
+        self.w.copy_(w0)  # capture records without executing; keep w0 anyway
+        self.graph = g
+
+    def epoch(self):
+        if self.graph is not None:
+            self.graph.replay()
+        else:
+            self._steps()
+        return self.w
 
 
-def train_data_parallel(dataset, config, world: int, rank: int, group=None):
+def train_data_parallel(dataset, config, world: int, rank: int, group=None, graph: bool = True):
     """DP-MGD on this rank's GPU; every rank returns the same weights and the risk trace (the
-    risk is all-reduced).  Launch one process per GPU (torchrun); NCCL all-reduces the gradient."""
+    risk is all-reduced).  Launch one process per GPU (torchrun); NCCL all-reduces the gradient,
+    and each epoch is one CUDA-graph replay (DeviceDPEpoch)."""
     import torch
     import torch.distributed as dist
 
     from .matrix import LabeledDataset
-    from .training import DeviceBatches, LossTrace, GlmModel, LOSS_CODE, shuffle_order
+    from .training import DeviceBatches, LossTrace, GlmModel, shuffle_order
 
     order = shuffle_order(dataset.n_rows, config.seed)
     plan = dp_step_plan(dataset.n_rows, config.batch_size, world, rank)
@@ -134,29 +220,15 @@ def train_data_parallel(dataset, config, world: int, rank: int, group=None):
     local = np.concatenate(idx) if idx else np.zeros(0, np.int64)
     sub = LabeledDataset(features=dataset.features.take_rows(local), labels=dataset.labels[local])
     batches = DeviceBatches(sub, config.batch_size) if len(local) else None
-    m = dataset.n_cols
-    w = torch.zeros(m, dtype=torch.float64, device="cuda")
-    step_to_local = {t: i for i, t in enumerate(steps_with_rows)}
-    views = [_OneBatch(batches, i) for i in range(len(steps_with_rows))] if batches else []
-    g_buf = torch.zeros((1, m), dtype=torch.float64, device="cuda")
-
-    def grad_fn(t, w_):
-        i = step_to_local.get(t)
-        if i is None:
-            g_buf.zero_()
-        else:
-            batch_gradients(views[i], config.loss_kind, w_, out=g_buf)
-        return g_buf[0]
-
-    def allreduce(g):
-        dist.all_reduce(g, op=dist.ReduceOp.SUM, group=group)
-
-    trainer = DataParallelGLM(m, plan, config.learning_rate, grad_fn, allreduce, w)
+    w = torch.zeros(dataset.n_cols, dtype=torch.float64, device="cuda")
+    runner = DeviceDPEpoch(batches, plan, steps_with_rows, config.loss_kind, config.learning_rate, w, group, graph)
     trace = LossTrace()
+    trace.graph = runner.graph is not None
+    trace.mode = runner.mode
     for _ in range(config.epochs):
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         start.record()
-        trainer.epoch()
+        runner.epoch()
         end.record()
         end.synchronize()
         t = torch.tensor([start.elapsed_time(end) / 1e3], dtype=torch.float64, device="cuda")

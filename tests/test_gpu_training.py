@@ -229,3 +229,42 @@ def test_parts_ragged_batches(oracle):
         tp.epoch()
         tr.epoch()
     assert within_rel(tp.weights(), tr.weights(), 1e-12), max_rel_err(tp.weights(), tr.weights())
+
+
+@pytest.mark.parametrize("loss", ["logistic", "hinge", "squared"])
+def test_dp_epoch_graph_world1_nccl(oracle, loss):
+    """The device DP-MGD epoch (toc_glm_grad -> NCCL all-reduce -> update per step, one CUDA graph
+    per epoch) on a one-rank NCCL group equals the eager sequence and the oracle trainer."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1702_06943_b200 import synth
+    from paper_1702_06943_b200.distributed import train_data_parallel
+    from paper_1702_06943_b200.matrix import LabeledDataset, SparseRowMatrix
+    from paper_1702_06943_b200.training import TrainConfig
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        rp, c, v, y = synth.cfg3_dataset(4000, seed=21)
+        if loss == "squared":
+            y = y * 0.5 + 0.1
+        ds = LabeledDataset(features=SparseRowMatrix.from_csr(68, rp, c, v), labels=y)
+        cfg = TrainConfig(loss, 250, 0.05, 2)
+        m_g, t_g = train_data_parallel(ds, cfg, 1, 0, graph=True)
+        m_e, t_e = train_data_parallel(ds, cfg, 1, 0, graph=False)
+        assert t_g.graph and not t_e.graph and t_g.mode == ("grad" if loss == "squared" else "parts")
+        assert np.array_equal(m_g.weights, m_e.weights)
+        w_ref, risks = oracle.train_glm(rp, c, v, y, 68, loss, 250, 0.05, 2, 0)
+        assert np.allclose(m_g.weights, w_ref, rtol=1e-9, atol=1e-12), np.max(np.abs(m_g.weights - w_ref))
+        assert np.allclose(t_g.risks, risks, rtol=1e-6)
+    finally:
+        dist.destroy_process_group()
