@@ -403,8 +403,8 @@ def run_mgd(cfg: int, rank: int, world: int, cpu_sample: bool):
 
 
 def run_mlp(rank: int, world: int, cpu_sample: bool):
-    """Config 5: 784-200-10 ReLU softmax-CE MLP, 1,000,000 rows, batch 250, lr 0.05, 5 epochs (N=1;
-    the data-parallel MLP is not built)."""
+    """Config 5: 784-200-10 ReLU softmax-CE MLP, 1,000,000 rows, batch 250, lr 0.05, 5 epochs (N>1:
+    synchronous data parallelism, global batch 250 N)."""
     from paper_1702_06943_b200 import synth
     from paper_1702_06943_b200.matrix import LabeledDataset, SparseRowMatrix
     from paper_1702_06943_b200.mlp import train_mlp
@@ -412,11 +412,17 @@ def run_mlp(rank: int, world: int, cpu_sample: bool):
     n, epochs = 1_000_000, 5
     out = {"rows": n, "n_cols": 784, "model": "784-200-10 ReLU softmax-CE f64", "batch_size": 250, "lr": 0.05,
            "epochs": epochs}
-    if world > 1:
-        out["unavailable"] = "data-parallel MLP not built; config 5 is reported at N=1"
-        return out
     rp, c, v, y = synth.cfg5_dataset(n)
     ds = LabeledDataset(features=SparseRowMatrix.from_csr(784, rp, c, v, check=False), labels=y)
+    if world > 1:
+        from paper_1702_06943_b200.distributed import train_mlp_data_parallel
+
+        _, trace = train_mlp_data_parallel(ds, world, rank, epochs=epochs)
+        out.update({"steps_per_epoch": -(-n // (250 * world)), "epoch_seconds": trace.seconds,
+                    "risk_per_epoch": trace.risks,
+                    "mode": f"data parallel x{world}: per step toc_mlp_step_grad (native step kernels, gradient "
+                            "only) -> NCCL all-reduce of the flat gradient -> update; one CUDA graph per epoch"})
+        return out
     t0 = time.perf_counter()
     _, trace = train_mlp(ds, epochs=epochs)
     out.update({"steps_per_epoch": n // 250, "epoch_seconds": trace.seconds, "risk_per_epoch": trace.risks,

@@ -387,6 +387,15 @@ int toc_mlp_epoch(const uint8_t* d_cache, const int64_t* h_cache_off, const int6
                   const int32_t* h_n_rows, int64_t n_blocks, int32_t m, int32_t h, int32_t k,
                   const double* d_labels, double* d_W1, double* d_b1, double* d_W2, double* d_b2, double lr,
                   int32_t dense, void* d_scratch, int64_t scratch_bytes, void* stream);
+/* One data-parallel step of the same model (the per-rank half of toc_mlp_epoch's step; the caller
+ * all-reduces and applies the update): the summed gradient of batch `step` at the given weights
+ * into d_grad = [W1 m*h | W2 h*k | b1 h | b2 k].  Steps of one epoch must be issued in batch order
+ * starting at step 0 (the decode buffers alternate by step parity). */
+int toc_mlp_step_grad(const uint8_t* d_cache, const int64_t* h_cache_off, const int64_t* h_row_base,
+                      const int32_t* h_n_rows, int64_t n_blocks, int64_t step, int32_t m, int32_t h, int32_t k,
+                      const double* d_labels, const double* d_W1, const double* d_b1, const double* d_W2,
+                      const double* d_b2, int32_t dense, double* d_grad, void* d_scratch, int64_t scratch_bytes,
+                      void* stream);
 
 /* ---- decode (codec.py:262-292 node_sequence / decode; cli.py:194-221 verify) -----------------
  * Two passes with a plan from toc_plan(kind = TOC_MATVEC) and its scratch: toc_decode_counts writes

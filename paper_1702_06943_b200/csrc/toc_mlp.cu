@@ -81,6 +81,8 @@ struct MlpStep {
   int64_t az_elems;      // its size (doubles, even); 0 when every row is dense (all overwritten)
   double* part;          // per tail CTA: sums over its rows of A1^T P [h x k], delta [h], P [k]
   double step;           // lr / n
+  double* grad;          // gradient-only mode (data-parallel step): the batch's summed gradient
+                         // [W1 m*h | W2 h*k | b1 h | b2 k] instead of the update; NULL: update
 };
 
 // The batch decoded into Ad: one thread per code walks its chain and stores each pair at (row,
@@ -286,7 +288,8 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_left_kernel(MlpStep s, uint32
       for (int u = 0; u < 8; ++u) t += v[u];
     }
     for (; c < n_tail; ++c) t += pe[(int64_t)c * pw];
-    if (e < h * k) s.W2[e] -= s.step * t;
+    if (s.grad) s.grad[(int64_t)m * h + e] = t;
+    else if (e < h * k) s.W2[e] -= s.step * t;
     else if (e < h * k + h) s.b1[e - h * k] -= s.step * t;
     else s.b2[e - h * k - h] -= s.step * t;
     return;
@@ -327,10 +330,14 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_left_kernel(MlpStep s, uint32
         for (uint32_t t = 0; t < kNT; ++t) dmma(acc[mt][t], a[u][mt], b[u][t]);
   }
   double* W1 = s.W1;
+  double* grad = s.grad;
   const double st = s.step;
   reduce_warps<MT, 8>(acc, red, [&](uint32_t row, uint32_t cc, double gsum) {
     const uint32_t c = c0 + row, col = n0 + cc;
-    if (c < m && col < h) W1[(int64_t)c * h + col] -= st * gsum;
+    if (c < m && col < h) {
+      if (grad) grad[(int64_t)c * h + col] = gsum;
+      else W1[(int64_t)c * h + col] -= st * gsum;
+    }
   });
 }
 
@@ -390,6 +397,81 @@ MlpGraphKey g_mlp_key{};
 cudaGraphExec_t g_mlp_exec = nullptr;
 }  // namespace
 
+namespace {
+// Dynamic shared memory of the three GEMM-shaped kernels (set once per process).
+int mlp_attrs(int32_t h, int32_t k) {
+  const int smem_right = 8 * (int)toc::kRightWarps * toc::kRightMT * toc::kNT * 64;
+  const int smem_left = 8 * 8 * toc::kLeftMT * toc::kNT * 64;
+  const int smem_tail = 8 * (8 * k + 16 * h);
+  if (smem_tail > 200 * 1024) return TOC_E_ARG;
+  if (cudaFuncSetAttribute(toc::mlp_right_kernel<toc::kRightMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           smem_right) != cudaSuccess ||
+      cudaFuncSetAttribute(toc::mlp_tail_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tail) !=
+          cudaSuccess ||
+      cudaFuncSetAttribute(toc::mlp_left_kernel<toc::kLeftMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           smem_left) != cudaSuccess)
+    return TOC_E_CUDA;
+  return TOC_OK;
+}
+
+// Launches of steps [b0, b1) (decode buffers zeroed first when b0 == 0; a later b0 continues the
+// parity of the preceding call).  grad: gradient-only mode for a single step (see MlpStep).
+int mlp_enqueue(const uint8_t* d_cache, const int64_t* h_cache_off, const int64_t* h_row_base,
+                const int32_t* h_n_rows, int64_t b0, int64_t b1, int32_t nmax, int32_t m, int32_t h, int32_t k,
+                const double* d_labels, double* d_W1, double* d_b1, double* d_W2, double* d_b2, double lr,
+                int32_t dense, void* d_scratch, double* d_grad, cudaStream_t st) {
+    const MlpScratch SL = mlp_scratch_layout(nmax, m, h, k);
+    const int smem_right = 8 * (int)toc::kRightWarps * toc::kRightMT * toc::kNT * 64;
+    const int smem_left = 8 * 8 * toc::kLeftMT * toc::kNT * 64;
+    const int smem_tail = 8 * (8 * k + 16 * h);
+    double* base = reinterpret_cast<double*>(d_scratch);
+    const int64_t ad_elems = ((int64_t)nmax * m + 1) & ~1ll;
+    double* adbuf[2] = {base + SL.ad, base + SL.ad + ad_elems};
+    if (b0 == 0 && cudaMemsetAsync(adbuf[0], 0, 8 * 2 * ad_elems, st) != cudaSuccess) return TOC_E_CUDA;
+    toc::MlpStep s{};
+    s.m = m;
+    s.h = h;
+    s.k = k;
+    s.W1 = d_W1;
+    s.b1 = d_b1;
+    s.W2 = d_W2;
+    s.b2 = d_b2;
+    s.A1 = base + SL.a1;
+    s.P = base + SL.p;
+    s.D = base + SL.d;
+    s.part = base + SL.part;
+    s.az_elems = dense ? 0 : ad_elems;
+    int sms = 148;
+    {
+      int dev = 0;
+      if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const uint32_t ncb = (uint32_t)((h + 8 * toc::kNT - 1) / (8 * toc::kNT));
+    const uint32_t n_gemm_left = (uint32_t)((m + 8 * toc::kLeftMT - 1) / (8 * toc::kLeftMT)) * ncb;
+    const uint32_t pw = (uint32_t)(h * k + h + k), n_upd = (pw + toc::kMlpThreads - 1) / toc::kMlpThreads;
+    s.grad = d_grad;
+    for (int64_t b = b0; b < b1; ++b) {
+      const uint32_t n = (uint32_t)h_n_rows[b];
+      if (n == 0) continue;
+      s.entry = d_cache + h_cache_off[b];
+      s.y = d_labels + h_row_base[b];
+      s.step = lr / (double)n;
+      s.Ad = adbuf[b & 1];
+      s.Az = adbuf[(b + 1) & 1];
+      const uint32_t n_tail = (n + 7) / 8;
+      if (g_mlp_mask & 1) toc::mlp_decode_kernel<<<(unsigned)(8 * sms), toc::kMlpThreads, 0, st>>>(s, n);
+      if (g_mlp_mask & 2)
+      toc::mlp_right_kernel<toc::kRightMT>
+          <<<dim3((n + 8 * toc::kRightMT - 1) / (8 * toc::kRightMT), ncb), 32 * toc::kRightWarps, smem_right, st>>>(s, n);
+      if (g_mlp_mask & 4) toc::mlp_tail_kernel<10><<<n_tail, toc::kMlpThreads, smem_tail, st>>>(s, n);
+      if (g_mlp_mask & 8)
+      toc::mlp_left_kernel<toc::kLeftMT>
+          <<<n_gemm_left + n_upd, toc::kMlpThreads, smem_left, st>>>(s, n, n_gemm_left, n_tail);
+    }
+    return cudaGetLastError() == cudaSuccess ? TOC_OK : TOC_E_CUDA;
+}
+}  // namespace
+
 extern "C" int toc_mlp_set_kernels(int32_t mask) {
   g_mlp_mask = mask & 15;
   return TOC_OK;
@@ -419,65 +501,12 @@ extern "C" int toc_mlp_epoch(const uint8_t* d_cache, const int64_t* h_cache_off,
   if (k != 10) return TOC_E_ARG;  // the tail kernel is instantiated for config 5's 10 classes
   int32_t nmax = 0;
   for (int64_t b = 0; b < n_blocks; ++b) nmax = h_n_rows[b] > nmax ? h_n_rows[b] : nmax;
-  const MlpScratch SL = mlp_scratch_layout(nmax, m, h, k);
-  if (scratch_bytes < 8 * SL.total) return TOC_E_ARG;
-  const int smem_right = 8 * (int)toc::kRightWarps * toc::kRightMT * toc::kNT * 64;
-  const int smem_left = 8 * 8 * toc::kLeftMT * toc::kNT * 64;
-  const int smem_tail = 8 * (8 * k + 16 * h);
-  if (smem_tail > 200 * 1024) return TOC_E_ARG;
-  if (cudaFuncSetAttribute(toc::mlp_right_kernel<toc::kRightMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           smem_right) != cudaSuccess ||
-      cudaFuncSetAttribute(toc::mlp_tail_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tail) !=
-          cudaSuccess ||
-      cudaFuncSetAttribute(toc::mlp_left_kernel<toc::kLeftMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           smem_left) != cudaSuccess)
-    return TOC_E_CUDA;
+  if (scratch_bytes < 8 * mlp_scratch_layout(nmax, m, h, k).total) return TOC_E_ARG;
+  if (const int rc = mlp_attrs(h, k)) return rc;
   // the whole epoch's launches; enqueued directly, or captured once into a CUDA graph and replayed
   auto enqueue = [&](cudaStream_t st) -> int {
-    double* base = reinterpret_cast<double*>(d_scratch);
-    const int64_t ad_elems = ((int64_t)nmax * m + 1) & ~1ll;
-    double* adbuf[2] = {base + SL.ad, base + SL.ad + ad_elems};
-    if (cudaMemsetAsync(adbuf[0], 0, 8 * 2 * ad_elems, st) != cudaSuccess) return TOC_E_CUDA;
-    toc::MlpStep s{};
-    s.m = m;
-    s.h = h;
-    s.k = k;
-    s.W1 = d_W1;
-    s.b1 = d_b1;
-    s.W2 = d_W2;
-    s.b2 = d_b2;
-    s.A1 = base + SL.a1;
-    s.P = base + SL.p;
-    s.D = base + SL.d;
-    s.part = base + SL.part;
-    s.az_elems = dense ? 0 : ad_elems;
-    int sms = 148;
-    {
-      int dev = 0;
-      if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    const uint32_t ncb = (uint32_t)((h + 8 * toc::kNT - 1) / (8 * toc::kNT));
-    const uint32_t n_gemm_left = (uint32_t)((m + 8 * toc::kLeftMT - 1) / (8 * toc::kLeftMT)) * ncb;
-    const uint32_t pw = (uint32_t)(h * k + h + k), n_upd = (pw + toc::kMlpThreads - 1) / toc::kMlpThreads;
-    for (int64_t b = 0; b < n_blocks; ++b) {
-      const uint32_t n = (uint32_t)h_n_rows[b];
-      if (n == 0) continue;
-      s.entry = d_cache + h_cache_off[b];
-      s.y = d_labels + h_row_base[b];
-      s.step = lr / (double)n;
-      s.Ad = adbuf[b & 1];
-      s.Az = adbuf[(b + 1) & 1];
-      const uint32_t n_tail = (n + 7) / 8;
-      if (g_mlp_mask & 1) toc::mlp_decode_kernel<<<(unsigned)(8 * sms), toc::kMlpThreads, 0, st>>>(s, n);
-      if (g_mlp_mask & 2)
-      toc::mlp_right_kernel<toc::kRightMT>
-          <<<dim3((n + 8 * toc::kRightMT - 1) / (8 * toc::kRightMT), ncb), 32 * toc::kRightWarps, smem_right, st>>>(s, n);
-      if (g_mlp_mask & 4) toc::mlp_tail_kernel<10><<<n_tail, toc::kMlpThreads, smem_tail, st>>>(s, n);
-      if (g_mlp_mask & 8)
-      toc::mlp_left_kernel<toc::kLeftMT>
-          <<<n_gemm_left + n_upd, toc::kMlpThreads, smem_left, st>>>(s, n, n_gemm_left, n_tail);
-    }
-    return cudaGetLastError() == cudaSuccess ? TOC_OK : TOC_E_CUDA;
+    return mlp_enqueue(d_cache, h_cache_off, h_row_base, h_n_rows, 0, n_blocks, nmax, m, h, k, d_labels, d_W1, d_b1,
+                       d_W2, d_b2, lr, dense, d_scratch, nullptr, st);
   };
   if (!g_mlp_graph) return enqueue((cudaStream_t)stream);
   MlpGraphKey key{d_cache, h_cache_off, h_row_base, h_n_rows, n_blocks, m, h, k, d_labels, d_W1, d_b1, d_W2, d_b2,
@@ -504,4 +533,26 @@ extern "C" int toc_mlp_epoch(const uint8_t* d_cache, const int64_t* h_cache_off,
     g_mlp_key = key;
   }
   return cudaGraphLaunch(g_mlp_exec, (cudaStream_t)stream) == cudaSuccess ? TOC_OK : TOC_E_CUDA;
+}
+
+extern "C" int toc_mlp_step_grad(const uint8_t* d_cache, const int64_t* h_cache_off, const int64_t* h_row_base,
+                                 const int32_t* h_n_rows, int64_t n_blocks, int64_t step, int32_t m, int32_t h,
+                                 int32_t k, const double* d_labels, const double* d_W1, const double* d_b1,
+                                 const double* d_W2, const double* d_b2, int32_t dense, double* d_grad,
+                                 void* d_scratch, int64_t scratch_bytes, void* stream) {
+  if (!d_cache || !h_cache_off || !h_row_base || !h_n_rows || step < 0 || step >= n_blocks || m < 1 || h < 1 ||
+      k != 10 || !d_labels || !d_W1 || !d_b1 || !d_W2 || !d_b2 || !d_grad || !d_scratch)
+    return TOC_E_ARG;
+  int32_t nmax = 0;
+  for (int64_t b = 0; b < n_blocks; ++b) nmax = h_n_rows[b] > nmax ? h_n_rows[b] : nmax;
+  if (scratch_bytes < 8 * mlp_scratch_layout(nmax, m, h, k).total) return TOC_E_ARG;
+  if (const int rc = mlp_attrs(h, k)) return rc;
+  if (h_n_rows[step] == 0)
+    return cudaMemsetAsync(d_grad, 0, 8 * ((size_t)m * h + (size_t)h * k + h + k), (cudaStream_t)stream) ==
+                   cudaSuccess
+               ? TOC_OK
+               : TOC_E_CUDA;
+  return mlp_enqueue(d_cache, h_cache_off, h_row_base, h_n_rows, step, step + 1, nmax, m, h, k, d_labels,
+                     const_cast<double*>(d_W1), const_cast<double*>(d_b1), const_cast<double*>(d_W2),
+                     const_cast<double*>(d_b2), 0.0, dense, d_scratch, d_grad, (cudaStream_t)stream);
 }

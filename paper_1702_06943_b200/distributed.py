@@ -105,6 +105,26 @@ def batch_gradients(batches, loss_kind: str, w, out=None):
     return out
 
 
+def capture_epoch(steps, probe, group=None):
+    """Record `steps()` (an epoch's launches and NCCL collectives) as one CUDA graph.  The
+    communicator is warmed with one all-reduce of `probe` on a side stream first (a collective's
+    first call sets up state that cannot be captured).  Capture executes nothing."""
+    import torch
+    import torch.distributed as dist
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        dist.all_reduce(probe, op=dist.ReduceOp.SUM, group=group)
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    probe.zero_()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        steps()
+    return g
+
+
 class DeviceDPEpoch:
     """One DP-MGD epoch on this rank's GPU, recorded once as a CUDA graph and replayed:
     per step t the summed gradient of the local batch, the NCCL all-reduce (sum) of the gradient,
@@ -178,21 +198,7 @@ class DeviceDPEpoch:
                 self.g.zero_()
 
     def _capture(self):
-        torch = self.torch
-        import torch.distributed as dist
-
-        w0 = self.w.clone()
-        s = torch.cuda.Stream()
-        s.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(s):  # warm the communicator and the kernels outside the capture
-            dist.all_reduce(self.g, op=dist.ReduceOp.SUM, group=self.group)
-        torch.cuda.current_stream().wait_stream(s)
-        torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            self._steps()
-        self.w.copy_(w0)  # capture records without executing; keep w0 anyway
-        self.graph = g
+        self.graph = capture_epoch(self._steps, self.g, self.group)
 
     def epoch(self):
         if self.graph is not None:
@@ -253,3 +259,98 @@ def _dp_risk(batches, w, loss_kind, n_total, group):
         s += part.sum()
     dist.all_reduce(s, op=dist.ReduceOp.SUM, group=group)
     return float(s.item()) / n_total
+
+
+def train_mlp_data_parallel(dataset, world: int, rank: int, hidden: int = 200, classes: int = 10,
+                            batch_size: int = 250, learning_rate: float = 0.05, epochs: int = 5, seed: int = 0,
+                            group=None, graph: bool = True):
+    """Config 5 (784-h-10 ReLU softmax-CE MLP) with synchronous data parallelism: the per-rank
+    batches as in train_data_parallel; per step the rank's summed gradient of all parameters from
+    the native step kernels in gradient-only mode (toc_mlp_step_grad: decode, A.W1 and A^T.delta on
+    the fp64 tensor cores, softmax-CE tail), one NCCL all-reduce of the flat gradient
+    [W1 | W2 | b1 | b2], and params -= (lr / |B_t|) * g; each epoch one CUDA-graph replay.
+    At world 1 this is train_mlp (mlp.py) step for step.  Returns (MlpModel, LossTrace)."""
+    import torch
+    import torch.distributed as dist
+
+    from .matrix import LabeledDataset
+    from .mlp import MlpModel, init_mlp
+    from .training import DeviceBatches, LossTrace, shuffle_order
+
+    L = N.lib()
+    n, m, h, k = dataset.n_rows, dataset.n_cols, hidden, classes
+    order = shuffle_order(n, seed)
+    plan = dp_step_plan(n, batch_size, world, rank)
+    idx = [order[lo:hi] for lo, hi in plan.local_rows if hi > lo]
+    steps_with_rows = [t for t, (lo, hi) in enumerate(plan.local_rows) if hi > lo]
+    local_of = {t: i for i, t in enumerate(steps_with_rows)}
+    local = np.concatenate(idx) if idx else np.zeros(0, np.int64)
+    sub = LabeledDataset(features=dataset.features.take_rows(local), labels=dataset.labels[local])
+    batches = DeviceBatches(sub, batch_size) if len(local) else None
+    sizes = (m * h, h * k, h, k)
+    P = torch.zeros(sum(sizes), dtype=torch.float64, device="cuda")
+    w1, w2, b1, b2 = torch.split(P, sizes)
+    w1, w2 = w1.view(m, h), w2.view(h, k)
+    iw1, ib1, iw2, ib2 = init_mlp(m, h, k, seed)
+    w1.copy_(torch.from_numpy(iw1))
+    w2.copy_(torch.from_numpy(iw2))
+    b1.copy_(torch.from_numpy(ib1))
+    b2.copy_(torch.from_numpy(ib2))
+    G = torch.zeros_like(P)
+    lr = float(learning_rate)
+    if batches is not None:
+        a = batches.arena
+        a.build_matcache()
+        nrows = np.ascontiguousarray(a.meta["n_rows"], np.int32)
+        cache_off = np.ascontiguousarray(a.matcache_off[:-1], np.int64)
+        row_base = np.ascontiguousarray(a.row_base, np.int64)
+        labels = batches.labels.to(torch.float64).contiguous()
+        lens = np.diff(np.asarray(sub.features.row_ptr))
+        dense = int(bool(len(lens) and np.all(lens == m)))
+        nb = ctypes.c_int64(0)
+        N.check(L.toc_mlp_scratch(int(nrows.max(initial=0)), m, h, k, ctypes.byref(nb)), "toc_mlp_scratch")
+        scratch = torch.empty(max(int(nb.value), 8), dtype=torch.uint8, device="cuda")
+
+    def steps():
+        for t, gsize in enumerate(plan.global_sizes):
+            i = local_of.get(t)
+            if i is None:
+                G.zero_()
+            else:
+                N.check(L.toc_mlp_step_grad(
+                    a.matcache.data_ptr(), cache_off.ctypes.data, row_base.ctypes.data, nrows.ctypes.data,
+                    a.n_blocks, i, m, h, k, labels.data_ptr(), w1.data_ptr(), b1.data_ptr(), w2.data_ptr(),
+                    b2.data_ptr(), dense, G.data_ptr(), scratch.data_ptr(), scratch.numel(), N.stream_handle()),
+                    "toc_mlp_step_grad")
+            dist.all_reduce(G, op=dist.ReduceOp.SUM, group=group)
+            P.add_(G, alpha=-lr / int(gsize))
+
+    g = None
+    if graph:
+        try:
+            g = capture_epoch(steps, G, group)
+        except Exception:  # capture unsupported here: eager sequence
+            g = None
+            torch.cuda.synchronize()
+    trace = LossTrace()
+    trace.graph = g is not None
+    for _ in range(epochs):
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record()
+        if g is not None:
+            g.replay()
+        else:
+            steps()
+        end.record()
+        end.synchronize()
+        t = torch.tensor([start.elapsed_time(end) / 1e3], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+        trace.seconds.append(float(t.item()))
+        ce = torch.zeros(1, dtype=torch.float64, device="cuda")
+        if batches is not None:  # mean cross-entropy over all rows (local sums, all-reduced)
+            logits = torch.relu(batches.arena.matmat(0, w1, h) + b1) @ w2 + b2
+            ce += torch.nn.functional.cross_entropy(logits, batches.labels.long(), reduction="sum")
+        dist.all_reduce(ce, op=dist.ReduceOp.SUM, group=group)
+        trace.risks.append(float(ce.item()) / n)
+    model = MlpModel(*(x.cpu().numpy() for x in (w1, b1, w2, b2)))
+    return model, trace

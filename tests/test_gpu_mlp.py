@@ -109,3 +109,45 @@ def test_cfg5_native_equals_per_step_path():
     assert np.allclose(t1.risks, t2.risks, rtol=1e-9, atol=0)
     for a, b in zip((m1.w1, m1.b1, m1.w2, m1.b2), (m2.w1, m2.b1, m2.w2, m2.b2)):
         assert within_rel(a, b, 1e-9), max_rel_err(a, b)
+
+
+@pytest.mark.parametrize("n_rows,batch", [(1000, 250), (1130, 250)])
+def test_dp_mlp_world1_nccl(oracle, n_rows, batch):
+    """The data-parallel config-5 trainer (toc_mlp_step_grad -> NCCL all-reduce -> update, one CUDA
+    graph per epoch) on a one-rank NCCL group: graph == eager bit for bit, == the single-GPU native
+    trainer to fp64 rounding, == the oracle's CPU restatement (1e-6); includes a short last batch."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1702_06943_b200 import synth
+    from paper_1702_06943_b200.distributed import train_mlp_data_parallel
+    from paper_1702_06943_b200.matrix import LabeledDataset, SparseRowMatrix
+    from paper_1702_06943_b200.mlp import train_mlp
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        rp, c, v, y = synth.cfg5_dataset(n_rows, seed=9)
+        ds = LabeledDataset(features=SparseRowMatrix.from_csr(784, rp, c, v), labels=y)
+        kw = dict(hidden=40, classes=10, batch_size=batch, learning_rate=0.05, epochs=2, seed=0)
+        mg, tg = train_mlp_data_parallel(ds, 1, 0, graph=True, **kw)
+        me, te = train_mlp_data_parallel(ds, 1, 0, graph=False, **kw)
+        assert tg.graph and not te.graph
+        for a, b in ((mg.w1, me.w1), (mg.b1, me.b1), (mg.w2, me.w2), (mg.b2, me.b2)):
+            assert np.array_equal(a, b)
+        mn, tn = train_mlp(ds, **kw)
+        for a, b in ((mg.w1, mn.w1), (mg.b1, mn.b1), (mg.w2, mn.w2), (mg.b2, mn.b2)):
+            assert within_rel(a, b, 1e-9), max_rel_err(a, b)
+        (w1, b1, w2, b2), risks = oracle.train_mlp(rp, c, v, y, 784, 40, 10, batch, 0.05, 2, 0)
+        assert np.all(np.abs(np.array(tg.risks) - np.array(risks)) <= REL * np.abs(risks)), (tg.risks, risks)
+        for got, want in ((mg.w1, w1), (mg.b1, b1), (mg.w2, w2), (mg.b2, b2)):
+            assert within_rel(got, want, REL), max_rel_err(got, want)
+    finally:
+        dist.destroy_process_group()

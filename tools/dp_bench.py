@@ -17,7 +17,18 @@ rank, world, local = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_S
 torch.cuda.set_device(local)
 dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 graph = os.environ.get("DP_GRAPH", "1") == "1"
-for cfg in (3, 4):
+cfgs = [int(x) for x in os.environ.get("DP_CFGS", "3,4").split(",")]
+for cfg in cfgs:
+    if cfg == 5:
+        from paper_1702_06943_b200.distributed import train_mlp_data_parallel
+
+        rp, c, v, y = synth.cfg5_dataset(int(os.environ.get("DP_ROWS5", "1000000")))
+        ds = LabeledDataset(features=SparseRowMatrix.from_csr(784, rp, c, v, check=False), labels=y)
+        _, tr = train_mlp_data_parallel(ds, world, rank, epochs=2, graph=graph)
+        if rank == 0:
+            print(json.dumps({"config": 5, "world": world, "graph": tr.graph, "epoch_seconds": tr.seconds,
+                              "risks": tr.risks}), flush=True)
+        continue
     if cfg == 3:
         rp, c, v, y = synth.cfg3_dataset()
         m, loss, lr, epochs = 68, "logistic", 0.1, 3
