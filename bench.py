@@ -47,6 +47,11 @@ def parse():
     return p.parse_args()
 
 
+# Exercise the N>1 MGD code paths (data-parallel trainers over NCCL) on one GPU: torchrun with one
+# rank and BENCH_FORCE_DP=1.  A check of the multi-GPU path's mechanics, not a measurement mode.
+FORCE_DP = os.environ.get("BENCH_FORCE_DP", "0") == "1"
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -182,8 +187,27 @@ def cpu_reference(arena_bytes_h, block_off, block_len, v, u, row_base, budget_s:
     return rows / dt, desc, threads, dt
 
 
+_RESULT = None  # the real stdout: only the result line goes there
+
+
+def claim_stdout():
+    """Send everything written to fd 1 (library banners such as NCCL's, warnings) to stderr, and
+    keep the original stdout for the one JSON result line the driver parses."""
+    global _RESULT
+    if _RESULT is None:
+        sys.stdout.flush()
+        _RESULT = os.fdopen(os.dup(1), "w")
+        os.dup2(2, 1)
+    return _RESULT
+
+
+def emit(line: dict) -> None:
+    print(json.dumps(line), file=claim_stdout(), flush=True)
+
+
 def main():
     args = parse()
+    claim_stdout()
     rank, world, local = dist_env()
     if args.impl == "reference":
         return run_reference(args, rank, world)
@@ -193,7 +217,7 @@ def main():
     from paper_1702_06943_b200.codec import compress_csr
 
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or FORCE_DP:
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
@@ -347,8 +371,8 @@ def main():
             "clocks": sampler.summary(),
             "mgd": mgd,
         }
-        print(json.dumps(line))
-    if world > 1:
+        emit(line)
+    if world > 1 or FORCE_DP:
         torch.distributed.destroy_process_group()
 
 
@@ -375,7 +399,7 @@ def run_mgd(cfg: int, rank: int, world: int, cpu_sample: bool):
         m, loss, lr, epochs = 47_236, "hinge", 0.01, 5
     ds = LabeledDataset(features=SparseRowMatrix.from_csr(m, rp, c, v, check=False), labels=y)
     out = {"rows": len(y), "n_cols": m, "loss": loss, "batch_size": 250, "lr": lr, "epochs": epochs}
-    if world == 1:
+    if world == 1 and not FORCE_DP:
         batches = DeviceBatches(shuffle_once(ds, 0), 250)
         tr = GlmTrainer(batches, loss, lr)
         secs, risks = [], []
@@ -414,7 +438,7 @@ def run_mlp(rank: int, world: int, cpu_sample: bool):
            "epochs": epochs}
     rp, c, v, y = synth.cfg5_dataset(n)
     ds = LabeledDataset(features=SparseRowMatrix.from_csr(784, rp, c, v, check=False), labels=y)
-    if world > 1:
+    if world > 1 or FORCE_DP:
         from paper_1702_06943_b200.distributed import train_mlp_data_parallel
 
         _, trace = train_mlp_data_parallel(ds, world, rank, epochs=epochs)
@@ -576,7 +600,7 @@ def run_reference(args, rank, world):
     value = sample * ROWS * args.steps / dt
     desc = (f"oracle port (C restatement of reference kernels.py:115-174, OpenMP {threads} threads): A.v+v^T.A over "
             f"the first {sample} of {nb} config-2 batches per step, trees prebuilt (cli.py:316-317)")
-    print(json.dumps({
+    emit({
         "impl": "reference", "metric": METRIC, "value": value, "unit": "rows/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
@@ -585,7 +609,7 @@ def run_reference(args, rank, world):
                    "batches_per_gpu": nb, "rows_per_batch": ROWS, "n_cols": COLS},
         "cpu_baseline": {"value": value, "unit": "rows/s", "cores": threads, "kind": "port", "sample": desc},
         "e2e": {"value": value, "unit": "rows/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-    }))
+    })
 
 
 if __name__ == "__main__":
