@@ -199,7 +199,7 @@ struct EncodeArgs {
 
 __global__ void __launch_bounds__(kEncThreads) encode_kernel(EncodeArgs a) {
   __shared__ uint32_t s_warp[33];
-  __shared__ uint32_t s_mcode[kRowCap], s_mend[kRowCap], s_npar[kRowCap], s_nkey[kRowCap];
+  __shared__ uint32_t s_mcode[kRowCap], s_mend[kRowCap], s_npar[kRowCap], s_nkey[kRowCap], s_pid[kRowCap];
   __shared__ uint32_t s_cnt[2];
   __shared__ unsigned long long s_bad;
   const int64_t b = blockIdx.x;
@@ -293,6 +293,11 @@ __global__ void __launch_bounds__(kEncThreads) encode_kernel(EncodeArgs a) {
     if (tid == 0) out_offs[r] = C;
     if (L == 0) continue;
     const uint32_t* P = e_pid + lo;
+    if (L <= kRowCap) {  // the row's pair ids in shared memory: the match walks and the greedy
+      for (uint32_t j = tid; j < L; j += blockDim.x) s_pid[j] = P[j];  // chain read them repeatedly
+      P = s_pid;
+      __syncthreads();
+    }
     uint32_t* mcode = L <= kRowCap ? s_mcode : a.w.e_c + e0 + lo;  // e_c reused: seeding is done
     uint32_t* mend = L <= kRowCap ? s_mend : a.w.e_d + e0 + lo;
     uint32_t* npar = L <= kRowCap ? s_npar : a.w.e_a + e0 + lo;    // e_a reused likewise
