@@ -331,6 +331,21 @@ int toc_glm_grad_parts(const uint8_t* d_images, const int64_t* d_part_off, const
 
 /* Diagnostic: CTA width (power of two, 64..1024; 0 = 512) of cluster epochs planned afterwards. */
 int toc_mgd_set_image_threads(int32_t threads);
+/* Data-parallel toc_glm_epoch_images with the gradient all-reduce fused into the kernel (NVLink
+ * peer memory, no NCCL on the step path): this rank's images are its local batch of every global
+ * step; each step CTA 0 writes the rank's dense gradient into every rank's receive buffer
+ * (d_peer_buf[q], 2 * world * n_cols doubles, double-buffered by step parity), fences, and sets
+ * d_peer_flag[q][rank] = seq0 + t + 1; every rank waits for all flags of step t and applies
+ * w -= (lr / d_gsize[t]) * (sum over ranks in rank order) -- training.py:296-300 at the global
+ * batch.  Pointers: device arrays of world device pointers (e.g. torch symmetric memory's buffer /
+ * signal-pad pointers).  seq0 must grow across epochs (e.g. epoch * n_blocks).  n_cols must not
+ * exceed the largest batch's pair count + 1 (the gradient scratch reuses the P1 table). */
+int toc_glm_epoch_images_dp(const uint8_t* d_images, const int64_t* d_image_off, const TocBlockMeta* d_meta,
+                            const TocBlockMeta* h_meta, int64_t n_blocks, int32_t n_cols, int32_t cluster,
+                            int32_t loss, double lr, double* d_w, int32_t world, int32_t rank,
+                            double* const* d_peer_buf, uint32_t* const* d_peer_flag, const int32_t* d_gsize,
+                            uint32_t seq0, void* stream);
+
 /* toc_glm_epoch_images plus 8 clock64 stamps per step from CTA 0 (step start, image landed, P1,
  * A.w and loss, bound, s^T.A, cluster barrier passed, update).  Diagnostic. */
 int toc_glm_epoch_images_traced(const uint8_t* d_images, const int64_t* d_image_off,

@@ -120,7 +120,27 @@ struct ImageArgs {
   uint32_t cluster, threads;  // the epoch kernel's shape, fixed into the images
   uint32_t max_shared, max_part, max_pairs, max_part_rows, max_segs, sort_slots, max_codes;
   long long* trace;  // optional: kTracePoints clock64 stamps per step (CTA 0)
+  // Data-parallel epoch with the gradient exchange fused into the kernel (world > 0): each step
+  // CTA 0 stores this rank's dense gradient into every rank's receive buffer over NVLink
+  // (peer_buf[q] + (t & 1) * world * m + rank * m), fences, and raises its flag in every rank's
+  // flag array (peer_flag[q][rank] = seq0 + t + 1); every CTA then waits for all ranks' flags and
+  // applies w -= (lr / gsize[t]) * (sum of the ranks' gradients in rank order).
+  double* const* peer_buf;
+  uint32_t* const* peer_flag;
+  const int32_t* gsize;
+  int32_t world, rank;
+  uint32_t seq0;
 };
+
+// System-scope release store / acquire load of a flag (NVLink peers).
+TOC_D void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+TOC_D uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // Rebuild each batch's decode tree in shared memory (toc_batch.cuh, the code the relay runs per
 // step) and write its image.  Grid-stride over batches; tables, sort keys and per-code lengths fit
@@ -431,42 +451,84 @@ __global__ void __launch_bounds__(1024, 1) epoch_cluster_kernel(ImageArgs a) {
       bound = 0.0;
       for (uint32_t w = 0; w < nwarps; ++w) bound += s_red[w];
     }
-    double g_scale, g_inv;
-    fix_scales(bound, g_scale, g_inv);
-    // G[i] = sum of s_r over this CTA's occurrences of pair i (vecmat, Algorithm 6), fixed point
+    // G[i] = sum of s_r over this CTA's occurrences of pair i (vecmat, Algorithm 6), exact fixed
+    // point in two carry-free limbs (limb_add; a pair occurs at most once per row, so at most nr adds)
+    const uint32_t L = limb_bits(nr);
+    const double g_scale = limb_scale(bound, L), g_inv = 1.0 / g_scale;
     for (uint32_t q = tid >> lg; q < nr; q += RP) {
       const long long wr = __double2ll_rn(srow[q] * g_scale);
       if (wr == 0) continue;
-      const uint32_t xl = (uint32_t)wr, xh = (uint32_t)((unsigned long long)wr >> 32);
+      const int32_t xh = (int32_t)(wr >> L);
+      const uint32_t xl = (uint32_t)(wr - ((long long)xh << L));
       walk_flat(N, split[(q << lg) + sub], split[(q << lg) + sub + 1],
-                [&](uint32_t i) { fix_add_pair(glo, ghi, i, xl, xh); });
+                [&](uint32_t i) { limb_add(glo, reinterpret_cast<int32_t*>(ghi), i, xl, xh); });
     }
     __syncthreads();
     trace_stamp(a, cta, t, 5);
-    // per-column partial sums of value * G: 4 lanes per column, pairs strided over the lanes,
+    // per-column partial sums of value * G: 8 lanes per column, pairs strided over the lanes,
     // then a fixed shuffle tree (deterministic)
     double* cp = cpart + (size_t)k * a.max_segs;
-    const uint32_t seg_span = ((n_segs + (nth >> 2) - 1) / (nth >> 2)) * (nth >> 2);
-    for (uint32_t sgi = tid >> 2; sgi < seg_span; sgi += nth >> 2) {
+    constexpr uint32_t LPC = 8;
+    const uint32_t seg_span = ((n_segs + (nth / LPC) - 1) / (nth / LPC)) * (nth / LPC);
+    for (uint32_t sgi = tid / LPC; sgi < seg_span; sgi += nth / LPC) {
       double c = 0.0;
       uint2 sg = make_uint2(0u, 0u);
       if (sgi < n_segs) {
         sg = segs[sgi];
         const uint32_t end = segs[sgi + 1].x;
-        for (uint32_t q = sg.x + (tid & 3u); q < end; q += 4) {
+        for (uint32_t q = sg.x + (tid % LPC); q < end; q += LPC) {
           const uint2 pr = prec[q];
-          c += uniq[pr.y] * fix_value(glo[pr.x + 1], ghi[pr.x + 1], g_inv);
+          c += uniq[pr.y] * limb_value(glo[pr.x + 1], (int32_t)ghi[pr.x + 1], L, g_inv);
         }
       }
-      c += __shfl_xor_sync(0xffffffffu, c, 1);
-      c += __shfl_xor_sync(0xffffffffu, c, 2);
-      if (sgi < n_segs && (tid & 3u) == 0) {
+#pragma unroll
+      for (uint32_t o = 1; o < LPC; o <<= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if (sgi < n_segs && (tid % LPC) == 0) {
         cp[sgi] = c;
         segcol[sgi] = sg.y;
       }
     }
     cluster_barrier_smem();  // every CTA's partials of step t are complete and visible
     trace_stamp(a, cta, t, 6);
+    if (a.world > 0) {  // data parallel: exchange the gradient over NVLink inside the step
+      const uint32_t W = (uint32_t)a.world, seq = a.seq0 + (uint32_t)t + 1u;
+      double* gl = p1;  // this batch's P1 is dead: dense local gradient scratch [m]
+      if (cta == 0) {
+        for (uint32_t c = tid; c < m; c += nth) gl[c] = 0.0;
+        __syncthreads();
+        for (uint32_t sgi = tid; sgi < n_segs; sgi += nth) {
+          double g = 0.0, r[kMaxCluster];
+#pragma unroll
+          for (uint32_t c = 0; c < kMaxCluster; ++c) r[c] = c < C ? ld_dsmem(cp + sgi, c) : 0.0;
+#pragma unroll
+          for (uint32_t c = 0; c < kMaxCluster; ++c) g += r[c];  // rank order (as the 1-GPU epoch)
+          gl[segcol[sgi]] = g;
+        }
+        __syncthreads();
+        const size_t slot = ((size_t)(t & 1) * W + (uint32_t)a.rank) * m;
+        for (uint32_t q = 0; q < W; ++q)
+          for (uint32_t c = tid; c < m; c += nth) a.peer_buf[q][slot + c] = gl[c];
+        __syncthreads();  // the CTA's stores happen before the flag releases (release is cumulative)
+        if (tid < W) st_release_sys(a.peer_flag[tid] + a.rank, seq);
+      }
+      if (tid < W) {  // every CTA: wait for every rank's gradient of step t (bounded: trap, not hang)
+        const uint32_t* f = a.peer_flag[a.rank] + tid;
+        const long long t0c = clock64();
+        while ((int32_t)(ld_acquire_sys(f) - seq) < 0)
+          if (clock64() - t0c > (1ll << 34)) __trap();
+      }
+      __syncthreads();
+      const double* recv = a.peer_buf[a.rank] + (size_t)(t & 1) * W * m;
+      const double stp = a.lr / (double)a.gsize[t];
+      for (uint32_t c = tid; c < m; c += nth) {
+        double g = __ldcv(recv + c);
+        for (uint32_t q = 1; q < W; ++q) g += __ldcv(recv + (size_t)q * m + c);  // rank order
+        ws[c] = __dsub_rn(ws[c], __dmul_rn(stp, g));
+      }
+      __syncthreads();
+      trace_stamp(a, cta, t, 7);
+      continue;
+    }
     // g[c] = partials summed in rank order (identical in every CTA), w[c] -= (lr/|B|) g[c]
     // (apply_update, training.py:296-300)
     for (uint32_t sgi = tid; sgi < n_segs; sgi += nth) {
@@ -640,10 +702,11 @@ extern "C" int toc_mgd_build_images(const uint8_t* d_arena, const int64_t* d_blo
              : TOC_E_CUDA;
 }
 
-extern "C" int toc_glm_epoch_images_traced(const uint8_t* d_images, const int64_t* d_image_off,
-                                           const TocBlockMeta* d_meta, const TocBlockMeta* h_meta, int64_t n_blocks,
-                                           int32_t n_cols, int32_t cluster, int32_t loss, double lr, double* d_w,
-                                           long long* d_trace, void* stream) {
+static int epoch_images_launch(const uint8_t* d_images, const int64_t* d_image_off, const TocBlockMeta* d_meta,
+                               const TocBlockMeta* h_meta, int64_t n_blocks, int32_t n_cols, int32_t cluster,
+                               int32_t loss, double lr, double* d_w, long long* d_trace, int32_t world, int32_t rank,
+                               double* const* d_peer_buf, uint32_t* const* d_peer_flag, const int32_t* d_gsize,
+                               uint32_t seq0, void* stream) {
   if (n_blocks <= 0) return n_blocks == 0 ? TOC_OK : TOC_E_ARG;
   if (!h_meta || !d_meta || !d_images || !d_image_off || !d_w || n_cols < 0 || loss < 0 || loss > 2 ||
       cluster < 1 || cluster > (int32_t)toc::kMaxCluster)
@@ -658,6 +721,16 @@ extern "C" int toc_glm_epoch_images_traced(const uint8_t* d_images, const int64_
   a.lr = lr;
   a.w = d_w;
   a.trace = d_trace;
+  if (world > 0) {  // the dense gradient scratch reuses the P1 table
+    if (rank < 0 || rank >= world || !d_peer_buf || !d_peer_flag || !d_gsize || n_cols > (int32_t)a.max_pairs + 1)
+      return TOC_E_ARG;
+    a.world = world;
+    a.rank = rank;
+    a.peer_buf = d_peer_buf;
+    a.peer_flag = d_peer_flag;
+    a.gsize = d_gsize;
+    a.seq0 = seq0;
+  }
   void* fn = P.wide ? (void*)toc::epoch_cluster_kernel<true> : (void*)toc::epoch_cluster_kernel<false>;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, P.epoch_smem) != cudaSuccess)
     return TOC_E_CUDA;
@@ -677,9 +750,27 @@ extern "C" int toc_glm_epoch_images_traced(const uint8_t* d_images, const int64_
   return cudaLaunchKernelExC(&cfg, fn, args) == cudaSuccess ? TOC_OK : TOC_E_CUDA;
 }
 
+extern "C" int toc_glm_epoch_images_traced(const uint8_t* d_images, const int64_t* d_image_off,
+                                           const TocBlockMeta* d_meta, const TocBlockMeta* h_meta, int64_t n_blocks,
+                                           int32_t n_cols, int32_t cluster, int32_t loss, double lr, double* d_w,
+                                           long long* d_trace, void* stream) {
+  return epoch_images_launch(d_images, d_image_off, d_meta, h_meta, n_blocks, n_cols, cluster, loss, lr, d_w, d_trace,
+                             0, 0, nullptr, nullptr, nullptr, 0, stream);
+}
+
 extern "C" int toc_glm_epoch_images(const uint8_t* d_images, const int64_t* d_image_off, const TocBlockMeta* d_meta,
                                     const TocBlockMeta* h_meta, int64_t n_blocks, int32_t n_cols, int32_t cluster,
                                     int32_t loss, double lr, double* d_w, void* stream) {
-  return toc_glm_epoch_images_traced(d_images, d_image_off, d_meta, h_meta, n_blocks, n_cols, cluster, loss, lr, d_w,
-                                     nullptr, stream);
+  return epoch_images_launch(d_images, d_image_off, d_meta, h_meta, n_blocks, n_cols, cluster, loss, lr, d_w, nullptr,
+                             0, 0, nullptr, nullptr, nullptr, 0, stream);
+}
+
+extern "C" int toc_glm_epoch_images_dp(const uint8_t* d_images, const int64_t* d_image_off, const TocBlockMeta* d_meta,
+                                       const TocBlockMeta* h_meta, int64_t n_blocks, int32_t n_cols, int32_t cluster,
+                                       int32_t loss, double lr, double* d_w, int32_t world, int32_t rank,
+                                       double* const* d_peer_buf, uint32_t* const* d_peer_flag,
+                                       const int32_t* d_gsize, uint32_t seq0, void* stream) {
+  if (world < 1) return TOC_E_ARG;
+  return epoch_images_launch(d_images, d_image_off, d_meta, h_meta, n_blocks, n_cols, cluster, loss, lr, d_w, nullptr,
+                             world, rank, d_peer_buf, d_peer_flag, d_gsize, seq0, stream);
 }

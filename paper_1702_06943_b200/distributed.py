@@ -208,7 +208,69 @@ class DeviceDPEpoch:
         return self.w
 
 
-def train_data_parallel(dataset, config, world: int, rank: int, group=None, graph: bool = True):
+class FusedDPEpoch:
+    """DP-MGD epoch with the gradient all-reduce fused into the cluster epoch kernel
+    (toc_glm_epoch_images_dp): one launch per epoch per GPU; every step CTA 0 stores the rank's
+    dense gradient into every rank's receive buffer over NVLink (torch symmetric memory maps the
+    peer buffers; each holds the receive slots and the flags), raises its flag there, and each rank
+    applies the update
+    once all ranks' gradients of the step have landed (sum in rank order, so every rank holds the
+    same weights).  Requires the step images to fit (GlmTrainer mode "images") and a local batch at
+    every global step; raises ValueError otherwise."""
+
+    def __init__(self, batches, plan: StepPlan, loss_kind: str, lr: float, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+
+        from .training import GlmTrainer, _bind
+
+        if batches is None or batches.arena.n_blocks != len(plan.global_sizes):
+            raise ValueError("the fused exchange needs a local batch at every step")
+        self.tr = GlmTrainer(batches, loss_kind, lr, mode="images")
+        if batches.n_cols > int(batches.arena.meta["n_pairs"].max()) + 1:
+            raise ValueError("the gradient scratch (the P1 table) is smaller than n_cols")
+        self.torch, self.L, self.symm = torch, _bind(), symm
+        self.group = group or dist.group.WORLD
+        self.world, self.rank = dist.get_world_size(self.group), dist.get_rank(self.group)
+        self.handle = None
+        self.gsize = torch.tensor(np.asarray(plan.global_sizes, np.int32), device="cuda")
+        self.n_steps = len(plan.global_sizes)
+        self.epochs = 0
+        self.w = self.tr.w
+
+    def connect(self):
+        """Collective: map every rank's receive buffer (call on all ranks once all can run).  Each
+        rank's symmetric buffer holds its receive slots [2][world][n_cols] f64 followed by its
+        flags [world] u32 (zeroed here; the barrier keeps peers from signalling earlier)."""
+        import torch.distributed as dist
+
+        torch = self.torch
+        m = max(self.tr.b.n_cols, 1)
+        n_dbl = 2 * self.world * m
+        self.recv = self.symm.empty(n_dbl + (self.world + 1) // 2, dtype=torch.float64, device="cuda")
+        self.recv.zero_()
+        self.handle = self.symm.rendezvous(self.recv, self.group)
+        ptrs = [int(x) for x in self.handle.buffer_ptrs]
+        self.buf_ptrs = torch.tensor(ptrs, dtype=torch.int64, device="cuda")
+        self.flag_ptrs = torch.tensor([x + 8 * n_dbl for x in ptrs], dtype=torch.int64, device="cuda")
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+        return self
+
+    def epoch(self):
+        tr, a = self.tr, self.tr.b.arena
+        N.check(self.L.toc_glm_epoch_images_dp(
+            tr.images.data_ptr(), tr.image_off_d.data_ptr(), a.meta_d.data_ptr(), a.meta.ctypes.data_as(ctypes.c_void_p),
+            a.n_blocks, tr.b.n_cols, tr.cluster, tr.loss, tr.lr, tr.w.data_ptr(), self.world, self.rank,
+            self.buf_ptrs.data_ptr(), self.flag_ptrs.data_ptr(), self.gsize.data_ptr(),
+            (self.epochs * self.n_steps) & 0xFFFFFFFF, N.stream_handle()), "toc_glm_epoch_images_dp")
+        self.epochs += 1
+        return self.w
+
+
+def train_data_parallel(dataset, config, world: int, rank: int, group=None, graph: bool = True,
+                        fused: bool = True):
     """DP-MGD on this rank's GPU; every rank returns the same weights and the risk trace (the
     risk is all-reduced).  Launch one process per GPU (torchrun); NCCL all-reduces the gradient,
     and each epoch is one CUDA-graph replay (DeviceDPEpoch)."""
@@ -226,11 +288,29 @@ def train_data_parallel(dataset, config, world: int, rank: int, group=None, grap
     local = np.concatenate(idx) if idx else np.zeros(0, np.int64)
     sub = LabeledDataset(features=dataset.features.take_rows(local), labels=dataset.labels[local])
     batches = DeviceBatches(sub, config.batch_size) if len(local) else None
-    w = torch.zeros(dataset.n_cols, dtype=torch.float64, device="cuda")
-    runner = DeviceDPEpoch(batches, plan, steps_with_rows, config.loss_kind, config.learning_rate, w, group, graph)
-    trace = LossTrace()
-    trace.graph = runner.graph is not None
-    trace.mode = runner.mode
+    runner = None
+    if fused:  # the fused NVLink exchange where every rank can run it (decided collectively)
+        try:
+            runner = FusedDPEpoch(batches, plan, config.loss_kind, config.learning_rate, group)
+            ok = 1
+        except Exception:  # images do not fit, a rank lacks some step, no symmetric memory
+            runner, ok = None, 0
+        flag = torch.tensor([ok], dtype=torch.int32, device="cuda")
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        if not int(flag.item()):
+            runner = None
+        else:
+            runner.connect()
+    if runner is not None:
+        w = runner.w
+        trace = LossTrace()
+        trace.graph, trace.mode = False, "fused"
+    else:
+        w = torch.zeros(dataset.n_cols, dtype=torch.float64, device="cuda")
+        runner = DeviceDPEpoch(batches, plan, steps_with_rows, config.loss_kind, config.learning_rate, w, group, graph)
+        trace = LossTrace()
+        trace.graph = runner.graph is not None
+        trace.mode = runner.mode
     for _ in range(config.epochs):
         start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         start.record()

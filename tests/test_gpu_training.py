@@ -244,7 +244,7 @@ def test_dp_epoch_graph_world1_nccl(oracle, loss):
     from paper_1702_06943_b200 import synth
     from paper_1702_06943_b200.distributed import train_data_parallel
     from paper_1702_06943_b200.matrix import LabeledDataset, SparseRowMatrix
-    from paper_1702_06943_b200.training import TrainConfig
+    from paper_1702_06943_b200.training import TrainConfig, train
 
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -259,10 +259,17 @@ def test_dp_epoch_graph_world1_nccl(oracle, loss):
             y = y * 0.5 + 0.1
         ds = LabeledDataset(features=SparseRowMatrix.from_csr(68, rp, c, v), labels=y)
         cfg = TrainConfig(loss, 250, 0.05, 2)
-        m_g, t_g = train_data_parallel(ds, cfg, 1, 0, graph=True)
-        m_e, t_e = train_data_parallel(ds, cfg, 1, 0, graph=False)
+        m_g, t_g = train_data_parallel(ds, cfg, 1, 0, graph=True, fused=False)
+        m_e, t_e = train_data_parallel(ds, cfg, 1, 0, graph=False, fused=False)
         assert t_g.graph and not t_e.graph and t_g.mode == ("grad" if loss == "squared" else "parts")
         assert np.array_equal(m_g.weights, m_e.weights)
+        # the exchange fused into the cluster epoch kernel (NVLink peer memory): at world 1 the very
+        # same arithmetic as the single-GPU cluster epoch, so bit-identical to train()
+        m_f, t_f = train_data_parallel(ds, cfg, 1, 0)
+        assert t_f.mode == "fused"
+        m_1, t_1 = train(ds, cfg)
+        assert np.array_equal(m_f.weights, m_1.weights)
+        assert np.allclose(m_f.weights, m_g.weights, rtol=1e-9, atol=1e-12)
         w_ref, risks = oracle.train_glm(rp, c, v, y, 68, loss, 250, 0.05, 2, 0)
         assert np.allclose(m_g.weights, w_ref, rtol=1e-9, atol=1e-12), np.max(np.abs(m_g.weights - w_ref))
         assert np.allclose(t_g.risks, risks, rtol=1e-6)
