@@ -9,6 +9,7 @@ single-matrix entry point and returns a host-side LogicalEncoding.
 from __future__ import annotations
 
 import ctypes
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -103,17 +104,27 @@ def compress_csr(n_cols: int, row_ptr, cols, vals, batch_row, *, max_work_bytes:
     elem_base_all = row_ptr[batch_row]
     dev = torch.device("cuda")
     stream = N.stream_handle()
-    # chunk the batches so the hash workspace stays bounded
+    # chunk the batches so the hash workspace stays bounded (the workspace grows with the chunk:
+    # binary search for the longest chunk that fits, at least one batch)
+    def work(b0, b1):
+        s = TocEncodeSizes()
+        eb = np.ascontiguousarray(elem_base_all[b0 : b1 + 1] - elem_base_all[b0])
+        N.check(L.toc_encode_sizes(b1 - b0, eb.ctypes.data_as(ctypes.c_void_p), ctypes.byref(s)), "sizes")
+        return s.work_bytes
+
     chunks, start = [], 0
     while start < n_batches:
-        end = start + 1
-        while end < n_batches:
-            s = TocEncodeSizes()
-            eb = np.ascontiguousarray(elem_base_all[start : end + 2] - elem_base_all[start])
-            N.check(L.toc_encode_sizes(end + 1 - start, eb.ctypes.data_as(ctypes.c_void_p), ctypes.byref(s)), "sizes")
-            if s.work_bytes > max_work_bytes:
-                break
-            end += 1
+        if work(start, n_batches) <= max_work_bytes:
+            end = n_batches
+        else:
+            lo, hi = start + 1, n_batches  # work(start, lo) may exceed: one batch is still a chunk
+            while hi - lo > 1:
+                mid = (lo + hi) // 2
+                if work(start, mid) <= max_work_bytes:
+                    lo = mid
+                else:
+                    hi = mid
+            end = lo
         chunks.append((start, end))
         start = end
     pieces, logical = [], []
@@ -127,8 +138,10 @@ def compress_csr(n_cols: int, row_ptr, cols, vals, batch_row, *, max_work_bytes:
         sizes = TocEncodeSizes()
         N.check(L.toc_encode_sizes(nb, eb.ctypes.data_as(ctypes.c_void_p), ctypes.byref(sizes)), "toc_encode_sizes")
         d_rp = torch.from_numpy(np.ascontiguousarray(rp)).to(dev)
-        d_cols = torch.from_numpy(cols[e0:e1].copy() if e1 > e0 else np.zeros(1, np.int32)).to(dev)
-        d_vals = torch.from_numpy(vals[e0:e1].copy() if e1 > e0 else np.zeros(1)).to(dev)
+        with warnings.catch_warnings():  # read-only views (matrix.py freezes its arrays): uploaded, never written
+            warnings.simplefilter("ignore", UserWarning)
+            d_cols = torch.from_numpy(cols[e0:e1] if e1 > e0 else np.zeros(1, np.int32)).to(dev)
+            d_vals = torch.from_numpy(vals[e0:e1] if e1 > e0 else np.zeros(1)).to(dev)
         d_br = torch.from_numpy(np.ascontiguousarray(br)).to(dev)
         d_eb = torch.from_numpy(eb).to(dev)
         n_el = max(int(sizes.n_elems), 1)
