@@ -422,7 +422,11 @@ def run_mgd(cfg: int, rank: int, world: int, cpu_sample: bool):
 
         _, trace = train_data_parallel(ds, TrainConfig(loss, 250, lr, epochs), world, rank)
         out.update({"steps_per_epoch": -(-len(y) // (250 * world)), "epoch_seconds": trace.seconds,
-                    "risk_per_epoch": trace.risks, "mode": f"data parallel x{world}, NCCL all-reduce per step"})
+                    "risk_per_epoch": trace.risks,
+                    "mode": f"data parallel x{world}: " + (
+                        "gradient exchange fused into the cluster epoch kernel over NVLink peer memory, one launch "
+                        "per epoch" if getattr(trace, "mode", "") == "fused" else
+                        "per step cluster gradient -> NCCL all-reduce -> update, one CUDA graph per epoch")})
     return out
 
 
