@@ -411,6 +411,13 @@ def run_mgd(cfg: int, rank: int, world: int, cpu_sample: bool):
                  "parts": f"one launch per epoch: a {tr.cluster}-CTA cluster over per-CTA part images (built once per "
                           "run), weights and an exact fixed-point gradient in global memory",
                  "relay": "one cooperative relay launch per epoch (tables rebuilt per step)"}
+        # HBM roofline of the epoch: each step reads its TOC1 block and labels once
+        ep_bytes = batches.arena.block_bytes + 8 * len(y)
+        peak, _ = measured_peaks()
+        out["roofline"] = {"bound": "hbm (latency-bound dependency chain in practice)",
+                           "algorithmic_bytes_per_epoch": int(ep_bytes),
+                           "frac": ep_bytes / min(secs) / 1e9 / peak, "peak_gbs": peak,
+                           "us_per_step": min(secs) / batches.arena.n_blocks * 1e6}
         out.update({"steps_per_epoch": int(batches.arena.n_blocks), "epoch_seconds": secs, "risk_per_epoch": risks,
                     "mode": modes[tr.mode], "image_build_seconds": tr.image_build_seconds,
                     "image_bytes": int(tr.image_off[-1]) if tr.mode in ("images", "parts") else 0})
