@@ -308,6 +308,68 @@ class BlockArena:
         N.check(rc, "toc_linalg")
         return R, O
 
+    def linalg_pipelined(self, kind: int, v_h, u_h, R_h, O_h, chunks: int = 4):
+        """A.v and / or v^T.A with the operands and results in pinned host tensors and the arena
+        (with its tree cache) resident: the batches go in `chunks` slices so that the upload of
+        slice k's u, its launch, and the read-back of slice k-1's R / O overlap on three streams.
+        v_h [n_cols], u_h [n_rows_total], R_h [n_rows_total], O_h [n_blocks, n_cols]: float64, pinned.
+        Returns when R_h / O_h hold the results."""
+        torch = self.torch
+        self.raise_corrupt()
+        if self.trees is None:
+            self.build_trees()
+        dev = self.data.device
+        mv, vm = bool(kind & N.TOC_MATVEC), bool(kind & N.TOC_VECMAT)
+        st = getattr(self, "_pipe", None)
+        if st is None:
+            st = self._pipe = {"up": torch.cuda.Stream(), "run": torch.cuda.Stream(), "down": torch.cuda.Stream(),
+                               "v": torch.empty(max(self.n_cols, 1), dtype=torch.float64, device=dev),
+                               "u": torch.empty(max(self.n_rows_total, 1), dtype=torch.float64, device=dev),
+                               "R": torch.empty(max(self.n_rows_total, 1), dtype=torch.float64, device=dev),
+                               "O": torch.empty((max(self.n_blocks, 1), max(self.n_cols, 1)), dtype=torch.float64,
+                                                device=dev)}
+        plan = self.plan(kind)
+        scratch = self._scratch_for(plan)
+        L = N.lib()
+        bounds = np.linspace(0, self.n_blocks, min(max(chunks, 1), max(self.n_blocks, 1)) + 1).astype(np.int64)
+        rb = np.concatenate([self.row_base, [self.n_rows_total]])
+        cur = torch.cuda.current_stream()
+        for s in (st["up"], st["run"], st["down"]):
+            s.wait_stream(cur)
+        with torch.cuda.stream(st["up"]):
+            if mv:
+                st["v"].copy_(v_h, non_blocking=True)
+        for b0, b1 in zip(bounds[:-1].tolist(), bounds[1:].tolist()):
+            if b1 <= b0:
+                continue
+            r0, r1 = int(rb[b0]), int(rb[b1])
+            up = torch.cuda.Event()
+            with torch.cuda.stream(st["up"]):
+                if vm:
+                    st["u"][r0:r1].copy_(u_h[r0:r1], non_blocking=True)
+                up.record()
+            done = torch.cuda.Event()
+            with torch.cuda.stream(st["run"]):
+                st["run"].wait_event(up)
+                rc = L.toc_linalg_trees(
+                    self.data.data_ptr(), self.block_off_d.data_ptr() + 8 * b0, self.meta_d.data_ptr() + 68 * b0,
+                    self.row_base_d.data_ptr() + 8 * b0, int(b1 - b0), ctypes.byref(plan), kind,
+                    st["v"].data_ptr() if mv else None, st["R"].data_ptr() if mv else None,
+                    st["u"].data_ptr() if vm else None,
+                    st["O"].data_ptr() + 8 * int(b0) * self.n_cols if vm else None,
+                    scratch.data_ptr() if scratch is not None else None, self.trees.data_ptr(),
+                    self.tree_off_d.data_ptr() + 8 * b0, ctypes.c_void_p(st["run"].cuda_stream))
+                N.check(rc, "toc_linalg_trees")
+                done.record()
+            with torch.cuda.stream(st["down"]):
+                st["down"].wait_event(done)
+                if mv:
+                    R_h[r0:r1].copy_(st["R"][r0:r1], non_blocking=True)
+                if vm:
+                    O_h[b0:b1].copy_(st["O"][b0:b1], non_blocking=True)
+        st["down"].synchronize()
+        return R_h, O_h
+
     def linalg32(self, kind: int, v=None, u=None, R=None, O=None):
         """The fp32 variant (toc_linalg32) over the tree cache (built on first use): v [n_cols], u
         [n_rows_total] float32 device tensors -> (R [n_rows_total], O [n_blocks, n_cols]) float32."""

@@ -194,3 +194,28 @@ def test_fp32_variant_vs_oracle(oracle, kind):
                 got = O[b].cpu().numpy().astype(np.float64)
                 assert within_rel(got, want, 1e-4), max_rel_err(got, want)
             base += e.n_rows
+
+
+def test_linalg_pipelined_equals_linalg(oracle):
+    """BlockArena.linalg_pipelined (host operands / results, sliced and overlapped) gives exactly
+    the per-batch results of the one-launch call."""
+    import torch
+
+    from paper_1702_06943_b200 import _native as N, synth
+
+    encs = [oracle.encode_csr(784, *synth.dense_to_csr(synth.cfg2_batch_dense(4, b))) for b in range(7)]
+    arena = _arena([oracle.serialize(e) for e in encs])
+    arena.build_trees()
+    rng = np.random.default_rng(2)
+    v = torch.from_numpy(rng.standard_normal(784)).pin_memory()
+    u = torch.from_numpy(rng.standard_normal(arena.n_rows_total)).pin_memory()
+    kind = N.TOC_MATVEC | N.TOC_VECMAT
+    R0, O0 = arena.linalg(kind, v=v.cuda(), u=u.cuda())
+    R = torch.empty(arena.n_rows_total, dtype=torch.float64).pin_memory()
+    O = torch.empty((arena.n_blocks, 784), dtype=torch.float64).pin_memory()
+    for chunks in (1, 3, 7):
+        R.zero_()
+        O.zero_()
+        arena.linalg_pipelined(kind, v, u, R, O, chunks=chunks)
+        assert torch.equal(R, R0.cpu()) and torch.equal(O, O0.cpu())
+
