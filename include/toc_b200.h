@@ -397,6 +397,7 @@ int toc_mlp_set_kernels(int32_t mask);
 /* 1 (default): toc_mlp_epoch captures the epoch's launches into a CUDA graph on its first call and
  * replays it while the arguments (and the host arrays' contents) are unchanged; 0: plain launches. */
 int toc_mlp_set_graph(int32_t on);
+int toc_mlp_set_pdl(int32_t on); /* tuning knob: programmatic dependent launch of the step kernels (default 1) */
 int toc_mlp_scratch(int32_t max_rows, int32_t m, int32_t h, int32_t k, int64_t* bytes);
 int toc_mlp_epoch(const uint8_t* d_cache, const int64_t* h_cache_off, const int64_t* h_row_base,
                   const int32_t* h_n_rows, int64_t n_blocks, int32_t m, int32_t h, int32_t k,

@@ -89,6 +89,13 @@ struct MlpStep {
 // column); the other buffer is zeroed meanwhile (it was read by the previous step).
 constexpr uint32_t kDecodeRowoff = 4096;  // rowoff entries kept in shared memory
 
+// Programmatic dependent launch (the step's kernels are launched with programmatic stream
+// serialization): a kernel waits for its predecessor's completion and memory only where it first
+// needs them, and lets its successor launch right after that wait -- so by induction every kernel
+// before the predecessor has completed whenever a kernel runs.  Both are no-ops without PDL.
+TOC_D void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+TOC_D void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 __global__ void __launch_bounds__(kMlpThreads) mlp_decode_kernel(MlpStep s, uint32_t n) {
   __shared__ uint32_t s_ro[kDecodeRowoff];
   const MlpEntry E = mlp_entry(s.entry);
@@ -96,8 +103,6 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_decode_kernel(MlpStep s, uint
   const bool ro_s = n < kDecodeRowoff;
   if (ro_s)
     for (uint32_t i = threadIdx.x; i <= n; i += blockDim.x) s_ro[i] = __ldg(E.rowoff + i);
-  double2* z = reinterpret_cast<double2*>(s.Az);
-  for (int64_t i = gt; i < s.az_elems / 2; i += gs) z[i] = make_double2(0.0, 0.0);
   __syncthreads();
   const uint32_t C = __ldg(E.rowoff + n), m = (uint32_t)s.m;
   for (int64_t j = gt; j < C; j += gs) {
@@ -115,6 +120,12 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_decode_kernel(MlpStep s, uint
       x = w.x;
     }
   }
+  // (the walks above only read the static cache and write this step's buffer, last read two steps
+  // ago; the other buffer is still read by the previous step's kernels)
+  pdl_wait();
+  pdl_trigger();
+  double2* z = reinterpret_cast<double2*>(s.Az);
+  for (int64_t i = gt; i < s.az_elems / 2; i += gs) z[i] = make_double2(0.0, 0.0);
 }
 
 // The NW warps' partial accumulator tiles (MT m-tiles x kNT n-tiles) summed in warp order; f(row,
@@ -144,6 +155,8 @@ constexpr uint32_t kRightWarps = 16;
 template <int MT>
 __global__ void __launch_bounds__(32 * kRightWarps) mlp_right_kernel(MlpStep s, uint32_t n) {
   extern __shared__ __align__(16) double red[];
+  pdl_wait();  // the decoded batch, and W1 / b1 as the previous step left them
+  pdl_trigger();
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
   const uint32_t m = (uint32_t)s.m, h = (uint32_t)s.h;
   const uint32_t r0 = blockIdx.x * (8 * MT), n0 = blockIdx.y * (8 * kNT);
@@ -194,6 +207,8 @@ __global__ void __launch_bounds__(32 * kRightWarps) mlp_right_kernel(MlpStep s, 
 template <int K>
 __global__ void __launch_bounds__(kMlpThreads) mlp_tail_kernel(MlpStep s, uint32_t n) {
   extern __shared__ __align__(16) double sh[];
+  pdl_wait();  // A1
+  pdl_trigger();
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, h = (uint32_t)s.h;
   double* ps = sh;               // [8][K]
   double* as = ps + 8 * K;       // [8][h]
@@ -271,6 +286,8 @@ template <int MT>
 __global__ void __launch_bounds__(kMlpThreads) mlp_left_kernel(MlpStep s, uint32_t n, uint32_t n_gemm,
                                                                uint32_t n_tail) {
   extern __shared__ __align__(16) double red[];
+  pdl_wait();  // delta and the tail's parts
+  pdl_trigger();
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
   const uint32_t m = (uint32_t)s.m, h = (uint32_t)s.h;
   if (blockIdx.x >= n_gemm) {
@@ -398,6 +415,25 @@ cudaGraphExec_t g_mlp_exec = nullptr;
 }  // namespace
 
 namespace {
+bool g_mlp_pdl = true;  // launch the step kernels with programmatic dependent launch
+
+// One launch, with programmatic stream serialization when enabled (the kernel's pdl_wait then
+// overlaps its launch -- and the decode's chain walks -- with the predecessor's tail).
+template <typename... KArgs, typename... Args>
+void pdl_launch(void (*fn)(KArgs...), dim3 grid, uint32_t block, int smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_mlp_pdl ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, fn, static_cast<KArgs>(args)...);
+}
+
 // Dynamic shared memory of the three GEMM-shaped kernels (set once per process).
 int mlp_attrs(int32_t h, int32_t k) {
   const int smem_right = 8 * (int)toc::kRightWarps * toc::kRightMT * toc::kNT * 64;
@@ -459,14 +495,15 @@ int mlp_enqueue(const uint8_t* d_cache, const int64_t* h_cache_off, const int64_
       s.Ad = adbuf[b & 1];
       s.Az = adbuf[(b + 1) & 1];
       const uint32_t n_tail = (n + 7) / 8;
-      if (g_mlp_mask & 1) toc::mlp_decode_kernel<<<(unsigned)(8 * sms), toc::kMlpThreads, 0, st>>>(s, n);
+      if (g_mlp_mask & 1) pdl_launch(toc::mlp_decode_kernel, dim3((unsigned)(8 * sms)), toc::kMlpThreads, 0, st, s, n);
       if (g_mlp_mask & 2)
-      toc::mlp_right_kernel<toc::kRightMT>
-          <<<dim3((n + 8 * toc::kRightMT - 1) / (8 * toc::kRightMT), ncb), 32 * toc::kRightWarps, smem_right, st>>>(s, n);
-      if (g_mlp_mask & 4) toc::mlp_tail_kernel<10><<<n_tail, toc::kMlpThreads, smem_tail, st>>>(s, n);
+        pdl_launch(toc::mlp_right_kernel<toc::kRightMT>,
+                   dim3((n + 8 * toc::kRightMT - 1) / (8 * toc::kRightMT), ncb), 32 * toc::kRightWarps, smem_right, st,
+                   s, n);
+      if (g_mlp_mask & 4) pdl_launch(toc::mlp_tail_kernel<10>, dim3(n_tail), toc::kMlpThreads, smem_tail, st, s, n);
       if (g_mlp_mask & 8)
-      toc::mlp_left_kernel<toc::kLeftMT>
-          <<<n_gemm_left + n_upd, toc::kMlpThreads, smem_left, st>>>(s, n, n_gemm_left, n_tail);
+        pdl_launch(toc::mlp_left_kernel<toc::kLeftMT>, dim3(n_gemm_left + n_upd), toc::kMlpThreads, smem_left, st, s, n,
+                   n_gemm_left, n_tail);
     }
     return cudaGetLastError() == cudaSuccess ? TOC_OK : TOC_E_CUDA;
 }
@@ -474,6 +511,13 @@ int mlp_enqueue(const uint8_t* d_cache, const int64_t* h_cache_off, const int64_
 
 extern "C" int toc_mlp_set_kernels(int32_t mask) {
   g_mlp_mask = mask & 15;
+  return TOC_OK;
+}
+
+extern "C" int toc_mlp_set_pdl(int32_t on) {
+  g_mlp_pdl = on != 0;
+  if (g_mlp_exec) cudaGraphExecDestroy(g_mlp_exec);  // the captured epoch depends on it
+  g_mlp_exec = nullptr;
   return TOC_OK;
 }
 

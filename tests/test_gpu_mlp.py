@@ -151,3 +151,25 @@ def test_dp_mlp_world1_nccl(oracle, n_rows, batch):
             assert within_rel(got, want, REL), max_rel_err(got, want)
     finally:
         dist.destroy_process_group()
+
+
+def test_mlp_epoch_pdl_matches_plain_launches():
+    """The native epoch with programmatic dependent launch (the default) equals the same epoch
+    launched without it, bit for bit."""
+    from paper_1702_06943_b200 import _native as N, synth
+    from paper_1702_06943_b200.matrix import LabeledDataset, SparseRowMatrix
+    from paper_1702_06943_b200.mlp import train_mlp
+
+    rp, c, v, y = synth.cfg5_dataset(1500, seed=4)
+    ds = LabeledDataset(features=SparseRowMatrix.from_csr(784, rp, c, v), labels=y)
+    kw = dict(hidden=40, classes=10, batch_size=250, learning_rate=0.05, epochs=2, seed=0)
+    try:
+        N.lib().toc_mlp_set_pdl(0)
+        m0, t0 = train_mlp(ds, **kw)
+    finally:
+        N.lib().toc_mlp_set_pdl(1)
+    m1, t1 = train_mlp(ds, **kw)
+    for a, b in ((m0.w1, m1.w1), (m0.b1, m1.b1), (m0.w2, m1.w2), (m0.b2, m1.b2)):
+        assert np.array_equal(a, b)
+    assert t0.risks == t1.risks
+
