@@ -321,6 +321,11 @@ int toc_glm_epoch_parts(const uint8_t* d_images, const int64_t* d_part_off, cons
                         const int32_t* h_counts, int64_t n_blocks, int32_t n_cols, int32_t cluster,
                         int32_t loss, double lr, double* d_w, unsigned long long* d_gacc, int64_t max_part,
                         void* stream);
+/* A-B knob: 1 runs toc_glm_epoch_parts on the DSMEM epoch kernel (weights and the gradient exchange
+ * in distributed shared memory; bit-identical results) when it fits, 0 (default) the global-memory
+ * kernel, which measured faster at config 4 (10.4 vs 12.3 us/step). */
+int toc_mgd_set_parts_dsmem(int32_t on);
+
 /* One data-parallel MGD step on the same part images (training.py:261-281 per rank; the caller
  * all-reduces and applies training.py:296-300): the summed gradient of batch `step` at weights d_w
  * into d_grad[touched columns] (d_grad zero elsewhere; d_gacc left zero). */
