@@ -131,6 +131,9 @@ int toc_linalg(const uint8_t* d_arena, const int64_t* d_block_off, const TocBloc
 int toc_tree_offsets(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t wide, int64_t* h_tree_off);
 /* tuning knob: 1 (default) = cached pair-balanced lane splits + flat chain walk for A.v, 0 = code-count splits */
 int toc_linalg_set_splits(int on);
+/* tuning knob: 1 (default) = toc_build_trees orders each lane range's codes by chain depth (a renumbering of
+ * each row's derived ids; the products are unchanged), 0 = reference order */
+int toc_tree_set_depth_order(int on);
 int toc_build_trees(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
                     int64_t n_blocks, const TocPlan* plan, const int64_t* d_tree_off, uint8_t* d_trees,
                     void* d_scratch, void* stream);

@@ -521,12 +521,10 @@ struct Batch {
   }
 
   // A.v with P1 in tab: emit(r, (A.v)[r]) once per row (by the row's first segment lane).
-  // (Code-count lane ranges: the lockstep two-chain walk measured no faster with the cached
-  // pair-balanced splits, which v^T.A's flat walk uses.)
+  // Lane ranges: the cached pair-balanced splits when present (the cache build orders each range's
+  // codes deepest first, so the lockstep walks of a warp's lanes stay in step), else code counts.
   template <typename E>
   TOC_D void matvec_rows(E&& emit) {
-    const uint16_t* sp = splits;
-    splits = nullptr;
     for (uint32_t k = 0; k < passes; ++k) {
       uint32_t r, lo, hi, db, j0, j1;
       double part = 0.0;
@@ -536,7 +534,6 @@ struct Batch {
       for (uint32_t o = S >> 1; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
       if (ok && sub == 0) emit(r, part);
     }
-    splits = sp;
   }
 
   // G[i] += sum over the pair occurrences of weight(r) (fixed point, scale g_scale); tab must be

@@ -25,7 +25,8 @@ struct LinalgArgs {
   uint8_t* scratch;
   const uint8_t* trees;     // optional device tree cache (toc_build_trees); NULL: rebuild per call
   const int64_t* tree_off;  // byte offset of batch b's tree prefix in `trees`
-  int32_t use_splits;       // cached pair-balanced lane splits + flat walk for A.v (tuning knob)
+  int32_t use_splits;       // cached pair-balanced lane splits (tuning knob)
+  int32_t depth_order;      // tree cache build: order each lane range's codes by depth (tuning knob)
 };
 
 // One batch of the sweep.  `tables` points either into shared memory or into this CTA's slab.
@@ -226,7 +227,73 @@ __global__ void __launch_bounds__(1024, 1) build_trees_kernel(LinalgArgs a) {
     }
     const uint4* src = reinterpret_cast<const uint4*>(tables);
     uint4* dst = reinterpret_cast<uint4*>(entry);
-    for (uint32_t k = threadIdx.x; k < L.tree / 16u; k += blockDim.x) dst[k] = src[k];
+    // (scratch: the old positions in the entry's node-table region, the id map in its pair-record
+    // regions -- both rewritten below)
+    const bool relabel = !kWide && a.depth_order && m.n_cols <= 65535u && m.n_derived < 65536u &&
+                         2u * m.n_derived <= CL.off_splits - CL.off_irec;
+    if (!relabel) {
+      for (uint32_t k = threadIdx.x; k < L.tree / 16u; k += blockDim.x) dst[k] = src[k];
+    } else {
+      // Depth order: within each lane range of every row, the positions are renumbered so that the
+      // codes come deepest first (stable) -- the lanes of a warp then walk chains of similar length
+      // in lockstep.  A renumbering of the row's derived ids: every reference (par fields, final
+      // codes) is remapped, keys (pairs) are unchanged, so every walk computes the same products.
+      const BatchLayout BL = batch_layout<false>(m);
+      uint16_t* sig = reinterpret_cast<uint16_t*>(entry + BL.off_pk);  // new index -> old position
+      const uint32_t S = seg_lanes(m.n_rows, kSplitThreads), nI = B.nI;
+      const uint16_t* sp = reinterpret_cast<const uint16_t*>(entry + CL.off_splits);
+      for (uint32_t r = threadIdx.x; r < B.n; r += blockDim.x) {
+        const uint32_t lo = B.rowoff[r], hi = B.rowoff[r + 1], db = B.dbase[r];
+        if (hi - lo < 2) continue;
+        for (uint32_t s2 = 0; s2 < S; ++s2) {
+          const uint32_t a0 = lo + __ldcg(sp + r * S + s2);
+          uint32_t a1 = s2 + 1 < S ? lo + __ldcg(sp + r * S + s2 + 1) : hi;
+          a1 = min(a1, hi - 1);  // the final code has no derived node: it stays last
+          // insertion sort of the range's positions by code depth (descending), kept in sig
+          for (uint32_t j = a0; j < a1; ++j) {
+            uint32_t x = B.pk.par(db + (j - lo)), dj = 1;
+            while (x > nI) {
+              x = B.pk.par(x - 1 - nI);
+              ++dj;
+            }
+            uint32_t k = j;
+            while (k > a0) {  // sig[db + (k - 1 - lo)] holds the old position now at k - 1
+              const uint32_t op = sig[db + (k - 1 - lo)];
+              uint32_t y = B.pk.par(db + (op - lo)), dk = 1;
+              while (y > nI) {
+                y = B.pk.par(y - 1 - nI);
+                ++dk;
+              }
+              if (dk >= dj) break;
+              sig[db + (k - lo)] = (uint16_t)op;
+              --k;
+            }
+            sig[db + (k - lo)] = (uint16_t)j;
+          }
+        }
+      }
+      __syncthreads();
+      // sig[new index] = old position; invert into the id map, then write the relabelled prefix
+      uint16_t* inv = reinterpret_cast<uint16_t*>(entry + CL.off_irec);  // old derived index -> new
+      for (uint32_t r = threadIdx.x; r < B.n; r += blockDim.x) {
+        const uint32_t lo = B.rowoff[r], hi = B.rowoff[r + 1], db = B.dbase[r];
+        for (uint32_t j = lo; j + 1 < hi; ++j) inv[db + (__ldcg(sig + db + (j - lo)) - lo)] = (uint16_t)(db + (j - lo));
+      }
+      __syncthreads();
+      auto map = [&](uint32_t x) -> uint32_t { return x <= nI ? x : nI + 1u + __ldcg(inv + (x - 1 - nI)); };
+      uint32_t* e32 = reinterpret_cast<uint32_t*>(entry);
+      for (uint32_t k = threadIdx.x; k < BL.off_last / 4u; k += blockDim.x)  // row offsets, derived bases
+        e32[k] = reinterpret_cast<const uint32_t*>(tables)[k];
+      uint32_t* elast = reinterpret_cast<uint32_t*>(entry + BL.off_last);
+      for (uint32_t r = threadIdx.x; r < B.n; r += blockDim.x)  // (empty rows have no final code)
+        elast[r] = B.rowoff[r + 1] > B.rowoff[r] ? map(B.last[r]) : 0u;
+      uint32_t* epk = reinterpret_cast<uint32_t*>(entry + BL.off_pk);
+      for (uint32_t d = threadIdx.x; d < m.n_derived; d += blockDim.x) {
+        uint32_t par, key;
+        B.pk.get(d, par, key);
+        epk[__ldcg(inv + d)] = (map(par) & 0xffffu) | (key << 16);
+      }
+    }
     // unpacked first-layer records, and the (column, pair)-sorted order with column segments
     const uint8_t* blk = a.arena + a.block_off[b];
     const uint32_t nI = m.n_pairs, tid = threadIdx.x, nth = blockDim.x;
@@ -299,6 +366,7 @@ __global__ void __launch_bounds__(1024, 1) build_trees_kernel(LinalgArgs a) {
 namespace {
 
 int g_use_splits = 1;
+int g_depth_order = 1;
 
 struct DevProps {
   int sm_count = 0, smem_optin = 0, smem_per_sm = 0;
@@ -411,6 +479,11 @@ extern "C" int toc_linalg_set_splits(int on) {
   return TOC_OK;
 }
 
+extern "C" int toc_tree_set_depth_order(int on) {
+  g_depth_order = on ? 1 : 0;
+  return TOC_OK;
+}
+
 extern "C" int toc_tree_offsets(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t wide, int64_t* h_tree_off) {
   if (!h_meta || !h_tree_off || n_blocks < 0) return TOC_E_ARG;
   int64_t o = 0;
@@ -438,6 +511,7 @@ extern "C" int toc_build_trees(const uint8_t* d_arena, const int64_t* d_block_of
   a.scratch = (uint8_t*)d_scratch;
   a.trees = d_trees;
   a.tree_off = d_tree_off;
+  a.depth_order = g_depth_order;
   void* fn = plan->wide ? (void*)toc::build_trees_kernel<true> : (void*)toc::build_trees_kernel<false>;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, plan->smem_bytes) != cudaSuccess)
     return TOC_E_CUDA;

@@ -16,6 +16,7 @@ p.add_argument("--trees", type=int, default=1)
 p.add_argument("--levels", type=int, default=0)
 p.add_argument("--prefetch", type=int, default=-1)
 p.add_argument("--splits", type=int, default=-1)
+p.add_argument("--depth", type=int, default=-1)
 a = p.parse_args()
 
 import torch  # noqa: E402
@@ -25,6 +26,9 @@ from paper_1702_06943_b200.codec import compress_csr  # noqa: E402
 
 rp, c, v, br = bench.make_shard(0, a.batches)
 arena = compress_csr(bench.COLS, rp, c, v, br)
+if a.depth >= 0:
+    from paper_1702_06943_b200 import _native as N
+    N.lib().toc_tree_set_depth_order(a.depth)
 if a.trees:
     arena.build_trees()
 if a.levels:
