@@ -587,32 +587,39 @@ struct Batch {
   TOC_D void column_sums(const typename PairRec<kWide>::T* prec, const uint2* segs, uint32_t n_segs, double g_inv,
                          Out&& out, uint32_t L = 0) const {
     using R = PairRec<kWide>;
-    constexpr uint32_t U = 4;
+    // G lanes per column, up to U record loads in flight per lane; the next round's segment bounds
+    // are loaded while this round's records are summed (the rounds are L2-latency bound)
+    constexpr uint32_t G = 2, U = 8;
     const uint32_t* lo = tabw;
     const uint32_t* hi = tabw + (nI + 1);
-    const uint32_t tid = threadIdx.x, quads = blockDim.x >> 2;
-    const uint32_t span = ((n_segs + quads - 1) / quads) * quads;
-    for (uint32_t s = tid >> 2; s < span; s += quads) {
+    const uint32_t tid = threadIdx.x, groups = blockDim.x / G, sub = tid % G;
+    const uint32_t span = ((n_segs + groups - 1) / groups) * groups;
+    uint32_t s = tid / G;
+    uint2 sg = s < n_segs ? __ldg(segs + s) : make_uint2(0u, 0u);
+    uint32_t end = s < n_segs ? __ldg(&segs[s + 1].x) : 0u;
+    for (; s < span; s += groups) {
+      const uint32_t sn = s + groups;
+      const uint2 sgn = sn < n_segs ? __ldg(segs + sn) : make_uint2(0u, 0u);
+      const uint32_t endn = sn < n_segs ? __ldg(&segs[sn + 1].x) : 0u;
       double c = 0.0;
-      uint2 sg = make_uint2(0u, 0u);
       if (s < n_segs) {
-        sg = __ldg(segs + s);
-        const uint32_t end = __ldg(&segs[s + 1].x);
-        for (uint32_t q0 = sg.x + (tid & 3u); q0 < end; q0 += 4 * U) {
+        for (uint32_t q0 = sg.x + sub; q0 < end; q0 += G * U) {
           typename R::T pr[U];
 #pragma unroll
-          for (uint32_t k = 0; k < U; ++k) pr[k] = q0 + 4 * k < end ? __ldg(prec + q0 + 4 * k) : R::none();
+          for (uint32_t k = 0; k < U; ++k) pr[k] = q0 + G * k < end ? __ldg(prec + q0 + G * k) : R::none();
 #pragma unroll
           for (uint32_t k = 0; k < U; ++k)
-            if (q0 + 4 * k < end) {
+            if (q0 + G * k < end) {
               const uint32_t i = R::a(pr[k]) + 1;
               c += uniq[R::b(pr[k])] * (L ? limb_value(lo[i], (int32_t)hi[i], L, g_inv) : fix_value(lo[i], hi[i], g_inv));
             }
         }
       }
-      c += __shfl_xor_sync(0xffffffffu, c, 1);
-      c += __shfl_xor_sync(0xffffffffu, c, 2);
-      if (s < n_segs && (tid & 3u) == 0) out(sg.y, c);
+#pragma unroll
+      for (uint32_t o = 1; o < G; o <<= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if (s < n_segs && sub == 0) out(sg.y, c);
+      sg = sgn;
+      end = endn;
     }
   }
 
