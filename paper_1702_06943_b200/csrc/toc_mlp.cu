@@ -204,6 +204,11 @@ __global__ void __launch_bounds__(32 * kRightWarps) mlp_right_kernel(MlpStep s, 
 // Per row (one warp, 8 rows per CTA): logits = A1 W2 + b2, P = softmax - onehot, delta = (P W2^T) *
 // [A1 > 0]; then the CTA's sums over its rows of A1^T P, delta and P (its part of the W2 / b1 / b2
 // gradients, summed over the CTAs by mlp_left in CTA order).
+#ifndef MLP_TAIL_ROWS
+#define MLP_TAIL_ROWS 8
+#endif
+constexpr uint32_t kTailRows = MLP_TAIL_ROWS;  // rows (one warp each) per tail CTA
+
 template <int K>
 __global__ void __launch_bounds__(kMlpThreads) mlp_tail_kernel(MlpStep s, uint32_t n) {
   extern __shared__ __align__(16) double sh[];
@@ -211,10 +216,10 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_tail_kernel(MlpStep s, uint32
   pdl_trigger();
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, h = (uint32_t)s.h;
   double* ps = sh;               // [8][K]
-  double* as = ps + 8 * K;       // [8][h]
-  double* ds = as + 8 * h;       // [8][h]
+  double* as = ps + kTailRows * K;  // [rows][h]
+  double* ds = as + kTailRows * h;  // [rows][h]
   const double* W2 = s.W2;       // [h x K], read through L1
-  const uint32_t r0 = blockIdx.x * 8, r = r0 + warp, nr = min(8u, n - r0);
+  const uint32_t r0 = blockIdx.x * kTailRows, r = r0 + warp, nr = min(kTailRows, n - r0);
   if (r < n) {
     const double* a1 = s.A1 + (int64_t)r * h;
     double* arow = as + warp * h;
@@ -358,8 +363,14 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_left_kernel(MlpStep s, uint32
   });
 }
 
-constexpr int kRightMT = 1;
-constexpr int kLeftMT = 2;
+#ifndef MLP_RIGHT_MT
+#define MLP_RIGHT_MT 2
+#endif
+constexpr int kRightMT = MLP_RIGHT_MT;
+#ifndef MLP_LEFT_MT
+#define MLP_LEFT_MT 2
+#endif
+constexpr int kLeftMT = MLP_LEFT_MT;
 
 }  // namespace toc
 
@@ -382,7 +393,7 @@ MlpScratch mlp_scratch_layout(int32_t nmax, int32_t m, int32_t h, int32_t k) {
   L.ad = o;  // two decode buffers
   o += 2 * (((int64_t)nmax * m + 1) & ~1ll);
   L.part = o;
-  o += (int64_t)((nmax + 7) / 8) * (h * k + h + k);
+  o += (int64_t)((nmax + toc::kTailRows - 1) / toc::kTailRows) * (h * k + h + k);
   L.total = o;
   return L;
 }
@@ -438,7 +449,7 @@ void pdl_launch(void (*fn)(KArgs...), dim3 grid, uint32_t block, int smem, cudaS
 int mlp_attrs(int32_t h, int32_t k) {
   const int smem_right = 8 * (int)toc::kRightWarps * toc::kRightMT * toc::kNT * 64;
   const int smem_left = 8 * 8 * toc::kLeftMT * toc::kNT * 64;
-  const int smem_tail = 8 * (8 * k + 16 * h);
+  const int smem_tail = 8 * (int)toc::kTailRows * (k + 2 * h);
   if (smem_tail > 200 * 1024) return TOC_E_ARG;
   if (cudaFuncSetAttribute(toc::mlp_right_kernel<toc::kRightMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            smem_right) != cudaSuccess ||
@@ -459,7 +470,7 @@ int mlp_enqueue(const uint8_t* d_cache, const int64_t* h_cache_off, const int64_
     const MlpScratch SL = mlp_scratch_layout(nmax, m, h, k);
     const int smem_right = 8 * (int)toc::kRightWarps * toc::kRightMT * toc::kNT * 64;
     const int smem_left = 8 * 8 * toc::kLeftMT * toc::kNT * 64;
-    const int smem_tail = 8 * (8 * k + 16 * h);
+    const int smem_tail = 8 * (int)toc::kTailRows * (k + 2 * h);
     double* base = reinterpret_cast<double*>(d_scratch);
     const int64_t ad_elems = ((int64_t)nmax * m + 1) & ~1ll;
     double* adbuf[2] = {base + SL.ad, base + SL.ad + ad_elems};
@@ -494,13 +505,13 @@ int mlp_enqueue(const uint8_t* d_cache, const int64_t* h_cache_off, const int64_
       s.step = lr / (double)n;
       s.Ad = adbuf[b & 1];
       s.Az = adbuf[(b + 1) & 1];
-      const uint32_t n_tail = (n + 7) / 8;
+      const uint32_t n_tail = (n + toc::kTailRows - 1) / toc::kTailRows;
       if (g_mlp_mask & 1) pdl_launch(toc::mlp_decode_kernel, dim3((unsigned)(8 * sms)), toc::kMlpThreads, 0, st, s, n);
       if (g_mlp_mask & 2)
         pdl_launch(toc::mlp_right_kernel<toc::kRightMT>,
                    dim3((n + 8 * toc::kRightMT - 1) / (8 * toc::kRightMT), ncb), 32 * toc::kRightWarps, smem_right, st,
                    s, n);
-      if (g_mlp_mask & 4) pdl_launch(toc::mlp_tail_kernel<10>, dim3(n_tail), toc::kMlpThreads, smem_tail, st, s, n);
+      if (g_mlp_mask & 4) pdl_launch(toc::mlp_tail_kernel<10>, dim3(n_tail), 32 * toc::kTailRows, smem_tail, st, s, n);
       if (g_mlp_mask & 8)
         pdl_launch(toc::mlp_left_kernel<toc::kLeftMT>, dim3(n_gemm_left + n_upd), toc::kMlpThreads, smem_left, st, s, n,
                    n_gemm_left, n_tail);
