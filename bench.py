@@ -538,8 +538,29 @@ def run_e2e(torch, arena, v_h, u_h, steps: int, world: int = 1):
     for _ in range(steps):
         sweep.run(v_h, u_h)
     dt = _wall_max(torch, time.perf_counter() - t0, world)
+    link = h2d_link_gbs(torch, sweep.h2d_bytes)
+    achieved = sweep.h2d_bytes * steps / dt / 1e9
     return {"value": world * sweep.n_rows * steps / dt, "unit": "rows/s", "h2d_bytes_per_step": sweep.h2d_bytes,
-            "d2h_bytes_per_step": sweep.d2h_bytes, "api": "paper_1702_06943_b200.kernels.BatchSweep.run"}
+            "d2h_bytes_per_step": sweep.d2h_bytes, "api": "paper_1702_06943_b200.kernels.BatchSweep.run",
+            "h2d_gbs": achieved, "h2d_link_gbs": link, "link_frac": achieved / link if link else None,
+            "link_note": "h2d_link_gbs: one pinned host->device copy of the same byte count, best of 5 "
+                         "(CUDA events); the streamed TOC1 upload bounds this e2e number"}
+
+
+def h2d_link_gbs(torch, nbytes: int) -> float:
+    """Host->device bandwidth of this box's link for one pinned copy of `nbytes`."""
+    src = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    dst = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    best = float("inf")
+    for _ in range(6):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dst.copy_(src, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1) / 1e3)
+    del src, dst
+    return nbytes / best / 1e9
 
 
 def run_e2e_resident(torch, arena, v_h, u_h, steps: int, world: int = 1):

@@ -329,6 +329,11 @@ int toc_glm_epoch_parts(const uint8_t* d_images, const int64_t* d_part_off, cons
  * kernel, which measured faster at config 4 (10.4 vs 12.3 us/step). */
 int toc_mgd_set_parts_dsmem(int32_t on);
 
+/* The largest power-of-two cluster (<= 16; sizes above 8 are non-portable) this device co-schedules
+ * for the part-image epoch with a full shared-memory carve-out per CTA, into *cluster.  The part
+ * images are built for one cluster size (toc_mgd_parts_count / _build take it). */
+int toc_mgd_parts_cluster_max(int32_t* cluster);
+
 /* One data-parallel MGD step on the same part images (training.py:261-281 per rank; the caller
  * all-reduces and applies training.py:296-300): the summed gradient of batch `step` at weights d_w
  * into d_grad[touched columns] (d_grad zero elsewhere; d_gacc left zero). */

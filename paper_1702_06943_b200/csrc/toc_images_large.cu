@@ -22,6 +22,10 @@
 
 namespace toc {
 
+// Part images and their epochs take clusters up to 16 CTAs (sizes above 8 are non-portable:
+// the launch opts in with cudaFuncAttributeNonPortableClusterSizeAllowed).
+constexpr uint32_t kMaxPartsCluster = 16;
+
 // Part header (64 B): u32 [0] rows [1] pairs nP [2] derived nD [3] codes [4] owned columns
 // [5] batch rows; f64 at 24: sum |y| of the batch, at 32: max |value| of the batch; i64 at 40:
 // byte offset of the same CTA's part of the NEXT batch relative to this part, u32 at 48: its bytes.
@@ -64,7 +68,11 @@ TOC_HD PartLayout part_layout(uint32_t nr, uint32_t nP, uint32_t nD, uint32_t nC
 
 // Bits of a 32-column word whose column is congruent to o mod C (C divides 32).
 TOC_HD uint32_t residue_mask(uint32_t o, uint32_t C) {
-  const uint32_t base = C == 1 ? 0xffffffffu : C == 2 ? 0x55555555u : C == 4 ? 0x11111111u : 0x01010101u;
+  const uint32_t base = C == 1    ? 0xffffffffu
+                        : C == 2  ? 0x55555555u
+                        : C == 4  ? 0x11111111u
+                        : C == 8  ? 0x01010101u
+                                  : 0x00010001u;  // C == 16 (cluster sizes are powers of two)
   return base << o;
 }
 
@@ -91,11 +99,11 @@ __global__ void __launch_bounds__(1024, 1) large_image_kernel(LargeArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   uint32_t* s_warp = reinterpret_cast<uint32_t*>(smem);
   double* s_red = reinterpret_cast<double*>(smem + 160);
-  __shared__ uint32_t s_cnt[4 + kMaxCluster];
+  __shared__ uint32_t s_cnt[4 + kMaxPartsCluster];
   uint8_t* p = smem + kFixedBytes;
   const uint32_t tid = threadIdx.x, nth = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nth >> 5;
   const uint32_t C = (uint32_t)a.cluster, m = (uint32_t)a.n_cols;
-  uint32_t* mark = a.scratch + (int64_t)blockIdx.x * (2 * a.id_words + (1 + kMaxCluster) * a.col_words);
+  uint32_t* mark = a.scratch + (int64_t)blockIdx.x * (2 * a.id_words + (1 + kMaxPartsCluster) * a.col_words);
   uint32_t* base = mark + a.id_words;
   uint32_t* colmark = base + a.id_words;
   uint32_t* rpre = colmark + a.col_words;  // per owner: touched owned columns in earlier words
@@ -113,7 +121,7 @@ __global__ void __launch_bounds__(1024, 1) large_image_kernel(LargeArgs a) {
     B.build_nodes();
     const uint32_t nI = B.nI, T = 1u + nI + mb.n_derived, n = B.n;
     for (uint32_t w = tid; w < (m + 31) / 32; w += nth) colmark[w] = 0u;
-    if (tid < kMaxCluster) s_cnt[4 + tid] = 0u;
+    if (tid < kMaxPartsCluster) s_cnt[4 + tid] = 0u;
     const int64_t rb = a.row_base[b];
     double ys = 0.0;
     for (uint32_t r = tid; r < n; r += nth) ys += fabs(a.labels[rb + r]);
@@ -259,7 +267,7 @@ __global__ void __launch_bounds__(1024, 1) large_image_kernel(LargeArgs a) {
         uint16_t* bslot = reinterpret_cast<uint16_t*>(img + L.off_bslot);
         uint32_t* bkt = reinterpret_cast<uint32_t*>(img + L.off_bkt);
         uint16_t* bown = reinterpret_cast<uint16_t*>(img + L.off_bown);
-        uint32_t cnt[kMaxCluster], st[kMaxCluster];
+        uint32_t cnt[kMaxPartsCluster], st[kMaxPartsCluster];
         for (uint32_t o = 0; o < C; ++o) cnt[o] = 0u;
         for (uint32_t l = 0; l < nP; ++l) ++cnt[__ldcg(pcol + l) % C];
         uint32_t acc = 0;
@@ -477,8 +485,8 @@ __global__ void __launch_bounds__(1024, 1) epoch_dsmem_kernel(DsmemEpochArgs a) 
   p += align16(4u * a.max_own);                        // two words (exact split-word adds, fix_add_pair)
   uint32_t* ghi_own = reinterpret_cast<uint32_t*>(p);
   p += align16(4u * a.max_own);
-  __shared__ uint32_t s_k0[kMaxCluster], s_k1[kMaxCluster];
-  __shared__ const uint16_t* s_bown[kMaxCluster];
+  __shared__ uint32_t s_k0[kMaxPartsCluster], s_k1[kMaxPartsCluster];
+  __shared__ const uint16_t* s_bown[kMaxPartsCluster];
   double* p1 = reinterpret_cast<double*>(p);
   unsigned long long* bucket = reinterpret_cast<unsigned long long*>(p);  // aliases P1 (dead by then)
   p += align16(8u * (a.max_pairs + 1));
@@ -662,7 +670,7 @@ int large_launch(const toc::LargeArgs& a0, const LargePlan& P, bool write, void*
   a.col_words = P.col_words;
   a.batch_smem_budget = P.budget;
   a.slab_bytes = P.slab;
-  a.slab = reinterpret_cast<uint8_t*>(d_scratch) + (int64_t)ctas * 4 * (2 * P.id_words + (1 + toc::kMaxCluster) * P.col_words);
+  a.slab = reinterpret_cast<uint8_t*>(d_scratch) + (int64_t)ctas * 4 * (2 * P.id_words + (1 + toc::kMaxPartsCluster) * P.col_words);
   void* fn = P.wide ? (write ? (void*)toc::large_image_kernel<true, true> : (void*)toc::large_image_kernel<true, false>)
                     : (write ? (void*)toc::large_image_kernel<false, true> : (void*)toc::large_image_kernel<false, false>);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, P.build_smem) != cudaSuccess)
@@ -678,7 +686,7 @@ extern "C" int toc_mgd_parts_scratch(const TocBlockMeta* h_meta, int64_t n_block
   const LargePlan P = large_plan(h_meta, n_blocks, n_cols);
   const int sms = la_attr(cudaDevAttrMultiProcessorCount, 148);
   const int64_t ctas = std::min<int64_t>(std::max<int64_t>(n_blocks, 1), sms);
-  *bytes = ctas * 4 * (2ll * P.id_words + (1 + toc::kMaxCluster) * P.col_words) + ctas * P.slab + 16;
+  *bytes = ctas * 4 * (2ll * P.id_words + (1 + toc::kMaxPartsCluster) * P.col_words) + ctas * P.slab + 16;
   return TOC_OK;
 }
 
@@ -687,7 +695,7 @@ extern "C" int toc_mgd_parts_count(const uint8_t* d_arena, const int64_t* d_bloc
                                    int32_t n_cols, int32_t cluster, const double* d_labels, int32_t* d_counts,
                                    void* d_scratch, void* stream) {
   if (n_blocks <= 0) return n_blocks == 0 ? TOC_OK : TOC_E_ARG;
-  if (!h_meta || !d_counts || !d_scratch || !d_labels || cluster < 1 || cluster > (int32_t)toc::kMaxCluster)
+  if (!h_meta || !d_counts || !d_scratch || !d_labels || cluster < 1 || cluster > (int32_t)toc::kMaxPartsCluster || (cluster & (cluster - 1)))
     return TOC_E_ARG;
   for (int64_t b = 0; b < n_blocks; ++b)
     if (h_meta[b].status != TOC_OK || h_meta[b].corrupt) return h_meta[b].status ? h_meta[b].status : TOC_E_CORRUPT;
@@ -731,7 +739,7 @@ extern "C" int toc_mgd_parts_build(const uint8_t* d_arena, const int64_t* d_bloc
                                    const int64_t* d_part_off, uint8_t* d_images, void* d_scratch, void* stream) {
   if (n_blocks <= 0) return n_blocks == 0 ? TOC_OK : TOC_E_ARG;
   if (!h_meta || !d_counts || !d_part_off || !d_images || !d_scratch || !d_labels || cluster < 1 ||
-      cluster > (int32_t)toc::kMaxCluster)
+      cluster > (int32_t)toc::kMaxPartsCluster || (cluster & (cluster - 1)))
     return TOC_E_ARG;
   toc::LargeArgs a{};
   a.arena = d_arena;
@@ -804,6 +812,9 @@ static int dsmem_launch(const uint8_t* d_images, const int64_t* d_part_off, cons
   a.max_rows = max_rows;
   a.max_own = max_own;
   a.w_slots = w_slots;
+  if (cluster > 8 && cudaFuncSetAttribute(toc::epoch_dsmem_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                          cudaSuccess)
+    return TOC_E_CUDA;
   if (cudaFuncSetAttribute(toc::epoch_dsmem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return TOC_E_CUDA;
@@ -829,7 +840,7 @@ static int parts_launch(const uint8_t* d_images, const int64_t* d_part_off, cons
                         double* d_grad, void* stream) {
   if (n_blocks <= 0) return n_blocks == 0 ? TOC_OK : TOC_E_ARG;
   if (!d_images || !d_part_off || !h_meta || !h_counts || !d_w || !d_gacc || cluster < 1 ||
-      cluster > (int32_t)toc::kMaxCluster || (loss != TOC_LOSS_LOGISTIC && loss != TOC_LOSS_HINGE))
+      cluster > (int32_t)toc::kMaxPartsCluster || (cluster & (cluster - 1)) || (loss != TOC_LOSS_LOGISTIC && loss != TOC_LOSS_HINGE))
     return TOC_E_ARG;
   if (g_parts_dsmem && !d_grad && t0 == 0 && t1 == n_blocks) {
     const int rc = dsmem_launch(d_images, d_part_off, h_meta, h_counts, n_blocks, n_cols, cluster, loss, lr, d_w,
@@ -856,6 +867,9 @@ static int parts_launch(const uint8_t* d_images, const int64_t* d_part_off, cons
   a.t0 = t0;
   a.t1 = t1;
   a.grad_out = d_grad;
+  if (cluster > 8 && cudaFuncSetAttribute(toc::epoch_large_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
+                          cudaSuccess)
+    return TOC_E_CUDA;
   if (cudaFuncSetAttribute(toc::epoch_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)
     return TOC_E_CUDA;
@@ -895,4 +909,33 @@ extern "C" int toc_glm_grad_parts(const uint8_t* d_images, const int64_t* d_part
 extern "C" int toc_mgd_set_parts_dsmem(int32_t on) {
   g_parts_dsmem = on ? 1 : 0;
   return TOC_OK;
+}
+
+extern "C" int toc_mgd_parts_cluster_max(int32_t* cluster) {
+  if (!cluster) return TOC_E_ARG;
+  const int optin = la_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin, 232448);
+  if (cudaFuncSetAttribute(toc::epoch_large_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, optin) !=
+          cudaSuccess ||
+      cudaFuncSetAttribute(toc::epoch_large_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+    return TOC_E_CUDA;
+  for (int32_t c = (int32_t)toc::kMaxPartsCluster; c >= 1; c >>= 1) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(c);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = (size_t)optin;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = c;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, (void*)toc::epoch_large_kernel, &cfg) == cudaSuccess && n >= 1) {
+      *cluster = c;
+      return TOC_OK;
+    }
+    (void)cudaGetLastError();
+  }
+  return TOC_E_CUDA;
 }
