@@ -33,7 +33,7 @@
 
 namespace toc {
 
-constexpr uint32_t kImageHeader = 208;
+constexpr uint32_t kImageHeader = 336;
 
 // Header (u32 words unless noted):
 //   [0] n_rows [1] n_pairs [2] n_derived [3] n_uniques [4] n_codes [5] n_segs [6] cluster [7] threads
@@ -41,12 +41,12 @@ constexpr uint32_t kImageHeader = 208;
 //   [10..15] codes, nodes, irec, prec, segs, uniq offsets
 //   [16] shared-region bytes [17] image bytes (the next image starts right after) [18] next
 //        image's shared-region bytes
-//   [20 + 2c], [21 + 2c]: rows and log2 lanes per row of CTA c's part
-//   [36 + 2c], [37 + 2c]: offset and bytes of CTA c's part in the NEXT image
+//   [20 + 2c], [21 + 2c]: rows and log2 lanes per row of CTA c's part (c < kMaxCluster = 16)
+//   [52 + 2c], [53 + 2c]: offset and bytes of CTA c's part in the NEXT image
 // so each step finds its own part and the next batch's copy parameters in the image it already
 // holds, with no dependent global load on the step's path.
 enum { kCodes, kNodes, kIrec, kPrec, kSegs, kUniq };
-enum { kHShared = 16, kHTotal = 17, kHNextShared = 18, kHPart = 20, kHNextPart = 36 };
+enum { kHShared = 16, kHTotal = 17, kHNextShared = 18, kHPart = 20, kHNextPart = 52 };
 
 struct ImageLayout {
   uint32_t off[6], shared;        // shared region [0, shared)
@@ -593,7 +593,7 @@ ImagePlan image_plan(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t n_col
   const uint64_t build = (uint64_t)toc::kFixedBytes + 8ull * P.sort_slots + toc::align16(2u * P.max_codes) + max_tables;
   P.build_ok = build <= (uint64_t)optin;
   P.build_smem = (int)std::min<uint64_t>(build, INT32_MAX);
-  for (uint32_t C : {8u, 4u, 2u, 1u}) {
+  for (uint32_t C : {16u, 8u, 4u, 2u, 1u}) {
     if (cluster_req > 0 && C != (uint32_t)cluster_req) continue;
     if (cluster_req <= 0 && C > 1 && max_rows < 24u * C) continue;
     const uint32_t T = C == 1 ? 1024u : (g_image_threads > 0 ? (uint32_t)g_image_threads : 512u);
@@ -733,6 +733,8 @@ static int epoch_images_launch(const uint8_t* d_images, const int64_t* d_image_o
   }
   void* fn = P.wide ? (void*)toc::epoch_cluster_kernel<true> : (void*)toc::epoch_cluster_kernel<false>;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, P.epoch_smem) != cudaSuccess)
+    return TOC_E_CUDA;
+  if (P.cluster > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
     return TOC_E_CUDA;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(P.cluster);

@@ -6,7 +6,7 @@
 
 namespace toc {
 
-constexpr uint32_t kMaxCluster = 8;  // portable cluster size
+constexpr uint32_t kMaxCluster = 16;  // 16: non-portable (cudaFuncAttributeNonPortableClusterSizeAllowed)
 
 // Node table of a step image.
 template <bool kWide>

@@ -182,7 +182,7 @@ class GlmTrainer:
         self.mode = "relay"
         self.image_build_seconds = 0.0
         self.cluster = 0
-        if mode == "images" or (mode == "auto" and cluster <= 8):  # step images: clusters of up to 8
+        if mode in ("auto", "images"):
             self._build_images(mode == "images", cluster)
         if self.mode == "relay" and mode in ("auto", "parts"):
             self._build_parts(mode == "parts", cluster or parts_cluster())

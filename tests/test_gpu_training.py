@@ -142,7 +142,7 @@ def _trainer(rp, c, v, y, n_cols, bs, loss, lr, mode, cluster=0):
 
 @pytest.mark.parametrize("loss,lr,cluster", [("logistic", 0.1, 1), ("logistic", 0.1, 2), ("logistic", 0.1, 4),
                                              ("logistic", 0.1, 8), ("hinge", 0.05, 8), ("squared", 1e-3, 1),
-                                             ("squared", 1e-3, 4)])
+                                             ("squared", 1e-3, 4), ("logistic", 0.1, 16)])
 def test_step_images_match_relay(loss, lr, cluster):
     """The cluster epoch over cached step images computes what the relay computes: the same fixed-
     point G per row set; only the per-column sums of value * G run in fp64 in (column, pair, CTA)
