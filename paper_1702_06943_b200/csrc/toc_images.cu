@@ -303,6 +303,19 @@ __global__ void __launch_bounds__(1024, 1) image_build_kernel(ImageArgs a) {
   }
 }
 
+// The C CTAs' partials at the offset of p, summed in rank order; loads issued 8 at a time.
+TOC_D double sum_partials(const double* p, uint32_t C) {
+  double g = 0.0;
+  for (uint32_t c0 = 0; c0 < C; c0 += 8) {
+    double r[8];
+#pragma unroll
+    for (uint32_t j = 0; j < 8; ++j) r[j] = c0 + j < C ? ld_dsmem(p, c0 + j) : 0.0;
+#pragma unroll
+    for (uint32_t j = 0; j < 8; ++j) g += r[j];
+  }
+  return g;
+}
+
 TOC_D void trace_stamp(const ImageArgs& a, uint32_t cta, int64_t t, int k) {
   if (a.trace && cta == 0 && threadIdx.x == 0) a.trace[t * kTracePoints + k] = clock64();
 }
@@ -497,12 +510,7 @@ __global__ void __launch_bounds__(1024, 1) epoch_cluster_kernel(ImageArgs a) {
         for (uint32_t c = tid; c < m; c += nth) gl[c] = 0.0;
         __syncthreads();
         for (uint32_t sgi = tid; sgi < n_segs; sgi += nth) {
-          double g = 0.0, r[kMaxCluster];
-#pragma unroll
-          for (uint32_t c = 0; c < kMaxCluster; ++c) r[c] = c < C ? ld_dsmem(cp + sgi, c) : 0.0;
-#pragma unroll
-          for (uint32_t c = 0; c < kMaxCluster; ++c) g += r[c];  // rank order (as the 1-GPU epoch)
-          gl[segcol[sgi]] = g;
+          gl[segcol[sgi]] = sum_partials(cp + sgi, C);  // rank order (as the 1-GPU epoch)
         }
         __syncthreads();
         const size_t slot = ((size_t)(t & 1) * W + (uint32_t)a.rank) * m;
@@ -532,12 +540,7 @@ __global__ void __launch_bounds__(1024, 1) epoch_cluster_kernel(ImageArgs a) {
     // g[c] = partials summed in rank order (identical in every CTA), w[c] -= (lr/|B|) g[c]
     // (apply_update, training.py:296-300)
     for (uint32_t sgi = tid; sgi < n_segs; sgi += nth) {
-      double g = 0.0;
-      double r[kMaxCluster];
-#pragma unroll
-      for (uint32_t c = 0; c < kMaxCluster; ++c) r[c] = c < C ? ld_dsmem(cp + sgi, c) : 0.0;
-#pragma unroll
-      for (uint32_t c = 0; c < kMaxCluster; ++c) g += r[c];  // rank order
+      const double g = sum_partials(cp + sgi, C);  // rank order
       const uint32_t col = segcol[sgi];
       ws[col] = __dsub_rn(ws[col], __dmul_rn(step, g));
     }
