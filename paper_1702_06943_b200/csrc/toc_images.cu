@@ -31,6 +31,10 @@
 
 #include "toc_images.cuh"
 
+#ifndef TOC_IMG_LPC
+#define TOC_IMG_LPC 4
+#endif
+
 namespace toc {
 
 constexpr uint32_t kImageHeader = 336;
@@ -478,10 +482,10 @@ __global__ void __launch_bounds__(1024, 1) epoch_cluster_kernel(ImageArgs a) {
     }
     __syncthreads();
     trace_stamp(a, cta, t, 5);
-    // per-column partial sums of value * G: 8 lanes per column, pairs strided over the lanes,
-    // then a fixed shuffle tree (deterministic)
+    // per-column partial sums of value * G: LPC lanes per column, pairs strided over the lanes
+    // (up to U record loads in flight per lane), then a fixed shuffle tree (deterministic)
     double* cp = cpart + (size_t)k * a.max_segs;
-    constexpr uint32_t LPC = 8;
+    constexpr uint32_t LPC = TOC_IMG_LPC, U = 4;
     const uint32_t seg_span = ((n_segs + (nth / LPC) - 1) / (nth / LPC)) * (nth / LPC);
     for (uint32_t sgi = tid / LPC; sgi < seg_span; sgi += nth / LPC) {
       double c = 0.0;
@@ -489,9 +493,14 @@ __global__ void __launch_bounds__(1024, 1) epoch_cluster_kernel(ImageArgs a) {
       if (sgi < n_segs) {
         sg = segs[sgi];
         const uint32_t end = segs[sgi + 1].x;
-        for (uint32_t q = sg.x + (tid % LPC); q < end; q += LPC) {
-          const uint2 pr = prec[q];
-          c += uniq[pr.y] * limb_value(glo[pr.x + 1], (int32_t)ghi[pr.x + 1], L, g_inv);
+        for (uint32_t q0 = sg.x + (tid % LPC); q0 < end; q0 += LPC * U) {
+          uint2 pr[U];
+#pragma unroll
+          for (uint32_t u = 0; u < U; ++u) pr[u] = q0 + LPC * u < end ? prec[q0 + LPC * u] : make_uint2(0u, 0u);
+#pragma unroll
+          for (uint32_t u = 0; u < U; ++u)
+            if (q0 + LPC * u < end)
+              c += uniq[pr[u].y] * limb_value(glo[pr[u].x + 1], (int32_t)ghi[pr[u].x + 1], L, g_inv);
         }
       }
 #pragma unroll
