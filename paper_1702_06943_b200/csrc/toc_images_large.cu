@@ -378,12 +378,23 @@ __global__ void __launch_bounds__(1024, 1) epoch_large_kernel(LargeEpochArgs a) 
       step = a.lr / (double)n;
       step_n = n;
     }
-    // P1 for this CTA's pairs from the current weights (global; updated by every CTA of the cluster)
-#pragma unroll 4
-    for (uint32_t i = tid; i < nP; i += nth) {
-      p1[i + 1] = pval[i] * __ldcg(a.w + pcol[i]);
-      glo[i + 1] = 0u;
-      ghi[i + 1] = 0u;
+    // P1 for this CTA's pairs from the current weights (global; updated by every CTA of the cluster):
+    // a thread's weight gathers (L2 round trips) are all in flight at once
+    for (uint32_t i0 = tid; i0 < nP; i0 += 4 * nth) {
+      uint32_t col[4];
+      double wv[4];
+#pragma unroll
+      for (uint32_t u = 0; u < 4; ++u) col[u] = i0 + u * nth < nP ? pcol[i0 + u * nth] : 0u;
+#pragma unroll
+      for (uint32_t u = 0; u < 4; ++u) wv[u] = i0 + u * nth < nP ? __ldcg(a.w + col[u]) : 0.0;
+#pragma unroll
+      for (uint32_t u = 0; u < 4; ++u)
+        if (i0 + u * nth < nP) {
+          const uint32_t i = i0 + u * nth;
+          p1[i + 1] = pval[i] * wv[u];
+          glo[i + 1] = 0u;
+          ghi[i + 1] = 0u;
+        }
     }
     uint32_t lg = 0;
     while (lg < 5 && (2u << lg) * (nr ? nr : 1u) <= nth) ++lg;
