@@ -258,6 +258,16 @@ TOC_D double fix_value(uint32_t lo, uint32_t hi, double inv_scale) {
   return (double)v * inv_scale;
 }
 
+// Fixed point is exact in the accumulation but rounds every addend to the quantum 1/scale, which
+// is set by the batch's whole sum |u|.  When n_rows * max|value| quanta could exceed 2^-31 (a
+// row weight far above the others, or a heavy-tailed u), the batch accumulates in fp64 instead
+// (shared-memory atomics; order-dependent only at the last bit): the reference's own
+// accuracy, since the 1e-9 bar applies to every output column.
+constexpr uint32_t kGF64 = 64;  // column_sums mode: G held as doubles in tab
+TOC_D bool fixed_point_too_coarse(uint32_t n_rows, double vmax, double err_per_unit_value) {
+  return (double)n_rows * vmax * err_per_unit_value > 0x1p-31;
+}
+
 // 2^F such that |sum| <= bound stays below 2^62.
 TOC_D double fix_scale(double bound) {
   if (!(bound > 0.0)) return 1.0;
@@ -549,6 +559,18 @@ struct Batch {
     }
   }
 
+  // G in fp64 (the fallback for coarse fixed point, see fixed_point_too_coarse); tab zeroed.
+  template <typename Wt>
+  TOC_D void vecmat_rows_f64(Wt&& weight) {
+    for (uint32_t k = 0; k < passes; ++k) {
+      uint32_t r, lo_, hi_, db, j0, j1;
+      if (!segment(k, r, lo_, hi_, db, j0, j1)) break;
+      const double w = weight(r);
+      if (w == 0.0) continue;
+      walk_flat(r, lo_, hi_, db, j0, j1, [&](uint32_t i) { atomicAdd(tab + i, w); });
+    }
+  }
+
   // G with split words (fix_add_split): lo = tabw[0..nI], hi = tabw[nI+1..2nI+1]; tab zeroed.
   template <typename Wt>
   TOC_D void vecmat_rows_split(Wt&& weight, double g_scale) {
@@ -580,7 +602,8 @@ struct Batch {
     }
   }
 
-  // out[col] = sum over the column's pairs of value * G (split words), in (column, pair) order:
+  // out[col] = sum over the column's pairs of value * G, in (column, pair) order (G: split words,
+  // limbs when L > 0, doubles when L == kGF64):
   // 4 lanes per column, a fixed shuffle tree.  prec / segs from the tree cache (global, in L2):
   // each lane issues its record loads as one batch, so a column costs one L2 round trip.
   template <typename Out>
@@ -611,7 +634,9 @@ struct Batch {
           for (uint32_t k = 0; k < U; ++k)
             if (q0 + G * k < end) {
               const uint32_t i = R::a(pr[k]) + 1;
-              c += uniq[R::b(pr[k])] * (L ? limb_value(lo[i], (int32_t)hi[i], L, g_inv) : fix_value(lo[i], hi[i], g_inv));
+              c += uniq[R::b(pr[k])] * (L == kGF64 ? tab[i]
+                                        : L ? limb_value(lo[i], (int32_t)hi[i], L, g_inv)
+                                            : fix_value(lo[i], hi[i], g_inv));
             }
         }
       }
@@ -655,6 +680,24 @@ struct Batch {
         const uint32_t c = rd.next();
         const long long g = __double2ll_rn(tab[i + 1] * o_scale);
         if (g) fix_add(out + 2 * c, g);
+      }
+    });
+  }
+
+  // out[col_i] += value_i * G[i] with G and out in fp64 (fallback of scatter_columns).
+  TOC_D void scatter_columns_f64(double* out) {
+    if (p0 >= p1) return;
+    with_width(m.w_refs, [&]<int W>() {
+      SeqReader<W> rd;
+      rd.init(blk + m.off_refs, p0);
+      for (uint32_t i = p0; i < p1; ++i) tab[i + 1] *= uniq[rd.next()];
+    });
+    with_width(m.w_cols, [&]<int W>() {
+      SeqReader<W> rd;
+      rd.init(blk + m.off_cols, p0);
+      for (uint32_t i = p0; i < p1; ++i) {
+        const uint32_t c = rd.next();
+        if (tab[i + 1] != 0.0) atomicAdd(out + c, tab[i + 1]);
       }
     });
   }

@@ -46,6 +46,7 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
   const Rec* prec = nullptr;
   const uint2* segs = nullptr;
   uint32_t n_segs = kNoSegs;
+  double vmax_c = 0.0;
   if (cached) {
     // Tree prefix from the device cache: one bulk copy into shared memory (or read in place
     // from global memory when the batch's tables do not fit), overlapped with the value work.
@@ -55,6 +56,7 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
     prec = reinterpret_cast<const Rec*>(tree + CL.off_prec);
     segs = reinterpret_cast<const uint2*>(tree + CL.off_segs);
     n_segs = __ldg(reinterpret_cast<const uint32_t*>(tree + CL.off_info));
+    vmax_c = __ldg(reinterpret_cast<const double*>(tree + CL.off_info + 8));
     B.init(blk, m, tables, in_smem ? nullptr : tree);
     if (a.use_splits && __ldg(reinterpret_cast<const uint32_t*>(tree + CL.off_info) + 1) == B.S)
       B.splits = reinterpret_cast<const uint16_t*>(tree + CL.off_splits);
@@ -67,12 +69,15 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
     for (int32_t c = tid; c < 2 * ncol; c += nth) acc_s[c] = 0u;
   if (!cached) B.load_index(s_warp);
   double g_scale = 1.0, o_scale = 1.0;
+  bool g_f64 = false;  // fixed point too coarse for this batch: accumulate in fp64
   if (do_vm && !cached) {  // a-priori bounds of every partial sum (see fix_add): sum |u| and max |value|
     double su = 0.0;
     for (uint32_t r = tid; r < B.n; r += nth) su += fabs(a.u[row_base + r]);
     su = block_sum(su, s_red);
+    const double vmax = block_max_d(B.vmax, s_red);
     g_scale = fix_scale(su);
-    o_scale = fix_scale(su * block_max_d(B.vmax, s_red));
+    o_scale = fix_scale(su * vmax);
+    g_f64 = fixed_point_too_coarse(B.n, vmax, 1.0 / g_scale + 1.0 / (o_scale * vmax));
   }
   if (cached) {
     if (do_vm) {  // sum |u| as warp partials, read after the barrier below (no extra barrier)
@@ -86,7 +91,9 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
       double su = 0.0;
       for (uint32_t w = 0; w < (nth >> 5); ++w) su += s_red[w];
       g_scale = n_segs != kNoSegs ? limb_scale(su, limb_bits(B.n)) : fix_scale(su);
-      if (n_segs == kNoSegs) o_scale = fix_scale(su * block_max_d(B.vmax, s_red));  // fixed-point scatter only
+      const double vmax = vmax_c;
+      if (n_segs == kNoSegs) o_scale = fix_scale(su * vmax);  // fixed-point scatter only
+      g_f64 = fixed_point_too_coarse(B.n, vmax, 1.0 / g_scale + (n_segs == kNoSegs ? 1.0 / (o_scale * vmax) : 0.0));
     }
     if (do_mv) B.compute_p1_records(irec, kVecSmem ? vec_s : a.v);
     else B.zero_tab();
@@ -112,8 +119,11 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
     }
     if (n_segs != kNoSegs) {
       // split-word G, then out[col] as a fixed-order segmented sum over the column-sorted pairs
-      const uint32_t L = limb_bits(B.n);
-      B.vecmat_rows_limbs([&](uint32_t r) { return a.u[row_base + r]; }, g_scale, L);
+      const uint32_t L = g_f64 ? kGF64 : limb_bits(B.n);
+      if (g_f64)
+        B.vecmat_rows_f64([&](uint32_t r) { return a.u[row_base + r]; });
+      else
+        B.vecmat_rows_limbs([&](uint32_t r) { return a.u[row_base + r]; }, g_scale, L);
       __syncthreads();
       double* o = a.O + b * (int64_t)ncol;
       if (kVecSmem) {
@@ -126,13 +136,23 @@ __device__ __forceinline__ void process_batch(const LinalgArgs& a, int64_t b, co
       }
       return;
     }
+    double* o = a.O + b * (int64_t)ncol;
+    if (g_f64) {  // fp64 G and out (O zeroed by the host when it is not staged in shared memory)
+      B.vecmat_rows_f64([&](uint32_t r) { return a.u[row_base + r]; });
+      __syncthreads();
+      double* os = kVecSmem ? reinterpret_cast<double*>(acc_s) : o;
+      B.scatter_columns_f64(os);
+      __syncthreads();
+      if (kVecSmem)
+        for (int32_t c = tid; c < ncol; c += nth) o[c] = os[c];
+      return;
+    }
     B.vecmat_rows([&](uint32_t r) { return a.u[row_base + r]; }, g_scale);
     __syncthreads();
     uint32_t* out = kVecSmem ? acc_s : reinterpret_cast<uint32_t*>(a.O + b * (int64_t)ncol);
     B.scatter_columns(out, 1.0 / g_scale, o_scale);
     __syncthreads();
     const double o_inv = 1.0 / o_scale;
-    double* o = a.O + b * (int64_t)ncol;
     if (kVecSmem) {
       for (int32_t c = tid; c < ncol; c += nth) o[c] = fix_value(acc_s[2 * c], acc_s[2 * c + 1], o_inv);
     } else {
@@ -219,6 +239,10 @@ __global__ void __launch_bounds__(1024, 1) build_trees_kernel(LinalgArgs a) {
     __syncthreads();
     uint8_t* entry = const_cast<uint8_t*>(a.trees) + a.tree_off[b];
     const CacheLayout CL = cache_layout<kWide>(m);
+    {  // max |value| of the value index (info[2..3]): the sweep's fixed-point accuracy check
+      const double vmax = block_max_d(B.vmax, reinterpret_cast<double*>(smem + 160));
+      if (threadIdx.x == 0) *reinterpret_cast<double*>(entry + CL.off_info + 8) = vmax;
+    }
     {  // pair-balanced lane splits for kSplitThreads-thread CTAs (row offsets fit u16: rows <= n_cols)
       const uint32_t S = seg_lanes(m.n_rows, kSplitThreads);
       const bool ok = m.n_cols <= 65535u;

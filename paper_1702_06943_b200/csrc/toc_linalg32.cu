@@ -98,11 +98,17 @@ __global__ void __launch_bounds__(1024, 1) linalg32_kernel(Linalg32Args a) {
     }
     __syncthreads();  // uniq and the partial sums complete
     double g_scale = 1.0;
+    bool g_f32 = false;  // 32-bit fixed point too coarse for this batch: accumulate G in fp32
     if (do_vm) {
       double su = 0.0;
       for (uint32_t w = 0; w < (nth >> 5); ++w) su += s_red[w];
       g_scale = fix32_scale(su);
+      // rounding errors of +-q/2 per addend (q = 1/g_scale) are independent: a column's error has
+      // standard deviation q * max|value| * sqrt(n/12); keep 6 of them under 2^-15 (the bar is 1e-4)
+      const double vmax = __ldg(reinterpret_cast<const double*>(tree + CL.off_info + 8));
+      g_f32 = 6.0 * vmax * sqrt((double)B.n / 12.0) / g_scale > 0x1p-15;
     }
+    float* gf = reinterpret_cast<float*>(g);
     for (uint32_t i = tid; i < B.nI; i += nth) {
       const Rec r = __ldg(irec + i);
       if (do_mv) p1[i + 1] = (float)(B.uniq[RP::b(r)] * (double)(kVecSmem ? vec_s[RP::a(r)] : a.v[RP::a(r)]));
@@ -117,8 +123,17 @@ __global__ void __launch_bounds__(1024, 1) linalg32_kernel(Linalg32Args a) {
       const bool ok = B.segment(k, r, lo, hi, db, j0, j1);
       float part = 0.0f;
       if (ok) {
-        const uint32_t wr = do_vm ? (uint32_t)__double2int_rn((double)a.u[rb + r] * g_scale) : 0u;
-        if (do_mv && do_vm)
+        const uint32_t wr = do_vm && !g_f32 ? (uint32_t)__double2int_rn((double)a.u[rb + r] * g_scale) : 0u;
+        const float wf = do_vm ? a.u[rb + r] : 0.0f;
+        if (do_vm && g_f32) {
+          if (do_mv)
+            B.walk_flat(r, lo, hi, db, j0, j1, [&](uint32_t i) {
+              part += p1[i];
+              atomicAdd(gf + i, wf);
+            });
+          else if (wf != 0.0f)
+            B.walk_flat(r, lo, hi, db, j0, j1, [&](uint32_t i) { atomicAdd(gf + i, wf); });
+        } else if (do_mv && do_vm)
           B.walk_flat(r, lo, hi, db, j0, j1, [&](uint32_t i) {
             part += p1[i];
             atomicAdd(g + i, wr);
@@ -149,7 +164,8 @@ __global__ void __launch_bounds__(1024, 1) linalg32_kernel(Linalg32Args a) {
         const uint32_t end = __ldg(&segs[s + 1].x);
         for (uint32_t q = sg.x + (tid & 3u); q < end; q += 4) {
           const Rec pr = __ldg(prec + q);
-          c += B.uniq[RP::b(pr)] * ((double)(int32_t)g[RP::a(pr) + 1] * g_inv);
+          const uint32_t i = RP::a(pr) + 1;
+          c += B.uniq[RP::b(pr)] * (g_f32 ? (double)gf[i] : (double)(int32_t)g[i] * g_inv);
         }
       }
       c += __shfl_xor_sync(0xffffffffu, c, 1);

@@ -219,3 +219,66 @@ def test_linalg_pipelined_equals_linalg(oracle):
         arena.linalg_pipelined(kind, v, u, R, O, chunks=chunks)
         assert torch.equal(R, R0.cpu()) and torch.equal(O, O0.cpu())
 
+
+
+def _heavy_u(rng, n, kind):
+    if kind == "outlier":  # one row weight ~1e7 among N(0,1) values (the rest keep |want| ~ 1)
+        u = rng.standard_normal(n)
+        u[int(rng.integers(0, n))] = 3.0e7
+        return u
+    return rng.standard_normal(n) * 10.0 ** rng.uniform(-8, 8, n)  # N(0,1) * 10^U(-8, 8)
+
+
+@pytest.mark.parametrize("u_kind", ["outlier", "heavy_tailed"])
+def test_vecmat_heavy_tailed_u(oracle, tree_mode, u_kind):
+    """v^T.A stays within the bar when the row weights span many orders of magnitude.  The
+    fixed-point accumulation quantises every addend relative to the batch's sum |u|; batches where
+    that could cost more than 2^-31 per output fall back to fp64 accumulation.  Checked in the
+    reference's within_rel form AND pure-relative against each column's own magnitude:
+    |got - want| <= 1e-9 |want| + 1e-13 S_c with S_c = sum_r |u_r a_rc| (the reference's own
+    rounding scale)."""
+    import torch
+
+    from paper_1702_06943_b200 import _native as N
+    from paper_1702_06943_b200 import synth
+
+    dense = [synth.cfg2_batch_dense(11, b) for b in range(3)]
+    encs = [oracle.encode_csr(784, *synth.dense_to_csr(A)) for A in dense]
+    arena = _arena([oracle.serialize(e) for e in encs])
+    if tree_mode == "tree_cache":
+        arena.build_trees()
+    if tree_mode == "levels":
+        assert arena.build_levels()
+    rng = np.random.default_rng(17)
+    u = _heavy_u(rng, 750, u_kind)
+    _, O = arena.linalg(N.TOC_VECMAT, u=torch.from_numpy(u).cuda(), use_levels=tree_mode == "levels")
+    O = O.cpu().numpy()
+    for b, (e, A) in enumerate(zip(encs, dense)):
+        ub = u[250 * b : 250 * (b + 1)]
+        want = oracle.Tree.from_encoding(e).vecmat(ub)
+        scale = np.abs(ub) @ np.abs(A)
+        assert within_rel(O[b], want, REL), max_rel_err(O[b], want)
+        err = np.abs(O[b] - want)
+        assert np.all(err <= 1e-9 * np.abs(want) + 1e-13 * scale), float(np.max(err / (np.abs(want) + scale)))
+
+
+@pytest.mark.parametrize("u_kind", ["outlier", "heavy_tailed"])
+def test_fp32_variant_heavy_tailed_u(oracle, u_kind):
+    """The fp32 variant's 32-bit fixed point falls back to fp32 accumulation when it would be too
+    coarse (within 1e-4 of the fp64 oracle, fused and alone)."""
+    import torch
+
+    from paper_1702_06943_b200 import synth
+
+    dense = [synth.cfg2_batch_dense(12, b) for b in range(3)]
+    encs = [oracle.encode_csr(784, *synth.dense_to_csr(A)) for A in dense]
+    arena = _arena([oracle.serialize(e) for e in encs])
+    rng = np.random.default_rng(18)
+    u = _heavy_u(rng, 750, u_kind).astype(np.float32)
+    v = rng.standard_normal(784).astype(np.float32)
+    for kind in (2, 3):
+        _, O = arena.linalg32(kind, v=torch.from_numpy(v).cuda(), u=torch.from_numpy(u).cuda())
+        for b, e in enumerate(encs):
+            want = oracle.Tree.from_encoding(e).vecmat(u[250 * b : 250 * (b + 1)].astype(np.float64))
+            got = O[b].cpu().numpy().astype(np.float64)
+            assert within_rel(got, want, 1e-4), (kind, max_rel_err(got, want))
