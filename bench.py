@@ -59,6 +59,33 @@ def dist_env():
     return rank, world, local
 
 
+def launch_ranks(args) -> None:
+    """``--gpus N`` without a launcher: re-run this command under torchrun with N ranks (one per
+    GPU, rendezvous on 127.0.0.1) and exit with its status.  Under a launcher, --gpus must equal
+    WORLD_SIZE.  Never runs more ranks than visible GPUs: that fails loudly instead."""
+    if "WORLD_SIZE" in os.environ:
+        world = int(os.environ["WORLD_SIZE"])
+        if args.gpus != world and not FORCE_DP:
+            sys.exit(f"bench.py: --gpus {args.gpus} but the launcher started WORLD_SIZE={world} ranks")
+        return
+    if args.gpus <= 1:
+        return
+    import socket
+    import subprocess
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} needs {args.gpus} GPUs, {have} visible")
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -184,7 +211,80 @@ def cpu_reference(arena_bytes_h, block_off, block_len, v, u, row_base, budget_s:
     rows = sample * ROWS * steps
     desc = (f"oracle port (C, OpenMP {threads} threads) A.v+v^T.A over the first {sample} of {nb} config-2 "
             f"batches x {steps} steps, trees prebuilt")
-    return rows / dt, desc, threads, dt
+    return rows / dt, desc, threads, dt, trees
+
+
+def _rel_err(got, want, pure: bool = False) -> float:
+    """max |got - want| / max(1, |want|) (the reference's within_rel form), or relative to |want|
+    itself with a 1e-12 x max|want| floor for exact zeros (pure)."""
+    got, want = np.asarray(got, np.float64), np.asarray(want, np.float64)
+    if got.size == 0:
+        return 0.0
+    den = np.abs(want) + 1e-12 * np.max(np.abs(want)) + 1e-300 if pure else np.maximum(1.0, np.abs(want))
+    return float(np.max(np.abs(got - want) / den))
+
+
+def sweep_parity(O, trees, row_base, v, u, outputs):
+    """Every batch's A.v and v^T.A from each timed mode against the oracle port's sweep over the
+    same TOC1 blocks (bar 1e-9 for the f64 modes, 1e-4 for the fp32 variant)."""
+    want_r, want_o = O.sweep(trees, row_base, v, u, 2, O.max_threads())
+    out = {"batches": len(trees), "rows": int(len(want_r))}
+    ok = True
+    for name, (r, o) in outputs.items():
+        bar = 1e-4 if name == "fp32_variant" else 1e-9
+        e = {"matvec_max_rel": _rel_err(r, want_r), "vecmat_max_rel": _rel_err(o, want_o), "bar": bar}
+        e["ok"] = e["matvec_max_rel"] <= bar and e["vecmat_max_rel"] <= bar
+        ok &= e["ok"]
+        out[name] = e
+    out["ok"] = bool(ok)
+    return out
+
+
+def glm_parity(rp, c, v, y, m, loss, lr, epochs, batch, risks, weights):
+    """The full-size MGD run against the oracle port's train (reference training.py:336-361) at
+    the same global batch size: risk per epoch and final weights within 1e-6 relative (weights
+    relative to each weight itself, not max(1, |w|))."""
+    from oracle import oracle as O
+
+    O.build()
+    t0 = time.perf_counter()
+    w_ref, risks_ref = O.train_glm(rp, c, v, y, m, loss, batch, lr, epochs, 0)
+    e = {"global_batch": batch, "risk_max_rel": _rel_err(risks, risks_ref, pure=True),
+         "weights_max_rel": _rel_err(weights, w_ref, pure=True), "bar": 1e-6,
+         "nonzero_weights": int(np.count_nonzero(w_ref)), "oracle_seconds": time.perf_counter() - t0}
+    e["ok"] = e["risk_max_rel"] <= 1e-6 and e["weights_max_rel"] <= 1e-6
+    return e
+
+
+def mlp_parity(steps: int = 40):
+    """Config 5 at hidden = 200 over `steps` steps (250 * steps rows, one epoch) against the oracle's
+    restatement (the reference has no such model: its first-layer matmat_right / matmat_left are
+    the pinned parts)."""
+    from oracle import oracle as O
+    from paper_1702_06943_b200 import synth
+    from paper_1702_06943_b200.matrix import LabeledDataset, SparseRowMatrix
+    from paper_1702_06943_b200.mlp import train_mlp
+
+    O.build()
+    rp, c, v, y = synth.cfg5_dataset(250 * steps)
+    ds = LabeledDataset(features=SparseRowMatrix.from_csr(784, rp, c, v, check=False), labels=y)
+    model, trace = train_mlp(ds, hidden=200, classes=10, batch_size=250, learning_rate=0.05, epochs=1, seed=0)
+    (w1, b1, w2, b2), risks = O.train_mlp(rp, c, v, y, 784, 200, 10, 250, 0.05, 1, 0)
+    e = {"steps": steps, "hidden": 200, "risk_max_rel": _rel_err(trace.risks, risks, pure=True),
+         "params_max_rel": max(_rel_err(g, w, pure=True) for g, w in
+                               ((model.w1, w1), (model.b1, b1), (model.w2, w2), (model.b2, b2))), "bar": 1e-6}
+    e["ok"] = e["risk_max_rel"] <= 1e-6 and e["params_max_rel"] <= 1e-6
+    return e
+
+
+def memory_line(toc1: int, cache: int, nnz: int, rows: int, cols: int, what: str) -> dict:
+    """Bytes resident for the run against the uncompressed forms of the same rows (the reference's
+    own accounting, reports.py:38-55: CSR = 12 B per entry + 4 B per row pointer)."""
+    csr = 12 * nnz + 4 * (rows + 1)
+    dense = 8 * rows * cols
+    return {"toc1_bytes": int(toc1), "cache_bytes": int(cache), "cache": what, "csr_bytes": int(csr),
+            "dense_bytes": int(dense), "cache_over_toc1": cache / max(toc1, 1), "cache_over_csr": cache / csr,
+            "cache_over_dense": cache / max(dense, 1), "toc1_over_csr": toc1 / csr}
 
 
 _RESULT = None  # the real stdout: only the result line goes there
@@ -207,6 +307,7 @@ def emit(line: dict) -> None:
 
 def main():
     args = parse()
+    launch_ranks(args)
     claim_stdout()
     rank, world, local = dist_env()
     if args.impl == "reference":
@@ -265,14 +366,17 @@ def main():
     rows_per_step = arena.n_rows_total  # per rank
     value = world * rows_per_step * args.steps / (total_ms / 1e3)
     ms_per_step = total_ms / args.steps
+    outputs = {"headline": (R.cpu().numpy(), O.cpu().numpy())}  # checked against the oracle below
 
     # separate A.v-only and v^T.A-only launches (same protocol) for the per-op rows/s
     nsub = max(args.steps // 4, 10)
     mv_t = time_kernel(torch, lambda: arena.linalg(N.TOC_MATVEC, v=v, R=R), nsub, 3, flush)
     vm_t = time_kernel(torch, lambda: arena.linalg(N.TOC_VECMAT, u=u, O=O), nsub, 3, flush)
+    outputs["separate"] = (R.cpu().numpy(), O.cpu().numpy())
     # block-only mode: the tree is rebuilt from the TOC1 codes inside every launch
     bo_t = time_kernel(torch, lambda: arena.linalg(kind, v=v, u=u, R=R, O=O, use_trees=False, use_levels=False),
                        nsub, 3, flush)
+    outputs["block_only"] = (R.cpu().numpy(), O.cpu().numpy())
     # the level-cache kernel (toc_levels.cu): the alternative cached form, measured beside the headline
     t0 = time.perf_counter()
     levels = arena.build_levels()
@@ -284,36 +388,45 @@ def main():
     R32 = torch.empty_like(R, dtype=torch.float32)
     O32 = torch.empty_like(O, dtype=torch.float32)
     f32_t = time_kernel(torch, lambda: arena.linalg32(kind, v=v32, u=u32, R=R32, O=O32), nsub, 3, flush)
+    outputs["fp32_variant"] = (R32.double().cpu().numpy(), O32.double().cpu().numpy())
 
     peak, peak_src = measured_peaks()
     alg = algorithmic_bytes(arena, kind)
     achieved = alg / (ms_per_step / 1e3) / 1e9
-    traffic = bo_traffic = None
+    traffic = bo_traffic = traffic_src = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath):  # DRAM bytes per launch from the last ncu --set full capture (dated there)
         tj = json.load(open(tpath))
         traffic = tj.get("linalg_kernel_both_tree_cache")  # the mode `value` is measured in
         bo_traffic = tj.get("linalg_kernel_both")
+        traffic_src = {k: tj[k] for k in ("captured", "source", "kernel_build") if k in tj}
 
     # ---- e2e: public API call with host buffers (pinned), copies inside the timed region ----
     e2e = run_e2e(torch, arena, v_h, u_h, args.e2e_steps, world)
     e2e_resident = run_e2e_resident(torch, arena, v_h, u_h, args.e2e_steps, world)
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    parity = {}
+    if rank == 0 and not args.no_cpu_baseline:
         from oracle import oracle as Omod
 
         data_h = arena.data.cpu().numpy()
-        rps, desc, cores, dt = cpu_reference(data_h, arena.block_off, arena.block_len, v_h, u_h,
-                                             arena.row_base, 12.0, 5, 1, Omod)
+        rps, desc, cores, dt, trees = cpu_reference(data_h, arena.block_off, arena.block_len, v_h, u_h,
+                                                    arena.row_base, 12.0, 5, 1, Omod)
         cpu = {"value": rps, "unit": "rows/s", "cores": cores, "kind": "port", "sample": desc}
+        parity["config2_sweep"] = sweep_parity(Omod, trees, arena.row_base, v_h, u_h, outputs)
 
     mgd = {}
     if not args.no_mgd:
         cs = rank == 0 and world == 1 and not args.no_cpu_baseline
-        mgd["config3_logistic"] = run_mgd(3, rank, world, cpu_sample=cs)
-        mgd["config4_hinge"] = run_mgd(4, rank, world, cpu_sample=cs)
+        chk = rank == 0 and not args.no_cpu_baseline
+        mgd["config3_logistic"] = run_mgd(3, rank, world, cpu_sample=cs, parity=parity if chk else None)
+        mgd["config4_hinge"] = run_mgd(4, rank, world, cpu_sample=cs, parity=parity if chk else None)
         mgd["config5_mlp"] = run_mgd(5, rank, world, cpu_sample=cs)
+        if chk and world == 1:
+            parity["config5_40_steps"] = mlp_parity()
+    if parity:
+        parity["all_ok"] = all(p.get("ok", False) for p in parity.values() if isinstance(p, dict))
 
     if rank == 0:
         line = {
@@ -339,6 +452,9 @@ def main():
                 "csr_bytes_per_gpu": int(len(c) * 12 + (len(rp)) * 8),
                 "encode_seconds": t_enc, "generate_seconds": t_gen,
             },
+            "memory": memory_line(arena.block_bytes, arena.tree_bytes, len(c), len(rp) - 1, COLS,
+                                  "tree cache (read by every launch)"),
+            "parity": parity or None,
             "matvec_rows_per_s": world * rows_per_step / (np.mean(mv_t) / 1e3),
             "vecmat_rows_per_s": world * rows_per_step / (np.mean(vm_t) / 1e3),
             "tree_cache": {"used_for_value": True, "bytes_per_gpu": arena.tree_bytes, "build_seconds": t_trees,
@@ -362,7 +478,8 @@ def main():
                              "note": "toc_linalg32: fp32 operands, fixed-point 32-bit v^T.A, one walk for both "
                                      "products; 1e-4 of the fp64 oracle (not the headline: the reference is f64)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": alg, "kernel": "toc::linalg_kernel (A.v + v^T.A)"},
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -376,7 +493,7 @@ def main():
         torch.distributed.destroy_process_group()
 
 
-def run_mgd(cfg: int, rank: int, world: int, cpu_sample: bool):
+def run_mgd(cfg: int, rank: int, world: int, cpu_sample: bool, parity=None):
     """MGD epoch seconds at the config's full size (BASELINE.json configs[2] / [3] / [4]).  N=1: one
     launch per epoch (GLMs: a thread-block cluster over cached step images when they fit shared
     memory, else the relay; config 5: per-step first-layer matmat kernels over the node-record
@@ -421,13 +538,20 @@ def run_mgd(cfg: int, rank: int, world: int, cpu_sample: bool):
         out.update({"steps_per_epoch": int(batches.arena.n_blocks), "epoch_seconds": secs, "risk_per_epoch": risks,
                     "mode": modes[tr.mode], "image_build_seconds": tr.image_build_seconds,
                     "image_bytes": int(tr.image_off[-1]) if tr.mode in ("images", "parts") else 0})
+        out["memory"] = memory_line(batches.arena.block_bytes, out["image_bytes"], len(c), len(y), m,
+                                    f"{tr.mode} step images (read by every epoch)")
+        if parity is not None:
+            parity[f"config{cfg}_{loss}"] = glm_parity(rp, c, v, y, m, loss, lr, epochs, 250, risks, tr.weights())
         if cpu_sample:
             out["cpu_port"] = cpu_mgd_sample(rp, c, v, y, m, loss, lr, batches.arena.n_blocks,
                                              sample_batches=400 if cfg == 3 else 100)
     else:
         from paper_1702_06943_b200.distributed import train_data_parallel
 
-        _, trace = train_data_parallel(ds, TrainConfig(loss, 250, lr, epochs), world, rank)
+        model, trace = train_data_parallel(ds, TrainConfig(loss, 250, lr, epochs), world, rank)
+        if parity is not None:  # the data-parallel run is the reference's at the global batch 250 N
+            parity[f"config{cfg}_{loss}"] = glm_parity(rp, c, v, y, m, loss, lr, epochs, 250 * world, trace.risks,
+                                                       model.weights)
         out.update({"steps_per_epoch": -(-len(y) // (250 * world)), "epoch_seconds": trace.seconds,
                     "risk_per_epoch": trace.risks,
                     "mode": f"data parallel x{world}: " + (
