@@ -479,6 +479,32 @@ int toc_sizeof_sweep_chunk(void); /* 136 */
 int toc_sweep_set_timing(int32_t on);
 int toc_sweep_timeline(int64_t n_chunks, float* out);
 
+/* ---- the uncompressed baselines (matrix.py:164-279), bit for bit --------------------------------
+ * Each output element is accumulated by one thread in the reference's ascending order with
+ * separate IEEE multiplies and adds, so results equal the reference's Python / numpy sums exactly.
+ * Dense operands row-major; CSR row_ptr int64 (n_rows + 1), cols int32; the CSC forms take the same
+ * entries grouped by column with rows ascending (the reference's row-order scatters as ordered
+ * per-column sums).
+ *   toc_dense_matvec      replaces matrix.dense_matvec      (matrix.py:164-173)
+ *   toc_dense_vecmat      replaces matrix.dense_vecmat      (matrix.py:176-186)
+ *   toc_dense_matmat      replaces matrix.dense_matmat      (matrix.py:189-206)
+ *   toc_csr_matvec        replaces matrix.csr_matvec        (matrix.py:225-239)
+ *   toc_csc_vecmat        replaces matrix.csr_vecmat        (matrix.py:242-249)
+ *   toc_csr_matmat_right  replaces matrix.csr_matmat_right  (matrix.py:252-264)
+ *   toc_csc_matmat_left   replaces matrix.csr_matmat_left   (matrix.py:267-279) */
+int toc_dense_matvec(const double* d_A, int64_t n, int64_t m, const double* d_v, double* d_out, void* stream);
+int toc_dense_vecmat(const double* d_v, const double* d_A, int64_t n, int64_t m, double* d_out, void* stream);
+int toc_dense_matmat(const double* d_A, const double* d_M, int64_t n, int64_t k, int64_t p, double* d_out,
+                     void* stream);
+int toc_csr_matvec(const int64_t* d_row_ptr, const int32_t* d_cols, const double* d_vals, int64_t n_rows,
+                   const double* d_v, double* d_out, void* stream);
+int toc_csc_vecmat(const int64_t* d_col_ptr, const int32_t* d_rows, const double* d_vals, int64_t n_cols,
+                   const double* d_v, double* d_out, void* stream);
+int toc_csr_matmat_right(const int64_t* d_row_ptr, const int32_t* d_cols, const double* d_vals, int64_t n_rows,
+                         const double* d_M, int64_t p, double* d_out, void* stream);
+int toc_csc_matmat_left(const int64_t* d_col_ptr, const int32_t* d_rows, const double* d_vals, int64_t n_cols,
+                        const double* d_M, int64_t p, int64_t n_rows, double* d_out, void* stream);
+
 /* ---- version / self-description ---------------------------------------------------------- */
 const char* toc_version(void);
 int toc_device_info(int32_t* sm_count, int32_t* smem_optin, int64_t* l2_bytes);

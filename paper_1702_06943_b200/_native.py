@@ -101,6 +101,13 @@ def lib():
     L.toc_levels_smem.argtypes = [I32, I32, I32, I32, I32]
     L.toc_linalg_levels.argtypes = [P, P, P, P, I64, I32, I32, I32, I32, I32, P, P, P, P, P, P, P]
     L.toc_tree_arrays.argtypes = [P, P, P, I64, ctypes.POINTER(TocPlan), P, P, P, P, P, P, P, P]
+    L.toc_dense_matvec.argtypes = [P, I64, I64, P, P, P]
+    L.toc_dense_vecmat.argtypes = [P, P, I64, I64, P, P]
+    L.toc_dense_matmat.argtypes = [P, P, I64, I64, I64, P, P]
+    L.toc_csr_matvec.argtypes = [P, P, P, I64, P, P, P]
+    L.toc_csc_vecmat.argtypes = [P, P, P, I64, P, P, P]
+    L.toc_csr_matmat_right.argtypes = [P, P, P, I64, P, I64, P, P]
+    L.toc_csc_matmat_left.argtypes = [P, P, P, I64, P, I64, I64, P, P]
     for name in EXPORTS:
         getattr(L, name).restype = getattr(L, name).restype or ctypes.c_int
     if (L.toc_sizeof_meta() != META_DTYPE.itemsize or L.toc_sizeof_plan() != ctypes.sizeof(TocPlan)

@@ -263,3 +263,101 @@ def decode(enc: LogicalEncoding) -> SparseRowMatrix:
 
     rp, c, v = BlockArena.from_bytes([serialize_block(enc)]).decode()
     return SparseRowMatrix.from_csr(enc.n_cols, rp.cpu().numpy(), c.cpu().numpy(), v.cpu().numpy(), check=False)
+
+
+class EncoderDictionary:
+    """The encoder's prefix-tree dictionary (reference codec.py:37-87) as a host data structure.
+
+    Codes 0..n_cols-1 are per-column start markers; every later code extends its parent's pair
+    sequence by one (column, value) pair, looked up by the key (parent, column, value).  Value
+    equality is Python float equality, as in the reference.  The device encoder (toc_encode) keeps
+    its own hash tables in HBM; this class is the reference-API view of the same dictionary
+    (``encode_rows`` rebuilds it from the device's output)."""
+
+    __slots__ = ("n_cols", "_entries", "_child")
+
+    def __init__(self, n_cols: int):
+        if n_cols < 0:
+            raise ValueError(f"n_cols must be non-negative, got {n_cols}")
+        self.n_cols = n_cols
+        # entry = (parent code or NOT_FOUND, column, value, start column)
+        self._entries = [(NOT_FOUND, c, 0.0, c) for c in range(n_cols)]
+        self._child = {}
+
+    def __len__(self) -> int:
+        return len(self._entries)
+
+    def add(self, parent_code: int, column: int, value: float) -> int:
+        """Append the child of parent_code that extends it by (column, value); returns its code."""
+        code = len(self._entries)
+        start = column if parent_code == NOT_FOUND else self._entries[parent_code][3]
+        self._entries.append((parent_code, column, value, start))
+        self._child[(parent_code, column, value)] = code
+        return code
+
+    def get(self, parent_code: int, column: int, value: float) -> int:
+        return self._child.get((parent_code, column, value), NOT_FOUND)
+
+    def sequence(self, code: int) -> list:
+        """The (column, value) pairs code stands for, in row order."""
+        if not 0 <= code < len(self._entries):
+            raise ValueError(f"code {code} out of range")
+        out = []
+        while code >= self.n_cols:
+            parent, column, value, _ = self._entries[code]
+            out.append((column, value))
+            code = parent
+        return out[::-1]
+
+    def start_index(self, code: int) -> int:
+        return self._entries[code][3]
+
+    @property
+    def parent(self) -> list:
+        return [e[0] for e in self._entries]
+
+    @property
+    def column(self) -> list:
+        return [e[1] for e in self._entries]
+
+    @property
+    def value(self) -> list:
+        return [e[2] for e in self._entries]
+
+    @property
+    def start(self) -> list:
+        return [e[3] for e in self._entries]
+
+
+def get_longest_match(dictionary: EncoderDictionary, row, pos: int) -> tuple:
+    """Greedy longest match of row[pos:] (reference codec.py:90-109): (code, end) with the matched
+    pairs row[pos:end]; never crosses the row's end.  The first pair must be a seeded entry."""
+    col, val = row[pos]
+    code = dictionary.get(col, col, val)
+    if code == NOT_FOUND:
+        raise ValueError(f"pair ({col}, {val}) not present in dictionary")
+    end = pos + 1
+    while end < len(row):
+        nxt = dictionary.get(code, row[end][0], row[end][1])
+        if nxt == NOT_FOUND:
+            break
+        code, end = nxt, end + 1
+    return code, end
+
+
+def encode_rows(s: SparseRowMatrix):
+    """The encoder's dictionary and per-row codes in its working numbering, start markers at
+    0..n_cols-1 (reference codec.py:112-139).  The encoding runs on the device (toc_encode);
+    the dictionary is then rebuilt from the decode tree, whose nodes are exactly the encoder's
+    entries in creation order (seeds = the pairs I, then one entry per non-final code in scan
+    order, codec.py:227-251): stored code k is working code k + n_cols - 1."""
+    enc = encode(s)
+    m = s.n_cols
+    shift = m - 1
+    d = EncoderDictionary(m)
+    if enc.pairs:
+        tree = build_prefix_tree(enc)
+        for k in range(1, len(tree)):
+            par = tree.parent[k]
+            d.add(tree.column[k] if par == 0 else par + shift, tree.column[k], tree.value[k])
+    return d, [[c + shift for c in row] for row in enc.rows]

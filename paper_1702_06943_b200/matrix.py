@@ -215,3 +215,134 @@ def dense_to_sparse(a: DenseMatrix) -> SparseRowMatrix:
     np.cumsum(mask.sum(axis=1), out=rp[1:])
     r, c = np.nonzero(mask)
     return SparseRowMatrix.from_csr(a.n_cols, rp, c.astype(np.int32), a.values[r, c], check=False)
+
+
+# ---- the reference's uncompressed baselines (matrix.py:164-279), on the device ------------------
+# Same ascending accumulation order and separate multiply / add as the reference, one device
+# thread per output element (csrc/toc_dense.cu): results equal the reference's bit for bit.  They
+# back train(execution="dense" | "csr") and empirical_risk; the compressed hot path never uses them.
+
+def _device():
+    from . import _native as N
+
+    torch = N.require_cuda()
+    return torch, N
+
+
+def _d(torch, a, dtype):
+    return torch.from_numpy(np.array(a, dtype=dtype, order="C")).cuda()
+
+
+def _inner(left_cols: int, right_rows: int) -> None:
+    if left_cols != right_rows:
+        raise ValueError(f"inner dimensions differ: left has {left_cols} columns, right has {right_rows} rows")
+
+
+def _csc(torch, s: SparseRowMatrix):
+    """The entries of s grouped by column, rows ascending within a column (stable sort by column
+    of the row-major entries): the reference's row-order scatters become ordered column sums."""
+    rows = np.repeat(np.arange(s.n_rows, dtype=np.int32), np.diff(s.row_ptr))
+    order = np.argsort(s.cols, kind="stable")
+    cp = np.zeros(s.n_cols + 1, np.int64)
+    np.cumsum(np.bincount(s.cols, minlength=s.n_cols)[: s.n_cols], out=cp[1:])
+    return _d(torch, cp, np.int64), _d(torch, rows[order], np.int32), _d(torch, s.vals[order], np.float64)
+
+
+def _run(N, rc: int, what: str) -> None:
+    N.check(rc, what)
+
+
+def dense_matvec(a: DenseMatrix, v: Sequence[float]) -> np.ndarray:
+    """A @ v, each row summed left to right (reference matrix.py:164-173)."""
+    vec = as_vector(v, a.n_cols, "vector")
+    if a.n_rows == 0:
+        return np.zeros(0)
+    torch, N = _device()
+    A, x = _d(torch, a.values, np.float64), _d(torch, vec, np.float64)
+    out = torch.empty(a.n_rows, dtype=torch.float64, device="cuda")
+    _run(N, N.lib().toc_dense_matvec(A.data_ptr(), a.n_rows, a.n_cols, x.data_ptr(), out.data_ptr(),
+                                     N.stream_handle()), "toc_dense_matvec")
+    return out.cpu().numpy()
+
+
+def dense_vecmat(v: Sequence[float], a: DenseMatrix) -> np.ndarray:
+    """v @ A, each column summed over rows in ascending order (reference matrix.py:176-186)."""
+    vec = as_vector(v, a.n_rows, "vector")
+    if a.n_cols == 0:
+        return np.zeros(0)
+    torch, N = _device()
+    A, x = _d(torch, a.values, np.float64), _d(torch, vec, np.float64)
+    out = torch.empty(a.n_cols, dtype=torch.float64, device="cuda")
+    _run(N, N.lib().toc_dense_vecmat(x.data_ptr(), A.data_ptr(), a.n_rows, a.n_cols, out.data_ptr(),
+                                     N.stream_handle()), "toc_dense_vecmat")
+    return out.cpu().numpy()
+
+
+def dense_matmat(a: DenseMatrix, m: DenseMatrix) -> DenseMatrix:
+    """A @ M with the inner dimension accumulated in ascending order (reference matrix.py:189-206)."""
+    _inner(a.n_cols, m.n_rows)
+    if a.n_rows * m.n_cols == 0:
+        return DenseMatrix(np.zeros((a.n_rows, m.n_cols)))
+    torch, N = _device()
+    A, M = _d(torch, a.values, np.float64), _d(torch, m.values, np.float64)
+    out = torch.empty((a.n_rows, m.n_cols), dtype=torch.float64, device="cuda")
+    _run(N, N.lib().toc_dense_matmat(A.data_ptr(), M.data_ptr(), a.n_rows, a.n_cols, m.n_cols, out.data_ptr(),
+                                     N.stream_handle()), "toc_dense_matmat")
+    return DenseMatrix(out.cpu().numpy())
+
+
+def csr_matvec(s: SparseRowMatrix, v: Sequence[float]) -> np.ndarray:
+    """S @ v; bit-identical to dense_matvec of the densified matrix (reference matrix.py:225-239)."""
+    vec = as_vector(v, s.n_cols, "vector")
+    if s.n_rows == 0:
+        return np.zeros(0)
+    torch, N = _device()
+    rp, c, x = _d(torch, s.row_ptr, np.int64), _d(torch, s.cols, np.int32), _d(torch, s.vals, np.float64)
+    vd = _d(torch, vec, np.float64)
+    out = torch.empty(s.n_rows, dtype=torch.float64, device="cuda")
+    _run(N, N.lib().toc_csr_matvec(rp.data_ptr(), c.data_ptr(), x.data_ptr(), s.n_rows, vd.data_ptr(),
+                                   out.data_ptr(), N.stream_handle()), "toc_csr_matvec")
+    return out.cpu().numpy()
+
+
+def csr_vecmat(v: Sequence[float], s: SparseRowMatrix) -> np.ndarray:
+    """v @ S, each column accumulated over rows in ascending order (reference matrix.py:242-249)."""
+    vec = as_vector(v, s.n_rows, "vector")
+    if s.n_cols == 0:
+        return np.zeros(0)
+    torch, N = _device()
+    cp, rows, x = _csc(torch, s)
+    vd = _d(torch, vec, np.float64)
+    out = torch.empty(s.n_cols, dtype=torch.float64, device="cuda")
+    _run(N, N.lib().toc_csc_vecmat(cp.data_ptr(), rows.data_ptr(), x.data_ptr(), s.n_cols, vd.data_ptr(),
+                                   out.data_ptr(), N.stream_handle()), "toc_csc_vecmat")
+    return out.cpu().numpy()
+
+
+def csr_matmat_right(s: SparseRowMatrix, m: DenseMatrix) -> DenseMatrix:
+    """S @ M for sparse S and dense M (reference matrix.py:252-264)."""
+    _inner(s.n_cols, m.n_rows)
+    if s.n_rows * m.n_cols == 0:
+        return DenseMatrix(np.zeros((s.n_rows, m.n_cols)))
+    torch, N = _device()
+    rp, c, x = _d(torch, s.row_ptr, np.int64), _d(torch, s.cols, np.int32), _d(torch, s.vals, np.float64)
+    M = _d(torch, m.values, np.float64)
+    out = torch.empty((s.n_rows, m.n_cols), dtype=torch.float64, device="cuda")
+    _run(N, N.lib().toc_csr_matmat_right(rp.data_ptr(), c.data_ptr(), x.data_ptr(), s.n_rows, M.data_ptr(),
+                                         m.n_cols, out.data_ptr(), N.stream_handle()), "toc_csr_matmat_right")
+    return DenseMatrix(out.cpu().numpy())
+
+
+def csr_matmat_left(m: DenseMatrix, s: SparseRowMatrix) -> DenseMatrix:
+    """M @ S for dense M and sparse S (reference matrix.py:267-279)."""
+    _inner(m.n_cols, s.n_rows)
+    if m.n_rows * s.n_cols == 0:
+        return DenseMatrix(np.zeros((m.n_rows, s.n_cols)))
+    torch, N = _device()
+    cp, rows, x = _csc(torch, s)
+    M = _d(torch, m.values, np.float64)
+    out = torch.empty((m.n_rows, s.n_cols), dtype=torch.float64, device="cuda")
+    _run(N, N.lib().toc_csc_matmat_left(cp.data_ptr(), rows.data_ptr(), x.data_ptr(), s.n_cols, M.data_ptr(),
+                                        m.n_rows, s.n_rows, out.data_ptr(), N.stream_handle()),
+         "toc_csc_matmat_left")
+    return DenseMatrix(out.cpu().numpy())

@@ -63,6 +63,27 @@ def unpack_ints(data: bytes, offset: int = 0):
     return [int(v) for v in vals], end
 
 
+def build_value_index(values) -> tuple:
+    """(uniques, refs): the distinct values by bit pattern in first-occurrence order and each
+    value's index into them (reference physical.py:88-101; the device serializer,
+    toc_serialize_sizes, builds the same index for every block)."""
+    bits = np.asarray(values, dtype=np.float64).view(np.uint64)
+    if bits.size == 0:
+        return [], []
+    _, first, inverse = np.unique(bits, return_index=True, return_inverse=True)
+    rank = np.empty(len(first), np.int64)  # unique slot -> position in first-occurrence order
+    rank[np.argsort(first, kind="stable")] = np.arange(len(first))
+    order = np.sort(first)
+    return bits[order].view(np.float64).tolist(), rank[inverse.reshape(-1)].tolist()
+
+
+def value_index_lookup(uniques, ref: int) -> float:
+    """uniques[ref] with the format's range check (reference physical.py:104-107)."""
+    if not 0 <= ref < len(uniques):
+        raise BlockFormatError(f"value ref {ref} out of range for {len(uniques)} unique values")
+    return uniques[ref]
+
+
 def serialize_block(enc: LogicalEncoding) -> bytes:
     """TOC1 bytes of one logical encoding, produced on the device (physical.py:110-130)."""
     torch = N.require_cuda()

@@ -384,3 +384,60 @@ def verify_store(path, dataset) -> int:
                     raise VerificationError(f"batch {ch.first + b}: re-encoding does not reproduce the stored block")
             row += n
     return row
+
+
+# ---- TOCM model container (reference store.py:131-172) ------------------------------------------
+#     magic "TOCM" | version u8 (= 1) | loss code u8 | n_cols u32 | hidden u32 | f64 weights
+# hidden = 0 marks a linear model; a network stores W1 row-major, then W2.  Labels for the loss
+# code: the position of the loss kind in training.LOSS_KINDS.
+
+MODEL_MAGIC = b"TOCM"
+MODEL_VERSION = 1
+_MODEL_HEADER = struct.Struct("<BBII")  # after the magic: 10 bytes
+
+
+def save_model(path, model, loss_kind: str) -> None:
+    from .training import LOSS_KINDS, GlmModel
+
+    if loss_kind not in LOSS_KINDS:
+        raise ValueError(f"loss_kind must be one of {LOSS_KINDS}, got {loss_kind!r}")
+    code = LOSS_KINDS.index(loss_kind)
+    if isinstance(model, GlmModel):
+        head = _MODEL_HEADER.pack(MODEL_VERSION, code, len(model.weights), 0)
+        body = np.ascontiguousarray(model.weights, "<f8").tobytes()
+    else:
+        n_cols, hidden = model.w1.shape
+        head = _MODEL_HEADER.pack(MODEL_VERSION, code, n_cols, hidden)
+        body = (np.ascontiguousarray(model.w1, "<f8").tobytes() + np.ascontiguousarray(model.w2, "<f8").tobytes())
+    Path(path).write_bytes(MODEL_MAGIC + head + body)
+
+
+def load_model(path):
+    """(model, loss_kind) with the reference's checks in its order: magic, header, version, loss
+    code, weight bytes, trailing bytes."""
+    from .training import LOSS_KINDS, GlmModel, NnModel
+
+    data = Path(path).read_bytes()
+    if len(data) < 4:
+        raise TruncatedBlockError("model magic truncated at offset 0")
+    if data[:4] != MODEL_MAGIC:
+        raise BadMagicError(f"bad model magic {data[:4]!r}")
+    if len(data) < 4 + _MODEL_HEADER.size:
+        raise TruncatedBlockError("model header truncated at offset 4")
+    version, code, n_cols, hidden = _MODEL_HEADER.unpack_from(data, 4)
+    if version != MODEL_VERSION:
+        raise UnsupportedVersionError(f"unsupported model version {version}")
+    if code >= len(LOSS_KINDS):
+        raise BlockFormatError(f"unknown loss code {code}")
+    count = n_cols if hidden == 0 else (n_cols + 1) * hidden
+    start = 4 + _MODEL_HEADER.size
+    end = start + 8 * count
+    if end > len(data):
+        raise TruncatedBlockError(f"model weights truncated at offset {start}")
+    if end != len(data):
+        raise BlockFormatError(f"{len(data) - end} trailing bytes after model")
+    flat = np.frombuffer(data, "<f8", count, start).astype(np.float64)
+    if hidden == 0:
+        return GlmModel(weights=flat), LOSS_KINDS[code]
+    return NnModel(w1=flat[: n_cols * hidden].reshape(n_cols, hidden),
+                   w2=flat[n_cols * hidden :].reshape(hidden, 1)), LOSS_KINDS[code]

@@ -14,15 +14,18 @@ from __future__ import annotations
 import ctypes
 import math
 import random
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
 
 from . import _native as N
 from .codec import compress_csr
-from .kernels import OpCounter
-from .matrix import LabeledDataset, SparseRowMatrix, as_vector
-from .mlp import NnModel  # noqa: F401  (reference training.NnModel)
+from . import kernels
+from .kernels import CompressedMatrix, OpCounter
+from .matrix import (DenseMatrix, LabeledDataset, SparseRowMatrix, as_vector, csr_matmat_left, csr_matmat_right,
+                     csr_matvec, csr_vecmat, dense_matmat, dense_matvec, dense_vecmat, sparse_to_dense)
+from .mlp import NnModel, init_nn
 
 LOSS_KINDS = ("squared", "logistic", "hinge", "nn_mse")
 EXECUTION_MODES = ("compressed", "dense", "csr")
@@ -319,10 +322,198 @@ class GlmTrainer:
 
 
 def init_model(config: TrainConfig, n_cols: int):
-    """Zero weights for GLMs (training.py:319-326)."""
+    """Zero weights for GLMs; the network's seeded uniform weights (training.py:319-333)."""
     if config.loss_kind != "nn_mse":
         return GlmModel(weights=np.zeros(n_cols, dtype=np.float64))
-    raise NotImplementedError("nn_mse is trained by paper_1702_06943_b200.mlp (matmat kernels)")
+    w1, w2 = init_nn(n_cols, config.hidden_units, config.seed)
+    return NnModel(w1=w1, w2=w2)
+
+
+# ---- the reference's per-batch API (training.py:103-316) ------------------------------------------
+# Layout-generic building blocks: a Batch carries a CompressedMatrix, DenseMatrix or
+# SparseRowMatrix, and every touch of the features runs on the device -- the TOC kernels for
+# compressed batches, the bit-exact uncompressed baselines (csrc/toc_dense.cu) otherwise.  The loss
+# scalars between the two touches are torch ops on the device.  ``train`` uses these only for the
+# dense / csr layouts; compressed GLM training runs the fused epoch kernels (GlmTrainer).
+
+@dataclass
+class Batch:
+    """One mini-batch: features in some layout plus its labels (training.py:103-111)."""
+
+    features: object
+    labels: np.ndarray
+
+    @property
+    def size(self) -> int:
+        return len(self.labels)
+
+
+@dataclass
+class BatchStore:
+    """Batches in shuffle order, all in one layout (training.py:114-120)."""
+
+    batches: list
+    n_cols: int
+    execution: str
+
+
+def make_batches(dataset: LabeledDataset, batch_size: int, execution: str) -> BatchStore:
+    """Consecutive batches, the last possibly short (training.py:145-167); compressed batches are
+    encoded on the device, each with a fresh dictionary."""
+    if execution not in EXECUTION_MODES:
+        raise ValueError(f"execution must be one of {EXECUTION_MODES}, got {execution!r}")
+    if batch_size < 1:
+        raise ValueError(f"batch_size must be at least 1, got {batch_size}")
+    if dataset.n_rows == 0:
+        raise ValueError("cannot batch an empty dataset")
+    out = []
+    for lo in range(0, dataset.n_rows, batch_size):
+        hi = min(lo + batch_size, dataset.n_rows)
+        piece = dataset.features.take_rows(np.arange(lo, hi))
+        if execution == "compressed":
+            feats = CompressedMatrix.from_sparse(piece)
+        elif execution == "dense":
+            feats = sparse_to_dense(piece)
+        else:
+            feats = piece
+        out.append(Batch(features=feats, labels=dataset.labels[lo:hi]))
+    return BatchStore(batches=out, n_cols=dataset.features.n_cols, execution=execution)
+
+
+def _matvec(features, w, counter):
+    if isinstance(features, CompressedMatrix):
+        return kernels.matvec(features, w, counter)
+    if isinstance(features, DenseMatrix):
+        return dense_matvec(features, w)
+    return csr_matvec(features, w)
+
+
+def _vecmat(v, features, counter):
+    if isinstance(features, CompressedMatrix):
+        return kernels.vecmat(v, features, counter)
+    if isinstance(features, DenseMatrix):
+        return dense_vecmat(v, features)
+    return csr_vecmat(v, features)
+
+
+def _matmat_right(features, m: DenseMatrix, counter):
+    if isinstance(features, CompressedMatrix):
+        return kernels.matmat_right(features, m, counter)
+    if isinstance(features, DenseMatrix):
+        return dense_matmat(features, m)
+    return csr_matmat_right(features, m)
+
+
+def _matmat_left(m: DenseMatrix, features, counter):
+    if isinstance(features, CompressedMatrix):
+        return kernels.matmat_left(m, features, counter)
+    if isinstance(features, DenseMatrix):
+        return dense_matmat(m, features)
+    return csr_matmat_left(m, features)
+
+
+def _cuda(x):
+    torch = N.require_cuda()
+    return torch.from_numpy(np.array(x, dtype=np.float64)).cuda()
+
+
+def _sigmoid(z):
+    """training.py:215-221 on the device: 1/(1+e^-z) for z >= 0, e^z/(1+e^z) below (no overflow)."""
+    torch = N.require_cuda()
+    ez = torch.exp(-torch.abs(z))
+    return torch.where(z >= 0, 1.0 / (1.0 + ez), ez / (1.0 + ez))
+
+
+def _nn_forward(features, model: NnModel, counter):
+    """(h1, yhat) on the device; the first layer through the features' own layout."""
+    h1 = _sigmoid(_cuda(_matmat_right(features, DenseMatrix(model.w1), counter).values))
+    return h1, h1 @ _cuda(model.w2)
+
+
+def empirical_risk(model, dataset: LabeledDataset, loss_kind: str) -> float:
+    """Mean loss over the whole (unshuffled) dataset on its plain sparse features
+    (training.py:231-258): the scores by the device CSR kernel, the losses on the device."""
+    if loss_kind not in LOSS_KINDS:
+        raise ValueError(f"loss_kind must be one of {LOSS_KINDS}, got {loss_kind!r}")
+    if dataset.n_rows == 0:
+        raise ValueError("empirical risk of an empty dataset is undefined")
+    y = _cuda(dataset.labels)
+    if loss_kind == "nn_mse":
+        if not isinstance(model, NnModel):
+            raise TypeError("nn_mse risk needs an NnModel")
+        _, yhat = _nn_forward(dataset.features, model, None)
+        return float((0.5 * (y - yhat[:, 0]) ** 2).mean().item())
+    if not isinstance(model, GlmModel):
+        raise TypeError(f"{loss_kind} risk needs a GlmModel")
+    import torch
+
+    z = _cuda(csr_matvec(dataset.features, model.weights))
+    if loss_kind == "squared":
+        losses = 0.5 * (y - z) ** 2
+    elif loss_kind == "logistic":
+        t = -y * z  # softplus(t) = log(1 + e^t), written overflow-free like training.py:206-212
+        losses = torch.clamp(t, min=0.0) + torch.log1p(torch.exp(-torch.abs(t)))
+    else:
+        losses = torch.clamp(1.0 - y * z, min=0.0)
+    return float(losses.mean().item())
+
+
+def glm_gradient(batch: Batch, model: GlmModel, loss_kind: str, counter: OpCounter | None = None) -> np.ndarray:
+    """Summed gradient of the batch loss (training.py:261-281): one matvec scores the batch, the
+    per-row loss derivative is formed on the device, one vecmat folds it back."""
+    if loss_kind not in LOSS_CODE:
+        raise ValueError(f"glm_gradient cannot handle loss_kind {loss_kind!r}")
+    import torch
+
+    z = _cuda(_matvec(batch.features, model.weights, counter))
+    y = _cuda(batch.labels)
+    if loss_kind == "squared":
+        s = z - y
+    elif loss_kind == "logistic":
+        s = -y / (1.0 + torch.exp(y * z))
+    else:  # hinge subgradient: the flat side of the kink contributes zero
+        s = torch.where(y * z < 1.0, -y, torch.zeros_like(y))
+    return _vecmat(s.cpu().numpy(), batch.features, counter)
+
+
+def nn_gradient(batch: Batch, model: NnModel, counter: OpCounter | None = None):
+    """Summed (dW1, dW2) of the half squared error (training.py:284-293): the first layer's two
+    products through the batch's layout, the rest on the device."""
+    h1, yhat = _nn_forward(batch.features, model, counter)
+    err = yhat - _cuda(batch.labels)[:, None]
+    g_w2 = h1.t() @ err
+    delta = (err @ _cuda(model.w2).t()) * h1 * (1.0 - h1)
+    g_w1_t = _matmat_left(DenseMatrix(delta.t().cpu().numpy()), batch.features, counter)
+    return np.ascontiguousarray(g_w1_t.values.T), g_w2.cpu().numpy()
+
+
+def apply_update(weights: np.ndarray, gradient: np.ndarray, learning_rate: float, batch_size: int) -> np.ndarray:
+    """weights - (learning_rate / batch_size) * gradient (training.py:296-300)."""
+    return weights - (learning_rate / batch_size) * gradient
+
+
+def mgd_step(model, batch: Batch, config: TrainConfig, counter: OpCounter | None = None):
+    """One descent step on one batch, returning a new model (training.py:303-316)."""
+    if config.loss_kind == "nn_mse":
+        g_w1, g_w2 = nn_gradient(batch, model, counter)
+        return NnModel(w1=apply_update(model.w1, g_w1, config.learning_rate, batch.size),
+                       w2=apply_update(model.w2, g_w2, config.learning_rate, batch.size))
+    g = glm_gradient(batch, model, config.loss_kind, counter)
+    return GlmModel(weights=apply_update(model.weights, g, config.learning_rate, batch.size))
+
+
+def _train_batches(dataset: LabeledDataset, config: TrainConfig, counter):
+    """The reference's own epoch loop over a BatchStore (training.py:349-361), step by step."""
+    store = make_batches(shuffle_once(dataset, config.seed), config.batch_size, config.execution)
+    model = init_model(config, dataset.n_cols)
+    trace = LossTrace()
+    for _ in range(config.epochs):
+        t0 = time.perf_counter()
+        for batch in store.batches:
+            model = mgd_step(model, batch, config, counter)
+        trace.seconds.append(time.perf_counter() - t0)
+        trace.risks.append(empirical_risk(model, dataset, config.loss_kind))
+    return model, trace
 
 
 def train(dataset: LabeledDataset, config: TrainConfig, counter: OpCounter | None = None):
@@ -333,12 +524,12 @@ def train(dataset: LabeledDataset, config: TrainConfig, counter: OpCounter | Non
         bad = [float(v) for v in np.unique(dataset.labels) if v not in (-1.0, 1.0)]
         if bad:
             raise ValueError(f"{config.loss_kind} loss needs labels in {{-1, +1}}, found {bad}")
+    if config.execution != "compressed":  # dense / csr layouts: the reference's per-batch loop
+        return _train_batches(dataset, config, counter)
     if config.loss_kind == "nn_mse":
         from .mlp import train_nn
 
         return train_nn(dataset, config, counter)
-    if config.execution != "compressed":
-        raise ValueError(f"execution {config.execution!r}: the device path trains on compressed batches only")
     shuffled = shuffle_once(dataset, config.seed)
     batches = DeviceBatches(shuffled, config.batch_size)
     trainer = GlmTrainer(batches, config.loss_kind, config.learning_rate)
