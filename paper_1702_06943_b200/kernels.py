@@ -159,7 +159,7 @@ def scalar_add(a: CompressedMatrix, c: float) -> DenseMatrix:
 def _dev(x: np.ndarray):
     import torch
 
-    return torch.from_numpy(np.ascontiguousarray(x, np.float64)).cuda()
+    return torch.from_numpy(np.array(x, dtype=np.float64, order="C")).cuda()
 
 
 def matvec(a: CompressedMatrix, v, counter: OpCounter | None = None) -> np.ndarray:
