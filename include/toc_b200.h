@@ -142,30 +142,35 @@ int toc_linalg_trees(const uint8_t* d_arena, const int64_t* d_block_off, const T
                      const double* d_v, double* d_R, const double* d_u, double* d_O, void* d_scratch,
                      const uint8_t* d_trees, const int64_t* d_tree_off, void* stream);
 
-/* ---- level cache (csrc/toc_levels.cu; replaces the per-call tree walk of kernels.py:115-174 with
- * the reference's own node-by-node H recurrence, one tree depth at a time) ------------------
- * toc_levels_build (host): from a HOST copy of the arena, per batch the decode tree's used nodes
- * renumbered breadth first (pairs, then depth 2, 3, ...; siblings contiguous), their (parent, key)
- * records, the code stream in the new ids, each node's occurrence rows and a column-sorted node
- * list -- built once, like the reference's cached CompressedMatrix.tree (kernels.py:68-77).
- * Returns an opaque handle (NULL on bad arguments).  toc_levels_info: total bytes, the largest
- * node count, and the build status (TOC_E_CORRUPT for a block the reference's tree build rejects,
- * codec.py:235-244; TOC_E_ARG when some batch needs ids wider than 16 bits -- keep the tree-cache
- * path then).  toc_levels_copy: the entries back to back into h_out, offsets (n_blocks + 1) into
- * h_off.  toc_levels_smem: dynamic shared memory toc_linalg_levels needs (it returns TOC_E_ARG if
- * that exceeds the device's per-CTA limit).  toc_linalg_levels: A.v / v^T.A as toc_linalg, same
- * operand layout; A.v is bit-identical to the reference's H values, summed per row by a warp;
- * v^T.A uses no atomics (fixed-order fp64 sums, deterministic). */
+/* ---- slot cache (csrc/toc_levels.cu; replaces the per-call tree walk of kernels.py:115-174 with
+ * the reference's node recurrence H[x] = H[par] + P1[key] evaluated only where a node is shared) --
+ * toc_levels_build (host): from a HOST copy of the arena, per batch a self-contained entry: the
+ * value index and row offsets, the pairs numbered by column (slots 1..|I|), the "inner" derived
+ * nodes -- those some used derived node hangs off, closed under parents -- with their (parent,
+ * key) slot records, and the code stream as per-code slot references (the node's own slot, or
+ * parent slot + key slot for a leaf) cut into equal per-thread ranges -- built once, like the
+ * reference's cached CompressedMatrix.tree (kernels.py:68-77).  Returns an opaque handle (NULL on
+ * bad arguments).  toc_levels_info: total bytes, the largest slot count and staged-region size,
+ * and the build status (TOC_E_CORRUPT for a block the reference's tree build rejects,
+ * codec.py:235-244; TOC_E_ARG when some batch needs slots wider than 15 bits or columns wider
+ * than 16 -- keep the tree-cache path then).  toc_levels_copy: the entries back to back into
+ * h_out, offsets (n_blocks + 1) into h_off.  toc_levels_smem: dynamic shared memory
+ * toc_linalg_levels needs (it returns TOC_E_ARG if that exceeds the device's per-CTA limit).
+ * toc_linalg_levels: A.v / v^T.A as toc_linalg, same operand layout (d_row_base: first row of
+ * each batch); reads only the cache entries and the operands; every sum has a fixed order (v^T.A
+ * in exact fixed point, fp64 when that would be too coarse), deterministic.
+ * toc_levels_set_trace: tools only (per-phase clock64 stamps of CTA 0; NULL turns it off). */
 void* toc_levels_build(const uint8_t* h_arena, const int64_t* h_block_off, const TocBlockMeta* h_meta,
                        int64_t n_blocks, int32_t n_threads);
-int toc_levels_info(const void* handle, int64_t* total_bytes, int32_t* max_nodes);
+int toc_levels_info(const void* handle, int64_t* total_bytes, int32_t* max_slots, int32_t* max_stage,
+                    int32_t* max_rows);
 int toc_levels_copy(const void* handle, uint8_t* h_out, int64_t* h_off);
 void toc_levels_free(void* handle);
-int toc_levels_set_prefetch(int mode); /* tuning knob: L2 prefetch of the next entry (0 off, 1 one bulk op, 2 16-KB ops) */
-int64_t toc_levels_smem(int32_t kind, int32_t n_cols, int32_t max_nodes, int32_t max_rows, int32_t max_uniques);
-int toc_linalg_levels(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
-                      const int64_t* d_row_base, int64_t n_blocks, int32_t kind, int32_t n_cols, int32_t max_nodes,
-                      int32_t max_rows, int32_t max_uniques, const double* d_v, double* d_R, const double* d_u,
+int toc_levels_set_prefetch(int mode); /* tuning knob: L2 prefetch of the CTA's next entry (1, default) or none (0) */
+int toc_levels_set_trace(long long* d_trace);
+int64_t toc_levels_smem(int32_t kind, int32_t n_cols, int32_t max_slots, int32_t max_stage, int32_t max_rows);
+int toc_linalg_levels(const int64_t* d_row_base, int64_t n_blocks, int32_t kind, int32_t n_cols, int32_t max_slots,
+                      int32_t max_stage, int32_t max_rows, const double* d_v, double* d_R, const double* d_u,
                       double* d_O, const uint8_t* d_lvl, const int64_t* d_lvl_off, void* stream);
 
 /* ---- compressed matrix-matrix products (reference kernels.py:177-234) ----------------------

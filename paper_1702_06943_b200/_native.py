@@ -93,13 +93,15 @@ def lib():
     L.toc_mlp_step_grad.argtypes = [P, P, P, P, I64, I64, I32, I32, I32, P, P, P, P, P, I32, P, P, I64, P]
     L.toc_levels_build.restype = P
     L.toc_levels_build.argtypes = [P, P, P, I64, I32]
-    L.toc_levels_info.argtypes = [P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int32)]
+    L.toc_levels_info.argtypes = [P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int32),
+                                  ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32)]
     L.toc_levels_copy.argtypes = [P, P, P]
     L.toc_levels_free.restype = None
     L.toc_levels_free.argtypes = [P]
     L.toc_levels_smem.restype = I64
     L.toc_levels_smem.argtypes = [I32, I32, I32, I32, I32]
-    L.toc_linalg_levels.argtypes = [P, P, P, P, I64, I32, I32, I32, I32, I32, P, P, P, P, P, P, P]
+    L.toc_linalg_levels.argtypes = [P, I64, I32, I32, I32, I32, I32, P, P, P, P, P, P, P]
+    L.toc_levels_set_trace.argtypes = [P]
     L.toc_tree_arrays.argtypes = [P, P, P, I64, ctypes.POINTER(TocPlan), P, P, P, P, P, P, P, P]
     L.toc_dense_matvec.argtypes = [P, I64, I64, P, P, P]
     L.toc_dense_vecmat.argtypes = [P, P, I64, I64, P, P]

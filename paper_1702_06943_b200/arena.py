@@ -229,11 +229,13 @@ class BlockArena:
         return self
 
     def build_levels(self, n_threads: int = 0) -> bool:
-        """Build the level cache (toc_levels_build, csrc/toc_levels.cu): per batch the used nodes
-        of C' renumbered breadth first, built once on the host from a copy of the arena -- the
-        counterpart of the reference's cached CompressedMatrix.tree (kernels.py:68-77).  Returns
-        False (and keeps no cache) when some batch needs ids wider than 16 bits or the tables do
-        not fit shared memory; linalg then uses the tree cache / block-only paths."""
+        """Build the slot cache (toc_levels_build, csrc/toc_levels.cu): per batch the pairs in
+        column order, the inner nodes of C' (those a used derived node hangs off) with their
+        (parent, key) records, and the code stream as slot references cut into equal per-thread
+        ranges -- built once on the host from a copy of the arena, the counterpart of the
+        reference's cached CompressedMatrix.tree (kernels.py:68-77).  Returns False (and keeps no
+        cache) when some batch needs slots wider than 16 bits or the tables do not fit shared
+        memory; linalg then uses the tree cache / block-only paths."""
         torch = self.torch
         self.raise_corrupt()
         L = N.lib()
@@ -243,8 +245,9 @@ class BlockArena:
         if not h:
             raise N.NativeError("toc_levels_build failed")
         try:
-            total, max_nodes = ctypes.c_int64(), ctypes.c_int32()
-            rc = L.toc_levels_info(h, ctypes.byref(total), ctypes.byref(max_nodes))
+            total, max_slots, max_stage, max_rows = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+            rc = L.toc_levels_info(h, ctypes.byref(total), ctypes.byref(max_slots), ctypes.byref(max_stage),
+                                   ctypes.byref(max_rows))
             if rc == N.TOC_E_ARG:
                 self.levels = None
                 return False
@@ -255,18 +258,17 @@ class BlockArena:
                     "toc_levels_copy")
         finally:
             L.toc_levels_free(h)
-        max_rows = int(self.meta["n_rows"].max()) if self.n_blocks else 0
-        max_uniq = int(self.meta["n_uniques"].max()) if self.n_blocks else 0
         _, optin, _ = N.device_info()
-        need = L.toc_levels_smem(N.TOC_MATVEC | N.TOC_VECMAT, self.n_cols, max_nodes.value, max_rows, max_uniq)
-        if need > optin:
+        need = L.toc_levels_smem(N.TOC_MATVEC | N.TOC_VECMAT, self.n_cols, max_slots.value, max_stage.value,
+                                 max_rows.value)
+        if need < 0 or need > optin or self.n_cols > 65536:
             self.levels = None
             return False
         dev = self.data.device
         self.levels = torch.from_numpy(buf).to(dev)
         self.levels_off_d = torch.from_numpy(off).to(dev)
         self.levels_bytes = int(total.value)
-        self.levels_dims = (max_nodes.value, max_rows, max_uniq)
+        self.levels_dims = (max_slots.value, max_stage.value, max_rows.value)
         return True
 
     def linalg(self, kind: int, v=None, u=None, R=None, O=None, use_trees: bool = True, use_levels: bool = False):
@@ -286,10 +288,9 @@ class BlockArena:
                 O = torch.empty(max(self.n_blocks * self.n_cols, 1), dtype=torch.float64,
                                 device=dev)[: self.n_blocks * self.n_cols].view(self.n_blocks, self.n_cols)
         if use_levels and getattr(self, "levels", None) is not None:
-            nodes, rows, uniq = self.levels_dims
+            slots, stage, rows = self.levels_dims
             rc = N.lib().toc_linalg_levels(
-                self.data.data_ptr(), self.block_off_d.data_ptr(), self.meta_d.data_ptr(), self.row_base_d.data_ptr(),
-                self.n_blocks, kind, self.n_cols, nodes, rows, uniq,
+                self.row_base_d.data_ptr(), self.n_blocks, kind, self.n_cols, slots, stage, rows,
                 _ptr(v) if kind & N.TOC_MATVEC else None, _ptr(R) if kind & N.TOC_MATVEC else None,
                 _ptr(u) if kind & N.TOC_VECMAT else None, _ptr(O) if kind & N.TOC_VECMAT else None,
                 self.levels.data_ptr(), self.levels_off_d.data_ptr(), N.stream_handle())

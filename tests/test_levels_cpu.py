@@ -1,11 +1,12 @@
-"""CPU checks of the level-cache builder (toc_levels_build, csrc/toc_levels.cu; host code, no GPU).
+"""CPU checks of the slot-cache builder (toc_levels_build, csrc/toc_levels.cu; host code, no GPU).
 
 The entries the library builds are decoded here and evaluated with a numpy restatement of the
-level kernel's arithmetic (P1, top-down H by depth, row sums; occurrence sums, bottom-up sibling
-runs, column-sorted sums), then compared with the oracle's matvec / vecmat (kernels.py:115-174)
-at the 1e-9 bar.  The structural invariants the kernel relies on are asserted too: breadth-first
-ids, parents one level up, siblings contiguous, every code's id valid.  This pins the builder
-before any GPU run; tests/test_gpu_linalg.py runs the kernel itself ("levels" mode).
+slot kernel's arithmetic (P1 for the pair slots, inner-node H by chain, per-thread code ranges
+with head / tail partials; T scatter, push along inner chains, column sums), then compared with
+the oracle's matvec / vecmat (kernels.py:115-174) at the 1e-9 bar.  The structural invariants the
+kernel relies on are asserted too: column-sorted pair slots, inner nodes after their parents,
+keys are pairs, every stream reference a valid slot, column starts monotone.  This pins the
+builder before any GPU run; tests/test_gpu_linalg.py runs the kernel itself ("levels" mode).
 """
 
 from __future__ import annotations
@@ -20,9 +21,8 @@ from conftest import max_rel_err, within_rel
 from helpers import TOY_ROWS, TREE_ROWS, random_alphabet_rows
 
 REL = 1e-9
-HDR = ["nP", "nD", "N", "C", "n_rows", "maxd", "n_multi", "n_segs", "off_lvl", "off_prs", "off_nrec", "off_codes",
-       "off_occ", "off_multi", "off_slnode", "off_kl", "off_wsplit", "off_segs"]
-W = 32  # slices (one per warp)
+HDR = ["nP", "nQ", "S", "C", "K", "T", "n_rows", "n_cols", "nU", "off_uniq", "off_rowoff", "off_prs", "off_inner",
+       "off_colst", "off_stream", "pad"]
 
 
 def host_meta(block: bytes, N):
@@ -69,8 +69,8 @@ def build(blocks):
                            meta.ctypes.data_as(ctypes.c_void_p), len(blocks), 2)
     assert h
     try:
-        total, nodes = ctypes.c_int64(), ctypes.c_int32()
-        rc = L.toc_levels_info(h, ctypes.byref(total), ctypes.byref(nodes))
+        total, slots, stage, rows = ctypes.c_int64(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        rc = L.toc_levels_info(h, ctypes.byref(total), ctypes.byref(slots), ctypes.byref(stage), ctypes.byref(rows))
         if rc:
             return rc, None, None
         buf = np.zeros(total.value + 16, np.uint8)
@@ -81,22 +81,21 @@ def build(blocks):
     return 0, buf, eo
 
 
-def entry(buf, o, occ_w=1):
-    h = dict(zip(HDR, struct.unpack_from("<18I", buf, o)))
+def entry(buf, o):
+    h = dict(zip(HDR, struct.unpack_from("<16I", buf, o)))
+    h["vmax"] = struct.unpack_from("<d", buf, o + 64)[0]
     u32 = lambda off, n: np.frombuffer(buf, np.uint32, n, o + off).astype(np.int64)  # noqa: E731
-    u16 = lambda off, n: np.frombuffer(buf, np.uint16, n, o + off).astype(np.int64)  # noqa: E731
-    nl = h["maxd"] + 1 if h["maxd"] else 1
-    h["lvl"] = u32(h["off_lvl"], nl)
     h["prs"] = u32(h["off_prs"], h["nP"])
-    h["nrec"] = u32(h["off_nrec"], h["nD"])
-    h["codes"] = u16(h["off_codes"], h["C"])
-    h["occ"] = np.frombuffer(buf, np.uint8 if occ_w == 1 else np.uint16, h["N"], o + h["off_occ"]).astype(np.int64)
-    h["occ_w"] = occ_w
-    h["multi"] = u32(h["off_multi"], h["n_multi"])
-    h["slnode"] = u16(h["off_slnode"], (h["maxd"] + 1) * (W + 1)).reshape(-1, W + 1)
-    h["kl"] = u16(h["off_kl"], h["nD"])
-    h["wsplit"] = u16(h["off_wsplit"], 2 * (W + 1)).reshape(2, W + 1)
-    h["segs"] = u32(h["off_segs"], h["n_segs"] + 1)
+    h["inner"] = u32(h["off_inner"], h["nQ"])
+    T, K = h["T"], h["K"]
+    st = u32(h["off_stream"], T * K)
+    # record k of thread t at (k // 4) * 4T + 4t + k % 4  ->  row order j = t*K + k
+    k = np.arange(K)
+    pos = (k[None, :] // 4) * 4 * T + 4 * np.arange(T)[:, None] + (k[None, :] % 4)
+    h["stream"] = st[pos.reshape(-1)][: h["C"]]
+    h["colst"] = np.frombuffer(buf, np.uint16, h["n_cols"] + 1, o + h["off_colst"]).astype(np.int64)
+    h["uniq"] = np.frombuffer(buf, np.float64, h["nU"], o + h["off_uniq"]).copy()
+    h["rowoff"] = u32(h["off_rowoff"], h["n_rows"] + 1)
     return h
 
 
@@ -114,73 +113,103 @@ def value_index(block):
 
 
 def emulate(h, enc, uniq, refs, v, u):
-    """The level kernel's arithmetic in numpy (same operation order per node), walking the
-    per-warp slices the way the kernel does."""
-    nP, N = h["nP"], h["N"]
-    par, key = h["nrec"] & 0xFFFF, h["nrec"] >> 16
-    prs = h["prs"]
-    # pairs renumbered by (column, old id): the same (column, ref) records as the block
+    """The slot kernel's arithmetic in numpy, in the kernel's operation order (per-thread ranges,
+    head / tail partials combined in thread order)."""
+    nP, nQ, S, C, K, T = h["nP"], h["nQ"], h["S"], h["C"], h["K"], h["T"]
+    prs, inner, st = h["prs"], h["inner"], h["stream"]
+    # pairs numbered by (column, old id): the same (column, ref) records as the block
     old = sorted(range(nP), key=lambda i: (enc.I_cols[i], i))
     assert np.array_equal(prs & 0xFFFF, np.asarray(enc.I_cols, np.int64)[old])
-    assert np.array_equal(prs >> 16, refs[old])
-    tab = np.zeros(N)
-    tab[:nP] = uniq[prs >> 16] * v[prs & 0xFFFF]
-    for w in range(W):
-        for d in range(1, h["maxd"]):
-            for x in range(h["slnode"][d, w], h["slnode"][d, w + 1]):
-                tab[x] = tab[key[x - nP]] + tab[par[x - nP]]
+    assert np.array_equal((prs >> 16) & 0x7FFF, refs[old])
+    last = np.r_[(prs[1:] & 0xFFFF) != (prs[:-1] & 0xFFFF), True] if nP else np.zeros(0, bool)
+    assert np.array_equal((prs >> 31) == 1, last), "column-end flags"
+    prs = prs & 0x7FFFFFFF
+    H = np.zeros(S)
+    H[1:nP + 1] = uniq[prs >> 16] * v[prs & 0xFFFF]
+
+    def chain(y):  # slots visited from inner slot y: keys, then the root pair
+        rec = inner[y - nP - 1]
+        out, p = [rec >> 16], rec & 0xFFFF
+        while p > nP:
+            rec = inner[p - nP - 1]
+            out.append(rec >> 16)
+            p = rec & 0xFFFF
+        return out + [p]
+
+    for y in range(nP + 1, S):
+        hv = 0.0
+        for i, x in enumerate(chain(y)):
+            hv = H[x] if i == 0 else hv + H[x]
+        H[y] = hv
     off = np.asarray(enc.offsets, np.int64)
-    R = np.array([tab[h["codes"][off[r]:off[r + 1]]].sum() for r in range(h["n_rows"])])
-    none, multi = (0xFF, 0xFE) if h["occ_w"] == 1 else (0xFFFF, 0xFFFE)
-    S = np.where(h["occ"] < multi, u[np.minimum(h["occ"], len(u) - 1)], 0.0)
-    mrec = h["multi"]
-    ws = h["wsplit"]
-    assert ws[1][0] == 0 and ws[1][-1] == h["n_multi"] and ws[0][0] == 0 and ws[0][-1] == h["nD"]
-    for w in range(W):  # multi records: a warp's range never splits a node
-        a, b = ws[1][w], ws[1][w + 1]
-        if 0 < a < h["n_multi"]:
-            assert (mrec[a] & 0xFFFF) != (mrec[a - 1] & 0xFFFF)
-    mx = mrec & 0xFFFF
-    for x in np.unique(mx):
-        S[x] = u[mrec[mx == x] >> 16].sum()
-    for w in range(W):
-        for d in range(h["maxd"] - 1, 0, -1):
-            for x in range(h["slnode"][d, w], h["slnode"][d, w + 1]):
-                S[par[x - nP]] += S[x]
-    kl = h["kl"]
-    assert np.all(np.diff(key[kl - nP]) >= 0), "kl not sorted by key"
-    for x in kl:
-        S[key[x - nP]] += S[x]
+    n = h["n_rows"]
+    row_of = np.repeat(np.arange(n), np.diff(off))
+    R = np.zeros(n)
+    head, tail = np.zeros(T), np.zeros(T)
+    for t in range(T):
+        s0, e0 = t * K, min(t * K + K, C)
+        if s0 >= e0:
+            continue
+        acc = 0.0
+        for j in range(s0, e0):
+            a_, b_ = st[j] & 0x7FFF, st[j] >> 16
+            acc += H[a_]
+            if b_:
+                acc += H[b_]
+            r = row_of[j]
+            if j + 1 == off[r + 1]:
+                if off[r] >= s0:
+                    R[r] = acc
+                else:
+                    head[t] = acc
+                acc = 0.0
+        tail[t] = acc
+    for r in range(n):
+        lo, hi = off[r], off[r + 1]
+        if lo < hi and lo // K != (hi - 1) // K:
+            t0, t1 = lo // K, (hi - 1) // K
+            x = tail[t0]
+            for t in range(t0 + 1, t1):
+                x += tail[t]
+            R[r] = x + head[t1]
+    # v^T.A: T[slot] += u[r] (the kernel's fixed point is exact; fp64 here), push, columns
+    Tv = np.zeros(S)
+    for j in range(C):
+        a_, b_ = st[j] & 0x7FFF, st[j] >> 16
+        Tv[a_] += u[row_of[j]]
+        if b_:
+            Tv[b_] += u[row_of[j]]
+    own = Tv.copy()
+    for y in range(nP + 1, S):
+        for x in chain(y):
+            Tv[x] += own[y]
     O = np.zeros(enc.n_cols)
-    for s in range(h["n_segs"]):
-        a, b = h["segs"][s] & 0xFFFF, h["segs"][s + 1] & 0xFFFF
-        assert np.all((prs[a:b] & 0xFFFF) == h["segs"][s] >> 16)
-        O[h["segs"][s] >> 16] = np.sum(uniq[prs[a:b] >> 16] * S[a:b])
+    cs = h["colst"]
+    for c in range(enc.n_cols):
+        p = np.arange(cs[c], cs[c + 1])
+        O[c] = np.sum(uniq[prs[p - 1] >> 16] * Tv[p]) if len(p) else 0.0
     return R, O
 
 
 def structure(h, enc):
-    nP, N, lvl = h["nP"], h["N"], h["lvl"]
-    par = h["nrec"] & 0xFFFF
-    assert nP == len(enc.I_cols) and lvl[0] == 0 and lvl[-1] == N
-    if h["maxd"] >= 1:
-        assert lvl[1] == nP
-    assert np.all(np.diff(lvl) >= 0) and np.all(np.diff(h["prs"] & 0xFFFF) >= 0), "pairs not column-sorted"
-    for d in range(1, h["maxd"]):
-        p = par[lvl[d] - nP:lvl[d + 1] - nP]
-        assert np.all((p >= lvl[d - 1]) & (p < lvl[d])), "parent not one level up"
-        assert np.all(np.diff(p) >= 0), "siblings not contiguous"
-    assert np.all(h["codes"] < N) and np.all((h["nrec"] >> 16) < nP)
-    used = np.zeros(N, bool)
-    used[h["codes"]] = True
-    assert used[nP:].all(), "every derived node in the cache is a code"
-    for d in range(1, h["maxd"]):  # the slices tile each level; a slice's parents are in the slice
-        sl = h["slnode"][d]
-        assert sl[0] == lvl[d] and sl[-1] == lvl[d + 1] and np.all(np.diff(sl) >= 0)
-        if d >= 2:
-            for w in range(W):
-                p = par[sl[w] - nP:sl[w + 1] - nP]
-                assert np.all((p >= h["slnode"][d - 1][w]) & (p < h["slnode"][d - 1][w + 1]))
+    nP, nQ, S = h["nP"], h["nQ"], h["S"]
+    assert nP == len(enc.I_cols) and S == 1 + nP + nQ and h["C"] == len(enc.codes)
+    assert h["K"] % 4 == 0 and h["K"] * h["T"] >= h["C"]
+    assert np.all(np.diff(h["prs"] & 0xFFFF) >= 0), "pairs not column-sorted"
+    par, key = h["inner"] & 0xFFFF, h["inner"] >> 16
+    assert np.all((key >= 1) & (key <= nP)), "inner keys must be pairs"
+    assert np.all((par >= 1) & (par < nP + 1 + np.arange(nQ))), "inner parent after its child"
+    a_, b_ = h["stream"] & 0x7FFF, h["stream"] >> 16
+    assert np.all((a_ >= 1) & (a_ < S)) and np.all(b_ <= nP), "stream references"
+    off = np.asarray(enc.offsets, np.int64)
+    ends = np.zeros(h["C"], bool)
+    ends[off[1:][np.diff(off) > 0] - 1] = True
+    assert np.array_equal((h["stream"] & 0x8000) != 0, ends), "row-end flags"
+    cs = h["colst"]
+    assert cs[0] == 1 and cs[-1] == nP + 1 and np.all(np.diff(cs) >= 0)
+    cols = h["prs"] & 0xFFFF
+    for c in np.unique(cols):
+        assert np.all(cols[cs[c] - 1:cs[c + 1] - 1] == c)
 
 
 def cases():
@@ -201,9 +230,11 @@ def test_level_cache_matches_oracle(oracle, name, rows, m):
     assert rc == 0
     rng = np.random.default_rng(3)
     for b, e in enumerate(encs):
-        h = entry(buf, int(eo[b]), 1 if e.n_rows <= 253 else 2)
+        h = entry(buf, int(eo[b]))
         structure(h, e)
         uniq, refs = value_index(blocks[b])
+        assert np.array_equal(h["uniq"], uniq) and h["vmax"] == (np.abs(uniq).max() if len(uniq) else 0.0)
+        assert np.array_equal(h["rowoff"], np.asarray(e.offsets, np.int64))
         v = rng.standard_normal(m)
         u = rng.standard_normal(e.n_rows)
         R, O = emulate(h, e, uniq, refs, v, u)
@@ -225,10 +256,12 @@ def test_level_cache_config2_batches(oracle):
     assert rc == 0
     rng = np.random.default_rng(5)
     for b, e in enumerate(encs):
-        h = entry(buf, int(eo[b]), 1 if e.n_rows <= 253 else 2)
+        h = entry(buf, int(eo[b]))
         structure(h, e)
-        assert h["N"] < 32768 and h["maxd"] <= 16
+        assert h["S"] < 32768 and h["nQ"] < h["C"] // 4
         uniq, refs = value_index(blocks[b])
+        assert np.array_equal(h["uniq"], uniq) and h["vmax"] == (np.abs(uniq).max() if len(uniq) else 0.0)
+        assert np.array_equal(h["rowoff"], np.asarray(e.offsets, np.int64))
         v, u = rng.standard_normal(784), rng.standard_normal(e.n_rows)
         R, O = emulate(h, e, uniq, refs, v, u)
         t = oracle.Tree.from_encoding(e)

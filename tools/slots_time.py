@@ -1,0 +1,62 @@
+"""Device time of the config-2 sweep over 1024 batches: slot cache (toc_levels.cu) per kind
+(1 = A.v, 2 = v^T.A, 3 = both) beside the tree-cache chain walk, L2 flushed between reps, and the
+slot-cache results checked against the chain walk.  usage: python tools/slots_time.py [prefetch]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_1702_06943_b200 import _native as N, codec  # noqa: E402
+
+
+def timeit(fn, flush, reps=30):
+    for _ in range(3):
+        fn()
+    ts = []
+    for _ in range(reps):
+        flush.fill_(1)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ts.sort()
+    return ts[len(ts) // 2] * 1000.0
+
+
+rp, c, v, br = bench.make_shard(0, 1024)
+arena = codec.compress_csr(bench.COLS, rp, c, v, br)
+arena.build_trees()
+import time  # noqa: E402
+
+t0 = time.perf_counter()
+ok = arena.build_levels()
+print("slot cache built", ok, "in", round(time.perf_counter() - t0, 3), "s;", arena.levels_bytes, "bytes; dims",
+      arena.levels_dims, "tree cache", arena.tree_bytes, flush=True)
+if len(sys.argv) > 1:
+    N.check(N.lib().toc_levels_set_prefetch(int(sys.argv[1])), "prefetch")
+vd = torch.randn(bench.COLS, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(1))
+ud = torch.randn(arena.n_rows_total, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(2))
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+Rt, Ot = arena.linalg(3, v=vd, u=ud)
+Rt, Ot = Rt.clone(), Ot.clone()
+Rl, Ol = arena.linalg(3, v=vd, u=ud, use_levels=True)
+torch.cuda.synchronize()
+
+
+def rel(a, b):
+    return ((a - b).abs() / b.abs().clamp_min(1.0)).max().item()
+
+
+print("parity vs chain walk: R", rel(Rl, Rt), "O", rel(Ol, Ot), flush=True)
+R1, _ = arena.linalg(1, v=vd, use_levels=True)
+_, O2 = arena.linalg(2, u=ud, use_levels=True)
+print("parity single kinds: R", rel(R1, Rt), "O", rel(O2, Ot), flush=True)
+out = {}
+for k in (1, 2, 3):
+    out[f"slots{k}"] = timeit(lambda: arena.linalg(k, v=vd, u=ud, use_levels=True), flush)
+out["trees3"] = timeit(lambda: arena.linalg(3, v=vd, u=ud), flush)
+print({k: round(t, 1) for k, t in out.items()}, "us", flush=True)
