@@ -84,7 +84,7 @@ TOC_HD uint32_t align4(uint32_t x) { return (x + 3u) & ~3u; }
 
 // Shared-memory layout (bytes from the dynamic base).
 struct LvlSmem {
-  uint32_t red, v, part, rowcur, stage, tab, total;
+  uint32_t red, v, u, part, rowcur, stage, tab, total;
 };
 
 TOC_HD LvlSmem lvl_smem(int kind, uint32_t n_cols, uint32_t max_slots, uint32_t max_stage, uint32_t max_rows) {
@@ -94,6 +94,8 @@ TOC_HD LvlSmem lvl_smem(int kind, uint32_t n_cols, uint32_t max_slots, uint32_t 
   o += 48 * 8;  // sum |u| partials and total
   L.v = o;
   o += (kind & TOC_MATVEC) ? align16(8u * n_cols) : 0u;
+  L.u = o;
+  o += (kind & TOC_VECMAT) ? align16(8u * max_rows) : 0u;
   L.part = o;
   o += 16u * kLvlThreads;  // head / tail partials (rows, columns)
   L.rowcur = o;
@@ -159,13 +161,32 @@ TOC_D void issue_stage(const LvlArgs& a, int64_t bn, uint8_t* stage, uint64_t* m
   }
 }
 
-// This warp's part of sum |u| over batch bn's rows (v^T.A's fixed-point bound), into s_red[warp].
-TOC_D void su_partial(const LvlArgs& a, int64_t bn, double* s_red) {
-  const uint8_t* ent = a.lvl + a.lvl_off[bn];
-  const uint32_t n = __ldg(reinterpret_cast<const uint32_t*>(ent) + offsetof(LvlHdr, n_rows) / 4);
-  const int64_t rb = a.row_base[bn];
-  double su = 0.0;
-  for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) su += fabs(__ldg(a.u + rb + r));
+// The next batch's u in three steps so no load latency sits on a phase: its row base and row
+// count (at the batch start), the first u per thread (a phase later), then all of them into
+// shared memory (u_s, the scatter's row weights) and this thread's part of sum |u| (v^T.A's
+// fixed-point bound).
+struct UPrefetch {
+  int64_t rb = 0;
+  uint32_t n = 0;
+  double u0 = 0.0;
+  TOC_D void bounds(const LvlArgs& a, int64_t bn) {
+    rb = a.row_base[bn];
+    n = __ldg(reinterpret_cast<const uint32_t*>(a.lvl + a.lvl_off[bn]) + offsetof(LvlHdr, n_rows) / 4);
+  }
+  TOC_D void load(const LvlArgs& a) { u0 = threadIdx.x < n ? __ldg(a.u + rb + threadIdx.x) : 0.0; }
+  TOC_D double stash(const LvlArgs& a, double* u_s) const {
+    double su = fabs(u0);
+    if (threadIdx.x < n) u_s[threadIdx.x] = u0;
+    for (uint32_t r = threadIdx.x + blockDim.x; r < n; r += blockDim.x) {
+      const double x = __ldg(a.u + rb + r);
+      u_s[r] = x;
+      su += fabs(x);
+    }
+    return su;
+  }
+};
+
+TOC_D void su_store(double su, double* s_red) {
   su = warp_sum(su);
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = su;
 }
@@ -186,6 +207,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
   double* s_red = reinterpret_cast<double*>(smem + SL.red);  // [0, 32) partials; [32] this batch's sum |u|
   double* v_s = reinterpret_cast<double*>(smem + SL.v);
+  double* u_s = reinterpret_cast<double*>(smem + SL.u);  // this batch's u (v^T.A row weights)
   double* head_s = reinterpret_cast<double*>(smem + SL.part);
   double* tail_s = head_s + kLvlThreads;
   uint32_t* rowcur_s = reinterpret_cast<uint32_t*>(smem + SL.rowcur);
@@ -204,7 +226,12 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
   __syncthreads();
   if (b < a.n_blocks) {
     if (tid == 0) issue_stage(a, b, stage, mbar);
-    if (VM) su_partial(a, b, s_red);
+    if (VM) {
+      UPrefetch p0;
+      p0.bounds(a, b);
+      p0.load(a);
+      su_store(p0.stash(a, u_s), s_red);
+    }
   }
   __syncthreads();
   if (VM && warp == 0) {
@@ -233,6 +260,8 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
     uint4 w0 = active ? __ldg(stream) : z4, w1 = active && K > 4 ? __ldg(stream + nth) : z4;
     const uint32_t r0 = active ? row_of(rowoff_s, n, tid * K) : 0u;  // this thread's first row
     const bool here0 = active && rowoff_s[r0] == tid * K;
+    UPrefetch pre;  // the next batch's u (v^T.A)
+    if (VM && has_next) pre.bounds(a, bn);
 
     if (VM) {
       const uint32_t S4 = align4(h.S);
@@ -247,7 +276,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
         uint32_t r = r0;
         if (!f64) {
           auto weight = [&](uint32_t row, uint32_t& xl, int32_t& xh) {
-            const long long w = __double2ll_rn(__ldg(a.u + rb + row) * g_scale);
+            const long long w = __double2ll_rn(u_s[row] * g_scale);
             xh = (int32_t)(w >> L);
             xl = (uint32_t)(w - ((long long)xh << L));
           };
@@ -267,7 +296,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
             }
           });
         } else {
-          double wu = __ldg(a.u + rb + r);
+          double wu = u_s[r];
           walk_stream(stream, nth, K, w0, w1, [&](const uint4& w) {
             const uint32_t rec[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
@@ -278,7 +307,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
               }
               if (rec[i] & kRowEnd) {
                 r = next_row(rowoff_s, n, r);
-                if (r < n) wu = __ldg(a.u + rb + r);
+                if (r < n) wu = u_s[r];
               }
             }
           });
@@ -323,6 +352,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
       }
       __syncthreads();
       TOC_LVL_STAMP(2);
+      pre.load(a);
       // column partials: thread t sums value * T over pair slots [1 + tM, 1 + tM + M) (M odd, so
       // the lanes' slot reads are conflict-free), column by column; a column ending inside the
       // range is complete (started here) or the range's head partial
@@ -364,7 +394,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
           }
         }
       }
-      if (has_next) su_partial(a, bn, s_red);
+      su_store(pre.stash(a, u_s), s_red);
     }
     if (MV) {
       // P1 for the pair slots (Algorithm 5's H at depth 1); the row offsets into a private copy
@@ -483,6 +513,59 @@ struct LvlCache {
   int32_t status = TOC_OK;
 };
 
+// Bank-aware placement of the records (the kernel's row sums and T scatter are bound by shared-
+// memory wavefronts, and a warp-wide gather or atomic costs one wavefront per distinct word in the
+// most loaded bank).  Position j = t*K + k is thread t's k-th record; a row's positions keep their
+// row (so the per-thread row logic and the row-end flags are unchanged) but which of the row's
+// codes sits at which of its positions is free (the row sum does not depend on it), and a
+// two-slot record may be stored (key, par) instead of (par, key).  Warp by warp, step by step,
+// each lane (fewest choices first) takes from its row's remaining codes the one whose slots hit
+// the least used banks (slot mod 32) among the lanes placed so far in this step.
+void schedule_banks(std::vector<uint32_t>& rec, const std::vector<uint32_t>& rowid, const std::vector<uint32_t>& off,
+                    uint32_t n, uint32_t C, uint32_t K, uint32_t T) {
+  std::vector<std::vector<uint32_t>> pool(n);
+  for (uint32_t r = 0; r < n; ++r) pool[r].assign(rec.begin() + off[r], rec.begin() + off[r + 1]);
+  uint32_t lanes[32];
+  for (uint32_t w = 0; w < T / 32; ++w) {
+    if ((uint64_t)w * 32 * K >= C) break;
+    for (uint32_t k = 0; k < K; ++k) {
+      uint32_t na = 0;
+      for (uint32_t l = 0; l < 32; ++l) {
+        const uint64_t j = (uint64_t)(w * 32 + l) * K + k;
+        if (j < C) lanes[na++] = l;
+      }
+      if (!na) continue;
+      std::stable_sort(lanes, lanes + na, [&](uint32_t x, uint32_t y) {
+        return pool[rowid[(w * 32 + x) * K + k]].size() < pool[rowid[(w * 32 + y) * K + k]].size();
+      });
+      uint8_t ca[32] = {0}, cb[32] = {0};
+      for (uint32_t q = 0; q < na; ++q) {
+        const uint32_t j = (w * 32 + lanes[q]) * K + k;
+        std::vector<uint32_t>& P = pool[rowid[j]];
+        size_t best = 0;
+        bool swap = false;
+        uint32_t bc = ~0u;
+        for (size_t i = 0; i < P.size() && bc; ++i) {
+          const uint32_t a = P[i] & 0xffffu, b = P[i] >> 16;
+          const uint32_t c = 3u * ca[a & 31] + (b ? 2u * cb[b & 31] : 0u);
+          if (c < bc) bc = c, best = i, swap = false;
+          if (b) {
+            const uint32_t c2 = 3u * ca[b & 31] + 2u * cb[a & 31];
+            if (c2 < bc) bc = c2, best = i, swap = true;
+          }
+        }
+        uint32_t x = P[best];
+        P[best] = P.back();
+        P.pop_back();
+        if (swap) x = (x >> 16) | ((x & 0xffffu) << 16);
+        ++ca[(x & 0xffffu) & 31];
+        if (x >> 16) ++cb[(x >> 16) & 31];
+        rec[j] = x;
+      }
+    }
+  }
+}
+
 // One batch's entry.  Fails with TOC_E_CORRUPT for blocks the reference's tree build rejects, and
 // TOC_E_ARG when slots or columns do not fit the 15/16-bit fields (the caller then keeps the
 // chain-walk path).
@@ -582,15 +665,22 @@ int build_entry(const uint8_t* blk, const TocBlockMeta& m, LvlEntry& out) {
     while (k < nI && pcol[order[k]] < c) ++k;
     cs[c] = (uint16_t)(k + 1);
   }
-  uint32_t* st = reinterpret_cast<uint32_t*>(e + hd.off_stream);
+  // records in row order (row-end flag on each row's last code)
+  std::vector<uint32_t> rec(C), rowid(C);
   for (uint32_t r = 0; r < n; ++r)
     for (uint32_t j = off[r]; j < off[r + 1]; ++j) {
       const uint32_t x = code[j];
-      uint32_t rec = (x <= nI || inner[x]) ? slot[x] : (slot[par[x]] | (slot[key[x]] << 16));
-      if (j + 1 == off[r + 1]) rec |= toc::kRowEnd;  // last code of its row
-      const uint32_t t = j / K, k = j % K;
-      st[(uint64_t)(k >> 2) * 4 * T + 4 * t + (k & 3u)] = rec;
+      rec[j] = (x <= nI || inner[x]) ? slot[x] : (slot[par[x]] | (slot[key[x]] << 16));
+      rowid[j] = r;
     }
+  schedule_banks(rec, rowid, off, n, C, K, T);
+  uint32_t* st = reinterpret_cast<uint32_t*>(e + hd.off_stream);
+  for (uint32_t j = 0; j < C; ++j) {
+    const uint32_t r = rowid[j];
+    const uint32_t flag = (j + 1 == off[r + 1]) ? toc::kRowEnd : 0u;  // last code of its row
+    const uint32_t t = j / K, k = j % K;
+    st[(uint64_t)(k >> 2) * 4 * T + 4 * t + (k & 3u)] = rec[j] | flag;
+  }
   out.S = S;
   out.stage = hd.off_stream;  // header included
   out.n_rows = n;

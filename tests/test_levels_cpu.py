@@ -200,7 +200,7 @@ def structure(h, enc):
     assert np.all((key >= 1) & (key <= nP)), "inner keys must be pairs"
     assert np.all((par >= 1) & (par < nP + 1 + np.arange(nQ))), "inner parent after its child"
     a_, b_ = h["stream"] & 0x7FFF, h["stream"] >> 16
-    assert np.all((a_ >= 1) & (a_ < S)) and np.all(b_ <= nP), "stream references"
+    assert np.all((a_ >= 1) & (a_ < S)) and np.all(b_ < S), "stream references"
     off = np.asarray(enc.offsets, np.int64)
     ends = np.zeros(h["C"], bool)
     ends[off[1:][np.diff(off) > 0] - 1] = True
