@@ -62,24 +62,6 @@ struct LvlHdr {
 static_assert(sizeof(LvlHdr) == 72, "slot cache header");
 constexpr uint32_t kHdrBytes = 80;
 
-struct LvlArgs {
-  const int64_t* row_base;
-  int64_t n_blocks;
-  int32_t kind, n_cols, max_slots, max_stage, max_rows;
-  const uint8_t* lvl;
-  const int64_t* lvl_off;
-  const double* v;
-  double* R;
-  const double* u;
-  double* O;
-};
-
-// L2 prefetch knob: 1 (default) = the CTA's next entry at the start of the current batch; 0 = none.
-__constant__ int g_prefetch_mode = 1;
-// Phase trace (tools/slots_trace.py): when set, CTA 0 records clock64 after each phase of its
-// first 64 batches, 10 stamps per batch.
-__constant__ long long* g_trace = nullptr;
-
 TOC_HD uint32_t align4(uint32_t x) { return (x + 3u) & ~3u; }
 
 // Shared-memory layout (bytes from the dynamic base).
@@ -108,8 +90,29 @@ TOC_HD LvlSmem lvl_smem(int kind, uint32_t n_cols, uint32_t max_slots, uint32_t 
   return L;
 }
 
-// Stream records: slot a (bits 0-14) | row-end flag (bit 15) | slot b (bits 16-30; 0 = none).
-constexpr uint32_t kSlotMask = 0x7fffu, kRowEnd = 0x8000u;
+struct LvlArgs {
+  LvlSmem sl;  // shared-memory layout (host-computed: the offsets stay kernel parameters, not registers)
+  const int64_t* row_base;
+  int64_t n_blocks;
+  int32_t kind, n_cols, max_slots, max_stage, max_rows;
+  const uint8_t* lvl;
+  const int64_t* lvl_off;
+  const double* v;
+  double* R;
+  const double* u;
+  double* O;
+};
+
+// L2 prefetch knob: 1 (default) = the CTA's next entry at the start of the current batch; 0 = none.
+__constant__ int g_prefetch_mode = 1;
+// Phase trace (tools/slots_trace.py): when set, CTA 0 records clock64 after each phase of its
+// first 64 batches, 10 stamps per batch.
+__constant__ long long* g_trace = nullptr;
+
+
+// Stream records: slot a (bits 0-14) | row-end flag (bit 15) | slot b (bits 16-30; 0 = none) |
+// empty rows follow this row's end (bit 31: the next row is found by a search, else it is r + 1).
+constexpr uint32_t kSlotMask = 0x7fffu, kRowEnd = 0x8000u, kSkip = 0x80000000u, kSlotB = 0x7fffu;
 
 // The row containing code s (the largest r with rowoff[r] <= s; rowoff[r + 1] > s then).
 TOC_D uint32_t row_of(const uint32_t* rowoff_s, uint32_t n, uint32_t s) {
@@ -122,10 +125,12 @@ TOC_D uint32_t row_of(const uint32_t* rowoff_s, uint32_t n, uint32_t s) {
   return lo;
 }
 
-// The next non-empty row after row r ends (n past the last).
-TOC_D uint32_t next_row(const uint32_t* rowoff_s, uint32_t n, uint32_t r) {
+// The next non-empty row after row r ends (n past the last); rec's skip flag says whether empty
+// rows follow.
+TOC_D uint32_t next_row(const uint32_t* rowoff_s, uint32_t n, uint32_t r, uint32_t rec) {
   ++r;
-  while (r < n && rowoff_s[r + 1] == rowoff_s[r]) ++r;
+  if (rec & kSkip)
+    while (r < n && rowoff_s[r + 1] == rowoff_s[r]) ++r;
   return r;
 }
 
@@ -203,7 +208,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t tid = threadIdx.x, nth = blockDim.x, warp = tid >> 5, nwarps = nth >> 5;
   const uint32_t ncol = (uint32_t)a.n_cols;
-  const LvlSmem SL = lvl_smem(kKind, ncol, a.max_slots, a.max_stage, a.max_rows);
+  const LvlSmem& SL = a.sl;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
   double* s_red = reinterpret_cast<double*>(smem + SL.red);  // [0, 32) partials; [32] this batch's sum |u|
   double* v_s = reinterpret_cast<double*>(smem + SL.v);
@@ -288,9 +293,9 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
 #pragma unroll
             for (uint32_t i = 0; i < 4; ++i) {
               limb_add(lo_s, hi_s, rec[i] & kSlotMask, xl, xh);
-              if (rec[i] >> 16) limb_add(lo_s, hi_s, rec[i] >> 16, xl, xh);
+              if ((rec[i] >> 16) & kSlotB) limb_add(lo_s, hi_s, (rec[i] >> 16) & kSlotB, xl, xh);
               if (rec[i] & kRowEnd) {
-                r = next_row(rowoff_s, n, r);
+                r = next_row(rowoff_s, n, r, rec[i]);
                 if (r < n) weight(r, xl, xh);
               }
             }
@@ -303,10 +308,10 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
             for (uint32_t i = 0; i < 4; ++i) {
               if (wu != 0.0) {
                 atomicAdd(Tf + (rec[i] & kSlotMask), wu);
-                if (rec[i] >> 16) atomicAdd(Tf + (rec[i] >> 16), wu);
+                if ((rec[i] >> 16) & kSlotB) atomicAdd(Tf + ((rec[i] >> 16) & kSlotB), wu);
               }
               if (rec[i] & kRowEnd) {
-                r = next_row(rowoff_s, n, r);
+                r = next_row(rowoff_s, n, r, rec[i]);
                 if (r < n) wu = u_s[r];
               }
             }
@@ -437,7 +442,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
 #pragma unroll
           for (uint32_t i = 0; i < 4; ++i) {
             ha[i] = H[rec[i] & kSlotMask];
-            hb[i] = (rec[i] >> 16) ? H[rec[i] >> 16] : 0.0;
+            hb[i] = ((rec[i] >> 16) & kSlotB) ? H[(rec[i] >> 16) & kSlotB] : 0.0;
           }
 #pragma unroll
           for (uint32_t i = 0; i < 4; ++i) {
@@ -448,7 +453,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
               else head_s[tid] = acc;
               acc = 0.0;
               here = true;
-              r = next_row(rowcur_s, n, r);
+              r = next_row(rowcur_s, n, r, rec[i]);
             }
           }
         });
@@ -677,7 +682,11 @@ int build_entry(const uint8_t* blk, const TocBlockMeta& m, LvlEntry& out) {
   uint32_t* st = reinterpret_cast<uint32_t*>(e + hd.off_stream);
   for (uint32_t j = 0; j < C; ++j) {
     const uint32_t r = rowid[j];
-    const uint32_t flag = (j + 1 == off[r + 1]) ? toc::kRowEnd : 0u;  // last code of its row
+    uint32_t flag = 0;
+    if (j + 1 == off[r + 1]) {  // last code of its row; empty rows after it?
+      flag = toc::kRowEnd;
+      if (r + 1 < n && off[r + 2] == off[r + 1]) flag |= toc::kSkip;
+    }
     const uint32_t t = j / K, k = j % K;
     st[(uint64_t)(k >> 2) * 4 * T + 4 * t + (k & 3u)] = rec[j] | flag;
   }
@@ -774,8 +783,8 @@ extern "C" int toc_linalg_levels(const int64_t* d_row_base, int64_t n_blocks, in
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const int64_t smem = toc_levels_smem(kind, n_cols, max_slots, max_stage, max_rows);
   if (smem < 0 || smem > optin) return TOC_E_ARG;
-  toc::LvlArgs a{d_row_base, n_blocks, kind,    n_cols, max_slots, max_stage,
-                 max_rows,   d_lvl,    d_lvl_off, d_v, d_R,       d_u,       d_O};
+  toc::LvlArgs a{toc::lvl_smem(kind, (uint32_t)n_cols, (uint32_t)max_slots, (uint32_t)max_stage, (uint32_t)max_rows),
+                 d_row_base, n_blocks, kind, n_cols, max_slots, max_stage, max_rows, d_lvl, d_lvl_off, d_v, d_R, d_u, d_O};
   void* fn = kind == TOC_MATVEC   ? (void*)toc::levels_kernel<TOC_MATVEC>
              : kind == TOC_VECMAT ? (void*)toc::levels_kernel<TOC_VECMAT>
                                   : (void*)toc::levels_kernel<TOC_MATVEC | TOC_VECMAT>;

@@ -152,7 +152,7 @@ def emulate(h, enc, uniq, refs, v, u):
             continue
         acc = 0.0
         for j in range(s0, e0):
-            a_, b_ = st[j] & 0x7FFF, st[j] >> 16
+            a_, b_ = st[j] & 0x7FFF, (st[j] >> 16) & 0x7FFF
             acc += H[a_]
             if b_:
                 acc += H[b_]
@@ -175,7 +175,7 @@ def emulate(h, enc, uniq, refs, v, u):
     # v^T.A: T[slot] += u[r] (the kernel's fixed point is exact; fp64 here), push, columns
     Tv = np.zeros(S)
     for j in range(C):
-        a_, b_ = st[j] & 0x7FFF, st[j] >> 16
+        a_, b_ = st[j] & 0x7FFF, (st[j] >> 16) & 0x7FFF
         Tv[a_] += u[row_of[j]]
         if b_:
             Tv[b_] += u[row_of[j]]
@@ -199,7 +199,7 @@ def structure(h, enc):
     par, key = h["inner"] & 0xFFFF, h["inner"] >> 16
     assert np.all((key >= 1) & (key <= nP)), "inner keys must be pairs"
     assert np.all((par >= 1) & (par < nP + 1 + np.arange(nQ))), "inner parent after its child"
-    a_, b_ = h["stream"] & 0x7FFF, h["stream"] >> 16
+    a_, b_ = h["stream"] & 0x7FFF, (h["stream"] >> 16) & 0x7FFF
     assert np.all((a_ >= 1) & (a_ < S)) and np.all(b_ < S), "stream references"
     off = np.asarray(enc.offsets, np.int64)
     ends = np.zeros(h["C"], bool)
