@@ -301,6 +301,17 @@ def claim_stdout():
     return _RESULT
 
 
+def smem_pipe_line(wavefronts, ms_per_step: float, clocks):
+    """The kernel's shared-memory pipe fraction: shared wavefronts per launch (ncu, profiles/traffic.json)
+    over what the 148 SMs' pipes (one 128-byte wavefront per SM per cycle) serve in the measured step
+    at the sampled SM clock.  None without a capture."""
+    if not wavefronts or not clocks or not clocks.get("sm_mhz"):
+        return None
+    cycles = ms_per_step / 1e3 * clocks["sm_mhz"] * 1e6
+    return {"wavefronts_per_launch": wavefronts, "sm_cycles_per_launch": cycles, "sms": 148,
+            "frac": wavefronts / (148 * cycles), "unit": "wavefronts per SM-cycle (peak 1)"}
+
+
 def emit(line: dict) -> None:
     print(json.dumps(line), file=claim_stdout(), flush=True)
 
@@ -341,15 +352,20 @@ def main():
     O = torch.empty((arena.n_blocks, COLS), dtype=torch.float64, device="cuda")
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
-    # device tree cache (built once, outside the timed region -- like the reference's own
-    # bench-kernels, which builds trees before timing, cli.py:316-317)
+    # per-batch caches (built once, outside the timed region -- like the reference's own
+    # bench-kernels, which builds trees before timing, cli.py:316-317): the slot cache the headline
+    # launch reads (toc_levels.cu) and the tree cache of the chain-walk kernel (reported beside it)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     arena.build_trees()
     torch.cuda.synchronize()
     t_trees = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    slots = arena.build_levels()
+    torch.cuda.synchronize()
+    t_slots = time.perf_counter() - t0
 
-    def step():
+    def step():  # the slot cache when it fits (config 2: always), else the tree cache
         arena.linalg(kind, v=v, u=u, R=R, O=O)
 
     sampler = ClockSampler(local)
@@ -377,12 +393,9 @@ def main():
     bo_t = time_kernel(torch, lambda: arena.linalg(kind, v=v, u=u, R=R, O=O, use_trees=False, use_levels=False),
                        nsub, 3, flush)
     outputs["block_only"] = (R.cpu().numpy(), O.cpu().numpy())
-    # the level-cache kernel (toc_levels.cu): the alternative cached form, measured beside the headline
-    t0 = time.perf_counter()
-    levels = arena.build_levels()
-    t_levels = time.perf_counter() - t0
-    lv_t = (time_kernel(torch, lambda: arena.linalg(kind, v=v, u=u, R=R, O=O, use_levels=True), nsub, 3, flush)
-            if levels else None)
+    # the chain-walk kernel over the tree cache (toc_linalg.cu), measured beside the headline
+    tc_t = time_kernel(torch, lambda: arena.linalg(kind, v=v, u=u, R=R, O=O, use_levels=False), nsub, 3, flush)
+    outputs["tree_cache"] = (R.cpu().numpy(), O.cpu().numpy())
     # the fp32 variant (north_star: 1e-4 bar): same batches, fused single walk for both products
     v32, u32 = v.float(), u.float()
     R32 = torch.empty_like(R, dtype=torch.float32)
@@ -393,13 +406,14 @@ def main():
     peak, peak_src = measured_peaks()
     alg = algorithmic_bytes(arena, kind)
     achieved = alg / (ms_per_step / 1e3) / 1e9
-    traffic = bo_traffic = traffic_src = None
+    traffic = bo_traffic = traffic_src = smem_wf = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):  # DRAM bytes per launch from the last ncu --set full capture (dated there)
         tj = json.load(open(tpath))
-        traffic = tj.get("linalg_kernel_both_tree_cache")  # the mode `value` is measured in
+        traffic = tj.get("levels_kernel_both")  # the mode `value` is measured in (slot cache)
         bo_traffic = tj.get("linalg_kernel_both")
         traffic_src = {k: tj[k] for k in ("captured", "source", "kernel_build") if k in tj}
+        smem_wf = tj.get("levels_kernel_both_smem_wavefronts")
 
     # ---- e2e: public API call with host buffers (pinned), copies inside the timed region ----
     e2e = run_e2e(torch, arena, v_h, u_h, args.e2e_steps, world)
@@ -452,22 +466,25 @@ def main():
                 "csr_bytes_per_gpu": int(len(c) * 12 + (len(rp)) * 8),
                 "encode_seconds": t_enc, "generate_seconds": t_gen,
             },
-            "memory": memory_line(arena.block_bytes, arena.tree_bytes, len(c), len(rp) - 1, COLS,
-                                  "tree cache (read by every launch)"),
+            "memory": memory_line(arena.block_bytes, arena.levels_bytes if slots else arena.tree_bytes, len(c),
+                                  len(rp) - 1, COLS, "slot cache (read by every launch)" if slots
+                                  else "tree cache (read by every launch)"),
             "parity": parity or None,
             "matvec_rows_per_s": world * rows_per_step / (np.mean(mv_t) / 1e3),
             "vecmat_rows_per_s": world * rows_per_step / (np.mean(vm_t) / 1e3),
-            "tree_cache": {"used_for_value": True, "bytes_per_gpu": arena.tree_bytes, "build_seconds": t_trees,
-                           "note": "per-batch cache entry built once (the reference caches C' too, "
-                                   "kernels.py:68-77): decode-tree prefix plus unpacked and column-sorted "
-                                   "pair records; each launch reads it plus the TOC1 value index"},
-            "level_cache": None if not levels else {
-                "used_for_value": False, "bytes_per_gpu": arena.levels_bytes, "build_seconds": t_levels,
-                "ms_per_step": float(np.mean(lv_t)), "rows_per_s": world * rows_per_step / (np.mean(lv_t) / 1e3),
-                "roofline_frac": alg / (np.mean(lv_t) / 1e3) / 1e9 / peak,
-                "note": "toc_levels.cu: used nodes of C' renumbered breadth first (host-built once), the "
-                        "reference's H recurrence one tree level at a time, atomic-free fixed-order v^T.A; "
-                        "slower than the chain walk here (DESIGN.md 4.1)"},
+            "slot_cache": {"used_for_value": bool(slots), "bytes_per_gpu": arena.levels_bytes if slots else None,
+                           "build_seconds": t_slots,
+                           "note": "toc_levels.cu, per-batch entry built once on the host (the reference caches "
+                                   "C' too, kernels.py:68-77): value index, row offsets, column-sorted pair slots, "
+                                   "inner-node (parent, key) records, the code stream as slot references cut into "
+                                   "equal per-thread ranges (bank-aware placement); the launch reads only this"},
+            "tree_cache": {"used_for_value": not slots, "bytes_per_gpu": arena.tree_bytes, "build_seconds": t_trees,
+                           "ms_per_step": float(np.mean(tc_t)),
+                           "rows_per_s": world * rows_per_step / (np.mean(tc_t) / 1e3),
+                           "roofline_frac": alg / (np.mean(tc_t) / 1e3) / 1e9 / peak,
+                           "note": "toc_linalg.cu chain walk over the device tree cache (decode-tree prefix plus "
+                                   "unpacked and column-sorted pair records) and the TOC1 value index; round-1 "
+                                   "headline, kept as the path for batches the slot cache does not fit"},
             "block_only": {"ms_per_step": float(np.mean(bo_t)),
                            "rows_per_s": world * rows_per_step / (np.mean(bo_t) / 1e3),
                            "roofline_frac": alg / (np.mean(bo_t) / 1e3) / 1e9 / peak, "traffic": bo_traffic,
@@ -478,9 +495,12 @@ def main():
                              "note": "toc_linalg32: fp32 operands, fixed-point 32-bit v^T.A, one walk for both "
                                      "products; 1e-4 of the fp64 oracle (not the headline: the reference is f64)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "frac": achieved / peak, "traffic": traffic if slots else None, "traffic_source": traffic_src,
                          "peak_source": peak_src,
-                         "algorithmic_bytes_per_launch": alg, "kernel": "toc::linalg_kernel (A.v + v^T.A)"},
+                         "algorithmic_bytes_per_launch": alg,
+                         "kernel": "toc::levels_kernel<3> (A.v + v^T.A, slot cache)" if slots
+                         else "toc::linalg_kernel (A.v + v^T.A, tree cache)"},
+            "smem_pipe": smem_pipe_line(smem_wf if slots else None, ms_per_step, sampler.summary()),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "e2e_resident": e2e_resident,

@@ -271,12 +271,22 @@ class BlockArena:
         self.levels_dims = (max_slots.value, max_stage.value, max_rows.value)
         return True
 
-    def linalg(self, kind: int, v=None, u=None, R=None, O=None, use_trees: bool = True, use_levels: bool = False):
+    def _launch_levels(self, kind: int, v, R, u, O, b0: int, b1: int, stream) -> None:
+        """toc_linalg_levels over batches [b0, b1) of the slot cache (pointers are device
+        addresses; O points at batch b0's row)."""
+        slots, stage, rows = self.levels_dims
+        rc = N.lib().toc_linalg_levels(
+            self.row_base_d.data_ptr() + 8 * b0, int(b1 - b0), kind, self.n_cols, slots, stage, rows,
+            v if kind & N.TOC_MATVEC else None, R if kind & N.TOC_MATVEC else None,
+            u if kind & N.TOC_VECMAT else None, O if kind & N.TOC_VECMAT else None,
+            self.levels.data_ptr(), self.levels_off_d.data_ptr() + 8 * b0, stream)
+        N.check(rc, "toc_linalg_levels")
+
+    def linalg(self, kind: int, v=None, u=None, R=None, O=None, use_trees: bool = True, use_levels=None):
         """kind = TOC_MATVEC | TOC_VECMAT.  v: device float64 [n_cols]; u: device float64
         [n_rows_total].  Returns (R [n_rows_total], O [n_blocks, n_cols]) device tensors.  Uses
-        the level cache when asked (use_levels) and built, else the tree cache when it has been
-        built (and use_trees), else rebuilds trees per call.  (The level kernel is the slower of
-        the two cached forms at config 2 -- DESIGN.md 4.1 -- so it is opt-in.)"""
+        the slot cache when it has been built (use_levels None or True; False skips it), else the
+        tree cache when it has been built (and use_trees), else rebuilds trees per call."""
         torch = self.torch
         self.raise_corrupt()
         dev = self.data.device
@@ -287,14 +297,8 @@ class BlockArena:
             if O is None:
                 O = torch.empty(max(self.n_blocks * self.n_cols, 1), dtype=torch.float64,
                                 device=dev)[: self.n_blocks * self.n_cols].view(self.n_blocks, self.n_cols)
-        if use_levels and getattr(self, "levels", None) is not None:
-            slots, stage, rows = self.levels_dims
-            rc = N.lib().toc_linalg_levels(
-                self.row_base_d.data_ptr(), self.n_blocks, kind, self.n_cols, slots, stage, rows,
-                _ptr(v) if kind & N.TOC_MATVEC else None, _ptr(R) if kind & N.TOC_MATVEC else None,
-                _ptr(u) if kind & N.TOC_VECMAT else None, _ptr(O) if kind & N.TOC_VECMAT else None,
-                self.levels.data_ptr(), self.levels_off_d.data_ptr(), N.stream_handle())
-            N.check(rc, "toc_linalg_levels")
+        if use_levels is not False and getattr(self, "levels", None) is not None:
+            self._launch_levels(kind, _ptr(v), _ptr(R), _ptr(u), _ptr(O), 0, self.n_blocks, N.stream_handle())
             return R, O
         plan = self.plan(kind)
         scratch = self._scratch_for(plan)
@@ -311,13 +315,14 @@ class BlockArena:
 
     def linalg_pipelined(self, kind: int, v_h, u_h, R_h, O_h, chunks: int = 4):
         """A.v and / or v^T.A with the operands and results in pinned host tensors and the arena
-        (with its tree cache) resident: the batches go in `chunks` slices so that the upload of
+        (with its slot cache, else its tree cache) resident: the batches go in `chunks` slices so that the upload of
         slice k's u, its launch, and the read-back of slice k-1's R / O overlap on three streams.
         v_h [n_cols], u_h [n_rows_total], R_h [n_rows_total], O_h [n_blocks, n_cols]: float64, pinned.
         Returns when R_h / O_h hold the results."""
         torch = self.torch
         self.raise_corrupt()
-        if self.trees is None:
+        slots = getattr(self, "levels", None) is not None
+        if self.trees is None and not slots:
             self.build_trees()
         dev = self.data.device
         mv, vm = bool(kind & N.TOC_MATVEC), bool(kind & N.TOC_VECMAT)
@@ -329,8 +334,8 @@ class BlockArena:
                                "R": torch.empty(max(self.n_rows_total, 1), dtype=torch.float64, device=dev),
                                "O": torch.empty((max(self.n_blocks, 1), max(self.n_cols, 1)), dtype=torch.float64,
                                                 device=dev)}
-        plan = self.plan(kind)
-        scratch = self._scratch_for(plan)
+        plan = None if slots else self.plan(kind)
+        scratch = None if slots else self._scratch_for(plan)
         L = N.lib()
         bounds = np.linspace(0, self.n_blocks, min(max(chunks, 1), max(self.n_blocks, 1)) + 1).astype(np.int64)
         rb = np.concatenate([self.row_base, [self.n_rows_total]])
@@ -352,15 +357,21 @@ class BlockArena:
             done = torch.cuda.Event()
             with torch.cuda.stream(st["run"]):
                 st["run"].wait_event(up)
-                rc = L.toc_linalg_trees(
-                    self.data.data_ptr(), self.block_off_d.data_ptr() + 8 * b0, self.meta_d.data_ptr() + 68 * b0,
-                    self.row_base_d.data_ptr() + 8 * b0, int(b1 - b0), ctypes.byref(plan), kind,
-                    st["v"].data_ptr() if mv else None, st["R"].data_ptr() if mv else None,
-                    st["u"].data_ptr() if vm else None,
-                    st["O"].data_ptr() + 8 * int(b0) * self.n_cols if vm else None,
-                    scratch.data_ptr() if scratch is not None else None, self.trees.data_ptr(),
-                    self.tree_off_d.data_ptr() + 8 * b0, ctypes.c_void_p(st["run"].cuda_stream))
-                N.check(rc, "toc_linalg_trees")
+                if slots:
+                    self._launch_levels(kind, st["v"].data_ptr() if mv else None, st["R"].data_ptr() if mv else None,
+                                        st["u"].data_ptr() if vm else None,
+                                        st["O"].data_ptr() + 8 * int(b0) * self.n_cols if vm else None, b0, b1,
+                                        ctypes.c_void_p(st["run"].cuda_stream))
+                else:
+                    rc = L.toc_linalg_trees(
+                        self.data.data_ptr(), self.block_off_d.data_ptr() + 8 * b0, self.meta_d.data_ptr() + 68 * b0,
+                        self.row_base_d.data_ptr() + 8 * b0, int(b1 - b0), ctypes.byref(plan), kind,
+                        st["v"].data_ptr() if mv else None, st["R"].data_ptr() if mv else None,
+                        st["u"].data_ptr() if vm else None,
+                        st["O"].data_ptr() + 8 * int(b0) * self.n_cols if vm else None,
+                        scratch.data_ptr() if scratch is not None else None, self.trees.data_ptr(),
+                        self.tree_off_d.data_ptr() + 8 * b0, ctypes.c_void_p(st["run"].cuda_stream))
+                    N.check(rc, "toc_linalg_trees")
                 done.record()
             with torch.cuda.stream(st["down"]):
                 st["down"].wait_event(done)

@@ -44,7 +44,7 @@ print("slot cache built", ok, "in", round(time.perf_counter() - t0, 3), "s;", ar
 vd = torch.randn(bench.COLS, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(1))
 ud = torch.randn(arena.n_rows_total, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(2))
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-Rt, Ot = arena.linalg(3, v=vd, u=ud)
+Rt, Ot = arena.linalg(3, v=vd, u=ud, use_levels=False)
 Rt, Ot = Rt.clone(), Ot.clone()
 Rl, Ol = arena.linalg(3, v=vd, u=ud, use_levels=True)
 torch.cuda.synchronize()
@@ -69,5 +69,5 @@ for rep in range(2):
         for k in (1, 2, 3):
             out[f"slots{k}"] = timeit(lambda: arena.linalg(k, v=vd, u=ud, use_levels=True), flush)
         if rep == 0 and lib == (libs or [N.LIB_PATH])[0]:
-            out["trees3"] = timeit(lambda: arena.linalg(3, v=vd, u=ud), flush)
+            out["trees3"] = timeit(lambda: arena.linalg(3, v=vd, u=ud, use_levels=False), flush)
         print(os.path.basename(lib), {k: round(t, 1) for k, t in out.items()}, "us", flush=True)
