@@ -364,6 +364,27 @@ int toc_glm_epoch_images_dp(const uint8_t* d_images, const int64_t* d_image_off,
                             double* const* d_peer_buf, uint32_t* const* d_peer_flag, const int32_t* d_gsize,
                             uint32_t seq0, void* stream);
 
+/* One rank's data for toc_glm_epoch_images_dp_emulated (device pointers, as for
+ * toc_glm_epoch_images_dp). */
+typedef struct {
+  const uint8_t* images;
+  const int64_t* image_off;
+  const TocBlockMeta* meta;
+  double* w;
+} TocDpRank;
+
+/* toc_glm_epoch_images_dp for `world` ranks in ONE cooperative launch on one GPU: thread-block
+ * cluster r runs rank r (d_ranks[r]: its step images, metadata and weights) and exchanges its
+ * gradient with the other clusters through the same receive-slot / flag protocol (the buffers can
+ * be plain device memory).  Separate launches that spin on each other's flags are never
+ * guaranteed to be co-resident on one GPU, so this is how the multi-rank protocol is exercised
+ * with fewer GPUs than ranks.  h_meta_all: the ranks' host metadata, rank-major (world x n_blocks);
+ * every rank's images must have been built for the same cluster shape. */
+int toc_glm_epoch_images_dp_emulated(const TocDpRank* d_ranks, const TocBlockMeta* h_meta_all, int64_t n_blocks,
+                                     int32_t n_cols, int32_t cluster, int32_t loss, double lr, int32_t world,
+                                     double* const* d_peer_buf, uint32_t* const* d_peer_flag, const int32_t* d_gsize,
+                                     uint32_t seq0, void* stream);
+
 /* toc_glm_epoch_images plus 8 clock64 stamps per step from CTA 0 (step start, image landed, P1,
  * A.w and loss, bound, s^T.A, cluster barrier passed, update).  Diagnostic. */
 int toc_glm_epoch_images_traced(const uint8_t* d_images, const int64_t* d_image_off,

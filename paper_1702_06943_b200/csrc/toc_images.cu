@@ -126,7 +126,7 @@ struct ImageArgs {
   long long* trace;  // optional: kTracePoints clock64 stamps per step (CTA 0)
   // Data-parallel epoch with the gradient exchange fused into the kernel (world > 0): each step
   // CTA 0 stores this rank's dense gradient into every rank's receive buffer over NVLink
-  // (peer_buf[q] + (t & 1) * world * m + rank * m), fences, and raises its flag in every rank's
+  // (peer_buf[q] + ((seq0 + t) & 1) * world * m + rank * m), fences, and raises its flag in every rank's
   // flag array (peer_flag[q][rank] = seq0 + t + 1); every CTA then waits for all ranks' flags and
   // applies w -= (lr / gsize[t]) * (sum of the ranks' gradients in rank order).
   double* const* peer_buf;
@@ -134,6 +134,9 @@ struct ImageArgs {
   const int32_t* gsize;
   int32_t world, rank;
   uint32_t seq0;
+  // Emulated data parallelism (toc_glm_epoch_images_dp_emulated): one launch of `world` clusters
+  // on one GPU, cluster r acting as rank r with its own images, metadata and weights.
+  const TocDpRank* ranks;
 };
 
 // System-scope release store / acquire load of a flag (NVLink peers).
@@ -360,6 +363,15 @@ template <bool kWide>
 __global__ void __launch_bounds__(1024, 1) epoch_cluster_kernel(ImageArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t cta = cluster_rank(), C = a.cluster;
+  if (a.ranks) {  // emulated ranks: this cluster is rank blockIdx.x / C
+    const uint32_t r = blockIdx.x / C;
+    const TocDpRank rk = a.ranks[r];
+    a.images = const_cast<uint8_t*>(rk.images);
+    a.image_off = rk.image_off;
+    a.meta = rk.meta;
+    a.w = rk.w;
+    a.rank = (int32_t)r;
+  }
   double* s_red = reinterpret_cast<double*>(smem + 160);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + 448);
   const uint32_t tid = threadIdx.x, nth = blockDim.x, m = (uint32_t)a.n_cols;
@@ -522,7 +534,8 @@ __global__ void __launch_bounds__(1024, 1) epoch_cluster_kernel(ImageArgs a) {
           gl[segcol[sgi]] = sum_partials(cp + sgi, C);  // rank order (as the 1-GPU epoch)
         }
         __syncthreads();
-        const size_t slot = ((size_t)(t & 1) * W + (uint32_t)a.rank) * m;
+        // receive slot from the global step sequence, so back-to-back epochs alternate slots too
+        const size_t slot = ((size_t)((seq - 1u) & 1u) * W + (uint32_t)a.rank) * m;
         for (uint32_t q = 0; q < W; ++q)
           for (uint32_t c = tid; c < m; c += nth) a.peer_buf[q][slot + c] = gl[c];
         __syncthreads();  // the CTA's stores happen before the flag releases (release is cumulative)
@@ -535,7 +548,7 @@ __global__ void __launch_bounds__(1024, 1) epoch_cluster_kernel(ImageArgs a) {
           if (clock64() - t0c > (1ll << 34)) __trap();
       }
       __syncthreads();
-      const double* recv = a.peer_buf[a.rank] + (size_t)(t & 1) * W * m;
+      const double* recv = a.peer_buf[a.rank] + (size_t)((seq - 1u) & 1u) * W * m;
       const double stp = a.lr / (double)a.gsize[t];
       for (uint32_t c = tid; c < m; c += nth) {
         double g = __ldcv(recv + c);
@@ -777,6 +790,54 @@ extern "C" int toc_glm_epoch_images(const uint8_t* d_images, const int64_t* d_im
                                     int32_t loss, double lr, double* d_w, void* stream) {
   return epoch_images_launch(d_images, d_image_off, d_meta, h_meta, n_blocks, n_cols, cluster, loss, lr, d_w, nullptr,
                              0, 0, nullptr, nullptr, nullptr, 0, stream);
+}
+
+extern "C" int toc_glm_epoch_images_dp_emulated(const TocDpRank* d_ranks, const TocBlockMeta* h_meta_all,
+                                                int64_t n_blocks, int32_t n_cols, int32_t cluster, int32_t loss,
+                                                double lr, int32_t world, double* const* d_peer_buf,
+                                                uint32_t* const* d_peer_flag, const int32_t* d_gsize, uint32_t seq0,
+                                                void* stream) {
+  if (n_blocks <= 0 || world < 1 || !d_ranks || !h_meta_all || !d_peer_buf || !d_peer_flag || !d_gsize ||
+      n_cols < 0 || loss < 0 || loss > 2 || cluster < 1 || cluster > (int32_t)toc::kMaxCluster)
+    return TOC_E_ARG;
+  // the shared-memory plan covers every rank's batches; each rank's images were built for the same
+  // shape (cluster, threads, node-id width)
+  const ImagePlan P = image_plan(h_meta_all, world * n_blocks, n_cols, cluster);
+  if (!P.epoch_ok || n_cols > (int32_t)P.max_pairs + 1) return TOC_E_ARG;
+  for (int32_t r = 0; r < world; ++r) {
+    const ImagePlan Pr = image_plan(h_meta_all + (int64_t)r * n_blocks, n_blocks, n_cols, cluster);
+    if (!Pr.epoch_ok || Pr.wide != P.wide || Pr.threads != P.threads || Pr.cluster != P.cluster) return TOC_E_ARG;
+  }
+  toc::ImageArgs a = plan_args(P, n_blocks, n_cols);
+  a.loss = loss;
+  a.lr = lr;
+  a.world = world;
+  a.peer_buf = d_peer_buf;
+  a.peer_flag = d_peer_flag;
+  a.gsize = d_gsize;
+  a.seq0 = seq0;
+  a.ranks = d_ranks;
+  void* fn = P.wide ? (void*)toc::epoch_cluster_kernel<true> : (void*)toc::epoch_cluster_kernel<false>;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, P.epoch_smem) != cudaSuccess)
+    return TOC_E_CUDA;
+  if (P.cluster > 8 && cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+    return TOC_E_CUDA;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(P.cluster * (uint32_t)world);
+  cfg.blockDim = dim3(P.threads);
+  cfg.dynamicSmemBytes = (size_t)P.epoch_smem;
+  cfg.stream = (cudaStream_t)stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = P.cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeCooperative;  // the ranks spin on each other: all co-resident
+  attr[1].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  void* args[] = {&a};
+  return cudaLaunchKernelExC(&cfg, fn, args) == cudaSuccess ? TOC_OK : TOC_E_CUDA;
 }
 
 extern "C" int toc_glm_epoch_images_dp(const uint8_t* d_images, const int64_t* d_image_off, const TocBlockMeta* d_meta,

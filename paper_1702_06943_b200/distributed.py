@@ -269,6 +269,63 @@ class FusedDPEpoch:
         return self.w
 
 
+class EmulatedDPEpochs:
+    """The fused data-parallel epoch (toc_glm_epoch_images_dp) for `world` ranks on ONE GPU, in one
+    cooperative launch (toc_glm_epoch_images_dp_emulated): cluster r runs rank r's local batches
+    of dp_step_plan with its own weights, and the clusters exchange gradients through the same
+    receive-slot / flag protocol as the NVLink path (plain device memory here).  Separate launches
+    spinning on each other are never guaranteed co-resident on one GPU, so this is how the
+    multi-rank protocol runs with fewer GPUs than ranks.  Every rank's weights must equal the
+    reference trainer's at batch_size = local_batch * world."""
+
+    def __init__(self, dataset, local_batch: int, world: int, loss_kind: str, lr: float, seed: int = 0):
+        import torch
+
+        from .matrix import LabeledDataset
+        from .training import DeviceBatches, GlmTrainer, _bind, shuffle_order
+
+        order = shuffle_order(dataset.n_rows, seed)
+        self.torch, self.L, self.world = torch, _bind(), world
+        self.trainers, metas = [], []
+        plans = [dp_step_plan(dataset.n_rows, local_batch, world, r) for r in range(world)]
+        self.n_steps = len(plans[0].global_sizes)
+        cluster = 0
+        for r, plan in enumerate(plans):
+            if any(hi <= lo for lo, hi in plan.local_rows):
+                raise ValueError("every rank needs a local batch at every step")
+            local = np.concatenate([order[lo:hi] for lo, hi in plan.local_rows])
+            sub = LabeledDataset(features=dataset.features.take_rows(local), labels=dataset.labels[local])
+            tr = GlmTrainer(DeviceBatches(sub, local_batch), loss_kind, lr, mode="images", cluster=cluster)
+            if tr.mode != "images":
+                raise ValueError("the step images do not fit shared memory")
+            cluster = tr.cluster
+            self.trainers.append(tr)
+            metas.append(tr.b.arena.meta)
+        self.cluster = cluster
+        self.h_meta = np.ascontiguousarray(np.concatenate(metas))
+        m = max(dataset.n_cols, 1)
+        n_dbl = 2 * world * m
+        self.recv = [torch.zeros(n_dbl + (world + 1) // 2, dtype=torch.float64, device="cuda") for _ in range(world)]
+        ptrs = [t.data_ptr() for t in self.recv]
+        self.buf_ptrs = torch.tensor(ptrs, dtype=torch.int64, device="cuda")
+        self.flag_ptrs = torch.tensor([x + 8 * n_dbl for x in ptrs], dtype=torch.int64, device="cuda")
+        self.ranks = torch.tensor([[t.images.data_ptr(), t.image_off_d.data_ptr(), t.b.arena.meta_d.data_ptr(),
+                                    t.w.data_ptr()] for t in self.trainers], dtype=torch.int64, device="cuda")
+        self.gsize = torch.tensor(np.asarray(plans[0].global_sizes, np.int32), device="cuda")
+        self.n_cols, self.loss, self.lr = dataset.n_cols, self.trainers[0].loss, float(lr)
+        self.epochs = 0
+
+    def epoch(self):
+        """One epoch on every rank (one launch); returns the ranks' weight tensors."""
+        N.check(self.L.toc_glm_epoch_images_dp_emulated(
+            self.ranks.data_ptr(), self.h_meta.ctypes.data_as(ctypes.c_void_p), self.trainers[0].b.arena.n_blocks,
+            self.n_cols, self.cluster, self.loss, self.lr, self.world, self.buf_ptrs.data_ptr(),
+            self.flag_ptrs.data_ptr(), self.gsize.data_ptr(), (self.epochs * self.n_steps) & 0xFFFFFFFF,
+            N.stream_handle()), "toc_glm_epoch_images_dp_emulated")
+        self.epochs += 1
+        return [t.w for t in self.trainers]
+
+
 def train_data_parallel(dataset, config, world: int, rank: int, group=None, graph: bool = True,
                         fused: bool = True):
     """DP-MGD on this rank's GPU; every rank returns the same weights and the risk trace (the

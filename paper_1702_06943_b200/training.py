@@ -135,6 +135,7 @@ def _bind():
         L.toc_mgd_parts_cluster_max.argtypes = [ctypes.c_void_p]
         L.toc_glm_epoch_images_dp.argtypes = [P, P, P, P, I64, I32, I32, I32, D, P, I32, I32, P, P, P,
                                                ctypes.c_uint32, P]
+        L.toc_glm_epoch_images_dp_emulated.argtypes = [P, P, I64, I32, I32, I32, D, I32, P, P, P, ctypes.c_uint32, P]
         L._mgd_bound = True
     return L
 

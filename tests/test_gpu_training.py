@@ -330,3 +330,29 @@ def test_parts_dsmem_equals_global_kernel(loss, lr, cluster):
         L.toc_mgd_set_parts_dsmem(0)
     assert np.array_equal(td.weights(), wg)
     assert td.risk() == rg
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("loss,world", [("logistic", 2), ("hinge", 2), ("logistic", 4)])
+def test_dp_fused_exchange_emulated_ranks(oracle, loss, world):
+    """The fused NVLink gradient exchange of toc_glm_epoch_images_dp with `world` ranks, run on one
+    GPU as one cooperative launch of `world` clusters (rank = cluster; receive slots and flags in
+    device memory).  Every rank's weights after 3 back-to-back epochs (the receive slot alternates
+    with the global step sequence, no host barrier between epochs) equal the reference trainer at
+    the global batch size 250 * world, and equal each other bit for bit."""
+    from paper_1702_06943_b200 import synth
+    from paper_1702_06943_b200.distributed import EmulatedDPEpochs
+    from paper_1702_06943_b200.matrix import LabeledDataset, SparseRowMatrix
+
+    n = 250 * world * 10 - 100  # last global step short (the last rank holds 150 rows)
+    rp, c, v, y = synth.cfg3_dataset(n, seed=41)
+    ds = LabeledDataset(features=SparseRowMatrix.from_csr(68, rp, c, v), labels=y)
+    lr, epochs = 0.05, 3
+    run = EmulatedDPEpochs(ds, 250, world, loss, lr, seed=0)
+    for _ in range(epochs):
+        ws = run.epoch()
+    got = [w.cpu().numpy()[:68] for w in ws]
+    w_ref, _ = oracle.train_glm(rp, c, v, y, 68, loss, 250 * world, lr, epochs, 0)
+    for r in range(world):
+        assert within_rel(got[r], w_ref, 1e-9), max_rel_err(got[r], w_ref)
+        assert np.array_equal(got[r], got[0])
