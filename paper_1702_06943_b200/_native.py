@@ -12,7 +12,9 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtoc_b200.so")
+# TOC_LIB (tests only): load another build of the library, e.g. the bounds-checked one
+# (libtoc_b200_checked.so, `make checked`).
+LIB_PATH = os.environ.get("TOC_LIB") or os.path.join(_HERE, "libtoc_b200.so")
 
 TOC_OK, TOC_E_BAD_MAGIC, TOC_E_BAD_VERSION, TOC_E_TRUNCATED, TOC_E_FORMAT = 0, 1, 2, 3, 4
 TOC_E_CORRUPT, TOC_E_INPUT, TOC_E_CUDA, TOC_E_ARG = 5, 6, 7, 8

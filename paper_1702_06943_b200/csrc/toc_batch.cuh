@@ -485,6 +485,7 @@ struct Batch {
       uint32_t x = pk.par(db + (j - lo));  // j + 1 < j1 <= hi: j is never the final code
       uint32_t y = (j + 2 < hi) ? pk.par(db + (j + 1 - lo)) : last[r];
       while (x > nI || y > nI) {
+        TOC_CHECK((x <= nI || x - 1 - nI < m.n_derived) && (y <= nI || y - 1 - nI < m.n_derived));
         uint32_t px = x, kx = 0, py = y, ky = 0;
         if (x > nI) pk.get(x - 1 - nI, px, kx);
         if (y > nI) pk.get(y - 1 - nI, py, ky);
@@ -519,6 +520,7 @@ struct Batch {
     uint32_t x = (j + 1 < hi) ? pk.par(db + (j - lo)) : last[r];
     for (;;) {
       uint32_t par = 0, key = x;
+      TOC_CHECK(x >= 1 && (x <= nI || x - 1 - nI < m.n_derived));
       if (x > nI) pk.get(x - 1 - nI, par, key);
       visit(key);
       if (par) {

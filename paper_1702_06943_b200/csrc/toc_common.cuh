@@ -9,6 +9,24 @@
 #define TOC_HD __host__ __device__ __forceinline__
 #define TOC_D __device__ __forceinline__
 
+// Bounds checks of the checked build (make checked -> libtoc_b200_checked.so, -DTOC_CHECKED): the
+// compute-sanitizer tools are closed on this GPU pool, so index and size invariants of the hot
+// kernels are asserted in the kernels themselves (file:line printed, then a trap).  Compiled out
+// of the product library.
+#ifdef TOC_CHECKED
+#include <cstdio>
+#define TOC_CHECK(c)                                                                              \
+  do {                                                                                            \
+    if (!(c)) {                                                                                   \
+      printf("TOC_CHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, (int)blockIdx.x, \
+             (int)threadIdx.x, #c);                                                               \
+      __trap();                                                                                   \
+    }                                                                                             \
+  } while (0)
+#else
+#define TOC_CHECK(c) ((void)0)
+#endif
+
 namespace toc {
 
 constexpr int kWarp = 32;

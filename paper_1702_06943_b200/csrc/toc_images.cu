@@ -404,6 +404,7 @@ __global__ void __launch_bounds__(1024, 1) epoch_cluster_kernel(ImageArgs a) {
   if (tid == 0) {
     const NextImage x = first_image<kWide>(a, cta);
     src = x.src;
+    TOC_CHECK(x.shared <= a.max_shared && x.part_bytes <= a.max_part);
     fetch_image(x, buf0, &mbar[0], cta, C);
   }
   const bool squared = a.loss == TOC_LOSS_SQUARED;
@@ -425,6 +426,7 @@ __global__ void __launch_bounds__(1024, 1) epoch_cluster_kernel(ImageArgs a) {
       x.part_off = h[kHNextPart + 2 * cta];
       x.part_bytes = h[kHNextPart + 2 * cta + 1];
       src = x.src;
+      TOC_CHECK(x.shared <= a.max_shared && x.part_bytes <= a.max_part);
       fetch_image(x, k ? buf0 : buf1, &mbar[k ^ 1u], cta, C);
     }
     const uint32_t n = h[0], nI = h[1], n_segs = h[5];

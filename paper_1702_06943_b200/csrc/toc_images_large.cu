@@ -344,6 +344,7 @@ __global__ void __launch_bounds__(1024, 1) epoch_large_kernel(LargeEpochArgs a) 
     mbar_init(&mbar[0], 1);
     mbar_init(&mbar[1], 1);
     const uint32_t bytes = (uint32_t)(a.part_off[a.t0 * a.cluster + cta + 1] - a.part_off[a.t0 * a.cluster + cta]);
+    TOC_CHECK(bytes <= a.max_part);
     mbar_expect(&mbar[0], bytes);
     bulk_copy(buf0, src, bytes, &mbar[0]);
   }
@@ -517,6 +518,7 @@ __global__ void __launch_bounds__(1024, 1) epoch_dsmem_kernel(DsmemEpochArgs a) 
   if (tid == 0) {
     mbar_init(&mbar[0], 1);
     const uint32_t bytes = (uint32_t)(a.part_off[cta + 1] - a.part_off[cta]);
+    TOC_CHECK(bytes <= a.max_part);
     mbar_expect(&mbar[0], bytes);
     bulk_copy(buf, src, bytes, &mbar[0]);
   }

@@ -254,6 +254,8 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
     TOC_LVL_STAMP(0);
     const LvlHdr h = *reinterpret_cast<const LvlHdr*>(stage);  // the stage is refilled mid-batch
     const uint32_t n = h.n_rows, nP = h.nP, nQ = h.nQ, K = h.K;
+    TOC_CHECK(h.S <= (uint32_t)a.max_slots && h.off_stream <= (uint32_t)a.max_stage && n <= (uint32_t)a.max_rows &&
+              h.T == nth && h.n_cols == ncol && h.S == 1 + nP + nQ && K % 4 == 0 && h.C <= h.T * K);
     const double* uniq_s = reinterpret_cast<const double*>(stage + h.off_uniq);
     const uint32_t* rowoff_s = reinterpret_cast<const uint32_t*>(stage + h.off_rowoff);
     const uint32_t* prs_s = reinterpret_cast<const uint32_t*>(stage + h.off_prs);
@@ -292,6 +294,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
             const uint32_t rec[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
             for (uint32_t i = 0; i < 4; ++i) {
+              TOC_CHECK((rec[i] & kSlotMask) < h.S && ((rec[i] >> 16) & kSlotB) < h.S && (rec[i] == 0 || r < n));
               limb_add(lo_s, hi_s, rec[i] & kSlotMask, xl, xh);
               if ((rec[i] >> 16) & kSlotB) limb_add(lo_s, hi_s, (rec[i] >> 16) & kSlotB, xl, xh);
               if (rec[i] & kRowEnd) {
@@ -328,6 +331,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
       for (uint32_t y = tid; y < nQ; y += nth) {
         const uint32_t x = nP + 1 + y;
         uint32_t rec = inner_s[y];
+        TOC_CHECK((rec >> 16) >= 1 && (rec >> 16) <= nP && (rec & 0xffffu) >= 1 && (rec & 0xffffu) < x);
         if (!f64) {
           const uint32_t l = lo_s[x];
           const int32_t hh = hi_s[x];
@@ -335,6 +339,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
             uint32_t p = rec & 0xffffu;
             limb_add(lo_s, hi_s, rec >> 16, l, hh);
             while (p > nP) {
+              TOC_CHECK(p - nP - 1 < nQ);
               rec = inner_s[p - nP - 1];
               limb_add(lo_s, hi_s, rec >> 16, l, hh);
               p = rec & 0xffffu;
@@ -370,6 +375,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
           double acc = 0.0;
           for (uint32_t p = p0; p < p1; ++p) {
             const uint32_t x = prs_s[p - 1];
+            TOC_CHECK(((x >> 16) & 0x7fffu) < h.nU && (x & 0xffffu) < ncol);
             const double t = f64 ? Tf[p] : limb_value(lo_s[p], hi_s[p], L, g_inv);
             acc += uniq_s[(x >> 16) & 0x7fffu] * t;
             if (x >> 31) {  // last pair slot of its column
@@ -388,6 +394,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
       // for the columns no pair touches
       for (uint32_t c = tid; c < ncol; c += nth) {
         const uint32_t lo = colst_s[c], hi = colst_s[c + 1];
+        TOC_CHECK(lo >= 1 && lo <= hi && hi <= nP + 1);
         if (lo == hi) {
           o[c] = 0.0;
         } else {
@@ -405,6 +412,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
       // P1 for the pair slots (Algorithm 5's H at depth 1); the row offsets into a private copy
       for (uint32_t i = tid; i < nP; i += nth) {
         const uint32_t x = prs_s[i];
+        TOC_CHECK(((x >> 16) & 0x7fffu) < h.nU && (x & 0xffffu) < ncol);
         H[1 + i] = uniq_s[(x >> 16) & 0x7fffu] * v_s[x & 0xffffu];
       }
       if (tid == 0) H[0] = 0.0;
@@ -419,6 +427,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
         double hv = H[rec >> 16];
         uint32_t p = rec & 0xffffu;
         while (p > nP) {
+          TOC_CHECK(p - nP - 1 < nQ);
           rec = inner_s[p - nP - 1];
           hv += H[rec >> 16];
           p = rec & 0xffffu;
@@ -441,6 +450,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
           double ha[4], hb[4];
 #pragma unroll
           for (uint32_t i = 0; i < 4; ++i) {
+            TOC_CHECK((rec[i] & kSlotMask) < h.S && ((rec[i] >> 16) & kSlotB) < h.S);
             ha[i] = H[rec[i] & kSlotMask];
             hb[i] = ((rec[i] >> 16) & kSlotB) ? H[(rec[i] >> 16) & kSlotB] : 0.0;
           }
@@ -449,6 +459,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
             acc += ha[i];
             acc += hb[i];
             if (rec[i] & kRowEnd) {
+              TOC_CHECK(r < n);
               if (here) a.R[rb + r] = acc;
               else head_s[tid] = acc;
               acc = 0.0;
