@@ -606,9 +606,11 @@ def run_mlp(rank: int, world: int, cpu_sample: bool):
     _, trace = train_mlp(ds, epochs=epochs)
     out.update({"steps_per_epoch": n // 250, "epoch_seconds": trace.seconds, "risk_per_epoch": trace.risks,
                 "wall_seconds_incl_compress_and_cache": time.perf_counter() - t0,
-                "mode": "native epoch (toc_mlp_epoch, one CUDA graph): per step the batch decoded from the "
-                        "node-record cache into an L2-resident buffer, A.W1 and A^T.delta on the fp64 tensor cores "
-                        "(DMMA), softmax-CE tail and parameter updates in CUDA kernels"})
+                "memory": getattr(trace, "memory", None),
+                "mode": "native epoch (toc_mlp_epoch, one CUDA graph): per step the batch decoded from its TOC1 "
+                        "code stream and its step-cache entry (4-byte node records) into an L2-resident tile "
+                        "buffer, A.W1 and A^T.delta on the fp64 tensor cores (DMMA), softmax-CE tail and parameter "
+                        "updates in CUDA kernels"})
     if cpu_sample:
         out["cpu_port"] = cpu_mlp_sample(rp, c, v, y, n // 250)
     return out

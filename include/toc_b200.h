@@ -423,13 +423,26 @@ int toc_matcache_left(const uint8_t* d_entry, const TocBlockMeta* h_meta, int32_
                       const double* d_MT, double* d_out, void* d_scratch, int64_t scratch_bytes,
                       void* stream);
 
+/* ---- MLP step cache (csrc/toc_matcache.cu): the decode tree of each batch in 4 bytes per node
+ * (parent | key << 17), its pair records and value index -- read together with the TOC1 block's
+ * own code stream, so the cache does not repeat the codes (config 5: 0.45 MB per batch, 1.5x the
+ * TOC1 block; the node-record cache above is 2.3 MB).  toc_mlpcache_offsets (host): entry offsets,
+ * TOC_E_ARG if some batch's ids do not fit (more than 2^17 nodes, 2^15 pairs, 2^16 columns or
+ * values).  toc_mlpcache_build: every entry, once (plan from toc_plan(TOC_MATVEC) + its scratch). */
+int toc_mlpcache_offsets(const TocBlockMeta* h_meta, int64_t n_blocks, int64_t* h_cache_off);
+int toc_mlpcache_build(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+                       int64_t n_blocks, const TocPlan* plan, const int64_t* d_cache_off, uint8_t* d_cache,
+                       void* d_scratch, void* stream);
+
 /* ---- config-5 MLP epoch (oracle.train_mlp's step; first layer = kernels.py:177-234) ---------
- * One epoch over the batches in order, four kernels per step on `stream` (toc_mlp.cu): A_b . W1
- * and A_b^T . delta on the fp64 tensor cores over rows decoded from the node-record cache
- * (toc_matcache_build), the softmax cross-entropy tail and the parameter updates.  Weights are
- * updated in place.  h_cache_off / h_row_base / h_n_rows: host copies; d_labels: class ids (f64).
+ * One epoch over the batches in order, four kernels per step on `stream` (toc_mlp.cu): each
+ * step's batch decoded from its TOC1 block (d_arena + h_block_off[b]) and step-cache entry
+ * (toc_mlpcache_build) into a dense tile buffer, A_b . W1 and A_b^T . delta on the fp64 tensor
+ * cores, the softmax cross-entropy tail and the parameter updates.  Weights are updated in place.
+ * h_block_off / h_cache_off / h_row_base / h_n_rows: host copies; d_labels: class ids (f64).
  * k must be 10; dense = 1 only if every row has all m columns (the decode then skips zeroing);
- * scratch: toc_mlp_scratch(max rows per batch, m, h, k). */
+ * scratch: toc_mlp_scratch(max rows per batch, m, h, k).  toc_mlp_risk: the per-row cross-entropy
+ * of the current parameters over every batch (forward only) into d_loss [rows]. */
 /* Diagnostic: launch only the step kernels in mask (bit 0 decode, 1 right, 2 tail, 3 left; 15 =
  * all, the default) -- for timing them in the stream; any other mask trains wrongly. */
 int toc_mlp_set_kernels(int32_t mask);
@@ -437,20 +450,26 @@ int toc_mlp_set_kernels(int32_t mask);
  * replays it while the arguments (and the host arrays' contents) are unchanged; 0: plain launches. */
 int toc_mlp_set_graph(int32_t on);
 int toc_mlp_set_pdl(int32_t on); /* tuning knob: programmatic dependent launch of the step kernels (default 1) */
+int toc_mlp_set_decode_ctas(int32_t per_sm); /* tuning knob: decode CTAs per SM (1..32, default 8) */
 int toc_mlp_scratch(int32_t max_rows, int32_t m, int32_t h, int32_t k, int64_t* bytes);
-int toc_mlp_epoch(const uint8_t* d_cache, const int64_t* h_cache_off, const int64_t* h_row_base,
-                  const int32_t* h_n_rows, int64_t n_blocks, int32_t m, int32_t h, int32_t k,
-                  const double* d_labels, double* d_W1, double* d_b1, double* d_W2, double* d_b2, double lr,
-                  int32_t dense, void* d_scratch, int64_t scratch_bytes, void* stream);
+int toc_mlp_epoch(const uint8_t* d_arena, const int64_t* h_block_off, const uint8_t* d_cache,
+                  const int64_t* h_cache_off, const int64_t* h_row_base, const int32_t* h_n_rows, int64_t n_blocks,
+                  int32_t m, int32_t h, int32_t k, const double* d_labels, double* d_W1, double* d_b1, double* d_W2,
+                  double* d_b2, double lr, int32_t dense, void* d_scratch, int64_t scratch_bytes, void* stream);
+int toc_mlp_risk(const uint8_t* d_arena, const int64_t* h_block_off, const uint8_t* d_cache, const int64_t* h_cache_off,
+                 const int64_t* h_row_base, const int32_t* h_n_rows, int64_t n_blocks, int32_t m, int32_t h, int32_t k,
+                 const double* d_labels, const double* d_W1, const double* d_b1, const double* d_W2,
+                 const double* d_b2, int32_t dense, double* d_loss, void* d_scratch, int64_t scratch_bytes,
+                 void* stream);
 /* One data-parallel step of the same model (the per-rank half of toc_mlp_epoch's step; the caller
  * all-reduces and applies the update): the summed gradient of batch `step` at the given weights
  * into d_grad = [W1 m*h | W2 h*k | b1 h | b2 k].  Steps of one epoch must be issued in batch order
  * starting at step 0 (the decode buffers alternate by step parity). */
-int toc_mlp_step_grad(const uint8_t* d_cache, const int64_t* h_cache_off, const int64_t* h_row_base,
-                      const int32_t* h_n_rows, int64_t n_blocks, int64_t step, int32_t m, int32_t h, int32_t k,
-                      const double* d_labels, const double* d_W1, const double* d_b1, const double* d_W2,
-                      const double* d_b2, int32_t dense, double* d_grad, void* d_scratch, int64_t scratch_bytes,
-                      void* stream);
+int toc_mlp_step_grad(const uint8_t* d_arena, const int64_t* h_block_off, const uint8_t* d_cache,
+                      const int64_t* h_cache_off, const int64_t* h_row_base, const int32_t* h_n_rows, int64_t n_blocks,
+                      int64_t step, int32_t m, int32_t h, int32_t k, const double* d_labels, const double* d_W1,
+                      const double* d_b1, const double* d_W2, const double* d_b2, int32_t dense, double* d_grad,
+                      void* d_scratch, int64_t scratch_bytes, void* stream);
 
 /* ---- decode (codec.py:262-292 node_sequence / decode; cli.py:194-221 verify) -----------------
  * Two passes with a plan from toc_plan(kind = TOC_MATVEC) and its scratch: toc_decode_counts writes

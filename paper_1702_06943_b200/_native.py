@@ -90,9 +90,13 @@ def lib():
     L.toc_matcache_left_scratch.argtypes = [P, I32, I32, ctypes.POINTER(ctypes.c_int64)]
     L.toc_matcache_left.argtypes = [P, P, I32, I32, P, P, P, I64, P]
     L.toc_mlp_scratch.argtypes = [I32, I32, I32, I32, ctypes.POINTER(ctypes.c_int64)]
-    L.toc_mlp_epoch.argtypes = [P, P, P, P, I64, I32, I32, I32, P, P, P, P, P, ctypes.c_double, I32, P, I64, P]
+    L.toc_mlpcache_offsets.argtypes = [P, I64, P]
+    L.toc_mlpcache_build.argtypes = [P, P, P, I64, ctypes.POINTER(TocPlan), P, P, P, P]
+    L.toc_mlp_epoch.argtypes = [P, P, P, P, P, P, I64, I32, I32, I32, P, P, P, P, P, ctypes.c_double, I32, P, I64,
+                                P]
+    L.toc_mlp_risk.argtypes = [P, P, P, P, P, P, I64, I32, I32, I32, P, P, P, P, P, I32, P, P, I64, P]
     L.toc_mlp_set_pdl.argtypes = [I32]
-    L.toc_mlp_step_grad.argtypes = [P, P, P, P, I64, I64, I32, I32, I32, P, P, P, P, P, I32, P, P, I64, P]
+    L.toc_mlp_step_grad.argtypes = [P, P, P, P, P, P, I64, I64, I32, I32, I32, P, P, P, P, P, I32, P, P, I64, P]
     L.toc_levels_build.restype = P
     L.toc_levels_build.argtypes = [P, P, P, I64, I32]
     L.toc_levels_info.argtypes = [P, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int32),

@@ -424,6 +424,31 @@ class BlockArena:
         self.matcache, self.matcache_off, self.matcache_off_d = cache, off, off_d
         return self
 
+    def build_mlpcache(self) -> bool:
+        """The MLP step cache (toc_mlpcache_build): per batch the decode tree in 4 bytes per node,
+        pair records and the value index; each step decodes its batch from it and the TOC1 block's
+        own code stream.  Returns False (no cache) when some batch's ids do not fit its fields."""
+        torch = self.torch
+        self.raise_corrupt()
+        L = N.lib()
+        off = np.zeros(self.n_blocks + 1, np.int64)
+        rc = L.toc_mlpcache_offsets(self.meta.ctypes.data_as(ctypes.c_void_p), self.n_blocks,
+                                    off.ctypes.data_as(ctypes.c_void_p))
+        if rc == N.TOC_E_ARG:
+            self.mlpcache = None
+            return False
+        N.check(rc, "toc_mlpcache_offsets")
+        plan = self.plan(N.TOC_MATVEC)
+        scratch = self._scratch_for(plan)
+        cache = torch.empty(int(off[-1]) + 16, dtype=torch.uint8, device=self.data.device)
+        off_d = torch.from_numpy(off[:-1].copy()).to(self.data.device)
+        N.check(L.toc_mlpcache_build(self.data.data_ptr(), self.block_off_d.data_ptr(), self.meta_d.data_ptr(),
+                                     self.n_blocks, ctypes.byref(plan), off_d.data_ptr(), cache.data_ptr(),
+                                     scratch.data_ptr() if scratch is not None else None, N.stream_handle()),
+                "toc_mlpcache_build")
+        self.mlpcache, self.mlpcache_off = cache, off
+        return True
+
     def _matmat_cached(self, side: int, M, p: int, batch, out):
         torch = self.torch
         L = N.lib()

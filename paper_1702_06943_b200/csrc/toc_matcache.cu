@@ -156,6 +156,104 @@ __global__ void __launch_bounds__(1024, 1) mc_build_kernel(McArgs a) {
   }
 }
 
+// ---- the MLP step cache (toc_mlp.cu decodes each step's batch from it) -----------------------
+// The decode tree of a batch in 4 bytes per node, read together with the TOC1 block's own packed
+// code stream (the cache does not repeat the codes, a quarter of the node records above):
+//   header   u32[16]: n_rows, n_codes, T, |I|, n_cols, n_uniques, off_codes (in the block),
+//            w_codes, off_rowoff, off_pairs, off_nodes, off_uniq                             64 B
+//   rowoff   u32[n + 1]
+//   pairs    u32[|I| + 1]: column | value ref << 16 of pair id i (i >= 1)
+//   nodes    u32[T]: derived node x: parent | key << 17 (codec.py:243-251: its parent is the code
+//            at the position that created it, its key the first pair of the next code); 0 for pairs
+//   uniq     f64[n_uniques]: the value index
+// Batches whose ids do not fit (T > 2^17 nodes, 2^15 pairs, more than 2^16 columns or values) are
+// refused (toc_mlpcache_offsets returns TOC_E_ARG; the caller keeps the node-record cache).
+struct DcLayout {
+  uint32_t off_rowoff, off_pairs, off_nodes, off_uniq, total;
+};
+
+constexpr uint32_t kDcHeader = 64;
+
+TOC_HD bool dc_fits(const TocBlockMeta& m) {
+  return 1ull + m.n_pairs + m.n_derived <= (1ull << 17) && m.n_pairs < (1u << 15) && m.n_cols <= 65536u &&
+         m.n_uniques <= 65536u;
+}
+
+TOC_HD DcLayout dc_layout(const TocBlockMeta& m) {
+  DcLayout L;
+  uint32_t o = kDcHeader;
+  L.off_rowoff = o;
+  o += align16(4u * (m.n_rows + 1));
+  L.off_pairs = o;
+  o += align16(4u * (m.n_pairs + 1));
+  L.off_nodes = o;
+  o += align16(4u * (1u + m.n_pairs + m.n_derived));
+  L.off_uniq = o;
+  o += align16(8u * m.n_uniques);
+  L.total = o;
+  return L;
+}
+
+template <bool kWide>
+__global__ void __launch_bounds__(1024, 1) dc_build_kernel(McArgs a) {
+  extern __shared__ __align__(16) uint8_t smem[];
+  uint32_t* s_warp = reinterpret_cast<uint32_t*>(smem);
+  uint8_t* p = smem + kFixedBytes;
+  uint8_t* slab = a.scratch ? a.scratch + (int64_t)blockIdx.x * a.slab_bytes : nullptr;
+  const uint32_t tid = threadIdx.x, nth = blockDim.x;
+  for (int64_t b = blockIdx.x; b < a.n_blocks; b += gridDim.x) {
+    const TocBlockMeta m = a.meta[b];
+    if (m.status != TOC_OK || m.corrupt || !dc_fits(m)) continue;
+    uint8_t* tables = batch_layout<kWide>(m).total <= (uint32_t)a.batch_smem_budget ? p : slab;
+    __syncthreads();
+    Batch<kWide> B;
+    const uint8_t* blk = a.arena + a.block_off[b];
+    B.init(blk, m, tables);
+    B.load_index(s_warp);
+    B.build_nodes();
+    __syncthreads();
+    B.resolve_keys();
+    __syncthreads();
+    const DcLayout L = dc_layout(m);
+    uint8_t* e = a.cache + a.cache_off[b];
+    uint32_t* rowoff = reinterpret_cast<uint32_t*>(e + L.off_rowoff);
+    uint32_t* pairs = reinterpret_cast<uint32_t*>(e + L.off_pairs);
+    uint32_t* nodes = reinterpret_cast<uint32_t*>(e + L.off_nodes);
+    double* uniq = reinterpret_cast<double*>(e + L.off_uniq);
+    for (uint32_t r = tid; r <= B.n; r += nth) rowoff[r] = B.rowoff[r];
+    for (uint32_t i = tid; i < B.nI; i += nth)
+      pairs[i + 1] = ld_packed(blk + m.off_cols, i, m.w_cols) | (ld_packed(blk + m.off_refs, i, m.w_refs) << 16);
+    if (tid == 0) pairs[0] = 0u;
+    for (uint32_t i = tid; i < m.n_uniques; i += nth) uniq[i] = B.uniq[i];
+    const uint32_t T = 1u + B.nI + m.n_derived;
+    for (uint32_t x = tid; x < T; x += nth) {
+      uint32_t w = 0u;
+      if (x > B.nI) {
+        uint32_t par, key;
+        B.pk.get(x - 1 - B.nI, par, key);
+        w = par | (key << 17);
+      }
+      nodes[x] = w;
+    }
+    if (tid == 0) {
+      uint32_t* h = reinterpret_cast<uint32_t*>(e);
+      h[0] = B.n;
+      h[1] = m.n_codes;
+      h[2] = T;
+      h[3] = B.nI;
+      h[4] = m.n_cols;
+      h[5] = m.n_uniques;
+      h[6] = m.off_codes;
+      h[7] = m.w_codes;
+      h[8] = L.off_rowoff;
+      h[9] = L.off_pairs;
+      h[10] = L.off_nodes;
+      h[11] = L.off_uniq;
+      for (int k = 12; k < 16; ++k) h[k] = 0u;
+    }
+  }
+}
+
 TOC_D NodeRec ld_node(const NodeRec* nodes, uint32_t x) {
   const uint4 w = __ldg(reinterpret_cast<const uint4*>(nodes) + x);
   NodeRec n;
@@ -328,6 +426,44 @@ extern "C" int toc_matcache_offsets(const TocBlockMeta* h_meta, int64_t n_blocks
   }
   h_cache_off[n_blocks] = o;
   return TOC_OK;
+}
+
+extern "C" int toc_mlpcache_offsets(const TocBlockMeta* h_meta, int64_t n_blocks, int64_t* h_cache_off) {
+  if (!h_meta || n_blocks < 0 || !h_cache_off) return TOC_E_ARG;
+  int64_t o = 0;
+  for (int64_t b = 0; b < n_blocks; ++b) {
+    if (!toc::dc_fits(h_meta[b])) return TOC_E_ARG;
+    h_cache_off[b] = o;
+    o += toc::dc_layout(h_meta[b]).total;
+  }
+  h_cache_off[n_blocks] = o;
+  return TOC_OK;
+}
+
+extern "C" int toc_mlpcache_build(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,
+                                  int64_t n_blocks, const TocPlan* plan, const int64_t* d_cache_off, uint8_t* d_cache,
+                                  void* d_scratch, void* stream) {
+  if (!plan || n_blocks < 0 || !d_cache || !d_cache_off) return TOC_E_ARG;
+  if (plan->global_tables && !d_scratch) return TOC_E_ARG;
+  if (n_blocks == 0) return TOC_OK;
+  toc::McArgs a{};
+  a.arena = d_arena;
+  a.block_off = d_block_off;
+  a.meta = d_meta;
+  a.n_blocks = n_blocks;
+  a.scratch = (uint8_t*)d_scratch;
+  a.cache = d_cache;
+  a.cache_off = d_cache_off;
+  a.batch_smem_budget = plan->smem_bytes - (int32_t)toc::kFixedBytes;
+  a.slab_bytes = plan->global_tables ? plan->scratch_bytes / plan->ctas : 0;
+  void* fn = plan->wide ? (void*)toc::dc_build_kernel<true> : (void*)toc::dc_build_kernel<false>;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, plan->smem_bytes) != cudaSuccess)
+    return TOC_E_CUDA;
+  void* args[] = {&a};
+  return cudaLaunchKernel(fn, dim3(plan->ctas), dim3(plan->threads), args, plan->smem_bytes, (cudaStream_t)stream) ==
+                 cudaSuccess
+             ? TOC_OK
+             : TOC_E_CUDA;
 }
 
 extern "C" int toc_matcache_build(const uint8_t* d_arena, const int64_t* d_block_off, const TocBlockMeta* d_meta,

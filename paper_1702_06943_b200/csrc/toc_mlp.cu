@@ -24,32 +24,30 @@
 
 namespace toc {
 
-// node-record cache entry (layout: toc_matcache.cu)
-struct MlpNode {
-  uint32_t par, col;
-  double val;
-};
-
+// MLP step cache entry (layout: toc_matcache.cu, dc_layout): 4-byte node records (parent | key <<
+// 17), pair records (column | value ref << 16), the value index and row offsets; the code stream is
+// read from the batch's TOC1 block itself.
 struct MlpEntry {
   const uint32_t* rowoff;
-  const uint32_t* codes;
-  const uint4* nodes;
-  uint32_t n_rows;
+  const uint32_t* pairs;
+  const uint32_t* nodes;
+  const double* uniq;
+  uint32_t n_rows, n_codes, nI, nU, off_codes, w_codes;
 };
 
 TOC_D MlpEntry mlp_entry(const uint8_t* e) {
   const uint32_t* h = reinterpret_cast<const uint32_t*>(e);
-  const uint32_t n = h[0], C = h[1], T = h[2];
-  (void)T;
-  uint32_t o = 32u;  // kMcHeader
   MlpEntry E;
-  E.rowoff = reinterpret_cast<const uint32_t*>(e + o);
-  o += align16(4u * (n + 1));
-  E.codes = reinterpret_cast<const uint32_t*>(e + o);
-  o += align16(4u * C);
-  o += align16(4u * (C + 1));  // pstart
-  E.nodes = reinterpret_cast<const uint4*>(e + o);
-  E.n_rows = n;
+  E.n_rows = __ldg(h);
+  E.n_codes = __ldg(h + 1);
+  E.nI = __ldg(h + 3);
+  E.nU = __ldg(h + 5);
+  E.off_codes = __ldg(h + 6);
+  E.w_codes = __ldg(h + 7);
+  E.rowoff = reinterpret_cast<const uint32_t*>(e + __ldg(h + 8));
+  E.pairs = reinterpret_cast<const uint32_t*>(e + __ldg(h + 9));
+  E.nodes = reinterpret_cast<const uint32_t*>(e + __ldg(h + 10));
+  E.uniq = reinterpret_cast<const double*>(e + __ldg(h + 11));
   return E;
 }
 
@@ -66,7 +64,9 @@ constexpr uint32_t kNT = 5;            // n-tiles (8 hidden units each) per CTA:
 constexpr uint32_t kKMax = 16;         // classes
 
 struct MlpStep {
-  const uint8_t* entry;  // the batch's node-record cache entry
+  const uint8_t* entry;  // the batch's step cache entry
+  const uint8_t* blk;    // the batch's TOC1 block (its packed code stream is decoded in place)
+  double* loss;          // risk mode (toc_mlp_risk): per-row cross-entropy out, no backward pass
   int32_t m, h, k;
   double* W1;            // [m x h]
   double* b1;            // [h]
@@ -87,7 +87,6 @@ struct MlpStep {
 
 // The batch decoded into Ad: one thread per code walks its chain and stores each pair at (row,
 // column); the other buffer is zeroed meanwhile (it was read by the previous step).
-constexpr uint32_t kDecodeRowoff = 4096;  // rowoff entries kept in shared memory
 
 // Programmatic dependent launch (the step's kernels are launched with programmatic stream
 // serialization): a kernel waits for its predecessor's completion and memory only where it first
@@ -96,30 +95,53 @@ constexpr uint32_t kDecodeRowoff = 4096;  // rowoff entries kept in shared memor
 TOC_D void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 TOC_D void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
 
+constexpr uint32_t kDecodeUniq = 2048;  // value-index entries kept in shared memory
+
+constexpr uint32_t kDecodeRows = 1024;  // row offsets kept in shared memory
+
 __global__ void __launch_bounds__(kMlpThreads) mlp_decode_kernel(MlpStep s, uint32_t n) {
-  __shared__ uint32_t s_ro[kDecodeRowoff];
+  __shared__ uint32_t s_ro[kDecodeRows + 1];
+  __shared__ double s_uq[kDecodeUniq];
   const MlpEntry E = mlp_entry(s.entry);
-  const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
-  const bool ro_s = n < kDecodeRowoff;
+  const bool ro_s = n <= kDecodeRows, uq_s = E.nU <= kDecodeUniq;
   if (ro_s)
     for (uint32_t i = threadIdx.x; i <= n; i += blockDim.x) s_ro[i] = __ldg(E.rowoff + i);
+  if (uq_s)
+    for (uint32_t i = threadIdx.x; i < E.nU; i += blockDim.x) s_uq[i] = __ldg(E.uniq + i);
   __syncthreads();
-  const uint32_t C = __ldg(E.rowoff + n), m = (uint32_t)s.m;
-  for (int64_t j = gt; j < C; j += gs) {
-    uint32_t lo = 0, hi = n;  // row of code j: last r with rowoff[r] <= j
+  auto rowoff = [&](uint32_t r) { return ro_s ? s_ro[r] : __ldg(E.rowoff + r); };
+  const uint32_t C = E.n_codes, m = (uint32_t)s.m, nI = E.nI;
+  const uint8_t* codes = s.blk + E.off_codes;
+  // each CTA a contiguous range of codes, its threads consecutive codes: one row search per thread,
+  // then the row advances with the code index
+  const uint32_t per = (C + gridDim.x - 1) / gridDim.x, c0 = blockIdx.x * per, c1 = min(C, c0 + per);
+  uint32_t r = 0;
+  if (c0 + threadIdx.x < c1) {
+    uint32_t lo = 0, hi = n;  // row of the first code: last r with rowoff[r] <= j
     while (hi - lo > 1) {
       const uint32_t mid = (lo + hi) >> 1;
-      if ((ro_s ? s_ro[mid] : __ldg(E.rowoff + mid)) <= (uint32_t)j) lo = mid;
+      if (rowoff(mid) <= c0 + threadIdx.x) lo = mid;
       else hi = mid;
     }
-    double* row = s.Ad + (int64_t)lo * m;
-    uint32_t x = __ldg(E.codes + j);
-    while (x) {
-      const uint4 w = __ldg(E.nodes + x);
-      row[w.y] = __hiloint2double((int)w.w, (int)w.z);
-      x = w.x;
-    }
+    r = lo;
   }
+  for (uint32_t j = c0 + threadIdx.x; j < c1; j += blockDim.x) {
+    while (rowoff(r + 1) <= j) ++r;
+    double* row = s.Ad + (int64_t)r * m;
+    uint32_t x = ld_packed(codes, j, E.w_codes);  // the TOC1 code stream (physical.py:54-68)
+    while (x > nI) {  // the code's chain, last pair first: a derived node's own pair is its key
+      const uint32_t w = __ldg(E.nodes + x), pair = w >> 17;
+      TOC_CHECK(pair >= 1 && pair <= nI && (w & 0x1ffffu) >= 1 && (w & 0x1ffffu) < x);
+      const uint32_t pr = __ldg(E.pairs + pair);
+      row[pr & 0xffffu] = uq_s ? s_uq[pr >> 16] : __ldg(E.uniq + (pr >> 16));
+      x = w & 0x1ffffu;
+    }
+    TOC_CHECK(x >= 1);
+    const uint32_t pr = __ldg(E.pairs + x);
+    TOC_CHECK((pr & 0xffffu) < m && (pr >> 16) < E.nU);
+    row[pr & 0xffffu] = uq_s ? s_uq[pr >> 16] : __ldg(E.uniq + (pr >> 16));
+  }
+  const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, gs = (int64_t)gridDim.x * blockDim.x;
   // (the walks above only read the static cache and write this step's buffer, last read two steps
   // ago; the other buffer is still read by the previous step's kernels)
   pdl_wait();
@@ -246,6 +268,7 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_tail_kernel(MlpStep s, uint32
     const double e = (int)lane < K ? exp(mine - mx) : 0.0;
     const double se = warp_sum(e);
     const int y = (int)s.y[r];
+    if (s.loss && (int)lane == y) s.loss[r] = -((mine - mx) - log(se));  // risk mode: -log softmax[y]
     const double pr = e / se - ((int)lane == y ? 1.0 : 0.0);
     if ((int)lane < K) {
       s.P[(int64_t)r * K + lane] = pr;
@@ -266,6 +289,7 @@ __global__ void __launch_bounds__(kMlpThreads) mlp_tail_kernel(MlpStep s, uint32
       drow[j] = t;
     }
   }
+  if (s.loss) return;  // risk mode: no backward pass
   __syncthreads();
   const uint32_t pw = h * K + h + K;
   double* part = s.part + (int64_t)blockIdx.x * pw;
@@ -402,6 +426,7 @@ MlpScratch mlp_scratch_layout(int32_t nmax, int32_t m, int32_t h, int32_t k) {
 
 namespace {
 int32_t g_mlp_mask = 15;  // diagnostic: which of decode / right / tail / left launch (bits 0..3)
+int32_t g_mlp_decode_ctas = 8;  // decode CTAs per SM (tuning knob, toc_mlp_set_decode_ctas)
 bool g_mlp_graph = true;  // replay the epoch as one CUDA graph (built on the first call)
 
 // What a captured epoch depends on: every argument but the stream, plus a hash of the host arrays.
@@ -463,10 +488,11 @@ int mlp_attrs(int32_t h, int32_t k) {
 
 // Launches of steps [b0, b1) (decode buffers zeroed first when b0 == 0; a later b0 continues the
 // parity of the preceding call).  grad: gradient-only mode for a single step (see MlpStep).
-int mlp_enqueue(const uint8_t* d_cache, const int64_t* h_cache_off, const int64_t* h_row_base,
-                const int32_t* h_n_rows, int64_t b0, int64_t b1, int32_t nmax, int32_t m, int32_t h, int32_t k,
-                const double* d_labels, double* d_W1, double* d_b1, double* d_W2, double* d_b2, double lr,
-                int32_t dense, void* d_scratch, double* d_grad, cudaStream_t st) {
+int mlp_enqueue(const uint8_t* d_arena, const int64_t* h_block_off, const uint8_t* d_cache,
+                const int64_t* h_cache_off, const int64_t* h_row_base, const int32_t* h_n_rows, int64_t b0, int64_t b1,
+                int32_t nmax, int32_t m, int32_t h, int32_t k, const double* d_labels, double* d_W1, double* d_b1,
+                double* d_W2, double* d_b2, double lr, int32_t dense, void* d_scratch, double* d_grad, double* d_loss,
+                cudaStream_t st) {
     const MlpScratch SL = mlp_scratch_layout(nmax, m, h, k);
     const int smem_right = 8 * (int)toc::kRightWarps * toc::kRightMT * toc::kNT * 64;
     const int smem_left = 8 * 8 * toc::kLeftMT * toc::kNT * 64;
@@ -501,24 +527,35 @@ int mlp_enqueue(const uint8_t* d_cache, const int64_t* h_cache_off, const int64_
       const uint32_t n = (uint32_t)h_n_rows[b];
       if (n == 0) continue;
       s.entry = d_cache + h_cache_off[b];
+      s.blk = d_arena + h_block_off[b];
       s.y = d_labels + h_row_base[b];
+      s.loss = d_loss ? d_loss + h_row_base[b] : nullptr;
       s.step = lr / (double)n;
       s.Ad = adbuf[b & 1];
       s.Az = adbuf[(b + 1) & 1];
       const uint32_t n_tail = (n + toc::kTailRows - 1) / toc::kTailRows;
-      if (g_mlp_mask & 1) pdl_launch(toc::mlp_decode_kernel, dim3((unsigned)(8 * sms)), toc::kMlpThreads, 0, st, s, n);
+      if (g_mlp_mask & 1)
+        pdl_launch(toc::mlp_decode_kernel, dim3((unsigned)(g_mlp_decode_ctas * sms)), toc::kMlpThreads, 0, st, s, n);
       if (g_mlp_mask & 2)
         pdl_launch(toc::mlp_right_kernel<toc::kRightMT>,
                    dim3((n + 8 * toc::kRightMT - 1) / (8 * toc::kRightMT), ncb), 32 * toc::kRightWarps, smem_right, st,
                    s, n);
       if (g_mlp_mask & 4) pdl_launch(toc::mlp_tail_kernel<10>, dim3(n_tail), 32 * toc::kTailRows, smem_tail, st, s, n);
-      if (g_mlp_mask & 8)
+      if ((g_mlp_mask & 8) && !d_loss)
         pdl_launch(toc::mlp_left_kernel<toc::kLeftMT>, dim3(n_gemm_left + n_upd), toc::kMlpThreads, smem_left, st, s, n,
                    n_gemm_left, n_tail);
     }
     return cudaGetLastError() == cudaSuccess ? TOC_OK : TOC_E_CUDA;
 }
 }  // namespace
+
+extern "C" int toc_mlp_set_decode_ctas(int32_t per_sm) {
+  if (per_sm < 1 || per_sm > 32) return TOC_E_ARG;
+  g_mlp_decode_ctas = per_sm;
+  if (g_mlp_exec) cudaGraphExecDestroy(g_mlp_exec);  // the captured epoch depends on it
+  g_mlp_exec = nullptr;
+  return TOC_OK;
+}
 
 extern "C" int toc_mlp_set_kernels(int32_t mask) {
   g_mlp_mask = mask & 15;
@@ -546,11 +583,13 @@ extern "C" int toc_mlp_scratch(int32_t max_rows, int32_t m, int32_t h, int32_t k
 // One epoch: for each batch in order, the four kernels of the step.  h_cache_off / h_row_base /
 // h_n_rows are host copies (the launch loop reads them); d_labels holds class ids as f64.  dense:
 // every row has all m columns, so each decode overwrites the whole buffer and none is zeroed.
-extern "C" int toc_mlp_epoch(const uint8_t* d_cache, const int64_t* h_cache_off, const int64_t* h_row_base,
-                             const int32_t* h_n_rows, int64_t n_blocks, int32_t m, int32_t h, int32_t k,
-                             const double* d_labels, double* d_W1, double* d_b1, double* d_W2, double* d_b2, double lr,
-                             int32_t dense, void* d_scratch, int64_t scratch_bytes, void* stream) {
-  if (!d_cache || !h_cache_off || !h_row_base || !h_n_rows || n_blocks < 0 || m < 1 || h < 1 || k < 1 ||
+extern "C" int toc_mlp_epoch(const uint8_t* d_arena, const int64_t* h_block_off, const uint8_t* d_cache,
+                             const int64_t* h_cache_off, const int64_t* h_row_base, const int32_t* h_n_rows,
+                             int64_t n_blocks, int32_t m, int32_t h, int32_t k, const double* d_labels, double* d_W1,
+                             double* d_b1, double* d_W2, double* d_b2, double lr, int32_t dense, void* d_scratch,
+                             int64_t scratch_bytes, void* stream) {
+  if (!d_arena || !h_block_off || !d_cache || !h_cache_off || !h_row_base || !h_n_rows || n_blocks < 0 || m < 1 ||
+      h < 1 || k < 1 ||
       k > (int32_t)toc::kKMax || !d_labels || !d_W1 || !d_b1 || !d_W2 || !d_b2 || !d_scratch)
     return TOC_E_ARG;
   if (k != 10) return TOC_E_ARG;  // the tail kernel is instantiated for config 5's 10 classes
@@ -560,15 +599,16 @@ extern "C" int toc_mlp_epoch(const uint8_t* d_cache, const int64_t* h_cache_off,
   if (const int rc = mlp_attrs(h, k)) return rc;
   // the whole epoch's launches; enqueued directly, or captured once into a CUDA graph and replayed
   auto enqueue = [&](cudaStream_t st) -> int {
-    return mlp_enqueue(d_cache, h_cache_off, h_row_base, h_n_rows, 0, n_blocks, nmax, m, h, k, d_labels, d_W1, d_b1,
-                       d_W2, d_b2, lr, dense, d_scratch, nullptr, st);
+    return mlp_enqueue(d_arena, h_block_off, d_cache, h_cache_off, h_row_base, h_n_rows, 0, n_blocks, nmax, m, h, k,
+                       d_labels, d_W1, d_b1, d_W2, d_b2, lr, dense, d_scratch, nullptr, nullptr, st);
   };
   if (!g_mlp_graph) return enqueue((cudaStream_t)stream);
   MlpGraphKey key{d_cache, h_cache_off, h_row_base, h_n_rows, n_blocks, m, h, k, d_labels, d_W1, d_b1, d_W2, d_b2,
                   lr, dense, d_scratch, g_mlp_mask, 0};
+  key.hash = (uint64_t)(uintptr_t)d_arena;
   for (int64_t b = 0; b < n_blocks; ++b)
     key.hash = key.hash * 1099511628211ull ^ ((uint64_t)h_cache_off[b] * 31 + (uint64_t)h_row_base[b] * 7 +
-                                               (uint64_t)h_n_rows[b]);
+                                               (uint64_t)h_n_rows[b] + (uint64_t)h_block_off[b] * 131);
   if (!(g_mlp_exec && key == g_mlp_key)) {
     if (g_mlp_exec) cudaGraphExecDestroy(g_mlp_exec);
     g_mlp_exec = nullptr;
@@ -590,12 +630,14 @@ extern "C" int toc_mlp_epoch(const uint8_t* d_cache, const int64_t* h_cache_off,
   return cudaGraphLaunch(g_mlp_exec, (cudaStream_t)stream) == cudaSuccess ? TOC_OK : TOC_E_CUDA;
 }
 
-extern "C" int toc_mlp_step_grad(const uint8_t* d_cache, const int64_t* h_cache_off, const int64_t* h_row_base,
-                                 const int32_t* h_n_rows, int64_t n_blocks, int64_t step, int32_t m, int32_t h,
-                                 int32_t k, const double* d_labels, const double* d_W1, const double* d_b1,
-                                 const double* d_W2, const double* d_b2, int32_t dense, double* d_grad,
-                                 void* d_scratch, int64_t scratch_bytes, void* stream) {
-  if (!d_cache || !h_cache_off || !h_row_base || !h_n_rows || step < 0 || step >= n_blocks || m < 1 || h < 1 ||
+extern "C" int toc_mlp_step_grad(const uint8_t* d_arena, const int64_t* h_block_off, const uint8_t* d_cache,
+                                 const int64_t* h_cache_off, const int64_t* h_row_base, const int32_t* h_n_rows,
+                                 int64_t n_blocks, int64_t step, int32_t m, int32_t h, int32_t k,
+                                 const double* d_labels, const double* d_W1, const double* d_b1, const double* d_W2,
+                                 const double* d_b2, int32_t dense, double* d_grad, void* d_scratch,
+                                 int64_t scratch_bytes, void* stream) {
+  if (!d_arena || !h_block_off || !d_cache || !h_cache_off || !h_row_base || !h_n_rows || step < 0 ||
+      step >= n_blocks || m < 1 || h < 1 ||
       k != 10 || !d_labels || !d_W1 || !d_b1 || !d_W2 || !d_b2 || !d_grad || !d_scratch)
     return TOC_E_ARG;
   int32_t nmax = 0;
@@ -607,7 +649,26 @@ extern "C" int toc_mlp_step_grad(const uint8_t* d_cache, const int64_t* h_cache_
                    cudaSuccess
                ? TOC_OK
                : TOC_E_CUDA;
-  return mlp_enqueue(d_cache, h_cache_off, h_row_base, h_n_rows, step, step + 1, nmax, m, h, k, d_labels,
-                     const_cast<double*>(d_W1), const_cast<double*>(d_b1), const_cast<double*>(d_W2),
-                     const_cast<double*>(d_b2), 0.0, dense, d_scratch, d_grad, (cudaStream_t)stream);
+  return mlp_enqueue(d_arena, h_block_off, d_cache, h_cache_off, h_row_base, h_n_rows, step, step + 1, nmax, m, h, k,
+                     d_labels, const_cast<double*>(d_W1), const_cast<double*>(d_b1), const_cast<double*>(d_W2),
+                     const_cast<double*>(d_b2), 0.0, dense, d_scratch, d_grad, nullptr, (cudaStream_t)stream);
+}
+
+// The per-row cross-entropy of the current parameters over every batch (forward only: decode, A.W1
+// on the tensor cores with the ReLU epilogue, logits and -log softmax[y]); d_loss [rows].
+extern "C" int toc_mlp_risk(const uint8_t* d_arena, const int64_t* h_block_off, const uint8_t* d_cache,
+                            const int64_t* h_cache_off, const int64_t* h_row_base, const int32_t* h_n_rows,
+                            int64_t n_blocks, int32_t m, int32_t h, int32_t k, const double* d_labels,
+                            const double* d_W1, const double* d_b1, const double* d_W2, const double* d_b2,
+                            int32_t dense, double* d_loss, void* d_scratch, int64_t scratch_bytes, void* stream) {
+  if (!d_arena || !h_block_off || !d_cache || !h_cache_off || !h_row_base || !h_n_rows || n_blocks < 0 || m < 1 ||
+      h < 1 || k != 10 || !d_labels || !d_W1 || !d_b1 || !d_W2 || !d_b2 || !d_loss || !d_scratch)
+    return TOC_E_ARG;
+  int32_t nmax = 0;
+  for (int64_t b = 0; b < n_blocks; ++b) nmax = h_n_rows[b] > nmax ? h_n_rows[b] : nmax;
+  if (scratch_bytes < 8 * mlp_scratch_layout(nmax, m, h, k).total) return TOC_E_ARG;
+  if (const int rc = mlp_attrs(h, k)) return rc;
+  return mlp_enqueue(d_arena, h_block_off, d_cache, h_cache_off, h_row_base, h_n_rows, 0, n_blocks, nmax, m, h, k,
+                     d_labels, const_cast<double*>(d_W1), const_cast<double*>(d_b1), const_cast<double*>(d_W2),
+                     const_cast<double*>(d_b2), 0.0, dense, d_scratch, nullptr, d_loss, (cudaStream_t)stream);
 }

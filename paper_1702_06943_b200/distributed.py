@@ -437,9 +437,11 @@ def train_mlp_data_parallel(dataset, world: int, rank: int, hidden: int = 200, c
     lr = float(learning_rate)
     if batches is not None:
         a = batches.arena
-        a.build_matcache()
+        if not a.build_mlpcache():
+            raise ValueError("a batch's decode-tree ids do not fit the MLP step cache")
         nrows = np.ascontiguousarray(a.meta["n_rows"], np.int32)
-        cache_off = np.ascontiguousarray(a.matcache_off[:-1], np.int64)
+        cache_off = np.ascontiguousarray(a.mlpcache_off[:-1], np.int64)
+        block_off = np.ascontiguousarray(a.block_off, np.int64)
         row_base = np.ascontiguousarray(a.row_base, np.int64)
         labels = batches.labels.to(torch.float64).contiguous()
         lens = np.diff(np.asarray(sub.features.row_ptr))
@@ -455,7 +457,8 @@ def train_mlp_data_parallel(dataset, world: int, rank: int, hidden: int = 200, c
                 G.zero_()
             else:
                 N.check(L.toc_mlp_step_grad(
-                    a.matcache.data_ptr(), cache_off.ctypes.data, row_base.ctypes.data, nrows.ctypes.data,
+                    a.data.data_ptr(), block_off.ctypes.data, a.mlpcache.data_ptr(), cache_off.ctypes.data,
+                    row_base.ctypes.data, nrows.ctypes.data,
                     a.n_blocks, i, m, h, k, labels.data_ptr(), w1.data_ptr(), b1.data_ptr(), w2.data_ptr(),
                     b2.data_ptr(), dense, G.data_ptr(), scratch.data_ptr(), scratch.numel(), N.stream_handle()),
                     "toc_mlp_step_grad")

@@ -72,13 +72,17 @@ def init_mlp(n_in: int, hidden: int, classes: int, seed: int = 0):
 class _Net:
     """Device-resident batches + per-step first-layer products on them."""
 
-    def __init__(self, dataset: LabeledDataset, batch_size: int, seed: int):
+    def __init__(self, dataset: LabeledDataset, batch_size: int, seed: int, step_cache: bool = False):
         from .training import DeviceBatches, shuffle_once
 
         self.torch = N.require_cuda()
         self.batches = DeviceBatches(shuffle_once(dataset, seed), batch_size)
         self.arena = self.batches.arena
-        self.arena.build_matcache()  # node records once per run: both first-layer products read them
+        # once per run: the compact step cache the native epoch decodes from (with the TOC1 codes),
+        # else the node records both per-step first-layer products read
+        self.step_cache = step_cache and self.arena.build_mlpcache()
+        if not self.step_cache:
+            self.arena.build_matcache()
         self.rb = self.arena.row_base
         self.nrows = self.arena.meta["n_rows"].astype(np.int64)
         lens = np.diff(np.asarray(dataset.features.row_ptr))
@@ -134,11 +138,12 @@ def train_nn(dataset: LabeledDataset, config, counter=None):
 
 
 def _native_epoch(net, hidden: int, classes: int):
-    """toc_mlp_epoch's closure over the run's fixed buffers, or None where it does not apply (its tail
-    kernel is built for 10 classes and keeps W2 plus 8 rows in shared memory)."""
+    """toc_mlp_epoch's and toc_mlp_risk's closures over the run's fixed buffers, or None where they do
+    not apply (no step cache; the tail kernel is built for 10 classes and keeps W2 plus 8 rows in
+    shared memory)."""
     import ctypes
 
-    if classes != 10 or 8 * (hidden * classes + 9 * classes + 16 * hidden) > 200 * 1024:
+    if not net.step_cache or classes != 10 or 8 * (hidden * classes + 9 * classes + 16 * hidden) > 200 * 1024:
         return None
     torch = net.torch
     L = N.lib()
@@ -148,17 +153,28 @@ def _native_epoch(net, hidden: int, classes: int):
     N.check(L.toc_mlp_scratch(int(nrows.max(initial=0)), a.n_cols, hidden, classes, ctypes.byref(nb)),
             "toc_mlp_scratch")
     scratch = torch.empty(max(int(nb.value), 8), dtype=torch.uint8, device=a.data.device)
-    cache_off = np.ascontiguousarray(a.matcache_off[:-1], np.int64)
+    cache_off = np.ascontiguousarray(a.mlpcache_off[:-1], np.int64)
+    block_off = np.ascontiguousarray(a.block_off, np.int64)
     row_base = np.ascontiguousarray(net.rb, np.int64)
     labels = net.batches.labels.to(torch.float64).contiguous()
+    loss = torch.empty(max(int(nrows.sum()), 1), dtype=torch.float64, device=a.data.device)
 
     def run(w1, b1, w2, b2, lr):
-        N.check(L.toc_mlp_epoch(a.matcache.data_ptr(), cache_off.ctypes.data, row_base.ctypes.data, nrows.ctypes.data,
-                                a.n_blocks, a.n_cols, hidden, classes, labels.data_ptr(), w1.data_ptr(), b1.data_ptr(),
-                                w2.data_ptr(), b2.data_ptr(), lr, int(net.dense_rows), scratch.data_ptr(),
-                                scratch.numel(),
-                                N.stream_handle()), "toc_mlp_epoch")
+        N.check(L.toc_mlp_epoch(a.data.data_ptr(), block_off.ctypes.data, a.mlpcache.data_ptr(), cache_off.ctypes.data,
+                                row_base.ctypes.data, nrows.ctypes.data, a.n_blocks, a.n_cols, hidden, classes,
+                                labels.data_ptr(), w1.data_ptr(), b1.data_ptr(), w2.data_ptr(), b2.data_ptr(), lr,
+                                int(net.dense_rows), scratch.data_ptr(), scratch.numel(), N.stream_handle()),
+                "toc_mlp_epoch")
 
+    def risk(w1, b1, w2, b2):  # mean cross-entropy over every row (forward pass only)
+        N.check(L.toc_mlp_risk(a.data.data_ptr(), block_off.ctypes.data, a.mlpcache.data_ptr(), cache_off.ctypes.data,
+                               row_base.ctypes.data, nrows.ctypes.data, a.n_blocks, a.n_cols, hidden, classes,
+                               labels.data_ptr(), w1.data_ptr(), b1.data_ptr(), w2.data_ptr(), b2.data_ptr(),
+                               int(net.dense_rows), loss.data_ptr(), scratch.data_ptr(), scratch.numel(),
+                               N.stream_handle()), "toc_mlp_risk")
+        return float(loss[: int(nrows.sum())].mean().item())
+
+    run.risk = risk
     return run
 
 
@@ -171,13 +187,26 @@ def train_mlp(dataset: LabeledDataset, hidden: int = 200, classes: int = 10, bat
     torch ops for the dense tail).  Both compute the same step; results agree to fp64 rounding."""
     from .training import LossTrace
 
-    net = _Net(dataset, batch_size, seed)
+    net = _Net(dataset, batch_size, seed, step_cache=native)
     torch = net.torch
+    trace = LossTrace()
     w1, b1, w2, b2 = (torch.from_numpy(x).cuda() for x in init_mlp(dataset.n_cols, hidden, classes, seed))
     lr = float(learning_rate)
-    trace = LossTrace()
     labels_all = net.batches.labels.long()
     epoch_fn = _native_epoch(net, hidden, classes) if native else None
+    a = net.arena
+    if epoch_fn is not None:  # what the run keeps in HBM and what each step reads of it
+        meta = a.meta
+        codes = (meta["n_codes"].astype(np.int64) * meta["w_codes"].astype(np.int64)).sum()
+        entries = int(a.mlpcache_off[-1])
+        trace.memory = {"toc1_bytes": int(a.block_bytes), "step_cache_bytes": entries,
+                        "step_cache_over_toc1": entries / max(int(a.block_bytes), 1),
+                        "dense_bytes": 8 * int(meta["n_rows"].sum()) * a.n_cols,
+                        "decode_reads_per_step": float((codes + entries) / max(a.n_blocks, 1)),
+                        "note": "per step the decode reads the batch's TOC1 code stream and its step-cache entry "
+                                "(4-byte node records, pair records, value index)"}
+    if native and epoch_fn is None and net.step_cache:  # a shape the native step does not cover
+        net.arena.build_matcache()
 
     def forward(z1):
         a1 = torch.relu(z1 + b1)
@@ -206,7 +235,10 @@ def train_mlp(dataset: LabeledDataset, hidden: int = 200, classes: int = 10, bat
         end.record()
         end.synchronize()
         trace.seconds.append(start.elapsed_time(end) / 1e3)
-        _, logits = forward(net.arena.matmat(0, w1, hidden))
-        trace.risks.append(float(torch.nn.functional.cross_entropy(logits, labels_all).item()))
+        if epoch_fn is not None:
+            trace.risks.append(epoch_fn.risk(w1, b1, w2, b2))
+        else:
+            _, logits = forward(net.arena.matmat(0, w1, hidden))
+            trace.risks.append(float(torch.nn.functional.cross_entropy(logits, labels_all).item()))
     model = MlpModel(*(x.cpu().numpy() for x in (w1, b1, w2, b2)))
     return model, trace

@@ -178,26 +178,37 @@ def cfg5_teacher(n_in: int = 784, hidden: int = 200, classes: int = 10, seed: in
 
 
 def cfg5_batches(n_rows: int, seed: int = 5, batch: int = 250, n_cols: int = 784):
-    """BASELINE.json configs[4] (decision): rows "generated as in config 1" -- each
-    250-row batch from its own 32 templates over a 16-value Zipf(1.2) vocabulary U[-1,1] with 10%
-    mutation, widened to 784 columns -- and labels argmax of a random 784-200-10 ReLU teacher.
-    Yields (row_ptr, cols, vals, labels) per batch."""
+    """BASELINE.json configs[4] (decision): rows "generated as in config 1", widened to
+    784 columns -- ONE 16-value Zipf(1.2) vocabulary U[-1,1] and 32 template rows for the whole
+    dataset (config 1's recipe), each row a random template with 10% of its elements re-drawn --
+    and raw teacher logits of a random 784-200-10 ReLU MLP.  Rows are generated in chunks of
+    `batch` with their own seeded streams.  Yields (row_ptr, cols, vals, logits) per chunk."""
     W1, b1, W2 = cfg5_teacher(n_cols, seed=seed)
-    # each batch's teacher logits are centred per class so the classes come out near uniform
+    rng = np.random.default_rng(np.random.SeedSequence([seed, 0x7e]))
+    words = rng.uniform(-1.0, 1.0, 16)
+    p = _zipf_probs(16, 1.2)
+    templates = words[rng.choice(16, size=(32, n_cols), p=p)]
     for lo in range(0, n_rows, batch):
         k = min(batch, n_rows - lo)
-        A = cfg1_dense(seed=int(np.random.SeedSequence([seed, lo]).generate_state(1)[0]), n_rows=k, n_cols=n_cols)
+        r = np.random.default_rng(np.random.SeedSequence([seed, lo]))
+        A = templates[r.integers(0, 32, size=k)]
+        mask = r.random((k, n_cols)) < 0.1
+        A[mask] = words[r.choice(16, size=int(mask.sum()), p=p)]
         logits = np.maximum(A @ W1 + b1, 0.0) @ W2
         rp, c, v = dense_to_csr(A)
-        yield rp, c, v, np.argmax(logits - logits.mean(axis=0), axis=1).astype(np.float64)
+        yield rp, c, v, logits
 
 
 def cfg5_dataset(n_rows: int, seed: int = 5):
-    ptrs, cols, vals, labels, base = [np.zeros(1, np.int64)], [], [], [], 0
-    for rp, c, v, y in cfg5_batches(n_rows, seed):
+    """The config-5 rows (cfg5_batches) with labels argmax of the teacher logits centred per class
+    over the whole dataset (so the ten classes come out near uniform)."""
+    ptrs, cols, vals, logits, base = [np.zeros(1, np.int64)], [], [], [], 0
+    for rp, c, v, lg in cfg5_batches(n_rows, seed):
         ptrs.append(rp[1:] + base)
         base += int(rp[-1])
         cols.append(c)
         vals.append(v)
-        labels.append(y)
-    return np.concatenate(ptrs), np.concatenate(cols), np.concatenate(vals), np.concatenate(labels)
+        logits.append(lg)
+    lg = np.concatenate(logits) if logits else np.zeros((0, 10))
+    labels = np.argmax(lg - lg.mean(axis=0), axis=1).astype(np.float64)
+    return np.concatenate(ptrs), np.concatenate(cols), np.concatenate(vals), labels

@@ -25,4 +25,4 @@ t = time.time()
 model, trace = train_mlp(ds, epochs=a.epochs)
 tt = time.time() - t
 print(json.dumps({"rows": a.rows, "nnz": int(rp[-1]), "gen_s": tg, "train_wall_s": tt, "epoch_seconds": trace.seconds,
-                  "risks": trace.risks}))
+                  "risks": trace.risks, "memory": getattr(trace, "memory", None)}))

@@ -13,13 +13,25 @@ from paper_1702_06943_b200.matrix import LabeledDataset, SparseRowMatrix  # noqa
 rows = int(sys.argv[1]) if len(sys.argv) > 1 else 200_000
 rp, c, v, y = synth.cfg5_dataset(rows)
 ds = LabeledDataset(features=SparseRowMatrix.from_csr(784, rp, c, v, check=False), labels=y)
-net = mlp._Net(ds, 250, 0)
+net = mlp._Net(ds, 250, 0, step_cache=True)
 w1, b1, w2, b2 = (torch.from_numpy(x).cuda() for x in mlp.init_mlp(784, 200, 10, 0))
 run = mlp._native_epoch(net, 200, 10)
 L = N.lib()
 L.toc_mlp_set_kernels.argtypes = [ctypes.c_int32]
 L.toc_mlp_set_graph.argtypes = [ctypes.c_int32]
 steps = net.arena.n_blocks
+L.toc_mlp_set_decode_ctas.argtypes = [ctypes.c_int32]
+for dc in [int(x) for x in os.environ.get("DECODE_CTAS", "").split(",") if x]:
+    N.check(L.toc_mlp_set_decode_ctas(dc), "decode ctas")
+    L.toc_mlp_set_kernels(15)
+    run(w1, b1, w2, b2, 0.0)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    run(w1, b1, w2, b2, 0.0)
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"decode ctas/SM {dc:2d}: all {e0.elapsed_time(e1) * 1000 / steps:7.2f} us/step", flush=True)
 for graph in (0, 1):
     L.toc_mlp_set_graph(graph)
     for name, mask in [("all", 15), ("decode", 1), ("right", 2), ("tail", 4), ("left", 8), ("none", 0)]:
