@@ -451,6 +451,7 @@ int toc_mlp_set_kernels(int32_t mask);
 int toc_mlp_set_graph(int32_t on);
 int toc_mlp_set_pdl(int32_t on); /* tuning knob: programmatic dependent launch of the step kernels (default 1) */
 int toc_mlp_set_decode_ctas(int32_t per_sm); /* tuning knob: decode CTAs per SM (1..32, default 8) */
+int toc_mlp_set_fused(int32_t on); /* 1 (default): A.W1 and the softmax tail as one cluster kernel; 0: two kernels */
 int toc_mlp_scratch(int32_t max_rows, int32_t m, int32_t h, int32_t k, int64_t* bytes);
 int toc_mlp_epoch(const uint8_t* d_arena, const int64_t* h_block_off, const uint8_t* d_cache,
                   const int64_t* h_cache_off, const int64_t* h_row_base, const int32_t* h_n_rows, int64_t n_blocks,

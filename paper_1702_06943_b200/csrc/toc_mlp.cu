@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "toc_batch.cuh"
+#include "toc_images.cuh"  // cluster barrier / rank / DSMEM load helpers
 
 namespace toc {
 
@@ -221,6 +222,146 @@ __global__ void __launch_bounds__(32 * kRightWarps) mlp_right_kernel(MlpStep s, 
     const uint32_t r = r0 + row, col = n0 + c;
     if (r < n && col < h) A1[(int64_t)r * h + col] = fmax(z + b1[col], 0.0);
   });
+}
+
+// mlp_right with the tail fused in: a thread-block cluster of the ncb CTAs that share a row tile
+// (one per 40 hidden units).  Each CTA computes its A1 tile as mlp_right does, then the partial
+// logits of its units, A1_tile . W2[units]; after a cluster barrier every CTA sums the ncb partials
+// over DSMEM in rank order (identical in every CTA), adds b2 and forms P = softmax - onehot for the
+// tile's rows; then delta = (P W2^T) * [A1 > 0] for its own units and its parts of the W2 / b1 / b2
+// gradients (sums over the tile's rows in row order; the P sums by rank 0), laid out as the tail's
+// parts, one per row tile.  Risk mode: rank 0 writes each row's -log softmax[y] instead.
+template <int MT, int K>
+__global__ void __launch_bounds__(32 * kRightWarps) mlp_right_tail_kernel(MlpStep s, uint32_t n) {
+  extern __shared__ __align__(16) double red[];
+  constexpr uint32_t RT = 8 * MT, NU = 8 * kNT;
+  double* a1s = red + kRightWarps * MT * kNT * 64;  // [RT][NU] this CTA's A1 tile
+  double* lgp = a1s + RT * NU;                      // [RT][K] its partial logits (read by the cluster)
+  double* ps = lgp + RT * K;                        // [RT][K] P = softmax - onehot
+  double* w2s = ps + RT * K;                        // [NU][K] its rows of W2
+  pdl_wait();  // the decoded batch, and the parameters as the previous step left them
+  pdl_trigger();
+  const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, tq = lane & 3;
+  const uint32_t m = (uint32_t)s.m, h = (uint32_t)s.h;
+  const uint32_t r0 = blockIdx.x * RT, n0 = blockIdx.y * NU, rank = cluster_rank(), C = gridDim.y;
+  double acc[MT][kNT][2];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (uint32_t t = 0; t < kNT; ++t) acc[mt][t][0] = acc[mt][t][1] = 0.0;
+  const uint32_t ksteps = (m + 3) >> 2, ks0 = warp * ksteps / kRightWarps, ks1 = (warp + 1) * ksteps / kRightWarps;
+  const double* W1 = s.W1;
+  const double* Ad = s.Ad;
+  constexpr uint32_t G = 4;  // k-steps per group: all their fragments loaded before their DMMAs
+  for (uint32_t k0 = ks0; k0 < ks1; k0 += G) {
+    double a[G][MT], b[G][kNT];
+#pragma unroll
+    for (uint32_t u = 0; u < G; ++u) {
+      const uint32_t kr = (k0 + u) * 4 + tq;
+      const bool kin = k0 + u < ks1 && kr < m;
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt) {
+        const uint32_t r = r0 + mt * 8 + g;
+        a[u][mt] = (kin && r < n) ? Ad[(int64_t)r * m + kr] : 0.0;
+      }
+#pragma unroll
+      for (uint32_t t = 0; t < kNT; ++t) {
+        const uint32_t col = n0 + t * 8 + g;
+        b[u][t] = (kin && col < h) ? W1[(int64_t)kr * h + col] : 0.0;
+      }
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < G; ++u)
+#pragma unroll
+      for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+        for (uint32_t t = 0; t < kNT; ++t) dmma(acc[mt][t], a[u][mt], b[u][t]);
+  }
+  const double* b1 = s.b1;
+  const double* W2 = s.W2;
+  double* A1 = s.A1;
+  for (uint32_t e = tid; e < NU * K; e += blockDim.x) {
+    const uint32_t col = n0 + e / K;
+    w2s[e] = col < h ? W2[(int64_t)col * K + e % K] : 0.0;
+  }
+  reduce_warps<MT, kRightWarps>(acc, red, [&](uint32_t row, uint32_t c, double z) {
+    const uint32_t r = r0 + row, col = n0 + c;
+    double a = 0.0;
+    if (r < n && col < h) {
+      a = fmax(z + b1[col], 0.0);
+      A1[(int64_t)r * h + col] = a;
+    }
+    a1s[row * NU + c] = a;
+  });
+  __syncthreads();
+  for (uint32_t e = tid; e < RT * K; e += blockDim.x) {  // partial logits of this CTA's units
+    const uint32_t r = e / K, c = e % K;
+    double t = 0.0;
+    for (uint32_t u = 0; u < NU; ++u) t = fma(a1s[r * NU + u], w2s[u * K + c], t);
+    lgp[e] = t;
+  }
+  cluster_barrier();  // every CTA's partial logits are visible
+  double* lgs = ps;  // [RT][K] the logits (P overwrites them row by row below, after a barrier)
+  for (uint32_t e = tid; e < RT * K; e += blockDim.x) {  // logits: the C partials in rank order, + b2
+    double v[8];
+#pragma unroll
+    for (uint32_t q = 0; q < 8; ++q) v[q] = q < C ? ld_dsmem(lgp + e, q) : 0.0;  // all in flight
+    double t = 0.0;
+#pragma unroll
+    for (uint32_t q = 0; q < 8; ++q) t += v[q];
+    lgs[e] = t + __ldg(s.b2 + e % K);
+  }
+  __syncthreads();
+  double pv = 0.0;
+  const uint32_t pr = tid / K, pc = tid % K, prow = r0 + pr;
+  if (tid < RT * K) {  // P = softmax - onehot for (row, class) = (pr, pc)
+    double mx = -INFINITY, se = 0.0;
+#pragma unroll
+    for (int c = 0; c < K; ++c) mx = fmax(mx, lgs[pr * K + c]);
+#pragma unroll
+    for (int c = 0; c < K; ++c) se += exp(lgs[pr * K + c] - mx);
+    const int y = prow < n ? (int)s.y[prow] : -1;
+    pv = prow < n ? exp(lgs[tid] - mx) / se - ((int)pc == y ? 1.0 : 0.0) : 0.0;
+    if (s.loss && prow < n && rank == 0 && (int)pc == y) s.loss[prow] = -((lgs[tid] - mx) - log(se));
+  }
+  __syncthreads();
+  if (tid < RT * K) ps[tid] = pv;
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");  // done reading the others' partials
+  __syncthreads();
+  if (!s.loss) {
+    double* dsm = red;  // [RT][NU] delta (the reduction buffer is free)
+    for (uint32_t e = tid; e < RT * NU; e += blockDim.x) {  // delta = (P W2^T) * [A1 > 0], own units
+      const uint32_t r = e / NU, u = e % NU, row = r0 + r, col = n0 + u;
+      double t = 0.0;
+#pragma unroll
+      for (int c = 0; c < K; ++c) t = fma(ps[r * K + c], w2s[u * K + c], t);
+      t = a1s[e] > 0.0 ? t : 0.0;
+      dsm[e] = t;
+      if (row < n && col < h) s.D[(int64_t)row * h + col] = t;
+    }
+    __syncthreads();
+    const uint32_t pw = h * K + h + K;
+    double* part = s.part + (int64_t)blockIdx.x * pw;
+    for (uint32_t e = tid; e < NU * K + NU + K; e += blockDim.x) {
+      double t = 0.0;
+      if (e < NU * K) {  // A1^T P over the tile's rows, own units
+        const uint32_t u = e / K, c = e % K;
+        if (n0 + u >= h) continue;
+        for (uint32_t r = 0; r < RT; ++r) t = fma(a1s[r * NU + u], ps[r * K + c], t);
+        part[(n0 + u) * K + c] = t;
+      } else if (e < NU * K + NU) {  // delta sums, own units
+        const uint32_t u = e - NU * K;
+        if (n0 + u >= h) continue;
+        for (uint32_t r = 0; r < RT; ++r) t += dsm[r * NU + u];
+        part[h * K + n0 + u] = t;
+      } else if (rank == 0) {  // P sums
+        const uint32_t c = e - NU * K - NU;
+        for (uint32_t r = 0; r < RT; ++r) t += ps[r * K + c];
+        part[h * K + h + c] = t;
+      }
+    }
+  }
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");  // my partials may now go
 }
 
 // Per row (one warp, 8 rows per CTA): logits = A1 W2 + b2, P = softmax - onehot, delta = (P W2^T) *
@@ -427,6 +568,7 @@ MlpScratch mlp_scratch_layout(int32_t nmax, int32_t m, int32_t h, int32_t k) {
 namespace {
 int32_t g_mlp_mask = 15;  // diagnostic: which of decode / right / tail / left launch (bits 0..3)
 int32_t g_mlp_decode_ctas = 8;  // decode CTAs per SM (tuning knob, toc_mlp_set_decode_ctas)
+bool g_mlp_fuse = true;  // right + tail as one cluster kernel (mlp_right_tail_kernel) where it applies
 bool g_mlp_graph = true;  // replay the epoch as one CUDA graph (built on the first call)
 
 // What a captured epoch depends on: every argument but the stream, plus a hash of the host arrays.
@@ -470,6 +612,31 @@ void pdl_launch(void (*fn)(KArgs...), dim3 grid, uint32_t block, int smem, cudaS
   cudaLaunchKernelEx(&cfg, fn, static_cast<KArgs>(args)...);
 }
 
+// The same with a (1, cy, 1) thread-block cluster.
+template <typename... KArgs, typename... Args>
+void pdl_launch_cluster(void (*fn)(KArgs...), dim3 grid, uint32_t cy, uint32_t block, int smem, cudaStream_t st,
+                        Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = cy;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = g_mlp_pdl ? 2 : 1;
+  cudaLaunchKernelEx(&cfg, fn, static_cast<KArgs>(args)...);
+}
+
+constexpr int kFusedSmem = 8 * ((int)toc::kRightWarps * toc::kRightMT * toc::kNT * 64 +
+                                (8 * toc::kRightMT) * (8 * toc::kNT) + 2 * (8 * toc::kRightMT) * 10 +
+                                (8 * toc::kNT) * 10);
+
 // Dynamic shared memory of the three GEMM-shaped kernels (set once per process).
 int mlp_attrs(int32_t h, int32_t k) {
   const int smem_right = 8 * (int)toc::kRightWarps * toc::kRightMT * toc::kNT * 64;
@@ -478,6 +645,8 @@ int mlp_attrs(int32_t h, int32_t k) {
   if (smem_tail > 200 * 1024) return TOC_E_ARG;
   if (cudaFuncSetAttribute(toc::mlp_right_kernel<toc::kRightMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            smem_right) != cudaSuccess ||
+      cudaFuncSetAttribute(toc::mlp_right_tail_kernel<toc::kRightMT, 10>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kFusedSmem) != cudaSuccess ||
       cudaFuncSetAttribute(toc::mlp_tail_kernel<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tail) !=
           cudaSuccess ||
       cudaFuncSetAttribute(toc::mlp_left_kernel<toc::kLeftMT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -533,14 +702,19 @@ int mlp_enqueue(const uint8_t* d_arena, const int64_t* h_block_off, const uint8_
       s.step = lr / (double)n;
       s.Ad = adbuf[b & 1];
       s.Az = adbuf[(b + 1) & 1];
-      const uint32_t n_tail = (n + toc::kTailRows - 1) / toc::kTailRows;
+      const uint32_t row_tiles = (n + 8 * toc::kRightMT - 1) / (8 * toc::kRightMT);
+      const bool fused = g_mlp_fuse && k == 10 && ncb <= 8;  // parts: one per row tile
+      const uint32_t n_tail = fused ? row_tiles : (n + toc::kTailRows - 1) / toc::kTailRows;
       if (g_mlp_mask & 1)
         pdl_launch(toc::mlp_decode_kernel, dim3((unsigned)(g_mlp_decode_ctas * sms)), toc::kMlpThreads, 0, st, s, n);
-      if (g_mlp_mask & 2)
-        pdl_launch(toc::mlp_right_kernel<toc::kRightMT>,
-                   dim3((n + 8 * toc::kRightMT - 1) / (8 * toc::kRightMT), ncb), 32 * toc::kRightWarps, smem_right, st,
+      if ((g_mlp_mask & 2) && fused)
+        pdl_launch_cluster(toc::mlp_right_tail_kernel<toc::kRightMT, 10>, dim3(row_tiles, ncb), ncb,
+                           32 * toc::kRightWarps, kFusedSmem, st, s, n);
+      if ((g_mlp_mask & 2) && !fused)
+        pdl_launch(toc::mlp_right_kernel<toc::kRightMT>, dim3(row_tiles, ncb), 32 * toc::kRightWarps, smem_right, st,
                    s, n);
-      if (g_mlp_mask & 4) pdl_launch(toc::mlp_tail_kernel<10>, dim3(n_tail), 32 * toc::kTailRows, smem_tail, st, s, n);
+      if ((g_mlp_mask & 4) && !fused)
+        pdl_launch(toc::mlp_tail_kernel<10>, dim3(n_tail), 32 * toc::kTailRows, smem_tail, st, s, n);
       if ((g_mlp_mask & 8) && !d_loss)
         pdl_launch(toc::mlp_left_kernel<toc::kLeftMT>, dim3(n_gemm_left + n_upd), toc::kMlpThreads, smem_left, st, s, n,
                    n_gemm_left, n_tail);
@@ -548,6 +722,13 @@ int mlp_enqueue(const uint8_t* d_arena, const int64_t* h_block_off, const uint8_
     return cudaGetLastError() == cudaSuccess ? TOC_OK : TOC_E_CUDA;
 }
 }  // namespace
+
+extern "C" int toc_mlp_set_fused(int32_t on) {
+  g_mlp_fuse = on != 0;
+  if (g_mlp_exec) cudaGraphExecDestroy(g_mlp_exec);  // the captured epoch depends on it
+  g_mlp_exec = nullptr;
+  return TOC_OK;
+}
 
 extern "C" int toc_mlp_set_decode_ctas(int32_t per_sm) {
   if (per_sm < 1 || per_sm > 32) return TOC_E_ARG;

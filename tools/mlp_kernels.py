@@ -21,6 +21,18 @@ L.toc_mlp_set_kernels.argtypes = [ctypes.c_int32]
 L.toc_mlp_set_graph.argtypes = [ctypes.c_int32]
 steps = net.arena.n_blocks
 L.toc_mlp_set_decode_ctas.argtypes = [ctypes.c_int32]
+L.toc_mlp_set_fused.argtypes = [ctypes.c_int32]
+for fz in (0, 1):
+    L.toc_mlp_set_fused(fz)
+    L.toc_mlp_set_kernels(15)
+    run(w1, b1, w2, b2, 0.0)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    run(w1, b1, w2, b2, 0.0)
+    e1.record()
+    torch.cuda.synchronize()
+    print(f"fused {fz}: all {e0.elapsed_time(e1) * 1000 / steps:7.2f} us/step", flush=True)
 for dc in [int(x) for x in os.environ.get("DECODE_CTAS", "").split(",") if x]:
     N.check(L.toc_mlp_set_decode_ctas(dc), "decode ctas")
     L.toc_mlp_set_kernels(15)
