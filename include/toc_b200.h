@@ -329,10 +329,6 @@ int toc_glm_epoch_parts(const uint8_t* d_images, const int64_t* d_part_off, cons
                         const int32_t* h_counts, int64_t n_blocks, int32_t n_cols, int32_t cluster,
                         int32_t loss, double lr, double* d_w, unsigned long long* d_gacc, int64_t max_part,
                         void* stream);
-/* A-B knob: 1 runs toc_glm_epoch_parts on the DSMEM epoch kernel (weights and the gradient exchange
- * in distributed shared memory; bit-identical results) when it fits, 0 (default) the global-memory
- * kernel, which measured faster at config 4 (10.4 vs 12.3 us/step). */
-int toc_mgd_set_parts_dsmem(int32_t on);
 
 /* The largest power-of-two cluster (<= 16; sizes above 8 are non-portable) this device co-schedules
  * for the part-image epoch with a full shared-memory carve-out per CTA, into *cluster.  The part
@@ -492,7 +488,10 @@ int toc_tree_arrays(const uint8_t* d_arena, const int64_t* d_block_off, const To
 
 /* ---- the batched public sweep's pipeline (kernels.BatchSweep; reference cli.py:299-383) --------
  * One chunk of the sweep: its byte range in the host and device block buffers, its indexed view
- * (offsets relative to d_arena; rows relative to the chunk) and its plan / scratch. */
+ * (offsets relative to d_arena; rows relative to the chunk), its plan / scratch, and the chunk's
+ * own CUDA events (upload done, operands done, compute done; toc_sweep_events creates them,
+ * toc_sweep_events_free destroys them) -- per-sweep state, so sweeps on several threads or devices
+ * do not share events. */
 typedef struct TocSweepChunk {
   int64_t byte_lo, byte_hi;
   const uint8_t* d_arena;
@@ -503,7 +502,12 @@ typedef struct TocSweepChunk {
   void* d_scratch;
   int64_t n_blocks, b0, row0, n_rows;
   TocPlan plan;
-} TocSweepChunk; /* 136 bytes */
+  void* ev_upload;
+  void* ev_operands;
+  void* ev_done;
+} TocSweepChunk; /* 160 bytes */
+int toc_sweep_events(TocSweepChunk* chunks, int64_t n_chunks);
+int toc_sweep_events_free(TocSweepChunk* chunks, int64_t n_chunks);
 
 /* Enqueue the block bytes of chunks [k0, k1) host -> device on copy_stream (pinned h_blocks). */
 int toc_sweep_upload(const uint8_t* h_blocks, uint8_t* d_blocks, const TocSweepChunk* chunks, int64_t k0,
@@ -518,7 +522,7 @@ int toc_sweep_operands(const TocSweepChunk* chunks, int64_t n_chunks, int32_t n_
 int toc_sweep_compute(const TocSweepChunk* chunks, int64_t n_chunks, int32_t n_cols, const double* d_v,
                       const double* d_u, double* d_R, double* h_R, double* d_O, double* h_O,
                       TocBlockMeta* h_meta, void* compute_stream, void* d2h_stream);
-int toc_sizeof_sweep_chunk(void); /* 136 */
+int toc_sizeof_sweep_chunk(void); /* 160 */
 /* Diagnostic: record timed events in later runs; toc_sweep_timeline reads chunk k's upload end,
  * validation start / end, compute end and download end (out[5k..5k+4], ms from the first upload)
  * after a synchronized run. */

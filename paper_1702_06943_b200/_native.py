@@ -45,7 +45,8 @@ class TocSweepChunk(ctypes.Structure):
     _fields_ = [("byte_lo", ctypes.c_int64), ("byte_hi", ctypes.c_int64), ("d_arena", ctypes.c_void_p),
                 ("d_block_off", ctypes.c_void_p), ("d_block_len", ctypes.c_void_p), ("d_meta", ctypes.c_void_p),
                 ("d_row_base", ctypes.c_void_p), ("d_scratch", ctypes.c_void_p), ("n_blocks", ctypes.c_int64),
-                ("b0", ctypes.c_int64), ("row0", ctypes.c_int64), ("n_rows", ctypes.c_int64), ("plan", TocPlan)]
+                ("b0", ctypes.c_int64), ("row0", ctypes.c_int64), ("n_rows", ctypes.c_int64), ("plan", TocPlan),
+                ("ev_upload", ctypes.c_void_p), ("ev_operands", ctypes.c_void_p), ("ev_done", ctypes.c_void_p)]
 
 
 class NativeError(RuntimeError):
@@ -81,6 +82,8 @@ def lib():
     L.toc_decode_counts.argtypes = [P, P, P, P, I64, ctypes.POINTER(TocPlan), P, P, P]
     L.toc_decode_rows.argtypes = [P, P, P, P, I64, ctypes.POINTER(TocPlan), P, P, P, P, P]
     L.toc_sweep_upload.argtypes = [P, P, P, I64, I64, P]
+    L.toc_sweep_events.argtypes = [P, I64]
+    L.toc_sweep_events_free.argtypes = [P, I64]
     L.toc_sweep_operands.argtypes = [P, I64, I32, P, P, P, P, P]
     L.toc_sweep_compute.argtypes = [P, I64, I32, P, P, P, P, P, P, P, P, P]
     L.toc_linalg32.argtypes = [P, P, P, P, I64, ctypes.POINTER(TocPlan), I32, P, P, P, P, P, P, P]

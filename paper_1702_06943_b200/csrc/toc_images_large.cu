@@ -31,12 +31,8 @@ constexpr uint32_t kMaxPartsCluster = 16;
 // byte offset of the same CTA's part of the NEXT batch relative to this part, u32 at 48: its bytes.
 constexpr uint32_t kPartHeader = 64;
 
-// After the labels, for the DSMEM epoch (epoch_dsmem_kernel): each local pair's slot in the
-// part's owner-grouped bucket array (u16), the C buckets (first slot | count << 16), and each slot's
-// index in its owner's sorted own list (u16; read from global memory by the owner).
 struct PartLayout {
-  uint32_t off_rowoff, off_codes, off_nodes, off_pcol, off_pval, off_own, off_labels, off_bslot, off_bkt, off_bown,
-      total;
+  uint32_t off_rowoff, off_codes, off_nodes, off_pcol, off_pval, off_own, off_labels, total;
 };
 
 TOC_HD PartLayout part_layout(uint32_t nr, uint32_t nP, uint32_t nD, uint32_t nC, uint32_t n_own, uint32_t C) {
@@ -56,12 +52,6 @@ TOC_HD PartLayout part_layout(uint32_t nr, uint32_t nP, uint32_t nD, uint32_t nC
   o += align16(4u * n_own);
   L.off_labels = o;
   o += align16(8u * nr);
-  L.off_bslot = o;
-  o += align16(2u * nP);
-  L.off_bkt = o;
-  o += align16(4u * C);
-  L.off_bown = o;
-  o += align16(2u * nP);
   L.total = o;
   return L;
 }
@@ -262,26 +252,6 @@ __global__ void __launch_bounds__(1024, 1) large_image_kernel(LargeArgs a) {
           nodes[l] = make_uint2(lid(par), lid(key));
         }
       }
-      __syncthreads();  // pcol complete
-      if (tid == 0) {  // owner-grouped bucket slots of the local pairs (stable by local pair id)
-        uint16_t* bslot = reinterpret_cast<uint16_t*>(img + L.off_bslot);
-        uint32_t* bkt = reinterpret_cast<uint32_t*>(img + L.off_bkt);
-        uint16_t* bown = reinterpret_cast<uint16_t*>(img + L.off_bown);
-        uint32_t cnt[kMaxPartsCluster], st[kMaxPartsCluster];
-        for (uint32_t o = 0; o < C; ++o) cnt[o] = 0u;
-        for (uint32_t l = 0; l < nP; ++l) ++cnt[__ldcg(pcol + l) % C];
-        uint32_t acc = 0;
-        for (uint32_t o = 0; o < C; ++o) {
-          st[o] = acc;
-          bkt[o] = acc | (cnt[o] << 16);
-          acc += cnt[o];
-        }
-        for (uint32_t l = 0; l < nP; ++l) {
-          const uint32_t col = __ldcg(pcol + l), slot = st[col % C]++;
-          bslot[l] = (uint16_t)slot;
-          bown[slot] = (uint16_t)own_rank(col);
-        }
-      }
       if (tid == 0) {
         uint32_t* h = reinterpret_cast<uint32_t*>(img);
         h[0] = r1 - r0;
@@ -456,183 +426,6 @@ __global__ void __launch_bounds__(1024, 1) epoch_large_kernel(LargeEpochArgs a) 
 }
 
 
-// Load a 64-bit integer from CTA `rank`'s shared memory at the offset of `p` in this CTA.
-TOC_D unsigned long long ld_dsmem_u64(const unsigned long long* p, uint32_t rank) {
-  uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(p)), "r"(rank));
-  unsigned long long v;
-  asm volatile("ld.shared::cluster.u64 %0, [%1];" : "=l"(v) : "r"(remote) : "memory");
-  return v;
-}
-
-struct DsmemEpochArgs {
-  const uint8_t* images;
-  const int64_t* part_off;  // [n_blocks * C + 1]
-  int64_t n_blocks;
-  int32_t n_cols, loss, cluster;
-  double lr;
-  double* w;  // n_cols, global: read at the start, written at the end
-  uint32_t max_part, max_pairs, max_rows, max_own, w_slots;
-};
-
-// One epoch on a cluster of C CTAs with the weights and the gradient exchange in distributed
-// shared memory: CTA c owns the columns col = c (mod C), kept at ws[col / C] in its shared memory.
-// Per step each CTA computes P1 for its pairs from the owners' weights (DSMEM reads), A.w, s and
-// G on its rows exactly as epoch_large_kernel does, writes each pair's fixed-point contribution
-// value * G into its own bucket array grouped by owner column; cluster barrier (shared-memory data
-// only: no GPU-scope fence); each owner pulls its buckets from every CTA (DSMEM), adds them per own
-// column (integer adds: exact, order-independent -- bit-identical to the global RED.ADD.U64 sums of
-// epoch_large_kernel) and applies w -= (lr/|B|) g to its columns; cluster barrier.  One part buffer
-// (the weights take the second's room): the next part's copy starts once this CTA's update is done.
-// Shared memory: fixed | ws | own gradient | P1 / buckets | G lo | G hi | s | part buffer.
-__global__ void __launch_bounds__(1024, 1) epoch_dsmem_kernel(DsmemEpochArgs a) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + 448);
-  const uint32_t cta = cluster_rank(), C = (uint32_t)a.cluster;
-  const uint32_t tid = threadIdx.x, nth = blockDim.x, m = (uint32_t)a.n_cols;
-  uint8_t* p = smem + kFixedBytes;
-  double* ws = reinterpret_cast<double*>(p);
-  p += align16(8u * a.w_slots);
-  uint32_t* glo_own = reinterpret_cast<uint32_t*>(p);  // own-column gradient, 64-bit fixed point in
-  p += align16(4u * a.max_own);                        // two words (exact split-word adds, fix_add_pair)
-  uint32_t* ghi_own = reinterpret_cast<uint32_t*>(p);
-  p += align16(4u * a.max_own);
-  __shared__ uint32_t s_k0[kMaxPartsCluster], s_k1[kMaxPartsCluster];
-  __shared__ const uint16_t* s_bown[kMaxPartsCluster];
-  double* p1 = reinterpret_cast<double*>(p);
-  unsigned long long* bucket = reinterpret_cast<unsigned long long*>(p);  // aliases P1 (dead by then)
-  p += align16(8u * (a.max_pairs + 1));
-  uint32_t* glo = reinterpret_cast<uint32_t*>(p);
-  p += align16(4u * (a.max_pairs + 1));
-  uint32_t* ghi = reinterpret_cast<uint32_t*>(p);
-  p += align16(4u * (a.max_pairs + 1));
-  double* srow = reinterpret_cast<double*>(p);
-  p += align16(8u * a.max_rows);
-  uint8_t* buf = p;
-  for (uint32_t j = tid; j < a.w_slots; j += nth) {
-    const uint32_t col = j * C + cta;
-    ws[j] = col < m ? a.w[col] : 0.0;
-  }
-  for (uint32_t j = tid; j < a.max_own; j += nth) glo_own[j] = ghi_own[j] = 0u;
-  const uint8_t* src = a.images + a.part_off[cta];  // thread 0: global address of the current part
-  if (tid == 0) {
-    mbar_init(&mbar[0], 1);
-    const uint32_t bytes = (uint32_t)(a.part_off[cta + 1] - a.part_off[cta]);
-    TOC_CHECK(bytes <= a.max_part);
-    mbar_expect(&mbar[0], bytes);
-    bulk_copy(buf, src, bytes, &mbar[0]);
-  }
-  cluster_barrier();  // every CTA's weights are in place before any remote read
-  uint32_t step_n = 0;
-  double step = 0.0;
-  for (int64_t t = 0; t < a.n_blocks; ++t) {
-    mbar_wait_bounded(&mbar[0], (uint32_t)t & 1u);
-    const uint8_t* img = buf;
-    const uint32_t* h = reinterpret_cast<const uint32_t*>(img);
-    const uint32_t nr = h[0], nP = h[1], nD = h[2], nC = h[3], n_own = h[4], n = h[5];
-    const double ysum = reinterpret_cast<const double*>(img)[3], vmax = reinterpret_cast<const double*>(img)[4];
-    const int64_t next_d = *reinterpret_cast<const int64_t*>(img + 40);
-    const uint32_t next_bytes = h[12];
-    const PartLayout L = part_layout(nr, nP, nD, nC, n_own, C);
-    const uint32_t* rowoff = reinterpret_cast<const uint32_t*>(img + L.off_rowoff);
-    Nodes<true> N;
-    N.codes = reinterpret_cast<const uint32_t*>(img + L.off_codes);
-    N.p = reinterpret_cast<const uint2*>(img + L.off_nodes);
-    const uint32_t* pcol = reinterpret_cast<const uint32_t*>(img + L.off_pcol);
-    const double* pval = reinterpret_cast<const double*>(img + L.off_pval);
-    const uint32_t* own = reinterpret_cast<const uint32_t*>(img + L.off_own);
-    const double* y = reinterpret_cast<const double*>(img + L.off_labels);
-    const uint16_t* bslot = reinterpret_cast<const uint16_t*>(img + L.off_bslot);
-    if (n != step_n) {
-      step = a.lr / (double)n;
-      step_n = n;
-    }
-    // P1 for this CTA's pairs from the owners' weights (DSMEM)
-#pragma unroll 4
-    for (uint32_t i = tid; i < nP; i += nth) {
-      const uint32_t col = pcol[i];
-      p1[i + 1] = pval[i] * ld_dsmem(ws + col / C, col % C);
-      glo[i + 1] = 0u;
-      ghi[i + 1] = 0u;
-    }
-    uint32_t lg = 0;
-    while (lg < 5 && (2u << lg) * (nr ? nr : 1u) <= nth) ++lg;
-    const uint32_t S = 1u << lg, RP = nth >> lg, sub = tid & (S - 1u);
-    __syncthreads();
-    // z = A.w and s = loss'(y, z) (training.py:272-280) for this CTA's rows
-    const uint32_t nr_up = ((nr + RP - 1) / RP) * RP;
-    for (uint32_t q = tid >> lg; q < nr_up; q += RP) {
-      double part = 0.0;
-      if (q < nr) {
-        const uint32_t lo = rowoff[q], len = rowoff[q + 1] - lo;
-        walk_flat(N, lo + ((len * sub) >> lg), lo + ((len * (sub + 1)) >> lg), [&](uint32_t i) { part += p1[i]; });
-      }
-      for (uint32_t o = S >> 1; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      if (q < nr && sub == 0) srow[q] = loss_scalar(a.loss, y[q], part);
-    }
-    __syncthreads();
-    double g_scale, g_inv, o_scale, o_inv;
-    fix_scales(ysum, g_scale, g_inv);  // |s| <= |y| (logistic, hinge)
-    fix_scales(ysum * vmax, o_scale, o_inv);
-    for (uint32_t q = tid >> lg; q < nr; q += RP) {
-      const long long wr = __double2ll_rn(srow[q] * g_scale);
-      if (wr == 0) continue;
-      const uint32_t lo = rowoff[q], len = rowoff[q + 1] - lo;
-      const uint32_t xl = (uint32_t)wr, xh = (uint32_t)((unsigned long long)wr >> 32);
-      walk_flat(N, lo + ((len * sub) >> lg), lo + ((len * (sub + 1)) >> lg),
-                [&](uint32_t i) { fix_add_pair(glo, ghi, i, xl, xh); });
-    }
-    __syncthreads();
-    // each pair's contribution value * G (fixed point, as epoch_large_kernel) into its bucket slot
-    for (uint32_t i = tid; i < nP; i += nth) {
-      const double c = pval[i] * fix_value(glo[i + 1], ghi[i + 1], g_inv);
-      bucket[bslot[i]] = (unsigned long long)__double2ll_rn(c * o_scale);
-    }
-    cluster_barrier_smem();  // every CTA's buckets are complete
-    // pull this CTA's bucket from every CTA and add per own column (integer adds: order-free)
-    if (tid < C) {  // where CTA tid's bucket for this owner lies (its part image, global memory)
-      const uint8_t* pimg = a.images + a.part_off[t * C + tid];
-      const uint32_t* ph = reinterpret_cast<const uint32_t*>(pimg);
-      const PartLayout PL = part_layout(__ldg(ph), __ldg(ph + 1), __ldg(ph + 2), __ldg(ph + 3), __ldg(ph + 4), C);
-      const uint32_t bk = __ldg(reinterpret_cast<const uint32_t*>(pimg + PL.off_bkt) + cta);
-      s_k0[tid] = bk & 0xffffu;
-      s_k1[tid] = (bk & 0xffffu) + (bk >> 16);
-      s_bown[tid] = reinterpret_cast<const uint16_t*>(pimg + PL.off_bown);
-    }
-    __syncthreads();
-    for (uint32_t c = 0; c < C; ++c) {
-      const uint16_t* bown = s_bown[c];
-      for (uint32_t k = s_k0[c] + tid; k < s_k1[c]; k += nth) {
-        const unsigned long long f = ld_dsmem_u64(bucket + k, c);
-        if (f) fix_add_pair(glo_own, ghi_own, __ldg(bown + k), (uint32_t)f, (uint32_t)(f >> 32));
-      }
-    }
-    __syncthreads();
-    // apply_update (training.py:296-300) for the columns this CTA owns (same operations as
-    // epoch_large_kernel), then clear them
-    for (uint32_t o = tid; o < n_own; o += nth) {
-      const unsigned long long f = ((unsigned long long)ghi_own[o] << 32) | glo_own[o];
-      if (f) {
-        glo_own[o] = ghi_own[o] = 0u;
-        const uint32_t col = own[o];
-        ws[col / C] = __dsub_rn(ws[col / C], __dmul_rn(step, (double)(long long)f * o_inv));
-      }
-    }
-    __syncthreads();  // this CTA is done with its part buffer
-    if (tid == 0 && t + 1 < a.n_blocks) {
-      src += next_d;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect(&mbar[0], next_bytes);
-      bulk_copy(buf, src, next_bytes, &mbar[0]);
-    }
-    cluster_barrier_smem();  // the weights of step t are final before step t+1 reads them
-  }
-  for (uint32_t j = tid; j < a.w_slots; j += nth) {
-    const uint32_t col = j * C + cta;
-    if (col < m) a.w[col] = ws[j];
-  }
-  cluster_barrier();  // no CTA exits while another may still read its shared memory
-}
 }  // namespace toc
 
 // ------------------------------------------------------------------------------------------
@@ -795,58 +588,6 @@ extern "C" int toc_mgd_parts_fit(const TocBlockMeta* h_meta, const int32_t* h_co
   return TOC_OK;
 }
 
-int g_parts_dsmem = 0;  // the DSMEM epoch where it fits: opt-in (measured slower)
-
-// The DSMEM epoch (epoch_dsmem_kernel) for a whole epoch, if its shared memory fits: returns
-// TOC_E_ARG (nothing launched) otherwise.
-static int dsmem_launch(const uint8_t* d_images, const int64_t* d_part_off, const TocBlockMeta* h_meta,
-                        const int32_t* h_counts, int64_t n_blocks, int32_t n_cols, int32_t cluster, int32_t loss,
-                        double lr, double* d_w, int64_t max_part, void* stream) {
-  uint32_t max_pairs = 0, max_rows = 0, max_own = 0;
-  (void)parts_smem(h_meta, h_counts, n_blocks, cluster, max_part, max_pairs, max_rows);
-  for (int64_t i = 0; i < n_blocks * cluster; ++i) max_own = std::max(max_own, (uint32_t)h_counts[i * 4 + 3]);
-  if (max_pairs >= 65536u || max_own >= 65536u) return TOC_E_ARG;  // 16-bit bucket slots / own ranks
-  const uint32_t w_slots = (uint32_t)((n_cols + cluster - 1) / cluster);
-  const uint64_t smem = (uint64_t)toc::kFixedBytes + toc::align16(8u * w_slots) + 2ull * toc::align16(4u * max_own) +
-                        toc::align16(8u * (max_pairs + 1)) + 2ull * toc::align16(4u * (max_pairs + 1)) +
-                        toc::align16(8u * max_rows) + toc::align16((uint32_t)max_part);
-  if (smem > (uint64_t)la_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin, 232448)) return TOC_E_ARG;
-  toc::DsmemEpochArgs a{};
-  a.images = d_images;
-  a.part_off = d_part_off;
-  a.n_blocks = n_blocks;
-  a.n_cols = n_cols;
-  a.loss = loss;
-  a.cluster = cluster;
-  a.lr = lr;
-  a.w = d_w;
-  a.max_part = toc::align16((uint32_t)max_part);
-  a.max_pairs = max_pairs;
-  a.max_rows = max_rows;
-  a.max_own = max_own;
-  a.w_slots = w_slots;
-  if (cluster > 8 && cudaFuncSetAttribute(toc::epoch_dsmem_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) !=
-                          cudaSuccess)
-    return TOC_E_CUDA;
-  if (cudaFuncSetAttribute(toc::epoch_dsmem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-      cudaSuccess)
-    return TOC_E_CUDA;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(cluster);
-  cfg.blockDim = dim3(512);
-  cfg.dynamicSmemBytes = (size_t)smem;
-  cfg.stream = (cudaStream_t)stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = cluster;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  void* args[] = {&a};
-  return cudaLaunchKernelExC(&cfg, (void*)toc::epoch_dsmem_kernel, args) == cudaSuccess ? TOC_OK : TOC_E_CUDA;
-}
-
 static int parts_launch(const uint8_t* d_images, const int64_t* d_part_off, const TocBlockMeta* h_meta,
                         const int32_t* h_counts, int64_t n_blocks, int32_t n_cols, int32_t cluster, int32_t loss,
                         double lr, double* d_w, unsigned long long* d_gacc, int64_t max_part, int64_t t0, int64_t t1,
@@ -855,11 +596,6 @@ static int parts_launch(const uint8_t* d_images, const int64_t* d_part_off, cons
   if (!d_images || !d_part_off || !h_meta || !h_counts || !d_w || !d_gacc || cluster < 1 ||
       cluster > (int32_t)toc::kMaxPartsCluster || (cluster & (cluster - 1)) || (loss != TOC_LOSS_LOGISTIC && loss != TOC_LOSS_HINGE))
     return TOC_E_ARG;
-  if (g_parts_dsmem && !d_grad && t0 == 0 && t1 == n_blocks) {
-    const int rc = dsmem_launch(d_images, d_part_off, h_meta, h_counts, n_blocks, n_cols, cluster, loss, lr, d_w,
-                                max_part, stream);
-    if (rc != TOC_E_ARG) return rc;  // launched (or failed); TOC_E_ARG: does not fit, use the global kernel
-  }
   uint32_t max_pairs = 0, max_rows = 0;
   const uint32_t mp = toc::align16((uint32_t)max_part);
   const uint64_t smem = parts_smem(h_meta, h_counts, n_blocks, cluster, max_part, max_pairs, max_rows);
@@ -917,11 +653,6 @@ extern "C" int toc_glm_grad_parts(const uint8_t* d_images, const int64_t* d_part
   if (step < 0 || step >= n_blocks || !d_grad) return TOC_E_ARG;
   return parts_launch(d_images, d_part_off, h_meta, h_counts, n_blocks, n_cols, cluster, loss, 0.0,
                       const_cast<double*>(d_w), d_gacc, max_part, step, step + 1, d_grad, stream);
-}
-
-extern "C" int toc_mgd_set_parts_dsmem(int32_t on) {
-  g_parts_dsmem = on ? 1 : 0;
-  return TOC_OK;
 }
 
 extern "C" int toc_mgd_parts_cluster_max(int32_t* cluster) {

@@ -4,6 +4,10 @@
 // Algorithm 6).  A persistent grid walks the arena, one CTA per mini-batch at a time, the next
 // block prefetched into L2; the per-batch machinery (node tables rebuilt from the block in
 // shared memory, chain walks, fixed-point v^T.A) is in toc_batch.cuh.  DESIGN.md section 4.1.
+#include <atomic>
+#include <functional>
+#include <mutex>
+
 #include "toc_batch.cuh"
 
 namespace toc {
@@ -389,46 +393,70 @@ __global__ void __launch_bounds__(1024, 1) build_trees_kernel(LinalgArgs a) {
 // Host side: planning and launch.
 namespace {
 
-int g_use_splits = 1;
-int g_depth_order = 1;
+// Process-wide tuning knobs (tools only; set before launching, read at planning / launch time).
+std::atomic<int> g_use_splits{1};
+std::atomic<int> g_depth_order{1};
 
 struct DevProps {
   int sm_count = 0, smem_optin = 0, smem_per_sm = 0;
   int64_t l2 = 0;
 };
 
-const DevProps& dev_props() {
-  static DevProps p;
-  static bool init = false;
-  if (!init) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&p.sm_count, cudaDevAttrMultiProcessorCount, dev);
-    cudaDeviceGetAttribute(&p.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    cudaDeviceGetAttribute(&p.smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-    int l2 = 0;
-    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
-    p.l2 = l2;
+constexpr int kMaxDevices = 64;
+
+// The current device's properties, queried once per device (thread-safe).
+DevProps dev_props() {
+  static DevProps props[kMaxDevices];
+  static std::once_flag once[kMaxDevices];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = -1;
+  auto query = [](int d, DevProps& p) {
+    if (d >= 0) {
+      cudaDeviceGetAttribute(&p.sm_count, cudaDevAttrMultiProcessorCount, d);
+      cudaDeviceGetAttribute(&p.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, d);
+      cudaDeviceGetAttribute(&p.smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, d);
+      int l2 = 0;
+      cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, d);
+      p.l2 = l2;
+    }
     if (p.sm_count <= 0) {  // no device visible (planning on a CPU host): B200 figures
       p.sm_count = 148;
       p.smem_optin = 232448;
       p.smem_per_sm = 233472;
       p.l2 = 126 << 20;
     }
-    init = true;
+  };
+  if (dev < 0) {
+    DevProps p;
+    query(-1, p);
+    return p;
   }
-  return p;
+  std::call_once(once[dev], query, dev, std::ref(props[dev]));
+  return props[dev];
+}
+
+// Raise the kernel's dynamic shared-memory limit to `bytes` on the current device (once per device
+// and size; concurrent callers may both set it, which is harmless).
+template <typename K>
+cudaError_t ensure_smem(K* fn, int bytes, std::atomic<int>* configured) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices)
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (configured[dev].load() >= bytes) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) {
+    int cur = configured[dev].load();
+    while (cur < bytes && !configured[dev].compare_exchange_weak(cur, bytes)) {
+    }
+  }
+  return e;
 }
 
 template <bool W, bool V, bool C>
 cudaError_t launch_mode(const toc::LinalgArgs& a, const TocPlan& plan, cudaStream_t s) {
-  static int configured = -1;
-  if (configured < plan.smem_bytes) {
-    cudaError_t e = cudaFuncSetAttribute(toc::linalg_kernel<W, V, C>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, plan.smem_bytes);
-    if (e != cudaSuccess) return e;
-    configured = plan.smem_bytes;
-  }
+  static std::atomic<int> configured[kMaxDevices];  // zero-initialised (static storage)
+  if (const cudaError_t e = ensure_smem(toc::linalg_kernel<W, V, C>, plan.smem_bytes, configured); e != cudaSuccess)
+    return e;
   toc::linalg_kernel<W, V, C><<<plan.ctas, plan.threads, plan.smem_bytes, s>>>(a);
   return cudaGetLastError();
 }
@@ -443,7 +471,7 @@ cudaError_t launch(const toc::LinalgArgs& a, const TocPlan& plan, cudaStream_t s
 extern "C" int toc_plan(const TocBlockMeta* h_meta, int64_t n_blocks, int32_t kind, TocPlan* plan) {
   if (!plan || (n_blocks > 0 && !h_meta) || !(kind & (TOC_MATVEC | TOC_VECMAT))) return TOC_E_ARG;
   memset(plan, 0, sizeof(*plan));
-  const DevProps& d = dev_props();
+  const DevProps d = dev_props();
   uint64_t max_T = 0;
   int32_t n_cols = n_blocks ? (int32_t)h_meta[0].n_cols : 0;
   for (int64_t b = 0; b < n_blocks; b++) {

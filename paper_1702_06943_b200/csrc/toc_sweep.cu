@@ -26,19 +26,7 @@ extern "C" int toc_linalg(const uint8_t* d_arena, const int64_t* d_block_off, co
 
 namespace {
 
-struct EventPool {
-  std::vector<cudaEvent_t> ev;
-  cudaEvent_t get(size_t i) {
-    while (ev.size() <= i) {
-      cudaEvent_t e;
-      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
-      ev.push_back(e);
-    }
-    return ev[i];
-  }
-};
-
-EventPool g_upload, g_opnd, g_done;
+cudaEvent_t ev(void* e) { return static_cast<cudaEvent_t>(e); }
 
 // diagnostic timeline (toc_sweep_set_timing): timed events per chunk
 bool g_timing = false;
@@ -53,6 +41,28 @@ cudaEvent_t tev(size_t i) {
 }
 
 }  // namespace
+
+extern "C" int toc_sweep_events(TocSweepChunk* chunks, int64_t n_chunks) {
+  if (!chunks || n_chunks < 0) return TOC_E_ARG;
+  for (int64_t k = 0; k < n_chunks; ++k)
+    for (void** slot : {&chunks[k].ev_upload, &chunks[k].ev_operands, &chunks[k].ev_done}) {
+      if (*slot) continue;
+      cudaEvent_t e;
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return TOC_E_CUDA;
+      *slot = e;
+    }
+  return TOC_OK;
+}
+
+extern "C" int toc_sweep_events_free(TocSweepChunk* chunks, int64_t n_chunks) {
+  if (!chunks || n_chunks < 0) return TOC_E_ARG;
+  for (int64_t k = 0; k < n_chunks; ++k)
+    for (void** slot : {&chunks[k].ev_upload, &chunks[k].ev_operands, &chunks[k].ev_done}) {
+      if (*slot) cudaEventDestroy(ev(*slot));
+      *slot = nullptr;
+    }
+  return TOC_OK;
+}
 
 extern "C" int toc_sweep_set_timing(int32_t on) {
   g_timing = on != 0;
@@ -80,8 +90,7 @@ extern "C" int toc_sweep_upload(const uint8_t* h_blocks, uint8_t* d_blocks, cons
     if (cudaMemcpyAsync(d_blocks + c.byte_lo, h_blocks + c.byte_lo, (size_t)(c.byte_hi - c.byte_lo),
                         cudaMemcpyHostToDevice, cs) != cudaSuccess)
       return TOC_E_CUDA;
-    cudaEvent_t e = g_upload.get((size_t)k);
-    if (!e || cudaEventRecord(e, cs) != cudaSuccess) return TOC_E_CUDA;
+    if (!c.ev_upload || cudaEventRecord(ev(c.ev_upload), cs) != cudaSuccess) return TOC_E_CUDA;
     if (g_timing) cudaEventRecord(tev(1 + 5 * k), cs);
   }
   return TOC_OK;
@@ -101,8 +110,7 @@ extern "C" int toc_sweep_operands(const TocSweepChunk* chunks, int64_t n_chunks,
     if (cudaMemcpyAsync(d_u + c.row0, h_u + c.row0, sizeof(double) * (size_t)c.n_rows, cudaMemcpyHostToDevice, cs) !=
         cudaSuccess)
       return TOC_E_CUDA;
-    cudaEvent_t e = g_opnd.get((size_t)k);
-    if (!e || cudaEventRecord(e, cs) != cudaSuccess) return TOC_E_CUDA;
+    if (!c.ev_operands || cudaEventRecord(ev(c.ev_operands), cs) != cudaSuccess) return TOC_E_CUDA;
   }
   return TOC_OK;
 }
@@ -118,18 +126,18 @@ extern "C" int toc_sweep_compute(const TocSweepChunk* chunks, int64_t n_chunks, 
   int64_t meta_pos = 0;
   for (int64_t k = 0; k < n_chunks; ++k) {
     const TocSweepChunk& c = chunks[k];
-    if (cudaStreamWaitEvent(comp, g_upload.get((size_t)k), 0) != cudaSuccess) return TOC_E_CUDA;
+    if (!c.ev_upload || !c.ev_operands || !c.ev_done) return TOC_E_ARG;
+    if (cudaStreamWaitEvent(comp, ev(c.ev_upload), 0) != cudaSuccess) return TOC_E_CUDA;
     if (g_timing) cudaEventRecord(tev(2 + 5 * k), comp);
     int rc = toc_index_blocks(c.d_arena, c.d_block_off, c.d_block_len, c.n_blocks, c.d_meta, comp);
     if (rc) return rc;
     if (g_timing) cudaEventRecord(tev(3 + 5 * k), comp);
-    if (cudaStreamWaitEvent(comp, g_opnd.get((size_t)k), 0) != cudaSuccess) return TOC_E_CUDA;
+    if (cudaStreamWaitEvent(comp, ev(c.ev_operands), 0) != cudaSuccess) return TOC_E_CUDA;
     rc = toc_linalg(c.d_arena, c.d_block_off, c.d_meta, c.d_row_base, c.n_blocks, &c.plan, TOC_MATVEC | TOC_VECMAT,
                     d_v, d_R + c.row0, d_u + c.row0, d_O + c.b0 * (int64_t)n_cols, c.d_scratch, comp);
     if (rc) return rc;
     if (g_timing) cudaEventRecord(tev(4 + 5 * k), comp);
-    cudaEvent_t done = g_done.get((size_t)k);
-    if (!done || cudaEventRecord(done, comp) != cudaSuccess || cudaStreamWaitEvent(ds, done, 0) != cudaSuccess)
+    if (cudaEventRecord(ev(c.ev_done), comp) != cudaSuccess || cudaStreamWaitEvent(ds, ev(c.ev_done), 0) != cudaSuccess)
       return TOC_E_CUDA;
     if (cudaMemcpyAsync(h_R + c.row0, d_R + c.row0, sizeof(double) * (size_t)c.n_rows, cudaMemcpyDeviceToHost, ds) !=
             cudaSuccess ||

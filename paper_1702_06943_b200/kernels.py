@@ -298,6 +298,7 @@ class BatchSweep:
             d.d_scratch = scratch.data_ptr() if scratch is not None else None
             d.n_blocks, d.b0, d.row0, d.n_rows = arena.n_blocks, b0, r0, arena.n_rows_total
             d.plan = plan
+        N.check(N.lib().toc_sweep_events(self.cdesc, len(self.chunks)), "toc_sweep_events")  # this sweep's own
         self.h2d_bytes = nbytes + 8 * self.n_cols + 8 * self.n_rows
         self.d2h_bytes = 8 * self.n_rows + 8 * nb * self.n_cols + sum(c[0].meta_d.numel() for c in self.chunks)
 
@@ -305,11 +306,20 @@ class BatchSweep:
     def from_host_blocks(cls, blocks_h, block_off, block_len, chunks: int = 8) -> "BatchSweep":
         return cls(np.asarray(blocks_h, np.uint8), block_off, block_len, chunks)
 
-    def run(self, v, u):
+    def __del__(self):
+        try:
+            N.lib().toc_sweep_events_free(self.cdesc, len(self.chunks))
+        except Exception:  # interpreter shutdown
+            pass
+
+    def run(self, v, u, out=None):
         """The first chunk's block bytes are enqueued and stream in while the host prepares v / u;
         then the operands, the other chunks' bytes (all on one copy stream: host -> device copies
         are served in submission order), every chunk's validation and fused A.v + v^T.A (each as
-        soon as its bytes and operands are in) and the result downloads (toc_sweep.cu)."""
+        soon as its bytes and operands are in) and the result downloads (toc_sweep.cu).
+        Returns (R [n_rows], O [n_blocks, n_cols]) as new arrays; with out=(R_h, O_h) -- float64
+        CPU tensors of those shapes, pinned for asynchronous copies -- the results are downloaded
+        straight into them and they are returned (no extra host copy)."""
         torch = self.torch
         L = N.lib()
         caller = torch.cuda.current_stream()
@@ -325,8 +335,17 @@ class BatchSweep:
                                      self.u_h.data_ptr(), self.u_d.data_ptr(), cs.cuda_stream), "toc_sweep_operands")
         N.check(L.toc_sweep_upload(self.host.data_ptr(), self.dev.data_ptr(), self.cdesc, min(n, 1), n, cs.cuda_stream),
                 "toc_sweep_upload")
+        if out is not None:
+            R_o, O_o = out
+            if (R_o.dtype != torch.float64 or O_o.dtype != torch.float64 or R_o.device.type != "cpu"
+                    or O_o.device.type != "cpu" or R_o.numel() < self.n_rows or O_o.numel() < self.n_blocks * self.n_cols
+                    or not R_o.is_contiguous() or not O_o.is_contiguous()):
+                raise ValueError("out must be contiguous float64 CPU tensors of n_rows and n_blocks x n_cols")
+            R_dst, O_dst = R_o.data_ptr(), O_o.data_ptr()
+        else:
+            R_dst, O_dst = self.R_h.data_ptr(), self.O_h.data_ptr()
         N.check(L.toc_sweep_compute(self.cdesc, n, self.n_cols, self.v_d.data_ptr(), self.u_d.data_ptr(),
-                                    self.R_d.data_ptr(), self.R_h.data_ptr(), self.O_d.data_ptr(), self.O_h.data_ptr(),
+                                    self.R_d.data_ptr(), R_dst, self.O_d.data_ptr(), O_dst,
                                     self.meta_all_h.data_ptr(), comp.cuda_stream, ds.cuda_stream), "toc_sweep_compute")
         ds.synchronize()
         caller.wait_stream(ds)
@@ -336,4 +355,6 @@ class BatchSweep:
                 arena.meta = meta[b0:b1].copy()
                 arena.raise_format_errors()
                 arena.raise_corrupt()
-        return self.R_h.numpy()[: self.n_rows], self.O_h.numpy()[: self.n_blocks, : self.n_cols]
+        if out is not None:
+            return out
+        return self.R_h.numpy()[: self.n_rows].copy(), self.O_h.numpy()[: self.n_blocks, : self.n_cols].copy()

@@ -131,7 +131,6 @@ def _bind():
         L.toc_mgd_parts_fit.argtypes = [P, P, I64, I32, I64, ctypes.POINTER(ctypes.c_int32)]
         L.toc_glm_epoch_parts.argtypes = [P, P, P, P, I64, I32, I32, I32, D, P, P, I64, P]
         L.toc_glm_grad_parts.argtypes = [P, P, P, P, I64, I32, I32, I32, I64, P, P, P, I64, P]
-        L.toc_mgd_set_parts_dsmem.argtypes = [I32]
         L.toc_mgd_parts_cluster_max.argtypes = [ctypes.c_void_p]
         L.toc_glm_epoch_images_dp.argtypes = [P, P, P, P, I64, I32, I32, I32, D, P, I32, I32, P, P, P,
                                                ctypes.c_uint32, P]

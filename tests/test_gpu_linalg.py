@@ -161,6 +161,18 @@ def test_batch_sweep_public_api(oracle):
         assert within_rel(R[250 * b : 250 * (b + 1)], t.matvec(x), REL)
         assert within_rel(O[b], t.vecmat(u[250 * b : 250 * (b + 1)]), REL)
     assert sweep.h2d_bytes == end + 8 * 784 + 8 * 250 * nb
+    # results are the caller's: a later run does not change them; out= fills the caller's buffers
+    import torch
+
+    R0, O0 = R.copy(), O.copy()
+    sweep.run(-x, -u)
+    assert np.array_equal(R, R0) and np.array_equal(O, O0)
+    out = (torch.empty(250 * nb, dtype=torch.float64).pin_memory(), torch.empty((nb, 784), dtype=torch.float64).pin_memory())
+    Ro, Oo = sweep.run(x, u, out=out)
+    assert Ro is out[0] and np.array_equal(out[0].numpy(), R0) and np.array_equal(out[1].numpy(), O0)
+    other = BatchSweep.from_host_blocks(host, arena.block_off, arena.block_len, chunks=3)  # its own events
+    R2, O2 = other.run(x, u)
+    assert np.array_equal(R2, R0) and np.array_equal(O2, O0)
 
 
 @pytest.mark.parametrize("kind", [1, 2, 3])

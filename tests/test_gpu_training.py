@@ -307,31 +307,6 @@ def test_dp_epoch_graph_world1_nccl(oracle, loss):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("loss,lr,cluster", [("hinge", 0.01, 8), ("logistic", 0.1, 8), ("hinge", 0.01, 16)])
-def test_parts_dsmem_equals_global_kernel(loss, lr, cluster):
-    """The DSMEM parts epoch (weights and the gradient exchange in distributed shared memory) is
-    bit-identical to the global-memory parts epoch: the same fixed-point contributions, summed as
-    integers, the same update operations."""
-    from paper_1702_06943_b200 import synth
-    from paper_1702_06943_b200.training import _bind
-
-    rp, c, v, y = synth.cfg4_dataset(4_000, seed=37)
-    L = _bind()
-    tg = _trainer(rp, c, v, y, 47_236, 250, loss, lr, "parts", cluster)
-    for _ in range(2):
-        tg.epoch()
-    wg, rg = tg.weights(), tg.risk()
-    try:
-        L.toc_mgd_set_parts_dsmem(1)
-        td = _trainer(rp, c, v, y, 47_236, 250, loss, lr, "parts", cluster)
-        for _ in range(2):
-            td.epoch()
-    finally:
-        L.toc_mgd_set_parts_dsmem(0)
-    assert np.array_equal(td.weights(), wg)
-    assert td.risk() == rg
-
-
 @pytest.mark.gpu
 @pytest.mark.parametrize("loss,world", [("logistic", 2), ("hinge", 2), ("logistic", 4)])
 def test_dp_fused_exchange_emulated_ranks(oracle, loss, world):

@@ -16,7 +16,6 @@ p.add_argument("--epochs", type=int, default=0)
 p.add_argument("--max-ctas", type=int, default=0)
 p.add_argument("--cluster", type=int, default=0)
 p.add_argument("--threads", type=int, default=0)
-p.add_argument("--dsmem", action="store_true")
 a = p.parse_args()
 
 from paper_1702_06943_b200 import synth  # noqa: E402
@@ -35,9 +34,6 @@ t = time.time(); batches = DeviceBatches(sh, 250); import torch; torch.cuda.sync
 if a.threads:
     from paper_1702_06943_b200 import _native as _N0
     _N0.lib().toc_mgd_set_image_threads(a.threads)
-if a.dsmem:
-    from paper_1702_06943_b200 import training as _T
-    _T._bind().toc_mgd_set_parts_dsmem(1)
 tr = GlmTrainer(batches, loss, lr, cluster=a.cluster)
 if a.max_ctas:
     from paper_1702_06943_b200 import _native as _N
