@@ -37,6 +37,7 @@ def test_abi_struct_sizes_and_binding():
     assert L.toc_sizeof_meta() == N.META_DTYPE.itemsize == 68
     assert L.toc_sizeof_plan() == ctypes.sizeof(N.TocPlan) == 40
     assert L.toc_sizeof_batch_info() == INFO_DTYPE.itemsize == 48
+    assert L.toc_sizeof_sweep_chunk() == ctypes.sizeof(N.TocSweepChunk) == 160
     assert b"sm_100a" in L.toc_version()
 
 
