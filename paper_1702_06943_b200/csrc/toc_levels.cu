@@ -456,8 +456,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
           }
 #pragma unroll
           for (uint32_t i = 0; i < 4; ++i) {
-            acc += ha[i];
-            acc += hb[i];
+            acc += ha[i] + hb[i];  // the code's value: one add on the row's dependency chain
             if (rec[i] & kRowEnd) {
               TOC_CHECK(r < n);
               if (here) a.R[rb + r] = acc;
