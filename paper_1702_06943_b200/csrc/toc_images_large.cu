@@ -28,28 +28,35 @@ constexpr uint32_t kMaxPartsCluster = 16;
 
 // Part header (64 B): u32 [0] rows [1] pairs nP [2] derived nD [3] codes [4] owned columns
 // [5] batch rows; f64 at 24: sum |y| of the batch, at 32: max |value| of the batch; i64 at 40:
-// byte offset of the same CTA's part of the NEXT batch relative to this part, u32 at 48: its bytes.
+// byte offset of the same CTA's part of the NEXT batch relative to this part, u32 at 48: its bytes;
+// u32 [13]: the batch's value-index size nU.
 constexpr uint32_t kPartHeader = 64;
 
+// Local ids (1 + nP + nD per part), columns and value refs fit 16 bits (toc_mgd_parts_fit checks):
+// codes, columns and value refs are u16, node records u32 (parent | key << 16, Nodes<false>), and
+// each part carries the batch's value index (nU doubles, header u32 [13]).
 struct PartLayout {
-  uint32_t off_rowoff, off_codes, off_nodes, off_pcol, off_pval, off_own, off_labels, total;
+  uint32_t off_rowoff, off_codes, off_nodes, off_pcol, off_pref, off_uniq, off_own, off_labels, total;
 };
 
-TOC_HD PartLayout part_layout(uint32_t nr, uint32_t nP, uint32_t nD, uint32_t nC, uint32_t n_own, uint32_t C) {
+TOC_HD PartLayout part_layout(uint32_t nr, uint32_t nP, uint32_t nD, uint32_t nC, uint32_t n_own, uint32_t C,
+                              uint32_t nU) {
   PartLayout L;
   uint32_t o = kPartHeader;
   L.off_rowoff = o;
   o += align16(4u * (nr + 1));
   L.off_codes = o;
-  o += align16(4u * nC);
+  o += align16(2u * nC);
   L.off_nodes = o;
-  o += align16(8u * (1u + nP + nD));
+  o += align16(4u * (1u + nP + nD));
   L.off_pcol = o;
-  o += align16(4u * nP);
-  L.off_pval = o;
-  o += align16(8u * nP);
+  o += align16(2u * nP);
+  L.off_pref = o;
+  o += align16(2u * nP);
+  L.off_uniq = o;
+  o += align16(8u * nU);
   L.off_own = o;
-  o += align16(4u * n_own);
+  o += align16(2u * n_own);
   L.off_labels = o;
   o += align16(8u * nr);
   L.total = o;
@@ -148,8 +155,8 @@ __global__ void __launch_bounds__(1024, 1) large_image_kernel(LargeArgs a) {
           bits &= bits - 1u;
           const uint32_t* h = reinterpret_cast<const uint32_t*>(a.counts + (b * C + o) * 4);
           const uint32_t pr0 = (uint32_t)(((uint64_t)n * o) / C), pr1 = (uint32_t)(((uint64_t)n * (o + 1)) / C);
-          const PartLayout PL = part_layout(pr1 - pr0, h[0], h[1], h[2], h[3], C);
-          reinterpret_cast<uint32_t*>(a.images + a.part_off[b * C + o] + PL.off_own)[own_rank(col)] = col;
+          const PartLayout PL = part_layout(pr1 - pr0, h[0], h[1], h[2], h[3], C, mb.n_uniques);
+          reinterpret_cast<uint16_t*>(a.images + a.part_off[b * C + o] + PL.off_own)[own_rank(col)] = (uint16_t)col;
         }
       }
     }
@@ -222,13 +229,15 @@ __global__ void __launch_bounds__(1024, 1) large_image_kernel(LargeArgs a) {
       };
       const int32_t* cn = a.counts + (b * C + part) * 4;
       const uint32_t n_own = (uint32_t)cn[3];
-      const PartLayout L = part_layout(r1 - r0, nP, nD, nC, n_own, C);
+      const PartLayout L = part_layout(r1 - r0, nP, nD, nC, n_own, C, mb.n_uniques);
       uint8_t* img = a.images + a.part_off[b * C + part];
       uint32_t* rowoff = reinterpret_cast<uint32_t*>(img + L.off_rowoff);
-      uint32_t* codes = reinterpret_cast<uint32_t*>(img + L.off_codes);
-      uint2* nodes = reinterpret_cast<uint2*>(img + L.off_nodes);
-      uint32_t* pcol = reinterpret_cast<uint32_t*>(img + L.off_pcol);
-      double* pval = reinterpret_cast<double*>(img + L.off_pval);
+      uint16_t* codes = reinterpret_cast<uint16_t*>(img + L.off_codes);
+      uint32_t* nodes = reinterpret_cast<uint32_t*>(img + L.off_nodes);
+      uint16_t* pcol = reinterpret_cast<uint16_t*>(img + L.off_pcol);
+      uint16_t* pref = reinterpret_cast<uint16_t*>(img + L.off_pref);
+      double* puq = reinterpret_cast<double*>(img + L.off_uniq);
+      for (uint32_t i = tid; i < mb.n_uniques; i += nth) puq[i] = B.uniq[i];
       double* y = reinterpret_cast<double*>(img + L.off_labels);
       for (uint32_t r = r0 + tid; r <= r1; r += nth) rowoff[r - r0] = B.rowoff[r] - q0;
       for (uint32_t r = r0 + tid; r < r1; r += nth) y[r - r0] = a.labels[rb + r];
@@ -236,20 +245,21 @@ __global__ void __launch_bounds__(1024, 1) large_image_kernel(LargeArgs a) {
         uint32_t r, lo, hi, db, j0, j1;
         if (!B.segment(k, r, lo, hi, db, j0, j1)) break;
         if (r < r0 || r >= r1) continue;
-        for (uint32_t j = j0; j < j1; ++j) codes[j - q0] = lid((j + 1 < hi) ? B.pk.par(db + (j - lo)) : B.last[r]);
+        for (uint32_t j = j0; j < j1; ++j)
+          codes[j - q0] = (uint16_t)lid((j + 1 < hi) ? B.pk.par(db + (j - lo)) : B.last[r]);
       }
-      if (tid == 0) nodes[0] = make_uint2(0u, 0u);
+      if (tid == 0) nodes[0] = 0u;
       for (uint32_t x = 1 + tid; x < T; x += nth) {
         if (!(__ldcg(mark + (x >> 5)) & (1u << (x & 31)))) continue;
         const uint32_t l = lid(x);
         if (x <= nI) {
-          nodes[l] = make_uint2(0u, l);
-          pcol[l - 1] = ld_packed(blk + mb.off_cols, x - 1, mb.w_cols);
-          pval[l - 1] = B.uniq[ld_packed(blk + mb.off_refs, x - 1, mb.w_refs)];
+          nodes[l] = Nodes<false>::pack(0u, l);
+          pcol[l - 1] = (uint16_t)ld_packed(blk + mb.off_cols, x - 1, mb.w_cols);
+          pref[l - 1] = (uint16_t)ld_packed(blk + mb.off_refs, x - 1, mb.w_refs);
         } else {
           uint32_t par, key;
           B.pk.get(x - 1 - nI, par, key);
-          nodes[l] = make_uint2(lid(par), lid(key));
+          nodes[l] = Nodes<false>::pack(lid(par), lid(key));
         }
       }
       if (tid == 0) {
@@ -260,6 +270,7 @@ __global__ void __launch_bounds__(1024, 1) large_image_kernel(LargeArgs a) {
         h[3] = nC;
         h[4] = n_own;
         h[5] = n;
+        h[13] = mb.n_uniques;
         reinterpret_cast<double*>(img)[3] = ysum;
         reinterpret_cast<double*>(img)[4] = vmax;
         const int64_t here = a.part_off[b * C + part];
@@ -336,14 +347,15 @@ __global__ void __launch_bounds__(1024, 1) epoch_large_kernel(LargeEpochArgs a) 
     }
     const uint32_t nr = h[0], nP = h[1], nD = h[2], nC = h[3], n_own = h[4], n = h[5];
     const double ysum = reinterpret_cast<const double*>(img)[3], vmax = reinterpret_cast<const double*>(img)[4];
-    const PartLayout L = part_layout(nr, nP, nD, nC, n_own, (uint32_t)a.cluster);
+    const PartLayout L = part_layout(nr, nP, nD, nC, n_own, (uint32_t)a.cluster, h[13]);
     const uint32_t* rowoff = reinterpret_cast<const uint32_t*>(img + L.off_rowoff);
-    Nodes<true> N;
-    N.codes = reinterpret_cast<const uint32_t*>(img + L.off_codes);
-    N.p = reinterpret_cast<const uint2*>(img + L.off_nodes);
-    const uint32_t* pcol = reinterpret_cast<const uint32_t*>(img + L.off_pcol);
-    const double* pval = reinterpret_cast<const double*>(img + L.off_pval);
-    const uint32_t* own = reinterpret_cast<const uint32_t*>(img + L.off_own);
+    Nodes<false> N;
+    N.codes = reinterpret_cast<const uint16_t*>(img + L.off_codes);
+    N.p = reinterpret_cast<const uint32_t*>(img + L.off_nodes);
+    const uint16_t* pcol = reinterpret_cast<const uint16_t*>(img + L.off_pcol);
+    const uint16_t* pref = reinterpret_cast<const uint16_t*>(img + L.off_pref);
+    const double* puq = reinterpret_cast<const double*>(img + L.off_uniq);
+    const uint16_t* own = reinterpret_cast<const uint16_t*>(img + L.off_own);
     const double* y = reinterpret_cast<const double*>(img + L.off_labels);
     if (n != step_n) {
       step = a.lr / (double)n;
@@ -362,7 +374,7 @@ __global__ void __launch_bounds__(1024, 1) epoch_large_kernel(LargeEpochArgs a) 
       for (uint32_t u = 0; u < 4; ++u)
         if (i0 + u * nth < nP) {
           const uint32_t i = i0 + u * nth;
-          p1[i + 1] = pval[i] * wv[u];
+          p1[i + 1] = puq[pref[i]] * wv[u];
           glo[i + 1] = 0u;
           ghi[i + 1] = 0u;
         }
@@ -398,7 +410,7 @@ __global__ void __launch_bounds__(1024, 1) epoch_large_kernel(LargeEpochArgs a) 
     __syncthreads();
     // value * G per pair into the global fixed-point gradient: integer adds, order-independent
     for (uint32_t i = tid; i < nP; i += nth) {
-      const double c = pval[i] * fix_value(glo[i + 1], ghi[i + 1], g_inv);
+      const double c = puq[pref[i]] * fix_value(glo[i + 1], ghi[i + 1], g_inv);
       const long long f = __double2ll_rn(c * o_scale);
       if (f) atomicAdd(a.gacc + pcol[i], (unsigned long long)f);
     }
@@ -528,7 +540,8 @@ extern "C" int toc_mgd_parts_offsets(const TocBlockMeta* h_meta, const int32_t* 
       const uint32_t r0 = (uint32_t)(((uint64_t)n * c) / cluster), r1 = (uint32_t)(((uint64_t)n * (c + 1)) / cluster);
       const int32_t* cn = h_counts + (b * cluster + c) * 4;
       const uint32_t sz =
-          toc::part_layout(r1 - r0, (uint32_t)cn[0], (uint32_t)cn[1], (uint32_t)cn[2], (uint32_t)cn[3], (uint32_t)cluster)
+          toc::part_layout(r1 - r0, (uint32_t)cn[0], (uint32_t)cn[1], (uint32_t)cn[2], (uint32_t)cn[3], (uint32_t)cluster,
+                           h_meta[b].n_uniques)
               .total;
       h_part_off[b * cluster + c] = o;
       o += sz;
@@ -585,6 +598,13 @@ extern "C" int toc_mgd_parts_fit(const TocBlockMeta* h_meta, const int32_t* h_co
                   (uint64_t)la_attr(cudaDevAttrMaxSharedMemoryPerBlockOptin, 232448)
               ? 1
               : 0;
+  for (int64_t b = 0; b < n_blocks && *fits; ++b) {  // 16-bit local ids and columns (PartLayout)
+    if (h_meta[b].n_cols > 65536u || h_meta[b].n_uniques > 65536u) *fits = 0;
+    for (int32_t c = 0; c < cluster; ++c) {
+      const int32_t* cn = h_counts + (b * cluster + c) * 4;
+      if (1ll + cn[0] + cn[1] > 65535ll) *fits = 0;
+    }
+  }
   return TOC_OK;
 }
 
