@@ -333,6 +333,8 @@ int toc_glm_epoch_parts(const uint8_t* d_images, const int64_t* d_part_off, cons
 /* The largest power-of-two cluster (<= 16; sizes above 8 are non-portable) this device co-schedules
  * for the part-image epoch with a full shared-memory carve-out per CTA, into *cluster.  The part
  * images are built for one cluster size (toc_mgd_parts_count / _build take it). */
+/* Diagnostic: per-step clock64 stamps of toc_glm_epoch_parts (8 per step from step t0; NULL: off). */
+int toc_mgd_parts_set_trace(long long* d_trace);
 int toc_mgd_parts_cluster_max(int32_t* cluster);
 
 /* One data-parallel MGD step on the same part images (training.py:261-281 per rank; the caller

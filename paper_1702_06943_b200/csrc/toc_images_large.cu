@@ -302,6 +302,13 @@ struct LargeEpochArgs {
                              // batch into grad_out[touched columns] instead of the update
 };
 
+// Phase trace (tools/mgd_bench.py, toc_mgd_parts_set_trace): when set, CTA 0 of the cluster stamps
+// clock64 at 7 points of each step: start, part landed, P1, A.w + loss, s^T.A, gradient added +
+// cluster barrier, update + cluster barrier.
+__constant__ long long* g_parts_trace = nullptr;
+#define parts_stamp(t, k) \
+  if (g_parts_trace && cluster_rank() == 0 && tid == 0) g_parts_trace[((t) - a.t0) * 8 + (k)] = clock64()
+
 // One epoch on a cluster of C CTAs; w and the fixed-point gradient live in global memory.
 // Shared memory: fixed | P1 | G lo | G hi | s | part buffer 0 | part buffer 1.
 __global__ void __launch_bounds__(1024, 1) epoch_large_kernel(LargeEpochArgs a) {
@@ -333,9 +340,11 @@ __global__ void __launch_bounds__(1024, 1) epoch_large_kernel(LargeEpochArgs a) 
   uint32_t step_n = 0;
   double step = 0.0;
   for (int64_t t = a.t0; t < a.t1; ++t) {
+    parts_stamp(t, 0);
     const uint32_t k = (uint32_t)(t - a.t0) & 1u;
     const uint8_t* img = k ? buf1 : buf0;
     mbar_wait_bounded(&mbar[k], (uint32_t)((t - a.t0) >> 1) & 1u);
+    parts_stamp(t, 1);
     const uint32_t* h = reinterpret_cast<const uint32_t*>(img);
     if (tid == 0 && t + 1 < a.t1) {  // every thread is past step t-1: the other buffer is free
       const int64_t d = *reinterpret_cast<const int64_t*>(img + 40);
@@ -383,6 +392,7 @@ __global__ void __launch_bounds__(1024, 1) epoch_large_kernel(LargeEpochArgs a) 
     while (lg < 5 && (2u << lg) * (nr ? nr : 1u) <= nth) ++lg;
     const uint32_t S = 1u << lg, RP = nth >> lg, sub = tid & (S - 1u);
     __syncthreads();
+    parts_stamp(t, 2);
     // z = A.w and s = loss'(y, z) (training.py:272-280) for this CTA's rows
     const uint32_t nr_up = ((nr + RP - 1) / RP) * RP;
     for (uint32_t q = tid >> lg; q < nr_up; q += RP) {
@@ -395,6 +405,7 @@ __global__ void __launch_bounds__(1024, 1) epoch_large_kernel(LargeEpochArgs a) 
       if (q < nr && sub == 0) srow[q] = loss_scalar(a.loss, y[q], part);
     }
     __syncthreads();
+    parts_stamp(t, 3);
     double g_scale, g_inv, o_scale, o_inv;
     fix_scales(ysum, g_scale, g_inv);  // |s| <= |y| (logistic, hinge)
     fix_scales(ysum * vmax, o_scale, o_inv);
@@ -408,6 +419,7 @@ __global__ void __launch_bounds__(1024, 1) epoch_large_kernel(LargeEpochArgs a) 
                 [&](uint32_t i) { fix_add_pair(glo, ghi, i, xl, xh); });
     }
     __syncthreads();
+    parts_stamp(t, 4);
     // value * G per pair into the global fixed-point gradient: integer adds, order-independent
     for (uint32_t i = tid; i < nP; i += nth) {
       const double c = puq[pref[i]] * fix_value(glo[i + 1], ghi[i + 1], g_inv);
@@ -415,6 +427,7 @@ __global__ void __launch_bounds__(1024, 1) epoch_large_kernel(LargeEpochArgs a) 
       if (f) atomicAdd(a.gacc + pcol[i], (unsigned long long)f);
     }
     cluster_barrier();  // every CTA's contributions are in the gradient
+    parts_stamp(t, 5);
     if (a.grad_out) {  // data-parallel step: hand the summed gradient to the all-reduce
       for (uint32_t o = tid; o < n_own; o += nth) {
         const uint32_t c = own[o];
@@ -434,6 +447,7 @@ __global__ void __launch_bounds__(1024, 1) epoch_large_kernel(LargeEpochArgs a) 
       }
     }
     cluster_barrier();  // the weights of step t are final before step t+1 reads them
+    parts_stamp(t, 6);
   }
 }
 
@@ -673,6 +687,10 @@ extern "C" int toc_glm_grad_parts(const uint8_t* d_images, const int64_t* d_part
   if (step < 0 || step >= n_blocks || !d_grad) return TOC_E_ARG;
   return parts_launch(d_images, d_part_off, h_meta, h_counts, n_blocks, n_cols, cluster, loss, 0.0,
                       const_cast<double*>(d_w), d_gacc, max_part, step, step + 1, d_grad, stream);
+}
+
+extern "C" int toc_mgd_parts_set_trace(long long* d_trace) {
+  return cudaMemcpyToSymbol(toc::g_parts_trace, &d_trace, sizeof d_trace) == cudaSuccess ? TOC_OK : TOC_E_CUDA;
 }
 
 extern "C" int toc_mgd_parts_cluster_max(int32_t* cluster) {

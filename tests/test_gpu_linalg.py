@@ -37,9 +37,9 @@ def _check_sweep(oracle, encs, v, seed=0, mode="rebuild"):
     if mode == "tree_cache":
         arena.build_trees()
     if mode == "levels":
-        # the level cache takes every narrow batch (ids < 65536); wider ones keep the other paths
+        # the slot cache takes every batch whose slots fit 15 bits; wider ones keep the other paths
         built = arena.build_levels()
-        assert built or max(e.tree_length() for e in encs) > 65536
+        assert built or max(e.tree_length() for e in encs) > 32767
     trees = [oracle.Tree.from_encoding(e) for e in encs]
     n_total = sum(e.n_rows for e in encs)
     u = np.random.default_rng(seed).standard_normal(n_total)

@@ -92,3 +92,17 @@ if tr.mode == "images":
     m = ar.meta
     print("batch shape (median): rows", int(np.median(m["n_rows"])), "pairs", int(np.median(m["n_pairs"])),
           "codes", int(np.median(m["n_codes"])), "derived", int(np.median(m["n_derived"])))
+
+if tr.mode == "parts":
+    L.toc_mgd_parts_set_trace.argtypes = [P]
+    trace = torch.zeros(ar.n_blocks * 8, dtype=torch.int64, device="cuda")
+    N.check(L.toc_mgd_parts_set_trace(trace.data_ptr()), "parts trace")
+    tr.epoch()
+    torch.cuda.synchronize()
+    N.check(L.toc_mgd_parts_set_trace(None), "parts trace off")
+    T = trace.view(-1, 8).cpu().numpy().astype(np.int64)[:, :7]
+    d = np.diff(T, axis=1)
+    names = ["part wait", "p1", "matvec+loss", "vecmat", "gradient REDs+cluster barrier", "update+cluster barrier"]
+    print("cluster", tr.cluster, "phase cycles (median per step):",
+          {n: int(np.median(d[:, i])) for i, n in enumerate(names)})
+    print("step (median cycles):", int(np.median(np.diff(T[:, 0]))))
