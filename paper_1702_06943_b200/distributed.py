@@ -17,6 +17,7 @@ tested) on CPU with the gloo backend; on the device path they are toc_glm_grad a
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass
 from typing import Callable
 
@@ -346,18 +347,28 @@ def train_data_parallel(dataset, config, world: int, rank: int, group=None, grap
     sub = LabeledDataset(features=dataset.features.take_rows(local), labels=dataset.labels[local])
     batches = DeviceBatches(sub, config.batch_size) if len(local) else None
     runner = None
-    if fused:  # the fused NVLink exchange where every rank can run it (decided collectively)
+    if fused and os.environ.get("TOC_DP_FUSED", "1") != "0":
+        # the fused NVLink exchange where every rank can run it (decided collectively, twice: the
+        # step images, then the symmetric-memory rendezvous; any failure -> NCCL on every rank)
         try:
             runner = FusedDPEpoch(batches, plan, config.loss_kind, config.learning_rate, group)
             ok = 1
-        except Exception:  # images do not fit, a rank lacks some step, no symmetric memory
+        except Exception:  # images do not fit, a rank lacks some step
             runner, ok = None, 0
         flag = torch.tensor([ok], dtype=torch.int32, device="cuda")
         dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
         if not int(flag.item()):
             runner = None
         else:
-            runner.connect()
+            try:
+                runner.connect()
+                ok = 1
+            except Exception:  # no symmetric memory / peer access on this node
+                ok = 0
+            flag = torch.tensor([ok], dtype=torch.int32, device="cuda")
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+            if not int(flag.item()):
+                runner = None
     if runner is not None:
         w = runner.w
         trace = LossTrace()
