@@ -342,6 +342,14 @@ def main():
     arena = compress_csr(COLS, rp, c, vals, batch_row)
     torch.cuda.synchronize()
     t_enc = time.perf_counter() - t0
+    # encoder throughput (a second run, device time by CUDA events: the CSR upload, encode,
+    # value index, widths and packing of every batch)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    compress_csr(COLS, rp, c, vals, batch_row)
+    e1.record()
+    e1.synchronize()
+    enc_ms = e0.elapsed_time(e1)
     rng = np.random.default_rng(np.random.SeedSequence([SEED, 7, rank]))
     v_h = rng.standard_normal(COLS)
     u_h = rng.standard_normal(arena.n_rows_total)
@@ -466,6 +474,11 @@ def main():
                 "csr_bytes_per_gpu": int(len(c) * 12 + (len(rp)) * 8),
                 "encode_seconds": t_enc, "generate_seconds": t_gen,
             },
+            "encode": {"ms": enc_ms, "rows_per_s": world * arena.n_rows_total / (enc_ms / 1e3),
+                       "csr_in_bytes": int(len(c) * 12 + len(rp) * 8), "toc1_out_bytes": arena.block_bytes,
+                       "csr_in_gbs": (len(c) * 12 + len(rp) * 8) / (enc_ms / 1e3) / 1e9,
+                       "note": "codec.compress_csr device time (CUDA events), H2D of the CSR inputs included; "
+                               "one CTA per batch, hash tables in global memory (latency-bound, DESIGN.md 4.2)"},
             "memory": memory_line(arena.block_bytes, arena.levels_bytes if slots else arena.tree_bytes, len(c),
                                   len(rp) - 1, COLS, "slot cache (read by every launch)" if slots
                                   else "tree cache (read by every launch)"),
