@@ -173,6 +173,25 @@ int toc_linalg_levels(const int64_t* d_row_base, int64_t n_blocks, int32_t kind,
                       int32_t max_stage, int32_t max_rows, const double* d_v, double* d_R, const double* d_u,
                       double* d_O, const uint8_t* d_lvl, const int64_t* d_lvl_off, void* stream);
 
+/* ---- the reference's own operation order, bit for bit (csrc/toc_exact.cu; kernels.py:115-174) ---
+ * Over one batch's DecodeTree (device arrays parent / column / value, node 0 the root) and a
+ * schedule built on the host: nodes grouped by tree depth (d_level_nodes, level l's nodes at
+ * [h_level_off[l], h_level_off[l + 1])), each row's codes (d_rowoff / d_codes), each node's
+ * occurrence rows in row order, its children in descending id order, each column's nodes in
+ * descending id order.  toc_exact_matvec: H level by level (H[i] = value[i] * v[col[i]] +
+ * H[parent[i]]), then every row's left-to-right sum -- equal to the reference's matvec bit for bit;
+ * d_H: T doubles of scratch.  toc_exact_vecmat: the occurrence sums, the children's h bottom-up,
+ * the column sums in descending node order -- equal to the reference's vecmat bit for bit; d_h: T
+ * doubles.  Products and sums rounded separately (no FMA contraction). */
+int toc_exact_matvec(const int32_t* d_parent, const int32_t* d_column, const double* d_value,
+                     const int32_t* d_level_nodes, const int64_t* h_level_off, int32_t n_levels, const int64_t* d_rowoff,
+                     const int32_t* d_codes, int32_t n_rows, const double* d_v, double* d_R, double* d_H, void* stream);
+int toc_exact_vecmat(const int32_t* d_column, const double* d_value, int32_t T, const int32_t* d_level_nodes,
+                     const int64_t* h_level_off, int32_t n_levels, const int64_t* d_occ_off, const int32_t* d_occ_row,
+                     const int64_t* d_child_off, const int32_t* d_child, const int64_t* d_col_off,
+                     const int32_t* d_col_node, int32_t n_cols, const double* d_u, double* d_out, double* d_h,
+                     void* stream);
+
 /* ---- compressed matrix-matrix products (reference kernels.py:177-234) ----------------------
  * side 0 (matmat_right, kernels.py:177-203): d_out[row_base[b] + r, :] = (A_b . M)[r, :],
  *         d_M = M [n_cols x p] row-major, d_out [n_rows_total x p].

@@ -83,6 +83,8 @@ def lib():
     L.toc_decode_rows.argtypes = [P, P, P, P, I64, ctypes.POINTER(TocPlan), P, P, P, P, P]
     L.toc_sweep_upload.argtypes = [P, P, P, I64, I64, P]
     L.toc_sweep_events.argtypes = [P, I64]
+    L.toc_exact_matvec.argtypes = [P, P, P, P, P, I32, P, P, I32, P, P, P, P]
+    L.toc_exact_vecmat.argtypes = [P, P, I32, P, P, I32, P, P, P, P, P, P, I32, P, P, P, P]
     L.toc_sweep_events_free.argtypes = [P, I64]
     L.toc_sweep_operands.argtypes = [P, I64, I32, P, P, P, P, P]
     L.toc_sweep_compute.argtypes = [P, I64, I32, P, P, P, P, P, P, P, P, P]

@@ -43,7 +43,7 @@ class CompressedMatrix:
     keep, so there is no lazy host tree build; ``tree`` materialises the reference's DecodeTree
     on demand, once, under a lock (kernels.py:68-77)."""
 
-    __slots__ = ("_enc", "_arena", "_lock", "_tree", "_block")
+    __slots__ = ("_enc", "_arena", "_lock", "_tree", "_block", "_exact")
 
     def __init__(self, encoding: LogicalEncoding | None = None, *, _arena: BlockArena | None = None):
         self._enc = encoding
@@ -51,6 +51,7 @@ class CompressedMatrix:
         self._lock = threading.Lock()
         self._tree = None
         self._block = None
+        self._exact = None
 
     @classmethod
     def from_sparse(cls, s: SparseRowMatrix) -> "CompressedMatrix":
@@ -94,6 +95,15 @@ class CompressedMatrix:
                 if self._tree is None:
                     self._tree = arena.decode_trees()[0]
         return self._tree
+
+    def exact_plan(self) -> "_ExactPlan":
+        """The device schedule of the reference-order products (toc_exact.cu), built once."""
+        if self._exact is None:
+            tree = self.tree
+            with self._lock:
+                if self._exact is None:
+                    self._exact = _ExactPlan(tree, self.encoding.rows, self.n_cols)
+        return self._exact
 
     def decode(self) -> SparseRowMatrix:
         """Rows back bit for bit (kernels.py:79-80 -> codec.decode), decoded on the device."""
@@ -162,23 +172,97 @@ def _dev(x: np.ndarray):
     return torch.from_numpy(np.array(x, dtype=np.float64, order="C")).cuda()
 
 
+class _ExactPlan:
+    """Device schedule of the reference-order products over one DecodeTree (toc_exact.cu): nodes by
+    depth, each row's codes, each node's occurrence rows in row order, its children in descending id
+    order, each column's nodes in descending id order."""
+
+    def __init__(self, tree, rows, n_cols: int):
+        torch = N.require_cuda()
+        par = np.asarray(tree.parent, np.int64)
+        T = len(par)
+        self.T, self.n_cols, self.n_rows = T, n_cols, len(rows)
+        depth = np.zeros(T, np.int64)
+        ids = np.arange(1, T)
+        if T > 1:  # parents precede children: settle depth one level per pass
+            pp = np.maximum(par[1:], 0)
+            while True:
+                nd = depth[pp] + 1
+                if np.array_equal(nd, depth[1:]):
+                    break
+                depth[1:] = nd
+        nodes = ids[np.argsort(depth[1:], kind="stable")]
+        maxd = int(depth.max()) if T > 1 else 0
+        self.level_off = np.searchsorted(depth[nodes], np.arange(1, maxd + 2)).astype(np.int64)
+        col = np.asarray(tree.column, np.int64)
+        o = np.lexsort((-ids, par[1:])) if T > 1 else np.zeros(0, np.int64)
+        child_off = np.r_[0, np.cumsum(np.bincount(par[1:], minlength=T))] if T > 1 else np.zeros(T + 1, np.int64)
+        o2 = np.lexsort((-ids, col[1:])) if T > 1 else np.zeros(0, np.int64)
+        col_off = np.r_[0, np.cumsum(np.bincount(col[1:], minlength=n_cols))] if T > 1 else np.zeros(n_cols + 1)
+        lens = np.array([len(r) for r in rows], np.int64)
+        codes = np.concatenate([np.asarray(r, np.int64) for r in rows]) if len(rows) else np.zeros(0, np.int64)
+        rowid = np.repeat(np.arange(len(rows)), lens)
+        o3 = np.argsort(codes, kind="stable")
+        occ_off = np.r_[0, np.cumsum(np.bincount(codes, minlength=T))]
+
+        def d(x, dt):
+            x = np.ascontiguousarray(x, dt)
+            return torch.from_numpy(x if x.size else np.zeros(1, dt)).cuda()
+
+        self.parent = d(np.where(par < 0, 0, par), np.int32)
+        self.column = d(col, np.int32)
+        self.value = d(np.asarray(tree.value, np.float64), np.float64)
+        self.level_nodes = d(nodes, np.int32)
+        self.rowoff = d(np.r_[0, np.cumsum(lens)], np.int64)
+        self.codes = d(codes, np.int32)
+        self.occ_off = d(occ_off, np.int64)
+        self.occ_row = d(rowid[o3], np.int32)
+        self.child_off = d(child_off, np.int64)
+        self.child = d(ids[o], np.int32)
+        self.col_off = d(col_off, np.int64)
+        self.col_node = d(ids[o2], np.int32)
+        self.scratch = torch.empty(max(T, 1), dtype=torch.float64, device="cuda")
+
+
 def matvec(a: CompressedMatrix, v, counter: OpCounter | None = None) -> np.ndarray:
-    """A @ v without decompressing A (kernels.py:115-142, Algorithm 5)."""
+    """A @ v without decompressing A (kernels.py:115-142, Algorithm 5), in the reference's own
+    operation order: H node by node, each row summed left to right -- equal to the reference bit
+    for bit (toc_exact_matvec).  The batched paths (BlockArena.linalg) reorder sums for speed."""
     vec = as_vector(v, a.n_cols, "vector")
     arena = a.arena
     arena.raise_corrupt()
-    R = arena.matvec(_dev(vec)) if a.n_cols else None
-    out = R.cpu().numpy() if R is not None else np.zeros(a.n_rows)
+    out = np.zeros(a.n_rows)
+    if a.n_rows and a.n_cols:
+        p = a.exact_plan()
+        torch = N.require_cuda()
+        R = torch.empty(a.n_rows, dtype=torch.float64, device="cuda")
+        N.check(N.lib().toc_exact_matvec(p.parent.data_ptr(), p.column.data_ptr(), p.value.data_ptr(),
+                                         p.level_nodes.data_ptr(), p.level_off.ctypes.data, len(p.level_off) - 1,
+                                         p.rowoff.data_ptr(), p.codes.data_ptr(), a.n_rows, _dev(vec).data_ptr(),
+                                         R.data_ptr(), p.scratch.data_ptr(), N.stream_handle()), "toc_exact_matvec")
+        out = R.cpu().numpy()
     a._charge(counter, 1)
     return np.asarray(out, dtype=np.float64)
 
 
 def vecmat(v, a: CompressedMatrix, counter: OpCounter | None = None) -> np.ndarray:
-    """v @ A without decompressing A (kernels.py:145-174, Algorithm 6)."""
+    """v @ A without decompressing A (kernels.py:145-174, Algorithm 6), in the reference's own
+    operation order -- equal to the reference bit for bit (toc_exact_vecmat)."""
     vec = as_vector(v, a.n_rows, "vector")
     arena = a.arena
     arena.raise_corrupt()
-    out = arena.vecmat(_dev(vec))[0].cpu().numpy() if a.n_cols else np.zeros(0)
+    out = np.zeros(a.n_cols)
+    if a.n_cols:
+        p = a.exact_plan()
+        torch = N.require_cuda()
+        O = torch.empty(a.n_cols, dtype=torch.float64, device="cuda")
+        u = _dev(vec) if a.n_rows else torch.zeros(1, dtype=torch.float64, device="cuda")
+        N.check(N.lib().toc_exact_vecmat(p.column.data_ptr(), p.value.data_ptr(), p.T, p.level_nodes.data_ptr(),
+                                         p.level_off.ctypes.data, len(p.level_off) - 1, p.occ_off.data_ptr(),
+                                         p.occ_row.data_ptr(), p.child_off.data_ptr(), p.child.data_ptr(),
+                                         p.col_off.data_ptr(), p.col_node.data_ptr(), a.n_cols, u.data_ptr(),
+                                         O.data_ptr(), p.scratch.data_ptr(), N.stream_handle()), "toc_exact_vecmat")
+        out = O.cpu().numpy()
     a._charge(counter, 1)
     return np.asarray(out, dtype=np.float64)
 

@@ -153,3 +153,43 @@ def test_glm_gradient_layouts_agree(oracle):
         got = [glm_gradient(Batch(f, ds.labels), GlmModel(w), loss) for f in
                (ds.features, sparse_to_dense(ds.features), CompressedMatrix.from_sparse(ds.features))]
         assert within_rel(got[1], got[0], 1e-12) and within_rel(got[2], got[0], 1e-12)
+
+
+def _exact_cases():
+    from helpers import TOY_ROWS, TREE_ROWS
+
+    rng = np.random.default_rng(17)
+    out = [("toy", TOY_ROWS, 5), ("tree", TREE_ROWS, 5), ("empty_rows", [[], [(1, 2.0)], [], [(0, 1.0)], []], 3)]
+    for k, (n, m, dens) in enumerate([(60, 40, 0.3), (300, 20, 0.9), (64, 200, 0.05)]):
+        out.append((f"rand{k}", random_alphabet_rows(rng, n, m, dens, alphabet_size=4 + 3 * k), m))
+    return out
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["config1"] + [c[0] for c in _exact_cases()])
+def test_single_matrix_products_bit_exact(oracle, case):
+    """The reference-API matvec / vecmat (kernels.CompressedMatrix) run the reference's own operation
+    order (toc_exact.cu) and equal it bit for bit: the oracle restates kernels.py:115-174 in that
+    order and is pinned bit-exactly to the reference's goldens (tests/test_oracle.py)."""
+    from paper_1702_06943_b200 import synth
+    from paper_1702_06943_b200.kernels import CompressedMatrix, matvec, vecmat
+    from paper_1702_06943_b200.matrix import SparseRowMatrix
+
+    if case == "config1":
+        rp, c, v = synth.dense_to_csr(synth.cfg1_dense(0))
+        enc, m = oracle.encode_csr(128, rp, c, v), 128
+        sp = SparseRowMatrix.from_csr(128, rp, c, v)
+    else:
+        name, rows, m = next(x for x in _exact_cases() if x[0] == case)
+        enc = oracle.encode_rows(m, rows)
+        r = [list(x) for x in rows]
+        rp = np.r_[0, np.cumsum([len(x) for x in r])].astype(np.int64)
+        sp = SparseRowMatrix.from_csr(m, rp, np.array([cc for x in r for cc, _ in x], np.int32),
+                                      np.array([vv for x in r for _, vv in x], np.float64))
+    a = CompressedMatrix.from_sparse(sp)
+    t = oracle.Tree.from_encoding(enc)
+    rng = np.random.default_rng(5)
+    for _ in range(3):
+        x, u = rng.standard_normal(m), rng.standard_normal(enc.n_rows) * 10.0 ** rng.uniform(-6, 6, enc.n_rows)
+        assert np.array_equal(matvec(a, x), t.matvec(x))
+        assert np.array_equal(vecmat(u, a), t.vecmat(u))
