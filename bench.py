@@ -693,17 +693,19 @@ def run_e2e(torch, arena, v_h, u_h, steps: int, world: int = 1):
                                         arena.block_off, arena.block_len)
     out = (torch.empty(sweep.n_rows, dtype=torch.float64).pin_memory(),  # the caller's pinned result buffers
            torch.empty((sweep.n_blocks, sweep.n_cols), dtype=torch.float64).pin_memory())
+    vh, uh = torch.from_numpy(v_h).pin_memory(), torch.from_numpy(u_h).pin_memory()  # pinned operands
     for _ in range(2):
-        sweep.run(v_h, u_h, out=out)
+        sweep.run(vh, uh, out=out)
     t0 = _wall_start(torch, world)
     for _ in range(steps):
-        sweep.run(v_h, u_h, out=out)
+        sweep.run(vh, uh, out=out)
     dt = _wall_max(torch, time.perf_counter() - t0, world)
     link = h2d_link_gbs(torch, sweep.h2d_bytes)
     achieved = sweep.h2d_bytes * steps / dt / 1e9
     return {"value": world * sweep.n_rows * steps / dt, "unit": "rows/s", "h2d_bytes_per_step": sweep.h2d_bytes,
             "d2h_bytes_per_step": sweep.d2h_bytes,
-            "api": "paper_1702_06943_b200.kernels.BatchSweep.run(v, u, out=(R, O)) into the caller's pinned buffers",
+            "api": "paper_1702_06943_b200.kernels.BatchSweep.run(v, u, out=(R, O)): pinned host v / u in, results "
+                   "into the caller's pinned buffers",
             "h2d_gbs": achieved, "h2d_link_gbs": link, "link_frac": achieved / link if link else None,
             "link_note": "h2d_link_gbs: one pinned host->device copy of the same byte count, best of 5 "
                          "(CUDA events); the streamed TOC1 upload bounds this e2e number"}

@@ -328,11 +328,11 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
       __syncthreads();
       TOC_LVL_STAMP(1);
       // push: each inner slot's own T goes to every pair slot of its chain
-      for (uint32_t y = tid; y < nQ; y += nth) {
-        const uint32_t x = nP + 1 + y;
-        uint32_t rec = inner_s[y];
-        TOC_CHECK((rec >> 16) >= 1 && (rec >> 16) <= nP && (rec & 0xffffu) >= 1 && (rec & 0xffffu) < x);
-        if (!f64) {
+      if (!f64) {
+        for (uint32_t y = tid; y < nQ; y += nth) {
+          const uint32_t x = nP + 1 + y;
+          uint32_t rec = inner_s[y];
+          TOC_CHECK((rec >> 16) >= 1 && (rec >> 16) <= nP && (rec & 0xffffu) >= 1 && (rec & 0xffffu) < x);
           const uint32_t l = lo_s[x];
           const int32_t hh = hi_s[x];
           if (l | (uint32_t)hh) {
@@ -346,8 +346,11 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
             }
             limb_add(lo_s, hi_s, p, l, hh);
           }
-        } else {
-          const double t = Tf[x];
+        }
+      } else {
+        for (uint32_t y = tid; y < nQ; y += nth) {
+          uint32_t rec = inner_s[y];
+          const double t = Tf[nP + 1 + y];
           if (t != 0.0) {
             uint32_t p = rec & 0xffffu;
             atomicAdd(Tf + (rec >> 16), t);
@@ -373,18 +376,21 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
         if (p0 < p1) {
           bool here = colst_s[prs_s[p0 - 1] & 0xffffu] == p0;
           double acc = 0.0;
-          for (uint32_t p = p0; p < p1; ++p) {
-            const uint32_t x = prs_s[p - 1];
-            TOC_CHECK(((x >> 16) & 0x7fffu) < h.nU && (x & 0xffffu) < ncol);
-            const double t = f64 ? Tf[p] : limb_value(lo_s[p], hi_s[p], L, g_inv);
-            acc += uniq_s[(x >> 16) & 0x7fffu] * t;
-            if (x >> 31) {  // last pair slot of its column
-              if (here) o[x & 0xffffu] = acc;
-              else head_s[tid] = acc;
-              acc = 0.0;
-              here = true;
+          auto pass = [&](auto tval) {  // one loop per accumulation mode (no per-pair select)
+            for (uint32_t p = p0; p < p1; ++p) {
+              const uint32_t x = prs_s[p - 1];
+              TOC_CHECK(((x >> 16) & 0x7fffu) < h.nU && (x & 0xffffu) < ncol);
+              acc += uniq_s[(x >> 16) & 0x7fffu] * tval(p);
+              if (x >> 31) {  // last pair slot of its column
+                if (here) o[x & 0xffffu] = acc;
+                else head_s[tid] = acc;
+                acc = 0.0;
+                here = true;
+              }
             }
-          }
+          };
+          if (f64) pass([&](uint32_t p) { return Tf[p]; });
+          else pass([&](uint32_t p) { return limb_value(lo_s[p], hi_s[p], L, g_inv); });
           tail_s[tid] = acc;
         }
       }

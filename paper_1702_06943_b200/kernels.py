@@ -397,7 +397,8 @@ class BatchSweep:
             pass
 
     def run(self, v, u, out=None):
-        """The first chunk's block bytes are enqueued and stream in while the host prepares v / u;
+        """The first chunk's block bytes are enqueued (two chunks when v / u must be staged into
+        pinned buffers first; v and u given as pinned float64 CPU tensors are copied from in place);
         then the operands, the other chunks' bytes (all on one copy stream: host -> device copies
         are served in submission order), every chunk's validation and fused A.v + v^T.A (each as
         soon as its bytes and operands are in) and the result downloads (toc_sweep.cu).
@@ -411,13 +412,26 @@ class BatchSweep:
         for st in (cs, comp, ds):
             st.wait_stream(caller)  # the caller's earlier work on these buffers is done
         n = len(self.chunks)
-        N.check(L.toc_sweep_upload(self.host.data_ptr(), self.dev.data_ptr(), self.cdesc, 0, min(n, 1), cs.cuda_stream),
+
+        def pinned(x, size):  # the caller's own pinned float64 vector: copied from in place
+            return (isinstance(x, torch.Tensor) and x.device.type == "cpu" and x.dtype == torch.float64
+                    and x.dim() == 1 and x.numel() == size and x.is_contiguous() and x.is_pinned())
+
+        direct = pinned(v, self.n_cols) and pinned(u, self.n_rows)
+        # with staged operands the host copies v / u into pinned buffers first: two chunks go ahead
+        # so the link stays busy meanwhile; pinned operands follow the first chunk at once
+        k_first = min(n, 1 if direct else 2)
+        N.check(L.toc_sweep_upload(self.host.data_ptr(), self.dev.data_ptr(), self.cdesc, 0, k_first, cs.cuda_stream),
                 "toc_sweep_upload")
-        self.v_h.numpy()[: self.n_cols] = as_vector(v, self.n_cols, "vector")
-        self.u_h.numpy()[: self.n_rows] = as_vector(u, self.n_rows, "vector")
-        N.check(L.toc_sweep_operands(self.cdesc, n, self.n_cols, self.v_h.data_ptr(), self.v_d.data_ptr(),
-                                     self.u_h.data_ptr(), self.u_d.data_ptr(), cs.cuda_stream), "toc_sweep_operands")
-        N.check(L.toc_sweep_upload(self.host.data_ptr(), self.dev.data_ptr(), self.cdesc, min(n, 1), n, cs.cuda_stream),
+        if direct:
+            v_src, u_src = v.data_ptr(), u.data_ptr()
+        else:
+            self.v_h.numpy()[: self.n_cols] = as_vector(v, self.n_cols, "vector")
+            self.u_h.numpy()[: self.n_rows] = as_vector(u, self.n_rows, "vector")
+            v_src, u_src = self.v_h.data_ptr(), self.u_h.data_ptr()
+        N.check(L.toc_sweep_operands(self.cdesc, n, self.n_cols, v_src, self.v_d.data_ptr(), u_src,
+                                     self.u_d.data_ptr(), cs.cuda_stream), "toc_sweep_operands")
+        N.check(L.toc_sweep_upload(self.host.data_ptr(), self.dev.data_ptr(), self.cdesc, k_first, n, cs.cuda_stream),
                 "toc_sweep_upload")
         if out is not None:
             R_o, O_o = out

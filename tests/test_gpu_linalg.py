@@ -173,6 +173,12 @@ def test_batch_sweep_public_api(oracle):
     other = BatchSweep.from_host_blocks(host, arena.block_off, arena.block_len, chunks=3)  # its own events
     R2, O2 = other.run(x, u)
     assert np.array_equal(R2, R0) and np.array_equal(O2, O0)
+    # pinned float64 operands are copied from in place (no staging); same results
+    xp, up = torch.from_numpy(x).pin_memory(), torch.from_numpy(u).pin_memory()
+    R3, O3 = sweep.run(xp, up)
+    assert np.array_equal(R3, R0) and np.array_equal(O3, O0)
+    with pytest.raises(ValueError):  # a wrong length is still refused (through the staging path)
+        sweep.run(xp[:-1], up)
 
 
 @pytest.mark.parametrize("kind", [1, 2, 3])
