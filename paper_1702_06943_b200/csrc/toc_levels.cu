@@ -21,6 +21,7 @@
 //     prs    u32[nP]    column | value ref << 16 of pair slot 1 + i
 //     inner  u32[nQ]    slot(par) | slot(key) << 16 of inner slot nP + 1 + q   (key is a pair)
 //     colst  u16[n_cols + 1]  first pair slot of every column (pairs are column-sorted)
+//     trow   u16[T]     row of thread t's first code | (the code starts its row) << 15
 //   stream u32[T*K]  per code in row order: slot a | row-end flag | slot b << 16 -- a = the code's
 //                    own slot (b = 0), or a = slot(par), b = slot(key) for a leaf; thread t owns
 //                    codes [t*K, t*K + K), stored interleaved in groups of four so a warp's 16-byte
@@ -56,7 +57,7 @@ struct LvlHdr {
   uint32_t C, K, T;    // codes, codes per thread (a multiple of 4), threads
   uint32_t n_rows, n_cols, nU;
   uint32_t off_uniq, off_rowoff, off_prs, off_inner, off_colst, off_stream;
-  uint32_t pad;
+  uint32_t off_trow;
   double vmax;  // max |value| of the value index (fixed-point precision check)
 };
 static_assert(sizeof(LvlHdr) == 72, "slot cache header");
@@ -69,17 +70,18 @@ struct LvlSmem {
   uint32_t red, v, u, part, rowcur, stage, tab, total;
 };
 
+// The fixed-size regions come first, at compile-time offsets (no address arithmetic from kernel
+// parameters in the loops that use them): mbarrier | sum |u| partials | head / tail partials | u.
+constexpr uint32_t kRedOff = 16, kPartOff = kRedOff + 48 * 8, kUOff = kPartOff + 16u * kLvlThreads;
+
 TOC_HD LvlSmem lvl_smem(int kind, uint32_t n_cols, uint32_t max_slots, uint32_t max_stage, uint32_t max_rows) {
   LvlSmem L;
-  uint32_t o = 16;  // mbarrier
-  L.red = o;
-  o += 48 * 8;  // sum |u| partials and total
+  L.red = kRedOff;  // sum |u| partials and total
+  L.part = kPartOff;  // head / tail partials (rows, columns)
+  L.u = kUOff;
+  uint32_t o = kUOff + ((kind & TOC_VECMAT) ? align16(8u * max_rows) : 0u);
   L.v = o;
   o += (kind & TOC_MATVEC) ? align16(8u * n_cols) : 0u;
-  L.u = o;
-  o += (kind & TOC_VECMAT) ? align16(8u * max_rows) : 0u;
-  L.part = o;
-  o += 16u * kLvlThreads;  // head / tail partials (rows, columns)
   L.rowcur = o;
   o += (kind & TOC_MATVEC) ? align16(4u * (max_rows + 1)) : 0u;
   L.stage = o;
@@ -148,8 +150,9 @@ TOC_D void walk_stream(const uint4* __restrict__ st, uint32_t nth, uint32_t K, u
   }
 }
 
-#define TOC_LVL_STAMP(k)                                                     \
-  if (g_trace && blockIdx.x == 0 && tid == 0 && b < 64 * (int64_t)gridDim.x) \
+#define TOC_LVL_STAMP(k)                                                                      \
+  if constexpr (kTrace)                                                                       \
+    if (g_trace && blockIdx.x == 0 && tid == 0 && b < 64 * (int64_t)gridDim.x) \
   g_trace[(b / gridDim.x) * 10 + (k)] = clock64()
 
 // Stage entry bn (header + value index + row offsets + pair / inner records + column starts) into
@@ -202,7 +205,7 @@ TOC_D void su_store(double su, double* s_red) {
 //   VM  zero T for the next batch (beside the row totals)
 // The next batch's staged region is copied in while the A.v rows run (the rows read only the
 // stream, H and a private copy of the row offsets).
-template <int kKind>
+template <int kKind, bool kTrace>
 __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
   constexpr bool MV = kKind & TOC_MATVEC, VM = kKind & TOC_VECMAT;
   extern __shared__ __align__(16) uint8_t smem[];
@@ -210,10 +213,10 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
   const uint32_t ncol = (uint32_t)a.n_cols;
   const LvlSmem& SL = a.sl;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
-  double* s_red = reinterpret_cast<double*>(smem + SL.red);  // [0, 32) partials; [32] this batch's sum |u|
+  double* s_red = reinterpret_cast<double*>(smem + kRedOff);  // [0, 32) partials; [32] this batch's sum |u|
   double* v_s = reinterpret_cast<double*>(smem + SL.v);
-  double* u_s = reinterpret_cast<double*>(smem + SL.u);  // this batch's u (v^T.A row weights)
-  double* head_s = reinterpret_cast<double*>(smem + SL.part);
+  double* u_s = reinterpret_cast<double*>(smem + kUOff);  // this batch's u (v^T.A row weights)
+  double* head_s = reinterpret_cast<double*>(smem + kPartOff);
   double* tail_s = head_s + kLvlThreads;
   uint32_t* rowcur_s = reinterpret_cast<uint32_t*>(smem + SL.rowcur);
   uint8_t* stage = smem + SL.stage;
@@ -265,8 +268,10 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
     const uint4* stream = reinterpret_cast<const uint4*>(a.lvl + a.lvl_off[b] + h.off_stream) + tid;
     const bool active = tid * K < h.C;
     uint4 w0 = active ? __ldg(stream) : z4, w1 = active && K > 4 ? __ldg(stream + nth) : z4;
-    const uint32_t r0 = active ? row_of(rowoff_s, n, tid * K) : 0u;  // this thread's first row
-    const bool here0 = active && rowoff_s[r0] == tid * K;
+    const uint32_t tr0 = active ? reinterpret_cast<const uint16_t*>(stage + h.off_trow)[tid] : 0u;
+    const uint32_t r0 = tr0 & 0x7fffu;  // this thread's first row, and whether its range starts it
+    const bool here0 = (tr0 >> 15) != 0;
+    TOC_CHECK(!active || (r0 == row_of(rowoff_s, n, tid * K) && here0 == (rowoff_s[r0] == tid * K)));
     UPrefetch pre;  // the next batch's u (v^T.A)
     if (VM && has_next) pre.bounds(a, bn);
 
@@ -596,7 +601,7 @@ int build_entry(const uint8_t* blk, const TocBlockMeta& m, LvlEntry& out) {
   if (m.corrupt) return TOC_E_CORRUPT;
   const uint32_t n = m.n_rows, nI = m.n_pairs, C = m.n_codes, nU = m.n_uniques;
   const uint64_t NT = 1ull + nI + m.n_derived;
-  if (NT > (1ull << 26) || m.n_cols > 65536u || nU > 32768u || nI >= 32767u) return TOC_E_ARG;
+  if (NT > (1ull << 26) || m.n_cols > 65536u || nU > 32768u || nI >= 32767u || n >= 32768u) return TOC_E_ARG;
   std::vector<uint32_t> off(n + 1), code(C);
   for (uint32_t r = 0; r <= n; ++r) off[r] = rd_packed(blk + m.off_offsets, r, m.w_offsets);
   for (uint32_t j = 0; j < C; ++j) code[j] = rd_packed(blk + m.off_codes, j, m.w_codes);
@@ -661,6 +666,7 @@ int build_entry(const uint8_t* blk, const TocBlockMeta& m, LvlEntry& out) {
   hd.off_prs = sec(4ull * nI);
   hd.off_inner = sec(4ull * nQ);
   hd.off_colst = sec(2ull * (m.n_cols + 1));
+  hd.off_trow = sec(2ull * T);
   hd.off_stream = sec(4ull * T * K);
   out.bytes.assign(o, 0);
   uint8_t* e = out.bytes.data();
@@ -695,6 +701,11 @@ int build_entry(const uint8_t* blk, const TocBlockMeta& m, LvlEntry& out) {
       rowid[j] = r;
     }
   schedule_banks(rec, rowid, off, n, C, K, T);
+  uint16_t* tr = reinterpret_cast<uint16_t*>(e + hd.off_trow);
+  for (uint32_t t = 0; t < T && (uint64_t)t * K < C; ++t) {
+    const uint32_t r = rowid[t * K];
+    tr[t] = (uint16_t)(r | (off[r] == t * K ? 0x8000u : 0u));
+  }
   uint32_t* st = reinterpret_cast<uint32_t*>(e + hd.off_stream);
   for (uint32_t j = 0; j < C; ++j) {
     const uint32_t r = rowid[j];
@@ -711,6 +722,8 @@ int build_entry(const uint8_t* blk, const TocBlockMeta& m, LvlEntry& out) {
   out.n_rows = n;
   return TOC_OK;
 }
+
+std::atomic<bool> g_lvl_traced{false};  // toc_levels_set_trace: launch the stamped kernel instances
 
 }  // namespace
 
@@ -772,7 +785,9 @@ extern "C" int toc_levels_set_prefetch(int mode) {
 }
 
 extern "C" int toc_levels_set_trace(long long* d_trace) {
-  return cudaMemcpyToSymbol(toc::g_trace, &d_trace, sizeof d_trace) == cudaSuccess ? TOC_OK : TOC_E_CUDA;
+  if (cudaMemcpyToSymbol(toc::g_trace, &d_trace, sizeof d_trace) != cudaSuccess) return TOC_E_CUDA;
+  g_lvl_traced.store(d_trace != nullptr);  // the stamped kernel instance is launched only then
+  return TOC_OK;
 }
 
 extern "C" void toc_levels_free(void* handle) { delete static_cast<LvlCache*>(handle); }
@@ -801,9 +816,11 @@ extern "C" int toc_linalg_levels(const int64_t* d_row_base, int64_t n_blocks, in
   if (smem < 0 || smem > optin) return TOC_E_ARG;
   toc::LvlArgs a{toc::lvl_smem(kind, (uint32_t)n_cols, (uint32_t)max_slots, (uint32_t)max_stage, (uint32_t)max_rows),
                  d_row_base, n_blocks, kind, n_cols, max_slots, max_stage, max_rows, d_lvl, d_lvl_off, d_v, d_R, d_u, d_O};
-  void* fn = kind == TOC_MATVEC   ? (void*)toc::levels_kernel<TOC_MATVEC>
-             : kind == TOC_VECMAT ? (void*)toc::levels_kernel<TOC_VECMAT>
-                                  : (void*)toc::levels_kernel<TOC_MATVEC | TOC_VECMAT>;
+  const bool tr = g_lvl_traced.load();
+  void* fn = kind == TOC_MATVEC   ? (tr ? (void*)toc::levels_kernel<TOC_MATVEC, true> : (void*)toc::levels_kernel<TOC_MATVEC, false>)
+             : kind == TOC_VECMAT ? (tr ? (void*)toc::levels_kernel<TOC_VECMAT, true> : (void*)toc::levels_kernel<TOC_VECMAT, false>)
+             : (tr ? (void*)toc::levels_kernel<TOC_MATVEC | TOC_VECMAT, true>
+                   : (void*)toc::levels_kernel<TOC_MATVEC | TOC_VECMAT, false>);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return TOC_E_CUDA;
   const int64_t grid = std::min<int64_t>(n_blocks, sms > 0 ? sms : 148);

@@ -22,7 +22,7 @@ from helpers import TOY_ROWS, TREE_ROWS, random_alphabet_rows
 
 REL = 1e-9
 HDR = ["nP", "nQ", "S", "C", "K", "T", "n_rows", "n_cols", "nU", "off_uniq", "off_rowoff", "off_prs", "off_inner",
-       "off_colst", "off_stream", "pad"]
+       "off_colst", "off_stream", "off_trow"]
 
 
 def host_meta(block: bytes, N):
@@ -96,6 +96,7 @@ def entry(buf, o):
     h["colst"] = np.frombuffer(buf, np.uint16, h["n_cols"] + 1, o + h["off_colst"]).astype(np.int64)
     h["uniq"] = np.frombuffer(buf, np.float64, h["nU"], o + h["off_uniq"]).copy()
     h["rowoff"] = u32(h["off_rowoff"], h["n_rows"] + 1)
+    h["trow"] = np.frombuffer(buf, np.uint16, T, o + h["off_trow"]).astype(np.int64)
     return h
 
 
@@ -207,6 +208,10 @@ def structure(h, enc):
     assert np.array_equal((h["stream"] & 0x8000) != 0, ends), "row-end flags"
     cs = h["colst"]
     assert cs[0] == 1 and cs[-1] == nP + 1 and np.all(np.diff(cs) >= 0)
+    starts = np.arange(0, h["C"], h["K"])  # each thread's first code: its row, and whether it starts it
+    rows = np.searchsorted(off, starts, side="right") - 1
+    assert np.array_equal(h["trow"][: len(starts)] & 0x7FFF, rows)
+    assert np.array_equal(h["trow"][: len(starts)] >> 15, (off[rows] == starts).astype(np.int64))
     cols = h["prs"] & 0xFFFF
     for c in np.unique(cols):
         assert np.all(cols[cs[c] - 1:cs[c + 1] - 1] == c)
