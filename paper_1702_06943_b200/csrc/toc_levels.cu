@@ -67,7 +67,7 @@ TOC_HD uint32_t align4(uint32_t x) { return (x + 3u) & ~3u; }
 
 // Shared-memory layout (bytes from the dynamic base).
 struct LvlSmem {
-  uint32_t red, v, u, part, rowcur, stage, tab, total;
+  uint32_t red, v, u, wt, part, rowcur, stage, tab, total;
 };
 
 // The fixed-size regions come first, at compile-time offsets (no address arithmetic from kernel
@@ -80,6 +80,8 @@ TOC_HD LvlSmem lvl_smem(int kind, uint32_t n_cols, uint32_t max_slots, uint32_t 
   L.part = kPartOff;  // head / tail partials (rows, columns)
   L.u = kUOff;
   uint32_t o = kUOff + ((kind & TOC_VECMAT) ? align16(8u * max_rows) : 0u);
+  L.wt = o;  // each row's fixed-point weight (v^T.A)
+  o += (kind & TOC_VECMAT) ? align16(8u * max_rows) : 0u;
   L.v = o;
   o += (kind & TOC_MATVEC) ? align16(8u * n_cols) : 0u;
   L.rowcur = o;
@@ -199,6 +201,22 @@ TOC_D void su_store(double su, double* s_red) {
   if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = su;
 }
 
+// The fixed-point weight of every row of the batch whose u is in u_s (limb_add's two words, see
+// limb_scale): each warp sums the sum |u| partials itself, then thread r converts u[r].  Thread 0
+// keeps the batch's sum |u| in s_red[32].
+TOC_D void row_weights(double* s_red, const double* u_s, uint2* wt_s, uint32_t n) {
+  const uint32_t lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const double su = warp_sum(lane < nwarps ? s_red[lane] : 0.0);
+  const uint32_t L = limb_bits(n);
+  const double g = limb_scale(su, L);
+  for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) {
+    const long long w = __double2ll_rn(u_s[r] * g);
+    const int32_t xh = (int32_t)(w >> L);
+    wt_s[r] = make_uint2((uint32_t)(w - ((long long)xh << L)), (uint32_t)xh);
+  }
+  if (threadIdx.x == 0) s_red[32] = su;
+}
+
 // Per batch, phases separated by block barriers (MV: A.v, VM: v^T.A):
 //   VM  scatter T  |  push  |  column partials  |  column totals, next batch's sum |u|
 //   MV  P1 (beside the column totals)  |  inner H  |  row partials  |  row totals
@@ -209,13 +227,14 @@ template <int kKind, bool kTrace>
 __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
   constexpr bool MV = kKind & TOC_MATVEC, VM = kKind & TOC_VECMAT;
   extern __shared__ __align__(16) uint8_t smem[];
-  const uint32_t tid = threadIdx.x, nth = blockDim.x, warp = tid >> 5, nwarps = nth >> 5;
+  const uint32_t tid = threadIdx.x, nth = blockDim.x;
   const uint32_t ncol = (uint32_t)a.n_cols;
   const LvlSmem& SL = a.sl;
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem);
   double* s_red = reinterpret_cast<double*>(smem + kRedOff);  // [0, 32) partials; [32] this batch's sum |u|
   double* v_s = reinterpret_cast<double*>(smem + SL.v);
   double* u_s = reinterpret_cast<double*>(smem + kUOff);  // this batch's u (v^T.A row weights)
+  uint2* wt_s = reinterpret_cast<uint2*>(smem + SL.wt);    // and its rows' fixed-point weights
   double* head_s = reinterpret_cast<double*>(smem + kPartOff);
   double* tail_s = head_s + kLvlThreads;
   uint32_t* rowcur_s = reinterpret_cast<uint32_t*>(smem + SL.rowcur);
@@ -234,19 +253,15 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
   __syncthreads();
   if (b < a.n_blocks) {
     if (tid == 0) issue_stage(a, b, stage, mbar);
-    if (VM) {
-      UPrefetch p0;
-      p0.bounds(a, b);
-      p0.load(a);
-      su_store(p0.stash(a, u_s), s_red);
-    }
+  }
+  UPrefetch p0;
+  if (VM && b < a.n_blocks) {
+    p0.bounds(a, b);
+    p0.load(a);
+    su_store(p0.stash(a, u_s), s_red);
   }
   __syncthreads();
-  if (VM && warp == 0) {
-    double su = (tid & 31) < nwarps ? s_red[tid & 31] : 0.0;
-    su = warp_sum(su);
-    if (tid == 0) s_red[32] = su;
-  }
+  if (VM && b < a.n_blocks) row_weights(s_red, u_s, wt_s, p0.n);
   __syncthreads();
 
   for (; b < a.n_blocks; b += gridDim.x) {
@@ -288,9 +303,9 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
         uint32_t r = r0;
         if (!f64) {
           auto weight = [&](uint32_t row, uint32_t& xl, int32_t& xh) {
-            const long long w = __double2ll_rn(u_s[row] * g_scale);
-            xh = (int32_t)(w >> L);
-            xl = (uint32_t)(w - ((long long)xh << L));
+            const uint2 q = wt_s[row];
+            xl = q.x;
+            xh = (int32_t)q.y;
           };
           uint32_t xl;
           int32_t xh;
@@ -497,13 +512,9 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
         }
       }
     }
-    if (VM) {  // a zero T table and the next batch's sum |u| (partials written before a barrier)
+    if (VM) {  // a zero T table and the next batch's row weights (its u and partials are in)
       for (uint32_t i = tid; i < S4max / 2; i += nth) reinterpret_cast<uint4*>(tabp)[i] = z4;
-      if (warp == 0) {
-        double su = (tid & 31) < nwarps ? s_red[tid & 31] : 0.0;
-        su = warp_sum(su);
-        if (tid == 0) s_red[32] = su;
-      }
+      if (has_next) row_weights(s_red, u_s, wt_s, pre.n);
     }
     __syncthreads();  // tables and partials are reused by the next batch
     TOC_LVL_STAMP(7);
