@@ -19,10 +19,11 @@
 //     uniq   f64[nU]    the block's value index (physical.py:49-130), aligned
 //     rowoff u32[n+1]   row offsets into the code stream
 //     prs    u32[nP]    column | value ref << 16 of pair slot 1 + i
-//     inner  u32[nQ]    slot(par) | slot(key) << 16 of inner slot nP + 1 + q   (key is a pair)
+//     inner  u32[nQ]    ref(par) | ref(key) << 16 of inner slot nP + 1 + q   (key is a pair; a
+//                       reference is the slot's low-limb word index, see slot_ref)
 //     colst  u16[n_cols + 1]  first pair slot of every column (pairs are column-sorted)
 //     trow   u16[T]     row of thread t's first code | (the code starts its row) << 15
-//   stream u32[T*K]  per code in row order: slot a | row-end flag | slot b << 16 -- a = the code's
+//   stream u32[T*K]  per code in row order: ref a | row-end flag | ref b << 16 -- a = the code's
 //                    own slot (b = 0), or a = slot(par), b = slot(key) for a leaf; thread t owns
 //                    codes [t*K, t*K + K), stored interleaved in groups of four so a warp's 16-byte
 //                    loads are contiguous
@@ -114,9 +115,36 @@ __constant__ int g_prefetch_mode = 1;
 __constant__ long long* g_trace = nullptr;
 
 
-// Stream records: slot a (bits 0-14) | row-end flag (bit 15) | slot b (bits 16-30; 0 = none) |
-// empty rows follow this row's end (bit 31: the next row is found by a search, else it is r + 1).
-constexpr uint32_t kSlotMask = 0x7fffu, kRowEnd = 0x8000u, kSkip = 0x80000000u, kSlotB = 0x7fffu;
+// Slot references.  Slot p owns the 8 table bytes at 8p: H[p] as a double (A.v), or the two 32-bit
+// limbs of T[p] (v^T.A) with the low limb in the first or the second word by bit 4 of p, so that the
+// low limbs of any 32 consecutive slots (and the high limbs) cover all 32 banks -- a warp-wide
+// atomic on one limb of random slots spreads like one on a plain 32-bit array, while a slot's T
+// and H share their bytes (the fused kernel turns T[p] into H[p] in place, pair by pair).  A
+// reference is q = 2p + ((p >> 4) & 1), the word index of the low limb: low limb at byte 4q, high
+// limb at 4(q ^ 1), the double at 4(q & ~1).
+// Stream records: reference a (bits 0-14) | row-end flag (bit 15) | reference b (bits 16-30; 0 =
+// none) | empty rows follow this row's end (bit 31: the next row is found by a search, else r + 1).
+constexpr uint32_t kRowEnd = 0x8000u, kSkip = 0x80000000u;
+constexpr uint32_t kMaxSlots = 16384;  // 15-bit references
+
+TOC_HD uint32_t slot_ref(uint32_t p) { return 2u * p + ((p >> 4) & 1u); }
+
+// Byte offsets into the table from a record: the low limb of reference a / b, and the double.
+TOC_D uint32_t ref_a(uint32_t rec) { return (rec << 2) & 0x1fffcu; }
+TOC_D uint32_t ref_b(uint32_t rec) { return (rec >> 14) & 0x1fffcu; }
+
+// T[slot] += x (carry-free limbs, see limb_add in toc_batch.cuh) for the slot whose low limb is at
+// byte `lo` of the table.
+TOC_D void limb_add_at(uint8_t* tab, uint32_t lo, uint32_t xl, int32_t xh) {
+  atomicAdd(reinterpret_cast<uint32_t*>(tab + lo), xl);
+  atomicAdd(reinterpret_cast<int32_t*>(tab + (lo ^ 4u)), xh);
+}
+
+// Slot p's limbs (lo, hi) from its 8 bytes.
+TOC_D uint2 limbs_of(const uint8_t* tab, uint32_t p) {
+  const uint2 w = *reinterpret_cast<const uint2*>(tab + 8u * p);
+  return (p & 16u) ? make_uint2(w.y, w.x) : w;
+}
 
 // The row containing code s (the largest r with rowoff[r] <= s; rowoff[r + 1] > s then).
 TOC_D uint32_t row_of(const uint32_t* rowoff_s, uint32_t n, uint32_t s) {
@@ -219,8 +247,10 @@ TOC_D void row_weights(double* s_red, const double* u_s, uint2* wt_s, uint32_t n
 
 // Per batch, phases separated by block barriers (MV: A.v, VM: v^T.A):
 //   VM  scatter T  |  push  |  column partials  |  column totals, next batch's sum |u|
-//   MV  P1 (beside the column totals)  |  inner H  |  row partials  |  row totals
+//   MV  P1  |  inner H  |  row partials  |  row totals
 //   VM  zero T for the next batch (beside the row totals)
+// Fused kernel: P1 is formed in the column-partials pass (each pair slot's T becomes its H in
+// place) and the inner H sits beside the column totals: 6 barriers per batch.
 // The next batch's staged region is copied in while the A.v rows run (the rows read only the
 // stream, H and a private copy of the row offsets).
 template <int kKind, bool kTrace>
@@ -291,9 +321,6 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
     if (VM && has_next) pre.bounds(a, bn);
 
     if (VM) {
-      const uint32_t S4 = align4(h.S);
-      uint32_t* lo_s = reinterpret_cast<uint32_t*>(tabp);
-      int32_t* hi_s = reinterpret_cast<int32_t*>(tabp + 4u * S4);
       double* Tf = reinterpret_cast<double*>(tabp);
       const uint32_t L = limb_bits(n);
       const double g_scale = limb_scale(s_red[32], L), g_inv = 1.0 / g_scale;
@@ -314,9 +341,9 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
             const uint32_t rec[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
             for (uint32_t i = 0; i < 4; ++i) {
-              TOC_CHECK((rec[i] & kSlotMask) < h.S && ((rec[i] >> 16) & kSlotB) < h.S && (rec[i] == 0 || r < n));
-              limb_add(lo_s, hi_s, rec[i] & kSlotMask, xl, xh);
-              if ((rec[i] >> 16) & kSlotB) limb_add(lo_s, hi_s, (rec[i] >> 16) & kSlotB, xl, xh);
+              TOC_CHECK(ref_a(rec[i]) < 8 * h.S && ref_b(rec[i]) < 8 * h.S && (rec[i] == 0 || r < n));
+              limb_add_at(tabp, ref_a(rec[i]), xl, xh);
+              if (ref_b(rec[i])) limb_add_at(tabp, ref_b(rec[i]), xl, xh);
               if (rec[i] & kRowEnd) {
                 r = next_row(rowoff_s, n, r, rec[i]);
                 if (r < n) weight(r, xl, xh);
@@ -330,8 +357,8 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
 #pragma unroll
             for (uint32_t i = 0; i < 4; ++i) {
               if (wu != 0.0) {
-                atomicAdd(Tf + (rec[i] & kSlotMask), wu);
-                if ((rec[i] >> 16) & kSlotB) atomicAdd(Tf + ((rec[i] >> 16) & kSlotB), wu);
+                atomicAdd(reinterpret_cast<double*>(tabp + (ref_a(rec[i]) & ~7u)), wu);
+                if (ref_b(rec[i])) atomicAdd(reinterpret_cast<double*>(tabp + (ref_b(rec[i]) & ~7u)), wu);
               }
               if (rec[i] & kRowEnd) {
                 r = next_row(rowoff_s, n, r, rec[i]);
@@ -347,24 +374,27 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
       }
       __syncthreads();
       TOC_LVL_STAMP(1);
-      // push: each inner slot's own T goes to every pair slot of its chain
+      // push: each inner slot's own T goes to every pair slot of its chain (inner records hold
+      // references: parent | key << 16)
+      const uint32_t q_inner = 2u * nP + 2u;  // references from here on are inner slots
       if (!f64) {
         for (uint32_t y = tid; y < nQ; y += nth) {
           const uint32_t x = nP + 1 + y;
           uint32_t rec = inner_s[y];
-          TOC_CHECK((rec >> 16) >= 1 && (rec >> 16) <= nP && (rec & 0xffffu) >= 1 && (rec & 0xffffu) < x);
-          const uint32_t l = lo_s[x];
-          const int32_t hh = hi_s[x];
+          TOC_CHECK((rec >> 17) >= 1 && (rec >> 17) <= nP && ((rec & 0xffffu) >> 1) >= 1 && ((rec & 0xffffu) >> 1) < x);
+          const uint2 t = limbs_of(tabp, x);
+          const uint32_t l = t.x;
+          const int32_t hh = (int32_t)t.y;
           if (l | (uint32_t)hh) {
-            uint32_t p = rec & 0xffffu;
-            limb_add(lo_s, hi_s, rec >> 16, l, hh);
-            while (p > nP) {
-              TOC_CHECK(p - nP - 1 < nQ);
-              rec = inner_s[p - nP - 1];
-              limb_add(lo_s, hi_s, rec >> 16, l, hh);
-              p = rec & 0xffffu;
+            uint32_t q = rec & 0xffffu;
+            limb_add_at(tabp, (rec >> 14) & 0x3fffcu, l, hh);
+            while (q >= q_inner) {
+              TOC_CHECK((q >> 1) - nP - 1 < nQ);
+              rec = inner_s[(q >> 1) - nP - 1];
+              limb_add_at(tabp, (rec >> 14) & 0x3fffcu, l, hh);
+              q = rec & 0xffffu;
             }
-            limb_add(lo_s, hi_s, p, l, hh);
+            limb_add_at(tabp, q << 2, l, hh);
           }
         }
       } else {
@@ -372,14 +402,14 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
           uint32_t rec = inner_s[y];
           const double t = Tf[nP + 1 + y];
           if (t != 0.0) {
-            uint32_t p = rec & 0xffffu;
-            atomicAdd(Tf + (rec >> 16), t);
-            while (p > nP) {
-              rec = inner_s[p - nP - 1];
-              atomicAdd(Tf + (rec >> 16), t);
-              p = rec & 0xffffu;
+            uint32_t q = rec & 0xffffu;
+            atomicAdd(Tf + (rec >> 17), t);
+            while (q >= q_inner) {
+              rec = inner_s[(q >> 1) - nP - 1];
+              atomicAdd(Tf + (rec >> 17), t);
+              q = rec & 0xffffu;
             }
-            atomicAdd(Tf + p, t);
+            atomicAdd(Tf + (q >> 1), t);
           }
         }
       }
@@ -388,7 +418,9 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
       pre.load(a);
       // column partials: thread t sums value * T over pair slots [1 + tM, 1 + tM + M) (M odd, so
       // the lanes' slot reads are conflict-free), column by column; a column ending inside the
-      // range is complete (started here) or the range's head partial
+      // range is complete (started here) or the range's head partial.  Fused kernel: the same pass
+      // turns each pair slot into A.v's P1 = value * v[column] (Algorithm 5's H at depth 1) once
+      // its T has been read -- one pair record and one value-index gather for both products.
       double* o = a.O + b * (int64_t)ncol;
       const uint32_t M = ((nP + nth - 1) / nth) | 1u;
       {
@@ -400,7 +432,9 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
             for (uint32_t p = p0; p < p1; ++p) {
               const uint32_t x = prs_s[p - 1];
               TOC_CHECK(((x >> 16) & 0x7fffu) < h.nU && (x & 0xffffu) < ncol);
-              acc += uniq_s[(x >> 16) & 0x7fffu] * tval(p);
+              const double val = uniq_s[(x >> 16) & 0x7fffu];
+              acc += val * tval(p);
+              if (MV) H[p] = val * v_s[x & 0xffffu];
               if (x >> 31) {  // last pair slot of its column
                 if (here) o[x & 0xffffu] = acc;
                 else head_s[tid] = acc;
@@ -410,7 +444,10 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
             }
           };
           if (f64) pass([&](uint32_t p) { return Tf[p]; });
-          else pass([&](uint32_t p) { return limb_value(lo_s[p], hi_s[p], L, g_inv); });
+          else pass([&](uint32_t p) {
+            const uint2 t = limbs_of(tabp, p);
+            return limb_value(t.x, (int32_t)t.y, L, g_inv);
+          });
           tail_s[tid] = acc;
         }
       }
@@ -435,30 +472,33 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
       su_store(pre.stash(a, u_s), s_red);
     }
     if (MV) {
-      // P1 for the pair slots (Algorithm 5's H at depth 1); the row offsets into a private copy
-      for (uint32_t i = tid; i < nP; i += nth) {
-        const uint32_t x = prs_s[i];
-        TOC_CHECK(((x >> 16) & 0x7fffu) < h.nU && (x & 0xffffu) < ncol);
-        H[1 + i] = uniq_s[(x >> 16) & 0x7fffu] * v_s[x & 0xffffu];
+      if (!VM) {
+        // P1 for the pair slots (Algorithm 5's H at depth 1)
+        for (uint32_t i = tid; i < nP; i += nth) {
+          const uint32_t x = prs_s[i];
+          TOC_CHECK(((x >> 16) & 0x7fffu) < h.nU && (x & 0xffffu) < ncol);
+          H[1 + i] = uniq_s[(x >> 16) & 0x7fffu] * v_s[x & 0xffffu];
+        }
       }
-      if (tid == 0) H[0] = 0.0;
+      if (tid == 0) H[0] = 0.0;  // padding records scatter to slot 0
+      // the row offsets into a private copy (the stage is refilled while the rows run)
       for (uint32_t r = tid; r <= n; r += nth) rowcur_s[r] = rowoff_s[r];
-    }
-    __syncthreads();
-    TOC_LVL_STAMP(4);
-    if (MV) {
-      // H of the inner slots: the sum of P1 over the node's chain (reads pair slots only)
+      if (!VM) __syncthreads();
+      TOC_LVL_STAMP(4);
+      // H of the inner slots: the sum of P1 over the node's chain (reads pair slots only); fused
+      // kernel: beside the column totals (slot 0 keeps its zero: no record scatters to it)
+      const uint32_t q_inner = 2u * nP + 2u;
       for (uint32_t y = tid; y < nQ; y += nth) {
         uint32_t rec = inner_s[y];
-        double hv = H[rec >> 16];
-        uint32_t p = rec & 0xffffu;
-        while (p > nP) {
-          TOC_CHECK(p - nP - 1 < nQ);
-          rec = inner_s[p - nP - 1];
-          hv += H[rec >> 16];
-          p = rec & 0xffffu;
+        double hv = H[rec >> 17];
+        uint32_t q = rec & 0xffffu;
+        while (q >= q_inner) {
+          TOC_CHECK((q >> 1) - nP - 1 < nQ);
+          rec = inner_s[(q >> 1) - nP - 1];
+          hv += H[rec >> 17];
+          q = rec & 0xffffu;
         }
-        H[nP + 1 + y] = hv + H[p];
+        H[nP + 1 + y] = hv + H[q >> 1];
       }
       __syncthreads();
       TOC_LVL_STAMP(5);
@@ -476,9 +516,9 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
           double ha[4], hb[4];
 #pragma unroll
           for (uint32_t i = 0; i < 4; ++i) {
-            TOC_CHECK((rec[i] & kSlotMask) < h.S && ((rec[i] >> 16) & kSlotB) < h.S);
-            ha[i] = H[rec[i] & kSlotMask];
-            hb[i] = ((rec[i] >> 16) & kSlotB) ? H[(rec[i] >> 16) & kSlotB] : 0.0;
+            TOC_CHECK(ref_a(rec[i]) < 8 * h.S && ref_b(rec[i]) < 8 * h.S);
+            ha[i] = *reinterpret_cast<const double*>(tabp + (ref_a(rec[i]) & ~7u));
+            hb[i] = ref_b(rec[i]) ? *reinterpret_cast<const double*>(tabp + (ref_b(rec[i]) & ~7u)) : 0.0;
           }
 #pragma unroll
           for (uint32_t i = 0; i < 4; ++i) {
@@ -657,7 +697,7 @@ int build_entry(const uint8_t* blk, const TocBlockMeta& m, LvlEntry& out) {
     if (inner[x]) inn.push_back((uint32_t)x);
   std::stable_sort(inn.begin(), inn.end(), [&](uint32_t x, uint32_t y) { return depth[x] < depth[y]; });
   const uint32_t nQ = (uint32_t)inn.size();
-  if (1ull + nI + nQ > 32767u) return TOC_E_ARG;  // 15-bit slot fields
+  if (1ull + nI + nQ > toc::kMaxSlots) return TOC_E_ARG;  // 15-bit slot references
   for (uint32_t q = 0; q < nQ; ++q) slot[inn[q]] = nI + 1 + q;
   const uint32_t S = 1 + nI + nQ;
   // stream: thread t owns codes [t*K, t*K + K); record k of thread t at (k/4)*4T + 4t + k%4
@@ -697,7 +737,8 @@ int build_entry(const uint8_t* blk, const TocBlockMeta& m, LvlEntry& out) {
     pr[k] = pcol[order[k]] | (pref[order[k]] << 16) | (last ? 0x80000000u : 0u);
   }
   uint32_t* ir = reinterpret_cast<uint32_t*>(e + hd.off_inner);
-  for (uint32_t q = 0; q < nQ; ++q) ir[q] = slot[par[inn[q]]] | (slot[key[inn[q]]] << 16);
+  for (uint32_t q = 0; q < nQ; ++q)  // references: parent | key << 16
+    ir[q] = toc::slot_ref(slot[par[inn[q]]]) | (toc::slot_ref(slot[key[inn[q]]]) << 16);
   uint16_t* cs = reinterpret_cast<uint16_t*>(e + hd.off_colst);
   for (uint32_t c = 0, k = 0; c <= m.n_cols; ++c) {
     while (k < nI && pcol[order[k]] < c) ++k;
@@ -708,7 +749,8 @@ int build_entry(const uint8_t* blk, const TocBlockMeta& m, LvlEntry& out) {
   for (uint32_t r = 0; r < n; ++r)
     for (uint32_t j = off[r]; j < off[r + 1]; ++j) {
       const uint32_t x = code[j];
-      rec[j] = (x <= nI || inner[x]) ? slot[x] : (slot[par[x]] | (slot[key[x]] << 16));
+      rec[j] = (x <= nI || inner[x]) ? toc::slot_ref(slot[x])
+                                     : (toc::slot_ref(slot[par[x]]) | (toc::slot_ref(slot[key[x]]) << 16));
       rowid[j] = r;
     }
   schedule_banks(rec, rowid, off, n, C, K, T);

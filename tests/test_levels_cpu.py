@@ -86,18 +86,28 @@ def entry(buf, o):
     h["vmax"] = struct.unpack_from("<d", buf, o + 64)[0]
     u32 = lambda off, n: np.frombuffer(buf, np.uint32, n, o + off).astype(np.int64)  # noqa: E731
     h["prs"] = u32(h["off_prs"], h["nP"])
-    h["inner"] = u32(h["off_inner"], h["nQ"])
+    inner = u32(h["off_inner"], h["nQ"])  # references -> slot numbers: par | key << 16
+    h["inner"] = slot_of(inner & 0xFFFF) | (slot_of(inner >> 16) << 16)
     T, K = h["T"], h["K"]
     st = u32(h["off_stream"], T * K)
     # record k of thread t at (k // 4) * 4T + 4t + k % 4  ->  row order j = t*K + k
     k = np.arange(K)
     pos = (k[None, :] // 4) * 4 * T + 4 * np.arange(T)[:, None] + (k[None, :] % 4)
-    h["stream"] = st[pos.reshape(-1)][: h["C"]]
+    st = st[pos.reshape(-1)][: h["C"]]
+    h["stream"] = slot_of(st & 0x7FFF) | (st & 0x8000) | (slot_of((st >> 16) & 0x7FFF) << 16) | (st & 0x80000000)
     h["colst"] = np.frombuffer(buf, np.uint16, h["n_cols"] + 1, o + h["off_colst"]).astype(np.int64)
     h["uniq"] = np.frombuffer(buf, np.float64, h["nU"], o + h["off_uniq"]).copy()
     h["rowoff"] = u32(h["off_rowoff"], h["n_rows"] + 1)
     h["trow"] = np.frombuffer(buf, np.uint16, T, o + h["off_trow"]).astype(np.int64)
     return h
+
+
+def slot_of(ref):
+    """Slot number of a reference (toc_levels.cu slot_ref: 2p + bit 4 of p)."""
+    ref = np.asarray(ref, np.int64)
+    p = ref >> 1
+    assert np.all((ref & 1) == ((p >> 4) & 1)), "reference parity"
+    return p
 
 
 def value_index(block):
@@ -263,7 +273,7 @@ def test_level_cache_config2_batches(oracle):
     for b, e in enumerate(encs):
         h = entry(buf, int(eo[b]))
         structure(h, e)
-        assert h["S"] < 32768 and h["nQ"] < h["C"] // 4
+        assert h["S"] <= 16384 and h["nQ"] < h["C"] // 4
         uniq, refs = value_index(blocks[b])
         assert np.array_equal(h["uniq"], uniq) and h["vmax"] == (np.abs(uniq).max() if len(uniq) else 0.0)
         assert np.array_equal(h["rowoff"], np.asarray(e.offsets, np.int64))
