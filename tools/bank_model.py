@@ -1,0 +1,103 @@
+"""Modelled shared-memory wavefronts of the slot kernel's two stream phases (CPU only).
+
+Builds the slot-cache entries of a few config-2 batches with the library's host builder
+(toc_levels_build) and counts, per warp and step of the code stream, the wavefronts of
+  * the v^T.A scatter: 32-bit atomics on the low limb word q of reference a, then of reference b
+    (lanes whose record has one); the high limb (word q ^ 1) costs the same.  One wavefront per
+    lane in the most loaded bank (same-word atomics serialise too);
+  * the A.v row gathers: 64-bit loads of H[slot]; per half-warp one wavefront per distinct
+    8-byte word in the most loaded of the 16 bank pairs.
+The ideal is one wavefront per 32-bit warp access and two per 64-bit access.  Used to choose the
+record placement (schedule_banks in csrc/toc_levels.cu) before spending GPU time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+
+def model(st_raw: np.ndarray, T: int, K: int, C: int):
+    """st_raw: the entry's stream as stored (interleaved), u32[T*K].  Returns modelled wavefronts."""
+    k = np.arange(K)
+    pos = (k[None, :] // 4) * 4 * T + 4 * np.arange(T)[:, None] + (k[None, :] % 4)
+    st = st_raw[pos]  # [T, K]
+    qa = st & 0x7FFF
+    qb = (st >> 16) & 0x7FFF
+    act = np.broadcast_to((np.arange(T)[:, None] * K) < C, (T, K))  # inactive threads skip the walk
+    W = T // 32
+    at_a = at_b = ga = gb = 0
+    ideal_at_a = ideal_at_b = ideal_ga = ideal_gb = 0
+    for w in range(W):
+        sl = slice(w * 32, w * 32 + 32)
+        if not act[sl].any():
+            break
+        A, B, M = qa[sl], qb[sl], act[sl]
+        for s in range(K):
+            m = M[:, s]
+            a = A[m, s]
+            if a.size:
+                at_a += np.bincount(a & 31, minlength=32).max()
+                ideal_at_a += 1
+                for half in (slice(0, 16), slice(16, 32)):
+                    ah = A[half, s][M[half, s]]
+                    if ah.size:
+                        wds = np.unique(ah >> 1)
+                        ga += np.bincount(wds & 15, minlength=16).max()
+                        ideal_ga += 1
+            mb = m & (B[:, s] != 0)
+            b = B[mb, s]
+            if b.size:
+                at_b += np.bincount(b & 31, minlength=32).max()
+                ideal_at_b += 1
+                for half in (slice(0, 16), slice(16, 32)):
+                    hb = B[half, s]
+                    hb = hb[M[half, s] & (hb != 0)]
+                    if hb.size:
+                        wds = np.unique(hb >> 1)
+                        gb += np.bincount(wds & 15, minlength=16).max()
+                        ideal_gb += 1
+    return dict(atom=2 * (at_a + at_b), atom_ideal=2 * (ideal_at_a + ideal_at_b), gather=ga + gb,
+                gather_ideal=ideal_ga + ideal_gb)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--batches", type=int, default=4)
+    args = ap.parse_args()
+    from oracle import oracle as O
+    from paper_1702_06943_b200 import synth
+    import test_levels_cpu as TL
+
+    O.build()
+    blocks = []
+    for b in range(args.batches):
+        rp, c, v = synth.dense_to_csr(synth.cfg2_batch_dense(0, b))
+        blocks.append(O.serialize(O.encode_csr(784, rp, c, v)))
+    t0 = time.time()
+    rc, buf, eo = TL.build(blocks)
+    dt = time.time() - t0
+    assert rc == 0
+    tot = {}
+    for b in range(args.batches):
+        o = int(eo[b])
+        h = TL.entry(buf, o)
+        st_raw = np.frombuffer(buf, np.uint32, h["T"] * h["K"], o + h["off_stream"]).astype(np.int64)
+        r = model(st_raw, h["T"], h["K"], h["C"])
+        for k_, v_ in r.items():
+            tot[k_] = tot.get(k_, 0) + v_
+    n = args.batches
+    print(f"build {dt / n * 1e3:.1f} ms per batch (2 threads)")
+    print("per batch: " + "  ".join(f"{k_} {v_ / n:.0f}" for k_, v_ in tot.items()))
+
+
+if __name__ == "__main__":
+    main()
