@@ -42,6 +42,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstddef>
+#include <cstdlib>
 #include <thread>
 #include <vector>
 
@@ -381,7 +382,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
         for (uint32_t y = tid; y < nQ; y += nth) {
           const uint32_t x = nP + 1 + y;
           uint32_t rec = inner_s[y];
-          TOC_CHECK((rec >> 17) >= 1 && (rec >> 17) <= nP && ((rec & 0xffffu) >> 1) >= 1 && ((rec & 0xffffu) >> 1) < x);
+          TOC_CHECK((rec >> 17) >= 1 && (rec >> 17) <= nP && ((rec & 0xffffu) >> 1) >= 1 && ((rec & 0xffffu) >> 1) < h.S);
           const uint2 t = limbs_of(tabp, x);
           const uint32_t l = t.x;
           const int32_t hh = (int32_t)t.y;
@@ -600,9 +601,42 @@ struct LvlCache {
 // the least used banks (slot mod 32) among the lanes placed so far in this step.
 void schedule_banks(std::vector<uint32_t>& rec, const std::vector<uint32_t>& rowid, const std::vector<uint32_t>& off,
                     uint32_t n, uint32_t C, uint32_t K, uint32_t T) {
-  std::vector<std::vector<uint32_t>> pool(n);
-  for (uint32_t r = 0; r < n; ++r) pool[r].assign(rec.begin() + off[r], rec.begin() + off[r + 1]);
+  const char* e_old = getenv("TOC_LVL_SCHED");  // experiment knob: 0 = atomics' banks only (round-2f placement)
+  const bool old = e_old && atoi(e_old) == 0;
+  const bool spread = e_old && atoi(e_old) <= 1;  // 1 = banks + bank pairs, two-reference records anywhere
+  // Two-reference records (leaves: parent + key) go to the row's positions with the smallest step
+  // index, so that a warp's second-reference accesses are either (nearly) full or empty: a step
+  // costs at least one wavefront per access instruction that has any lane, however few.
+  std::vector<std::vector<uint32_t>> pool2(n), pool1(n);
+  std::vector<uint8_t> two(C, 0);
+  {
+    std::vector<uint32_t> cnt(K + 1);
+    for (uint32_t r = 0; r < n; ++r) {
+      uint32_t n2 = 0;
+      for (uint32_t j = off[r]; j < off[r + 1]; ++j) {
+        if (rec[j] >> 16) pool2[r].push_back(rec[j]), ++n2;
+        else pool1[r].push_back(rec[j]);
+      }
+      if (!spread) {
+        // the n2 positions of the row with the smallest steps (ties: first come)
+        std::fill(cnt.begin(), cnt.end(), 0u);
+        for (uint32_t j = off[r]; j < off[r + 1]; ++j) ++cnt[j % K];
+        uint32_t thr = 0, left = n2;
+        while (thr < K && cnt[thr] <= left) left -= cnt[thr++];
+        for (uint32_t j = off[r]; j < off[r + 1]; ++j) {
+          const uint32_t k = j % K;
+          if (k < thr) two[j] = 1;
+          else if (k == thr && left) two[j] = 1, --left;
+        }
+      }
+    }
+  }
+  // seen[h][word] == stamp: the 8-byte word is already gathered by a placed lane of half-warp h in
+  // this step (a 64-bit gather of the same word is a broadcast, not a conflict)
+  std::vector<uint32_t> seen[2] = {std::vector<uint32_t>(toc::kMaxSlots, 0), std::vector<uint32_t>(toc::kMaxSlots, 0)};
+  uint32_t stamp = 0;
   uint32_t lanes[32];
+  const uint32_t wa = old ? 3u : 4u, wb = old ? 2u : 4u, wg = old ? 0u : 3u;
   for (uint32_t w = 0; w < T / 32; ++w) {
     if ((uint64_t)w * 32 * K >= C) break;
     for (uint32_t k = 0; k < K; ++k) {
@@ -613,21 +647,32 @@ void schedule_banks(std::vector<uint32_t>& rec, const std::vector<uint32_t>& row
       }
       if (!na) continue;
       std::stable_sort(lanes, lanes + na, [&](uint32_t x, uint32_t y) {
-        return pool[rowid[(w * 32 + x) * K + k]].size() < pool[rowid[(w * 32 + y) * K + k]].size();
+        const uint32_t rx = rowid[(w * 32 + x) * K + k], ry = rowid[(w * 32 + y) * K + k];
+        return pool1[rx].size() + pool2[rx].size() < pool1[ry].size() + pool2[ry].size();
       });
-      uint8_t ca[32] = {0}, cb[32] = {0};
+      // ca / cb: lanes per 32-bit bank of the low-limb words (the scatter's atomics: reference a,
+      // then reference b); ga / gb: distinct 8-byte words per bank pair and half-warp (the row
+      // gathers)
+      uint8_t ca[32] = {0}, cb[32] = {0}, ga[2][16] = {{0}}, gb[2][16] = {{0}};
+      ++stamp;
       for (uint32_t q = 0; q < na; ++q) {
-        const uint32_t j = (w * 32 + lanes[q]) * K + k;
-        std::vector<uint32_t>& P = pool[rowid[j]];
+        const uint32_t j = (w * 32 + lanes[q]) * K + k, hf = lanes[q] >> 4;
+        const uint32_t rj = rowid[j];
+        // the position's class; with the classes spread (knob) whichever pool is relatively fuller
+        const bool use2 = spread ? (pool1[rj].empty() || (!pool2[rj].empty() && (stamp + j) % (pool1[rj].size() + pool2[rj].size()) < pool2[rj].size()))
+                                 : (two[j] != 0);
+        std::vector<uint32_t>& P = use2 ? pool2[rj] : pool1[rj];
+        auto cost_a = [&](uint32_t a) { return wa * ca[a & 31] + (seen[hf][a >> 1] == stamp ? 0u : wg * ga[hf][(a >> 1) & 15]); };
+        auto cost_b = [&](uint32_t b) { return wb * cb[b & 31] + (seen[hf][b >> 1] == stamp ? 0u : wg * gb[hf][(b >> 1) & 15]); };
         size_t best = 0;
         bool swap = false;
         uint32_t bc = ~0u;
         for (size_t i = 0; i < P.size() && bc; ++i) {
           const uint32_t a = P[i] & 0xffffu, b = P[i] >> 16;
-          const uint32_t c = 3u * ca[a & 31] + (b ? 2u * cb[b & 31] : 0u);
+          const uint32_t c = cost_a(a) + (b ? cost_b(b) : 0u);
           if (c < bc) bc = c, best = i, swap = false;
           if (b) {
-            const uint32_t c2 = 3u * ca[b & 31] + 2u * cb[a & 31];
+            const uint32_t c2 = cost_a(b) + cost_b(a);
             if (c2 < bc) bc = c2, best = i, swap = true;
           }
         }
@@ -635,11 +680,153 @@ void schedule_banks(std::vector<uint32_t>& rec, const std::vector<uint32_t>& row
         P[best] = P.back();
         P.pop_back();
         if (swap) x = (x >> 16) | ((x & 0xffffu) << 16);
-        ++ca[(x & 0xffffu) & 31];
-        if (x >> 16) ++cb[(x >> 16) & 31];
+        const uint32_t a = x & 0xffffu, b = x >> 16;
+        ++ca[a & 31];
+        if (seen[hf][a >> 1] != stamp) ++ga[hf][(a >> 1) & 15];
+        if (b) {
+          ++cb[b & 31];
+          if (seen[hf][b >> 1] != stamp) ++gb[hf][(b >> 1) & 15];
+        }
+        // a and b gathers are separate instructions: separate word sets would be exact; one set
+        // is a close bound (a word shared between an a and a b lane is rare)
+        seen[hf][a >> 1] = stamp;
+        if (b) seen[hf][b >> 1] = stamp;
         rec[j] = x;
       }
     }
+  }
+}
+
+// Local search after the greedy placement: for every (warp, step) above its conflict-free cost, a
+// lane sitting in a most loaded bank trades records with another position of its row (either
+// orientation of a two-reference record) when that lowers the modelled wavefronts of the two steps
+// involved.  Model (what tools/bank_model.py reports, with lanes counted instead of distinct
+// words): per step 2 x (most loaded 32-bit bank of the a atomics + of the b atomics) + per
+// half-warp the most loaded bank pair of the a gathers + of the b gathers.
+struct StepBanks {
+  uint8_t ca[32], cb[32], ga[2][16], gb[2][16];
+  void add(uint32_t lane, uint32_t x, int d) {
+    const uint32_t a = x & 0xffffu, b = x >> 16, h = lane >> 4;
+    ca[a & 31] += d, ga[h][(a >> 1) & 15] += d;
+    if (b) cb[b & 31] += d, gb[h][(b >> 1) & 15] += d;
+  }
+  struct Max {
+    uint32_t a, b, g[2][2];  // most loaded bank: a atomics, b atomics, gathers [a / b][half-warp]
+    uint32_t cost() const { return 2u * (a + b) + g[0][0] + g[0][1] + g[1][0] + g[1][1]; }
+  };
+  Max maxes() const {
+    Max m{0, 0, {{0, 0}, {0, 0}}};
+    for (uint32_t i = 0; i < 32; ++i) m.a = std::max<uint32_t>(m.a, ca[i]), m.b = std::max<uint32_t>(m.b, cb[i]);
+    for (uint32_t i = 0; i < 16; ++i) {
+      m.g[0][0] = std::max<uint32_t>(m.g[0][0], ga[0][i]), m.g[0][1] = std::max<uint32_t>(m.g[0][1], ga[1][i]);
+      m.g[1][0] = std::max<uint32_t>(m.g[1][0], gb[0][i]), m.g[1][1] = std::max<uint32_t>(m.g[1][1], gb[1][i]);
+    }
+    return m;
+  }
+  uint32_t cost() const { return maxes().cost(); }
+  // the step's cost with record x added at `lane`, given the maxes without it
+  uint32_t cost_with(const Max& m, uint32_t lane, uint32_t x) const {
+    const uint32_t a = x & 0xffffu, b = x >> 16, h = lane >> 4;
+    uint32_t c = m.cost();
+    c += 2u * (std::max<uint32_t>(m.a, ca[a & 31] + 1u) - m.a);
+    c += std::max<uint32_t>(m.g[0][h], ga[h][(a >> 1) & 15] + 1u) - m.g[0][h];
+    if (b) {
+      c += 2u * (std::max<uint32_t>(m.b, cb[b & 31] + 1u) - m.b);
+      c += std::max<uint32_t>(m.g[1][h], gb[h][(b >> 1) & 15] + 1u) - m.g[1][h];
+    }
+    return c;
+  }
+  // is lane's record x in a most loaded (> 1) bank of any component?
+  bool hot(uint32_t lane, uint32_t x) const {
+    const uint32_t a = x & 0xffffu, b = x >> 16, h = lane >> 4;
+    auto top = [](const uint8_t* c, uint32_t n, uint32_t i) {
+      if (c[i] < 2) return false;
+      for (uint32_t k = 0; k < n; ++k)
+        if (c[k] > c[i]) return false;
+      return true;
+    };
+    return top(ca, 32, a & 31) || top(ga[h], 16, (a >> 1) & 15) ||
+           (b && (top(cb, 32, b & 31) || top(gb[h], 16, (b >> 1) & 15)));
+  }
+};
+
+void refine_banks(std::vector<uint32_t>& rec, const std::vector<uint32_t>& rowid, const std::vector<uint32_t>& off,
+                  uint32_t C, uint32_t K, uint32_t T, int passes) {
+  const uint32_t W = (uint32_t)std::min<uint64_t>(T / 32, ((uint64_t)C + 32ull * K - 1) / (32ull * K));
+  std::vector<StepBanks> sb((size_t)W * K);
+  memset(sb.data(), 0, sb.size() * sizeof(StepBanks));
+  std::vector<uint32_t> cost((size_t)W * K);
+  for (uint32_t j = 0; j < C; ++j) sb[(size_t)(j / K / 32) * K + j % K].add((j / K) & 31, rec[j], 1);
+  for (size_t i = 0; i < sb.size(); ++i) cost[i] = sb[i].cost();
+  auto flip = [](uint32_t x) { return (x >> 16) | ((x & 0xffffu) << 16); };
+  // the cheaper orientation of record y at (step s, lane l), whose own record is already removed
+  // (m: the step's maxes without it)
+  auto best_in = [&](const StepBanks& s, const StepBanks::Max& m, uint32_t l, uint32_t y, uint32_t& c) {
+    c = s.cost_with(m, l, y);
+    if (!(y >> 16)) return y;
+    const uint32_t f = flip(y), c2 = s.cost_with(m, l, f);
+    if (c2 < c) return c = c2, f;
+    return y;
+  };
+  for (int pass = 0; pass < passes; ++pass) {
+    bool any = false;
+    for (uint32_t w = 0; w < W; ++w)
+      for (uint32_t k = 0; k < K; ++k) {
+        const size_t si = (size_t)w * K + k;
+        StepBanks& s = sb[si];
+        for (uint32_t l = 0; l < 32; ++l) {
+          const uint64_t j64 = (uint64_t)(w * 32 + l) * K + k;
+          if (j64 >= C) break;
+          const uint32_t j = (uint32_t)j64;
+          if (!s.hot(l, rec[j])) continue;
+          const uint32_t r = rowid[j], x = rec[j];
+          s.add(l, x, -1);
+          const StepBanks::Max m = s.maxes();
+          if (m.cost() >= cost[si]) {  // removing x alone does not lower the step: no trade of x can
+            s.add(l, x, 1);
+            continue;
+          }
+          uint32_t cx;
+          const uint32_t xb = best_in(s, m, l, x, cx);  // flipping alone
+          uint32_t best_gain = cost[si] - cx, best_j2 = j, best_y = xb, best_x2 = 0, best_c = cx, best_c2 = 0;
+          for (uint32_t j2 = off[r]; j2 < off[r + 1]; ++j2) {
+            if (j2 == j || rec[j2] == x) continue;
+            const uint32_t t2 = j2 / K, l2 = t2 & 31;
+            const size_t si2 = (size_t)(t2 / 32) * K + j2 % K;
+            if (si2 == si) continue;  // same step: only the half-warp would change
+            const uint32_t y = rec[j2];
+            uint32_t c1, c2;
+            const uint32_t yo = best_in(s, m, l, y, c1);
+            if (c1 >= cost[si]) continue;  // the gain has to come from this step
+            StepBanks& s2 = sb[si2];
+            s2.add(l2, y, -1);
+            const uint32_t xo = best_in(s2, s2.maxes(), l2, x, c2);
+            s2.add(l2, y, 1);
+            const uint32_t before = cost[si] + cost[si2], after = c1 + c2;
+            if (after < before && before - after > best_gain)
+              best_gain = before - after, best_j2 = j2, best_y = yo, best_x2 = xo, best_c = c1, best_c2 = c2;
+          }
+          if (best_gain == 0) {
+            s.add(l, x, 1);
+            continue;
+          }
+          any = true;
+          if (best_j2 == j) {
+            rec[j] = best_y;
+            s.add(l, best_y, 1);
+            cost[si] = best_c;
+          } else {
+            const uint32_t t2 = best_j2 / K, l2 = t2 & 31;
+            const size_t si2 = (size_t)(t2 / 32) * K + best_j2 % K;
+            sb[si2].add(l2, rec[best_j2], -1);
+            sb[si2].add(l2, best_x2, 1);
+            s.add(l, best_y, 1);
+            rec[j] = best_y, rec[best_j2] = best_x2;
+            cost[si] = best_c, cost[si2] = best_c2;
+          }
+        }
+      }
+    if (!any) break;
   }
 }
 
@@ -698,6 +885,55 @@ int build_entry(const uint8_t* blk, const TocBlockMeta& m, LvlEntry& out) {
   std::stable_sort(inn.begin(), inn.end(), [&](uint32_t x, uint32_t y) { return depth[x] < depth[y]; });
   const uint32_t nQ = (uint32_t)inn.size();
   if (1ull + nI + nQ > toc::kMaxSlots) return TOC_E_ARG;  // 15-bit slot references
+  // Which inner node gets which inner slot is free (push and inner H touch pair slots only), and
+  // the kernel's warps take 32 consecutive inner slots, level by level up their chains.  Within a
+  // depth class (equal chain lengths: no divergence) each lane takes, from the next nodes of the
+  // class, the one whose chain slots (own key, ancestors' keys, root pair) hit the least used banks
+  // of its warp at every level: 32-bit banks of the low limb for the push atomics, bank pairs per
+  // half-warp for the inner-H gathers.
+  if (!getenv("TOC_LVL_INNER_PLAIN")) {
+    constexpr uint32_t kLv = 8, kScan = 1024;  // levels tracked (deeper ones share the last), candidates scanned
+    std::vector<uint32_t> placed;
+    placed.reserve(nQ);
+    std::vector<uint8_t> used(nQ, 0);
+    uint8_t ca[kLv][32], ga[kLv][2][16];
+    uint32_t lo = 0;  // first unplaced node of the sorted list
+    auto refs_of = [&](uint32_t x, uint32_t* r) {  // chain references of node x, the root last
+      uint32_t nl = 0;
+      for (uint32_t y = x; y > nI; y = par[y]) {
+        if (nl < kLv - 1) r[nl++] = toc::slot_ref(slot[key[y]]);
+        if (par[y] <= nI) r[nl++] = toc::slot_ref(slot[par[y]]);
+      }
+      return nl;
+    };
+    for (uint32_t q = 0; q < nQ; ++q) {
+      const uint32_t lane = q & 31, hf = lane >> 4;
+      if (lane == 0) memset(ca, 0, sizeof ca), memset(ga, 0, sizeof ga);
+      while (lo < nQ && used[lo]) ++lo;
+      const uint32_t d0 = depth[inn[lo]];
+      uint32_t best = lo, bc = ~0u, seen = 0;
+      for (uint32_t i = lo; i < nQ && seen < kScan && depth[inn[i]] == d0 && bc; ++i) {
+        if (used[i]) continue;
+        ++seen;
+        uint32_t r[kLv], c = 0;
+        const uint32_t nl = refs_of(inn[i], r);
+        for (uint32_t l = 0; l < nl; ++l) {
+          const uint32_t lv = l + 1 == nl ? kLv - 1 : l;  // the root adds run converged, after the loop
+          c += 4u * ca[lv][r[l] & 31] + 3u * ga[lv][hf][(r[l] >> 1) & 15];
+        }
+        if (c < bc) bc = c, best = i;
+      }
+      used[best] = 1;
+      uint32_t r[kLv];
+      const uint32_t nl = refs_of(inn[best], r);
+      for (uint32_t l = 0; l < nl; ++l) {
+        const uint32_t lv = l + 1 == nl ? kLv - 1 : l;
+        ++ca[lv][r[l] & 31], ++ga[lv][hf][(r[l] >> 1) & 15];
+      }
+      placed.push_back(inn[best]);
+    }
+    inn.swap(placed);
+  }
   for (uint32_t q = 0; q < nQ; ++q) slot[inn[q]] = nI + 1 + q;
   const uint32_t S = 1 + nI + nQ;
   // stream: thread t owns codes [t*K, t*K + K); record k of thread t at (k/4)*4T + 4t + k%4
@@ -754,6 +990,11 @@ int build_entry(const uint8_t* blk, const TocBlockMeta& m, LvlEntry& out) {
       rowid[j] = r;
     }
   schedule_banks(rec, rowid, off, n, C, K, T);
+  {
+    const char* e_ref = getenv("TOC_LVL_REFINE");  // experiment knob: local-search passes (default 2)
+    const int passes = e_ref ? atoi(e_ref) : 2;
+    if (passes > 0) refine_banks(rec, rowid, off, C, K, T, passes);
+  }
   uint16_t* tr = reinterpret_cast<uint16_t*>(e + hd.off_trow);
   for (uint32_t t = 0; t < T && (uint64_t)t * K < C; ++t) {
     const uint32_t r = rowid[t * K];

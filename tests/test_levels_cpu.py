@@ -209,7 +209,12 @@ def structure(h, enc):
     assert np.all(np.diff(h["prs"] & 0xFFFF) >= 0), "pairs not column-sorted"
     par, key = h["inner"] & 0xFFFF, h["inner"] >> 16
     assert np.all((key >= 1) & (key <= nP)), "inner keys must be pairs"
-    assert np.all((par >= 1) & (par < nP + 1 + np.arange(nQ))), "inner parent after its child"
+    assert np.all((par >= 1) & (par < S) & (par != nP + 1 + np.arange(nQ))), "inner parents"
+    for y in range(nQ):  # parent chains end at a pair (inner slots are numbered for banks, not by depth)
+        p, steps = par[y], 0
+        while p > nP:
+            p, steps = par[p - nP - 1], steps + 1
+            assert steps <= nQ, "inner parent cycle"
     a_, b_ = h["stream"] & 0x7FFF, (h["stream"] >> 16) & 0x7FFF
     assert np.all((a_ >= 1) & (a_ < S)) and np.all(b_ < S), "stream references"
     off = np.asarray(enc.offsets, np.int64)

@@ -69,6 +69,43 @@ def model(st_raw: np.ndarray, T: int, K: int, C: int):
                 gather_ideal=ideal_ga + ideal_gb)
 
 
+def model_inner(inner_raw: np.ndarray, nP: int):
+    """Push (32-bit atomics on the low limb of each chain slot; the high limb costs the same) and
+    inner H (64-bit gathers) over the inner records, 32 consecutive inner slots per warp."""
+    par = inner_raw & 0xFFFF  # references (word index of the low limb)
+    key = inner_raw >> 16
+    nQ = len(inner_raw)
+    q_inner = 2 * nP + 2
+    at = ga = at_i = ga_i = 0
+    for w0 in range(0, nQ, 32):
+        lanes = np.arange(w0, min(w0 + 32, nQ))
+        cur_key = key[lanes].copy()
+        cur_par = par[lanes].copy()
+        alive = np.ones(len(lanes), bool)
+        while alive.any():
+            k_ = cur_key[alive]
+            at += np.bincount(k_ & 31, minlength=32).max()
+            at_i += 1
+            idx = np.nonzero(alive)[0]
+            for half in (idx[idx < 16], idx[idx >= 16]):
+                if half.size:
+                    ga += np.bincount(np.unique(cur_key[half] >> 1) & 15, minlength=16).max()
+                    ga_i += 1
+            nxt = alive & (cur_par >= q_inner)
+            y = (cur_par[nxt] >> 1) - nP - 1
+            cur_key[nxt] = key[y]
+            cur_par[nxt] = par[y]
+            alive = nxt
+        root = cur_par  # every lane's root pair (added after the loop, lanes converged)
+        at += np.bincount(root & 31, minlength=32).max()
+        at_i += 1
+        for half in (root[:16], root[16:]):
+            if half.size:
+                ga += np.bincount(np.unique(half >> 1) & 15, minlength=16).max()
+                ga_i += 1
+    return dict(push=2 * at, push_ideal=2 * at_i, innerH=ga, innerH_ideal=ga_i)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--batches", type=int, default=4)
@@ -92,6 +129,7 @@ def main():
         h = TL.entry(buf, o)
         st_raw = np.frombuffer(buf, np.uint32, h["T"] * h["K"], o + h["off_stream"]).astype(np.int64)
         r = model(st_raw, h["T"], h["K"], h["C"])
+        r.update(model_inner(np.frombuffer(buf, np.uint32, h["nQ"], o + h["off_inner"]).astype(np.int64), h["nP"]))
         for k_, v_ in r.items():
             tot[k_] = tot.get(k_, 0) + v_
     n = args.batches
