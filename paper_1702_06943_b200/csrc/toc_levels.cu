@@ -61,8 +61,10 @@ struct LvlHdr {
   uint32_t off_uniq, off_rowoff, off_prs, off_inner, off_colst, off_stream;
   uint32_t off_trow;
   double vmax;  // max |value| of the value index (fixed-point precision check)
+  uint32_t invK, invM;  // 2^32 / K and 2^32 / M rounded up (M = pair slots per thread in the column pass):
+                        // x / K == umulhi(x, invK) for x < 2^16
 };
-static_assert(sizeof(LvlHdr) == 72, "slot cache header");
+static_assert(sizeof(LvlHdr) == 80, "slot cache header");
 constexpr uint32_t kHdrBytes = 80;
 
 TOC_HD uint32_t align4(uint32_t x) { return (x + 3u) & ~3u; }
@@ -85,7 +87,9 @@ TOC_HD LvlSmem lvl_smem(int kind, uint32_t n_cols, uint32_t max_slots, uint32_t 
   L.wt = o;  // each row's fixed-point weight (v^T.A)
   o += (kind & TOC_VECMAT) ? align16(8u * max_rows) : 0u;
   L.v = o;
-  o += (kind & TOC_MATVEC) ? align16(8u * n_cols) : 0u;
+  // A.v: v; v^T.A alone: a private copy of the column starts (the stage is refilled while the
+  // column totals still read them)
+  o += (kind & TOC_MATVEC) ? align16(8u * n_cols) : align16(2u * (n_cols + 1));
   L.rowcur = o;
   o += (kind & TOC_MATVEC) ? align16(4u * (max_rows + 1)) : 0u;
   L.stage = o;
@@ -373,6 +377,8 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
           w1 = K > 4 ? __ldg(stream + nth) : z4;
         }
       }
+      if (!MV)  // the column starts into a private copy: the stage is refilled before the column totals
+        for (uint32_t c = tid; c <= ncol; c += nth) reinterpret_cast<uint16_t*>(v_s)[c] = colst_s[c];
       __syncthreads();
       TOC_LVL_STAMP(1);
       // push: each inner slot's own T goes to every pair slot of its chain (inner records hold
@@ -456,13 +462,15 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
       TOC_LVL_STAMP(3);
       // column totals: columns spanning several ranges (tail, whole middle ranges, head), and 0
       // for the columns no pair touches
+      const uint16_t* colst_t = MV ? colst_s : reinterpret_cast<const uint16_t*>(v_s);
       for (uint32_t c = tid; c < ncol; c += nth) {
-        const uint32_t lo = colst_s[c], hi = colst_s[c + 1];
+        const uint32_t lo = colst_t[c], hi = colst_t[c + 1];
         TOC_CHECK(lo >= 1 && lo <= hi && hi <= nP + 1);
         if (lo == hi) {
           o[c] = 0.0;
         } else {
-          const uint32_t t0 = (lo - 1) / M, t1 = (hi - 2) / M;
+          const uint32_t t0 = M == 1 ? lo - 1 : __umulhi(lo - 1, h.invM), t1 = M == 1 ? hi - 2 : __umulhi(hi - 2, h.invM);
+          TOC_CHECK(t0 == (lo - 1) / M && t1 == (hi - 2) / M);
           if (t0 != t1) {
             double x = tail_s[t0];
             for (uint32_t t = t0 + 1; t < t1; ++t) x += tail_s[t];
@@ -544,7 +552,8 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
         if (lo == hi) {
           a.R[rb + r] = 0.0;
         } else {
-          const uint32_t t0 = lo / K, t1 = (hi - 1) / K;
+          const uint32_t t0 = __umulhi(lo, h.invK), t1 = __umulhi(hi - 1, h.invK);
+          TOC_CHECK(t0 == lo / K && t1 == (hi - 1) / K);
           if (t0 != t1) {
             double x = tail_s[t0];
             for (uint32_t t = t0 + 1; t < t1; ++t) x += tail_s[t];
@@ -790,7 +799,7 @@ void refine_banks(std::vector<uint32_t>& rec, const std::vector<uint32_t>& rowid
           const uint32_t xb = best_in(s, m, l, x, cx);  // flipping alone
           uint32_t best_gain = cost[si] - cx, best_j2 = j, best_y = xb, best_x2 = 0, best_c = cx, best_c2 = 0;
           for (uint32_t j2 = off[r]; j2 < off[r + 1]; ++j2) {
-            if (j2 == j || rec[j2] == x) continue;
+            if (j2 == j || rec[j2] == x || ((rec[j2] >> 16) != 0) != ((x >> 16) != 0)) continue;  // same class
             const uint32_t t2 = j2 / K, l2 = t2 & 31;
             const size_t si2 = (size_t)(t2 / 32) * K + j2 % K;
             if (si2 == si) continue;  // same step: only the half-warp would change
@@ -878,6 +887,42 @@ int build_entry(const uint8_t* blk, const TocBlockMeta& m, LvlEntry& out) {
   order.reserve(nI);
   for (uint32_t i = 1; i <= nI; ++i) order.push_back(i);
   std::stable_sort(order.begin(), order.end(), [&](uint32_t x, uint32_t y) { return pcol[x] < pcol[y]; });
+  // Which of a column's pairs takes which of the column's slots is free too.  The column pass
+  // walks slots [1 + tM, 1 + tM + M) in thread t, gathering each pair's value from the value index:
+  // per iteration and half-warp, the 16 lanes' value refs should fall into distinct bank pairs (ref
+  // mod 16; equal refs are a broadcast).  Column by column, each slot takes the remaining pair of
+  // its column whose ref is least loaded in its (warp, iteration, half-warp) group so far.
+  if (!getenv("TOC_LVL_PAIRS_PLAIN")) {
+    const uint32_t M = ((nI + T - 1) / T) | 1u;
+    std::vector<uint8_t> cnt((size_t)(T / 16) * M * 16, 0);       // [half-warp][iteration][bank pair]
+    std::vector<uint16_t> grp((size_t)(T / 16) * M * 16, 0xffffu);  // refs already gathered by the group
+    for (uint32_t k0 = 0; k0 < nI;) {
+      uint32_t k1 = k0 + 1;
+      while (k1 < nI && pcol[order[k1]] == pcol[order[k0]]) ++k1;
+      for (uint32_t k = k0; k < k1; ++k) {
+        const size_t g = ((size_t)(k / M / 16) * M + k % M) * 16;
+        uint32_t best = k, bc = ~0u;
+        for (uint32_t i = k; i < k1 && bc; ++i) {
+          const uint32_t ref = pref[order[i]];
+          uint32_t c = 1u + cnt[g + (ref & 15)];
+          for (uint32_t e = 0; e < 16 && grp[g + e] != 0xffffu; ++e)
+            if (grp[g + e] == ref) c = 0;
+          if (c < bc) bc = c, best = i;
+        }
+        std::swap(order[k], order[best]);
+        const uint32_t ref = pref[order[k]];
+        if (bc) {  // a new word for the group
+          ++cnt[g + (ref & 15)];
+          for (uint32_t e = 0; e < 16; ++e)
+            if (grp[g + e] == 0xffffu) {
+              grp[g + e] = (uint16_t)ref;
+              break;
+            }
+        }
+      }
+      k0 = k1;
+    }
+  }
   for (uint32_t k = 0; k < nI; ++k) slot[order[k]] = k + 1;
   std::vector<uint32_t> inn;
   for (uint64_t x = nI + 1; x < NT; ++x)
@@ -965,6 +1010,8 @@ int build_entry(const uint8_t* blk, const TocBlockMeta& m, LvlEntry& out) {
     vmax = std::max(vmax, std::fabs(x));
   }
   hd.vmax = vmax;
+  hd.invK = (uint32_t)(0xffffffffu / K + 1u);
+  hd.invM = (uint32_t)(0xffffffffu / (((nI + T - 1) / T) | 1u) + 1u);
   memcpy(e, &hd, sizeof hd);
   memcpy(e + hd.off_rowoff, off.data(), 4ull * (n + 1));
   uint32_t* pr = reinterpret_cast<uint32_t*>(e + hd.off_prs);

@@ -128,10 +128,11 @@ def emulate(h, enc, uniq, refs, v, u):
     head / tail partials combined in thread order)."""
     nP, nQ, S, C, K, T = h["nP"], h["nQ"], h["S"], h["C"], h["K"], h["T"]
     prs, inner, st = h["prs"], h["inner"], h["stream"]
-    # pairs numbered by (column, old id): the same (column, ref) records as the block
-    old = sorted(range(nP), key=lambda i: (enc.I_cols[i], i))
-    assert np.array_equal(prs & 0xFFFF, np.asarray(enc.I_cols, np.int64)[old])
-    assert np.array_equal((prs >> 16) & 0x7FFF, refs[old])
+    # pairs numbered by column (any order within a column: the builder picks it for the value
+    # gather's banks): the same (column, ref) records as the block
+    cols_b, refs_b = np.asarray(enc.I_cols, np.int64), np.asarray(refs, np.int64)
+    assert np.all(np.diff(prs & 0xFFFF) >= 0)
+    assert np.array_equal(np.sort((prs & 0xFFFF) << 16 | ((prs >> 16) & 0x7FFF)), np.sort(cols_b << 16 | refs_b))
     last = np.r_[(prs[1:] & 0xFFFF) != (prs[:-1] & 0xFFFF), True] if nP else np.zeros(0, bool)
     assert np.array_equal((prs >> 31) == 1, last), "column-end flags"
     prs = prs & 0x7FFFFFFF

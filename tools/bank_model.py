@@ -106,6 +106,27 @@ def model_inner(inner_raw: np.ndarray, nP: int):
     return dict(push=2 * at, push_ideal=2 * at_i, innerH=ga, innerH_ideal=ga_i)
 
 
+def model_pairs(prs: np.ndarray, T: int):
+    """Column-partials pass: thread t walks pair slots [1 + tM, 1 + tM + M); per iteration the value
+    index gather (64-bit, by value ref) and the v gather (64-bit, by column) of each half-warp."""
+    nP = len(prs)
+    M = ((nP + T - 1) // T) | 1
+    ref = (prs >> 16) & 0x7FFF
+    col = prs & 0xFFFF
+    gu = gv = ideal = 0
+    for w0 in range(0, T, 32):
+        for i in range(M):
+            for h0 in (w0, w0 + 16):
+                k = (np.arange(h0, h0 + 16) * M + i)
+                k = k[k < nP]
+                if not k.size:
+                    continue
+                ideal += 1
+                gu += np.bincount(np.unique(ref[k]) & 15, minlength=16).max()
+                gv += np.bincount(np.unique(col[k]) & 15, minlength=16).max()
+    return dict(uniq=gu, vcol=gv, pairs_ideal=ideal)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--batches", type=int, default=4)
@@ -129,6 +150,7 @@ def main():
         h = TL.entry(buf, o)
         st_raw = np.frombuffer(buf, np.uint32, h["T"] * h["K"], o + h["off_stream"]).astype(np.int64)
         r = model(st_raw, h["T"], h["K"], h["C"])
+        r.update(model_pairs(np.frombuffer(buf, np.uint32, h["nP"], o + h["off_prs"]).astype(np.int64), h["T"]))
         r.update(model_inner(np.frombuffer(buf, np.uint32, h["nQ"], o + h["off_inner"]).astype(np.int64), h["nP"]))
         for k_, v_ in r.items():
             tot[k_] = tot.get(k_, 0) + v_

@@ -38,4 +38,4 @@ for i, nm in enumerate(names):
     if col.any():
         print(f"  {nm:16s} {col.mean():8.0f}  ({100 * col.mean() / tot.mean():4.1f}%)")
 gap = t[1:, 0] - t[:-1, 7]
-print(f"  stage wait       {gap.mean():8.0f}")
+print(f"  between batches  {gap.mean():8.0f}  (includes the stamps' own 64-bit divisions)")
