@@ -129,14 +129,14 @@ __constant__ long long* g_trace = nullptr;
 // limb at 4(q ^ 1), the double at 4(q & ~1).
 // Stream records: reference a (bits 0-14) | row-end flag (bit 15) | reference b (bits 16-30; 0 =
 // none) | empty rows follow this row's end (bit 31: the next row is found by a search, else r + 1).
-constexpr uint32_t kRowEnd = 0x8000u, kSkip = 0x80000000u;
+constexpr uint32_t kRowEnd = 0x8000u;
 constexpr uint32_t kMaxSlots = 16384;  // 15-bit references
 
 TOC_HD uint32_t slot_ref(uint32_t p) { return 2u * p + ((p >> 4) & 1u); }
 
 // Byte offsets into the table from a record: the low limb of reference a / b, and the double.
-TOC_D uint32_t ref_a(uint32_t rec) { return (rec << 2) & 0x1fffcu; }
-TOC_D uint32_t ref_b(uint32_t rec) { return (rec >> 14) & 0x1fffcu; }
+TOC_D uint32_t ref_lo(uint32_t w) { return (w << 2) & 0x1fffcu; }   // the record in the low half of w
+TOC_D uint32_t ref_hi(uint32_t w) { return (w >> 14) & 0x1fffcu; }  // and in the high half
 
 // T[slot] += x (carry-free limbs, see limb_add in toc_batch.cuh) for the slot whose low limb is at
 // byte `lo` of the table.
@@ -162,21 +162,12 @@ TOC_D uint32_t row_of(const uint32_t* rowoff_s, uint32_t n, uint32_t s) {
   return lo;
 }
 
-// The next non-empty row after row r ends (n past the last); rec's skip flag says whether empty
-// rows follow.
-TOC_D uint32_t next_row(const uint32_t* rowoff_s, uint32_t n, uint32_t r, uint32_t rec) {
-  ++r;
-  if (rec & kSkip)
-    while (r < n && rowoff_s[r + 1] == rowoff_s[r]) ++r;
-  return r;
-}
-
-// Walk this thread's K records (zero-padded past the last code: slot 0, no row end), four per
-// 16-byte load, two loads in flight.  chunk(w) handles four records; w0 / w1 are the first two
+// Walk this thread's K records (zero-padded past the last one: slot 0, no row end), eight per
+// 16-byte load, two loads in flight.  chunk(w) handles eight records; w0 / w1 are the first two
 // chunks, loaded by the caller ahead of time.
 template <typename Chunk>
 TOC_D void walk_stream(const uint4* __restrict__ st, uint32_t nth, uint32_t K, uint4 w0, uint4 w1, Chunk&& chunk) {
-  const uint32_t nq = K >> 2;
+  const uint32_t nq = K >> 3;
   for (uint32_t q = 0; q < nq; ++q) {
     const uint4 w = w0;
     w0 = w1;
@@ -308,7 +299,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
     const LvlHdr h = *reinterpret_cast<const LvlHdr*>(stage);  // the stage is refilled mid-batch
     const uint32_t n = h.n_rows, nP = h.nP, nQ = h.nQ, K = h.K;
     TOC_CHECK(h.S <= (uint32_t)a.max_slots && h.off_stream <= (uint32_t)a.max_stage && n <= (uint32_t)a.max_rows &&
-              h.T == nth && h.n_cols == ncol && h.S == 1 + nP + nQ && K % 4 == 0 && h.C <= h.T * K);
+              h.T == nth && h.n_cols == ncol && h.S == 1 + nP + nQ && K % 8 == 0 && h.C <= h.T * K);
     const double* uniq_s = reinterpret_cast<const double*>(stage + h.off_uniq);
     const uint32_t* rowoff_s = reinterpret_cast<const uint32_t*>(stage + h.off_rowoff);
     const uint32_t* prs_s = reinterpret_cast<const uint32_t*>(stage + h.off_prs);
@@ -317,7 +308,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
     const int64_t rb = a.row_base[b];
     const uint4* stream = reinterpret_cast<const uint4*>(a.lvl + a.lvl_off[b] + h.off_stream) + tid;
     const bool active = tid * K < h.C;
-    uint4 w0 = active ? __ldg(stream) : z4, w1 = active && K > 4 ? __ldg(stream + nth) : z4;
+    uint4 w0 = active ? __ldg(stream) : z4, w1 = active && K > 8 ? __ldg(stream + nth) : z4;
     const uint32_t tr0 = active ? reinterpret_cast<const uint16_t*>(stage + h.off_trow)[tid] : 0u;
     const uint32_t r0 = tr0 & 0x7fffu;  // this thread's first row, and whether its range starts it
     const bool here0 = (tr0 >> 15) != 0;
@@ -346,13 +337,13 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
             const uint32_t rec[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
             for (uint32_t i = 0; i < 4; ++i) {
-              TOC_CHECK(ref_a(rec[i]) < 8 * h.S && ref_b(rec[i]) < 8 * h.S && (rec[i] == 0 || r < n));
-              limb_add_at(tabp, ref_a(rec[i]), xl, xh);
-              if (ref_b(rec[i])) limb_add_at(tabp, ref_b(rec[i]), xl, xh);
-              if (rec[i] & kRowEnd) {
-                r = next_row(rowoff_s, n, r, rec[i]);
-                if (r < n) weight(r, xl, xh);
-              }
+              TOC_CHECK(ref_lo(rec[i]) < 8 * h.S && ref_hi(rec[i]) < 8 * h.S && (rec[i] == 0 || r < n));
+              limb_add_at(tabp, ref_lo(rec[i]), xl, xh);
+              if (rec[i] & kRowEnd)
+                if (++r < n) weight(r, xl, xh);
+              limb_add_at(tabp, ref_hi(rec[i]), xl, xh);
+              if (rec[i] & (kRowEnd << 16))
+                if (++r < n) weight(r, xl, xh);
             }
           });
         } else {
@@ -361,20 +352,18 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
             const uint32_t rec[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
             for (uint32_t i = 0; i < 4; ++i) {
-              if (wu != 0.0) {
-                atomicAdd(reinterpret_cast<double*>(tabp + (ref_a(rec[i]) & ~7u)), wu);
-                if (ref_b(rec[i])) atomicAdd(reinterpret_cast<double*>(tabp + (ref_b(rec[i]) & ~7u)), wu);
-              }
-              if (rec[i] & kRowEnd) {
-                r = next_row(rowoff_s, n, r, rec[i]);
-                if (r < n) wu = u_s[r];
-              }
+              if (wu != 0.0) atomicAdd(reinterpret_cast<double*>(tabp + (ref_lo(rec[i]) & ~7u)), wu);
+              if (rec[i] & kRowEnd)
+                if (++r < n) wu = u_s[r];
+              if (wu != 0.0) atomicAdd(reinterpret_cast<double*>(tabp + (ref_hi(rec[i]) & ~7u)), wu);
+              if (rec[i] & (kRowEnd << 16))
+                if (++r < n) wu = u_s[r];
             }
           });
         }
         if (MV) {  // the stream again for A.v
           w0 = __ldg(stream);
-          w1 = K > 4 ? __ldg(stream + nth) : z4;
+          w1 = K > 8 ? __ldg(stream + nth) : z4;
         }
       }
       if (!MV)  // the column starts into a private copy: the stage is refilled before the column totals
@@ -525,21 +514,24 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
           double ha[4], hb[4];
 #pragma unroll
           for (uint32_t i = 0; i < 4; ++i) {
-            TOC_CHECK(ref_a(rec[i]) < 8 * h.S && ref_b(rec[i]) < 8 * h.S);
-            ha[i] = *reinterpret_cast<const double*>(tabp + (ref_a(rec[i]) & ~7u));
-            hb[i] = ref_b(rec[i]) ? *reinterpret_cast<const double*>(tabp + (ref_b(rec[i]) & ~7u)) : 0.0;
+            TOC_CHECK(ref_lo(rec[i]) < 8 * h.S && ref_hi(rec[i]) < 8 * h.S);
+            ha[i] = *reinterpret_cast<const double*>(tabp + (ref_lo(rec[i]) & ~7u));
+            hb[i] = *reinterpret_cast<const double*>(tabp + (ref_hi(rec[i]) & ~7u));
           }
+          auto row_end = [&]() {
+            TOC_CHECK(r < n);
+            if (here) a.R[rb + r] = acc;
+            else head_s[tid] = acc;
+            acc = 0.0;
+            here = true;
+            ++r;
+          };
 #pragma unroll
           for (uint32_t i = 0; i < 4; ++i) {
-            acc += ha[i] + hb[i];  // the code's value: one add on the row's dependency chain
-            if (rec[i] & kRowEnd) {
-              TOC_CHECK(r < n);
-              if (here) a.R[rb + r] = acc;
-              else head_s[tid] = acc;
-              acc = 0.0;
-              here = true;
-              r = next_row(rowcur_s, n, r, rec[i]);
-            }
+            acc += ha[i];
+            if (rec[i] & kRowEnd) row_end();
+            acc += hb[i];
+            if (rec[i] & (kRowEnd << 16)) row_end();
           }
         });
         tail_s[tid] = acc;
@@ -981,12 +973,35 @@ int build_entry(const uint8_t* blk, const TocBlockMeta& m, LvlEntry& out) {
   }
   for (uint32_t q = 0; q < nQ; ++q) slot[inn[q]] = nI + 1 + q;
   const uint32_t S = 1 + nI + nQ;
-  // stream: thread t owns codes [t*K, t*K + K); record k of thread t at (k/4)*4T + 4t + k%4
-  uint32_t K = (C + T - 1) / T;
-  K = std::max(4u, (K + 3u) & ~3u);
+  // records in row order, one slot reference each: a code whose node has a slot is one record, a
+  // leaf two (its parent's slot and its key's); an empty row is one record of slot 0 (a zero), so
+  // every row ends with a flagged record and the kernel never searches for the next row
+  std::vector<uint32_t> rec, rowid, roff(n + 1, 0);
+  rec.reserve((size_t)C + C / 2 + n);
+  rowid.reserve(rec.capacity());
+  for (uint32_t r = 0; r < n; ++r) {
+    roff[r] = (uint32_t)rec.size();
+    for (uint32_t j = off[r]; j < off[r + 1]; ++j) {
+      const uint32_t x = code[j];
+      if (x <= nI || inner[x]) {
+        rec.push_back(toc::slot_ref(slot[x]));
+      } else {
+        rec.push_back(toc::slot_ref(slot[par[x]]));
+        rec.push_back(toc::slot_ref(slot[key[x]]));
+      }
+    }
+    if (rec.size() == roff[r]) rec.push_back(0u);
+    rowid.resize(rec.size(), r);
+  }
+  roff[n] = (uint32_t)rec.size();
+  const uint32_t NR = (uint32_t)rec.size();
+  // stream: thread t owns records [t*K, t*K + K); record k of thread t is the u16 at
+  // (k/8)*8T + 8t + k%8
+  uint32_t K = (NR + T - 1) / T;
+  K = std::max(8u, (K + 7u) & ~7u);
   // serialize
   LvlHdr hd{};
-  hd.nP = nI, hd.nQ = nQ, hd.S = S, hd.C = C, hd.K = K, hd.T = T, hd.n_rows = n, hd.n_cols = m.n_cols, hd.nU = nU;
+  hd.nP = nI, hd.nQ = nQ, hd.S = S, hd.C = NR, hd.K = K, hd.T = T, hd.n_rows = n, hd.n_cols = m.n_cols, hd.nU = nU;
   uint32_t o = toc::kHdrBytes;
   auto sec = [&](uint64_t bytes) {
     const uint32_t s = o;
@@ -999,7 +1014,7 @@ int build_entry(const uint8_t* blk, const TocBlockMeta& m, LvlEntry& out) {
   hd.off_inner = sec(4ull * nQ);
   hd.off_colst = sec(2ull * (m.n_cols + 1));
   hd.off_trow = sec(2ull * T);
-  hd.off_stream = sec(4ull * T * K);
+  hd.off_stream = sec(2ull * T * K);
   out.bytes.assign(o, 0);
   uint8_t* e = out.bytes.data();
   double vmax = 0.0;
@@ -1013,7 +1028,7 @@ int build_entry(const uint8_t* blk, const TocBlockMeta& m, LvlEntry& out) {
   hd.invK = (uint32_t)(0xffffffffu / K + 1u);
   hd.invM = (uint32_t)(0xffffffffu / (((nI + T - 1) / T) | 1u) + 1u);
   memcpy(e, &hd, sizeof hd);
-  memcpy(e + hd.off_rowoff, off.data(), 4ull * (n + 1));
+  memcpy(e + hd.off_rowoff, roff.data(), 4ull * (n + 1));
   uint32_t* pr = reinterpret_cast<uint32_t*>(e + hd.off_prs);
   for (uint32_t k = 0; k < nI; ++k) {  // column | value ref << 16 | last-of-its-column << 31
     const bool last = k + 1 == nI || pcol[order[k + 1]] != pcol[order[k]];
@@ -1027,36 +1042,22 @@ int build_entry(const uint8_t* blk, const TocBlockMeta& m, LvlEntry& out) {
     while (k < nI && pcol[order[k]] < c) ++k;
     cs[c] = (uint16_t)(k + 1);
   }
-  // records in row order (row-end flag on each row's last code)
-  std::vector<uint32_t> rec(C), rowid(C);
-  for (uint32_t r = 0; r < n; ++r)
-    for (uint32_t j = off[r]; j < off[r + 1]; ++j) {
-      const uint32_t x = code[j];
-      rec[j] = (x <= nI || inner[x]) ? toc::slot_ref(slot[x])
-                                     : (toc::slot_ref(slot[par[x]]) | (toc::slot_ref(slot[key[x]]) << 16));
-      rowid[j] = r;
-    }
-  schedule_banks(rec, rowid, off, n, C, K, T);
+  schedule_banks(rec, rowid, roff, n, NR, K, T);
   {
     const char* e_ref = getenv("TOC_LVL_REFINE");  // experiment knob: local-search passes (default 2)
     const int passes = e_ref ? atoi(e_ref) : 2;
-    if (passes > 0) refine_banks(rec, rowid, off, C, K, T, passes);
+    if (passes > 0) refine_banks(rec, rowid, roff, NR, K, T, passes);
   }
   uint16_t* tr = reinterpret_cast<uint16_t*>(e + hd.off_trow);
-  for (uint32_t t = 0; t < T && (uint64_t)t * K < C; ++t) {
+  for (uint32_t t = 0; t < T && (uint64_t)t * K < NR; ++t) {
     const uint32_t r = rowid[t * K];
-    tr[t] = (uint16_t)(r | (off[r] == t * K ? 0x8000u : 0u));
+    tr[t] = (uint16_t)(r | (roff[r] == t * K ? 0x8000u : 0u));
   }
-  uint32_t* st = reinterpret_cast<uint32_t*>(e + hd.off_stream);
-  for (uint32_t j = 0; j < C; ++j) {
-    const uint32_t r = rowid[j];
-    uint32_t flag = 0;
-    if (j + 1 == off[r + 1]) {  // last code of its row; empty rows after it?
-      flag = toc::kRowEnd;
-      if (r + 1 < n && off[r + 2] == off[r + 1]) flag |= toc::kSkip;
-    }
+  uint16_t* st = reinterpret_cast<uint16_t*>(e + hd.off_stream);
+  for (uint32_t j = 0; j < NR; ++j) {
+    const uint32_t flag = j + 1 == roff[rowid[j] + 1] ? toc::kRowEnd : 0u;  // last record of its row
     const uint32_t t = j / K, k = j % K;
-    st[(uint64_t)(k >> 2) * 4 * T + 4 * t + (k & 3u)] = rec[j] | flag;
+    st[(uint64_t)(k >> 3) * 8 * T + 8 * t + (k & 7u)] = (uint16_t)(rec[j] | flag);
   }
   out.S = S;
   out.stage = hd.off_stream;  // header included

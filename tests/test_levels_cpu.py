@@ -89,12 +89,12 @@ def entry(buf, o):
     inner = u32(h["off_inner"], h["nQ"])  # references -> slot numbers: par | key << 16
     h["inner"] = slot_of(inner & 0xFFFF) | (slot_of(inner >> 16) << 16)
     T, K = h["T"], h["K"]
-    st = u32(h["off_stream"], T * K)
-    # record k of thread t at (k // 4) * 4T + 4t + k % 4  ->  row order j = t*K + k
+    st = np.frombuffer(buf, np.uint16, T * K, o + h["off_stream"]).astype(np.int64)
+    # record k of thread t is the u16 at (k // 8) * 8T + 8t + k % 8  ->  row order j = t*K + k
     k = np.arange(K)
-    pos = (k[None, :] // 4) * 4 * T + 4 * np.arange(T)[:, None] + (k[None, :] % 4)
+    pos = (k[None, :] // 8) * 8 * T + 8 * np.arange(T)[:, None] + (k[None, :] % 8)
     st = st[pos.reshape(-1)][: h["C"]]
-    h["stream"] = slot_of(st & 0x7FFF) | (st & 0x8000) | (slot_of((st >> 16) & 0x7FFF) << 16) | (st & 0x80000000)
+    h["stream"] = slot_of(st & 0x7FFF) | (st & 0x8000)  # one slot per record | row-end flag
     h["colst"] = np.frombuffer(buf, np.uint16, h["n_cols"] + 1, o + h["off_colst"]).astype(np.int64)
     h["uniq"] = np.frombuffer(buf, np.float64, h["nU"], o + h["off_uniq"]).copy()
     h["rowoff"] = u32(h["off_rowoff"], h["n_rows"] + 1)
@@ -153,7 +153,7 @@ def emulate(h, enc, uniq, refs, v, u):
         for i, x in enumerate(chain(y)):
             hv = H[x] if i == 0 else hv + H[x]
         H[y] = hv
-    off = np.asarray(enc.offsets, np.int64)
+    off = h["rowoff"]  # row offsets into the record stream
     n = h["n_rows"]
     row_of = np.repeat(np.arange(n), np.diff(off))
     R = np.zeros(n)
@@ -164,10 +164,7 @@ def emulate(h, enc, uniq, refs, v, u):
             continue
         acc = 0.0
         for j in range(s0, e0):
-            a_, b_ = st[j] & 0x7FFF, (st[j] >> 16) & 0x7FFF
-            acc += H[a_]
-            if b_:
-                acc += H[b_]
+            acc += H[st[j] & 0x7FFF]
             r = row_of[j]
             if j + 1 == off[r + 1]:
                 if off[r] >= s0:
@@ -187,10 +184,8 @@ def emulate(h, enc, uniq, refs, v, u):
     # v^T.A: T[slot] += u[r] (the kernel's fixed point is exact; fp64 here), push, columns
     Tv = np.zeros(S)
     for j in range(C):
-        a_, b_ = st[j] & 0x7FFF, (st[j] >> 16) & 0x7FFF
-        Tv[a_] += u[row_of[j]]
-        if b_:
-            Tv[b_] += u[row_of[j]]
+        Tv[st[j] & 0x7FFF] += u[row_of[j]]
+    Tv[0] = 0.0  # slot 0 collects the empty rows' records; nothing reads it
     own = Tv.copy()
     for y in range(nP + 1, S):
         for x in chain(y):
@@ -205,8 +200,13 @@ def emulate(h, enc, uniq, refs, v, u):
 
 def structure(h, enc):
     nP, nQ, S = h["nP"], h["nQ"], h["S"]
-    assert nP == len(enc.I_cols) and S == 1 + nP + nQ and h["C"] == len(enc.codes)
-    assert h["K"] % 4 == 0 and h["K"] * h["T"] >= h["C"]
+    assert nP == len(enc.I_cols) and S == 1 + nP + nQ
+    assert h["K"] % 8 == 0 and h["K"] * h["T"] >= h["C"]
+    # records: one per code with a slot, two per leaf, one (slot 0) per empty row
+    codes_per_row = np.diff(np.asarray(enc.offsets, np.int64))
+    recs_per_row = np.diff(h["rowoff"])
+    assert h["rowoff"][0] == 0 and h["rowoff"][-1] == h["C"]
+    assert np.all(recs_per_row >= np.maximum(codes_per_row, 1)) and np.all(recs_per_row <= np.maximum(2 * codes_per_row, 1))
     assert np.all(np.diff(h["prs"] & 0xFFFF) >= 0), "pairs not column-sorted"
     par, key = h["inner"] & 0xFFFF, h["inner"] >> 16
     assert np.all((key >= 1) & (key <= nP)), "inner keys must be pairs"
@@ -216,11 +216,13 @@ def structure(h, enc):
         while p > nP:
             p, steps = par[p - nP - 1], steps + 1
             assert steps <= nQ, "inner parent cycle"
-    a_, b_ = h["stream"] & 0x7FFF, (h["stream"] >> 16) & 0x7FFF
-    assert np.all((a_ >= 1) & (a_ < S)) and np.all(b_ < S), "stream references"
-    off = np.asarray(enc.offsets, np.int64)
+    a_ = h["stream"] & 0x7FFF
+    assert np.all(a_ < S), "stream references"
+    off = h["rowoff"]
+    empty = np.repeat(codes_per_row == 0, recs_per_row)
+    assert np.array_equal(a_ == 0, empty), "slot 0 marks exactly the empty rows"
     ends = np.zeros(h["C"], bool)
-    ends[off[1:][np.diff(off) > 0] - 1] = True
+    ends[off[1:] - 1] = True
     assert np.array_equal((h["stream"] & 0x8000) != 0, ends), "row-end flags"
     cs = h["colst"]
     assert cs[0] == 1 and cs[-1] == nP + 1 and np.all(np.diff(cs) >= 0)
@@ -255,7 +257,6 @@ def test_level_cache_matches_oracle(oracle, name, rows, m):
         structure(h, e)
         uniq, refs = value_index(blocks[b])
         assert np.array_equal(h["uniq"], uniq) and h["vmax"] == (np.abs(uniq).max() if len(uniq) else 0.0)
-        assert np.array_equal(h["rowoff"], np.asarray(e.offsets, np.int64))
         v = rng.standard_normal(m)
         u = rng.standard_normal(e.n_rows)
         R, O = emulate(h, e, uniq, refs, v, u)
@@ -282,7 +283,6 @@ def test_level_cache_config2_batches(oracle):
         assert h["S"] <= 16384 and h["nQ"] < h["C"] // 4
         uniq, refs = value_index(blocks[b])
         assert np.array_equal(h["uniq"], uniq) and h["vmax"] == (np.abs(uniq).max() if len(uniq) else 0.0)
-        assert np.array_equal(h["rowoff"], np.asarray(e.offsets, np.int64))
         v, u = rng.standard_normal(784), rng.standard_normal(e.n_rows)
         R, O = emulate(h, e, uniq, refs, v, u)
         t = oracle.Tree.from_encoding(e)

@@ -28,10 +28,10 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 def model(st_raw: np.ndarray, T: int, K: int, C: int):
     """st_raw: the entry's stream as stored (interleaved), u32[T*K].  Returns modelled wavefronts."""
     k = np.arange(K)
-    pos = (k[None, :] // 4) * 4 * T + 4 * np.arange(T)[:, None] + (k[None, :] % 4)
+    pos = (k[None, :] // 8) * 8 * T + 8 * np.arange(T)[:, None] + (k[None, :] % 8)
     st = st_raw[pos]  # [T, K]
     qa = st & 0x7FFF
-    qb = (st >> 16) & 0x7FFF
+    qb = np.zeros_like(qa)  # one reference per record
     act = np.broadcast_to((np.arange(T)[:, None] * K) < C, (T, K))  # inactive threads skip the walk
     W = T // 32
     at_a = at_b = ga = gb = 0
@@ -148,7 +148,7 @@ def main():
     for b in range(args.batches):
         o = int(eo[b])
         h = TL.entry(buf, o)
-        st_raw = np.frombuffer(buf, np.uint32, h["T"] * h["K"], o + h["off_stream"]).astype(np.int64)
+        st_raw = np.frombuffer(buf, np.uint16, h["T"] * h["K"], o + h["off_stream"]).astype(np.int64)
         r = model(st_raw, h["T"], h["K"], h["C"])
         r.update(model_pairs(np.frombuffer(buf, np.uint32, h["nP"], o + h["off_prs"]).astype(np.int64), h["T"]))
         r.update(model_inner(np.frombuffer(buf, np.uint32, h["nQ"], o + h["off_inner"]).astype(np.int64), h["nP"]))
