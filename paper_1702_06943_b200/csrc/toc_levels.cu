@@ -9,34 +9,38 @@
 // every pair of x's expansion (v^T.A).  A derived node x is (par, key) with H[x] = H[par] + P1[key],
 // so a code whose node is a *leaf* of the used tree is evaluated from two slots, H[par] + H[key],
 // and needs no slot itself.  Slots exist only for
-//   the pairs (depth 1: H = P1 = value * v[col]), numbered by (column, pair id), and
+//   the pairs (depth 1: H = P1 = value * v[col]), numbered by column (within a column in the
+//   order that spreads the value-index gather over the banks), and
 //   the inner nodes: derived nodes some used derived node hangs off (closed under parents) --
-//   ~3.5 k of a config-2 batch's ~24 k derived nodes.
+//   ~3.2 k of a config-2 batch's ~24 k derived nodes -- numbered for the banks of their chains.
 // Cache entry (built once per arena on the host, the counterpart of the reference's cached
 // CompressedMatrix.tree, kernels.py:68-77), self-contained so a launch reads nothing else:
 //   header  LvlHdr (80 B)
 //   staged region, one TMA bulk copy into shared memory per batch:
 //     uniq   f64[nU]    the block's value index (physical.py:49-130), aligned
-//     rowoff u32[n+1]   row offsets into the code stream
+//     rowoff u32[n+1]   row offsets into the record stream
 //     prs    u32[nP]    column | value ref << 16 of pair slot 1 + i
 //     inner  u32[nQ]    ref(par) | ref(key) << 16 of inner slot nP + 1 + q   (key is a pair; a
 //                       reference is the slot's low-limb word index, see slot_ref)
 //     colst  u16[n_cols + 1]  first pair slot of every column (pairs are column-sorted)
-//     trow   u16[T]     row of thread t's first code | (the code starts its row) << 15
-//   stream u32[T*K]  per code in row order: ref a | row-end flag | ref b << 16 -- a = the code's
-//                    own slot (b = 0), or a = slot(par), b = slot(key) for a leaf; thread t owns
-//                    codes [t*K, t*K + K), stored interleaved in groups of four so a warp's 16-byte
-//                    loads are contiguous
+//     trow   u16[T]     row of thread t's first record | (the record starts its row) << 15
+//   stream u16[T*K]  one record per slot reference, in row order: reference | row-end flag << 15.
+//                    A code whose node has a slot is one record, a leaf two (slot(par), slot(key)),
+//                    an empty row one record of slot 0 (a zero) -- every row ends with a flagged
+//                    record, every access instruction runs with full warps.  Thread t owns records
+//                    [t*K, t*K + K), stored interleaved in groups of eight so a warp's 16-byte
+//                    loads are contiguous; which of a row's records sits at which of the row's
+//                    positions is chosen for the banks (schedule_banks, refine_banks)
 // Per batch (one 1024-thread CTA, tables in shared memory):
 //   A.v   P1 for the pair slots; H of the inner slots, each the sum of P1 over its own chain (no
-//         level barriers); every thread sums its K codes row by row; rows crossing a range
+//         level barriers); every thread sums its K records row by row; rows crossing a range
 //         boundary are finished from per-thread head / tail partials in thread order
-//   v^T.A T[slot] += u[r] for every code's slot(s): exact fixed point (two 32-bit limbs added with
+//   v^T.A T[slot] += u[r] for every record: exact fixed point (two 32-bit limbs added with
 //         native shared-memory atomics, carry-free, see limb_add) -- order-independent
 //         push: every inner slot adds its T to each pair slot of its chain
 //         O[c] = sum over column c's pair slots of value * T, in slot order
-// Every thread does the same number of codes (no divergence on chain lengths), the stream is read
-// with coalesced loads, a code costs one or two table accesses, every sum has a fixed order.
+// Every thread does the same number of records (no divergence on chain lengths), the stream is
+// read with coalesced loads, a record costs one table access, every sum has a fixed order.
 // DESIGN.md 4.1.
 #include <algorithm>
 #include <atomic>
@@ -127,14 +131,13 @@ __constant__ long long* g_trace = nullptr;
 // and H share their bytes (the fused kernel turns T[p] into H[p] in place, pair by pair).  A
 // reference is q = 2p + ((p >> 4) & 1), the word index of the low limb: low limb at byte 4q, high
 // limb at 4(q ^ 1), the double at 4(q & ~1).
-// Stream records: reference a (bits 0-14) | row-end flag (bit 15) | reference b (bits 16-30; 0 =
-// none) | empty rows follow this row's end (bit 31: the next row is found by a search, else r + 1).
+// Stream records (16 bits): reference (bits 0-14) | row-end flag (bit 15); two per 32-bit word.
 constexpr uint32_t kRowEnd = 0x8000u;
 constexpr uint32_t kMaxSlots = 16384;  // 15-bit references
 
 TOC_HD uint32_t slot_ref(uint32_t p) { return 2u * p + ((p >> 4) & 1u); }
 
-// Byte offsets into the table from a record: the low limb of reference a / b, and the double.
+// Byte offset of the low limb from a record (the double: & ~7).
 TOC_D uint32_t ref_lo(uint32_t w) { return (w << 2) & 0x1fffcu; }   // the record in the low half of w
 TOC_D uint32_t ref_hi(uint32_t w) { return (w >> 14) & 0x1fffcu; }  // and in the high half
 
@@ -592,52 +595,24 @@ struct LvlCache {
   int32_t status = TOC_OK;
 };
 
-// Bank-aware placement of the records (the kernel's row sums and T scatter are bound by shared-
-// memory wavefronts, and a warp-wide gather or atomic costs one wavefront per distinct word in the
-// most loaded bank).  Position j = t*K + k is thread t's k-th record; a row's positions keep their
-// row (so the per-thread row logic and the row-end flags are unchanged) but which of the row's
-// codes sits at which of its positions is free (the row sum does not depend on it), and a
-// two-slot record may be stored (key, par) instead of (par, key).  Warp by warp, step by step,
-// each lane (fewest choices first) takes from its row's remaining codes the one whose slots hit
-// the least used banks (slot mod 32) among the lanes placed so far in this step.
+// Bank-aware placement of the records.  The kernel's T scatter and row sums are bound by shared-
+// memory wavefronts: a warp's 32-bit atomics cost one wavefront per lane in the most loaded bank
+// (the low-limb word q mod 32; the high limb q ^ 1 mirrors it), a 64-bit gather one per distinct
+// word in the most loaded bank pair ((q >> 1) mod 16) of each half-warp.  Position j = t*K + k is
+// thread t's k-th record; a row's positions keep their row (so the per-thread row logic and the
+// row-end flags are unchanged) but which of the row's records sits at which of its positions is
+// free (the row's sums do not depend on it).  Warp by warp, step by step, each lane (fewest choices
+// first) takes from its row's remaining records the one whose word hits the least used bank and
+// bank pair among the lanes placed so far in this step.
 void schedule_banks(std::vector<uint32_t>& rec, const std::vector<uint32_t>& rowid, const std::vector<uint32_t>& off,
                     uint32_t n, uint32_t C, uint32_t K, uint32_t T) {
-  const char* e_old = getenv("TOC_LVL_SCHED");  // experiment knob: 0 = atomics' banks only (round-2f placement)
-  const bool old = e_old && atoi(e_old) == 0;
-  const bool spread = e_old && atoi(e_old) <= 1;  // 1 = banks + bank pairs, two-reference records anywhere
-  // Two-reference records (leaves: parent + key) go to the row's positions with the smallest step
-  // index, so that a warp's second-reference accesses are either (nearly) full or empty: a step
-  // costs at least one wavefront per access instruction that has any lane, however few.
-  std::vector<std::vector<uint32_t>> pool2(n), pool1(n);
-  std::vector<uint8_t> two(C, 0);
-  {
-    std::vector<uint32_t> cnt(K + 1);
-    for (uint32_t r = 0; r < n; ++r) {
-      uint32_t n2 = 0;
-      for (uint32_t j = off[r]; j < off[r + 1]; ++j) {
-        if (rec[j] >> 16) pool2[r].push_back(rec[j]), ++n2;
-        else pool1[r].push_back(rec[j]);
-      }
-      if (!spread) {
-        // the n2 positions of the row with the smallest steps (ties: first come)
-        std::fill(cnt.begin(), cnt.end(), 0u);
-        for (uint32_t j = off[r]; j < off[r + 1]; ++j) ++cnt[j % K];
-        uint32_t thr = 0, left = n2;
-        while (thr < K && cnt[thr] <= left) left -= cnt[thr++];
-        for (uint32_t j = off[r]; j < off[r + 1]; ++j) {
-          const uint32_t k = j % K;
-          if (k < thr) two[j] = 1;
-          else if (k == thr && left) two[j] = 1, --left;
-        }
-      }
-    }
-  }
+  std::vector<std::vector<uint32_t>> pool(n);
+  for (uint32_t r = 0; r < n; ++r) pool[r].assign(rec.begin() + off[r], rec.begin() + off[r + 1]);
   // seen[h][word] == stamp: the 8-byte word is already gathered by a placed lane of half-warp h in
   // this step (a 64-bit gather of the same word is a broadcast, not a conflict)
   std::vector<uint32_t> seen[2] = {std::vector<uint32_t>(toc::kMaxSlots, 0), std::vector<uint32_t>(toc::kMaxSlots, 0)};
   uint32_t stamp = 0;
   uint32_t lanes[32];
-  const uint32_t wa = old ? 3u : 4u, wb = old ? 2u : 4u, wg = old ? 0u : 3u;
   for (uint32_t w = 0; w < T / 32; ++w) {
     if ((uint64_t)w * 32 * K >= C) break;
     for (uint32_t k = 0; k < K; ++k) {
@@ -648,106 +623,69 @@ void schedule_banks(std::vector<uint32_t>& rec, const std::vector<uint32_t>& row
       }
       if (!na) continue;
       std::stable_sort(lanes, lanes + na, [&](uint32_t x, uint32_t y) {
-        const uint32_t rx = rowid[(w * 32 + x) * K + k], ry = rowid[(w * 32 + y) * K + k];
-        return pool1[rx].size() + pool2[rx].size() < pool1[ry].size() + pool2[ry].size();
+        return pool[rowid[(w * 32 + x) * K + k]].size() < pool[rowid[(w * 32 + y) * K + k]].size();
       });
-      // ca / cb: lanes per 32-bit bank of the low-limb words (the scatter's atomics: reference a,
-      // then reference b); ga / gb: distinct 8-byte words per bank pair and half-warp (the row
-      // gathers)
-      uint8_t ca[32] = {0}, cb[32] = {0}, ga[2][16] = {{0}}, gb[2][16] = {{0}};
+      // ca: lanes per 32-bit bank of the low-limb words (the scatter's atomics); ga: distinct 8-byte
+      // words per bank pair and half-warp (the row gathers)
+      uint8_t ca[32] = {0}, ga[2][16] = {{0}};
       ++stamp;
       for (uint32_t q = 0; q < na; ++q) {
         const uint32_t j = (w * 32 + lanes[q]) * K + k, hf = lanes[q] >> 4;
-        const uint32_t rj = rowid[j];
-        // the position's class; with the classes spread (knob) whichever pool is relatively fuller
-        const bool use2 = spread ? (pool1[rj].empty() || (!pool2[rj].empty() && (stamp + j) % (pool1[rj].size() + pool2[rj].size()) < pool2[rj].size()))
-                                 : (two[j] != 0);
-        std::vector<uint32_t>& P = use2 ? pool2[rj] : pool1[rj];
-        auto cost_a = [&](uint32_t a) { return wa * ca[a & 31] + (seen[hf][a >> 1] == stamp ? 0u : wg * ga[hf][(a >> 1) & 15]); };
-        auto cost_b = [&](uint32_t b) { return wb * cb[b & 31] + (seen[hf][b >> 1] == stamp ? 0u : wg * gb[hf][(b >> 1) & 15]); };
+        std::vector<uint32_t>& P = pool[rowid[j]];
         size_t best = 0;
-        bool swap = false;
         uint32_t bc = ~0u;
         for (size_t i = 0; i < P.size() && bc; ++i) {
-          const uint32_t a = P[i] & 0xffffu, b = P[i] >> 16;
-          const uint32_t c = cost_a(a) + (b ? cost_b(b) : 0u);
-          if (c < bc) bc = c, best = i, swap = false;
-          if (b) {
-            const uint32_t c2 = cost_a(b) + cost_b(a);
-            if (c2 < bc) bc = c2, best = i, swap = true;
-          }
+          const uint32_t a = P[i];
+          const uint32_t c = 4u * ca[a & 31] + (seen[hf][a >> 1] == stamp ? 0u : 3u * ga[hf][(a >> 1) & 15]);
+          if (c < bc) bc = c, best = i;
         }
-        uint32_t x = P[best];
+        const uint32_t a = P[best];
         P[best] = P.back();
         P.pop_back();
-        if (swap) x = (x >> 16) | ((x & 0xffffu) << 16);
-        const uint32_t a = x & 0xffffu, b = x >> 16;
         ++ca[a & 31];
         if (seen[hf][a >> 1] != stamp) ++ga[hf][(a >> 1) & 15];
-        if (b) {
-          ++cb[b & 31];
-          if (seen[hf][b >> 1] != stamp) ++gb[hf][(b >> 1) & 15];
-        }
-        // a and b gathers are separate instructions: separate word sets would be exact; one set
-        // is a close bound (a word shared between an a and a b lane is rare)
         seen[hf][a >> 1] = stamp;
-        if (b) seen[hf][b >> 1] = stamp;
-        rec[j] = x;
+        rec[j] = a;
       }
     }
   }
 }
 
 // Local search after the greedy placement: for every (warp, step) above its conflict-free cost, a
-// lane sitting in a most loaded bank trades records with another position of its row (either
-// orientation of a two-reference record) when that lowers the modelled wavefronts of the two steps
-// involved.  Model (what tools/bank_model.py reports, with lanes counted instead of distinct
-// words): per step 2 x (most loaded 32-bit bank of the a atomics + of the b atomics) + per
-// half-warp the most loaded bank pair of the a gathers + of the b gathers.
+// lane sitting in a most loaded bank trades records with another position of its row when that
+// lowers the modelled wavefronts of the two steps involved.  Model (what tools/bank_model.py
+// reports, with lanes counted instead of distinct words): per step 2 x the most loaded 32-bit bank
+// of the atomics + per half-warp the most loaded bank pair of the gathers.
 struct StepBanks {
-  uint8_t ca[32], cb[32], ga[2][16], gb[2][16];
-  void add(uint32_t lane, uint32_t x, int d) {
-    const uint32_t a = x & 0xffffu, b = x >> 16, h = lane >> 4;
-    ca[a & 31] += d, ga[h][(a >> 1) & 15] += d;
-    if (b) cb[b & 31] += d, gb[h][(b >> 1) & 15] += d;
-  }
+  uint8_t ca[32], ga[2][16];
+  void add(uint32_t lane, uint32_t x, int d) { ca[x & 31u] += d, ga[lane >> 4][(x >> 1) & 15u] += d; }
   struct Max {
-    uint32_t a, b, g[2][2];  // most loaded bank: a atomics, b atomics, gathers [a / b][half-warp]
-    uint32_t cost() const { return 2u * (a + b) + g[0][0] + g[0][1] + g[1][0] + g[1][1]; }
+    uint32_t a, g[2];  // most loaded bank of the atomics, bank pair of the gathers per half-warp
+    uint32_t cost() const { return 2u * a + g[0] + g[1]; }
   };
   Max maxes() const {
-    Max m{0, 0, {{0, 0}, {0, 0}}};
-    for (uint32_t i = 0; i < 32; ++i) m.a = std::max<uint32_t>(m.a, ca[i]), m.b = std::max<uint32_t>(m.b, cb[i]);
-    for (uint32_t i = 0; i < 16; ++i) {
-      m.g[0][0] = std::max<uint32_t>(m.g[0][0], ga[0][i]), m.g[0][1] = std::max<uint32_t>(m.g[0][1], ga[1][i]);
-      m.g[1][0] = std::max<uint32_t>(m.g[1][0], gb[0][i]), m.g[1][1] = std::max<uint32_t>(m.g[1][1], gb[1][i]);
-    }
+    Max m{0, {0, 0}};
+    for (uint32_t i = 0; i < 32; ++i) m.a = std::max<uint32_t>(m.a, ca[i]);
+    for (uint32_t i = 0; i < 16; ++i)
+      m.g[0] = std::max<uint32_t>(m.g[0], ga[0][i]), m.g[1] = std::max<uint32_t>(m.g[1], ga[1][i]);
     return m;
   }
   uint32_t cost() const { return maxes().cost(); }
   // the step's cost with record x added at `lane`, given the maxes without it
   uint32_t cost_with(const Max& m, uint32_t lane, uint32_t x) const {
-    const uint32_t a = x & 0xffffu, b = x >> 16, h = lane >> 4;
-    uint32_t c = m.cost();
-    c += 2u * (std::max<uint32_t>(m.a, ca[a & 31] + 1u) - m.a);
-    c += std::max<uint32_t>(m.g[0][h], ga[h][(a >> 1) & 15] + 1u) - m.g[0][h];
-    if (b) {
-      c += 2u * (std::max<uint32_t>(m.b, cb[b & 31] + 1u) - m.b);
-      c += std::max<uint32_t>(m.g[1][h], gb[h][(b >> 1) & 15] + 1u) - m.g[1][h];
-    }
-    return c;
+    const uint32_t h = lane >> 4;
+    return m.cost() + 2u * (std::max<uint32_t>(m.a, ca[x & 31u] + 1u) - m.a) +
+           (std::max<uint32_t>(m.g[h], ga[h][(x >> 1) & 15u] + 1u) - m.g[h]);
   }
-  // is lane's record x in a most loaded (> 1) bank of any component?
+  // is lane's record x in a most loaded (> 1) bank?
   bool hot(uint32_t lane, uint32_t x) const {
-    const uint32_t a = x & 0xffffu, b = x >> 16, h = lane >> 4;
     auto top = [](const uint8_t* c, uint32_t n, uint32_t i) {
       if (c[i] < 2) return false;
       for (uint32_t k = 0; k < n; ++k)
         if (c[k] > c[i]) return false;
       return true;
     };
-    return top(ca, 32, a & 31) || top(ga[h], 16, (a >> 1) & 15) ||
-           (b && (top(cb, 32, b & 31) || top(gb[h], 16, (b >> 1) & 15)));
+    return top(ca, 32, x & 31u) || top(ga[lane >> 4], 16, (x >> 1) & 15u);
   }
 };
 
@@ -759,16 +697,6 @@ void refine_banks(std::vector<uint32_t>& rec, const std::vector<uint32_t>& rowid
   std::vector<uint32_t> cost((size_t)W * K);
   for (uint32_t j = 0; j < C; ++j) sb[(size_t)(j / K / 32) * K + j % K].add((j / K) & 31, rec[j], 1);
   for (size_t i = 0; i < sb.size(); ++i) cost[i] = sb[i].cost();
-  auto flip = [](uint32_t x) { return (x >> 16) | ((x & 0xffffu) << 16); };
-  // the cheaper orientation of record y at (step s, lane l), whose own record is already removed
-  // (m: the step's maxes without it)
-  auto best_in = [&](const StepBanks& s, const StepBanks::Max& m, uint32_t l, uint32_t y, uint32_t& c) {
-    c = s.cost_with(m, l, y);
-    if (!(y >> 16)) return y;
-    const uint32_t f = flip(y), c2 = s.cost_with(m, l, f);
-    if (c2 < c) return c = c2, f;
-    return y;
-  };
   for (int pass = 0; pass < passes; ++pass) {
     bool any = false;
     for (uint32_t w = 0; w < W; ++w)
@@ -787,44 +715,36 @@ void refine_banks(std::vector<uint32_t>& rec, const std::vector<uint32_t>& rowid
             s.add(l, x, 1);
             continue;
           }
-          uint32_t cx;
-          const uint32_t xb = best_in(s, m, l, x, cx);  // flipping alone
-          uint32_t best_gain = cost[si] - cx, best_j2 = j, best_y = xb, best_x2 = 0, best_c = cx, best_c2 = 0;
+          uint32_t best_gain = 0, best_j2 = j, best_c = 0, best_c2 = 0;
           for (uint32_t j2 = off[r]; j2 < off[r + 1]; ++j2) {
-            if (j2 == j || rec[j2] == x || ((rec[j2] >> 16) != 0) != ((x >> 16) != 0)) continue;  // same class
+            if (j2 == j || rec[j2] == x) continue;
             const uint32_t t2 = j2 / K, l2 = t2 & 31;
             const size_t si2 = (size_t)(t2 / 32) * K + j2 % K;
             if (si2 == si) continue;  // same step: only the half-warp would change
             const uint32_t y = rec[j2];
-            uint32_t c1, c2;
-            const uint32_t yo = best_in(s, m, l, y, c1);
+            const uint32_t c1 = s.cost_with(m, l, y);
             if (c1 >= cost[si]) continue;  // the gain has to come from this step
             StepBanks& s2 = sb[si2];
             s2.add(l2, y, -1);
-            const uint32_t xo = best_in(s2, s2.maxes(), l2, x, c2);
+            const uint32_t c2 = s2.cost_with(s2.maxes(), l2, x);
             s2.add(l2, y, 1);
             const uint32_t before = cost[si] + cost[si2], after = c1 + c2;
             if (after < before && before - after > best_gain)
-              best_gain = before - after, best_j2 = j2, best_y = yo, best_x2 = xo, best_c = c1, best_c2 = c2;
+              best_gain = before - after, best_j2 = j2, best_c = c1, best_c2 = c2;
           }
           if (best_gain == 0) {
             s.add(l, x, 1);
             continue;
           }
           any = true;
-          if (best_j2 == j) {
-            rec[j] = best_y;
-            s.add(l, best_y, 1);
-            cost[si] = best_c;
-          } else {
-            const uint32_t t2 = best_j2 / K, l2 = t2 & 31;
-            const size_t si2 = (size_t)(t2 / 32) * K + best_j2 % K;
-            sb[si2].add(l2, rec[best_j2], -1);
-            sb[si2].add(l2, best_x2, 1);
-            s.add(l, best_y, 1);
-            rec[j] = best_y, rec[best_j2] = best_x2;
-            cost[si] = best_c, cost[si2] = best_c2;
-          }
+          const uint32_t t2 = best_j2 / K, l2 = t2 & 31;
+          const size_t si2 = (size_t)(t2 / 32) * K + best_j2 % K;
+          const uint32_t y = rec[best_j2];
+          sb[si2].add(l2, y, -1);
+          sb[si2].add(l2, x, 1);
+          s.add(l, y, 1);
+          rec[j] = y, rec[best_j2] = x;
+          cost[si] = best_c, cost[si2] = best_c2;
         }
       }
     if (!any) break;
