@@ -128,6 +128,28 @@ def test_empty_and_zero_rows(oracle, tree_mode):
     _check_sweep(oracle, encs[:1], np.ones(4), mode=tree_mode)
 
 
+def test_long_record_streams(oracle, tree_mode):
+    """Batches whose record stream (one 16-bit record per slot reference, toc_levels.cu) exceeds
+    1024 x 32 records -- per-thread ranges of 40 records and more -- beside a short and an
+    all-empty batch in the same launch, and empty rows between long ones."""
+    from paper_1702_06943_b200 import synth
+
+    rng = np.random.default_rng(17)
+    big = synth.cfg2_batch_dense(0, 40, n_rows=280)  # ~34 k records, ~15.7 k slots: still the slot kernel
+    big[5] = 0.0
+    big[6] = 0.0
+    big[-1] = 0.0
+    encs = [oracle.encode_csr(784, *synth.dense_to_csr(big)),
+            oracle.encode_csr(784, *synth.dense_to_csr(synth.cfg2_batch_dense(0, 42)[:7])),
+            oracle.encode_csr(784, *synth.dense_to_csr(np.zeros((3, 784)))),
+            oracle.encode_csr(784, *synth.dense_to_csr(synth.cfg2_batch_dense(0, 43)))]
+    assert len(encs[0].codes) > 26000
+    if tree_mode == "levels":
+        arena = _arena([oracle.serialize(e) for e in encs])
+        assert arena.build_levels(), "every batch here fits the slot cache"
+    _check_sweep(oracle, encs, rng.standard_normal(784), seed=21, mode=tree_mode)
+
+
 def test_wide_tree_global_tables(oracle, tree_mode):
     """A batch whose tree exceeds 65536 nodes (32-bit node ids) and shared memory (global
     table fallback): identical rows compress into long chains."""
