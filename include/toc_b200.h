@@ -147,9 +147,10 @@ int toc_linalg_trees(const uint8_t* d_arena, const int64_t* d_block_off, const T
  * toc_levels_build (host): from a HOST copy of the arena, per batch a self-contained entry: the
  * value index and row offsets, the pairs numbered by column (slots 1..|I|), the "inner" derived
  * nodes -- those some used derived node hangs off, closed under parents -- with their (parent,
- * key) slot records, and the code stream as per-code slot references (the node's own slot, or
- * parent slot + key slot for a leaf) cut into equal per-thread ranges -- built once, like the
- * reference's cached CompressedMatrix.tree (kernels.py:68-77).  Returns an opaque handle (NULL on
+ * key) slot records, and the code stream as 16-bit slot records (the node's own slot, or two
+ * records -- parent slot, key slot -- for a leaf; one record of slot 0 for an empty row) cut into
+ * equal per-thread ranges and placed within each row to spread the shared-memory banks -- built
+ * once, like the reference's cached CompressedMatrix.tree (kernels.py:68-77).  Returns an opaque handle (NULL on
  * bad arguments).  toc_levels_info: total bytes, the largest slot count and staged-region size,
  * and the build status (TOC_E_CORRUPT for a block the reference's tree build rejects,
  * codec.py:235-244; TOC_E_ARG when some batch needs slots wider than 15 bits or columns wider
