@@ -397,7 +397,17 @@ class BatchSweep:
             pass
 
     def run(self, v, u, out=None):
-        """The first chunk's block bytes are enqueued (two chunks when v / u must be staged into
+        """``submit`` then ``finish``: one step, results ready on return."""
+        self.submit(v, u, out=out)
+        return self.finish()
+
+    def submit(self, v, u, out=None):
+        """Enqueue one step without waiting for it (``finish`` waits and returns the results).  Two
+        BatchSweep objects over the same host blocks, submitted alternately, keep the host link busy
+        across steps: while one's last chunks are validated, swept and downloaded, the other's
+        uploads are already under way.  At most one step per object may be in flight.
+
+        The first chunk's block bytes are enqueued (two chunks when v / u must be staged into
         pinned buffers first; v and u given as pinned float64 CPU tensors are copied from in place);
         then the operands, the other chunks' bytes (all on one copy stream: host -> device copies
         are served in submission order), every chunk's validation and fused A.v + v^T.A (each as
@@ -405,6 +415,8 @@ class BatchSweep:
         Returns (R [n_rows], O [n_blocks, n_cols]) as new arrays; with out=(R_h, O_h) -- float64
         CPU tensors of those shapes, pinned for asynchronous copies -- the results are downloaded
         straight into them and they are returned (no extra host copy)."""
+        if getattr(self, "_pending", None) is not None:
+            raise RuntimeError("BatchSweep.submit(): the previous step has not been finished")
         torch = self.torch
         L = N.lib()
         caller = torch.cuda.current_stream()
@@ -445,6 +457,17 @@ class BatchSweep:
         N.check(L.toc_sweep_compute(self.cdesc, n, self.n_cols, self.v_d.data_ptr(), self.u_d.data_ptr(),
                                     self.R_d.data_ptr(), R_dst, self.O_d.data_ptr(), O_dst,
                                     self.meta_all_h.data_ptr(), comp.cuda_stream, ds.cuda_stream), "toc_sweep_compute")
+        self._pending = (caller, out, (v, u))  # operands stay referenced until the copies are done
+
+    def finish(self):
+        """Wait for the submitted step: block-format / corrupt-tree errors are raised here (the
+        reference's exception classes); returns (R, O) as ``run`` does."""
+        pending = getattr(self, "_pending", None)
+        if pending is None:
+            raise RuntimeError("BatchSweep.finish() without a submitted step")
+        caller, out, _operands = pending
+        self._pending = None
+        ds = self.d2h_stream
         ds.synchronize()
         caller.wait_stream(ds)
         meta = np.frombuffer(self.meta_all_h.numpy().tobytes(), dtype=N.META_DTYPE)[: self.n_blocks]

@@ -201,6 +201,27 @@ def test_batch_sweep_public_api(oracle):
     assert np.array_equal(R3, R0) and np.array_equal(O3, O0)
     with pytest.raises(ValueError):  # a wrong length is still refused (through the staging path)
         sweep.run(xp[:-1], up)
+    # submit / finish: two sweeps over the same host blocks keep two steps in flight; each step's
+    # results land in its own buffers and equal run()'s
+    outs = [(torch.empty(250 * nb, dtype=torch.float64).pin_memory(),
+             torch.empty((nb, 784), dtype=torch.float64).pin_memory()) for _ in range(2)]
+    pair = [sweep, other]
+    ops = [(xp, up), (torch.from_numpy(-x).pin_memory(), torch.from_numpy(-u).pin_memory())]
+    pair[0].submit(*ops[0], out=outs[0])
+    for i in range(1, 6):
+        pair[i & 1].submit(*ops[i & 1], out=outs[i & 1])
+        Rf, Of = pair[(i - 1) & 1].finish()
+        sign = 1.0 if (i - 1) & 1 == 0 else -1.0
+        assert Rf is outs[(i - 1) & 1][0] and np.array_equal(Rf.numpy(), sign * R0) and np.array_equal(Of.numpy(), sign * O0)
+    pair[1].finish()
+    assert np.array_equal(outs[1][0].numpy(), -R0) and np.array_equal(outs[1][1].numpy(), -O0)
+    with pytest.raises(RuntimeError):
+        sweep.finish()  # nothing submitted
+    sweep.submit(xp, up)
+    with pytest.raises(RuntimeError):
+        sweep.submit(xp, up)  # one step per object in flight
+    R4, O4 = sweep.finish()
+    assert np.array_equal(R4, R0) and np.array_equal(O4, O0)
 
 
 @pytest.mark.parametrize("kind", [1, 2, 3])
