@@ -186,14 +186,8 @@ TOC_D void walk_stream(const uint4* __restrict__ st, uint32_t nth, uint32_t K, u
 
 // Stage entry bn (header + value index + row offsets + pair / inner records + column starts) into
 // shared memory with one TMA bulk copy, and pull the entry after it into L2.  One thread.
-TOC_D void issue_stage(const LvlArgs& a, int64_t bn, uint8_t* stage, uint64_t* mbar, bool first = false) {
-  const int64_t eo = a.lvl_off[bn];
-  const uint8_t* ent = a.lvl + eo;
-  if (first) {  // the CTA's first entry: its stream towards L2 too (later entries are prefetched a batch ahead)
-    const uint32_t ebytes = (uint32_t)(a.lvl_off[bn + 1] - eo) & ~15u;
-    if (g_prefetch_mode == 1 && ebytes)
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(ent), "r"(ebytes) : "memory");
-  }
+TOC_D void issue_stage(const LvlArgs& a, int64_t bn, uint8_t* stage, uint64_t* mbar) {
+  const uint8_t* ent = a.lvl + a.lvl_off[bn];
   const uint32_t bytes = __ldg(reinterpret_cast<const uint32_t*>(ent) + offsetof(LvlHdr, off_stream) / 4);
   bulk_load(stage, ent, bytes, mbar);
   const int64_t bp = bn + gridDim.x;
@@ -280,16 +274,15 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
   const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
   uint32_t phase = 0;
   int64_t b = blockIdx.x;
-  // the first entry's copy starts before anything else: its dependent cold loads (entry offset,
-  // staged size, the copy itself) are the longest chain of the prologue
-  if (tid == 0) {
-    mbar_init(mbar, 1);
-    if (b < a.n_blocks) issue_stage(a, b, stage, mbar, true);
-  }
+  if (tid == 0) mbar_init(mbar, 1);
   if (MV)
     for (uint32_t c = tid; c < ncol; c += nth) v_s[c] = a.v[c];
   if (VM)
     for (uint32_t i = tid; i < S4max / 2; i += nth) reinterpret_cast<uint4*>(tabp)[i] = z4;
+  __syncthreads();
+  if (b < a.n_blocks) {
+    if (tid == 0) issue_stage(a, b, stage, mbar);
+  }
   UPrefetch p0;
   if (VM && b < a.n_blocks) {
     p0.bounds(a, b);
