@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
   const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
   uint32_t phase = 0;
   int64_t b = blockIdx.x;
+  TOC_LVL_STAMP(9);  // kernel entry (the first batch's row of the trace)
   if (tid == 0) mbar_init(mbar, 1);
   if (MV)
     for (uint32_t c = tid; c < ncol; c += nth) v_s[c] = a.v[c];

@@ -28,6 +28,8 @@ torch.cuda.synchronize()
 N.check(L.toc_levels_set_trace(None), "trace")
 t = tr.cpu().numpy().reshape(64, 10)
 nb = (arena.n_blocks + 147) // 148
+print(f"prologue: kernel entry to the first batch's staged region landed {t[0, 0] - t[0, 9]} cycles; "
+      f"first batch {t[0, 7] - t[0, 0]} cycles; CTA 0 entry to its last batch's end {t[nb - 1, 7] - t[0, 9]} cycles")
 t = t[: nb - 1]
 names = ["scatterT", "push", "colparts", "coltot+P1", "innerH", "rowsAv", "rowtot+zeroT"]
 d = np.diff(t[:, :8], axis=1)
