@@ -505,8 +505,9 @@ def main():
             "fp32_variant": {"ms_per_step": float(np.mean(f32_t)),
                              "rows_per_s": world * rows_per_step / (np.mean(f32_t) / 1e3),
                              "roofline_frac": alg / (np.mean(f32_t) / 1e3) / 1e9 / peak, "dtype": "f32",
-                             "note": "toc_linalg32: fp32 operands, fixed-point 32-bit v^T.A, one walk for both "
-                                     "products; 1e-4 of the fp64 oracle (not the headline: the reference is f64)"},
+                             "note": "toc_linalg_levels32 over the slot cache (toc_linalg32 over the tree cache when "
+                                     "there is none): fp32 operands and H, 32-bit fixed-point v^T.A (one atomic per "
+                                     "record); 1e-4 of the fp64 oracle (not the headline: the reference is f64)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic if slots else None, "traffic_source": traffic_src,
                          "peak_source": peak_src,

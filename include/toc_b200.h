@@ -173,6 +173,13 @@ int64_t toc_levels_smem(int32_t kind, int32_t n_cols, int32_t max_slots, int32_t
 int toc_linalg_levels(const int64_t* d_row_base, int64_t n_blocks, int32_t kind, int32_t n_cols, int32_t max_slots,
                       int32_t max_stage, int32_t max_rows, const double* d_v, double* d_R, const double* d_u,
                       double* d_O, const uint8_t* d_lvl, const int64_t* d_lvl_off, void* stream);
+/* The fp32 variant (BASELINE.json north_star: within 1e-4 of the fp64 results; the reference is fp64
+ * only) over the same cache entries: float operands and results, H in fp32, v^T.A in 32-bit fixed
+ * point -- one native shared-memory atomic per record -- or float atomics when that would be too
+ * coarse for the bar (heavy-tailed u). */
+int toc_linalg_levels32(const int64_t* d_row_base, int64_t n_blocks, int32_t kind, int32_t n_cols, int32_t max_slots,
+                        int32_t max_stage, int32_t max_rows, const float* d_v, float* d_R, const float* d_u,
+                        float* d_O, const uint8_t* d_lvl, const int64_t* d_lvl_off, void* stream);
 
 /* ---- the reference's own operation order, bit for bit (csrc/toc_exact.cu; kernels.py:115-174) ---
  * Over one batch's DecodeTree (device arrays parent / column / value, node 0 the root) and a

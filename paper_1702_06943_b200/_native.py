@@ -112,6 +112,7 @@ def lib():
     L.toc_levels_smem.restype = I64
     L.toc_levels_smem.argtypes = [I32, I32, I32, I32, I32]
     L.toc_linalg_levels.argtypes = [P, I64, I32, I32, I32, I32, I32, P, P, P, P, P, P, P]
+    L.toc_linalg_levels32.argtypes = [P, I64, I32, I32, I32, I32, I32, P, P, P, P, P, P, P]
     L.toc_levels_set_trace.argtypes = [P]
     L.toc_tree_arrays.argtypes = [P, P, P, I64, ctypes.POINTER(TocPlan), P, P, P, P, P, P, P, P]
     L.toc_dense_matvec.argtypes = [P, I64, I64, P, P, P]

@@ -382,19 +382,30 @@ class BlockArena:
         st["down"].synchronize()
         return R_h, O_h
 
-    def linalg32(self, kind: int, v=None, u=None, R=None, O=None):
-        """The fp32 variant (toc_linalg32) over the tree cache (built on first use): v [n_cols], u
-        [n_rows_total] float32 device tensors -> (R [n_rows_total], O [n_blocks, n_cols]) float32."""
+    def linalg32(self, kind: int, v=None, u=None, R=None, O=None, use_levels=None):
+        """The fp32 variant: v [n_cols], u [n_rows_total] float32 device tensors -> (R [n_rows_total],
+        O [n_blocks, n_cols]) float32.  Over the slot cache when it has been built
+        (toc_linalg_levels32; use_levels False skips it), else over the tree cache (toc_linalg32,
+        built on first use)."""
         torch = self.torch
-        if getattr(self, "trees", None) is None:
-            self.build_trees()
-        plan = self.plan(N.TOC_MATVEC | N.TOC_VECMAT)
         dev = self.data.device
         if kind & N.TOC_MATVEC and R is None:
             R = torch.empty(max(self.n_rows_total, 1), dtype=torch.float32, device=dev)[: self.n_rows_total]
         if kind & N.TOC_VECMAT and O is None:
             O = torch.empty((max(self.n_blocks, 1), max(self.n_cols, 1)), dtype=torch.float32,
                             device=dev)[: self.n_blocks, : self.n_cols]
+        if use_levels is not False and getattr(self, "levels", None) is not None and self.n_blocks:
+            self.raise_corrupt()
+            slots, stage, rows = self.levels_dims
+            N.check(N.lib().toc_linalg_levels32(
+                self.row_base_d.data_ptr(), self.n_blocks, kind, self.n_cols, slots, stage, rows,
+                _ptr(v) if kind & N.TOC_MATVEC else None, _ptr(R) if kind & N.TOC_MATVEC else None,
+                _ptr(u) if kind & N.TOC_VECMAT else None, _ptr(O) if kind & N.TOC_VECMAT else None,
+                self.levels.data_ptr(), self.levels_off_d.data_ptr(), N.stream_handle()), "toc_linalg_levels32")
+            return R, O
+        if getattr(self, "trees", None) is None:
+            self.build_trees()
+        plan = self.plan(N.TOC_MATVEC | N.TOC_VECMAT)
         N.check(N.lib().toc_linalg32(self.data.data_ptr(), self.block_off_d.data_ptr(), self.meta_d.data_ptr(),
                                      self.row_base_d.data_ptr(), self.n_blocks, ctypes.byref(plan), kind,
                                      _ptr(v) if kind & N.TOC_MATVEC else None, _ptr(R) if kind & N.TOC_MATVEC else None,

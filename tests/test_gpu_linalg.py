@@ -242,19 +242,22 @@ def test_fp32_variant_vs_oracle(oracle, kind):
         rng = np.random.default_rng(kind)
         v = rng.standard_normal(m).astype(np.float32)
         u = rng.standard_normal(sum(e.n_rows for e in encs)).astype(np.float32)
-        R, O = arena.linalg32(kind, v=torch.from_numpy(v).cuda(), u=torch.from_numpy(u).cuda())
-        base = 0
-        for b, e in enumerate(encs):
-            t = oracle.Tree.from_encoding(e)
-            if kind & 1:
-                want = t.matvec(v.astype(np.float64))
-                got = R[base : base + e.n_rows].cpu().numpy().astype(np.float64)
-                assert within_rel(got, want, 1e-4), max_rel_err(got, want)
-            if kind & 2:
-                want = t.vecmat(u[base : base + e.n_rows].astype(np.float64))
-                got = O[b].cpu().numpy().astype(np.float64)
-                assert within_rel(got, want, 1e-4), max_rel_err(got, want)
-            base += e.n_rows
+        for slots in (False, True):  # over the tree cache (toc_linalg32), then over the slot cache (toc_linalg_levels32)
+            if slots:
+                assert arena.build_levels()
+            R, O = arena.linalg32(kind, v=torch.from_numpy(v).cuda(), u=torch.from_numpy(u).cuda())
+            base = 0
+            for b, e in enumerate(encs):
+                t = oracle.Tree.from_encoding(e)
+                if kind & 1:
+                    want = t.matvec(v.astype(np.float64))
+                    got = R[base : base + e.n_rows].cpu().numpy().astype(np.float64)
+                    assert within_rel(got, want, 1e-4), (slots, max_rel_err(got, want))
+                if kind & 2:
+                    want = t.vecmat(u[base : base + e.n_rows].astype(np.float64))
+                    got = O[b].cpu().numpy().astype(np.float64)
+                    assert within_rel(got, want, 1e-4), (slots, max_rel_err(got, want))
+                base += e.n_rows
 
 
 def test_linalg_pipelined_equals_linalg(oracle):
@@ -337,9 +340,12 @@ def test_fp32_variant_heavy_tailed_u(oracle, u_kind):
     rng = np.random.default_rng(18)
     u = _heavy_u(rng, 750, u_kind).astype(np.float32)
     v = rng.standard_normal(784).astype(np.float32)
-    for kind in (2, 3):
-        _, O = arena.linalg32(kind, v=torch.from_numpy(v).cuda(), u=torch.from_numpy(u).cuda())
-        for b, e in enumerate(encs):
-            want = oracle.Tree.from_encoding(e).vecmat(u[250 * b : 250 * (b + 1)].astype(np.float64))
-            got = O[b].cpu().numpy().astype(np.float64)
-            assert within_rel(got, want, 1e-4), (kind, max_rel_err(got, want))
+    for slots in (False, True):  # the tree-cache kernel, then the slot-cache kernel
+        if slots:
+            assert arena.build_levels()
+        for kind in (2, 3):
+            _, O = arena.linalg32(kind, v=torch.from_numpy(v).cuda(), u=torch.from_numpy(u).cuda())
+            for b, e in enumerate(encs):
+                want = oracle.Tree.from_encoding(e).vecmat(u[250 * b : 250 * (b + 1)].astype(np.float64))
+                got = O[b].cpu().numpy().astype(np.float64)
+                assert within_rel(got, want, 1e-4), (slots, kind, max_rel_err(got, want))
