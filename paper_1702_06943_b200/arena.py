@@ -313,27 +313,70 @@ class BlockArena:
         N.check(rc, "toc_linalg")
         return R, O
 
-    def linalg_pipelined(self, kind: int, v_h, u_h, R_h, O_h, chunks: int = 4):
+    def linalg_pipelined(self, kind: int, v_h, u_h, R_h, O_h, chunks: int = 4, slot: int = 0, wait: bool = True):
         """A.v and / or v^T.A with the operands and results in pinned host tensors and the arena
         (with its slot cache, else its tree cache) resident: the batches go in `chunks` slices so that the upload of
         slice k's u, its launch, and the read-back of slice k-1's R / O overlap on three streams.
         v_h [n_cols], u_h [n_rows_total], R_h [n_rows_total], O_h [n_blocks, n_cols]: float64, pinned.
-        Returns when R_h / O_h hold the results."""
+        The step's stream work is captured into a CUDA graph the second time it is called with the
+        same host tensors and replayed from then on (one launch call per step instead of dozens).
+        Returns when R_h / O_h hold the results; with wait=False it returns once the step is
+        enqueued (``pipelined_wait(slot)`` waits) -- `slot` selects one of several sets of device
+        buffers, so steps submitted alternately on slots 0 and 1 overlap one step's read-back with
+        the next step's upload and launches."""
         torch = self.torch
         self.raise_corrupt()
         slots = getattr(self, "levels", None) is not None
         if self.trees is None and not slots:
             self.build_trees()
         dev = self.data.device
-        mv, vm = bool(kind & N.TOC_MATVEC), bool(kind & N.TOC_VECMAT)
-        st = getattr(self, "_pipe", None)
+        pipes = getattr(self, "_pipes", None)
+        if pipes is None:
+            pipes = self._pipes = {}
+        st = pipes.get(slot)
         if st is None:
-            st = self._pipe = {"up": torch.cuda.Stream(), "run": torch.cuda.Stream(), "down": torch.cuda.Stream(),
-                               "v": torch.empty(max(self.n_cols, 1), dtype=torch.float64, device=dev),
-                               "u": torch.empty(max(self.n_rows_total, 1), dtype=torch.float64, device=dev),
-                               "R": torch.empty(max(self.n_rows_total, 1), dtype=torch.float64, device=dev),
-                               "O": torch.empty((max(self.n_blocks, 1), max(self.n_cols, 1)), dtype=torch.float64,
-                                                device=dev)}
+            st = pipes[slot] = {"up": torch.cuda.Stream(), "run": torch.cuda.Stream(), "down": torch.cuda.Stream(),
+                                "main": torch.cuda.Stream(), "graphs": {}, "seen": set(),
+                                "v": torch.empty(max(self.n_cols, 1), dtype=torch.float64, device=dev),
+                                "u": torch.empty(max(self.n_rows_total, 1), dtype=torch.float64, device=dev),
+                                "R": torch.empty(max(self.n_rows_total, 1), dtype=torch.float64, device=dev),
+                                "O": torch.empty((max(self.n_blocks, 1), max(self.n_cols, 1)), dtype=torch.float64,
+                                                 device=dev)}
+        key = (kind, v_h.data_ptr(), u_h.data_ptr(), R_h.data_ptr(), O_h.data_ptr(), chunks, slots)
+        main = st["main"]
+        main.wait_stream(torch.cuda.current_stream())
+        g = st["graphs"].get(key)
+        if g is not None:
+            with torch.cuda.stream(main):
+                g.replay()
+        elif key in st["seen"] and len(st["graphs"]) < 8:
+            main.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=main):
+                self._pipeline_enqueue(st, kind, v_h, u_h, R_h, O_h, chunks, slots)
+            st["graphs"][key] = g
+            st["keep"] = (v_h, u_h, R_h, O_h)  # the graph holds their addresses
+            with torch.cuda.stream(main):
+                g.replay()
+        else:
+            st["seen"].add(key)
+            with torch.cuda.stream(main):
+                self._pipeline_enqueue(st, kind, v_h, u_h, R_h, O_h, chunks, slots)
+        if wait:
+            main.synchronize()
+        return R_h, O_h
+
+    def pipelined_wait(self, slot: int = 0) -> None:
+        """Wait for the step submitted on `slot` with linalg_pipelined(..., wait=False)."""
+        st = getattr(self, "_pipes", {}).get(slot)
+        if st is not None:
+            st["main"].synchronize()
+
+    def _pipeline_enqueue(self, st, kind, v_h, u_h, R_h, O_h, chunks, slots) -> None:
+        """One pipelined step on the current stream (eager, or under CUDA graph capture): fork to the
+        upload / launch / read-back streams, slice by slice, and join them back."""
+        torch = self.torch
+        mv, vm = bool(kind & N.TOC_MATVEC), bool(kind & N.TOC_VECMAT)
         plan = None if slots else self.plan(kind)
         scratch = None if slots else self._scratch_for(plan)
         L = N.lib()
@@ -379,8 +422,8 @@ class BlockArena:
                     R_h[r0:r1].copy_(st["R"][r0:r1], non_blocking=True)
                 if vm:
                     O_h[b0:b1].copy_(st["O"][b0:b1], non_blocking=True)
-        st["down"].synchronize()
-        return R_h, O_h
+        for s in (st["up"], st["run"], st["down"]):
+            cur.wait_stream(s)
 
     def linalg32(self, kind: int, v=None, u=None, R=None, O=None, use_levels=None):
         """The fp32 variant: v [n_cols], u [n_rows_total] float32 device tensors -> (R [n_rows_total],

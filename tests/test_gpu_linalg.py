@@ -278,10 +278,31 @@ def test_linalg_pipelined_equals_linalg(oracle):
     R = torch.empty(arena.n_rows_total, dtype=torch.float64).pin_memory()
     O = torch.empty((arena.n_blocks, 784), dtype=torch.float64).pin_memory()
     for chunks in (1, 3, 7):
-        R.zero_()
-        O.zero_()
-        arena.linalg_pipelined(kind, v, u, R, O, chunks=chunks)
-        assert torch.equal(R, R0.cpu()) and torch.equal(O, O0.cpu())
+        for _ in range(3):  # eager, then captured into a CUDA graph, then replayed
+            R.zero_()
+            O.zero_()
+            arena.linalg_pipelined(kind, v, u, R, O, chunks=chunks)
+            assert torch.equal(R, R0.cpu()) and torch.equal(O, O0.cpu())
+    # the slot cache's kernel, two steps in flight on two sets of device buffers (new operands in
+    # the same pinned tensors are picked up by the replayed graph)
+    assert arena.build_levels()
+    outs = [(torch.empty_like(R).pin_memory(), torch.empty_like(O).pin_memory()) for _ in range(2)]
+    for rnd in range(2):
+        if rnd == 1:  # new operands in the same pinned tensors (no step in flight while they change)
+            v.mul_(-2.0)
+            u.mul_(0.5)
+        R0, O0 = arena.linalg(kind, v=v.cuda(), u=u.cuda())  # the slot kernel, one launch
+        for it in range(5):
+            s_ = it & 1
+            arena.pipelined_wait(s_)
+            if it >= 2:
+                assert torch.equal(outs[s_][0], R0.cpu()) and torch.equal(outs[s_][1], O0.cpu())
+            outs[s_][0].zero_()
+            outs[s_][1].zero_()
+            arena.linalg_pipelined(kind, v, u, outs[s_][0], outs[s_][1], chunks=4, slot=s_, wait=False)
+        for s_ in (0, 1):
+            arena.pipelined_wait(s_)
+            assert torch.equal(outs[s_][0], R0.cpu()) and torch.equal(outs[s_][1], O0.cpu())
 
 
 
