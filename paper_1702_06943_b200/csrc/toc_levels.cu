@@ -603,6 +603,53 @@ TOC_D void issue_stage32(const Lvl32Args& a, int64_t bn, uint8_t* stage, uint64_
   }
 }
 
+// The next batch's u a batch ahead, as UPrefetch does for the fp64 kernel.
+struct UPrefetch32 {
+  int64_t rb = 0;
+  uint32_t n = 0;
+  float u0 = 0.0f;
+  TOC_D void bounds(const Lvl32Args& a, int64_t bn) {
+    rb = a.row_base[bn];
+    n = __ldg(reinterpret_cast<const uint32_t*>(a.lvl + a.lvl_off[bn]) + offsetof(LvlHdr, n_rows) / 4);
+  }
+  TOC_D void load(const Lvl32Args& a) { u0 = threadIdx.x < n ? __ldg(a.u + rb + threadIdx.x) : 0.0f; }
+  TOC_D double stash(const Lvl32Args& a, float* u_s) const {
+    double su = fabs((double)u0);
+    if (threadIdx.x < n) u_s[threadIdx.x] = u0;
+    for (uint32_t r = threadIdx.x + blockDim.x; r < n; r += blockDim.x) {
+      const float x = __ldg(a.u + rb + r);
+      u_s[r] = x;
+      su += fabs((double)x);
+    }
+    return su;
+  }
+};
+
+// 2^(30 - e) for sum |u| < 2^e: no partial sum of the fixed-point weights leaves int32.
+TOC_D double fix32_scale_of(double su) {
+  if (!(su > 0.0)) return 1.0;
+  int e;
+  frexp(su, &e);
+  return ldexp(1.0, 30 - e);
+}
+
+// Rounding errors of +-q/2 per addend (q = 1/scale) are independent: a column's error has standard
+// deviation q * max|value| * sqrt(n/12); fixed point is used while 6 of them stay under 2^-15 (the
+// bar is 1e-4), float atomics otherwise.
+TOC_D bool fix32_too_coarse(uint32_t n, double vmax, double scale) {
+  return 6.0 * vmax * sqrt((double)n / 12.0) / scale > 0x1p-15;
+}
+
+// The fixed-point weight of every row of the batch whose u is in u_s; thread 0 keeps the batch's
+// sum |u| in s_red[32].
+TOC_D void row_weights32(double* s_red, const float* u_s, int32_t* wt_s, uint32_t n) {
+  const uint32_t lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+  const double su = warp_sum(lane < nwarps ? s_red[lane] : 0.0);
+  const double g = fix32_scale_of(su);
+  for (uint32_t r = threadIdx.x; r < n; r += blockDim.x) wt_s[r] = __double2int_rn((double)u_s[r] * g);
+  if (threadIdx.x == 0) s_red[32] = su;
+}
+
 template <int kKind>
 __global__ void __launch_bounds__(1024, 1) levels32_kernel(Lvl32Args a) {
   constexpr bool MV = kKind & TOC_MATVEC, VM = kKind & TOC_VECMAT;
@@ -632,6 +679,15 @@ __global__ void __launch_bounds__(1024, 1) levels32_kernel(Lvl32Args a) {
   __syncthreads();
   int64_t b = blockIdx.x;
   if (tid == 0 && b < a.n_blocks) issue_stage32(a, b, stage, mbar);
+  UPrefetch32 p0;
+  if (VM && b < a.n_blocks) {
+    p0.bounds(a, b);
+    p0.load(a);
+    su_store(p0.stash(a, u_s), s_red);
+  }
+  __syncthreads();
+  if (VM && b < a.n_blocks) row_weights32(s_red, u_s, wt_s, p0.n);
+  __syncthreads();
 
   for (; b < a.n_blocks; b += gridDim.x) {
     const int64_t bn = b + gridDim.x;
@@ -640,6 +696,8 @@ __global__ void __launch_bounds__(1024, 1) levels32_kernel(Lvl32Args a) {
     phase ^= 1u;
     const LvlHdr h = *reinterpret_cast<const LvlHdr*>(stage);  // the stage is refilled mid-batch
     const uint32_t n = h.n_rows, nP = h.nP, nQ = h.nQ, K = h.K;
+    UPrefetch32 pre;  // the next batch's u
+    if (VM && has_next) pre.bounds(a, bn);
     TOC_CHECK(h.S <= (uint32_t)a.max_slots && h.off_stream <= (uint32_t)a.max_stage && n <= (uint32_t)a.max_rows &&
               h.T == nth && h.n_cols == ncol && h.S == 1 + nP + nQ && K % 8 == 0 && h.C <= h.T * K);
     const double* uniq_s = reinterpret_cast<const double*>(stage + h.off_uniq);
@@ -658,32 +716,10 @@ __global__ void __launch_bounds__(1024, 1) levels32_kernel(Lvl32Args a) {
     const uint32_t M = ((nP + nth - 1) / nth) | 1u;
 
     if (VM) {
-      // this batch's u into shared memory, sum |u| for the fixed-point scale
-      double su = 0.0;
-      for (uint32_t r = tid; r < n; r += nth) {
-        const float x = __ldg(a.u + rb + r);
-        u_s[r] = x;
-        su += fabs((double)x);
-      }
-      su_store(su, s_red);
-      __syncthreads();
-      {
-        const uint32_t lane = tid & 31, nwarps = nth >> 5;
-        su = warp_sum(lane < nwarps ? s_red[lane] : 0.0);
-      }
-      double g_scale = 1.0;
-      if (su > 0.0) {
-        int e;
-        frexp(su, &e);
-        g_scale = ldexp(1.0, 30 - e);
-      }
-      // rounding errors of +-q/2 per addend (q = 1/g_scale) are independent: a column's error has
-      // standard deviation q * max|value| * sqrt(n/12); keep 6 of them under 2^-15 (the bar is 1e-4)
-      const bool flt = 6.0 * h.vmax * sqrt((double)n / 12.0) / g_scale > 0x1p-15;
+      // u_s, wt_s and s_red[32] (sum |u|) were prepared during the previous batch (or the prologue)
+      const double g_scale = fix32_scale_of(s_red[32]);
+      const bool flt = fix32_too_coarse(n, h.vmax, g_scale);  // float accumulation instead
       const float g_inv = (float)(1.0 / g_scale);
-      if (!flt)
-        for (uint32_t r = tid; r < n; r += nth) wt_s[r] = __double2int_rn((double)u_s[r] * g_scale);
-      __syncthreads();
       // T[slot] += u[r] for every record of this thread's range
       if (active) {
         uint32_t r = r0;
@@ -756,6 +792,7 @@ __global__ void __launch_bounds__(1024, 1) levels32_kernel(Lvl32Args a) {
         }
       }
       __syncthreads();
+      pre.load(a);
       // column partials (and, fused, each pair slot's T turned into its P1 in place)
       float* o = a.O + b * (int64_t)ncol;
       {
@@ -797,6 +834,7 @@ __global__ void __launch_bounds__(1024, 1) levels32_kernel(Lvl32Args a) {
           }
         }
       }
+      su_store(pre.stash(a, u_s), s_red);  // the next batch's u (this batch's was last read by the scatter)
     }
     if (MV) {
       if (!VM) {
@@ -871,8 +909,10 @@ __global__ void __launch_bounds__(1024, 1) levels32_kernel(Lvl32Args a) {
         }
       }
     }
-    if (VM)
+    if (VM) {  // a zero T table and the next batch's row weights (its u and partials are in)
       for (uint32_t i = tid; i < S4max / 2; i += nth) reinterpret_cast<uint4*>(tabp)[i] = z4;
+      if (has_next) row_weights32(s_red, u_s, wt_s, pre.n);
+    }
     __syncthreads();  // tables and partials are reused by the next batch
   }
 }
