@@ -54,7 +54,15 @@
 
 namespace toc {
 
-constexpr uint32_t kLvlThreads = 1024;  // the CTA size the streams are cut for
+// Probe builds (tools/probe_two_ctas.sh) override these: CTA size the streams are cut for, and CTAs
+// per SM the kernels are compiled and launched for.
+#ifndef TOC_LVL_THREADS
+#define TOC_LVL_THREADS 1024
+#endif
+#ifndef TOC_LVL_CTAS_PER_SM
+#define TOC_LVL_CTAS_PER_SM 1
+#endif
+constexpr uint32_t kLvlThreads = TOC_LVL_THREADS;  // the CTA size the streams are cut for
 
 // Entry header; section offsets relative to the entry start, 16-B aligned.  The staged region is
 // [off_uniq, off_stream).
@@ -253,7 +261,7 @@ TOC_D void row_weights(double* s_red, const double* u_s, uint2* wt_s, uint32_t n
 // The next batch's staged region is copied in while the A.v rows run (the rows read only the
 // stream, H and a private copy of the row offsets).
 template <int kKind, bool kTrace>
-__global__ void __launch_bounds__(1024, 1) levels_kernel(LvlArgs a) {
+__global__ void __launch_bounds__(TOC_LVL_THREADS, TOC_LVL_CTAS_PER_SM) levels_kernel(LvlArgs a) {
   constexpr bool MV = kKind & TOC_MATVEC, VM = kKind & TOC_VECMAT;
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t tid = threadIdx.x, nth = blockDim.x;
@@ -651,7 +659,7 @@ TOC_D void row_weights32(double* s_red, const float* u_s, int32_t* wt_s, uint32_
 }
 
 template <int kKind>
-__global__ void __launch_bounds__(1024, 1) levels32_kernel(Lvl32Args a) {
+__global__ void __launch_bounds__(TOC_LVL_THREADS, TOC_LVL_CTAS_PER_SM) levels32_kernel(Lvl32Args a) {
   constexpr bool MV = kKind & TOC_MATVEC, VM = kKind & TOC_VECMAT;
   extern __shared__ __align__(16) uint8_t smem[];
   const uint32_t tid = threadIdx.x, nth = blockDim.x;
@@ -1432,7 +1440,7 @@ extern "C" int toc_linalg_levels32(const int64_t* d_row_base, int64_t n_blocks, 
                                   : (void*)toc::levels32_kernel<TOC_MATVEC | TOC_VECMAT>;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return TOC_E_CUDA;
-  const int64_t grid = std::min<int64_t>(n_blocks, sms > 0 ? sms : 148);
+  const int64_t grid = std::min<int64_t>(n_blocks, (int64_t)TOC_LVL_CTAS_PER_SM * (sms > 0 ? sms : 148));
   void* args[] = {&a};
   return cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(toc::kLvlThreads), args, (size_t)smem,
                           (cudaStream_t)stream) == cudaSuccess
@@ -1465,7 +1473,7 @@ extern "C" int toc_linalg_levels(const int64_t* d_row_base, int64_t n_blocks, in
                    : (void*)toc::levels_kernel<TOC_MATVEC | TOC_VECMAT, false>);
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return TOC_E_CUDA;
-  const int64_t grid = std::min<int64_t>(n_blocks, sms > 0 ? sms : 148);
+  const int64_t grid = std::min<int64_t>(n_blocks, (int64_t)TOC_LVL_CTAS_PER_SM * (sms > 0 ? sms : 148));
   void* args[] = {&a};
   return cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(toc::kLvlThreads), args, (size_t)smem,
                           (cudaStream_t)stream) == cudaSuccess
