@@ -513,7 +513,9 @@ __global__ void __launch_bounds__(TOC_LVL_THREADS, TOC_LVL_CTAS_PER_SM) levels_k
       __syncthreads();
       TOC_LVL_STAMP(5);
     }
-    if (tid == 0 && has_next) issue_stage(a, bn, stage, mbar);  // the stage is no longer read
+    // issued by the last thread: its warp has few or no records, while thread 0's warp would start its
+    // row walk only after the issue's dependent global loads
+    if (tid == nth - 1 && has_next) issue_stage(a, bn, stage, mbar);  // the stage is no longer read
     if (MV) {
       // row partials over this thread's codes; a row ending inside the range is complete (started
       // here) or the range's head partial

@@ -12,7 +12,20 @@ import bench  # noqa: E402
 from paper_1702_06943_b200 import _native as N, codec  # noqa: E402
 
 kind = int(sys.argv[1]) if len(sys.argv) > 1 else 3
-rp, c, v, br = bench.make_shard(0, 1024)
+p_zero = float(sys.argv[2]) if len(sys.argv) > 2 else None  # e.g. 0.995: nearly empty batches (the per-batch floor)
+if p_zero is None:
+    rp, c, v, br = bench.make_shard(0, 1024)
+else:
+    from paper_1702_06943_b200 import synth  # noqa: E402
+
+    ptr, cols, vals, base = [np.zeros(1, np.int64)], [], [], 0
+    for b_ in range(1024):
+        r_, c_, v_ = synth.dense_to_csr(synth.cfg2_batch_dense(0, b_, p_zero=p_zero))
+        ptr.append(r_[1:] + base)
+        base += int(r_[-1])
+        cols.append(c_)
+        vals.append(v_)
+    rp, c, v, br = np.concatenate(ptr), np.concatenate(cols), np.concatenate(vals), np.arange(1025) * 250
 arena = codec.compress_csr(bench.COLS, rp, c, v, br)
 assert arena.build_levels()
 vd = torch.randn(bench.COLS, dtype=torch.float64, device="cuda")
