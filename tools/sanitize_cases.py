@@ -63,6 +63,15 @@ if case in ("linalg", "slots", "encode"):
         assert arena.build_levels()
         for k in (1, 2, 3):
             runs.append((f"slots{k}", arena.linalg(k, v=vd, u=ud)))
+        for k in (1, 2, 3):  # the fp32 slot kernel (toc_linalg_levels32), fixed point and float atomics
+            for scale in (1.0, None):
+                u32 = ud.float() if scale else (ud * torch.pow(10.0, 16 * torch.rand_like(ud) - 8)).float()
+                want_o = wantO if scale else oracle_sweep(rp, c, v, br, vv, u32.double().cpu().numpy())[1]
+                R32, O32 = arena.linalg32(k, v=vd.float(), u=u32)
+                if k & 1:
+                    assert rel(R32.double().cpu(), wantR) < 1e-4
+                if k & 2:
+                    assert rel(O32.double().cpu(), want_o) < 1e-4
     for name, (R, Ox) in runs:
         if R is not None and name[-1] in "13k":
             assert rel(R.cpu(), wantR) < 1e-9, (name, rel(R.cpu(), wantR))
